@@ -1,0 +1,237 @@
+"""Curved triangular patches from exact surface maps.
+
+Every patch P is the image X_P(s,t) of the reference triangle (0,0),(1,0),(0,1).  Nodes are the
+collapsed Gauss-Legendre rule (s,t) = (u, v(1-u)), u-major order, weights w_u w_v (1-u)|X_s x X_t|
+(SURVEY §8(c) A1).  Edge e runs vertex e -> vertex e+1 (CCW about the outward normal), sampled at the
+q Gauss-Legendre parameters tau in (-1,1); edge_dx = dX/dtau.  Derivatives of X are taken by torch
+autograd in float64 (exact up to rounding), so every map only has to be written once.
+"""
+from dataclasses import dataclass
+import numpy as np
+import torch
+
+
+@dataclass
+class Surface:
+    p: int
+    q: int
+    nodes: np.ndarray      # [P, n, 3]
+    normals: np.ndarray    # [P, n, 3]
+    weights: np.ndarray    # [P, n]
+    verts: np.ndarray      # [P, 3, 3]
+    edge_x: np.ndarray     # [P, 3, q, 3]
+    edge_dx: np.ndarray    # [P, 3, q, 3]
+    uv: np.ndarray         # [n, 2] reference (s, t) of the nodes
+    # parameters of the per-patch map, kept so targets can be generated on the exact surface
+    kind: str = ""
+    pdata: np.ndarray = None
+
+    @property
+    def n_patches(self):
+        return self.nodes.shape[0]
+
+    @property
+    def n(self):
+        return self.nodes.shape[1]
+
+
+def gauss_legendre_01(n):
+    x, w = np.polynomial.legendre.leggauss(n)
+    return (x + 1.0) / 2.0, w / 2.0
+
+
+def collapsed_nodes(p):
+    """Collapsed p x p Gauss-Legendre rule on the reference triangle, u-major."""
+    u, wu = gauss_legendre_01(p)
+    v, wv = gauss_legendre_01(p)
+    U, V = np.meshgrid(u, v, indexing="ij")
+    WU, WV = np.meshgrid(wu, wv, indexing="ij")
+    s = U.ravel()
+    t = (V * (1.0 - U)).ravel()
+    w = (WU * WV * (1.0 - U)).ravel()
+    return s, t, w
+
+
+def _eval_map(fmap, pdata, s, t):
+    """X, X_s, X_t for per-point parameter rows pdata[k] at (s[k], t[k]) (torch autograd)."""
+    s = torch.as_tensor(s, dtype=torch.float64).clone().requires_grad_(True)
+    t = torch.as_tensor(t, dtype=torch.float64).clone().requires_grad_(True)
+    X = fmap(pdata, s, t)
+    Xs = torch.empty_like(X)
+    Xt = torch.empty_like(X)
+    for c in range(3):
+        gs, gt = torch.autograd.grad(X[:, c].sum(), (s, t), retain_graph=True)
+        Xs[:, c] = gs
+        Xt[:, c] = gt
+    return X.detach().numpy(), Xs.detach().numpy(), Xt.detach().numpy()
+
+
+def build_surface(fmap, pdata, p, q, kind=""):
+    """Discretise patches X_P = fmap(pdata[P], s, t) (pdata: torch [P, k])."""
+    P = pdata.shape[0]
+    s0, t0, w0 = collapsed_nodes(p)
+    n = s0.size
+    rep = pdata.repeat_interleave(n, dim=0)
+    X, Xs, Xt = _eval_map(fmap, rep, np.tile(s0, P), np.tile(t0, P))
+    cr = np.cross(Xs, Xt)
+    J = np.linalg.norm(cr, axis=1)
+    nodes = X.reshape(P, n, 3)
+    normals = (cr / J[:, None]).reshape(P, n, 3)
+    weights = (np.tile(w0, P) * J).reshape(P, n)
+    # vertices
+    vs = np.array([0.0, 1.0, 0.0])
+    vt = np.array([0.0, 0.0, 1.0])
+    Xv, _, _ = _eval_map(fmap, pdata.repeat_interleave(3, dim=0), np.tile(vs, P), np.tile(vt, P))
+    verts = Xv.reshape(P, 3, 3)
+    # edges: e0 v0->v1, e1 v1->v2, e2 v2->v0, tau in (-1,1) Gauss-Legendre
+    tau, _ = np.polynomial.legendre.leggauss(q)
+    es = np.concatenate([(1 + tau) / 2, (1 - tau) / 2, np.zeros(q)])
+    et = np.concatenate([np.zeros(q), (1 + tau) / 2, (1 - tau) / 2])
+    dsd = np.concatenate([np.full(q, 0.5), np.full(q, -0.5), np.zeros(q)])
+    dtd = np.concatenate([np.zeros(q), np.full(q, 0.5), np.full(q, -0.5)])
+    Xe, Xes, Xet = _eval_map(fmap, pdata.repeat_interleave(3 * q, dim=0), np.tile(es, P), np.tile(et, P))
+    edge_x = Xe.reshape(P, 3, q, 3)
+    edge_dx = (Xes * np.tile(dsd, P)[:, None] + Xet * np.tile(dtd, P)[:, None]).reshape(P, 3, q, 3)
+    return Surface(p=p, q=q, nodes=nodes, normals=normals, weights=weights, verts=verts,
+                   edge_x=edge_x, edge_dx=edge_dx, uv=np.stack([s0, t0], 1), kind=kind,
+                   pdata=pdata.numpy())
+
+
+# ----------------------------------------------------------------------------- icosahedral spheres
+
+def icosahedron():
+    g = (1 + 5 ** 0.5) / 2
+    V = []
+    for a in (-1, 1):
+        for b in (-g, g):
+            V += [(0, a, b), (a, b, 0), (b, 0, a)]
+    V = np.array(V, dtype=np.float64)
+    V /= np.linalg.norm(V, axis=1, keepdims=True)
+    el = min(np.linalg.norm(V[i] - V[j]) for i in range(12) for j in range(i + 1, 12))
+    F = []
+    for i in range(12):
+        for j in range(i + 1, 12):
+            for k in range(j + 1, 12):
+                if all(abs(np.linalg.norm(V[x] - V[y]) - el) < 1e-9 for x, y in ((i, j), (j, k), (i, k))):
+                    a, b, c = V[i], V[j], V[k]
+                    if np.dot(np.cross(b - a, c - a), a + b + c) < 0:
+                        j2, k2 = k, j
+                    else:
+                        j2, k2 = j, k
+                    F.append((i, j2, k2))
+    assert len(F) == 20
+    return V, np.array(F)
+
+
+def subdivided_flat_triangles(freq):
+    """Frequency-`freq` grid on every flat icosahedron face: 20*freq^2 flat triangles [P,3,3]."""
+    V, F = icosahedron()
+    tris = []
+    for (i, j, k) in F:
+        A, B, C = V[i], V[j], V[k]
+        P = lambda a, b: A + (a / freq) * (B - A) + (b / freq) * (C - A)
+        for a in range(freq):
+            for b in range(freq - a):
+                tris.append((P(a, b), P(a + 1, b), P(a, b + 1)))
+                if a + b <= freq - 2:
+                    tris.append((P(a + 1, b), P(a + 1, b + 1), P(a, b + 1)))
+    return np.array(tris)
+
+
+def _radial_map(radius_fn):
+    def fmap(pd, s, t):
+        a, b, c = pd[:, 0:3], pd[:, 3:6], pd[:, 6:9]
+        y = a + s[:, None] * (b - a) + t[:, None] * (c - a)
+        xh = y / torch.linalg.norm(y, dim=1, keepdim=True)
+        return xh * radius_fn(xh)[:, None]
+    return fmap
+
+
+def make_sphere_surface(freq, p, q, radius_fn=None):
+    tris = subdivided_flat_triangles(freq)
+    pdata = torch.as_tensor(tris.reshape(-1, 9))
+    rf = radius_fn if radius_fn is not None else (lambda xh: torch.ones_like(xh[:, 0]))
+    return build_surface(_radial_map(rf), pdata, p, q, kind="sphere")
+
+
+def make_cap_surface(chord, p, q):
+    """One unit-sphere cap: flat equilateral triangle with side `chord` about +z, projected (cfg 5)."""
+    rho = chord / 3 ** 0.5
+    zc = (1 - rho * rho) ** 0.5
+    ang = np.pi / 2 + 2 * np.pi * np.arange(3) / 3
+    tri = np.stack([rho * np.cos(ang), rho * np.sin(ang), np.full(3, zc)], 1)
+    pdata = torch.as_tensor(tri.reshape(1, 9))
+    return build_surface(_radial_map(lambda xh: torch.ones_like(xh[:, 0])), pdata, p, q, kind="cap")
+
+
+# ----------------------------------------------------------------------------- real spherical harmonics
+
+def real_sph_harm_torch(lmax, xh):
+    """Orthonormal real spherical harmonics Y_lm(xh) for unit vectors xh [N,3]; dict (l,m)->tensor.
+
+    Uses Q_l^m(z) = P_l^m(z)/(1-z^2)^{m/2} and sin^m(theta) e^{im phi} = (x+iy)^m, so it is a polynomial
+    in the Cartesian components (differentiable by autograd everywhere).  Test-input plumbing only.
+    """
+    import math
+    x, y, z = xh[:, 0], xh[:, 1], xh[:, 2]
+    out = {}
+    # (x+iy)^m real/imag parts
+    cr, ci = [torch.ones_like(x)], [torch.zeros_like(x)]
+    for m in range(1, lmax + 1):
+        cr.append(cr[-1] * x - ci[-1] * y)
+        ci.append(cr[-2] * y + ci[-1] * x)
+    for m in range(0, lmax + 1):
+        Q = {}
+        Q[m] = torch.full_like(z, float(np.prod(np.arange(1, 2 * m, 2))) if m > 0 else 1.0)
+        if m + 1 <= lmax:
+            Q[m + 1] = (2 * m + 1) * z * Q[m]
+        for l in range(m + 2, lmax + 1):
+            Q[l] = ((2 * l - 1) * z * Q[l - 1] - (l + m - 1) * Q[l - 2]) / (l - m)
+        for l in range(m, lmax + 1):
+            N = math.sqrt((2 * l + 1) / (4 * math.pi) * math.factorial(l - m) / math.factorial(l + m))
+            if m == 0:
+                out[(l, 0)] = N * Q[l]
+            else:
+                out[(l, m)] = math.sqrt(2) * N * Q[l] * cr[m]
+                out[(l, -m)] = math.sqrt(2) * N * Q[l] * ci[m]
+    return out
+
+
+def bumpy_radius_fn(coef, lmax=6, amp=0.2):
+    def rf(xh):
+        Y = real_sph_harm_torch(lmax, xh)
+        r = torch.ones_like(xh[:, 0])
+        for (l, m), c in coef.items():
+            r = r + amp * c * Y[(l, m)]
+        return r
+    return rf
+
+
+# ----------------------------------------------------------------------------- torus
+
+def make_torus_surface(R, r, n_theta, n_phi, p, q):
+    """Torus, theta minor (n_theta), phi major (n_phi); each (phi,theta) quad halved along the
+    lower-left -> upper-right diagonal.  Parameter order (phi, theta) makes
+    X_phi x X_theta the outward normal, so parameter-space CCW is CCW about the outward normal."""
+    dphi = 2 * np.pi / n_phi
+    dth = 2 * np.pi / n_theta
+    pd = []
+    for i in range(n_phi):
+        for j in range(n_theta):
+            LL = (i * dphi, j * dth)
+            LR = ((i + 1) * dphi, j * dth)
+            UR = ((i + 1) * dphi, (j + 1) * dth)
+            UL = (i * dphi, (j + 1) * dth)
+            pd.append(LL + LR + UR)
+            pd.append(LL + UR + UL)
+    pdata = torch.as_tensor(np.array(pd, dtype=np.float64))
+
+    def fmap(pdt, s, t):
+        P0, P1, P2 = pdt[:, 0:2], pdt[:, 2:4], pdt[:, 4:6]
+        ab = P0 + s[:, None] * (P1 - P0) + t[:, None] * (P2 - P0)
+        ph, th = ab[:, 0], ab[:, 1]
+        rho = R + r * torch.cos(th)
+        return torch.stack([rho * torch.cos(ph), rho * torch.sin(ph), r * torch.sin(th)], 1)
+
+    S = build_surface(fmap, pdata, p, q, kind="torus")
+    return S
