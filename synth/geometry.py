@@ -25,6 +25,14 @@ class Surface:
     # parameters of the per-patch map, kept so targets can be generated on the exact surface
     kind: str = ""
     pdata: np.ndarray = None
+    fmap: object = None     # X = fmap(pdata_rows, s, t) (torch); lets tests evaluate the exact map
+
+    def eval_patch(self, P, s, t):
+        """Exact map of patch P at reference points (s, t): X, X_s, X_t  (numpy [k,3] each)."""
+        s = np.atleast_1d(np.asarray(s, np.float64))
+        t = np.atleast_1d(np.asarray(t, np.float64))
+        rows = torch.as_tensor(self.pdata[P:P + 1]).repeat(s.size, 1)
+        return _eval_map(self.fmap, rows, s, t)
 
     @property
     def n_patches(self):
@@ -94,7 +102,7 @@ def build_surface(fmap, pdata, p, q, kind=""):
     edge_dx = (Xes * np.tile(dsd, P)[:, None] + Xet * np.tile(dtd, P)[:, None]).reshape(P, 3, q, 3)
     return Surface(p=p, q=q, nodes=nodes, normals=normals, weights=weights, verts=verts,
                    edge_x=edge_x, edge_dx=edge_dx, uv=np.stack([s0, t0], 1), kind=kind,
-                   pdata=pdata.numpy())
+                   pdata=pdata.numpy(), fmap=fmap)
 
 
 # ----------------------------------------------------------------------------- icosahedral spheres
@@ -235,3 +243,13 @@ def make_torus_surface(R, r, n_theta, n_phi, p, q):
 
     S = build_surface(fmap, pdata, p, q, kind="torus")
     return S
+
+
+def make_flat_surface(tris, p, q):
+    """Flat triangles [P,3,3] with the affine map (test geometry)."""
+    pdata = torch.as_tensor(np.asarray(tris, np.float64).reshape(-1, 9))
+
+    def fmap(pd, s, t):
+        a, b, c = pd[:, 0:3], pd[:, 3:6], pd[:, 6:9]
+        return a + s[:, None] * (b - a) + t[:, None] * (c - a)
+    return build_surface(fmap, pdata, p, q, kind="flat")
