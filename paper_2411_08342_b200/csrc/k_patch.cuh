@@ -1,0 +1,337 @@
+// Per-patch kernels: frame + edge geometry (reading A2, A4), near balls (A6), Step-3 edge tables
+// (P:L1436-1440), and the least-squares fit operators (Steps 1-2 in matrix mode, reading A1;
+// P:L715-746) by a CTA-level Householder QR.
+#pragma once
+#include "rrq_device.cuh"
+
+namespace rrq {
+
+// Near ball of patch P (reading A6): c_P = sum w x / sum w, R_P = max |x - c_P| over nodes, vertices
+// and edge samples, h_P = max vertex chord.  One warp per patch.  balls[P] = (c, R, h).
+__global__ void k_patch_balls(int64_t n_patches, int n, int q, const double *__restrict__ nodes,
+                              const double *__restrict__ weights, const double *__restrict__ verts,
+                              const double *__restrict__ edge_x, double *__restrict__ balls) {
+  int lane = threadIdx.x & 31;
+  int64_t P = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (P >= n_patches) return;
+  const double *x = nodes + P * n * 3, *w = weights + P * n;
+  double c[3] = {0, 0, 0}, ws = 0;
+  for (int i = lane; i < n; i += 32) {
+    ws += w[i];
+    for (int a = 0; a < 3; ++a) c[a] += w[i] * x[3 * i + a];
+  }
+  ws = warp_sum(ws);
+  for (int a = 0; a < 3; ++a) c[a] = warp_sum(c[a]) / ws;
+  double R = 0;
+  for (int i = lane; i < n + 3 + 3 * q; i += 32) {
+    const double *y = i < n ? x + 3 * i : (i < n + 3 ? verts + P * 9 + 3 * (i - n) : edge_x + (P * 3 * q + (i - n - 3)) * 3);
+    double d[3] = {y[0] - c[0], y[1] - c[1], y[2] - c[2]};
+    R = fmax(R, sqrt(dot3(d, d)));
+  }
+  for (int o = 16; o > 0; o >>= 1) R = fmax(R, __shfl_xor_sync(0xffffffffu, R, o));
+  double h = 0;
+  for (int e = 0; e < 3; ++e) {
+    const double *a = verts + P * 9 + 3 * e, *b = verts + P * 9 + 3 * ((e + 1) % 3);
+    double d[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+    h = fmax(h, sqrt(dot3(d, d)));
+  }
+  if (lane == 0) {
+    double *o = balls + P * 5;
+    o[0] = c[0]; o[1] = c[1]; o[2] = c[2]; o[3] = R; o[4] = h;
+  }
+}
+
+// Frame, local edge samples / tangents, monomial coefficients C = U y, height range.
+// One CTA (128 threads) per patch.
+template <int P>
+__global__ void k_patch_geom(int64_t n_patches, const double *__restrict__ nodes, const double *__restrict__ verts,
+                             const double *__restrict__ edge_x, const double *__restrict__ edge_dx,
+                             const double *__restrict__ balls, Tables T, double *__restrict__ fit) {
+  using D = Dims<P>;
+  using L = Layout<P>;
+  int64_t Pp = blockIdx.x;
+  if (Pp >= n_patches) return;
+  double *blk = fit + Pp * (int64_t)L::STRIDE;
+  __shared__ double fr[13];
+  __shared__ double red[2][128];
+  const double *v = verts + Pp * 9;
+  if (threadIdx.x == 0) {
+    double a[3], b[3], z[3], e1[3], e2[3];
+    for (int i = 0; i < 3; ++i) {
+      fr[i] = (v[i] + v[3 + i] + v[6 + i]) / 3.0;
+      a[i] = v[3 + i] - v[i];
+      b[i] = v[6 + i] - v[i];
+    }
+    cross3(a, b, z);
+    double nz = sqrt(dot3(z, z)), na = sqrt(dot3(a, a));
+    for (int i = 0; i < 3; ++i) { z[i] /= nz; e1[i] = a[i] / na; }
+    cross3(z, e1, e2);
+    for (int i = 0; i < 3; ++i) { fr[3 + i] = e1[i]; fr[6 + i] = e2[i]; fr[9 + i] = z[i]; }
+    fr[12] = balls[Pp * 5 + 4];   // h_P = max vertex chord
+  }
+  __syncthreads();
+  const double *o = fr, *Rm = fr + 3;
+  double invh = 1.0 / fr[12];
+  auto loc = [&](const double *x, double *y) {
+    double d[3] = {x[0] - o[0], x[1] - o[1], x[2] - o[2]};
+    for (int r = 0; r < 3; ++r) y[r] = (Rm[3 * r] * d[0] + Rm[3 * r + 1] * d[1] + Rm[3 * r + 2] * d[2]) * invh;
+  };
+  double zlo = 1e300, zhi = -1e300;
+  for (int k = threadIdx.x; k < D::E; k += blockDim.x) {
+    double y[3], t[3];
+    loc(edge_x + (Pp * D::E + k) * 3, y);
+    const double *dx = edge_dx + (Pp * D::E + k) * 3;
+    for (int r = 0; r < 3; ++r) t[r] = (Rm[3 * r] * dx[0] + Rm[3 * r + 1] * dx[1] + Rm[3 * r + 2] * dx[2]) * invh;
+    for (int r = 0; r < 3; ++r) { blk[L::YL + 3 * k + r] = y[r]; blk[L::TL + 3 * k + r] = t[r]; }
+    zlo = fmin(zlo, y[2]); zhi = fmax(zhi, y[2]);
+  }
+  for (int i = threadIdx.x; i < D::N; i += blockDim.x) {
+    double y[3];
+    loc(nodes + (Pp * D::N + i) * 3, y);
+    zlo = fmin(zlo, y[2]); zhi = fmax(zhi, y[2]);
+  }
+  if (threadIdx.x < 3) {
+    double y[3];
+    loc(v + 3 * threadIdx.x, y);
+    for (int r = 0; r < 3; ++r) blk[L::HDR + H_VL + 3 * threadIdx.x + r] = y[r];
+    zlo = fmin(zlo, y[2]); zhi = fmax(zhi, y[2]);
+  }
+  red[0][threadIdx.x] = zlo;
+  red[1][threadIdx.x] = zhi;
+  __syncthreads();
+  // edge interpolant coefficients C[e][c][a] = sum_k U[c][k] y[e][k][a]
+  for (int t = threadIdx.x; t < 9 * D::Q; t += blockDim.x) {
+    int e = t / (3 * D::Q), c = (t / 3) % D::Q, a = t % 3;
+    double s = 0;
+    for (int k = 0; k < D::Q; ++k) s += T.U[c * D::Q + k] * blk[L::YL + 3 * (e * D::Q + k) + a];
+    blk[L::CM + t] = s;
+  }
+  if (threadIdx.x == 0) {
+    double lo = 1e300, hi = -1e300;
+    for (int i = 0; i < blockDim.x; ++i) { lo = fmin(lo, red[0][i]); hi = fmax(hi, red[1][i]); }
+    for (int i = 0; i < 3; ++i) blk[L::HDR + H_O + i] = fr[i];
+    for (int i = 0; i < 9; ++i) blk[L::HDR + H_RM + i] = fr[3 + i];
+    blk[L::HDR + H_H] = fr[12];
+    blk[L::HDR + H_ZLO] = lo;
+    blk[L::HDR + H_ZHI] = hi;
+    for (int i = 0; i < 3; ++i) blk[L::HDR + H_CP + i] = balls[Pp * 5 + i];
+    blk[L::HDR + H_RP] = balls[Pp * 5 + 3];
+    blk[L::HDR + H_HP] = balls[Pp * 5 + 4];
+  }
+}
+
+// Step 3 edge tables, one thread per (patch, edge node):  g^{(j,k)} = Hess S^{(j,k)}(y) tau (2<=j<=p),
+// e^{(j,k)} = grad S^{(j,k)}(y) x tau (1<=j<=p), k >= 0, stored lane-coalesced [kappa][a][re/im][jk].
+template <int P>
+__global__ void k_edge_tables(int64_t n_patches, double *__restrict__ fit) {
+  using D = Dims<P>;
+  using L = Layout<P>;
+  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n_patches * D::E) return;
+  int64_t Pp = gid / D::E;
+  int kap = gid % D::E;
+  double *blk = fit + Pp * (int64_t)L::STRIDE;
+  double y[3], t[3];
+  for (int a = 0; a < 3; ++a) { y[a] = blk[L::YL + 3 * kap + a]; t[a] = blk[L::TL + 3 * kap + a]; }
+  cd R[D::NS];
+  r_table<P>(y[1], y[2], y[0], R);
+  double *GT = blk + L::GT + (int64_t)kap * 6 * D::NQ, *ET = blk + L::ET + (int64_t)kap * 6 * D::NV;
+  for (int j = 1; j <= P; ++j)
+    for (int k = 0; k <= j; ++k) {
+      cd g[3];
+      gradS(R, j, k, g);
+      cd e[3] = {g[1] * mk(t[2], 0) - g[2] * mk(t[1], 0), g[2] * mk(t[0], 0) - g[0] * mk(t[2], 0),
+                 g[0] * mk(t[1], 0) - g[1] * mk(t[0], 0)};
+      int vi = vidx(j, k);
+      for (int a = 0; a < 3; ++a) { ET[(2 * a) * D::NV + vi] = e[a].x; ET[(2 * a + 1) * D::NV + vi] = e[a].y; }
+      if (j >= 2) {
+        cd h[3];
+        hessS_v(R, j, k, t, h);
+        int qi = qidx(j, k);
+        for (int a = 0; a < 3; ++a) { GT[(2 * a) * D::NQ + qi] = h[a].x; GT[(2 * a + 1) * D::NQ + qi] = h[a].y; }
+      }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Fit operators.  One CTA (256 threads = 8 warps) per patch, persistent over patches; workspace per
+// CTA in global memory.  Householder QR (column-major, warp per column), Q^T formed on the identity,
+// back substitution -> A^+ (reading A1).
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+  v = warp_sum(v);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
+  return s;
+}
+
+// In-place pseudo-inverse of the m x k column-major matrix A (m >= k): writes X = A^+ (k x m,
+// column-major, ld = k) into Xo.  W: workspace m*m doubles (holds Q^T applied to I), rd: k doubles,
+// beta: k doubles.  Returns 1 if rank deficient (|R_jj| <= 1e-13 max|R_jj|).
+__device__ int cta_pinv(int m, int k, double *A, double *W, double *Xo, double *rd, double *beta, double *sh) {
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = 0; j < k; ++j) {
+    double *col = A + (int64_t)j * m;
+    double s = 0;
+    for (int i = j + threadIdx.x; i < m; i += blockDim.x) s += col[i] * col[i];
+    double nrm = sqrt(block_sum(s, sh));
+    double ajj = col[j];
+    double alpha = ajj > 0 ? -nrm : nrm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      col[j] = ajj - alpha;               // v_j (v stored in place, v_i = A_ij for i > j)
+      rd[j] = alpha;                      // R_jj
+      beta[j] = nrm * (nrm + fabs(ajj));  // v.v / 2
+    }
+    __syncthreads();
+    double bj = beta[j];
+    if (bj > 0)
+      for (int c = j + 1 + warp; c < k; c += nw) {
+        double *cc = A + (int64_t)c * m;
+        double d = 0;
+        for (int i = j + lane; i < m; i += 32) d += col[i] * cc[i];
+        d = warp_sum(d) / bj;
+        for (int i = j + lane; i < m; i += 32) cc[i] -= d * col[i];
+      }
+    __syncthreads();
+  }
+  // Q^T applied to the m unit vectors (W column-major m x m): only the first k rows are needed.
+  for (int c = warp; c < m; c += nw) {
+    double *w = W + (int64_t)c * m;
+    for (int i = lane; i < m; i += 32) w[i] = (i == c) ? 1.0 : 0.0;
+    __syncwarp();
+    for (int j = 0; j < k; ++j) {
+      double bj = beta[j];
+      if (!(bj > 0)) continue;
+      const double *col = A + (int64_t)j * m;
+      double d = 0;
+      for (int i = j + lane; i < m; i += 32) d += col[i] * w[i];
+      d = warp_sum(d) / bj;
+      for (int i = j + lane; i < m; i += 32) w[i] -= d * col[i];
+      __syncwarp();
+    }
+    // back substitution R x = (Q^T e_c)[0:k]; R_jj = rd[j], R_ji (i > j) = A[i*m + j]
+    if (lane == 0)
+      for (int r = k - 1; r >= 0; --r) {
+        double s = w[r];
+        for (int cc = r + 1; cc < k; ++cc) s -= A[(int64_t)cc * m + r] * w[cc];
+        w[r] = s / rd[r];
+      }
+    __syncwarp();
+    for (int r = lane; r < k; r += 32) Xo[(int64_t)c * k + r] = w[r];
+  }
+  __syncthreads();
+  double rmax = 0;
+  for (int j = 0; j < k; ++j) rmax = fmax(rmax, fabs(rd[j]));
+  int def = 0;
+  for (int j = 0; j < k; ++j) def |= fabs(rd[j]) <= 1e-13 * rmax;
+  return def;
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_patch_fit(int64_t n_patches, const double *__restrict__ nodes,
+                                                   const double *__restrict__ normals, double *__restrict__ fit,
+                                                   double *__restrict__ work, int32_t *__restrict__ status) {
+  using D = Dims<P>;
+  using L = Layout<P>;
+  constexpr int N = D::N, NP = D::NP, M4 = 4 * N, K4 = 4 * NP;
+  constexpr int64_t WS = (int64_t)M4 * K4 + (int64_t)M4 * M4 + (int64_t)K4 * M4 + 3 * N * NP + N * NP + 2 * N * N;
+  double *A = work + blockIdx.x * WS;
+  double *W = A + (int64_t)M4 * K4;
+  double *X = W + (int64_t)M4 * M4;
+  double *F = X + (int64_t)K4 * M4;   // [3][N][NP]
+  double *Hm = F + 3 * N * NP;        // [N][NP]
+  double *HP = Hm + N * NP;           // [N][N]
+  __shared__ double sh[32], rd[4 * 55], beta[4 * 55], xl[3 * 100], nl[3 * 100];
+  for (int64_t Pp = blockIdx.x; Pp < n_patches; Pp += gridDim.x) {
+    double *blk = fit + Pp * (int64_t)L::STRIDE;
+    const double *o = blk + L::HDR + H_O, *Rm = blk + L::HDR + H_RM;
+    double invh = 1.0 / blk[L::HDR + H_H];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double *x = nodes + (Pp * N + i) * 3, *nu = normals + (Pp * N + i) * 3;
+      double d[3] = {x[0] - o[0], x[1] - o[1], x[2] - o[2]};
+      for (int r = 0; r < 3; ++r) {
+        xl[3 * i + r] = (Rm[3 * r] * d[0] + Rm[3 * r + 1] * d[1] + Rm[3 * r + 2] * d[2]) * invh;
+        nl[3 * i + r] = Rm[3 * r] * nu[0] + Rm[3 * r + 1] * nu[1] + Rm[3 * r + 2] * nu[2];
+      }
+    }
+    __syncthreads();
+    // F_{a,i,lm} = d_a H^{(l,m)}(x_i), Hm_{i,lm} = H^{(l,m)}(x_i), H = sqrt2 Im S
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      cd R[D::NS];
+      r_table<P>(xl[3 * i + 1], xl[3 * i + 2], xl[3 * i], R);
+      for (int l = 1; l <= P; ++l)
+        for (int m = 1; m <= l; ++m) {
+          cd g[3];
+          gradS(R, l, m, g);
+          int c = lmidx(l, m);
+          for (int a = 0; a < 3; ++a) F[(a * N + i) * NP + c] = 1.4142135623730950488 * g[a].y;
+          Hm[i * NP + c] = 1.4142135623730950488 * R[sidx(l, m)].y;
+        }
+    }
+    __syncthreads();
+    // A (M4 x K4, column-major): blocks [[0,-F1,-F2,-F3],[F1,0,-F3,F2],[F2,F3,0,-F1],[F3,-F2,F1,0]]
+    const int blkmap[4][4] = {{0, -1, -2, -3}, {1, 0, -3, 2}, {2, 3, 0, -1}, {3, -2, 1, 0}};
+    for (int64_t t = threadIdx.x; t < (int64_t)M4 * K4; t += blockDim.x) {
+      int col = t / M4, row = t % M4;
+      int br = row / N, i = row % N, bc = col / NP, c = col % NP;
+      int s = blkmap[br][bc];
+      A[t] = s == 0 ? 0.0 : (s > 0 ? 1.0 : -1.0) * F[((abs(s) - 1) * N + i) * NP + c];
+    }
+    __syncthreads();
+    int st = cta_pinv(M4, K4, A, W, X, rd, beta, sh);
+    // X = A^+ column-major (K4 x M4): X[c * K4 + r].  P_D[r][i] = X[i][r]; P_Sp[r][i] = sum_a nu_a X[(a+1)N+i][r]
+    double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
+    for (int t = threadIdx.x; t < K4 * N; t += blockDim.x) {
+      int r = t / N, i = t % N;
+      PD[t] = X[(int64_t)i * K4 + r];
+      double s = 0;
+      for (int a = 0; a < 3; ++a) s += nl[3 * i + a] * X[(int64_t)((a + 1) * N + i) * K4 + r];
+      PSp[t] = s;
+    }
+    __syncthreads();
+    // B (N x NP) = F . nu -> P_Sd = B^+ 
+    for (int t = threadIdx.x; t < N * NP; t += blockDim.x) {
+      int c = t / N, i = t % N;
+      double s = 0;
+      for (int a = 0; a < 3; ++a) s += F[(a * N + i) * NP + c] * nl[3 * i + a];
+      A[t] = s;   // column-major (N x NP)
+    }
+    __syncthreads();
+    st |= cta_pinv(N, NP, A, W, X, rd, beta, sh);
+    for (int t = threadIdx.x; t < NP * N; t += blockDim.x) {
+      int r = t / N, i = t % N;
+      PSd[t] = X[(int64_t)i * NP + r];
+    }
+    __syncthreads();
+    // P_Sg = P_D (Hm P_Sd)
+    for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
+      int i = t / N, j = t % N;
+      double s = 0;
+      for (int c = 0; c < NP; ++c) s += Hm[i * NP + c] * PSd[c * N + j];
+      HP[t] = s;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < K4 * N; t += blockDim.x) {
+      int r = t / N, j = t % N;
+      double s = 0;
+      for (int i = 0; i < N; ++i) s += PD[r * N + i] * HP[i * N + j];
+      PSg[t] = s;
+    }
+    if (threadIdx.x == 0 && status) status[Pp] = st;
+    __syncthreads();
+  }
+}
+
+template <int P>
+constexpr int64_t fit_workspace_doubles() {
+  using D = Dims<P>;
+  constexpr int64_t M4 = 4 * D::N, K4 = 4 * D::NP;
+  return M4 * K4 + M4 * M4 + K4 * M4 + 3 * D::N * D::NP + D::N * D::NP + 2 * D::N * D::N;
+}
+
+}  // namespace rrq

@@ -1,0 +1,458 @@
+// C ABI of librrq.so (include/rrq.h): argument validation, scratch management, launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rrq.h"
+#include "k_build.cuh"
+#include "k_near.cuh"
+#include "k_patch.cuh"
+
+namespace rrq_host {
+void gauss_legendre(int n, double *x, double *w);
+void vandermonde_inverse(int n, const double *t, double *U);
+}  // namespace rrq_host
+
+using namespace rrq;
+
+struct rrq_ctx_s {
+  rrq_params prm;
+  std::string err;
+  int64_t launches = 0;
+  int num_sms = 148;
+  // constant tables (device) + host copies
+  double *d_tab = nullptr;
+  Tables T;
+  std::vector<double> h_t, h_w, h_U;
+  // scratch
+  struct Buf {
+    void *p = nullptr;
+    size_t n = 0;
+  };
+  Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one;
+};
+
+static thread_local std::string g_create_err;
+
+static rrq_status fail(rrq_ctx c, rrq_status s, const std::string &m) {
+  if (c) c->err = m; else g_create_err = m;
+  return s;
+}
+
+static rrq_status cuda_check(rrq_ctx c, const char *where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, RRQ_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return RRQ_OK;
+}
+
+static bool ensure(rrq_ctx c, rrq_ctx_s::Buf &b, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  if (b.n >= bytes) return true;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.n = 0;
+  if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    c->err = "scratch allocation of " + std::to_string(bytes) + " bytes failed";
+    return false;
+  }
+  b.n = bytes;
+  return true;
+}
+
+template <typename T>
+static T *bp(rrq_ctx_s::Buf &b) { return reinterpret_cast<T *>(b.p); }
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// Exported functions get C linkage from their declarations in include/rrq.h.
+
+rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
+  if (!out) return fail(nullptr, RRQ_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!params) return fail(nullptr, RRQ_ERR_INVALID_ARG, "params is NULL");
+  const rrq_params &p = *params;
+  if (p.p != 4 && p.p != 6 && p.p != 8 && p.p != 10)
+    return fail(nullptr, RRQ_ERR_NOT_IMPLEMENTED, "p must be one of 4, 6, 8, 10");
+  if (p.n_nodes != p.p * p.p) return fail(nullptr, RRQ_ERR_INVALID_ARG, "n_nodes must be p*p (collapsed GL, A1)");
+  if (p.p_edge != 2 * p.p) return fail(nullptr, RRQ_ERR_NOT_IMPLEMENTED, "p_edge must be 2p (reading A4)");
+  if (p.n_omega < 1 || p.n_omega > 128) return fail(nullptr, RRQ_ERR_INVALID_ARG, "n_omega must be in [1,128]");
+  if (!(p.rho_swap > 1.0)) return fail(nullptr, RRQ_ERR_INVALID_ARG, "rho_swap must be > 1");
+  if (!(p.eta >= 0.0)) return fail(nullptr, RRQ_ERR_INVALID_ARG, "eta must be >= 0");
+  rrq_ctx c = new rrq_ctx_s();
+  c->prm = p;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  int q = p.p_edge, no = p.n_omega;
+  c->h_t.resize(q);
+  c->h_w.resize(q);
+  c->h_U.resize(q * q);
+  rrq_host::gauss_legendre(q, c->h_t.data(), c->h_w.data());
+  rrq_host::vandermonde_inverse(q, c->h_t.data(), c->h_U.data());
+  std::vector<double> xo(no), wo(no), sqb(41 * 41, 0.0);
+  rrq_host::gauss_legendre(no, xo.data(), wo.data());
+  for (int n = 0; n <= 40; ++n) {
+    double b = 1;
+    for (int k = 0; k <= n; ++k) {
+      sqb[n * 41 + k] = std::sqrt(b);
+      b = b * (n - k) / (k + 1);
+    }
+  }
+  size_t tot = 2 * q + q * q + 2 * no + 41 * 41;
+  if (cudaMalloc(&c->d_tab, tot * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return fail(nullptr, RRQ_ERR_CUDA, "cudaMalloc of constant tables failed (no CUDA device?)");
+  }
+  std::vector<double> h(tot);
+  double *t = h.data();
+  std::copy(c->h_t.begin(), c->h_t.end(), t);
+  std::copy(c->h_w.begin(), c->h_w.end(), t + q);
+  std::copy(c->h_U.begin(), c->h_U.end(), t + 2 * q);
+  std::copy(xo.begin(), xo.end(), t + 2 * q + q * q);
+  std::copy(wo.begin(), wo.end(), t + 2 * q + q * q + no);
+  std::copy(sqb.begin(), sqb.end(), t + 2 * q + q * q + 2 * no);
+  cudaMemcpy(c->d_tab, h.data(), tot * sizeof(double), cudaMemcpyHostToDevice);
+  c->T.tgl = c->d_tab;
+  c->T.wgl = c->d_tab + q;
+  c->T.U = c->d_tab + 2 * q;
+  c->T.xo = c->d_tab + 2 * q + q * q;
+  c->T.wo = c->T.xo + no;
+  c->T.sqb = c->T.wo + no;
+  if (cuda_check(c, "rrq_create") != RRQ_OK) {
+    g_create_err = c->err;
+    rrq_destroy(c);
+    return RRQ_ERR_CUDA;
+  }
+  *out = c;
+  return RRQ_OK;
+}
+
+void rrq_destroy(rrq_ctx c) {
+  if (!c) return;
+  cudaFree(c->d_tab);
+  for (auto *b : {&c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
+                  &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
+    if (b->p) cudaFree(b->p);
+  delete c;
+}
+
+const char *rrq_last_error(rrq_ctx c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int64_t rrq_launch_count(rrq_ctx c) { return c ? c->launches : 0; }
+
+rrq_status rrq_get_tables(rrq_ctx c, double *t, double *w, double *U) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  int q = c->prm.p_edge;
+  if (t) std::copy(c->h_t.begin(), c->h_t.end(), t);
+  if (w) std::copy(c->h_w.begin(), c->h_w.end(), w);
+  if (U) std::copy(c->h_U.begin(), c->h_U.end(), U);
+  (void)q;
+  return RRQ_OK;
+}
+
+static rrq_status check_surface(rrq_ctx c, const rrq_surface *s) {
+  if (!s) return fail(c, RRQ_ERR_INVALID_ARG, "surface is NULL");
+  if (s->n_patches <= 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_patches must be > 0");
+  if (s->n_patches > (int64_t)INT32_MAX / c->prm.n_nodes) return fail(c, RRQ_ERR_CAPACITY, "too many nodes for int32 col_idx");
+  if (!s->nodes || !s->normals || !s->weights || !s->verts || !s->edge_x || !s->edge_dx)
+    return fail(c, RRQ_ERR_INVALID_ARG, "surface arrays must be non-NULL device pointers");
+  return RRQ_OK;
+}
+
+static rrq_status check_targets(rrq_ctx c, const rrq_targets *t) {
+  if (!t) return fail(c, RRQ_ERR_INVALID_ARG, "targets is NULL");
+  if (t->n_targets < 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_targets < 0");
+  if (t->n_targets > 0 && !t->x) return fail(c, RRQ_ERR_INVALID_ARG, "targets x is NULL");
+  return RRQ_OK;
+}
+
+static rrq_status compute_balls(rrq_ctx c, const rrq_surface *s, cudaStream_t st) {
+  if (!ensure(c, c->balls, s->n_patches * 5 * sizeof(double))) return RRQ_ERR_CUDA;
+  k_patch_balls<<<nblk(s->n_patches, 4), 128, 0, st>>>(s->n_patches, c->prm.n_nodes, c->prm.p_edge, s->nodes,
+                                                       s->weights, s->verts, s->edge_x, bp<double>(c->balls));
+  c->launches++;
+  return cuda_check(c, "k_patch_balls");
+}
+
+rrq_status rrq_near_list(rrq_ctx c, const rrq_surface *s, const rrq_targets *tg, int64_t *pair_ptr,
+                         int32_t *pair_patch, int64_t *n_pairs, rrq_stream_t stream) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  rrq_status r;
+  if ((r = check_surface(c, s)) || (r = check_targets(c, tg))) return r;
+  if (!pair_ptr || !n_pairs) return fail(c, RRQ_ERR_INVALID_ARG, "pair_ptr and n_pairs must be non-NULL");
+  const int64_t T = tg->n_targets, Pn = s->n_patches;
+  const int fill = pair_patch != nullptr;
+  if (T == 0) {
+    if (!fill) {
+      cudaMemsetAsync(pair_ptr, 0, sizeof(int64_t), st);
+      *n_pairs = 0;
+    }
+    return cuda_check(c, "rrq_near_list");
+  }
+  if (c->prm.all_pairs) {
+    if (!fill) {
+      k_near_all<<<nblk(T, 256), 256, 0, st>>>(T, Pn, 0, pair_ptr, nullptr);
+      if (!ensure(c, c->one, 64)) return RRQ_ERR_CUDA;
+      k_scan_i64<<<1, 1024, 0, st>>>(T + 1, pair_ptr, bp<int64_t>(c->one));
+      c->launches += 2;
+      cudaMemcpyAsync(n_pairs, bp<int64_t>(c->one), sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+    } else {
+      k_near_all<<<nblk(T, 256), 256, 0, st>>>(T, Pn, 1, pair_ptr, pair_patch);
+      c->launches++;
+    }
+    return cuda_check(c, "rrq_near_list(all)");
+  }
+  if ((r = compute_balls(c, s, st))) return r;
+  std::vector<double> hb(Pn * 5);
+  cudaMemcpyAsync(hb.data(), c->balls.p, Pn * 5 * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300}, rmax = 0;
+  for (int64_t P = 0; P < Pn; ++P) {
+    for (int a = 0; a < 3; ++a) { lo[a] = std::min(lo[a], hb[P * 5 + a]); hi[a] = std::max(hi[a], hb[P * 5 + a]); }
+    rmax = std::max(rmax, hb[P * 5 + 3] + c->prm.eta * hb[P * 5 + 4]);
+  }
+  Grid g;
+  double cell = std::max(rmax, 1e-300);
+  for (;;) {
+    int64_t tot = 1;
+    for (int a = 0; a < 3; ++a) {
+      g.lo[a] = lo[a] - cell;
+      g.dim[a] = (int)std::max<int64_t>(1, (int64_t)std::ceil((hi[a] - lo[a] + 2 * cell) / cell));
+      tot *= g.dim[a];
+    }
+    if (tot <= (1 << 22)) break;
+    cell *= 1.26;
+  }
+  g.inv_cell = 1.0 / cell;
+  const int ncell = g.dim[0] * g.dim[1] * g.dim[2];
+  if (!ensure(c, c->cell_cnt, (ncell + 1) * sizeof(int32_t)) || !ensure(c, c->cell_items, Pn * sizeof(int32_t)) ||
+      !ensure(c, c->patch_cell, Pn * sizeof(int32_t)) || !ensure(c, c->cursor, (ncell + 1) * sizeof(int32_t)) ||
+      !ensure(c, c->one, 64))
+    return RRQ_ERR_CUDA;
+  cudaMemsetAsync(c->cell_cnt.p, 0, (ncell + 1) * sizeof(int32_t), st);
+  k_cell_count<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<double>(c->balls), g, bp<int32_t>(c->cell_cnt), bp<int32_t>(c->patch_cell));
+  k_scan_i32<<<1, 1024, 0, st>>>(ncell + 1, bp<int32_t>(c->cell_cnt), bp<int32_t>(c->one));
+  cudaMemcpyAsync(c->cursor.p, c->cell_cnt.p, (ncell + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+  k_cell_fill<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<int32_t>(c->patch_cell), bp<int32_t>(c->cursor), bp<int32_t>(c->cell_items));
+  c->launches += 3;
+  if (!fill) {
+    k_near_targets<<<nblk(T, 128), 128, 0, st>>>(T, tg->x, tg->self_node, c->prm.n_nodes, bp<double>(c->balls),
+                                                 c->prm.eta, g, bp<int32_t>(c->cell_cnt), bp<int32_t>(c->cell_items), 0,
+                                                 pair_ptr, nullptr);
+    cudaMemsetAsync(pair_ptr + T, 0, sizeof(int64_t), st);
+    k_scan_i64<<<1, 1024, 0, st>>>(T + 1, pair_ptr, bp<int64_t>(c->one));
+    c->launches += 2;
+    cudaMemcpyAsync(n_pairs, c->one.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+  } else {
+    k_near_targets<<<nblk(T, 128), 128, 0, st>>>(T, tg->x, tg->self_node, c->prm.n_nodes, bp<double>(c->balls),
+                                                 c->prm.eta, g, bp<int32_t>(c->cell_cnt), bp<int32_t>(c->cell_items), 1,
+                                                 pair_ptr, pair_patch);
+    c->launches++;
+  }
+  return cuda_check(c, "rrq_near_list");
+}
+
+template <int P>
+static size_t stride_bytes() { return (size_t)Layout<P>::STRIDE * sizeof(double); }
+
+size_t rrq_fit_bytes(rrq_ctx c, int64_t n_patches) {
+  if (!c || n_patches <= 0) return 0;
+  size_t s = 0;
+  switch (c->prm.p) {
+    case 4: s = stride_bytes<4>(); break;
+    case 6: s = stride_bytes<6>(); break;
+    case 8: s = stride_bytes<8>(); break;
+    case 10: s = stride_bytes<10>(); break;
+  }
+  return s * (size_t)n_patches;
+}
+
+template <int P>
+static rrq_status patch_fit_impl(rrq_ctx c, const rrq_surface *s, double *fit, int32_t *status, cudaStream_t st) {
+  using D = Dims<P>;
+  const int64_t Pn = s->n_patches;
+  rrq_status r;
+  if ((r = compute_balls(c, s, st))) return r;
+  k_patch_geom<P><<<(unsigned)Pn, 128, 0, st>>>(Pn, s->nodes, s->verts, s->edge_x, s->edge_dx, bp<double>(c->balls), c->T, fit);
+  k_edge_tables<P><<<nblk(Pn * D::E, 128), 128, 0, st>>>(Pn, fit);
+  c->launches += 2;
+  if ((r = cuda_check(c, "k_patch_geom/k_edge_tables"))) return r;
+  int grid = (int)std::min<int64_t>(Pn, 2 * c->num_sms);
+  constexpr int64_t WS = fit_workspace_doubles<P>();
+  if (!ensure(c, c->fitwork, (size_t)grid * WS * sizeof(double))) return RRQ_ERR_CUDA;
+  k_patch_fit<P><<<grid, 256, 0, st>>>(Pn, s->nodes, s->normals, fit, bp<double>(c->fitwork), status);
+  c->launches++;
+  return cuda_check(c, "k_patch_fit");
+}
+
+rrq_status rrq_patch_fit(rrq_ctx c, const rrq_surface *s, void *fit, int32_t *patch_status, rrq_stream_t stream) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  rrq_status r;
+  if ((r = check_surface(c, s))) return r;
+  if (!fit) return fail(c, RRQ_ERR_INVALID_ARG, "fit is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (c->prm.p) {
+    case 4: return patch_fit_impl<4>(c, s, (double *)fit, patch_status, st);
+    case 6: return patch_fit_impl<6>(c, s, (double *)fit, patch_status, st);
+    case 8: return patch_fit_impl<8>(c, s, (double *)fit, patch_status, st);
+    case 10: return patch_fit_impl<10>(c, s, (double *)fit, patch_status, st);
+  }
+  return RRQ_ERR_NOT_IMPLEMENTED;
+}
+
+constexpr int kWPB = 4;
+
+template <int P>
+static size_t zeta_smem(int n_omega) {
+  using D = Dims<P>;
+  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + (2 * P + 1) * (2 * P + 1) + (2 * P + 2);
+  tab = (tab + 1) & ~1;
+  return (size_t)tab * sizeof(double) + kWPB * sizeof(WarpScratch<P>);
+}
+
+template <int P>
+static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets *tg, const int64_t *pair_ptr,
+                             const int32_t *pair_patch, int64_t row_begin, int64_t row_end, const double *fit,
+                             uint32_t mask, int64_t *row_ptr, int32_t *col_idx, double *const vals[4], int32_t *pstat,
+                             cudaStream_t st) {
+  using D = Dims<P>;
+  using CC = ContractCfg<P>;
+  const int64_t Pn = s->n_patches;
+  const int raw = (mask & RRQ_RAW) ? 1 : 0;
+  int64_t b[2];
+  cudaMemcpyAsync(&b[0], pair_ptr + row_begin, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&b[1], pair_ptr + row_end, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  const int64_t obase = b[0], total = b[1] - b[0];
+  // sub-chunks of rows bounded by the Z scratch (<= max_pairs pairs each)
+  const int64_t max_pairs = std::max<int64_t>(1 << 16, (int64_t)(6e9 / (D::NZ * 8.0)));
+  std::vector<int64_t> hptr;
+  std::vector<std::pair<int64_t, int64_t>> subs;
+  if (total <= max_pairs) {
+    subs.push_back({row_begin, row_end});
+  } else {
+    hptr.resize(row_end - row_begin + 1);
+    cudaMemcpyAsync(hptr.data(), pair_ptr + row_begin, hptr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    int64_t r0 = row_begin;
+    while (r0 < row_end) {
+      int64_t lim = hptr[r0 - row_begin] + max_pairs;
+      int64_t r1 = std::upper_bound(hptr.begin() + (r0 - row_begin), hptr.end(), lim) - hptr.begin() + row_begin - 1;
+      if (r1 <= r0) r1 = r0 + 1;   // a single row larger than the cap: take it whole
+      r1 = std::min(r1, row_end);
+      subs.push_back({r0, r1});
+      r0 = r1;
+    }
+  }
+  int64_t maxsub = 0;
+  for (auto &sr : subs) {
+    int64_t np_ = (hptr.empty() ? total : hptr[sr.second - row_begin] - hptr[sr.first - row_begin]);
+    maxsub = std::max(maxsub, np_);
+  }
+  if (!ensure(c, c->ptgt, maxsub * sizeof(int64_t)) || !ensure(c, c->perm, maxsub * sizeof(int64_t)) ||
+      !ensure(c, c->seg, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->cursor, (Pn + 1) * sizeof(int64_t)) ||
+      !ensure(c, c->items, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->Z, (size_t)maxsub * D::NZ * sizeof(double)) ||
+      !ensure(c, c->one, 64))
+    return RRQ_ERR_CUDA;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_pair_zeta<P, kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  for (auto &sr : subs) {
+    const int64_t r0 = sr.first, r1 = sr.second;
+    const int64_t kb = hptr.empty() ? obase : hptr[r0 - row_begin];
+    const int64_t np_ = hptr.empty() ? total : hptr[r1 - row_begin] - kb;
+    if (np_ == 0) continue;
+    // pair -> target (and, for the first sub-chunk, nothing else)
+    k_pair_targets<<<nblk(r1 - r0 + 1, 256), 256, 0, st>>>(r0, r1, pair_ptr, kb, bp<int64_t>(c->ptgt),
+                                                            nullptr, D::N);
+    // patch-major permutation (counting sort)
+    cudaMemsetAsync(c->seg.p, 0, (Pn + 1) * sizeof(int64_t), st);
+    k_patch_hist<<<nblk(np_, 256), 256, 0, st>>>(np_, kb, pair_patch, bp<int64_t>(c->seg));
+    k_scan_i64<<<1, 1024, 0, st>>>(Pn + 1, bp<int64_t>(c->seg), bp<int64_t>(c->one));
+    cudaMemcpyAsync(c->cursor.p, c->seg.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
+    k_patch_scatter<<<nblk(np_, 256), 256, 0, st>>>(np_, kb, pair_patch, bp<int64_t>(c->cursor), bp<int64_t>(c->perm));
+    k_items<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<int64_t>(c->seg), CC::TILE, bp<int64_t>(c->items));
+    cudaMemsetAsync(bp<int64_t>(c->items) + Pn, 0, sizeof(int64_t), st);
+    k_scan_i64<<<1, 1024, 0, st>>>(Pn + 1, bp<int64_t>(c->items), bp<int64_t>(c->one) + 1);
+    c->launches += 6;
+    int64_t n_items = 0;
+    cudaMemcpyAsync(&n_items, bp<int64_t>(c->one) + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    // zeta
+    size_t sm = zeta_smem<P>(c->prm.n_omega);
+    int64_t want = (np_ + kWPB - 1) / kWPB;
+    unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)c->num_sms * 8);
+    k_pair_zeta<P, kWPB><<<grid, kWPB * 32, sm, st>>>(np_, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), kb, pair_patch,
+                                                       fit, tg->x, tg->normal, tg->self_node, tg->side, c->T,
+                                                       c->prm.n_omega, c->prm.rho_swap, bp<double>(c->Z),
+                                                       pstat ? pstat + (kb - obase) : nullptr);
+    c->launches++;
+    rrq_status r;
+    if ((r = cuda_check(c, "k_pair_zeta"))) return r;
+    cudaStreamSynchronize(st);   // n_items
+    if (n_items > 0) {
+      k_contract<P><<<(unsigned)n_items, CC::THREADS, 0, st>>>(
+          n_items, bp<int64_t>(c->items), Pn, bp<int64_t>(c->seg), bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), kb,
+          pair_patch, fit, bp<double>(c->Z), s->nodes, s->normals, s->weights, tg->x, tg->normal, tg->self_node,
+          mask, raw, col_idx ? col_idx + (kb - obase) * D::N : nullptr,
+          vals[0] ? vals[0] + (kb - obase) * D::N : nullptr, vals[1] ? vals[1] + (kb - obase) * D::N : nullptr,
+          vals[2] ? vals[2] + (kb - obase) * D::N : nullptr, vals[3] ? vals[3] + (kb - obase) * D::N : nullptr,
+          pstat ? pstat + (kb - obase) : nullptr);
+      c->launches++;
+      if ((r = cuda_check(c, "k_contract"))) return r;
+    }
+  }
+  if (row_ptr) {
+    // row_ptr[i] = (pair_ptr[row_begin + i] - obase) * n
+    k_row_ptr<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase, row_ptr, D::N);
+    c->launches++;
+  }
+  return cuda_check(c, "rrq_build_correction");
+}
+
+rrq_status rrq_build_correction(rrq_ctx c, const rrq_surface *s, const rrq_targets *tg, const int64_t *pair_ptr,
+                                const int32_t *pair_patch, int64_t n_pairs, int64_t row_begin, int64_t row_end,
+                                const void *fit, uint32_t mask, int64_t *row_ptr, int32_t *col_idx,
+                                double *const vals[4], int32_t *pstat, rrq_stream_t stream) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  rrq_status r;
+  if ((r = check_surface(c, s)) || (r = check_targets(c, tg))) return r;
+  if (!pair_ptr || !pair_patch || !fit || !vals) return fail(c, RRQ_ERR_INVALID_ARG, "pair_ptr, pair_patch, fit, vals must be non-NULL");
+  if (row_begin < 0 || row_end < row_begin || row_end > tg->n_targets)
+    return fail(c, RRQ_ERR_INVALID_ARG, "row range must satisfy 0 <= row_begin <= row_end <= n_targets");
+  if (n_pairs < 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_pairs < 0");
+  if ((mask & (RRQ_SP | RRQ_DP)) && !tg->normal) return fail(c, RRQ_ERR_INVALID_ARG, "S' and D' need target normals");
+  if ((mask & RRQ_ALL) == 0) return fail(c, RRQ_ERR_INVALID_ARG, "kernel_mask selects no kernel");
+  if (row_end == row_begin) return RRQ_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (c->prm.p) {
+    case 4: return build_impl<4>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
+    case 6: return build_impl<6>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
+    case 8: return build_impl<8>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
+    case 10: return build_impl<10>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
+  }
+  return RRQ_ERR_NOT_IMPLEMENTED;
+}
+
+rrq_status rrq_apply_correction(rrq_ctx c, int64_t n_rows, const int64_t *row_ptr, const int32_t *col_idx,
+                                const double *vals, const double *density, double *y, rrq_stream_t stream) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  if (n_rows < 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_rows < 0");
+  if (n_rows == 0) return RRQ_OK;
+  if (!row_ptr || !col_idx || !vals || !density || !y) return fail(c, RRQ_ERR_INVALID_ARG, "NULL array");
+  k_apply<<<nblk(n_rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(n_rows, row_ptr, col_idx, vals, density, y);
+  c->launches++;
+  return cuda_check(c, "rrq_apply_correction");
+}
+

@@ -1,0 +1,199 @@
+// Device-side building blocks of the RRQ near-correction builder (sm_100a, fp64).
+// Complex arithmetic, regular solid harmonics R_l^m by the Cartesian three-term recurrence, their
+// first/second derivatives (reading A3), quaternion products.  Independent of oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rrq {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+struct cd {
+  double x, y;
+};
+__device__ __forceinline__ cd mk(double x, double y) { return cd{x, y}; }
+__device__ __forceinline__ cd operator+(cd a, cd b) { return cd{a.x + b.x, a.y + b.y}; }
+__device__ __forceinline__ cd operator-(cd a, cd b) { return cd{a.x - b.x, a.y - b.y}; }
+__device__ __forceinline__ cd operator*(cd a, cd b) { return cd{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__device__ __forceinline__ cd operator*(double s, cd a) { return cd{s * a.x, s * a.y}; }
+__device__ __forceinline__ cd conj(cd a) { return cd{a.x, -a.y}; }
+__device__ __forceinline__ cd cdiv(cd a, cd b) {
+  double s = 1.0 / (b.x * b.x + b.y * b.y);
+  return cd{(a.x * b.x + a.y * b.y) * s, (a.y * b.x - a.x * b.y) * s};
+}
+__device__ __forceinline__ double cabs_(cd a) { return hypot(a.x, a.y); }
+// acc += a * b
+__device__ __forceinline__ void cfma(cd &acc, cd a, cd b) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+}
+
+template <int P>
+struct Dims {
+  static constexpr int Q = 2 * P;                 // p~ = 2p edge nodes (reading A4)
+  static constexpr int E = 3 * Q;                 // edge nodes per patch
+  static constexpr int N = P * P;                 // nodes per patch (reading A1)
+  static constexpr int NP = P * (P + 1) / 2;      // basis functions
+  static constexpr int NS = (P + 1) * (P + 2) / 2;// (l, m >= 0), l <= p
+  static constexpr int NQ = NS - 3;               // (j, k >= 0), 2 <= j <= p
+  static constexpr int NV = NS - 1;               // (j, k >= 0), 1 <= j <= p
+  static constexpr int NZ = 13 * NP;              // per-pair contraction vector
+};
+
+// (l, m >= 0) -> flat index
+__host__ __device__ constexpr int sidx(int l, int m) { return l * (l + 1) / 2 + m; }
+__host__ __device__ constexpr int qidx(int j, int k) { return j * (j + 1) / 2 - 3 + k; }
+__host__ __device__ constexpr int vidx(int j, int k) { return j * (j + 1) / 2 - 1 + k; }
+// (l, m), 1 <= m <= l  -> c-layout index
+__host__ __device__ constexpr int lmidx(int l, int m) { return l * (l - 1) / 2 + (m - 1); }
+
+// Per-patch block layout in the fit buffer (doubles).
+template <int P>
+struct Layout {
+  using D = Dims<P>;
+  static constexpr int HDR = 0;       // o[3] Rm[9] h zlo zhi vl[9] cP[3] RP hP  (32 slots)
+  static constexpr int YL = 32;       // [E][3] local scaled edge samples
+  static constexpr int TL = YL + 3 * D::E;   // [E][3] local scaled tangents
+  static constexpr int CM = TL + 3 * D::E;   // [3][Q][3] monomial coefficients of the edge interpolants
+  static constexpr int FIT = CM + 9 * D::Q;  // [13 NP][N]: P_D (4NP) P_Sp (4NP) P_Sd (NP) P_Sg (4NP)
+  static constexpr int GT = FIT + 13 * D::NP * D::N;   // [E][3][2][NQ]  Hess S^{(j,k)} tau
+  static constexpr int ET = GT + D::E * 6 * D::NQ;     // [E][3][2][NV]  grad S^{(j,k)} x tau
+  static constexpr int END = ET + D::E * 6 * D::NV;
+  static constexpr int STRIDE = (END + 31) / 32 * 32;
+};
+enum { H_O = 0, H_RM = 3, H_H = 12, H_ZLO = 13, H_ZHI = 14, H_VL = 15, H_CP = 24, H_RP = 27, H_HP = 28 };
+
+// Constant tables uploaded by rrq_create (device global memory).
+struct Tables {
+  const double *tgl, *wgl;   // [q]
+  const double *U;           // [q][q]  c~_c = sum_k U[c][k] F_k
+  const double *xo, *wo;     // [n_omega] GL on (-1,1)
+  const double *sqb;         // [41][41] sqrt(binomial(n, k))
+};
+
+// R_l^m(X,Y,Z), 0 <= m <= l <= P (no Condon-Shortley phase, reading G5) by the Cartesian recurrences
+//  R_m^m = sqrt((2m-1)/(2m)) (X + iY) R_{m-1}^{m-1},  R_{m+1}^m = sqrt(2m+1) Z R_m^m,
+//  R_{l+1}^m = [(2l+1) Z R_l^m - sqrt((l+m)(l-m)) r^2 R_{l-1}^m] / sqrt((l+1+m)(l+1-m)),
+// which follow from P:L338-345 and P:L347-360 multiplied through by r^l (no trig, valid at r = 0).
+template <int P>
+__device__ __forceinline__ void r_column(double X, double Y, double Z, int m, cd *R) {
+  double r2 = X * X + Y * Y + Z * Z;
+  cd rmm = mk(1.0, 0.0);
+  for (int k = 1; k <= m; ++k) rmm = sqrt((2.0 * k - 1.0) / (2.0 * k)) * (mk(X, Y) * rmm);
+  R[sidx(m, m)] = rmm;
+  if (m + 1 <= P) {
+    cd a = sqrt(2.0 * m + 1.0) * Z * rmm;
+    R[sidx(m + 1, m)] = a;
+    cd b = rmm;
+    for (int l = m + 1; l < P; ++l) {
+      cd c = (1.0 / sqrt((double)(l + 1 + m) * (l + 1 - m))) *
+             ((2.0 * l + 1.0) * Z * a - (sqrt((double)(l + m) * (l - m)) * r2) * b);
+      R[sidx(l + 1, m)] = c;
+      b = a;
+      a = c;
+    }
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void r_table(double X, double Y, double Z, cd *R) {
+#pragma unroll 1
+  for (int m = 0; m <= P; ++m) r_column<P>(X, Y, Z, m, R);
+}
+
+// R_l^m for any -l <= m <= l from the m >= 0 table: R_l^{-m} = (-1)^m conj(R_l^m).
+__device__ __forceinline__ cd rget(const cd *R, int l, int m) {
+  if (l < 0 || m > l || m < -l) return mk(0.0, 0.0);
+  if (m >= 0) return R[sidx(l, m)];
+  cd v = R[sidx(l, -m)];
+  return (((-m) & 1) ? -1.0 : 1.0) * conj(v);
+}
+
+// Derivative of R_l^m along R-axis a (0 = X, 1 = Y, 2 = Z) as <= 2 terms (coef, l-1, m') (reading A3).
+struct Term {
+  cd c;
+  int m;
+};
+__device__ __forceinline__ int dterms(int l, int m, int a, Term *t) {
+  double lm = (double)(l - m), lp = (double)(l + m);
+  if (a == 2) {
+    t[0].c = mk(lm * lp > 0 ? sqrt(lm * lp) : 0.0, 0.0);
+    t[0].m = m;
+    return 1;
+  }
+  double cp = lm * (lm - 1) > 0 ? sqrt(lm * (lm - 1)) : 0.0;
+  double cm = lp * (lp - 1) > 0 ? sqrt(lp * (lp - 1)) : 0.0;
+  if (a == 0) {  // dX = (D+ + D-)/2, D+ = -cp R^{m+1}, D- = cm R^{m-1}
+    t[0].c = mk(-0.5 * cp, 0.0);
+    t[1].c = mk(0.5 * cm, 0.0);
+  } else {       // dY = (D+ - D-)/(2i) = i (D- - D+)/2
+    t[0].c = mk(0.0, 0.5 * cp);
+    t[1].c = mk(0.0, 0.5 * cm);
+  }
+  t[0].m = m + 1;
+  t[1].m = m - 1;
+  return 2;
+}
+
+__device__ __forceinline__ cd dR(const cd *R, int l, int m, int a) {
+  Term t[2];
+  int n = dterms(l, m, a, t);
+  cd s = mk(0.0, 0.0);
+  for (int i = 0; i < n; ++i) cfma(s, t[i].c, rget(R, l - 1, t[i].m));
+  return s;
+}
+
+__device__ __forceinline__ cd d2R(const cd *R, int l, int m, int a, int b) {
+  Term t[2];
+  int n = dterms(l, m, a, t);
+  cd s = mk(0.0, 0.0);
+  for (int i = 0; i < n; ++i)
+    if (t[i].m <= l - 1 && t[i].m >= -(l - 1)) cfma(s, t[i].c, dR(R, l - 1, t[i].m, b));
+  return s;
+}
+
+// S^{(l,m)}(x,y,z) = R_l^m(y,z,x): S-axis x,y,z -> R-axis Z, X, Y.
+__device__ __forceinline__ int sax(int a) { return a == 0 ? 2 : a - 1; }
+
+// grad S^{(l,m)} at the point whose R table is R (any m).
+__device__ __forceinline__ void gradS(const cd *R, int l, int m, cd g[3]) {
+  for (int a = 0; a < 3; ++a) g[a] = dR(R, l, m, sax(a));
+}
+// (Hess S^{(l,m)}) v
+__device__ __forceinline__ void hessS_v(const cd *R, int l, int m, const double v[3], cd out[3]) {
+  for (int a = 0; a < 3; ++a) {
+    cd s = mk(0.0, 0.0);
+    for (int b = 0; b < 3; ++b) {
+      cd h = d2R(R, l, m, sax(a), sax(b));
+      s = s + v[b] * h;
+    }
+    out[a] = s;
+  }
+}
+
+// Complex quaternion.
+struct cq {
+  cd s, v[3];
+};
+__device__ __forceinline__ cq qzero() {
+  cq r;
+  r.s = mk(0, 0);
+  r.v[0] = r.v[1] = r.v[2] = mk(0, 0);
+  return r;
+}
+
+__device__ __forceinline__ double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+__device__ __forceinline__ void cross3(const double *a, const double *b, double *c) {
+  c[0] = a[1] * b[2] - a[2] * b[1];
+  c[1] = a[2] * b[0] - a[0] * b[2];
+  c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace rrq
