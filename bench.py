@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RRQ near-correction build (BASELINE.json metric: near-correction weights/s,
+fp64, S/D/S'/D', on 1 B200; % of the FP64 roofline).
+
+One STEP = one pass of the whole hot path over the workload:
+  rrq_near_list -> rrq_patch_fit -> rrq_build_correction over all rows (in row chunks whose CSR
+  output, 4 fp64 weights + 1 int32 column per entry, is written to HBM into reused chunk buffers).
+Workload (N=1): BASELINE.json configs[3] ("cfg4"): bumpy sphere, 50,000 curved triangles, p = 8
+(3.2M nodes), all on-surface node targets + 1M off-surface targets, near rule eta = 1.5, all four
+kernels.  Synthetic, seeded (synth/configs.py).  Inputs and outputs exceed L2 (fit blocks 22 GB,
+outputs ~300 GB per step), so no L2 flush is needed.
+
+value    = weights (S+D+S'+D' CSR values) built per second over the timed steps, device-timed
+           (CUDA events on the launch stream), max over ranks.
+e2e      = the same metric with host buffers: per step the inputs are copied H2D from pinned host
+           memory and every chunk's CSR (values + columns) is copied D2H into pinned host buffers,
+           overlapped with the next chunk on a copy stream.
+roofline = k_pair_zeta (the dominant kernel): algorithmic flops (paper_2411_08342_b200/flops.py)
+           / its CUDA-event time, against the measured FP64 peak (profiles/r01_fp64_peak.txt).
+--impl reference times the CPU oracle (oracle/, test infrastructure) on a bounded sample.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.1      # measured: DMMA m8n8k4 f64, 148 SMs @1965 MHz (profiles/r01_fp64_peak.txt)
+FP64_PEAK_SRC = "measured FP64 peak (DMMA m8n8k4 microbenchmark, profiles/r01_fp64_peak.txt; DFMA chains 34.2)"
+METRIC = "near-correction weights/s (fp64, S/D/S'/D') on 1 B200"
+UNIT = "weights/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--n-off", type=int, default=None, help="override off-surface target count (debug)")
+    ap.add_argument("--freq", type=int, default=None, help="override icosphere frequency (debug)")
+    ap.add_argument("--chunk-pairs", type=int, default=16_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-pairs", type=int, default=48000)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------ dist
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        import torch
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.rows, self.proc, self.idx = [], None, gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+# ------------------------------------------------------------------------------------------ workload
+def make_inputs(args, rank):
+    from synth.configs import make_config
+    kw = {}
+    if args.n_off is not None:
+        kw["n_off"] = args.n_off
+    if args.freq is not None:
+        kw["freq"] = args.freq
+    return make_config(args.config, seed_offset=rank, **kw)
+
+
+def cfg_desc(cfg, npairs, T):
+    S = cfg["surface"]
+    return {"workload": cfg["name"], "patches": int(S.n_patches), "p": int(S.p), "p_edge": int(S.q),
+            "nodes": int(S.n_patches * S.n), "targets": int(T), "pairs": int(npairs) if npairs is not None else None, "eta": cfg["eta"],
+            "kernels": "S,D,Sp,Dp", "l2": "inputs+outputs > L2 (fit 22 GB, CSR ~300 GB per step): no flush needed"}
+
+
+class Runner:
+    def __init__(self, cfg, args, device="cuda"):
+        import torch
+        from paper_2411_08342_b200 import RRQ, DeviceSurface, DeviceTargets
+        self.torch = torch
+        self.cfg, self.args = cfg, args
+        S = cfg["surface"]
+        self.S, self.n = S, S.n
+        eta = cfg["eta"] if math.isfinite(cfg["eta"]) else 0.0
+        self.ctx = RRQ(S.p, eta=eta, all_pairs=cfg["all_pairs"])
+        self.ds = DeviceSurface.from_numpy(S)
+        self.dt = DeviceTargets.from_numpy(cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
+        self.T = self.dt.n_targets
+        self.bufs = None
+        self.stream = torch.cuda.current_stream()
+
+    def alloc_out(self, cap):
+        t = self.torch
+        n = self.n
+        return dict(row_ptr=t.empty(self.T + 1, dtype=t.int64, device="cuda"),
+                    col_idx=t.empty(cap * n, dtype=t.int32, device="cuda"),
+                    vals=[t.empty(cap * n, dtype=t.float64, device="cuda") for _ in range(4)],
+                    status=t.empty(cap, dtype=t.int32, device="cuda"))
+
+    def chunks(self, hptr, cap):
+        T = hptr.shape[0] - 1
+        out, r0 = [], 0
+        while r0 < T:
+            r1 = int(np.searchsorted(hptr, hptr[r0] + cap, side="right")) - 1
+            r1 = max(r1, r0 + 1)
+            r1 = min(r1, T)
+            out.append((r0, r1))
+            r0 = r1
+        return out
+
+    def step(self, out_sets=None, on_chunk=None):
+        """One pass: near list, patch fit, build over all row chunks."""
+        ptr, pat = self.ctx.near_list(self.ds, self.dt)
+        fit, fst = self.ctx.patch_fit(self.ds)
+        hptr = ptr.cpu().numpy()
+        cap = self.args.chunk_pairs
+        sets = out_sets or self.bufs
+        ch = self.chunks(hptr, cap)
+        for i, (r0, r1) in enumerate(ch):
+            o = sets[i % len(sets)]
+            if on_chunk is not None:
+                on_chunk("before", i, o)
+            rp = o["row_ptr"][: r1 - r0 + 1]
+            self.ctx.build_correction(self.ds, self.dt, ptr, pat, fit, row_begin=r0, row_end=r1,
+                                      out=dict(row_ptr=rp, col_idx=o["col_idx"], vals=o["vals"], status=o["status"]))
+            if on_chunk is not None:
+                on_chunk("after", i, o, int(hptr[r1] - hptr[r0]))
+        self.npairs = int(hptr[-1])
+        self.fit = fit
+        return self.npairs
+
+
+def run_ours(args, ws, rank):
+    import torch
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    t0 = time.time()
+    cfg = make_inputs(args, rank)
+    gen_s = time.time() - t0
+    R = Runner(cfg, args)
+    R.bufs = [R.alloc_out(args.chunk_pairs)]
+    # warmup
+    for _ in range(args.warmup):
+        R.step()
+    torch.cuda.synchronize()
+    npairs = R.npairs
+    weights_per_step = npairs * R.n * 4
+    # timed region
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    R.ctx.reset_timing()
+    R.ctx.set_timing(True)
+    launches0 = R.ctx.launch_count()
+    barrier(ws)
+    torch.cuda.synchronize()
+    clk.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        R.step()
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    barrier(ws)
+    launches = R.ctx.launch_count() - launches0
+    R.ctx.set_timing(False)
+    ms = e0.elapsed_time(e1)
+    ms_max = max_over_ranks(ms, ws)
+    tim = R.ctx.timing()
+    total_weights = sum_over_ranks(weights_per_step * args.steps, ws)
+    value = total_weights / (ms_max / 1e3)
+    from paper_2411_08342_b200.flops import pair_flops, pair_bytes
+    pf = pair_flops(R.S.p)
+    swap_per_pair = tim["swap_edges"] / max(tim["pairs"], 1)
+    zeta_flops = (pf["zeta"] + swap_per_pair * pf["swap_edge"]) * tim["pairs"]
+    zeta_ms = tim["ms"]["pair_zeta"]
+    contract_flops = pf["contract"] * tim["pairs"]
+    achieved = zeta_flops / (zeta_ms / 1e3) / 1e12
+    build_ms = zeta_ms + tim["ms"]["contract"] + tim["ms"]["plumbing"]
+    build_tflops = (zeta_flops + contract_flops) / (build_ms / 1e3) / 1e12
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generator synth/configs.py; BASELINE.json configs[3] shape)",
+        "config": dict(cfg_desc(cfg, npairs, R.T), parallelism=f"replicas{ws}" if ws > 1 else "single",
+                       step="near_list+patch_fit+build(all rows, chunked)", chunk_pairs=args.chunk_pairs),
+        "roofline": {"bound": "alu", "kernel": "k_pair_zeta", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "peak_source": FP64_PEAK_SRC,
+                     "flops_per_pair": pf["zeta"] + swap_per_pair * pf["swap_edge"], "launches": tim["launches"]["pair_zeta"],
+                     "build_stage_tflops": build_tflops, "build_stage_frac": build_tflops / FP64_PEAK_TFLOPS},
+        "stages_ms_per_step": {k: v / args.steps for k, v in tim["ms"].items()},
+        "pairs_per_s": npairs * args.steps / (ms_max / 1e3) * ws,
+        "rows_per_s": R.T * args.steps / (ms_max / 1e3) * ws,
+        "swap_edges_per_pair": swap_per_pair,
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "gen_s": gen_s,
+    }
+    # e2e through host buffers
+    if not args.no_e2e and args.e2e_steps > 0:
+        res["e2e"] = run_e2e(R, cfg, args, ws)
+    else:
+        res["e2e"] = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            res["cpu_baseline"] = cpu_baseline(cfg, args, R)
+        except Exception as ex:  # report, never hide
+            res["cpu_baseline"] = {"error": repr(ex)}
+    return res
+
+
+def run_e2e(R, cfg, args, ws):
+    """Same metric with host buffers: pinned host inputs copied H2D each step, every chunk's CSR copied
+    D2H (overlapped on a copy stream, double-buffered device outputs)."""
+    import torch
+    from paper_2411_08342_b200 import DeviceSurface, DeviceTargets
+    S = cfg["surface"]
+    pin = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).pin_memory()
+    h_in = dict(nodes=pin(S.nodes, torch.float64), normals=pin(S.normals, torch.float64),
+                weights=pin(S.weights, torch.float64), verts=pin(S.verts, torch.float64),
+                edge_x=pin(S.edge_x, torch.float64), edge_dx=pin(S.edge_dx, torch.float64),
+                x=pin(cfg["tx"], torch.float64), normal=pin(cfg["tnormal"], torch.float64),
+                self_node=pin(cfg["self_node"], torch.int64), side=pin(cfg["side"], torch.int8))
+    d_in = {k: torch.empty(v.shape, dtype=v.dtype, device="cuda") for k, v in h_in.items()}
+    h2d = sum(v.numel() * v.element_size() for v in h_in.values())
+    cap = min(args.chunk_pairs, 4_000_000)
+    old_cap = args.chunk_pairs
+    args.chunk_pairs = cap
+    sets = [R.alloc_out(cap), R.alloc_out(cap)]
+    n = R.n
+    h_out = [dict(col=torch.empty(cap * n, dtype=torch.int32).pin_memory(),
+                  vals=[torch.empty(cap * n, dtype=torch.float64).pin_memory() for _ in range(4)]) for _ in range(2)]
+    copy_stream = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    done = [torch.cuda.Event(), torch.cuda.Event()]
+    d2h_bytes = [0]
+    slot_of = {}
+
+    def on_chunk(when, i, o, np_=0):
+        k = i % 2
+        if when == "before":
+            main.wait_event(done[k])          # the copy of this buffer's previous chunk has finished
+            return
+        ev = torch.cuda.Event()
+        ev.record(main)
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(ev)
+            m = np_ * n
+            h_out[k]["col"][:m].copy_(o["col_idx"][:m], non_blocking=True)
+            for j in range(4):
+                h_out[k]["vals"][j][:m].copy_(o["vals"][j][:m], non_blocking=True)
+            done[k].record(copy_stream)
+        d2h_bytes[0] += m * (4 + 4 * 8)
+
+    def one_step():
+        for k, v in h_in.items():
+            d_in[k].copy_(v, non_blocking=True)
+        R.ds = DeviceSurface(d_in["nodes"], d_in["normals"], d_in["weights"], d_in["verts"], d_in["edge_x"],
+                             d_in["edge_dx"])
+        R.dt = DeviceTargets(d_in["x"], d_in["normal"], d_in["self_node"], d_in["side"])
+        R.step(out_sets=sets, on_chunk=on_chunk)
+        copy_stream.synchronize()
+
+    one_step()   # warm (allocations)
+    torch.cuda.synchronize()
+    d2h_bytes[0] = 0
+    barrier(ws)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.e2e_steps):
+        one_step()
+    main.wait_stream(copy_stream)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    args.chunk_pairs = old_cap
+    w = sum_over_ranks(R.npairs * n * 4 * args.e2e_steps, ws)
+    return {"value": w / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h_bytes[0] / args.e2e_steps), "steps": args.e2e_steps,
+            "ms_per_step": ms / args.e2e_steps}
+
+
+def sample_pairs(cfg, budget, seed=7):
+    """Bounded sample for the CPU oracle: all near pairs (oracle near rule) of a few random patches, so
+    the per-patch Steps 1-3 cost is paid as in a full build; about `budget` pairs."""
+    from oracle import oracle as O
+    S = cfg["surface"]
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(S.n_patches)
+    chosen, tg, pa = [], [], []
+    tot = 0
+    for q in order[:200]:
+        t, p_ = O.near_pairs_for_patches(S, cfg["tx"], cfg["self_node"], cfg["eta"], [q], cfg["all_pairs"])
+        if t.size == 0:
+            continue
+        take = min(t.size, budget - tot)
+        tg.append(t[:take]); pa.append(p_[:take]); chosen.append(q)
+        tot += take
+        if tot >= budget:
+            break
+    return np.concatenate(tg), np.concatenate(pa), len(chosen)
+
+
+def cpu_baseline(cfg, args, R=None, steps=1):
+    from oracle import oracle as O
+    S = cfg["surface"]
+    tg, pa, npatch = sample_pairs(cfg, args.cpu_sample_pairs)
+    cores = os.cpu_count()
+    t0 = time.time()
+    for _ in range(steps):
+        O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa)
+    el = (time.time() - t0) / steps
+    w = tg.shape[0] * S.n * 4
+    return {"value": w / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{tg.shape[0]} pairs = all near pairs of {npatch} random patches of {cfg['name']} "
+                      f"(Steps 1-8 incl. per-patch fit, all 4 kernels), {el:.1f} s on {cores} OpenMP threads",
+            "seconds": el, "pairs": int(tg.shape[0])}
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle as it stands on a bounded sample of the same workload."""
+    if rank != 0:
+        return None
+    cfg = make_inputs(args, 0)
+    from oracle import oracle as O
+    S = cfg["surface"]
+    tg, pa, npatch = sample_pairs(cfg, args.cpu_sample_pairs)
+    for _ in range(args.warmup):
+        O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg[:50], pa[:50])
+    t0 = time.time()
+    for _ in range(args.steps):
+        O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa)
+    el = (time.time() - t0)
+    w = tg.shape[0] * S.n * 4 * args.steps
+    v = w / el
+    cores = os.cpu_count()
+    sample = (f"{tg.shape[0]} pairs per step = all near pairs of {npatch} random patches of {cfg['name']} "
+              f"(Steps 1-8 incl. per-patch fit, all 4 kernels)")
+    return {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": cfg_desc(cfg, None, cfg["tx"].shape[0]),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        res = run_reference(args, ws, rank)
+    else:
+        res = run_ours(args, ws, rank)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -198,3 +198,18 @@ def pairs_from_ptr(ptr, pat):
     T = ptr.shape[0] - 1
     tgt = np.repeat(np.arange(T, dtype=np.int64), np.diff(ptr))
     return tgt, pat
+
+
+def near_pairs_for_patches(S, tx, self_node, eta, patches, all_pairs=False, cap=10_000_000):
+    """(target, patch) near pairs of the listed patches (reading A6), brute force over targets."""
+    sel = np.ascontiguousarray(patches, dtype=np.int32)
+    ot = np.zeros(cap, np.int64); op = np.zeros(cap, np.int32)
+    lib().orc_near_pairs_for_patches.restype = ctypes.c_int64
+    k = lib().orc_near_pairs_for_patches(
+        ctypes.c_int(S.p), ctypes.c_int(S.q), _p(_c(S.nodes, np.float64)), _p(_c(S.weights, np.float64)),
+        _p(_c(S.verts, np.float64)), _p(_c(S.edge_x, np.float64)), ctypes.c_int64(tx.shape[0]),
+        _p(_c(tx, np.float64)), _p(_c(self_node, np.int64)) if self_node is not None else None,
+        ctypes.c_double(eta if np.isfinite(eta) else 1e300), ctypes.c_int(int(all_pairs)),
+        ctypes.c_int64(sel.size), _p(sel), ctypes.c_int64(cap), _p(ot), _p(op))
+    k = min(int(k), cap)
+    return ot[:k], op[:k]

@@ -1110,3 +1110,52 @@ void orc_tables(int q, double *t, double *w, double *U) {
   orc_gauss_legendre(q, t, w);
   orc_vandermonde_inverse(q, t, U);
 }
+
+/* Near pairs restricted to a list of patches (same rule as orc_near_list, reading A6), brute force
+ * over all targets; used to draw bounded samples.  Returns the number of pairs written (<= cap);
+ * out_t / out_p receive (target, patch) in patch-list order, targets ascending. */
+int64_t orc_near_pairs_for_patches(int p, int q, const double *nodes, const double *weights, const double *verts,
+                                   const double *edge_x, int64_t n_targets, const double *tx, const int64_t *self_node,
+                                   double eta, int all_pairs, int64_t n_sel, const int32_t *sel, int64_t cap,
+                                   int64_t *out_t, int32_t *out_p) {
+  int n = p * p;
+  int64_t k = 0;
+  for (int64_t s = 0; s < n_sel; ++s) {
+    int64_t P = sel[s];
+    double c[3] = {0, 0, 0}, ws = 0;
+    for (int i = 0; i < n; ++i) {
+      double w = weights[P * n + i];
+      ws += w;
+      for (int a = 0; a < 3; ++a) c[a] += w * nodes[(P * n + i) * 3 + a];
+    }
+    for (int a = 0; a < 3; ++a) c[a] /= ws;
+    double R = 0;
+    for (int i = 0; i < n; ++i) {
+      double d[3] = {nodes[(P * n + i) * 3] - c[0], nodes[(P * n + i) * 3 + 1] - c[1], nodes[(P * n + i) * 3 + 2] - c[2]};
+      double r = norm3(d);
+      if (r > R) R = r;
+    }
+    for (int v = 0; v < 3; ++v) {
+      double d[3] = {verts[P * 9 + 3 * v] - c[0], verts[P * 9 + 3 * v + 1] - c[1], verts[P * 9 + 3 * v + 2] - c[2]};
+      double r = norm3(d);
+      if (r > R) R = r;
+    }
+    for (int kk = 0; kk < 3 * q; ++kk) {
+      const double *y = edge_x + (P * 3 * q + kk) * 3;
+      double d[3] = {y[0] - c[0], y[1] - c[1], y[2] - c[2]};
+      double r = norm3(d);
+      if (r > R) R = r;
+    }
+    double h, o[3], Rm[3][3];
+    patch_frame(verts + P * 9, o, Rm, &h);
+    for (int64_t t = 0; t < n_targets; ++t) {
+      double d[3] = {tx[3 * t] - c[0], tx[3 * t + 1] - c[1], tx[3 * t + 2] - c[2]};
+      int near = all_pairs || norm3(d) <= R + eta * h || (self_node && self_node[t] >= 0 && self_node[t] / n == P);
+      if (near) {
+        if (k < cap) { out_t[k] = t; out_p[k] = (int32_t)P; }
+        ++k;
+      }
+    }
+  }
+  return k;
+}

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(WPB * 32)
                 const int32_t *__restrict__ pair_patch, const double *__restrict__ fit, const double *__restrict__ tx,
                 const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
                 const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Z,
-                int32_t *__restrict__ pstat) {
+                int32_t *__restrict__ pstat, unsigned long long *__restrict__ swapcnt) {
   using D = Dims<P>;
   using L = Layout<P>;
   constexpr int Q = D::Q, E = D::E, NP = D::NP, NQ = D::NQ, NV = D::NV, NS = D::NS, NZ = D::NZ;
@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(WPB * 32)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpScratch<P> &ws = wsall[warp];
   const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
+  unsigned long long nswap = 0;
 
   for (int64_t s = (int64_t)blockIdx.x * WPB + warp; s < npairs; s += (int64_t)gridDim.x * WPB) {
     const int64_t k = perm[s];
@@ -429,8 +430,10 @@ __global__ void __launch_bounds__(WPB * 32)
       for (int a = 0; a < 3; ++a) Zr[9 * NP + (1 + a) * NP + c] = -W[0] * nup[a] - nxW[a];
     }
     if (lane == 0 && pstat) pstat[k - kbase] = (ws.conv[0] && ws.conv[1] && ws.conv[2]) ? 0 : 1;
+    nswap += ws.swap[0] + ws.swap[1] + ws.swap[2];
     __syncwarp();
   }
+  if (swapcnt && lane == 0 && nswap) atomicAdd(swapcnt, nswap);
 }
 
 // ------------------------------------------------------------------------------------------------

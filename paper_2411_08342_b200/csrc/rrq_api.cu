@@ -34,8 +34,62 @@ struct rrq_ctx_s {
     void *p = nullptr;
     size_t n = 0;
   };
-  Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one;
+  Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one, swapcnt;
+  // device-time accounting (rrq_set_timing)
+  bool timing = false;
+  double t_ms[5] = {0, 0, 0, 0, 0};
+  int64_t t_n[5] = {0, 0, 0, 0, 0};
+  int64_t stats[2] = {0, 0};
+  struct Pend {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pend> pend;
+  std::vector<cudaEvent_t> pool;
 };
+
+static cudaEvent_t ev_get(rrq_ctx c) {
+  if (c->pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = c->pool.back();
+  c->pool.pop_back();
+  return e;
+}
+// Bracket a launch with events on its stream (only when timing is enabled).
+struct TScope {
+  rrq_ctx c;
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  TScope(rrq_ctx c_, int s_, cudaStream_t st_) : c(c_), stage(s_), st(st_) {
+    if (c->timing) {
+      a = ev_get(c);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~TScope() {
+    if (c->timing) {
+      cudaEvent_t b = ev_get(c);
+      cudaEventRecord(b, st);
+      c->pend.push_back({stage, a, b});
+    }
+  }
+};
+static void t_flush(rrq_ctx c) {
+  for (auto &p : c->pend) {
+    cudaEventSynchronize(p.b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    c->t_ms[p.stage] += ms;
+    c->t_n[p.stage] += 1;
+    c->pool.push_back(p.a);
+    c->pool.push_back(p.b);
+  }
+  c->pend.clear();
+}
 
 static thread_local std::string g_create_err;
 
@@ -136,6 +190,9 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
 
 void rrq_destroy(rrq_ctx c) {
   if (!c) return;
+  t_flush(c);
+  for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->swapcnt.p) cudaFree(c->swapcnt.p);
   cudaFree(c->d_tab);
   for (auto *b : {&c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
                   &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
@@ -146,6 +203,31 @@ void rrq_destroy(rrq_ctx c) {
 const char *rrq_last_error(rrq_ctx c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
 int64_t rrq_launch_count(rrq_ctx c) { return c ? c->launches : 0; }
+
+rrq_status rrq_set_timing(rrq_ctx c, int enable) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  c->timing = enable != 0;
+  return RRQ_OK;
+}
+
+rrq_status rrq_reset_timing(rrq_ctx c) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  t_flush(c);
+  for (int i = 0; i < 5; ++i) { c->t_ms[i] = 0; c->t_n[i] = 0; }
+  c->stats[0] = c->stats[1] = 0;
+  return RRQ_OK;
+}
+
+rrq_status rrq_get_timing(rrq_ctx c, double ms[5], int64_t launches[5], int64_t stats[2]) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  t_flush(c);
+  for (int i = 0; i < 5; ++i) {
+    if (ms) ms[i] = c->t_ms[i];
+    if (launches) launches[i] = c->t_n[i];
+  }
+  if (stats) { stats[0] = c->stats[0]; stats[1] = c->stats[1]; }
+  return RRQ_OK;
+}
 
 rrq_status rrq_get_tables(rrq_ctx c, double *t, double *w, double *U) {
   if (!c) return RRQ_ERR_INVALID_ARG;
@@ -190,6 +272,7 @@ rrq_status rrq_near_list(rrq_ctx c, const rrq_surface *s, const rrq_targets *tg,
   if (!pair_ptr || !n_pairs) return fail(c, RRQ_ERR_INVALID_ARG, "pair_ptr and n_pairs must be non-NULL");
   const int64_t T = tg->n_targets, Pn = s->n_patches;
   const int fill = pair_patch != nullptr;
+  TScope ts(c, 0, st);
   if (T == 0) {
     if (!fill) {
       cudaMemsetAsync(pair_ptr, 0, sizeof(int64_t), st);
@@ -282,6 +365,7 @@ static rrq_status patch_fit_impl(rrq_ctx c, const rrq_surface *s, double *fit, i
   using D = Dims<P>;
   const int64_t Pn = s->n_patches;
   rrq_status r;
+  TScope ts(c, 1, st);
   if ((r = compute_balls(c, s, st))) return r;
   k_patch_geom<P><<<(unsigned)Pn, 128, 0, st>>>(Pn, s->nodes, s->verts, s->edge_x, s->edge_dx, bp<double>(c->balls), c->T, fit);
   k_edge_tables<P><<<nblk(Pn * D::E, 128), 128, 0, st>>>(Pn, fit);
@@ -359,6 +443,10 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     int64_t np_ = (hptr.empty() ? total : hptr[sr.second - row_begin] - hptr[sr.first - row_begin]);
     maxsub = std::max(maxsub, np_);
   }
+  if (c->timing) {
+    if (!ensure(c, c->swapcnt, 64)) return RRQ_ERR_CUDA;
+    cudaMemsetAsync(c->swapcnt.p, 0, 8, st);
+  }
   if (!ensure(c, c->ptgt, maxsub * sizeof(int64_t)) || !ensure(c, c->perm, maxsub * sizeof(int64_t)) ||
       !ensure(c, c->seg, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->cursor, (Pn + 1) * sizeof(int64_t)) ||
       !ensure(c, c->items, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->Z, (size_t)maxsub * D::NZ * sizeof(double)) ||
@@ -374,7 +462,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     const int64_t kb = hptr.empty() ? obase : hptr[r0 - row_begin];
     const int64_t np_ = hptr.empty() ? total : hptr[r1 - row_begin] - kb;
     if (np_ == 0) continue;
-    // pair -> target (and, for the first sub-chunk, nothing else)
+    TScope* tsp = new TScope(c, 4, st);
     k_pair_targets<<<nblk(r1 - r0 + 1, 256), 256, 0, st>>>(r0, r1, pair_ptr, kb, bp<int64_t>(c->ptgt),
                                                             nullptr, D::N);
     // patch-major permutation (counting sort)
@@ -387,21 +475,27 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     cudaMemsetAsync(bp<int64_t>(c->items) + Pn, 0, sizeof(int64_t), st);
     k_scan_i64<<<1, 1024, 0, st>>>(Pn + 1, bp<int64_t>(c->items), bp<int64_t>(c->one) + 1);
     c->launches += 6;
+    delete tsp;
     int64_t n_items = 0;
     cudaMemcpyAsync(&n_items, bp<int64_t>(c->one) + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     // zeta
     size_t sm = zeta_smem<P>(c->prm.n_omega);
     int64_t want = (np_ + kWPB - 1) / kWPB;
     unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)c->num_sms * 8);
+    {
+    TScope tz(c, 2, st);
     k_pair_zeta<P, kWPB><<<grid, kWPB * 32, sm, st>>>(np_, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), kb, pair_patch,
                                                        fit, tg->x, tg->normal, tg->self_node, tg->side, c->T,
                                                        c->prm.n_omega, c->prm.rho_swap, bp<double>(c->Z),
-                                                       pstat ? pstat + (kb - obase) : nullptr);
+                                                       pstat ? pstat + (kb - obase) : nullptr,
+                                                       c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr);
+    }
     c->launches++;
     rrq_status r;
     if ((r = cuda_check(c, "k_pair_zeta"))) return r;
     cudaStreamSynchronize(st);   // n_items
     if (n_items > 0) {
+      TScope tc(c, 3, st);
       k_contract<P><<<(unsigned)n_items, CC::THREADS, 0, st>>>(
           n_items, bp<int64_t>(c->items), Pn, bp<int64_t>(c->seg), bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), kb,
           pair_patch, fit, bp<double>(c->Z), s->nodes, s->normals, s->weights, tg->x, tg->normal, tg->self_node,
@@ -417,6 +511,13 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     // row_ptr[i] = (pair_ptr[row_begin + i] - obase) * n
     k_row_ptr<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase, row_ptr, D::N);
     c->launches++;
+  }
+  if (c->timing) {
+    unsigned long long sw = 0;
+    cudaMemcpyAsync(&sw, c->swapcnt.p, 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    c->stats[0] += total;
+    c->stats[1] += (int64_t)sw;
   }
   return cuda_check(c, "rrq_build_correction");
 }

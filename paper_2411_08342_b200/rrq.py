@@ -68,6 +68,12 @@ def load_library():
     lib.rrq_get_tables.restype = ctypes.c_int
     lib.rrq_launch_count.argtypes = [vp]
     lib.rrq_launch_count.restype = ctypes.c_int64
+    lib.rrq_set_timing.argtypes = [vp, ctypes.c_int]
+    lib.rrq_set_timing.restype = ctypes.c_int
+    lib.rrq_reset_timing.argtypes = [vp]
+    lib.rrq_reset_timing.restype = ctypes.c_int
+    lib.rrq_get_timing.argtypes = [vp, vp, vp, vp]
+    lib.rrq_get_timing.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -153,6 +159,22 @@ class RRQ:
 
     def launch_count(self):
         return int(self.lib.rrq_launch_count(self.h))
+
+    STAGES = ("near_list", "patch_fit", "pair_zeta", "contract", "plumbing")
+
+    def set_timing(self, on=True):
+        self._check(self.lib.rrq_set_timing(self.h, int(on)), "rrq_set_timing")
+
+    def reset_timing(self):
+        self._check(self.lib.rrq_reset_timing(self.h), "rrq_reset_timing")
+
+    def timing(self):
+        """Accumulated device ms and launch counts per stage + (pairs, swap edges)."""
+        import numpy as np
+        ms = np.zeros(5); n = np.zeros(5, np.int64); st = np.zeros(2, np.int64)
+        self._check(self.lib.rrq_get_timing(self.h, ms.ctypes.data, n.ctypes.data, st.ctypes.data), "rrq_get_timing")
+        return dict(ms=dict(zip(self.STAGES, ms.tolist())), launches=dict(zip(self.STAGES, n.tolist())),
+                    pairs=int(st[0]), swap_edges=int(st[1]))
 
     def tables(self):
         q = 2 * self.p
