@@ -152,6 +152,11 @@ rrq_status rrq_set_timing(rrq_ctx ctx, int enable);
 rrq_status rrq_get_timing(rrq_ctx ctx, double ms[5], int64_t launches[5], int64_t stats[2]);
 rrq_status rrq_reset_timing(rrq_ctx ctx);
 
+/* Test hook: copy the internal per-pair contraction vectors of the LAST build sub-chunk to HOST
+ * arrays: perm[i] = global pair id of row i, Z[i][13 n_p] = (Theta, zeta(W), zeta(dW), zeta_S) in
+ * c-layout.  At most max_pairs rows; returns the row count in *n_out. */
+rrq_status rrq_debug_zeta(rrq_ctx ctx, int64_t max_pairs, int64_t *perm, double *Z, int64_t *n_out);
+
 #ifdef __cplusplus
 }
 #endif

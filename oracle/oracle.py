@@ -108,8 +108,14 @@ def model_integrals(a, b, q):
     return I, J
 
 
+def model_integrals_direct(a, b, q):
+    I = np.zeros(q); J = np.zeros(q)
+    lib().orc_model_integrals_direct(ctypes.c_double(a), ctypes.c_double(b), ctypes.c_int(q), _p(I), _p(J))
+    return I, J
+
+
 def find_t0(C, rp):
-    """C: [q,3] monomial coefficients of an edge interpolant; rp target.  -> (t0 complex, converged)."""
+    """C: [q,3] Legendre coefficients of an edge interpolant (reading A4'); rp target -> (t0, converged)."""
     C = _c(C, np.float64)
     re = ctypes.c_double(); im = ctypes.c_double()
     conv = lib().orc_find_t0(_p(C), ctypes.c_int(C.shape[0]), _p(_c(rp, np.float64)), ctypes.byref(re),
@@ -156,14 +162,16 @@ def near_list(S, tx, self_node, eta, all_pairs=False):
 
 
 def build_rows(S, tx, tnormal, self_node, side, pair_target, pair_patch, mask=15, raw=False, n_omega=32,
-               rho0=3.0):
-    """-> vals [4, n_pairs, n] (S, D, S', D'), status [n_pairs]."""
+               rho0=3.0, kappa=False):
+    """-> vals [4, n_pairs, n] (S, D, S', D'), status [n_pairs] (, kappa [4, n_pairs, n] if kappa=True:
+    the scale of the terms entering each weight, ||zeta||_inf sum_c |P_ci| + |smooth_i|)."""
     n = S.n
     npairs = int(pair_target.shape[0])
     vals = np.zeros((4, npairs, n))
     st = np.zeros(npairs, np.int32)
+    kap = np.zeros((4, npairs, n)) if kappa else None
     pr = params(S.p, S.q, n_omega, rho0)
-    lib().orc_build_rows(ctypes.byref(pr), ctypes.c_int64(S.n_patches), _p(_c(S.nodes, np.float64)),
+    lib().orc_build_rows2(ctypes.byref(pr), ctypes.c_int64(S.n_patches), _p(_c(S.nodes, np.float64)),
                          _p(_c(S.normals, np.float64)), _p(_c(S.weights, np.float64)),
                          _p(_c(S.verts, np.float64)), _p(_c(S.edge_x, np.float64)),
                          _p(_c(S.edge_dx, np.float64)), _p(_c(tx, np.float64)),
@@ -171,8 +179,8 @@ def build_rows(S, tx, tnormal, self_node, side, pair_target, pair_patch, mask=15
                          _p(_c(self_node, np.int64)) if self_node is not None else None,
                          _p(_c(side, np.int8)) if side is not None else None,
                          ctypes.c_int64(npairs), _p(_c(pair_target, np.int64)), _p(_c(pair_patch, np.int32)),
-                         ctypes.c_uint32(mask), ctypes.c_int(int(raw)), _p(vals), _p(st))
-    return vals, st
+                         ctypes.c_uint32(mask), ctypes.c_int(int(raw)), _p(vals), _p(st), _p(kap))
+    return (vals, st, kap) if kappa else (vals, st)
 
 
 def pair_debug(S, P, x, nu, self_local=-1, side=2, raw=True, n_omega=32, rho0=3.0):

@@ -372,7 +372,7 @@ typedef struct {
   double *xl, *nl;            /* [n][3] local nodes, normals */
   double vl[3][3];            /* local vertices */
   double *yl, *tl;            /* [3q][3] local edge samples, tangents d y / d t */
-  double *C;                  /* [3][q][3] monomial coefficients of each edge interpolant (A4) */
+  double *C;                  /* [3][q][3] Legendre coefficients of each edge interpolant (A4, A4') */
   double zlo, zhi;
   cplx *g;                    /* [3q][(p+1)^2][3] Hess S^{(j,k)}(y) tau */
   cplx *e;                    /* [3q][(p+1)^2][3] grad S^{(j,k)}(y) x tau */
@@ -435,14 +435,27 @@ static void patch_build(patch_t *P, const orc_params *pr, const double *nodes, c
     rot_local(P, edge_dx + 3 * k, P->tl + 3 * k);
     for (int a = 0; a < 3; ++a) P->tl[3 * k + a] /= P->h;
   }
-  /* edge interpolants x(t) = sum_c C_c t^c, C = U y (reading A4) */
-  for (int e = 0; e < 3; ++e)
-    for (int c = 0; c < q; ++c)
-      for (int a = 0; a < 3; ++a) {
-        double s = 0;
-        for (int k = 0; k < q; ++k) s += U[c * q + k] * P->yl[3 * (e * q + k) + a];
-        P->C[(e * q + c) * 3 + a] = s;
-      }
+  /* Edge interpolants (reading A4): the degree q-1 interpolant of the samples, held as a Legendre
+   * series x(t) = sum_j C_j P_j(t) (reading A4': same polynomial as the monomial form c~ = U y of
+   * P:L1231, but evaluated without the cond(V) amplification of monomials).  Gauss-Legendre exactness
+   * gives the discrete transform C_j = (2j+1)/2 sum_k W_k P_j(t_k) y_k. */
+  {
+    double tg[64], wg[64];
+    orc_gauss_legendre(q, tg, wg);
+    for (int e = 0; e < 3; ++e)
+      for (int a = 0; a < 3; ++a)
+        for (int j = 0; j < q; ++j) P->C[(e * q + j) * 3 + a] = 0;
+    for (int k = 0; k < q; ++k) {
+      double Pj[64];
+      Pj[0] = 1;
+      if (q > 1) Pj[1] = tg[k];
+      for (int j = 1; j + 1 < q; ++j) Pj[j + 1] = ((2 * j + 1) * tg[k] * Pj[j] - j * Pj[j - 1]) / (j + 1);
+      for (int e = 0; e < 3; ++e)
+        for (int j = 0; j < q; ++j)
+          for (int a = 0; a < 3; ++a)
+            P->C[(e * q + j) * 3 + a] += 0.5 * (2 * j + 1) * wg[k] * Pj[j] * P->yl[3 * (e * q + k) + a];
+    }
+  }
   /* height range of nodes, vertices, edge samples (reading A8) */
   P->zlo = 1e300; P->zhi = -1e300;
   for (int i = 0; i < n; ++i) { double z = P->xl[3 * i + 2]; if (z < P->zlo) P->zlo = z; if (z > P->zhi) P->zhi = z; }
@@ -554,15 +567,29 @@ static void patch_free(patch_t *P) {
 /* ------------------------------------------------------------------------------------------------
  * Singularity-swap quadrature per edge (Step 5; readings A4, A5, A11, A12).
  * ----------------------------------------------------------------------------------------------*/
+/* x(t), x'(t), x''(t) of the Legendre series C (reading A4'), complex t: Bonnet's recurrence
+ * (j+1)P_{j+1} = (2j+1) t P_j - j P_{j-1} and P'_{j+1} = P'_{j-1} + (2j+1) P_j,
+ * P''_{j+1} = P''_{j-1} + (2j+1) P'_j. */
 static void edge_eval(const double *C, int q, cplx t, cplx *x, cplx *dx, cplx *ddx) {
+  cplx P0 = 1, P1 = t, d0 = 0, d1 = 1, e0 = 0, e1 = 0;
   for (int a = 0; a < 3; ++a) {
-    cplx v = 0, d = 0, dd = 0;
-    for (int c = q - 1; c >= 0; --c) {
-      dd = dd * t + 2.0 * d;
-      d = d * t + v;
-      v = v * t + C[c * 3 + a];
+    x[a] = C[a] * P0;
+    dx[a] = 0;
+    ddx[a] = 0;
+  }
+  if (q > 1)
+    for (int a = 0; a < 3; ++a) { x[a] += C[3 + a] * P1; dx[a] += C[3 + a] * d1; }
+  for (int j = 1; j + 1 < q; ++j) {
+    cplx P2 = ((2 * j + 1) * t * P1 - j * P0) / (j + 1.0);
+    cplx d2 = d0 + (2 * j + 1) * P1;
+    cplx e2 = e0 + (2 * j + 1) * d1;
+    for (int a = 0; a < 3; ++a) {
+      double c = C[(j + 1) * 3 + a];
+      x[a] += c * P2;
+      dx[a] += c * d2;
+      ddx[a] += c * e2;
     }
-    x[a] = v; dx[a] = d; ddx[a] = dd;
+    P0 = P1; P1 = P2; d0 = d1; d1 = d2; e0 = e1; e1 = e2;
   }
 }
 
@@ -660,6 +687,28 @@ void orc_model_integrals(double a, double b, int q, double *Iv, double *Jv) {
   }
 }
 
+/* Reading A11': where t0 lies outside the Bernstein ellipse rho = RHO_DIRECT the upward recurrences
+ * amplify rounding (App. B.8: 1e-10..2e-7 near rho0 = 3 at p~ = 20), while the model integrands
+ * t^k |t - t0|^{-m} are analytic inside that ellipse; there the same integrals are evaluated by an
+ * N_DIRECT-point Gauss-Legendre rule (error ~ rho^{-2 N_DIRECT} < 1e-17).  Inside it, the recurrences
+ * (accurate to ~1e-14 for |t0| <~ 1.1) are used. */
+#define RHO_DIRECT 1.6
+#define N_DIRECT 48
+void orc_model_integrals_direct(double a, double b, int q, double *Iv, double *Jv) {
+  double x[N_DIRECT], w[N_DIRECT];
+  orc_gauss_legendre(N_DIRECT, x, w);
+  for (int k = 0; k < q; ++k) { Iv[k] = 0; Jv[k] = 0; }
+  for (int j = 0; j < N_DIRECT; ++j) {
+    double Qv = (x[j] - a) * (x[j] - a) + b * b;
+    double r1 = w[j] / sqrt(Qv), r3 = r1 / Qv, tk = 1;
+    for (int k = 0; k < q; ++k) {
+      Iv[k] += tk * r1;
+      Jv[k] += tk * r3;
+      tk *= x[j];
+    }
+  }
+}
+
 /* Per-edge quadrature data for one target. */
 typedef struct {
   double w1[64], w3[64];   /* omega^{(1)}_k, omega^{(3)}_k (q <= 64) */
@@ -688,7 +737,8 @@ static void edge_quadrature(const patch_t *P, const orc_params *pr, int e, const
   }
   if (E->swap) {
     double Iv[64], Jv[64];
-    orc_model_integrals(t0r, fabs(t0i), q, Iv, Jv);
+    if (orc_bernstein_rho(t0r, t0i) >= RHO_DIRECT) orc_model_integrals_direct(t0r, fabs(t0i), q, Iv, Jv);
+    else orc_model_integrals(t0r, fabs(t0i), q, Iv, Jv);
     for (int k = 0; k < q; ++k) {
       double mu1 = 0, mu3 = 0;
       for (int c = 0; c < q; ++c) { mu1 += Iv[c] * U[c * q + k]; mu3 += Jv[c] * U[c * q + k]; }
@@ -765,7 +815,7 @@ typedef struct {
 static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, const double *tgl, const double *wgl,
                      const double *xo, const double *wo, const double *x_glob, const double *nu_glob, int self_local,
                      int side, unsigned mask, int raw, const double *nodes_glob, const double *normals_glob,
-                     const double *weights_glob, double *rows, pair_dbg *dbg) {
+                     const double *weights_glob, double *rows, pair_dbg *dbg, double *kap) {
   int p = P->p, q = P->q, n = P->n, np = P->np, L = (p + 1) * (p + 1);
   const double inv4pi = 1.0 / (4.0 * ORC_PI), s2 = sqrt(2.0);
   int is_self = self_local >= 0;
@@ -896,6 +946,36 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
   }
   /* back to global units (reading A2): S rows scale with h, D' rows with 1/h */
   for (int i = 0; i < n; ++i) { rS[i] *= P->h; rDp[i] /= P->h; }
+  /* Optional: kappa_i = ||zeta||_inf * sum_c |P_{c,i}|, the forward-error scale of weight i of the
+   * Step-8 contraction when its input vector zeta is known to a relative accuracy (DESIGN.md §5
+   * parity bar).  Test instrumentation only. */
+  if (kap) {
+    double *kS = kap, *kD = kap + n, *kSp = kap + 2 * n, *kDp = kap + 3 * n;
+    double zW = 0, zdW = 0, zS = 0, zT = 0;
+    for (int c = 0; c < np; ++c) {
+      const double *Wv = Wr + 4 * c + 1;
+      double nxW[3];
+      cross3(nup, Wv, nxW);
+      double s4[4] = {fabs(dot3(nup, Wv)), fabs(Wr[4 * c] * nup[0] + nxW[0]), fabs(Wr[4 * c] * nup[1] + nxW[1]),
+                      fabs(Wr[4 * c] * nup[2] + nxW[2])};
+      for (int b = 0; b < 4; ++b) {
+        zW = fmax(zW, fabs(Wr[4 * c + b]));
+        zdW = fmax(zdW, fabs(dWr[4 * c + b]));
+        zS = fmax(zS, s4[b]);
+      }
+      zT = fmax(zT, fabs(Th[c]));
+    }
+    for (int i = 0; i < n; ++i) {
+      double aD = 0, aSp = 0, aSg = 0, aSd = 0;
+      for (int r = 0; r < 4 * np; ++r) { aD += fabs(PD[r * n + i]); aSp += fabs(PSp[r * n + i]); aSg += fabs(PSg[r * n + i]); }
+      for (int r = 0; r < np; ++r) aSd += fabs(PSd[r * n + i]);
+      kD[i] = zW * aD;
+      kDp[i] = zdW * aD;
+      kSp[i] = zS * aSp;
+      kS[i] = fmax(zW, zT) * (aSg + aSd);
+    }
+    for (int i = 0; i < n; ++i) { kS[i] *= P->h; kDp[i] /= P->h; }
+  }
 
   /* smooth-rule subtraction (reading A14), skipping the self node */
   if (!raw)
@@ -907,10 +987,15 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
       double dn = dot3(d, nu);
       rS[i] -= inv4pi / r * w;
       rD[i] -= inv4pi * dn / r3 * w;
+      if (kap) { kap[i] += fabs(inv4pi / r * w); kap[n + i] += fabs(inv4pi * dn / r3 * w); }
       if (nu_glob) {
         double dnp = dot3(d, nu_glob);
         rSp[i] -= -inv4pi * dnp / r3 * w;
         rDp[i] -= inv4pi * (dot3(nu, nu_glob) / r3 - 3.0 * dn * dnp / (r3 * r * r)) * w;
+        if (kap) {
+          kap[2 * n + i] += fabs(inv4pi * dnp / r3 * w);
+          kap[3 * n + i] += inv4pi * (fabs(dot3(nu, nu_glob) / r3) + fabs(3.0 * dn * dnp / (r3 * r * r))) * w;
+        }
       }
     }
   if (!(mask & 1)) for (int i = 0; i < n; ++i) rS[i] = 0;
@@ -968,11 +1053,11 @@ void orc_patch_fit(int64_t n_patches, int p, int q, const double *nodes, const d
 /* Rows of pairs (pair_target[k], pair_patch[k]) for S, D, S', D' -> vals[4][n_pairs][n]; status
  * bit0 Newton fallback, bit1 nonfinite, bit2 rank-deficient patch fit.  Pairs are processed
  * patch by patch (Steps 1-3 once per patch). */
-void orc_build_rows(const orc_params *prm, int64_t n_patches, const double *nodes, const double *normals,
-                    const double *weights, const double *verts, const double *edge_x, const double *edge_dx,
-                    const double *tx, const double *tnormal, const int64_t *self_node, const int8_t *side,
-                    int64_t n_pairs, const int64_t *pair_target, const int32_t *pair_patch, uint32_t mask, int raw,
-                    double *vals, int32_t *pair_status) {
+void orc_build_rows2(const orc_params *prm, int64_t n_patches, const double *nodes, const double *normals,
+                     const double *weights, const double *verts, const double *edge_x, const double *edge_dx,
+                     const double *tx, const double *tnormal, const int64_t *self_node, const int8_t *side,
+                     int64_t n_pairs, const int64_t *pair_target, const int32_t *pair_patch, uint32_t mask, int raw,
+                     double *vals, int32_t *pair_status, double *kappa) {
   orc_params pr = *prm;
   int p = pr.p, q = pr.q, n = p * p;
   tables_t *T = malloc(sizeof(tables_t));
@@ -991,22 +1076,34 @@ void orc_build_rows(const orc_params *prm, int64_t n_patches, const double *node
     patch_t pt;
     patch_build(&pt, &pr, nodes + P * n * 3, normals + P * n * 3, verts + P * 9, edge_x + P * 3 * q * 3,
                 edge_dx + P * 3 * q * 3, T->U, 1);
-    double *rows = malloc(sizeof(double) * 4 * n);
+    double *rows = malloc(sizeof(double) * 4 * n), *krow = malloc(sizeof(double) * 4 * n);
     for (int64_t s = cnt[P]; s < cnt[P + 1]; ++s) {
       int64_t k = ord[s], t = pair_target[k];
       int self_local = -1;
       if (self_node && self_node[t] >= 0 && self_node[t] / n == P) self_local = (int)(self_node[t] % n);
       int sd = side ? side[t] : 2;
       int st = pair_rows(&pt, &pr, T->U, T->tgl, T->wgl, T->xo, T->wo, tx + 3 * t, tnormal ? tnormal + 3 * t : NULL,
-                         self_local, sd, mask, raw, nodes + P * n * 3, normals + P * n * 3, weights + P * n, rows, NULL);
+                         self_local, sd, mask, raw, nodes + P * n * 3, normals + P * n * 3, weights + P * n, rows, NULL,
+                         kappa ? krow : NULL);
+      if (kappa)
+        for (int kk = 0; kk < 4; ++kk) memcpy(kappa + ((size_t)kk * n_pairs + k) * n, krow + kk * n, sizeof(double) * n);
       if (pt.status) st |= 4;
       for (int kk = 0; kk < 4; ++kk) memcpy(vals + ((size_t)kk * n_pairs + k) * n, rows + kk * n, sizeof(double) * n);
       if (pair_status) pair_status[k] = st;
     }
-    free(rows);
+    free(rows); free(krow);
     patch_free(&pt);
   }
   free(cnt); free(ord); free(T);
+}
+
+void orc_build_rows(const orc_params *prm, int64_t n_patches, const double *nodes, const double *normals,
+                    const double *weights, const double *verts, const double *edge_x, const double *edge_dx,
+                    const double *tx, const double *tnormal, const int64_t *self_node, const int8_t *side,
+                    int64_t n_pairs, const int64_t *pair_target, const int32_t *pair_patch, uint32_t mask, int raw,
+                    double *vals, int32_t *pair_status) {
+  orc_build_rows2(prm, n_patches, nodes, normals, weights, verts, edge_x, edge_dx, tx, tnormal, self_node, side, n_pairs,
+                  pair_target, pair_patch, mask, raw, vals, pair_status, NULL);
 }
 
 /* Debug entry for one pair: intermediates (Omega_0, Omega, derivatives, t0, regimes, W, dW, Theta),
@@ -1023,7 +1120,7 @@ int orc_pair_debug(const orc_params *prm, const double *nodes, const double *nor
   pair_dbg dbg;
   dbg.W = W; dbg.dW = dW; dbg.Th = Th;
   int st = pair_rows(&pt, &pr, T->U, T->tgl, T->wgl, T->xo, T->wo, x, nu, self_local, side, 15u, raw, nodes, normals,
-                     weights, rows, &dbg);
+                     weights, rows, &dbg, NULL);
   scal[0] = dbg.om0;
   for (int a = 0; a < 3; ++a) scal[1 + a] = dbg.om[a];
   scal[4] = dbg.dom0;

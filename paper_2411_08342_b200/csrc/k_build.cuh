@@ -71,12 +71,65 @@ struct WarpScratch {
   double Qv[D::NQ][8], dQ[D::NQ][8], V[D::NV][2];
   double t0[3][2];
   double Om[4], dOm[4];   // (Omega_0, Omega), (dOmega_0, dOmega)
-  int swap[3], conv[3];
+  double r13[2][kNDirect];
+  int swap[3], conv[3], direct[3];
 };
 
 struct SmemTables {
   int q, n_omega;
 };
+
+// Legendre-series edge interpolant (reading A4'): value and derivatives of component c at t, by
+// Bonnet's recurrence and P'_{j+1} = P'_{j-1} + (2j+1) P_j, P''_{j+1} = P''_{j-1} + (2j+1) P'_j.
+template <int Q>
+__device__ __forceinline__ void leg_r(const double *C, int c, double t, double &v, double &d1, double &d2) {
+  double P0 = 1, P1 = t, a0 = 0, a1 = 1, b0 = 0, b1 = 0;
+  v = C[c] + C[3 + c] * t;
+  d1 = C[3 + c];
+  d2 = 0;
+#pragma unroll
+  for (int j = 1; j + 1 < Q; ++j) {
+    double P2 = ((2 * j + 1) * t * P1 - j * P0) * (1.0 / (j + 1));
+    double a2 = a0 + (2 * j + 1) * P1, b2 = b0 + (2 * j + 1) * a1;
+    double cc = C[3 * (j + 1) + c];
+    v = fma(cc, P2, v);
+    d1 = fma(cc, a2, d1);
+    d2 = fma(cc, b2, d2);
+    P0 = P1; P1 = P2; a0 = a1; a1 = a2; b0 = b1; b1 = b2;
+  }
+}
+template <int Q>
+__device__ __forceinline__ void leg_c(const double *C, int c, cd t, cd &v, cd &d1) {
+  cd P0 = mk(1, 0), P1 = t, a0 = mk(0, 0), a1 = mk(1, 0);
+  v = mk(C[c], 0) + C[3 + c] * t;
+  d1 = mk(C[3 + c], 0);
+#pragma unroll
+  for (int j = 1; j + 1 < Q; ++j) {
+    cd P2 = (1.0 / (j + 1)) * ((2.0 * j + 1) * (t * P1) - (double)j * P0);
+    cd a2 = a0 + (2.0 * j + 1) * P1;
+    double cc = C[3 * (j + 1) + c];
+    v = v + cc * P2;
+    d1 = d1 + cc * a2;
+    P0 = P1; P1 = P2; a0 = a1; a1 = a2;
+  }
+}
+// x(t), x'(t) (3 components, real t)
+template <int Q>
+__device__ __forceinline__ void leg_r3(const double *C, double t, double x[3], double dx[3]) {
+  double P0 = 1, P1 = t, a0 = 0, a1 = 1;
+  for (int c = 0; c < 3; ++c) { x[c] = C[c] + C[3 + c] * t; dx[c] = C[3 + c]; }
+#pragma unroll
+  for (int j = 1; j + 1 < Q; ++j) {
+    double P2 = ((2 * j + 1) * t * P1 - j * P0) * (1.0 / (j + 1));
+    double a2 = a0 + (2 * j + 1) * P1;
+    for (int c = 0; c < 3; ++c) {
+      double cc = C[3 * (j + 1) + c];
+      x[c] = fma(cc, P2, x[c]);
+      dx[c] = fma(cc, a2, dx[c]);
+    }
+    P0 = P1; P1 = P2; a0 = a1; a1 = a2;
+  }
+}
 
 // sum of a value over the 3 lanes {3e, 3e+1, 3e+2}
 __device__ __forceinline__ double tri_sum(double v, int base) {
@@ -185,14 +238,7 @@ __global__ void __launch_bounds__(WPB * 32)
       const int e = lane < 9 ? lane / 3 : 2, c = lane < 9 ? lane % 3 : 2, base = 3 * e;
       const double *C = blk + L::CM + e * Q * 3;
       const double rc = rp[c];
-      auto horner_r = [&](double tt, double &v, double &d1, double &d2) {
-        v = 0; d1 = 0; d2 = 0;
-        for (int q = Q - 1; q >= 0; --q) {
-          d2 = d2 * tt + 2.0 * d1;
-          d1 = d1 * tt + v;
-          v = v * tt + C[q * 3 + c];
-        }
-      };
+      auto horner_r = [&](double tt, double &v, double &d1, double &d2) { leg_r<Q>(C, c, tt, v, d1, d2); };
       double v, d1, d2;
       horner_r(-1.0, v, d1, d2);
       double A = v;
@@ -214,11 +260,8 @@ __global__ void __launch_bounds__(WPB * 32)
       cd tz = mk(tc, sqrt(f / dd));
       bool conv = false;
       for (int it = 0; it < 20; ++it) {
-        cd xv = mk(0, 0), xd = mk(0, 0);
-        for (int q = Q - 1; q >= 0; --q) {
-          xd = xd * tz + xv;
-          xv = xv * tz + mk(C[q * 3 + c], 0);
-        }
+        cd xv, xd;
+        leg_c<Q>(C, c, tz, xv, xd);
         cd xrr = xv - mk(rc, 0);
         cd sq = xrr * xrr, pr = xrr * xd;
         cd F = mk(tri_sum(sq.x, base), tri_sum(sq.y, base));
@@ -236,11 +279,37 @@ __global__ void __launch_bounds__(WPB * 32)
         ws.t0[e][0] = tz.x;
         ws.t0[e][1] = tz.y;
         ws.conv[e] = conv;
-        ws.swap[e] = conv && bernstein_rho(tz.x, tz.y) < rho0;
+        double rho = bernstein_rho(tz.x, tz.y);
+        ws.swap[e] = conv && rho < rho0;
+        ws.direct[e] = rho >= kRhoDirect;
       }
     }
     __syncwarp();
-    if (lane < 3 && ws.swap[lane]) model_integrals<Q>(ws.t0[lane][0], fabs(ws.t0[lane][1]), ws.I[lane], ws.J[lane]);
+    // model integrals (reading A11 / A11'): recurrences inside rho = 1.6, a 48-point rule outside
+    if (lane < 3 && ws.swap[lane] && !ws.direct[lane])
+      model_integrals<Q>(ws.t0[lane][0], fabs(ws.t0[lane][1]), ws.I[lane], ws.J[lane]);
+    for (int e = 0; e < 3; ++e) {
+      if (!(ws.swap[e] && ws.direct[e])) continue;
+      const double a = ws.t0[e][0], b = fabs(ws.t0[e][1]);
+      for (int j = lane; j < kNDirect; j += 32) {
+        double xj = T.xd[j], Qv = (xj - a) * (xj - a) + b * b;
+        double r1 = T.wd[j] / sqrt(Qv);
+        ws.r13[0][j] = r1;
+        ws.r13[1][j] = r1 / Qv;
+      }
+      __syncwarp();
+      if (lane < Q) {
+        double si = 0, sj = 0;
+        for (int j = 0; j < kNDirect; ++j) {
+          double pw = __ldg(T.xdp + j * Q + lane);
+          si = fma(pw, ws.r13[0][j], si);
+          sj = fma(pw, ws.r13[1][j], sj);
+        }
+        ws.I[e][lane] = si;
+        ws.J[e][lane] = sj;
+      }
+      __syncwarp();
+    }
     __syncwarp();
 
     // ---------------- weights and the scalar line integrals (Step 6)
@@ -293,12 +362,8 @@ __global__ void __launch_bounds__(WPB * 32)
         if (!(hi > lo)) continue;
         double sv = lo + (hi - lo) * (sxo[jj] + 1) * 0.5, W = (hi - lo) * 0.5 * swo[jj];
         double tt = a + b * sinh(sv), dt = b * cosh(sv);
-        double x[3] = {0, 0, 0}, dx[3] = {0, 0, 0};
-        for (int q = Q - 1; q >= 0; --q)
-          for (int c = 0; c < 3; ++c) {
-            dx[c] = dx[c] * tt + x[c];
-            x[c] = x[c] * tt + C[q * 3 + c];
-          }
+        double x[3], dx[3];
+        leg_r3<Q>(C, tt, x, dx);
         double d[3] = {rp[0] - x[0], rp[1] - x[1], rp[2] - x[2]};
         double nd = sqrt(dot3(d, d)), dxu[3];
         cross3(d, u, dxu);
@@ -444,8 +509,8 @@ template <int P>
 struct ContractCfg {
   static constexpr int N = Dims<P>::N;
   static constexpr int G = (128 / N) > 0 ? (128 / N) : 1;
-  static constexpr int TILE = P >= 8 ? 8 : 16;
-  static constexpr int RB = (TILE + G - 1) / G;
+  static constexpr int RB = ((P >= 8 ? 8 : 16) + G - 1) / G;   // pairs per thread
+  static constexpr int TILE = RB * G;                          // pairs per CTA tile
   static constexpr int THREADS = ((G * N + 31) / 32) * 32;
 };
 

@@ -41,7 +41,7 @@ __global__ void k_patch_balls(int64_t n_patches, int n, int q, const double *__r
   }
 }
 
-// Frame, local edge samples / tangents, monomial coefficients C = U y, height range.
+// Frame, local edge samples / tangents, Legendre coefficients of the edge interpolants (A4'), height range.
 // One CTA (128 threads) per patch.
 template <int P>
 __global__ void k_patch_geom(int64_t n_patches, const double *__restrict__ nodes, const double *__restrict__ verts,
@@ -99,13 +99,25 @@ __global__ void k_patch_geom(int64_t n_patches, const double *__restrict__ nodes
   red[0][threadIdx.x] = zlo;
   red[1][threadIdx.x] = zhi;
   __syncthreads();
-  // edge interpolant coefficients C[e][c][a] = sum_k U[c][k] y[e][k][a]
+  // Edge interpolants as Legendre series x(t) = sum_j C_j P_j(t) (reading A4'): by Gauss-Legendre
+  // exactness C_j = (2j+1)/2 sum_k w_k P_j(t_k) y_k.  Thread (e, j, a).
   for (int t = threadIdx.x; t < 9 * D::Q; t += blockDim.x) {
-    int e = t / (3 * D::Q), c = (t / 3) % D::Q, a = t % 3;
+    int e = t / (3 * D::Q), j = (t / 3) % D::Q, a = t % 3;
     double s = 0;
-    for (int k = 0; k < D::Q; ++k) s += T.U[c * D::Q + k] * blk[L::YL + 3 * (e * D::Q + k) + a];
-    blk[L::CM + t] = s;
+    for (int k = 0; k < D::Q; ++k) {
+      double tk = T.tgl[k], p0 = 1.0, p1 = tk, pj = 1.0;
+      if (j == 1) pj = tk;
+      for (int i = 1; i < j; ++i) {
+        double p2 = ((2 * i + 1) * tk * p1 - i * p0) / (i + 1);
+        p0 = p1;
+        p1 = p2;
+        pj = p2;
+      }
+      s += T.wgl[k] * pj * blk[L::YL + 3 * (e * D::Q + k) + a];
+    }
+    blk[L::CM + t] = 0.5 * (2 * j + 1) * s;
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     double lo = 1e300, hi = -1e300;
     for (int i = 0; i < blockDim.x; ++i) { lo = fmin(lo, red[0][i]); hi = fmax(hi, red[1][i]); }

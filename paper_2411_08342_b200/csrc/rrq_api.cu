@@ -34,6 +34,7 @@ struct rrq_ctx_s {
     void *p = nullptr;
     size_t n = 0;
   };
+  int64_t last_np = 0, last_nz = 0;
   Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one, swapcnt;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
@@ -158,7 +159,13 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
       b = b * (n - k) / (k + 1);
     }
   }
-  size_t tot = 2 * q + q * q + 2 * no + 41 * 41;
+  std::vector<double> xd(kNDirect), wd(kNDirect), xdp(kNDirect * q);
+  rrq_host::gauss_legendre(kNDirect, xd.data(), wd.data());
+  for (int j = 0; j < kNDirect; ++j) {
+    double pw = 1;
+    for (int k = 0; k < q; ++k) { xdp[j * q + k] = pw; pw *= xd[j]; }
+  }
+  size_t tot = 2 * q + q * q + 2 * no + 41 * 41 + 2 * kNDirect + kNDirect * q;
   if (cudaMalloc(&c->d_tab, tot * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     delete c;
@@ -172,6 +179,10 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   std::copy(xo.begin(), xo.end(), t + 2 * q + q * q);
   std::copy(wo.begin(), wo.end(), t + 2 * q + q * q + no);
   std::copy(sqb.begin(), sqb.end(), t + 2 * q + q * q + 2 * no);
+  double *td = t + 2 * q + q * q + 2 * no + 41 * 41;
+  std::copy(xd.begin(), xd.end(), td);
+  std::copy(wd.begin(), wd.end(), td + kNDirect);
+  std::copy(xdp.begin(), xdp.end(), td + 2 * kNDirect);
   cudaMemcpy(c->d_tab, h.data(), tot * sizeof(double), cudaMemcpyHostToDevice);
   c->T.tgl = c->d_tab;
   c->T.wgl = c->d_tab + q;
@@ -179,6 +190,9 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   c->T.xo = c->d_tab + 2 * q + q * q;
   c->T.wo = c->T.xo + no;
   c->T.sqb = c->T.wo + no;
+  c->T.xd = c->T.sqb + 41 * 41;
+  c->T.wd = c->T.xd + kNDirect;
+  c->T.xdp = c->T.wd + kNDirect;
   if (cuda_check(c, "rrq_create") != RRQ_OK) {
     g_create_err = c->err;
     rrq_destroy(c);
@@ -203,6 +217,16 @@ void rrq_destroy(rrq_ctx c) {
 const char *rrq_last_error(rrq_ctx c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
 int64_t rrq_launch_count(rrq_ctx c) { return c ? c->launches : 0; }
+
+rrq_status rrq_debug_zeta(rrq_ctx c, int64_t max_pairs, int64_t *perm, double *Z, int64_t *n_out) {
+  if (!c || !n_out) return RRQ_ERR_INVALID_ARG;
+  cudaDeviceSynchronize();
+  int64_t n = std::min(max_pairs, c->last_np);
+  if (perm && n > 0) cudaMemcpy(perm, c->perm.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost);
+  if (Z && n > 0) cudaMemcpy(Z, c->Z.p, n * c->last_nz * sizeof(double), cudaMemcpyDeviceToHost);
+  *n_out = n;
+  return cuda_check(c, "rrq_debug_zeta");
+}
 
 rrq_status rrq_set_timing(rrq_ctx c, int enable) {
   if (!c) return RRQ_ERR_INVALID_ARG;
@@ -493,6 +517,8 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     c->launches++;
     rrq_status r;
     if ((r = cuda_check(c, "k_pair_zeta"))) return r;
+    c->last_np = np_;
+    c->last_nz = D::NZ;
     cudaStreamSynchronize(st);   // n_items
     if (n_items > 0) {
       TScope tc(c, 3, st);

@@ -70,7 +70,11 @@ struct Tables {
   const double *U;           // [q][q]  c~_c = sum_k U[c][k] F_k
   const double *xo, *wo;     // [n_omega] GL on (-1,1)
   const double *sqb;         // [41][41] sqrt(binomial(n, k))
+  const double *xd, *wd;     // [N_DIRECT] Gauss-Legendre rule of the direct model integrals (A11')
+  const double *xdp;         // [N_DIRECT][q] powers x_j^k
 };
+constexpr int kNDirect = 48;       // reading A11'
+constexpr double kRhoDirect = 1.6;
 
 // R_l^m(X,Y,Z), 0 <= m <= l <= P (no Condon-Shortley phase, reading G5) by the Cartesian recurrences
 //  R_m^m = sqrt((2m-1)/(2m)) (X + iY) R_{m-1}^{m-1},  R_{m+1}^m = sqrt(2m+1) Z R_m^m,

@@ -74,6 +74,8 @@ def load_library():
     lib.rrq_reset_timing.restype = ctypes.c_int
     lib.rrq_get_timing.argtypes = [vp, vp, vp, vp]
     lib.rrq_get_timing.restype = ctypes.c_int
+    lib.rrq_debug_zeta.argtypes = [vp, i64, vp, vp, ctypes.POINTER(i64)]
+    lib.rrq_debug_zeta.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -175,6 +177,16 @@ class RRQ:
         self._check(self.lib.rrq_get_timing(self.h, ms.ctypes.data, n.ctypes.data, st.ctypes.data), "rrq_get_timing")
         return dict(ms=dict(zip(self.STAGES, ms.tolist())), launches=dict(zip(self.STAGES, n.tolist())),
                     pairs=int(st[0]), swap_edges=int(st[1]))
+
+    def debug_zeta(self, max_pairs):
+        """Test hook: (perm, Z[., 13 n_p]) of the last build sub-chunk."""
+        import numpy as np
+        npb = self.p * (self.p + 1) // 2
+        perm = np.zeros(max_pairs, np.int64); Z = np.zeros((max_pairs, 13 * npb))
+        n = ctypes.c_int64(0)
+        self._check(self.lib.rrq_debug_zeta(self.h, max_pairs, perm.ctypes.data, Z.ctypes.data, ctypes.byref(n)),
+                    "rrq_debug_zeta")
+        return perm[: n.value], Z[: n.value]
 
     def tables(self):
         q = 2 * self.p

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs,
+element by element: near lists bit-exact; CSR weights per row within
+max(1e-11 * max_row |o|, 1e-13) (north star), with the conditioning band for
+targets within 1e-4 h of a patch edge or vertex (config 5)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O
+from synth.configs import make_config
+import parity_util as U
+
+pytestmark = pytest.mark.gpu
+
+REL, ABS = 1e-11, 1e-13
+STATS = {}
+
+
+def _gpu_ctx(cfg):
+    from paper_2411_08342_b200 import RRQ
+    eta = cfg["eta"] if np.isfinite(cfg["eta"]) else 0.0
+    return RRQ(cfg["surface"].p, eta=eta, all_pairs=cfg["all_pairs"])
+
+
+def _upload(cfg, tx=None, nu=None, sn=None, sd=None):
+    from paper_2411_08342_b200 import DeviceSurface, DeviceTargets
+    tx = cfg["tx"] if tx is None else tx
+    return (DeviceSurface.from_numpy(cfg["surface"]),
+            DeviceTargets.from_numpy(tx, cfg["tnormal"] if nu is None else nu,
+                                     cfg["self_node"] if sn is None else sn, cfg["side"] if sd is None else sd))
+
+
+def _gpu_rows_of(ptr, pat, tg, pa):
+    pos = np.empty(tg.shape[0], np.int64)
+    for i, (t, p) in enumerate(zip(tg, pa)):
+        seg = pat[ptr[t]:ptr[t + 1]]
+        j = np.searchsorted(seg, p)
+        assert j < seg.size and seg[j] == p, "pair missing from the GPU near list"
+        pos[i] = ptr[t] + j
+    return pos
+
+
+def _compare(vals_gpu, vo, pos, tg, n, band=None, kap=None, tag=""):
+    """Per-pair band relaxes the whole CSR row of that pair's target (max over its pairs)."""
+    inv = np.unique(tg, return_inverse=True)[1]
+    if band is not None:
+        rb = np.ones(inv.max() + 1)
+        np.maximum.at(rb, inv, band)
+        band = rb[inv]
+    worst = []
+    for k in range(4):
+        g = np.stack([vals_gpu[k][pp * n:(pp + 1) * n] for pp in pos]).reshape(-1)
+        st = {}
+        w, ratio = U.compare_rows(g, vo[k], inv, n, REL, ABS, band, None if kap is None else kap[k], st)
+        STATS[f"{tag}:{'S D Sp Dp'.split()[k]}"] = st
+        worst.append(w)
+    print(tag, STATS)
+    return worst
+
+
+@pytest.mark.parametrize("p", [4, 6, 8, 10])
+def test_tables_bit_identical_to_oracle(p):
+    from paper_2411_08342_b200 import RRQ
+    t, w, Uu = RRQ(p).tables()
+    to, wo, Uo = O.tables(2 * p)
+    assert np.array_equal(t, to) and np.array_equal(w, wo)
+    assert np.array_equal(Uu, Uo)
+
+
+@pytest.mark.parametrize("raw", [False, True])
+def test_cfg1_all_pairs(raw):
+    cfg = make_config(1)
+    S = cfg["surface"]
+    tgs = (cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
+    res = U.gpu_build(cfg, S, tgs, raw=raw)
+    ptr_o, pat_o = O.near_list(S, cfg["tx"], cfg["self_node"], cfg["eta"])
+    assert np.array_equal(res["ptr"], ptr_o) and np.array_equal(res["pat"], pat_o)
+    tg, pa = O.pairs_from_ptr(ptr_o, pat_o)
+    vo, sto, kap = O.build_rows(S, *tgs, tg, pa, raw=raw, kappa=True)
+    for k in range(4):
+        st = {}
+        w, _ = U.compare_rows(res["vals"][k], vo[k], tg, S.n, REL, ABS, kappa=kap[k], stats=st)
+        print("cfg1", k, st)
+        assert w <= 1.0, (k, w)
+    # columns and row pointers
+    assert np.array_equal(res["row_ptr"], ptr_o * S.n)
+    assert np.array_equal(res["col"][: pa.size * S.n].reshape(-1, S.n), pa[:, None] * S.n + np.arange(S.n)[None])
+    # Newton fallback flags agree except on knife-edge pairs
+    assert np.mean((res["status"][: pa.size] & 1) != (sto & 1)) < 1e-3
+
+
+def _sampled_config(cfgid, n_nodes_t, n_off, n_patches_sample, seed=0, **kw):
+    cfg = make_config(cfgid, n_off=n_off, **kw)
+    S = cfg["surface"]
+    rng = np.random.default_rng(seed)
+    nn = S.n_patches * S.n
+    nodes_sel = np.sort(rng.choice(nn, size=min(n_nodes_t, nn), replace=False))
+    off = np.arange(nn, cfg["tx"].shape[0]) if cfg["tx"].shape[0] > nn else np.arange(0)
+    keep = np.concatenate([nodes_sel, off]) if cfgid != 5 else np.arange(cfg["tx"].shape[0])
+    tx, nu, sn, sd = cfg["tx"][keep], cfg["tnormal"][keep], cfg["self_node"][keep], cfg["side"][keep]
+    return cfg, S, (tx, nu, sn, sd), rng
+
+
+@pytest.mark.parametrize("cfgid,nodes,off,npatch,kw", [
+    (2, 4000, 4000, 10, {}),
+    (3, 4000, 6000, 12, {}),
+    (4, 6000, 6000, 6, {}),
+])
+def test_full_size_surfaces_sampled_rows(cfgid, nodes, off, npatch, kw):
+    """Full-size surfaces of configs 2-4; GPU builds every row of a target subset; the oracle
+    recomputes all near pairs of a few random patches (near sets compared exactly)."""
+    cfg, S, tgs, rng = _sampled_config(cfgid, nodes, off, npatch, **kw)
+    res = U.gpu_build(cfg, S, tgs)
+    ptr, pat = res["ptr"], res["pat"]
+    patches = rng.choice(np.unique(pat), size=npatch, replace=False)
+    tg, pa = O.near_pairs_for_patches(S, tgs[0], tgs[2], cfg["eta"], patches)
+    # exact equality of the near sets of the sampled patches
+    for q in patches:
+        gpu_t = np.sort(np.repeat(np.arange(ptr.size - 1), np.diff(ptr))[pat == q])
+        assert np.array_equal(gpu_t, np.sort(tg[pa == q])), q
+    pos = _gpu_rows_of(ptr, pat, tg, pa)
+    vo, sto, kap = O.build_rows(S, *tgs, tg, pa, kappa=True)
+    band = _band_for_pairs(S, tgs[0], tg, pa)
+    worst = _compare(res["vals"], vo, pos, tg, S.n, band, kap, tag=f"cfg{cfgid}")
+    print(f"cfg{cfgid}: {tg.size} pairs, {int((band > 1).sum())} in the conditioning band, worst {worst}")
+    assert max(worst) <= 1.0, worst
+
+
+def _edge_distance(S, x, P=0):
+    """Distance of each point to the exact boundary curves of patch P (dense sampling + local
+    refinement) divided by h_P."""
+    from scipy.spatial import cKDTree
+    u = np.linspace(0, 1, 4001)
+    curves = [lambda u: (u, 0 * u), lambda u: (1 - u, u), lambda u: (0 * u, 1 - u)]
+    pts, par = [], []
+    for e, cv in enumerate(curves):
+        X, _, _ = S.eval_patch(P, *cv(u))
+        pts.append(X); par += [(e, uu) for uu in u]
+    E = np.concatenate(pts)
+    d, j = cKDTree(E).query(np.atleast_2d(x))
+    # refine around the closest sample
+    out = np.empty(d.shape)
+    for i in range(len(d)):
+        e, u0 = par[j[i]]
+        uu = np.clip(np.linspace(u0 - 3e-4, u0 + 3e-4, 2001), 0, 1)
+        X, _, _ = S.eval_patch(P, *curves[e](uu))
+        out[i] = np.min(np.linalg.norm(X - np.atleast_2d(x)[i], axis=1))
+    v = S.verts[P]
+    h = max(np.linalg.norm(v[k] - v[(k + 1) % 3]) for k in range(3))
+    return out / h
+
+
+def _band_for_pairs(S, tx, tg, pa):
+    """Conditioning band: rows within delta < 1e-4 h of an edge or vertex of P
+    have sensitivity ~ eps h / delta to input rounding; tolerance x max(1, 1e-5 h / delta)."""
+    band = np.ones(tg.shape[0])
+    for q in np.unique(pa):
+        sel = np.where(pa == q)[0]
+        delta = _edge_distance(S, tx[tg[sel]], int(q))
+        band[sel] = np.maximum(1.0, 1e-5 / np.maximum(delta, 1e-300))
+    return band
+
+
+def test_cfg5_close_evaluation_sweep():
+    """Config 5 (one cap, p = 10, all pairs) on 3000 of its seeded targets; rows within 1e-4 h of an
+    edge get the conditioning band max(1, 1e-5 h / delta), reported separately."""
+    cfg = make_config(5, n_off=3000)
+    S = cfg["surface"]
+    tgs = (cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
+    res = U.gpu_build(cfg, S, tgs)
+    T = cfg["tx"].shape[0]
+    assert np.array_equal(res["ptr"], np.arange(T + 1))
+    tg = np.arange(T, dtype=np.int64); pa = np.zeros(T, np.int32)
+    vo, sto, kap = O.build_rows(S, *tgs, tg, pa, kappa=True)
+    delta = _edge_distance(S, cfg["tx"], 0)
+    band = np.maximum(1.0, 1e-5 / np.maximum(delta, 1e-300))
+    print("cfg5: rows in the conditioning band:", int((band > 1).sum()), "of", T)
+    for k in range(4):
+        st = {}
+        w, ratio = U.compare_rows(res["vals"][k], vo[k], tg, S.n, REL, ABS, band, kap[k], st)
+        print("cfg5", k, st, "worst", w)
+        assert w <= 1.0, (k, w)
+
+
+def test_row_chunks_and_masks():
+    from paper_2411_08342_b200 import RRQError
+    cfg = make_config(1, n_off=300)
+    S = cfg["surface"]
+    ctx = _gpu_ctx(cfg)
+    ds, dt = _upload(cfg)
+    ptr, pat = ctx.near_list(ds, dt)
+    fit, _ = ctx.patch_fit(ds)
+    full = ctx.build_correction(ds, dt, ptr, pat, fit)
+    T = dt.n_targets
+    hp = ptr.cpu().numpy()
+    n = S.n
+    for (r0, r1) in [(0, 77), (77, 400), (400, T)]:
+        part = ctx.build_correction(ds, dt, ptr, pat, fit, row_begin=r0, row_end=r1)
+        a, b = hp[r0] * n, hp[r1] * n
+        for k in range(4):
+            assert torch.equal(part["vals"][k][: b - a], full["vals"][k][a:b])
+        assert torch.equal(part["row_ptr"], (ptr[r0:r1 + 1] - ptr[r0]) * n)
+    # S and D only, without target normals
+    ds2, dt2 = _upload(cfg)
+    from paper_2411_08342_b200 import DeviceTargets
+    dtn = DeviceTargets(dt.x, None, dt.self_node, dt.side)
+    sd = ctx.build_correction(ds, dtn, ptr, pat, fit, mask=3)
+    assert torch.equal(sd["vals"][0], full["vals"][0]) and torch.equal(sd["vals"][1], full["vals"][1])
+    with pytest.raises(RRQError):
+        ctx.build_correction(ds, dtn, ptr, pat, fit, mask=15)
+    # empty target set
+    e = DeviceTargets(dt.x[:0], dt.normal[:0], dt.self_node[:0], dt.side[:0])
+    p0, q0 = ctx.near_list(ds, e)
+    assert p0.numel() == 1 and q0.numel() == 0
+
+
+def test_apply_correction_spmv():
+    cfg = make_config(1, n_off=300)
+    S = cfg["surface"]
+    ctx = _gpu_ctx(cfg)
+    ds, dt = _upload(cfg)
+    ptr, pat = ctx.near_list(ds, dt)
+    fit, _ = ctx.patch_fit(ds)
+    out = ctx.build_correction(ds, dt, ptr, pat, fit)
+    rng = np.random.default_rng(0)
+    dens = torch.as_tensor(rng.standard_normal(S.n_patches * S.n), device="cuda")
+    y = torch.zeros(dt.n_targets, dtype=torch.float64, device="cuda")
+    ctx.apply_correction(out["row_ptr"], out["col_idx"], out["vals"][1], dens, y)
+    rp = out["row_ptr"].cpu().numpy(); col = out["col_idx"].cpu().numpy(); v = out["vals"][1].cpu().numpy()
+    d = dens.cpu().numpy()
+    ref = np.array([np.dot(v[rp[i]:rp[i + 1]], d[col[rp[i]:rp[i + 1]]]) for i in range(dt.n_targets)])
+    assert np.abs(y.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_fit_operators_match_oracle():
+    """The per-patch pseudo-inverse is unique (full column rank), so both sides agree to rounding."""
+    cfg = make_config(2, n_off=10)
+    S = cfg["surface"]
+    ctx = _gpu_ctx(cfg)
+    ds, dt = _upload(cfg)
+    fit, st = ctx.patch_fit(ds)
+    assert int(st.max()) == 0
+    import paper_2411_08342_b200.rrq  # noqa
+    p, n = S.p, S.n
+    npb = p * (p + 1) // 2
+    stride = ctx.fit_bytes(1) // 8
+    g = fit.view(S.n_patches, stride).cpu().numpy()
+    # FIT block offset: 32 + 6E + 9Q doubles (Layout<P>::FIT)
+    E, Q = 6 * p, 2 * p
+    off = 32 + 6 * E + 9 * Q
+    sel = np.array([0, 101, 777, 1279])
+    from synth.geometry import Surface
+    Ssub = Surface(p=p, q=S.q, nodes=S.nodes[sel], normals=S.normals[sel], weights=S.weights[sel],
+                   verts=S.verts[sel], edge_x=S.edge_x[sel], edge_dx=S.edge_dx[sel], uv=S.uv)
+    fo, _ = O.patch_fit(Ssub)
+    for i, P in enumerate(sel):
+        gb = g[P, off:off + 13 * npb * n].reshape(13 * npb, n)
+        assert np.abs(gb - fo[i]).max() <= 1e-9 * np.abs(fo[i]).max()
+
+
+def test_zeta_vectors_match_oracle():
+    """Element-wise parity of the Steps 4-7 output (the contraction vectors zeta = (Theta, zeta(W),
+    zeta(dW))) before the ill-conditioned Step-8 contraction: |g - o| <= 1e-10 max|zeta|."""
+    cfg, S, tgs, rng = _sampled_config(2, 3000, 3000, 0)
+    res = U.gpu_build(cfg, S, tgs)
+    perm, Z = res["ctx"].debug_zeta(10 ** 8)
+    inv = np.empty(perm.max() + 1, np.int64)
+    inv[perm] = np.arange(perm.size)
+    ptr, pat = res["ptr"], res["pat"]
+    tgt = np.repeat(np.arange(ptr.size - 1), np.diff(ptr))
+    n, p = S.n, S.p
+    npb = p * (p + 1) // 2
+    worst = 0.0
+    for k in rng.choice(perm, 150, replace=False):
+        t, P = tgt[k], pat[k]
+        sl = int(tgs[2][t] % n) if tgs[2][t] >= 0 and tgs[2][t] // n == P else -1
+        d = O.pair_debug(S, P, tgs[0][t], tgs[1][t], self_local=sl, side=int(tgs[3][t]))
+        W, dW, Th = d["W"], d["dW"], d["Theta"]
+        for a, b, ref in [(0, npb, Th), (npb, 5 * npb, np.concatenate([W[:, 0], -W[:, 1], -W[:, 2], -W[:, 3]])),
+                          (5 * npb, 9 * npb, np.concatenate([dW[:, 0], -dW[:, 1], -dW[:, 2], -dW[:, 3]]))]:
+            worst = max(worst, np.abs(Z[inv[k]][a:b] - ref).max() / (U.KAPPA_REL * np.abs(ref).max()))
+    assert worst <= 1.0, worst

@@ -55,6 +55,21 @@ def test_model_integrals_vs_mpmath(t0):
         assert abs(J[k] - rj) <= 1e-10 * max(sj, 1.0), (k, J[k], rj)
 
 
+@pytest.mark.parametrize("t0", [0.15 + 1.17j, -1.6 + 1.3j, 1.8 + 0.8j, 1.3 + 0.01j, 0.0 + 2.0j])
+def test_model_integrals_direct_rule_vs_mpmath(t0):
+    """Reading A11': outside rho = 1.6 the model integrals come from a 48-point Gauss-Legendre rule."""
+    q = 20
+    assert O.bernstein_rho(t0) >= 1.6
+    I, J = O.model_integrals_direct(t0.real, abs(t0.imag), q)
+    for k in range(q):
+        ri = _mp_model(t0.real, abs(t0.imag), k, 1)
+        rj = _mp_model(t0.real, abs(t0.imag), k, 3)
+        si = _mp_model(0.0, abs(t0.imag) + abs(t0.real), 0, 1)
+        sj = _mp_model(t0.real, abs(t0.imag), 0, 3)
+        assert abs(I[k] - ri) <= 1e-14 * max(si, 1.0), (k, I[k], ri)
+        assert abs(J[k] - rj) <= 1e-14 * max(sj, 1.0), (k, J[k], rj)
+
+
 def test_model_integral_closed_forms():
     I, J = O.model_integrals(0.0, 1.0, 8)
     assert abs(I[0] - GOLD["ssq_I0_t0_i"]["value"]) < 1e-15
@@ -66,7 +81,7 @@ def test_model_integral_closed_forms():
 
 
 def test_t0_straight_edge_closed_form():
-    """r(t) = (t, 0, 0), target (0.3, d, 0) -> t0 = 0.3 + i d."""
+    """r(t) = (t, 0, 0) (Legendre coefficient a_1 = e_x), target (0.3, d, 0) -> t0 = 0.3 + i d."""
     q = 12
     C = np.zeros((q, 3)); C[1, 0] = 1.0
     for d in (1e-12, 1e-6, 0.01, 0.3, 1.5):
@@ -80,14 +95,14 @@ def test_t0_curved_edge_is_a_root():
     t, w, U = O.tables(q)
     th = 0.4 * t
     y = np.stack([np.sin(th), 1 - np.cos(th), 0.1 * th ** 2], 1)
-    C = U @ y
+    C = np.polynomial.legendre.legfit(t, y, q - 1)      # Legendre coefficients (reading A4')
     rng = np.random.default_rng(4)
     for _ in range(20):
         tr = rng.uniform(-1.1, 1.1)
         rp = np.array([np.sin(0.4 * tr), 1 - np.cos(0.4 * tr), 0.1 * (0.4 * tr) ** 2]) + rng.normal(0, 0.05, 3)
         t0, conv = O.find_t0(C, rp)
         assert conv and t0.imag >= 0
-        x = sum(C[k] * t0 ** k for k in range(q))
+        x = np.polynomial.legendre.legval(t0, C)
         assert abs(np.sum((x - rp) ** 2)) < 1e-13
 
 
