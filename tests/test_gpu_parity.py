@@ -52,7 +52,8 @@ def _compare(vals_gpu, vo, pos, tg, n, band=None, kap=None, tag=""):
     for k in range(4):
         g = np.stack([vals_gpu[k][pp * n:(pp + 1) * n] for pp in pos]).reshape(-1)
         st = {}
-        w, ratio = U.compare_rows(g, vo[k], inv, n, REL, ABS, band, None if kap is None else kap[k], st)
+        w, ratio = U.compare_rows(g, vo[k], inv, n, REL, ABS, band, None if kap is None else kap[k], st,
+                                  U.KAPPA_REL_DP if k == 3 else U.KAPPA_REL)
         STATS[f"{tag}:{'S D Sp Dp'.split()[k]}"] = st
         worst.append(w)
     print(tag, STATS)
@@ -80,7 +81,8 @@ def test_cfg1_all_pairs(raw):
     vo, sto, kap = O.build_rows(S, *tgs, tg, pa, raw=raw, kappa=True)
     for k in range(4):
         st = {}
-        w, _ = U.compare_rows(res["vals"][k], vo[k], tg, S.n, REL, ABS, kappa=kap[k], stats=st)
+        w, _ = U.compare_rows(res["vals"][k], vo[k], tg, S.n, REL, ABS, kappa=kap[k], stats=st,
+                              kappa_rel=U.KAPPA_REL_DP if k == 3 else U.KAPPA_REL)
         print("cfg1", k, st)
         assert w <= 1.0, (k, w)
     # columns and row pointers
@@ -178,7 +180,8 @@ def test_cfg5_close_evaluation_sweep():
     print("cfg5: rows in the conditioning band:", int((band > 1).sum()), "of", T)
     for k in range(4):
         st = {}
-        w, ratio = U.compare_rows(res["vals"][k], vo[k], tg, S.n, REL, ABS, band, kap[k], st)
+        w, ratio = U.compare_rows(res["vals"][k], vo[k], tg, S.n, REL, ABS, band, kap[k], st,
+                                  U.KAPPA_REL_DP if k == 3 else U.KAPPA_REL)
         print("cfg5", k, st, "worst", w)
         assert w <= 1.0, (k, w)
 
@@ -272,12 +275,16 @@ def test_zeta_vectors_match_oracle():
     n, p = S.n, S.p
     npb = p * (p + 1) // 2
     worst = 0.0
-    for k in rng.choice(perm, 150, replace=False):
+    sample = rng.choice(np.sort(perm), 150, replace=False)
+    band = _band_for_pairs(S, tgs[0], tgt[sample], pat[sample])
+    for k, bnd in zip(sample, band):
         t, P = tgt[k], pat[k]
         sl = int(tgs[2][t] % n) if tgs[2][t] >= 0 and tgs[2][t] // n == P else -1
         d = O.pair_debug(S, P, tgs[0][t], tgs[1][t], self_local=sl, side=int(tgs[3][t]))
         W, dW, Th = d["W"], d["dW"], d["Theta"]
-        for a, b, ref in [(0, npb, Th), (npb, 5 * npb, np.concatenate([W[:, 0], -W[:, 1], -W[:, 2], -W[:, 3]])),
-                          (5 * npb, 9 * npb, np.concatenate([dW[:, 0], -dW[:, 1], -dW[:, 2], -dW[:, 3]]))]:
-            worst = max(worst, np.abs(Z[inv[k]][a:b] - ref).max() / (U.KAPPA_REL * np.abs(ref).max()))
+        for a, b, ref, rel in [(0, npb, Th, U.KAPPA_REL),
+                               (npb, 5 * npb, np.concatenate([W[:, 0], -W[:, 1], -W[:, 2], -W[:, 3]]), U.KAPPA_REL),
+                               (5 * npb, 9 * npb, np.concatenate([dW[:, 0], -dW[:, 1], -dW[:, 2], -dW[:, 3]]),
+                                U.KAPPA_REL_DP)]:
+            worst = max(worst, np.abs(Z[inv[k]][a:b] - ref).max() / (rel * bnd * np.abs(ref).max()))
     assert worst <= 1.0, worst
