@@ -144,12 +144,13 @@ int64_t rrq_launch_count(rrq_ctx ctx);
 
 /* Device-time accounting.  When enabled, every launch of the build is bracketed by CUDA events
  * recorded on the caller's stream; rrq_get_timing returns the accumulated milliseconds and launch
- * counts per stage: [0] near list, [1] patch fit (geometry, edge tables, QR), [2] k_pair_zeta
- * (Steps 4-7), [3] k_contract (Step 8 + smooth subtraction + store), [4] build plumbing (pair
- * permutation, work items).  stats[0] = pairs built, stats[1] = swap-regime edges (reading A5).
- * The accumulators are host-side; the build synchronises the stream before reading the events. */
+ * counts per stage: [0] near list, [1] patch fit (geometry, edge tables, QR), [2] k_pair_edge
+ * (Steps 4-5, scalar line integrals, I[gamma]), [3] k_qmap (Step 6 line-integral maps, DMMA GEMM),
+ * [4] k_translate (Step 7), [5] k_contract (Step 8 DMMA GEMMs + smooth subtraction + store),
+ * [6] build plumbing (pair permutation, work items).  stats[0] = pairs built, stats[1] = swap-regime
+ * edges (reading A5).  The build synchronises the stream before the events are read. */
 rrq_status rrq_set_timing(rrq_ctx ctx, int enable);
-rrq_status rrq_get_timing(rrq_ctx ctx, double ms[5], int64_t launches[5], int64_t stats[2]);
+rrq_status rrq_get_timing(rrq_ctx ctx, double ms[7], int64_t launches[7], int64_t stats[2]);
 rrq_status rrq_reset_timing(rrq_ctx ctx);
 
 /* Test hook: copy the internal per-pair contraction vectors of the LAST build sub-chunk to HOST

@@ -1,13 +1,16 @@
-// The per-pair hot path: Steps 4-7 -> contraction vector Z, then Step 8 in matrix
-// mode + smooth-rule subtraction (reading A14) -> CSR weights.
+// The per-pair hot path, Steps 4-8 + smooth-rule subtraction (A14), as
+// four kernels over a sub-chunk of pairs in patch-major order (s = position in the permutation):
 //
-// k_pair_zeta: one warp per (target, patch) pair, pairs visited patch-major so a CTA's warps share
-//   one patch's edge tables in L1/L2.  Lanes split: the R_l^m columns (m), the harmonic derivative
-//   table, the 9 (edge, component) polynomial evaluations of the complex Newton solve, the 3p~ edge
-//   nodes (weights, Omega, dOmega), the 2 n_Omega sinh-rule nodes, the 2 NQ + NV line-integral maps
-//   Q, dQ, V, and the NP translations.
-// k_contract: per patch, a CTA contracts TILE pairs' Z rows with the patch's fit operators
-//   (register-blocked over pairs), subtracts the smooth rule and stores n contiguous fp64 per pair.
+// k_pair_edge (warp per pair): target frame, harmonics at the target (Step 4), per-edge Newton /
+//   regime / model integrals / SSQ weights (Step 5), the GEMM rows a = omega1 d and
+//   b = omega1 nu' - omega3 (nu'.d) d, the scalar line integrals Omega, Omega_0 and derivatives
+//   (Step 6), and the I[gamma] part of W, dW and the S(r') Omega_0 part of Theta (Step 7).
+// k_qmap (CTA per tile of 32 pairs of one patch): the line-integral maps [Q | V](pair) = a M,
+//   dQ(pair) = b M_Q as one FP64 tensor-core GEMM (mma.sync m8n8k4 f64 = DMMA) against the patch's
+//   operand M (built in k_edge_tables).
+// k_translate (warp per pair): translation (Step 7) -> W, dW, Theta -> contraction vectors zeta.
+// k_contract (CTA per tile of 32 pairs of one patch): Step 8 in matrix mode as DMMA GEMMs
+//   zeta^T [P_D | P_Sp | P_Sd | P_Sg], then smooth subtraction, scaling and the CSR store.
 #pragma once
 #include "rrq_device.cuh"
 
@@ -32,7 +35,7 @@ __device__ __forceinline__ double bernstein_rho(double re, double im) {
 
 // Model integrals I_k, J_k (reading A11): upward recurrences, cancellation-free I_0, J_0.
 template <int Q>
-__device__ void model_integrals(double a, double b, double *I, double *J) {
+__device__ __noinline__ void model_integrals(double a, double b, double *I, double *J) {
   double Q1 = (1 - a) * (1 - a) + b * b, Qm = (1 + a) * (1 + a) + b * b;
   double s1 = sqrt(Q1), sm = sqrt(Qm);
   if (fabs(a) <= 1.0) {
@@ -58,36 +61,51 @@ __device__ void model_integrals(double a, double b, double *I, double *J) {
   }
 }
 
+// Per-pair row of k_pair_edge's output for k_translate (doubles): S^{(l,m)}(r') and nu'.grad S for
+// m >= 0 (complex), the I[gamma] parts of W and dW ([4][NP], zeta sign convention NOT applied), the
+// S(r') Omega_0 part of Theta ([NP]), and nu' in the patch frame.
 template <int P>
-struct WarpScratch {
+struct XRow {
+  using D = Dims<P>;
+  static constexpr int R = 0, NG = 2 * D::NS, W = 4 * D::NS, DW = W + 4 * D::NP, TH = DW + 4 * D::NP,
+                       NU = TH + D::NP, STRIDE = (NU + 3 + 1) / 2 * 2;
+};
+// Per-pair row of k_qmap's output: [Q (8 NQ) | dQ (8 NQ) | V (2 NV)] in the column convention of M.
+template <int P>
+struct QRow {
+  using D = Dims<P>;
+  static constexpr int Q = 0, DQ = D::NCQ, V = 2 * D::NCQ, STRIDE = (2 * D::NCQ + 2 * D::NV + 1) / 2 * 2;
+};
+
+template <int P>
+struct EdgeScratch {
   using D = Dims<P>;
   cd R[D::NS];        // R_l^m at (y', z', x'): S^{(l,m)}(r') for m >= 0
   cd GS[D::NS][3];    // grad S^{(l,m)}(r')
-  cd NG[D::NS];       // nu' . grad S^{(l,m)}(r')
   cd HN[D::NS][3];    // Hess S^{(l,m)}(r') nu'
-  double a[D::E][3];  // omega1_k d_k
-  double b[D::E][3];  // omega1_k nu' - omega3_k (nu'.d_k) d_k
   double I[3][D::Q], J[3][D::Q];
-  double Qv[D::NQ][8], dQ[D::NQ][8], V[D::NV][2];
   double t0[3][2];
-  double Om[4], dOm[4];   // (Omega_0, Omega), (dOmega_0, dOmega)
   double r13[2][kNDirect];
   int swap[3], conv[3], direct[3];
 };
 
-struct SmemTables {
-  int q, n_omega;
-};
+// D = A B + C for one 8x8x4 fp64 tile (FP64 tensor core, SASS DMMA).  Fragments: a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], c/d = C[lane/4][2 (lane%4) + {0,1}].
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 
 // Legendre-series edge interpolant (reading A4'): value and derivatives of component c at t, by
 // Bonnet's recurrence and P'_{j+1} = P'_{j-1} + (2j+1) P_j, P''_{j+1} = P''_{j-1} + (2j+1) P'_j.
 template <int Q>
-__device__ __forceinline__ void leg_r(const double *C, int c, double t, double &v, double &d1, double &d2) {
+__device__ __noinline__ void leg_r(const double *C, int c, double t, double &v, double &d1, double &d2) {
   double P0 = 1, P1 = t, a0 = 0, a1 = 1, b0 = 0, b1 = 0;
   v = C[c] + C[3 + c] * t;
   d1 = C[3 + c];
   d2 = 0;
-#pragma unroll
+#pragma unroll 2
   for (int j = 1; j + 1 < Q; ++j) {
     double P2 = ((2 * j + 1) * t * P1 - j * P0) * (1.0 / (j + 1));
     double a2 = a0 + (2 * j + 1) * P1, b2 = b0 + (2 * j + 1) * a1;
@@ -99,11 +117,11 @@ __device__ __forceinline__ void leg_r(const double *C, int c, double t, double &
   }
 }
 template <int Q>
-__device__ __forceinline__ void leg_c(const double *C, int c, cd t, cd &v, cd &d1) {
+__device__ __noinline__ void leg_c(const double *C, int c, cd t, cd &v, cd &d1) {
   cd P0 = mk(1, 0), P1 = t, a0 = mk(0, 0), a1 = mk(1, 0);
   v = mk(C[c], 0) + C[3 + c] * t;
   d1 = mk(C[3 + c], 0);
-#pragma unroll
+#pragma unroll 2
   for (int j = 1; j + 1 < Q; ++j) {
     cd P2 = (1.0 / (j + 1)) * ((2.0 * j + 1) * (t * P1) - (double)j * P0);
     cd a2 = a0 + (2.0 * j + 1) * P1;
@@ -115,10 +133,10 @@ __device__ __forceinline__ void leg_c(const double *C, int c, cd t, cd &v, cd &d
 }
 // x(t), x'(t) (3 components, real t)
 template <int Q>
-__device__ __forceinline__ void leg_r3(const double *C, double t, double x[3], double dx[3]) {
+__device__ __noinline__ void leg_r3(const double *C, double t, double x[3], double dx[3]) {
   double P0 = 1, P1 = t, a0 = 0, a1 = 1;
   for (int c = 0; c < 3; ++c) { x[c] = C[c] + C[3 + c] * t; dx[c] = C[3 + c]; }
-#pragma unroll
+#pragma unroll 2
   for (int j = 1; j + 1 < Q; ++j) {
     double P2 = ((2 * j + 1) * t * P1 - j * P0) * (1.0 / (j + 1));
     double a2 = a0 + (2 * j + 1) * P1;
@@ -140,14 +158,16 @@ __device__ __forceinline__ double tri_sum(double v, int base) {
 
 template <int P, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
-    k_pair_zeta(int64_t npairs, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt, int64_t kbase,
-                const int32_t *__restrict__ pair_patch, const double *__restrict__ fit, const double *__restrict__ tx,
-                const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
-                const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Z,
-                int32_t *__restrict__ pstat, unsigned long long *__restrict__ swapcnt) {
+    k_pair_edge(int64_t sA, int64_t sB, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt,
+                int64_t kbase, const int32_t *__restrict__ pair_patch, const double *__restrict__ fit,
+                const double *__restrict__ tx, const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
+                const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Arow,
+                double *__restrict__ Xrow, int32_t *__restrict__ pstat, int64_t obase,
+                unsigned long long *__restrict__ swapcnt) {
   using D = Dims<P>;
   using L = Layout<P>;
-  constexpr int Q = D::Q, E = D::E, NP = D::NP, NQ = D::NQ, NV = D::NV, NS = D::NS, NZ = D::NZ;
+  using XR = XRow<P>;
+  constexpr int Q = D::Q, E = D::E, NP = D::NP, NS = D::NS, K = D::K;
   extern __shared__ double smem[];
   double *sU = smem;                  // [Q][Q]
   double *stgl = sU + Q * Q, *swgl = stgl + Q;
@@ -155,9 +175,11 @@ __global__ void __launch_bounds__(WPB * 32)
   double *ssqb = swo + n_omega;       // [(2P+1)][(2P+1)] sqrt binomials
   double *sfac = ssqb + (2 * P + 1) * (2 * P + 1);  // [2P+2] factorials
   constexpr int SQ = 2 * P + 1;
-  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + SQ * SQ + (2 * P + 2);
+  double *shc = sfac + (2 * P + 2);   // [HC_SIZE]
+  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + SQ * SQ + (2 * P + 2) + HC_SIZE;
   tab_doubles = (tab_doubles + 1) & ~1;
-  WarpScratch<P> *wsall = reinterpret_cast<WarpScratch<P> *>(smem + tab_doubles);
+  EdgeScratch<P> *wsall = reinterpret_cast<EdgeScratch<P> *>(smem + tab_doubles);
+  for (int i = threadIdx.x; i < HC_SIZE; i += blockDim.x) shc[i] = T.hc[i];
   for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) sU[i] = T.U[i];
   for (int i = threadIdx.x; i < Q; i += blockDim.x) { stgl[i] = T.tgl[i]; swgl[i] = T.wgl[i]; }
   for (int i = threadIdx.x; i < n_omega; i += blockDim.x) { sxo[i] = T.xo[i]; swo[i] = T.wo[i]; }
@@ -169,18 +191,33 @@ __global__ void __launch_bounds__(WPB * 32)
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpScratch<P> &ws = wsall[warp];
+  EdgeScratch<P> &ws = wsall[warp];
+  (void)ssqb; (void)sfac;
   const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
   unsigned long long nswap = 0;
 
-  for (int64_t s = (int64_t)blockIdx.x * WPB + warp; s < npairs; s += (int64_t)gridDim.x * WPB) {
-    const int64_t k = perm[s];
-    const int64_t t = ptgt[k - kbase];
-    const int Pp = pair_patch[k];
-    const double *blk = fit + (int64_t)Pp * L::STRIDE;
+  // Phase-synchronous rounds: each warp takes one pair per round and all warps of the CTA step through
+  // the phases together (__syncthreads between phases), so the SM's instruction working set is one
+  // phase rather than the whole kernel (v1 was bound by instruction fetch, ncu "no instruction").
+  for (int64_t base = sA + (int64_t)blockIdx.x * WPB; base < sB; base += (int64_t)gridDim.x * WPB) {
+    const int64_t s = base + warp;
+    const bool active = s < sB;
+    int64_t k = 0, t = 0;
+    int Pp = 0;
+    double *X = Xrow, *Ar = Arow;
+    const double *blk = fit, *hd = fit;
+    double rp[3] = {0, 0, 0}, nup[3] = {0, 0, 0}, u[3] = {0, 0, 0};
+    int self_local = -1;
+    double om[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // Omega_0 Omega[3] dOmega_0 dOmega[3]
+    if (active) {
+    k = perm[s];
+    t = ptgt[k - kbase];
+    X = Xrow + (s - sA) * XR::STRIDE;
+    Ar = Arow + (s - sA) * 2 * K;
+    Pp = pair_patch[k];
+    blk = fit + (int64_t)Pp * L::STRIDE;
     // ---------------- target in the patch frame (reading A2)
-    const double *hd = blk + L::HDR;
-    double rp[3], nup[3] = {0, 0, 0};
+    hd = blk + L::HDR;
     {
       double invh = 1.0 / hd[H_H];
       double d[3] = {tx[3 * t] - hd[H_O], tx[3 * t + 1] - hd[H_O + 1], tx[3 * t + 2] - hd[H_O + 2]};
@@ -190,7 +227,6 @@ __global__ void __launch_bounds__(WPB * 32)
         for (int r = 0; r < 3; ++r) nup[r] = hd[H_RM + 3 * r] * nn[0] + hd[H_RM + 3 * r + 1] * nn[1] + hd[H_RM + 3 * r + 2] * nn[2];
       }
     }
-    int self_local = -1;
     if (self_node) {
       int64_t sn = self_node[t];
       if (sn >= 0 && sn / D::N == Pp) self_local = (int)(sn % D::N);
@@ -214,25 +250,36 @@ __global__ void __launch_bounds__(WPB * 32)
         else sg = (z - 0.5 * (zlo + zhi) > 0) ? 1.0 : -1.0;
       }
     }
-    const double u[3] = {0.0, 0.0, sg};
+    u[2] = sg;
 
     // ---------------- Step 4: harmonics at the target
-    if (lane <= P) r_column<P>(rp[1], rp[2], rp[0], lane, ws.R);
+    if (lane <= P) r_column<P>(rp[1], rp[2], rp[0], lane, ws.R, shc);
     __syncwarp();
     for (int e = lane; e < NS; e += 32) {
       int l = 0;
       while (sidx(l + 1, 0) <= e) ++l;
-      int m = e - sidx(l, 0);
+      const int m = e - sidx(l, 0);
       cd g[3];
-      gradS(ws.R, l, m, g);
+      grad_fast(ws.R, l, m, shc, g);
       cd ng = mk(0, 0);
       for (int a = 0; a < 3; ++a) { ws.GS[e][a] = g[a]; ng = ng + nup[a] * g[a]; }
-      ws.NG[e] = ng;
-      cd hn[3];
-      hessS_v(ws.R, l, m, nup, hn);
-      for (int a = 0; a < 3; ++a) ws.HN[e][a] = hn[a];
+      X[XR::R + 2 * e] = ws.R[e].x;
+      X[XR::R + 2 * e + 1] = ws.R[e].y;
+      X[XR::NG + 2 * e] = ng.x;
+      X[XR::NG + 2 * e + 1] = ng.y;
     }
+    __syncwarp();
+    for (int e = lane; e < NS; e += 32) {   // Hess S nu' for m >= 1 (needed by d I[gamma])
+      int l = 0;
+      while (sidx(l + 1, 0) <= e) ++l;
+      const int m = e - sidx(l, 0);
+      if (m >= 1) hess_fast(ws.GS, l, m, nup, shc, ws.HN[e]);
+    }
+    if (lane < 3) X[XR::NU + lane] = nup[lane];
 
+    }
+    __syncthreads();
+    if (active) {
     // ---------------- Step 5: t0 per edge (reading A12), lanes (e, c) = (lane/3, lane%3)
     {
       const int e = lane < 9 ? lane / 3 : 2, c = lane < 9 ? lane % 3 : 2, base = 3 * e;
@@ -312,8 +359,10 @@ __global__ void __launch_bounds__(WPB * 32)
     }
     __syncwarp();
 
+    }
+    __syncthreads();
+    if (active) {
     // ---------------- weights and the scalar line integrals (Step 6)
-    double om[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // Omega_0(plain) Omega[3] dOmega_0 dOmega[3]
     for (int kap = lane; kap < E; kap += 32) {
       const int e = kap / Q, kk = kap % Q;
       const double *y = blk + L::YL + 3 * kap, *tau = blk + L::TL + 3 * kap;
@@ -341,14 +390,17 @@ __global__ void __launch_bounds__(WPB * 32)
       double txd[3];
       cross3(tau, d, txd);
       for (int a = 0; a < 3; ++a) {
-        ws.a[kap][a] = w1 * d[a];
-        ws.b[kap][a] = w1 * nup[a] - w3 * nd * d[a];
+        Ar[3 * kap + a] = w1 * d[a];                       // GEMM row a (k = 3 kappa + axis)
+        Ar[K + 3 * kap + a] = w1 * nup[a] - w3 * nd * d[a]; // GEMM row b
         om[1 + a] -= w1 * tau[a];
         om[5 + a] += w3 * nd * tau[a];
       }
       om[4] += w3 * dot3(nup, txd);
     }
     for (int i = 0; i < 8; ++i) om[i] = warp_sum(om[i]);
+    }
+    __syncthreads();
+    if (active) {
     // Omega_0 on swap edges: sinh-split Gauss-Legendre on the interpolated edge (reading A9)
     for (int e = 0; e < 3; ++e) {
       if (!ws.swap[e]) continue;
@@ -374,80 +426,231 @@ __global__ void __launch_bounds__(WPB * 32)
     if (self_local >= 0) om[0] -= 2.0 * kPi;   // principal value (reading A7)
     __syncwarp();
 
-    // ---------------- line-integral maps Q, dQ, V (Step 6)
-    const double *GT = blk + L::GT, *ET = blk + L::ET;
-    for (int task = lane; task < 2 * NQ + NV; task += 32) {
-      if (task < 2 * NQ) {
-        const int jk = task < NQ ? task : task - NQ;
-        const double(*av)[3] = task < NQ ? ws.a : ws.b;
-        double s0r = 0, s0i = 0, vr[3] = {0, 0, 0}, vi[3] = {0, 0, 0};
-        for (int kap = 0; kap < E; ++kap) {
-          const double *g = GT + (int64_t)kap * 6 * NQ + jk;
-          double gr[3] = {__ldg(g), __ldg(g + 2 * NQ), __ldg(g + 4 * NQ)};
-          double gi[3] = {__ldg(g + NQ), __ldg(g + 3 * NQ), __ldg(g + 5 * NQ)};
-          double a0 = av[kap][0], a1 = av[kap][1], a2 = av[kap][2];
-          s0r -= a0 * gr[0] + a1 * gr[1] + a2 * gr[2];
-          s0i -= a0 * gi[0] + a1 * gi[1] + a2 * gi[2];
-          vr[0] += a1 * gr[2] - a2 * gr[1];
-          vr[1] += a2 * gr[0] - a0 * gr[2];
-          vr[2] += a0 * gr[1] - a1 * gr[0];
-          vi[0] += a1 * gi[2] - a2 * gi[1];
-          vi[1] += a2 * gi[0] - a0 * gi[2];
-          vi[2] += a0 * gi[1] - a1 * gi[0];
-        }
-        double *o = task < NQ ? ws.Qv[jk] : ws.dQ[jk];
-        o[0] = s0r; o[1] = s0i;
-        for (int a = 0; a < 3; ++a) { o[2 + 2 * a] = vr[a]; o[3 + 2 * a] = vi[a]; }
-      } else {
-        const int jk = task - 2 * NQ;
-        double sr = 0, si = 0;
-        for (int kap = 0; kap < E; ++kap) {
-          const double *g = ET + (int64_t)kap * 6 * NV + jk;
-          for (int a = 0; a < 3; ++a) {
-            sr += ws.a[kap][a] * __ldg(g + 2 * a * NV);
-            si += ws.a[kap][a] * __ldg(g + (2 * a + 1) * NV);
-          }
-        }
-        ws.V[jk][0] = sr;
-        ws.V[jk][1] = si;
-      }
     }
-    __syncwarp();
-
-    // ---------------- Step 7: translation
-    double *Zr = Z + s * NZ;
+    __syncthreads();
+    if (active) {
+    // ---------------- I[gamma]: (Omega_0, Omega)(0, grad S^{(l,m)}(r')), omega
+    // first; its derivative.  W_gamma = -sqrt2 Im I[gamma], and the S(r') Omega_0 part of
+    // Theta (G2); k_translate adds the lambda_1 / theta_1 parts.
     for (int c = lane; c < NP; c += 32) {
       int l = 1;
       while (lmidx(l + 1, 1) <= c) ++l;
-      int m = c - lmidx(l, 1) + 1;
+      const int m = c - lmidx(l, 1) + 1, hs = sidx(l, m);
+      const cd *g = ws.GS[hs], *hn = ws.HN[hs];
+      const double O0 = om[0], Ov[3] = {om[1], om[2], om[3]}, dO0 = om[4], dOv[3] = {om[5], om[6], om[7]};
+      double gs = 0, dgs = 0, gv[3], dgv[3];
+      for (int a = 0; a < 3; ++a) {
+        gs -= Ov[a] * g[a].y;
+        dgs -= dOv[a] * g[a].y + Ov[a] * hn[a].y;
+        const int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
+        gv[a] = O0 * g[a].y + (Ov[b1] * g[b2].y - Ov[b2] * g[b1].y);
+        dgv[a] = dO0 * g[a].y + (dOv[b1] * g[b2].y - dOv[b2] * g[b1].y) + O0 * hn[a].y +
+                 (Ov[b1] * hn[b2].y - Ov[b2] * hn[b1].y);
+      }
+      const double f = -s2 * inv4pi;
+      X[XR::W + c] = f * gs;
+      X[XR::DW + c] = f * dgs;
+      for (int a = 0; a < 3; ++a) {
+        X[XR::W + (1 + a) * NP + c] = f * gv[a];
+        X[XR::DW + (1 + a) * NP + c] = f * dgv[a];
+      }
+      X[XR::TH + c] = s2 * inv4pi * ws.R[hs].y * O0;
+    }
+    if (lane == 0 && pstat) pstat[k - obase] = (ws.conv[0] && ws.conv[1] && ws.conv[2]) ? 0 : 1;
+    nswap += ws.swap[0] + ws.swap[1] + ws.swap[2];
+    }
+    __syncthreads();
+  }
+  if (swapcnt && lane == 0 && nswap) atomicAdd(swapcnt, nswap);
+}
+
+
+// ------------------------------------------------------------------------------------------------
+// k_qmap: line-integral maps (Step 6) as a DMMA GEMM per tile of TP pairs
+// of one patch: rows [a(pairs) ; b(pairs)] x M (k_edge_tables).  Warp w owns M-tile (w % MT) and every
+// (W / MT)-th N-tile; the b-row M-tiles skip the V columns.  A tile staged in shared memory (row stride
+// == 4 mod 16 doubles: conflict-free fragments); B fragments straight from the patch operand (L1/L2).
+// ------------------------------------------------------------------------------------------------
+template <int P>
+struct QmapCfg {
+  using D = Dims<P>;
+  static constexpr int TP = P >= 10 ? 16 : 32, ROWS = 2 * TP, MT = ROWS / 8, WARPS = 16, NSPLIT = WARPS / MT;
+  static constexpr int KA = (D::K % 16 == 4) ? D::K : D::K + ((4 - D::K % 16) + 16) % 16;
+  static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8;
+  static constexpr int NTW = (NTALL + NSPLIT - 1) / NSPLIT;   // max N-tiles per warp
+  static constexpr size_t SMEM = (size_t)ROWS * KA * sizeof(double);
+};
+
+template <int P>
+__global__ void __launch_bounds__(512, 1)
+    k_qmap(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, int64_t n_patches,
+           const int64_t *__restrict__ seg_ptr, int64_t sA, const double *__restrict__ fit,
+           const double *__restrict__ Arow, double *__restrict__ Qrow) {
+  using D = Dims<P>;
+  using L = Layout<P>;
+  using C = QmapCfg<P>;
+  using QR = QRow<P>;
+  constexpr int K = D::K, KA = C::KA, TP = C::TP, NCS = D::NCS;
+  extern __shared__ double sA_[];
+  const int64_t item = item0 + blockIdx.x;
+  if (item >= item1) return;
+  int64_t lo = 0, hi = n_patches;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (item_ptr[mid] <= item) lo = mid; else hi = mid;
+  }
+  const int64_t Pp = lo;
+  const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
+  const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
+  // stage A: row r < TP -> a-row of pair s0 + r; row TP + r -> b-row
+  for (int i = threadIdx.x; i < C::ROWS * K; i += blockDim.x) {
+    const int r = i / K, k = i % K, pr = r % TP, ab = r / TP;
+    sA_[r * KA + k] = pr < cnt ? Arow[(s0 + pr - sA) * 2 * K + ab * K + k] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int mt = warp % C::MT, ns = warp / C::MT;
+  const bool brows = mt >= C::MT / 2;
+  const int ntiles = brows ? C::NTQ : C::NTALL;
+  const double *M = fit + Pp * (int64_t)L::STRIDE + L::MQ;
+  double acc[C::NTW][2];
+#pragma unroll
+  for (int t = 0; t < C::NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const double *arow = sA_ + (mt * 8 + (lane >> 2)) * KA + (lane & 3);
+  const double *bcol = M + (int64_t)(lane & 3) * NCS + (lane >> 2);
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    const double a = arow[k0];
+    const double *bk = bcol + (int64_t)k0 * NCS;
+#pragma unroll
+    for (int t = 0; t < C::NTW; ++t) {
+      const int nt = ns + t * C::NSPLIT;
+      if (nt < ntiles) dmma(acc[t][0], acc[t][1], a, __ldg(bk + nt * 8));
+    }
+  }
+  // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]
+  const int row = mt * 8 + (lane >> 2), pr = row % TP;
+  if (pr < cnt) {
+    double *out = Qrow + (s0 + pr - sA) * QR::STRIDE;
+#pragma unroll
+    for (int t = 0; t < C::NTW; ++t) {
+      const int nt = ns + t * C::NSPLIT;
+      if (nt >= ntiles) continue;
+      const int col = nt * 8 + 2 * (lane & 3);
+      if (!brows) {
+        if (col < D::NCQ) {
+          out[QR::Q + col] = acc[t][0];
+          out[QR::Q + col + 1] = acc[t][1];
+        } else if (col - D::NCQ < 2 * D::NV) {
+          out[QR::V + col - D::NCQ] = acc[t][0];
+          if (col + 1 - D::NCQ < 2 * D::NV) out[QR::V + col + 1 - D::NCQ] = acc[t][1];
+        }
+      } else {
+        out[QR::DQ + col] = acc[t][0];
+        out[QR::DQ + col + 1] = acc[t][1];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_translate: Step 7 (P:L1263-1268 eq cdlp1dintegral): for each (l,m),
+// lambda_1, its nu'-derivative and theta_1 from Q^{(j,k)}, dQ^{(j,k)}, V^{(j,k)} and S(r'), plus the
+// gamma parts from k_pair_edge -> W, dW, Theta -> zeta = (Theta, zeta(W), zeta(dW), zeta_S).
+// One warp per pair; the pair's rows are staged in shared memory; lanes take (l,m) in a cost-balanced
+// order (heaviest first, the lightest four doubled up).
+// ------------------------------------------------------------------------------------------------
+template <int P>
+struct TransCfg {
+  using D = Dims<P>;
+  static constexpr int WPB = 8;
+  static constexpr int PER_WARP = XRow<P>::STRIDE + QRow<P>::STRIDE;
+};
+
+template <int P>
+__global__ void __launch_bounds__(256)
+    k_translate(int64_t sA, int64_t sB, const double *__restrict__ Xrow, const double *__restrict__ Qrow,
+                const double *__restrict__ sqb_g, double *__restrict__ Zrow) {
+  using D = Dims<P>;
+  using XR = XRow<P>;
+  using QR = QRow<P>;
+  constexpr int NP = D::NP, NZS = D::NZS, SQ = 2 * P + 1, WPB = TransCfg<P>::WPB;
+  extern __shared__ double sm[];
+  double *ssqb = sm;                         // [SQ][SQ]
+  double *sfac = ssqb + SQ * SQ;             // [2P+2]
+  int *order = reinterpret_cast<int *>(sfac + 2 * P + 2);   // [NP] cost-balanced task order
+  double *wsb = sfac + 2 * P + 2 + (NP + 1) / 2 + 1;
+  for (int i = threadIdx.x; i < SQ * SQ; i += blockDim.x) ssqb[i] = sqb_g[(i / SQ) * 41 + (i % SQ)];
+  if (threadIdx.x == 0) {
+    double f = 1;
+    sfac[0] = 1;
+    for (int i = 1; i < 2 * P + 2; ++i) { f *= i; sfac[i] = f; }
+    // cost of (l,m) ~ number of (j,k) terms; sort descending (selection sort, NP <= 55)
+    int cost[64];
+    for (int c = 0; c < NP; ++c) {
+      int l = 1;
+      while (lmidx(l + 1, 1) <= c) ++l;
+      const int m = c - lmidx(l, 1) + 1;
+      int n = 0;
+      for (int j = 1; j <= l; ++j) n += min(j, m + l - j) - max(-j, m - (l - j)) + 1;
+      cost[c] = n;
+      order[c] = c;
+    }
+    for (int i = 0; i < NP; ++i)
+      for (int j = i + 1; j < NP; ++j)
+        if (cost[order[j]] > cost[order[i]]) { int t = order[i]; order[i] = order[j]; order[j] = t; }
+    // tasks beyond 32 go to the lanes holding the lightest of the first 32 (reverse them)
+    if (NP > 32) {
+      int extra = NP - 32;
+      for (int i = 0; i < extra / 2; ++i) { int t = order[32 + i]; order[32 + i] = order[NP - 1 - i]; order[NP - 1 - i] = t; }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double *X = wsb + warp * TransCfg<P>::PER_WARP;
+  double *Qv = X + XR::STRIDE;
+  const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
+  for (int64_t s = sA + (int64_t)blockIdx.x * WPB + warp; s < sB; s += (int64_t)gridDim.x * WPB) {
+    const double *xg = Xrow + (s - sA) * XR::STRIDE, *qg = Qrow + (s - sA) * QR::STRIDE;
+    for (int i = lane; i < XR::STRIDE; i += 32) X[i] = xg[i];
+    for (int i = lane; i < QR::STRIDE; i += 32) Qv[i] = qg[i];
+    __syncwarp();
+    const cd *Rt = reinterpret_cast<const cd *>(X + XR::R), *NGt = reinterpret_cast<const cd *>(X + XR::NG);
+    const double nup[3] = {X[XR::NU], X[XR::NU + 1], X[XR::NU + 2]};
+    double *Z = Zrow + (s - sA) * NZS;
+    for (int ti = lane; ti < NP; ti += 32) {
+      const int c = order[ti];
+      int l = 1;
+      while (lmidx(l + 1, 1) <= c) ++l;
+      const int m = c - lmidx(l, 1) + 1;
       cq lam = qzero(), dlam = qzero();
       cd th = mk(0, 0);
       for (int j = 1; j <= l; ++j) {
         const int lj = l - j;
         const int kmin = max(-j, m - lj), kmax = min(j, m + lj);
+        const double Dj = sfac[j - 1] * sfac[lj] / sfac[l];
+        const double Cj = j >= 2 ? sfac[j - 2] * sfac[lj] / sfac[l - 1] : 0.0;
         for (int kk = kmin; kk <= kmax; ++kk) {
           const double Tc = ssqb[(l + m) * SQ + (j + kk)] * ssqb[(l - m) * SQ + (j - kk)];
           const int mk_ = m - kk;
-          cd Sv = rget(ws.R, lj, mk_);
+          const cd Sv = rget(Rt, lj, mk_);
           cd NGv;
-          if (mk_ >= 0) NGv = ws.NG[sidx(lj, mk_)];
-          else NGv = (((-mk_) & 1) ? -1.0 : 1.0) * conj(ws.NG[sidx(lj, -mk_)]);
+          if (mk_ >= 0) NGv = NGt[sidx(lj, mk_)];
+          else NGv = (((-mk_) & 1) ? -1.0 : 1.0) * conj(NGt[sidx(lj, -mk_)]);
           const int ak = kk < 0 ? -kk : kk;
           const double sgn = (kk < 0 && (ak & 1)) ? -1.0 : 1.0;
-          const bool cj = kk < 0;
-          {  // theta_1 (j >= 1): D_{j,l} T V^{(j,k)} S^{(l-j,m-k)}
-            const double *vv = ws.V[vidx(j, ak)];
-            cd Vv = mk(sgn * vv[0], sgn * (cj ? -vv[1] : vv[1]));
-            double Dj = sfac[j - 1] * sfac[lj] / sfac[l];
-            cfma(th, (Dj * Tc) * Vv, Sv);
+          const double cjs = kk < 0 ? -sgn : sgn;   // sign applied to the imaginary part
+          {  // theta_1: D_{j,l} T V^{(j,k)} S^{(l-j,m-k)}
+            const double *vv = Qv + QR::V + 2 * vidx(j, ak);
+            cfma(th, (Dj * Tc) * mk(sgn * vv[0], cjs * vv[1]), Sv);
           }
           if (j >= 2) {
-            const double cT = sfac[j - 2] * sfac[lj] / sfac[l - 1] * Tc;
-            const double *qv = ws.Qv[qidx(j, ak)], *dq = ws.dQ[qidx(j, ak)];
-            cd cS = cT * Sv, cN = cT * NGv;
+            const double cT = Cj * Tc;
+            const double *qv = Qv + QR::Q + 8 * qidx(j, ak), *dq = Qv + QR::DQ + 8 * qidx(j, ak);
+            const cd cS = cT * Sv, cN = cT * NGv;
+#pragma unroll
             for (int b = 0; b < 4; ++b) {
-              cd qb = mk(sgn * qv[2 * b], sgn * (cj ? -qv[2 * b + 1] : qv[2 * b + 1]));
-              cd dqb = mk(sgn * dq[2 * b], sgn * (cj ? -dq[2 * b + 1] : dq[2 * b + 1]));
+              const cd qb = mk(sgn * qv[2 * b], cjs * qv[2 * b + 1]);
+              const cd dqb = mk(sgn * dq[2 * b], cjs * dq[2 * b + 1]);
               cd &L1 = b == 0 ? lam.s : lam.v[b - 1];
               cd &L2 = b == 0 ? dlam.s : dlam.v[b - 1];
               cfma(L1, qb, cS);
@@ -457,170 +660,165 @@ __global__ void __launch_bounds__(WPB * 32)
           }
         }
       }
-      // I[gamma]: (Omega_0, Omega)(0, grad S^{(l,m)}(r')), omega first
-      const int hs = sidx(l, m);
-      const cd *g = ws.GS[hs], *hn = ws.HN[hs];
-      const double O0 = om[0], Ov[3] = {om[1], om[2], om[3]}, dO0 = om[4], dOv[3] = {om[5], om[6], om[7]};
-      cd gs = mk(0, 0), dgs = mk(0, 0), gv[3], dgv[3];
-      for (int a = 0; a < 3; ++a) {
-        gs = gs - Ov[a] * g[a];
-        dgs = dgs - dOv[a] * g[a] - Ov[a] * hn[a];
-        int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
-        gv[a] = O0 * g[a] + (Ov[b1] * g[b2] - Ov[b2] * g[b1]);
-        dgv[a] = dO0 * g[a] + (dOv[b1] * g[b2] - dOv[b2] * g[b1]) + O0 * hn[a] + (Ov[b1] * hn[b2] - Ov[b2] * hn[b1]);
-      }
-      // W = -sqrt2 Im(I[lambda_1] + I[gamma]), dW likewise, Theta = sqrt2 Im I[theta_1] (G2)
+      const double f = -s2 * inv4pi;
       double W[4], dW[4];
-      W[0] = -s2 * inv4pi * (lam.s.y + gs.y);
-      dW[0] = -s2 * inv4pi * (dlam.s.y + dgs.y);
+      W[0] = f * lam.s.y + X[XR::W + c];
+      dW[0] = f * dlam.s.y + X[XR::DW + c];
       for (int a = 0; a < 3; ++a) {
-        W[1 + a] = -s2 * inv4pi * (lam.v[a].y + gv[a].y);
-        dW[1 + a] = -s2 * inv4pi * (dlam.v[a].y + dgv[a].y);
+        W[1 + a] = f * lam.v[a].y + X[XR::W + (1 + a) * NP + c];
+        dW[1 + a] = f * dlam.v[a].y + X[XR::DW + (1 + a) * NP + c];
       }
-      cd Slm = ws.R[hs];
-      double Th = s2 * inv4pi * (th.y + Slm.y * O0);
+      const double Th = s2 * inv4pi * th.y + X[XR::TH + c];
       // zeta vectors (Step 8, App. A.7; reading G3 for S')
       double nxW[3];
       cross3(nup, W + 1, nxW);
-      Zr[c] = Th;
-      Zr[NP + c] = W[0];
-      Zr[NP + NP + c] = -W[1];
-      Zr[NP + 2 * NP + c] = -W[2];
-      Zr[NP + 3 * NP + c] = -W[3];
-      Zr[5 * NP + c] = dW[0];
-      Zr[5 * NP + NP + c] = -dW[1];
-      Zr[5 * NP + 2 * NP + c] = -dW[2];
-      Zr[5 * NP + 3 * NP + c] = -dW[3];
-      Zr[9 * NP + c] = -dot3(nup, W + 1);
-      for (int a = 0; a < 3; ++a) Zr[9 * NP + (1 + a) * NP + c] = -W[0] * nup[a] - nxW[a];
+      Z[c] = Th;
+      Z[NP + c] = W[0];
+      Z[2 * NP + c] = -W[1];
+      Z[3 * NP + c] = -W[2];
+      Z[4 * NP + c] = -W[3];
+      Z[5 * NP + c] = dW[0];
+      Z[6 * NP + c] = -dW[1];
+      Z[7 * NP + c] = -dW[2];
+      Z[8 * NP + c] = -dW[3];
+      Z[9 * NP + c] = -dot3(nup, W + 1);
+      for (int a = 0; a < 3; ++a) Z[10 * NP + a * NP + c] = -W[0] * nup[a] - nxW[a];
     }
-    if (lane == 0 && pstat) pstat[k - kbase] = (ws.conv[0] && ws.conv[1] && ws.conv[2]) ? 0 : 1;
-    nswap += ws.swap[0] + ws.swap[1] + ws.swap[2];
+    for (int i = D::NZ + lane; i < NZS; i += 32) Z[i] = 0.0;
     __syncwarp();
   }
-  if (swapcnt && lane == 0 && nswap) atomicAdd(swapcnt, nswap);
 }
 
 // ------------------------------------------------------------------------------------------------
-// Step 8 contraction + smooth subtraction + CSR store.  One CTA per work item (patch, up to TILE
-// pairs).  Thread (i, g): node i, pair group g; each thread carries RB = TILE / G pairs.
+// k_contract: Step 8 in matrix mode (App. A.7) as DMMA GEMMs per tile of TP pairs of one
+// patch: D = zeta(W) P_D, D' = zeta(dW) P_D, S' = zeta_S P_Sp, S = Theta P_Sd + zeta(W) P_Sg, then global
+// units (A2), the smooth-rule subtraction (A14) and the CSR store.  Warp w owns the (M-tile, N-tile)
+// pairs w, w + 16, ...; 4 accumulator tiles (S, D, S', D') each.  Z tile staged in shared memory.
 // ------------------------------------------------------------------------------------------------
 template <int P>
 struct ContractCfg {
-  static constexpr int N = Dims<P>::N;
-  static constexpr int G = (128 / N) > 0 ? (128 / N) : 1;
-  static constexpr int RB = ((P >= 8 ? 8 : 16) + G - 1) / G;   // pairs per thread
-  static constexpr int TILE = RB * G;                          // pairs per CTA tile
-  static constexpr int THREADS = ((G * N + 31) / 32) * 32;
+  using D = Dims<P>;
+  static constexpr int TP = P >= 10 ? 16 : 32, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 16;
+  static constexpr int ZS = (D::NZS % 16 == 4) ? D::NZS : D::NZS + ((4 - D::NZS % 16) + 16) % 16;
+  static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
+  static constexpr size_t SMEM = (size_t)TP * ZS * sizeof(double) + TP * 8 * sizeof(double) + TP * 16;
 };
 
 template <int P>
-__global__ void __launch_bounds__(ContractCfg<P>::THREADS)
-    k_contract(int64_t n_items, const int64_t *__restrict__ item_ptr, int64_t n_patches,
-               const int64_t *__restrict__ seg_ptr, const int64_t *__restrict__ perm,
-               const int64_t *__restrict__ ptgt, int64_t kbase, const int32_t *__restrict__ pair_patch,
-               const double *__restrict__ fit, const double *__restrict__ Z, const double *__restrict__ nodes,
+__global__ void __launch_bounds__(512, 1)
+    k_contract(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, int64_t n_patches,
+               const int64_t *__restrict__ seg_ptr, int64_t sA, const int64_t *__restrict__ perm,
+               const int64_t *__restrict__ ptgt, int64_t kbase, const double *__restrict__ fit,
+               const double *__restrict__ Zrow, const double *__restrict__ nodes,
                const double *__restrict__ normals, const double *__restrict__ weights,
                const double *__restrict__ tx, const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
-               uint32_t mask, int raw, int32_t *__restrict__ col_idx, double *vS, double *vD, double *vSp,
-               double *vDp, int32_t *__restrict__ pstat) {
+               uint32_t mask, int raw, int64_t obase, int32_t *__restrict__ col_idx, double *vS, double *vD,
+               double *vSp, double *vDp, int32_t *__restrict__ pstat) {
   using D = Dims<P>;
   using L = Layout<P>;
   using CC = ContractCfg<P>;
-  constexpr int N = D::N, NP = D::NP, NZ = D::NZ, TILE = CC::TILE, G = CC::G, RB = CC::RB;
-  __shared__ double sZ[TILE][NZ];
-  __shared__ double sT[TILE][7];     // target x, nu'
-  __shared__ int64_t sK[TILE];
-  __shared__ int sSelf[TILE];
-  const int64_t item = blockIdx.x;
-  if (item >= n_items) return;
-  // patch of this item: largest P with item_ptr[P] <= item
+  constexpr int N = D::N, NP = D::NP, TP = CC::TP, ZS = CC::ZS, NZS = D::NZS;
+  extern __shared__ double sz[];
+  double *sT = sz + TP * ZS;                       // [TP][8] target x, nu'
+  int64_t *sK = reinterpret_cast<int64_t *>(sT + TP * 8);
+  int *sSelf = reinterpret_cast<int *>(sK + TP);
+  const int64_t item = item0 + blockIdx.x;
+  if (item >= item1) return;
   int64_t lo = 0, hi = n_patches;
   while (hi - lo > 1) {
     int64_t mid = (lo + hi) >> 1;
     if (item_ptr[mid] <= item) lo = mid; else hi = mid;
   }
   const int64_t Pp = lo;
-  const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TILE;
-  const int cnt = (int)min((int64_t)TILE, seg_ptr[Pp + 1] - s0);
+  const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
+  const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *blk = fit + Pp * (int64_t)L::STRIDE;
-  const double h = blk[L::HDR + H_H];
-  // stage the tile
-  for (int i = threadIdx.x; i < TILE * NZ; i += blockDim.x) {
-    int r = i / NZ, c = i % NZ;
-    sZ[r][c] = r < cnt ? Z[(s0 + r) * NZ + c] : 0.0;
+  for (int i = threadIdx.x; i < TP * NZS; i += blockDim.x) {
+    const int r = i / NZS, c = i % NZS;
+    sz[r * ZS + c] = r < cnt ? Zrow[(s0 + r - sA) * NZS + c] : 0.0;
   }
-  for (int r = threadIdx.x; r < TILE; r += blockDim.x) {
+  for (int r = threadIdx.x; r < TP; r += blockDim.x) {
     if (r < cnt) {
-      int64_t k = perm[s0 + r], t = ptgt[k - kbase];
+      const int64_t k = perm[s0 + r], t = ptgt[k - kbase];
       sK[r] = k;
       for (int a = 0; a < 3; ++a) {
-        sT[r][a] = tx[3 * t + a];
-        sT[r][3 + a] = tnorm ? tnorm[3 * t + a] : 0.0;
+        sT[r * 8 + a] = tx[3 * t + a];
+        sT[r * 8 + 3 + a] = tnorm ? tnorm[3 * t + a] : 0.0;
       }
       int sl = -1;
       if (self_node) {
-        int64_t sn = self_node[t];
+        const int64_t sn = self_node[t];
         if (sn >= 0 && sn / N == Pp) sl = (int)(sn % N);
       }
       sSelf[r] = sl;
     }
   }
   __syncthreads();
-  const int i = threadIdx.x % N, g = threadIdx.x / N;
-  if (g >= G) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
-  double aS[RB], aD[RB], aSp[RB], aDp[RB];
-#pragma unroll
-  for (int r = 0; r < RB; ++r) aS[r] = aD[r] = aSp[r] = aDp[r] = 0;
-  for (int c = 0; c < NP; ++c) {
-    double psd = __ldg(PSd + c * N + i);
-#pragma unroll
-    for (int r = 0; r < RB; ++r) aS[r] = fma(sZ[g + r * G][c], psd, aS[r]);
-  }
-  for (int c = 0; c < 4 * NP; ++c) {
-    double pd = __ldg(PD + c * N + i), psp = __ldg(PSp + c * N + i), psg = __ldg(PSg + c * N + i);
-#pragma unroll
-    for (int r = 0; r < RB; ++r) {
-      const double *z = sZ[g + r * G];
-      double zw = z[NP + c], zdw = z[5 * NP + c], zs = z[9 * NP + c];
-      aD[r] = fma(zw, pd, aD[r]);
-      aDp[r] = fma(zdw, pd, aDp[r]);
-      aSp[r] = fma(zs, psp, aSp[r]);
-      aS[r] = fma(zw, psg, aS[r]);
-    }
-  }
-  // epilogue: global units, smooth subtraction (reading A14), store
-  const double *xi = nodes + (Pp * N + i) * 3, *ni = normals + (Pp * N + i) * 3;
-  const double wi = weights[Pp * N + i];
-  const double x0 = xi[0], x1 = xi[1], x2 = xi[2], n0 = ni[0], n1 = ni[1], n2 = ni[2];
+  const double h = blk[L::HDR + H_H];
   const double inv4pi = 1.0 / (4.0 * kPi);
-#pragma unroll
-  for (int r = 0; r < RB; ++r) {
-    const int rr = g + r * G;
-    if (rr >= cnt) continue;
-    double S = aS[r] * h, Dv = aD[r], Sp = aSp[r], Dp = aDp[r] / h;
-    if (!raw && sSelf[rr] != i) {
-      double d0 = sT[rr][0] - x0, d1 = sT[rr][1] - x1, d2 = sT[rr][2] - x2;
-      double r2 = d0 * d0 + d1 * d1 + d2 * d2, ir = rsqrt(r2);
-      ir = ir * (1.5 - 0.5 * r2 * ir * ir);   // one Newton step -> full fp64 accuracy
-      double ir3 = ir * ir * ir;
-      double dn = d0 * n0 + d1 * n1 + d2 * n2;
-      double dnp = d0 * sT[rr][3] + d1 * sT[rr][4] + d2 * sT[rr][5];
-      double nn = n0 * sT[rr][3] + n1 * sT[rr][4] + n2 * sT[rr][5];
-      S -= inv4pi * ir * wi;
-      Dv -= inv4pi * dn * ir3 * wi;
-      Sp += inv4pi * dnp * ir3 * wi;
-      Dp -= inv4pi * (nn * ir3 - 3.0 * dn * dnp * ir3 * ir * ir) * wi;
+#pragma unroll 1
+  for (int tw = 0; tw < CC::TPW; ++tw) {
+    const int tile = warp + tw * CC::WARPS;
+    if (tile >= CC::TILES) break;
+    const int mt = tile % CC::MT, nt = tile / CC::MT;
+    const int bn = nt * 8 + (lane >> 2);           // B fragment column (node)
+    const bool bok = bn < N;
+    double aS0 = 0, aS1 = 0, aD0 = 0, aD1 = 0, aSp0 = 0, aSp1 = 0, aDp0 = 0, aDp1 = 0;
+    const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3);
+    // Theta . P_Sd  (k over NP, padded with zeros)
+    for (int k0 = 0; k0 < NP; k0 += 4) {
+      const int kk = k0 + (lane & 3);
+      const double b = (bok && kk < NP) ? __ldg(PSd + kk * N + bn) : 0.0;
+      const double a = kk < NP ? zr[k0] : 0.0;
+      dmma(aS0, aS1, a, b);
     }
-    const int64_t o = (sK[rr] - kbase) * N + i;
-    if (col_idx) col_idx[o] = (int32_t)(Pp * N + i);
-    bool bad = false;
-    if (vS) { vS[o] = (mask & 1) ? S : 0.0; bad |= !isfinite(S); }
-    if (vD) { vD[o] = (mask & 2) ? Dv : 0.0; bad |= !isfinite(Dv); }
-    if (vSp) { vSp[o] = (mask & 4) ? Sp : 0.0; bad |= !isfinite(Sp); }
-    if (vDp) { vDp[o] = (mask & 8) ? Dp : 0.0; bad |= !isfinite(Dp); }
-    if (bad && pstat) atomicOr(pstat + (sK[rr] - kbase), 2);
+    // the 4 NP blocks
+    for (int k0 = 0; k0 < 4 * NP; k0 += 4) {
+      const int kk = k0 + (lane & 3);
+      const double bd = bok ? __ldg(PD + kk * N + bn) : 0.0;
+      const double bsp = bok ? __ldg(PSp + kk * N + bn) : 0.0;
+      const double bsg = bok ? __ldg(PSg + kk * N + bn) : 0.0;
+      const double zw = zr[NP + k0], zdw = zr[5 * NP + k0], zs = zr[9 * NP + k0];
+      dmma(aD0, aD1, zw, bd);
+      dmma(aDp0, aDp1, zdw, bd);
+      dmma(aSp0, aSp1, zs, bsp);
+      dmma(aS0, aS1, zw, bsg);
+    }
+    // epilogue: C[row = lane/4][col = 2 (lane%4) + {0,1}]
+    const int row = mt * 8 + (lane >> 2);
+    if (row >= cnt) continue;
+    const double accS[2] = {aS0, aS1}, accD[2] = {aD0, aD1}, accSp[2] = {aSp0, aSp1}, accDp[2] = {aDp0, aDp1};
+    for (int q = 0; q < 2; ++q) {
+      const int i = nt * 8 + 2 * (lane & 3) + q;
+      if (i >= N) continue;
+      double S = accS[q] * h, Dv = accD[q], Sp = accSp[q], Dp = accDp[q] / h;
+      if (!raw && sSelf[row] != i) {
+        const double *xi = nodes + (Pp * N + i) * 3, *ni = normals + (Pp * N + i) * 3;
+        const double wi = weights[Pp * N + i];
+        const double d0 = sT[row * 8] - xi[0], d1 = sT[row * 8 + 1] - xi[1], d2 = sT[row * 8 + 2] - xi[2];
+        const double r2 = d0 * d0 + d1 * d1 + d2 * d2;
+        double ir = rsqrt(r2);
+        ir = ir * (1.5 - 0.5 * r2 * ir * ir);
+        const double ir3 = ir * ir * ir;
+        const double dn = d0 * ni[0] + d1 * ni[1] + d2 * ni[2];
+        const double dnp = d0 * sT[row * 8 + 3] + d1 * sT[row * 8 + 4] + d2 * sT[row * 8 + 5];
+        const double nn = ni[0] * sT[row * 8 + 3] + ni[1] * sT[row * 8 + 4] + ni[2] * sT[row * 8 + 5];
+        S -= inv4pi * ir * wi;
+        Dv -= inv4pi * dn * ir3 * wi;
+        Sp += inv4pi * dnp * ir3 * wi;
+        Dp -= inv4pi * (nn * ir3 - 3.0 * dn * dnp * ir3 * ir * ir) * wi;
+      }
+      const int64_t o = (sK[row] - obase) * N + i;
+      if (col_idx) col_idx[o] = (int32_t)(Pp * N + i);
+      bool bad = false;
+      if (vS) { vS[o] = (mask & 1) ? S : 0.0; bad |= !isfinite(S); }
+      if (vD) { vD[o] = (mask & 2) ? Dv : 0.0; bad |= !isfinite(Dv); }
+      if (vSp) { vSp[o] = (mask & 4) ? Sp : 0.0; bad |= !isfinite(Sp); }
+      if (vDp) { vDp[o] = (mask & 8) ? Dp : 0.0; bad |= !isfinite(Dp); }
+      if (bad && pstat) atomicOr(pstat + (sK[row] - obase), 2);
+    }
   }
 }
 

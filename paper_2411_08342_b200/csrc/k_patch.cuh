@@ -132,10 +132,16 @@ __global__ void k_patch_geom(int64_t n_patches, const double *__restrict__ nodes
   }
 }
 
-// Step 3 edge tables, one thread per (patch, edge node):  g^{(j,k)} = Hess S^{(j,k)}(y) tau (2<=j<=p),
-// e^{(j,k)} = grad S^{(j,k)}(y) x tau (1<=j<=p), k >= 0, stored lane-coalesced [kappa][a][re/im][jk].
+// Step 3: at each edge node y_kappa the tables g^{(j,k)} = Hess S^{(j,k)}(y) tau
+// (2<=j<=p, eq qjkdef2) and e^{(j,k)} = grad S^{(j,k)}(y) x tau (1<=j<=p, eq vjkdef), k >= 0, written as
+// the rows (kappa, axis) of the per-patch GEMM operand M of the line-integral maps (Step 6):
+//   Q^{(j,k)} = sum_kappa (0, a_kappa)(0, g) = (-a.g, a x g),  V^{(j,k)} = sum_kappa a_kappa . e,
+// so that [Q | V](pair) = a(pair) M with a = (omega1_kappa d_kappa) flattened (k = 3 kappa + axis), and
+// dQ(pair) = b(pair) M[:, Q cols] with b = omega1 nu' - omega3 (nu'.d) d.
+// Columns: Q block 8 jk + 2 comp + re/im (comp 0..3 = scalar, x, y, z), then V block 8 NQ + 2 jk + re/im.
+// One thread per (patch, edge node); it owns rows 3 kappa .. 3 kappa + 2.
 template <int P>
-__global__ void k_edge_tables(int64_t n_patches, double *__restrict__ fit) {
+__global__ void k_edge_tables(int64_t n_patches, const double *__restrict__ hc, double *__restrict__ fit) {
   using D = Dims<P>;
   using L = Layout<P>;
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -146,21 +152,35 @@ __global__ void k_edge_tables(int64_t n_patches, double *__restrict__ fit) {
   double y[3], t[3];
   for (int a = 0; a < 3; ++a) { y[a] = blk[L::YL + 3 * kap + a]; t[a] = blk[L::TL + 3 * kap + a]; }
   cd R[D::NS];
-  r_table<P>(y[1], y[2], y[0], R);
-  double *GT = blk + L::GT + (int64_t)kap * 6 * D::NQ, *ET = blk + L::ET + (int64_t)kap * 6 * D::NV;
+  r_table<P>(y[1], y[2], y[0], R, hc);
+  cd GS[D::NS][3];
+  for (int j = 0; j <= P; ++j)
+    for (int k = 0; k <= j; ++k) grad_fast(R, j, k, hc, GS[sidx(j, k)]);
+  double *M0 = blk + L::MQ + (int64_t)(3 * kap) * D::NCS;   // rows for axis 0, 1, 2 at stride NCS
+  for (int c = 0; c < D::NCS; ++c) { M0[c] = 0; M0[D::NCS + c] = 0; M0[2 * D::NCS + c] = 0; }
   for (int j = 1; j <= P; ++j)
     for (int k = 0; k <= j; ++k) {
-      cd g[3];
-      gradS(R, j, k, g);
+      const cd *g = GS[sidx(j, k)];
       cd e[3] = {g[1] * mk(t[2], 0) - g[2] * mk(t[1], 0), g[2] * mk(t[0], 0) - g[0] * mk(t[2], 0),
                  g[0] * mk(t[1], 0) - g[1] * mk(t[0], 0)};
-      int vi = vidx(j, k);
-      for (int a = 0; a < 3; ++a) { ET[(2 * a) * D::NV + vi] = e[a].x; ET[(2 * a + 1) * D::NV + vi] = e[a].y; }
+      const int vc = D::NCQ + 2 * vidx(j, k);
+      for (int a = 0; a < 3; ++a) { M0[a * D::NCS + vc] = e[a].x; M0[a * D::NCS + vc + 1] = e[a].y; }
       if (j >= 2) {
         cd h[3];
-        hessS_v(R, j, k, t, h);
-        int qi = qidx(j, k);
-        for (int a = 0; a < 3; ++a) { GT[(2 * a) * D::NQ + qi] = h[a].x; GT[(2 * a + 1) * D::NQ + qi] = h[a].y; }
+        hess_fast(GS, j, k, t, hc, h);
+        const int qc = 8 * qidx(j, k);
+        for (int ri = 0; ri < 2; ++ri) {
+          double hv[3] = {ri ? h[0].y : h[0].x, ri ? h[1].y : h[1].x, ri ? h[2].y : h[2].x};
+          // scalar part: -a.g
+          for (int a = 0; a < 3; ++a) M0[a * D::NCS + qc + ri] = -hv[a];
+          // x: a_y g_z - a_z g_y ; y: a_z g_x - a_x g_z ; z: a_x g_y - a_y g_x
+          M0[1 * D::NCS + qc + 2 + ri] = hv[2];
+          M0[2 * D::NCS + qc + 2 + ri] = -hv[1];
+          M0[2 * D::NCS + qc + 4 + ri] = hv[0];
+          M0[0 * D::NCS + qc + 4 + ri] = -hv[2];
+          M0[0 * D::NCS + qc + 6 + ri] = hv[1];
+          M0[1 * D::NCS + qc + 6 + ri] = -hv[0];
+        }
       }
     }
 }
@@ -246,8 +266,9 @@ __device__ int cta_pinv(int m, int k, double *A, double *W, double *Xo, double *
 
 template <int P>
 __global__ void __launch_bounds__(256) k_patch_fit(int64_t n_patches, const double *__restrict__ nodes,
-                                                   const double *__restrict__ normals, double *__restrict__ fit,
-                                                   double *__restrict__ work, int32_t *__restrict__ status) {
+                                                   const double *__restrict__ normals, const double *__restrict__ hc,
+                                                   double *__restrict__ fit, double *__restrict__ work,
+                                                   int32_t *__restrict__ status) {
   using D = Dims<P>;
   using L = Layout<P>;
   constexpr int N = D::N, NP = D::NP, M4 = 4 * N, K4 = 4 * NP;
@@ -275,11 +296,11 @@ __global__ void __launch_bounds__(256) k_patch_fit(int64_t n_patches, const doub
     // F_{a,i,lm} = d_a H^{(l,m)}(x_i), Hm_{i,lm} = H^{(l,m)}(x_i), H = sqrt2 Im S
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       cd R[D::NS];
-      r_table<P>(xl[3 * i + 1], xl[3 * i + 2], xl[3 * i], R);
+      r_table<P>(xl[3 * i + 1], xl[3 * i + 2], xl[3 * i], R, hc);
       for (int l = 1; l <= P; ++l)
         for (int m = 1; m <= l; ++m) {
           cd g[3];
-          gradS(R, l, m, g);
+          grad_fast(R, l, m, hc, g);
           int c = lmidx(l, m);
           for (int a = 0; a < 3; ++a) F[(a * N + i) * NP + c] = 1.4142135623730950488 * g[a].y;
           Hm[i * NP + c] = 1.4142135623730950488 * R[sidx(l, m)].y;

@@ -34,12 +34,13 @@ struct rrq_ctx_s {
     void *p = nullptr;
     size_t n = 0;
   };
-  int64_t last_np = 0, last_nz = 0;
+  int64_t last_np = 0, last_nz = 0, last_nzs = 0, last_sA = 0;
+  Buf Arow, Xrow, Qrow;
   Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one, swapcnt;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
-  double t_ms[5] = {0, 0, 0, 0, 0};
-  int64_t t_n[5] = {0, 0, 0, 0, 0};
+  double t_ms[7] = {0, 0, 0, 0, 0, 0, 0};
+  int64_t t_n[7] = {0, 0, 0, 0, 0, 0, 0};
   int64_t stats[2] = {0, 0};
   struct Pend {
     int stage;
@@ -165,7 +166,26 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
     double pw = 1;
     for (int k = 0; k < q; ++k) { xdp[j * q + k] = pw; pw *= xd[j]; }
   }
-  size_t tot = 2 * q + q * q + 2 * no + 41 * 41 + 2 * kNDirect + kNDirect * q;
+  std::vector<double> hcv(HC_SIZE, 0.0);
+  for (int l = 0; l <= HC_LMAX; ++l)
+    for (int m = -l; m <= l; ++m) {
+      double lm = l - m, lp = l + m;
+      double *dc = hcv.data() + HC_DC + 3 * (l * l + l + m);
+      dc[0] = lm * lp > 0 ? std::sqrt(lm * lp) : 0.0;
+      dc[1] = lm * (lm - 1) > 0 ? std::sqrt(lm * (lm - 1)) : 0.0;
+      dc[2] = lp * (lp - 1) > 0 ? std::sqrt(lp * (lp - 1)) : 0.0;
+    }
+  for (int m = 0; m <= HC_LMAX; ++m) {
+    hcv[HC_DG + m] = m > 0 ? std::sqrt((2.0 * m - 1.0) / (2.0 * m)) : 1.0;
+    hcv[HC_SB + m] = std::sqrt(2.0 * m + 1.0);
+  }
+  for (int l = 0; l <= HC_LMAX; ++l)
+    for (int m = 0; m <= l; ++m) {
+      double den = std::sqrt((double)(l + 1 + m) * (l + 1 - m));
+      hcv[HC_RA + sidx(l, m)] = (2.0 * l + 1.0) / den;
+      hcv[HC_RB + sidx(l, m)] = std::sqrt((double)(l + m) * (l - m)) / den;
+    }
+  size_t tot = 2 * q + q * q + 2 * no + 41 * 41 + 2 * kNDirect + kNDirect * q + HC_SIZE;
   if (cudaMalloc(&c->d_tab, tot * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     delete c;
@@ -183,6 +203,7 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   std::copy(xd.begin(), xd.end(), td);
   std::copy(wd.begin(), wd.end(), td + kNDirect);
   std::copy(xdp.begin(), xdp.end(), td + 2 * kNDirect);
+  std::copy(hcv.begin(), hcv.end(), td + 2 * kNDirect + kNDirect * q);
   cudaMemcpy(c->d_tab, h.data(), tot * sizeof(double), cudaMemcpyHostToDevice);
   c->T.tgl = c->d_tab;
   c->T.wgl = c->d_tab + q;
@@ -193,6 +214,7 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   c->T.xd = c->T.sqb + 41 * 41;
   c->T.wd = c->T.xd + kNDirect;
   c->T.xdp = c->T.wd + kNDirect;
+  c->T.hc = c->T.xdp + kNDirect * q;
   if (cuda_check(c, "rrq_create") != RRQ_OK) {
     g_create_err = c->err;
     rrq_destroy(c);
@@ -208,7 +230,7 @@ void rrq_destroy(rrq_ctx c) {
   for (auto e : c->pool) cudaEventDestroy(e);
   if (c->swapcnt.p) cudaFree(c->swapcnt.p);
   cudaFree(c->d_tab);
-  for (auto *b : {&c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
+  for (auto *b : {&c->Arow, &c->Xrow, &c->Qrow, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
                   &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
     if (b->p) cudaFree(b->p);
   delete c;
@@ -222,8 +244,10 @@ rrq_status rrq_debug_zeta(rrq_ctx c, int64_t max_pairs, int64_t *perm, double *Z
   if (!c || !n_out) return RRQ_ERR_INVALID_ARG;
   cudaDeviceSynchronize();
   int64_t n = std::min(max_pairs, c->last_np);
-  if (perm && n > 0) cudaMemcpy(perm, c->perm.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost);
-  if (Z && n > 0) cudaMemcpy(Z, c->Z.p, n * c->last_nz * sizeof(double), cudaMemcpyDeviceToHost);
+  if (perm && n > 0) cudaMemcpy(perm, bp<int64_t>(c->perm) + c->last_sA, n * sizeof(int64_t), cudaMemcpyDeviceToHost);
+  if (Z && n > 0)
+    cudaMemcpy2D(Z, c->last_nz * sizeof(double), c->Z.p, c->last_nzs * sizeof(double), c->last_nz * sizeof(double), n,
+                 cudaMemcpyDeviceToHost);
   *n_out = n;
   return cuda_check(c, "rrq_debug_zeta");
 }
@@ -237,15 +261,15 @@ rrq_status rrq_set_timing(rrq_ctx c, int enable) {
 rrq_status rrq_reset_timing(rrq_ctx c) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   t_flush(c);
-  for (int i = 0; i < 5; ++i) { c->t_ms[i] = 0; c->t_n[i] = 0; }
+  for (int i = 0; i < 7; ++i) { c->t_ms[i] = 0; c->t_n[i] = 0; }
   c->stats[0] = c->stats[1] = 0;
   return RRQ_OK;
 }
 
-rrq_status rrq_get_timing(rrq_ctx c, double ms[5], int64_t launches[5], int64_t stats[2]) {
+rrq_status rrq_get_timing(rrq_ctx c, double ms[7], int64_t launches[7], int64_t stats[2]) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   t_flush(c);
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 0; i < 7; ++i) {
     if (ms) ms[i] = c->t_ms[i];
     if (launches) launches[i] = c->t_n[i];
   }
@@ -392,13 +416,13 @@ static rrq_status patch_fit_impl(rrq_ctx c, const rrq_surface *s, double *fit, i
   TScope ts(c, 1, st);
   if ((r = compute_balls(c, s, st))) return r;
   k_patch_geom<P><<<(unsigned)Pn, 128, 0, st>>>(Pn, s->nodes, s->verts, s->edge_x, s->edge_dx, bp<double>(c->balls), c->T, fit);
-  k_edge_tables<P><<<nblk(Pn * D::E, 128), 128, 0, st>>>(Pn, fit);
+  k_edge_tables<P><<<nblk(Pn * D::E, 128), 128, 0, st>>>(Pn, c->T.hc, fit);
   c->launches += 2;
   if ((r = cuda_check(c, "k_patch_geom/k_edge_tables"))) return r;
   int grid = (int)std::min<int64_t>(Pn, 2 * c->num_sms);
   constexpr int64_t WS = fit_workspace_doubles<P>();
   if (!ensure(c, c->fitwork, (size_t)grid * WS * sizeof(double))) return RRQ_ERR_CUDA;
-  k_patch_fit<P><<<grid, 256, 0, st>>>(Pn, s->nodes, s->normals, fit, bp<double>(c->fitwork), status);
+  k_patch_fit<P><<<grid, 256, 0, st>>>(Pn, s->nodes, s->normals, c->T.hc, fit, bp<double>(c->fitwork), status);
   c->launches++;
   return cuda_check(c, "k_patch_fit");
 }
@@ -418,14 +442,20 @@ rrq_status rrq_patch_fit(rrq_ctx c, const rrq_surface *s, void *fit, int32_t *pa
   return RRQ_ERR_NOT_IMPLEMENTED;
 }
 
-constexpr int kWPB = 4;
+constexpr int kWPB = 8;   // warps per CTA of k_pair_edge
 
 template <int P>
-static size_t zeta_smem(int n_omega) {
+static size_t edge_smem(int n_omega) {
   using D = Dims<P>;
-  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + (2 * P + 1) * (2 * P + 1) + (2 * P + 2);
+  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + (2 * P + 1) * (2 * P + 1) + (2 * P + 2) + HC_SIZE;
   tab = (tab + 1) & ~1;
-  return (size_t)tab * sizeof(double) + kWPB * sizeof(WarpScratch<P>);
+  return (size_t)tab * sizeof(double) + kWPB * sizeof(EdgeScratch<P>);
+}
+template <int P>
+static size_t translate_smem() {
+  using D = Dims<P>;
+  size_t tab = (2 * P + 1) * (2 * P + 1) + 2 * P + 2 + (D::NP + 1) / 2 + 1;
+  return (tab + TransCfg<P>::WPB * (size_t)TransCfg<P>::PER_WARP) * sizeof(double);
 }
 
 template <int P>
@@ -434,7 +464,10 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
                              uint32_t mask, int64_t *row_ptr, int32_t *col_idx, double *const vals[4], int32_t *pstat,
                              cudaStream_t st) {
   using D = Dims<P>;
+  using QC = QmapCfg<P>;
   using CC = ContractCfg<P>;
+  static_assert(QmapCfg<P>::TP == ContractCfg<P>::TP, "k_qmap and k_contract share the work items");
+  constexpr int TP = QC::TP;
   const int64_t Pn = s->n_patches;
   const int raw = (mask & RRQ_RAW) ? 1 : 0;
   int64_t b[2];
@@ -442,102 +475,113 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   cudaMemcpyAsync(&b[1], pair_ptr + row_end, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   const int64_t obase = b[0], total = b[1] - b[0];
-  // sub-chunks of rows bounded by the Z scratch (<= max_pairs pairs each)
-  const int64_t max_pairs = std::max<int64_t>(1 << 16, (int64_t)(6e9 / (D::NZ * 8.0)));
-  std::vector<int64_t> hptr;
-  std::vector<std::pair<int64_t, int64_t>> subs;
-  if (total <= max_pairs) {
-    subs.push_back({row_begin, row_end});
-  } else {
-    hptr.resize(row_end - row_begin + 1);
-    cudaMemcpyAsync(hptr.data(), pair_ptr + row_begin, hptr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    int64_t r0 = row_begin;
-    while (r0 < row_end) {
-      int64_t lim = hptr[r0 - row_begin] + max_pairs;
-      int64_t r1 = std::upper_bound(hptr.begin() + (r0 - row_begin), hptr.end(), lim) - hptr.begin() + row_begin - 1;
-      if (r1 <= r0) r1 = r0 + 1;   // a single row larger than the cap: take it whole
-      r1 = std::min(r1, row_end);
-      subs.push_back({r0, r1});
-      r0 = r1;
+  if (total == 0) {
+    if (row_ptr) {
+      k_row_ptr<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase, row_ptr, D::N);
+      c->launches++;
     }
-  }
-  int64_t maxsub = 0;
-  for (auto &sr : subs) {
-    int64_t np_ = (hptr.empty() ? total : hptr[sr.second - row_begin] - hptr[sr.first - row_begin]);
-    maxsub = std::max(maxsub, np_);
+    return cuda_check(c, "rrq_build_correction");
   }
   if (c->timing) {
     if (!ensure(c, c->swapcnt, 64)) return RRQ_ERR_CUDA;
     cudaMemsetAsync(c->swapcnt.p, 0, 8, st);
   }
-  if (!ensure(c, c->ptgt, maxsub * sizeof(int64_t)) || !ensure(c, c->perm, maxsub * sizeof(int64_t)) ||
+  if (!ensure(c, c->ptgt, total * sizeof(int64_t)) || !ensure(c, c->perm, total * sizeof(int64_t)) ||
       !ensure(c, c->seg, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->cursor, (Pn + 1) * sizeof(int64_t)) ||
-      !ensure(c, c->items, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->Z, (size_t)maxsub * D::NZ * sizeof(double)) ||
-      !ensure(c, c->one, 64))
+      !ensure(c, c->items, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->one, 64))
     return RRQ_ERR_CUDA;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_pair_zeta<P, kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
-  for (auto &sr : subs) {
-    const int64_t r0 = sr.first, r1 = sr.second;
-    const int64_t kb = hptr.empty() ? obase : hptr[r0 - row_begin];
-    const int64_t np_ = hptr.empty() ? total : hptr[r1 - row_begin] - kb;
-    if (np_ == 0) continue;
-    TScope* tsp = new TScope(c, 4, st);
-    k_pair_targets<<<nblk(r1 - r0 + 1, 256), 256, 0, st>>>(r0, r1, pair_ptr, kb, bp<int64_t>(c->ptgt),
-                                                            nullptr, D::N);
-    // patch-major permutation (counting sort)
+  // ---- plumbing over the whole call: pair -> target, patch-major permutation, work items
+  std::vector<int64_t> hseg(Pn + 1), hitem(Pn + 1);
+  {
+    TScope tsp(c, 6, st);
+    k_pair_targets<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase,
+                                                                       bp<int64_t>(c->ptgt), nullptr, D::N);
     cudaMemsetAsync(c->seg.p, 0, (Pn + 1) * sizeof(int64_t), st);
-    k_patch_hist<<<nblk(np_, 256), 256, 0, st>>>(np_, kb, pair_patch, bp<int64_t>(c->seg));
+    k_patch_hist<<<nblk(total, 256), 256, 0, st>>>(total, obase, pair_patch, bp<int64_t>(c->seg));
     k_scan_i64<<<1, 1024, 0, st>>>(Pn + 1, bp<int64_t>(c->seg), bp<int64_t>(c->one));
     cudaMemcpyAsync(c->cursor.p, c->seg.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, st);
-    k_patch_scatter<<<nblk(np_, 256), 256, 0, st>>>(np_, kb, pair_patch, bp<int64_t>(c->cursor), bp<int64_t>(c->perm));
-    k_items<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<int64_t>(c->seg), CC::TILE, bp<int64_t>(c->items));
+    k_patch_scatter<<<nblk(total, 256), 256, 0, st>>>(total, obase, pair_patch, bp<int64_t>(c->cursor),
+                                                      bp<int64_t>(c->perm));
+    k_items<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<int64_t>(c->seg), TP, bp<int64_t>(c->items));
     cudaMemsetAsync(bp<int64_t>(c->items) + Pn, 0, sizeof(int64_t), st);
     k_scan_i64<<<1, 1024, 0, st>>>(Pn + 1, bp<int64_t>(c->items), bp<int64_t>(c->one) + 1);
     c->launches += 6;
-    delete tsp;
-    int64_t n_items = 0;
-    cudaMemcpyAsync(&n_items, bp<int64_t>(c->one) + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-    // zeta
-    size_t sm = zeta_smem<P>(c->prm.n_omega);
-    int64_t want = (np_ + kWPB - 1) / kWPB;
-    unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)c->num_sms * 8);
+    cudaMemcpyAsync(hseg.data(), c->seg.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hitem.data(), c->items.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  }
+  cudaStreamSynchronize(st);
+  hseg[Pn] = total;
+  // ---- sub-chunks: ranges of whole patches with at most `cap` pairs (scratch ~16 KB per pair at p = 8)
+  const int64_t per_pair = (int64_t)(2 * D::K + XRow<P>::STRIDE + QRow<P>::STRIDE + D::NZS) * 8;
+  const int64_t cap = std::max<int64_t>(4096, (int64_t)(20e9 / per_pair));
+  std::vector<std::pair<int64_t, int64_t>> subs;
+  int64_t maxsub = 0;
+  for (int64_t P0 = 0; P0 < Pn;) {
+    int64_t P1 = P0 + 1;
+    while (P1 < Pn && hseg[P1 + 1] - hseg[P0] <= cap) ++P1;
+    if (hseg[P1] > hseg[P0]) {
+      subs.push_back({P0, P1});
+      maxsub = std::max(maxsub, hseg[P1] - hseg[P0]);
+    }
+    P0 = P1;
+  }
+  if (!ensure(c, c->Arow, (size_t)maxsub * 2 * D::K * 8) || !ensure(c, c->Xrow, (size_t)maxsub * XRow<P>::STRIDE * 8) ||
+      !ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxsub * D::NZS * 8))
+    return RRQ_ERR_CUDA;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_pair_edge<P, kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_qmap<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_translate<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_contract<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  rrq_status r;
+  for (auto &sr : subs) {
+    const int64_t sA = hseg[sr.first], sB = hseg[sr.second];
+    const int64_t it0 = hitem[sr.first], it1 = hitem[sr.second];
+    const int64_t np_ = sB - sA;
     {
-    TScope tz(c, 2, st);
-    k_pair_zeta<P, kWPB><<<grid, kWPB * 32, sm, st>>>(np_, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), kb, pair_patch,
-                                                       fit, tg->x, tg->normal, tg->self_node, tg->side, c->T,
-                                                       c->prm.n_omega, c->prm.rho_swap, bp<double>(c->Z),
-                                                       pstat ? pstat + (kb - obase) : nullptr,
-                                                       c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr);
+      TScope t1(c, 2, st);
+      unsigned grid = (unsigned)std::min<int64_t>((np_ + kWPB - 1) / kWPB, (int64_t)c->num_sms * 4);
+      k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), st>>>(
+          sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
+          tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, bp<double>(c->Arow), bp<double>(c->Xrow),
+          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr);
     }
-    c->launches++;
-    rrq_status r;
-    if ((r = cuda_check(c, "k_pair_zeta"))) return r;
+    if ((r = cuda_check(c, "k_pair_edge"))) return r;
+    {
+      TScope t2(c, 3, st);
+      k_qmap<P><<<(unsigned)(it1 - it0), 512, QC::SMEM, st>>>(it0, it1, bp<int64_t>(c->items), Pn,
+                                                                bp<int64_t>(c->seg), sA, fit, bp<double>(c->Arow),
+                                                                bp<double>(c->Qrow));
+    }
+    if ((r = cuda_check(c, "k_qmap"))) return r;
+    {
+      TScope t3(c, 4, st);
+      unsigned grid = (unsigned)std::min<int64_t>((np_ + 7) / 8, (int64_t)c->num_sms * 8);
+      k_translate<P><<<grid, 256, translate_smem<P>(), st>>>(sA, sB, bp<double>(c->Xrow), bp<double>(c->Qrow),
+                                                              c->T.sqb, bp<double>(c->Z));
+    }
+    if ((r = cuda_check(c, "k_translate"))) return r;
+    {
+      TScope t4(c, 5, st);
+      k_contract<P><<<(unsigned)(it1 - it0), 512, CC::SMEM, st>>>(
+          it0, it1, bp<int64_t>(c->items), Pn, bp<int64_t>(c->seg), sA, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt),
+          obase, fit, bp<double>(c->Z), s->nodes, s->normals, s->weights, tg->x, tg->normal, tg->self_node, mask, raw,
+          obase, col_idx, vals[0], vals[1], vals[2], vals[3], pstat);
+    }
+    if ((r = cuda_check(c, "k_contract"))) return r;
+    c->launches += 4;
+    c->last_sA = sA;
     c->last_np = np_;
-    c->last_nz = D::NZ;
-    cudaStreamSynchronize(st);   // n_items
-    if (n_items > 0) {
-      TScope tc(c, 3, st);
-      k_contract<P><<<(unsigned)n_items, CC::THREADS, 0, st>>>(
-          n_items, bp<int64_t>(c->items), Pn, bp<int64_t>(c->seg), bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), kb,
-          pair_patch, fit, bp<double>(c->Z), s->nodes, s->normals, s->weights, tg->x, tg->normal, tg->self_node,
-          mask, raw, col_idx ? col_idx + (kb - obase) * D::N : nullptr,
-          vals[0] ? vals[0] + (kb - obase) * D::N : nullptr, vals[1] ? vals[1] + (kb - obase) * D::N : nullptr,
-          vals[2] ? vals[2] + (kb - obase) * D::N : nullptr, vals[3] ? vals[3] + (kb - obase) * D::N : nullptr,
-          pstat ? pstat + (kb - obase) : nullptr);
-      c->launches++;
-      if ((r = cuda_check(c, "k_contract"))) return r;
-    }
   }
   if (row_ptr) {
-    // row_ptr[i] = (pair_ptr[row_begin + i] - obase) * n
     k_row_ptr<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase, row_ptr, D::N);
     c->launches++;
   }
+  c->last_nz = D::NZ;
+  c->last_nzs = D::NZS;
   if (c->timing) {
     unsigned long long sw = 0;
     cudaMemcpyAsync(&sw, c->swapcnt.p, 8, cudaMemcpyDeviceToHost, st);

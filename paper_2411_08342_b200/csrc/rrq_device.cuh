@@ -39,6 +39,13 @@ struct Dims {
   static constexpr int NQ = NS - 3;               // (j, k >= 0), 2 <= j <= p
   static constexpr int NV = NS - 1;               // (j, k >= 0), 1 <= j <= p
   static constexpr int NZ = 13 * NP;              // per-pair contraction vector
+  static constexpr int K = 3 * E;                 // GEMM depth of the line-integral maps: (kappa, axis)
+  static constexpr int NCQ = 8 * NQ;              // Q columns: (jk, quaternion comp, re/im)
+  static constexpr int NC = 8 * NQ + 2 * NV;      // + V columns (jk, re/im)
+  static constexpr int NCP = (NC + 7) / 8 * 8;    // padded to whole 8-wide DMMA tiles
+  static constexpr int NCS = NCP % 16 == 8 ? NCP : NCP + 8;   // row stride == 8 (mod 16): conflict-free B frags
+  static constexpr int NV8 = (2 * NV + 7) / 8 * 8;           // V columns padded
+  static constexpr int NZS = (NZ + 3) / 4 * 4;    // Z row stride (k-steps of 4)
 };
 
 // (l, m >= 0) -> flat index
@@ -57,9 +64,8 @@ struct Layout {
   static constexpr int TL = YL + 3 * D::E;   // [E][3] local scaled tangents
   static constexpr int CM = TL + 3 * D::E;   // [3][Q][3] monomial coefficients of the edge interpolants
   static constexpr int FIT = CM + 9 * D::Q;  // [13 NP][N]: P_D (4NP) P_Sp (4NP) P_Sd (NP) P_Sg (4NP)
-  static constexpr int GT = FIT + 13 * D::NP * D::N;   // [E][3][2][NQ]  Hess S^{(j,k)} tau
-  static constexpr int ET = GT + D::E * 6 * D::NQ;     // [E][3][2][NV]  grad S^{(j,k)} x tau
-  static constexpr int END = ET + D::E * 6 * D::NV;
+  static constexpr int MQ = FIT + 13 * D::NP * D::N;   // [K][NCS]: GEMM operand of the Q / V maps
+  static constexpr int END = MQ + D::K * D::NCS;
   static constexpr int STRIDE = (END + 31) / 32 * 32;
 };
 enum { H_O = 0, H_RM = 3, H_H = 12, H_ZLO = 13, H_ZHI = 14, H_VL = 15, H_CP = 24, H_RP = 27, H_HP = 28 };
@@ -72,27 +78,38 @@ struct Tables {
   const double *sqb;         // [41][41] sqrt(binomial(n, k))
   const double *xd, *wd;     // [N_DIRECT] Gauss-Legendre rule of the direct model integrals (A11')
   const double *xdp;         // [N_DIRECT][q] powers x_j^k
+  const double *hc;          // [HC_SIZE] harmonic coefficients (see below)
 };
 constexpr int kNDirect = 48;       // reading A11'
 constexpr double kRhoDirect = 1.6;
+
+// Harmonic coefficient table (host-built by rrq_create, copied to shared memory by the kernels that use
+// it), so no square root is taken on the hot path:
+//   HC_DC + 3 (l*l + l + m) + {0,1,2} = sqrt((l-m)(l+m)), sqrt((l-m)(l-m-1)), sqrt((l+m)(l+m-1))  (|m|<=l<=10)
+//   HC_DG + m  = sqrt((2m-1)/(2m)),  HC_SB + m = sqrt(2m+1)                                       (m <= 10)
+//   HC_RA + sidx(l,m) = (2l+1)/sqrt((l+1+m)(l+1-m)),  HC_RB + sidx(l,m) = sqrt((l+m)(l-m))/sqrt((l+1+m)(l+1-m))
+constexpr int HC_LMAX = 10;
+constexpr int HC_DC = 0, HC_DG = 3 * (HC_LMAX + 1) * (HC_LMAX + 1), HC_SB = HC_DG + HC_LMAX + 1,
+              HC_RA = HC_SB + HC_LMAX + 1, HC_RB = HC_RA + (HC_LMAX + 1) * (HC_LMAX + 2) / 2,
+              HC_SIZE = HC_RB + (HC_LMAX + 1) * (HC_LMAX + 2) / 2;
 
 // R_l^m(X,Y,Z), 0 <= m <= l <= P (no Condon-Shortley phase, reading G5) by the Cartesian recurrences
 //  R_m^m = sqrt((2m-1)/(2m)) (X + iY) R_{m-1}^{m-1},  R_{m+1}^m = sqrt(2m+1) Z R_m^m,
 //  R_{l+1}^m = [(2l+1) Z R_l^m - sqrt((l+m)(l-m)) r^2 R_{l-1}^m] / sqrt((l+1+m)(l+1-m)),
 // which follow from P:L338-345 and P:L347-360 multiplied through by r^l (no trig, valid at r = 0).
 template <int P>
-__device__ __forceinline__ void r_column(double X, double Y, double Z, int m, cd *R) {
+__device__ __noinline__ void r_column(double X, double Y, double Z, int m, cd *R, const double *hc) {
   double r2 = X * X + Y * Y + Z * Z;
   cd rmm = mk(1.0, 0.0);
-  for (int k = 1; k <= m; ++k) rmm = sqrt((2.0 * k - 1.0) / (2.0 * k)) * (mk(X, Y) * rmm);
+  for (int k = 1; k <= m; ++k) rmm = hc[HC_DG + k] * (mk(X, Y) * rmm);
   R[sidx(m, m)] = rmm;
   if (m + 1 <= P) {
-    cd a = sqrt(2.0 * m + 1.0) * Z * rmm;
+    cd a = hc[HC_SB + m] * Z * rmm;
     R[sidx(m + 1, m)] = a;
     cd b = rmm;
     for (int l = m + 1; l < P; ++l) {
-      cd c = (1.0 / sqrt((double)(l + 1 + m) * (l + 1 - m))) *
-             ((2.0 * l + 1.0) * Z * a - (sqrt((double)(l + m) * (l - m)) * r2) * b);
+      const double ra = hc[HC_RA + sidx(l, m)], rb = hc[HC_RB + sidx(l, m)];
+      cd c = (ra * Z) * a - (rb * r2) * b;
       R[sidx(l + 1, m)] = c;
       b = a;
       a = c;
@@ -101,9 +118,9 @@ __device__ __forceinline__ void r_column(double X, double Y, double Z, int m, cd
 }
 
 template <int P>
-__device__ __forceinline__ void r_table(double X, double Y, double Z, cd *R) {
+__device__ __forceinline__ void r_table(double X, double Y, double Z, cd *R, const double *hc) {
 #pragma unroll 1
-  for (int m = 0; m <= P; ++m) r_column<P>(X, Y, Z, m, R);
+  for (int m = 0; m <= P; ++m) r_column<P>(X, Y, Z, m, R, hc);
 }
 
 // R_l^m for any -l <= m <= l from the m >= 0 table: R_l^{-m} = (-1)^m conj(R_l^m).
@@ -119,15 +136,14 @@ struct Term {
   cd c;
   int m;
 };
-__device__ __forceinline__ int dterms(int l, int m, int a, Term *t) {
-  double lm = (double)(l - m), lp = (double)(l + m);
+__device__ __forceinline__ int dterms(int l, int m, int a, Term *t, const double *hc) {
+  const double *dc = hc + HC_DC + 3 * (l * l + l + m);
   if (a == 2) {
-    t[0].c = mk(lm * lp > 0 ? sqrt(lm * lp) : 0.0, 0.0);
+    t[0].c = mk(dc[0], 0.0);
     t[0].m = m;
     return 1;
   }
-  double cp = lm * (lm - 1) > 0 ? sqrt(lm * (lm - 1)) : 0.0;
-  double cm = lp * (lp - 1) > 0 ? sqrt(lp * (lp - 1)) : 0.0;
+  const double cp = dc[1], cm = dc[2];
   if (a == 0) {  // dX = (D+ + D-)/2, D+ = -cp R^{m+1}, D- = cm R^{m-1}
     t[0].c = mk(-0.5 * cp, 0.0);
     t[1].c = mk(0.5 * cm, 0.0);
@@ -140,20 +156,20 @@ __device__ __forceinline__ int dterms(int l, int m, int a, Term *t) {
   return 2;
 }
 
-__device__ __forceinline__ cd dR(const cd *R, int l, int m, int a) {
+__device__ __noinline__ cd dR(const cd *R, int l, int m, int a, const double *hc) {
   Term t[2];
-  int n = dterms(l, m, a, t);
+  int n = dterms(l, m, a, t, hc);
   cd s = mk(0.0, 0.0);
   for (int i = 0; i < n; ++i) cfma(s, t[i].c, rget(R, l - 1, t[i].m));
   return s;
 }
 
-__device__ __forceinline__ cd d2R(const cd *R, int l, int m, int a, int b) {
+__device__ __noinline__ cd d2R(const cd *R, int l, int m, int a, int b, const double *hc) {
   Term t[2];
-  int n = dterms(l, m, a, t);
+  int n = dterms(l, m, a, t, hc);
   cd s = mk(0.0, 0.0);
   for (int i = 0; i < n; ++i)
-    if (t[i].m <= l - 1 && t[i].m >= -(l - 1)) cfma(s, t[i].c, dR(R, l - 1, t[i].m, b));
+    if (t[i].m <= l - 1 && t[i].m >= -(l - 1)) cfma(s, t[i].c, dR(R, l - 1, t[i].m, b, hc));
   return s;
 }
 
@@ -161,19 +177,51 @@ __device__ __forceinline__ cd d2R(const cd *R, int l, int m, int a, int b) {
 __device__ __forceinline__ int sax(int a) { return a == 0 ? 2 : a - 1; }
 
 // grad S^{(l,m)} at the point whose R table is R (any m).
-__device__ __forceinline__ void gradS(const cd *R, int l, int m, cd g[3]) {
-  for (int a = 0; a < 3; ++a) g[a] = dR(R, l, m, sax(a));
+__device__ __noinline__ void gradS(const cd *R, int l, int m, cd g[3], const double *hc) {
+  for (int a = 0; a < 3; ++a) g[a] = dR(R, l, m, sax(a), hc);
 }
 // (Hess S^{(l,m)}) v
-__device__ __forceinline__ void hessS_v(const cd *R, int l, int m, const double v[3], cd out[3]) {
+__device__ __noinline__ void hessS_v(const cd *R, int l, int m, const double v[3], cd out[3], const double *hc) {
   for (int a = 0; a < 3; ++a) {
     cd s = mk(0.0, 0.0);
     for (int b = 0; b < 3; ++b) {
-      cd h = d2R(R, l, m, sax(a), sax(b));
+      cd h = d2R(R, l, m, sax(a), sax(b), hc);
       s = s + v[b] * h;
     }
     out[a] = s;
   }
+}
+
+// Inline gradient of S^{(l,m)} from the R table (reading A3 rules with S(x,y,z) = R(y,z,x)):
+//   dS/dx = dZ R = cz R_{l-1}^m,  dS/dy = dX R = (cm R_{l-1}^{m-1} - cp R_{l-1}^{m+1})/2,
+//   dS/dz = dY R = i (cp R_{l-1}^{m+1} + cm R_{l-1}^{m-1})/2.
+__device__ __forceinline__ void grad_fast(const cd *R, int l, int m, const double *hc, cd g[3]) {
+  const double *dc = hc + HC_DC + 3 * (l * l + l + m);
+  const cd r0 = rget(R, l - 1, m), rp = rget(R, l - 1, m + 1), rm = rget(R, l - 1, m - 1);
+  g[0] = dc[0] * r0;
+  g[1] = 0.5 * (dc[2] * rm - dc[1] * rp);
+  const cd t = 0.5 * (dc[1] * rp + dc[2] * rm);
+  g[2] = mk(-t.y, t.x);
+}
+// GS table entry for any m from the m >= 0 table: grad S^{(l,-m)} = (-1)^m conj(grad S^{(l,m)}).
+__device__ __forceinline__ void gget(const cd (*GS)[3], int l, int m, cd g[3]) {
+  if (l < 0 || m > l || m < -l) { g[0] = g[1] = g[2] = mk(0, 0); return; }
+  if (m >= 0) { g[0] = GS[sidx(l, m)][0]; g[1] = GS[sidx(l, m)][1]; g[2] = GS[sidx(l, m)][2]; return; }
+  const double sg = ((-m) & 1) ? -1.0 : 1.0;
+  for (int a = 0; a < 3; ++a) g[a] = sg * conj(GS[sidx(l, -m)][a]);
+}
+// (Hess S^{(l,m)}) v = grad (v . grad S^{(l,m)}) with v . grad S^{(l,m)} = v_x cz S^{(l-1,m)} +
+// cp b+ S^{(l-1,m+1)} + cm b- S^{(l-1,m-1)},  b+- = (-+ v_y + i v_z)/2   (same rules, applied twice).
+__device__ __forceinline__ void hess_fast(const cd (*GS)[3], int l, int m, const double v[3], const double *hc,
+                                          cd out[3]) {
+  const double *dc = hc + HC_DC + 3 * (l * l + l + m);
+  const cd bp = (0.5 * dc[1]) * mk(-v[1], v[2]), bm = (0.5 * dc[2]) * mk(v[1], v[2]);
+  const double b0 = v[0] * dc[0];
+  cd g0[3], gp[3], gm[3];
+  gget(GS, l - 1, m, g0);
+  gget(GS, l - 1, m + 1, gp);
+  gget(GS, l - 1, m - 1, gm);
+  for (int a = 0; a < 3; ++a) out[a] = b0 * g0[a] + bp * gp[a] + bm * gm[a];
 }
 
 // Complex quaternion.

@@ -8,7 +8,8 @@ kernels S, D, S', D':
   F_tr   = 20 T_lam + 40 T_lam + 4 T_theta              translation (Step 7)
   F_edge = 3 (6 p~^2 + 300 p~) + 2 n_Omega (12 p~ + 40) per swap-regime edge   (Step 5)
   F_con  = 8 n_p n (D) + 8 n_p n (D') + 10 n_p n (S) + 8 n_p n + 40 n_p (S')   (Step 8)
-k_pair_zeta carries everything but F_con; k_contract carries F_con.
+Per kernel: k_pair_edge F_tgt + F_edge (+ swap extras); k_qmap F_Q + F_dQ + F_V; k_translate F_tr;
+k_contract F_con.
 Algorithmic bytes per pair: the CSR output (4 n fp64 values + n int32 columns) + target (56 B); the
 patch data is amortised over the pairs of a patch (added per patch).
 """
@@ -31,11 +32,14 @@ def pair_flops(p, q=None, n_omega=32):
     ns = (p + 1) * (p + 2) // 2
     nq, nv = ns - 3, ns - 1
     tl, tt = translation_terms(p, 2), translation_terms(p, 1)
-    zeta = (12 * (p + 3) ** 2 + 2 * 36 * 3 * q * nq + 12 * 3 * q * nv + 20 * tl + 40 * tl + 4 * tt
-            + 3 * (6 * q * q + 300 * q))
+    edge = 12 * (p + 3) ** 2 + 3 * (6 * q * q + 300 * q)
+    qmap = 2 * 36 * 3 * q * nq + 12 * 3 * q * nv
+    translate = 20 * tl + 40 * tl + 4 * tt
+    zeta = edge + qmap + translate
     contract = 8 * npb * n * 2 + 10 * npb * n + 8 * npb * n + 40 * npb
     swap_edge = 2 * n_omega * (12 * q + 40)
-    return dict(zeta=zeta, contract=contract, swap_edge=swap_edge, total=zeta + contract)
+    return dict(edge=edge, qmap=qmap, translate=translate, zeta=zeta, contract=contract, swap_edge=swap_edge,
+                total=zeta + contract)
 
 
 def pair_bytes(p):
