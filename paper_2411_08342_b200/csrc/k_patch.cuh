@@ -246,15 +246,25 @@ __device__ int cta_pinv(int m, int k, double *A, double *W, double *Xo, double *
       for (int i = j + lane; i < m; i += 32) w[i] -= d * col[i];
       __syncwarp();
     }
-    // back substitution R x = (Q^T e_c)[0:k]; R_jj = rd[j], R_ji (i > j) = A[i*m + j]
-    if (lane == 0)
-      for (int r = k - 1; r >= 0; --r) {
-        double s = w[r];
-        for (int cc = r + 1; cc < k; ++cc) s -= A[(int64_t)cc * m + r] * w[cc];
-        w[r] = s / rd[r];
+  }
+  __syncthreads();
+  // back substitution R x = (Q^T e_c)[0:k], one thread per right-hand side c (R_jj = rd[j],
+  // R_ji (i > j) = A[i*m + j], read by all threads in lockstep: broadcast)
+  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    double *w = W + (int64_t)c * m;
+    for (int r = k - 1; r >= 0; --r) {
+      double s0 = w[r], s1 = 0, s2 = 0, s3 = 0;
+      int cc = r + 1;
+      for (; cc + 3 < k; cc += 4) {
+        s0 -= A[(int64_t)cc * m + r] * w[cc];
+        s1 -= A[(int64_t)(cc + 1) * m + r] * w[cc + 1];
+        s2 -= A[(int64_t)(cc + 2) * m + r] * w[cc + 2];
+        s3 -= A[(int64_t)(cc + 3) * m + r] * w[cc + 3];
       }
-    __syncwarp();
-    for (int r = lane; r < k; r += 32) Xo[(int64_t)c * k + r] = w[r];
+      for (; cc < k; ++cc) s0 -= A[(int64_t)cc * m + r] * w[cc];
+      w[r] = ((s0 + s1) + (s2 + s3)) / rd[r];
+    }
+    for (int r = 0; r < k; ++r) Xo[(int64_t)c * k + r] = w[r];
   }
   __syncthreads();
   double rmax = 0;
