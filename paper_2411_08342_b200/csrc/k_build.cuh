@@ -97,51 +97,53 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// Legendre-series edge interpolant (reading A4'): value and derivatives of component c at t, by
-// Bonnet's recurrence and P'_{j+1} = P'_{j-1} + (2j+1) P_j, P''_{j+1} = P''_{j-1} + (2j+1) P'_j.
+// Legendre-series edge interpolant (reading A4'): value and derivatives of one component at t from
+// coefficients held in registers, by Bonnet's recurrence (j+1) P_{j+1} = (2j+1) t P_j - j P_{j-1} and
+// P'_{j+1} = P'_{j-1} + (2j+1) P_j, P''_{j+1} = P''_{j-1} + (2j+1) P'_j (fully unrolled: constant
+// coefficients, no divisions).
 template <int Q>
-__device__ __noinline__ void leg_r(const double *C, int c, double t, double &v, double &d1, double &d2) {
+__device__ __forceinline__ void leg_r(const double (&Cl)[Q], double t, double &v, double &d1, double &d2) {
   double P0 = 1, P1 = t, a0 = 0, a1 = 1, b0 = 0, b1 = 0;
-  v = C[c] + C[3 + c] * t;
-  d1 = C[3 + c];
+  v = fma(Cl[1], t, Cl[0]);
+  d1 = Cl[1];
   d2 = 0;
-#pragma unroll 2
+#pragma unroll
   for (int j = 1; j + 1 < Q; ++j) {
-    double P2 = ((2 * j + 1) * t * P1 - j * P0) * (1.0 / (j + 1));
-    double a2 = a0 + (2 * j + 1) * P1, b2 = b0 + (2 * j + 1) * a1;
-    double cc = C[3 * (j + 1) + c];
-    v = fma(cc, P2, v);
-    d1 = fma(cc, a2, d1);
-    d2 = fma(cc, b2, d2);
+    const double P2 = ((2.0 * j + 1.0) / (j + 1.0)) * t * P1 - ((double)j / (j + 1.0)) * P0;
+    const double a2 = fma(2.0 * j + 1.0, P1, a0), b2 = fma(2.0 * j + 1.0, a1, b0);
+    v = fma(Cl[j + 1], P2, v);
+    d1 = fma(Cl[j + 1], a2, d1);
+    d2 = fma(Cl[j + 1], b2, d2);
     P0 = P1; P1 = P2; a0 = a1; a1 = a2; b0 = b1; b1 = b2;
   }
 }
 template <int Q>
-__device__ __noinline__ void leg_c(const double *C, int c, cd t, cd &v, cd &d1) {
+__device__ __forceinline__ void leg_c(const double (&Cl)[Q], cd t, cd &v, cd &d1) {
   cd P0 = mk(1, 0), P1 = t, a0 = mk(0, 0), a1 = mk(1, 0);
-  v = mk(C[c], 0) + C[3 + c] * t;
-  d1 = mk(C[3 + c], 0);
-#pragma unroll 2
+  v = mk(fma(Cl[1], t.x, Cl[0]), Cl[1] * t.y);
+  d1 = mk(Cl[1], 0);
+#pragma unroll
   for (int j = 1; j + 1 < Q; ++j) {
-    cd P2 = (1.0 / (j + 1)) * ((2.0 * j + 1) * (t * P1) - (double)j * P0);
-    cd a2 = a0 + (2.0 * j + 1) * P1;
-    double cc = C[3 * (j + 1) + c];
-    v = v + cc * P2;
-    d1 = d1 + cc * a2;
+    const double ca = (2.0 * j + 1.0) / (j + 1.0), cb = (double)j / (j + 1.0);
+    const cd tp = t * P1;
+    const cd P2 = mk(ca * tp.x - cb * P0.x, ca * tp.y - cb * P0.y);
+    const cd a2 = mk(fma(2.0 * j + 1.0, P1.x, a0.x), fma(2.0 * j + 1.0, P1.y, a0.y));
+    v = mk(fma(Cl[j + 1], P2.x, v.x), fma(Cl[j + 1], P2.y, v.y));
+    d1 = mk(fma(Cl[j + 1], a2.x, d1.x), fma(Cl[j + 1], a2.y, d1.y));
     P0 = P1; P1 = P2; a0 = a1; a1 = a2;
   }
 }
-// x(t), x'(t) (3 components, real t)
+// x(t), x'(t) (3 components, real t) from coefficients C[j*3 + c] (read uniformly across the warp)
 template <int Q>
-__device__ __noinline__ void leg_r3(const double *C, double t, double x[3], double dx[3]) {
+__device__ __forceinline__ void leg_r3(const double *__restrict__ C, double t, double x[3], double dx[3]) {
   double P0 = 1, P1 = t, a0 = 0, a1 = 1;
-  for (int c = 0; c < 3; ++c) { x[c] = C[c] + C[3 + c] * t; dx[c] = C[3 + c]; }
-#pragma unroll 2
+  for (int c = 0; c < 3; ++c) { x[c] = fma(C[3 + c], t, C[c]); dx[c] = C[3 + c]; }
+#pragma unroll
   for (int j = 1; j + 1 < Q; ++j) {
-    double P2 = ((2 * j + 1) * t * P1 - j * P0) * (1.0 / (j + 1));
-    double a2 = a0 + (2 * j + 1) * P1;
+    const double P2 = ((2.0 * j + 1.0) / (j + 1.0)) * t * P1 - ((double)j / (j + 1.0)) * P0;
+    const double a2 = fma(2.0 * j + 1.0, P1, a0);
     for (int c = 0; c < 3; ++c) {
-      double cc = C[3 * (j + 1) + c];
+      const double cc = C[3 * (j + 1) + c];
       x[c] = fma(cc, P2, x[c]);
       dx[c] = fma(cc, a2, dx[c]);
     }
@@ -285,11 +287,15 @@ __global__ void __launch_bounds__(WPB * 32)
       const int e = lane < 9 ? lane / 3 : 2, c = lane < 9 ? lane % 3 : 2, base = 3 * e;
       const double *C = blk + L::CM + e * Q * 3;
       const double rc = rp[c];
-      auto horner_r = [&](double tt, double &v, double &d1, double &d2) { leg_r<Q>(C, c, tt, v, d1, d2); };
-      double v, d1, d2;
-      horner_r(-1.0, v, d1, d2);
-      double A = v;
-      horner_r(1.0, v, d1, d2);
+      double Cl[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) Cl[q] = C[q * 3 + c];
+      auto horner_r = [&](double tt, double &v, double &d1, double &d2) { leg_r<Q>(Cl, tt, v, d1, d2); };
+      // x(-1) = sum_j (-1)^j C_j, x(1) = sum_j C_j  (P_j(+-1) = (+-1)^j)
+      double v = 0, A = 0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) { v += Cl[q]; A += (q & 1) ? -Cl[q] : Cl[q]; }
+      double d1, d2;
       double ab = v - A, ar = rc - A;
       double tc = -1.0 + 2.0 * tri_sum(ar * ab, base) / tri_sum(ab * ab, base);
       bool go = true;
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(WPB * 32)
       bool conv = false;
       for (int it = 0; it < 20; ++it) {
         cd xv, xd;
-        leg_c<Q>(C, c, tz, xv, xd);
+        leg_c<Q>(Cl, tz, xv, xd);
         cd xrr = xv - mk(rc, 0);
         cd sq = xrr * xrr, pr = xrr * xd;
         cd F = mk(tri_sum(sq.x, base), tri_sum(sq.y, base));
