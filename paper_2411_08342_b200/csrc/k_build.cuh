@@ -484,8 +484,20 @@ struct QmapCfg {
   static constexpr int KA = (D::K % 16 == 4) ? D::K : D::K + ((4 - D::K % 16) + 16) % 16;
   static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8;
   static constexpr int NTW = (NTALL + NSPLIT - 1) / NSPLIT;   // max N-tiles per warp
-  static constexpr size_t SMEM = (size_t)ROWS * KA * sizeof(double);
+  static constexpr int KC = 12, NCH = D::K / KC;              // B staged in chunks of KC k-rows
+  static_assert(D::K % KC == 0, "K must be a multiple of the B chunk");
+  static constexpr size_t SMEM_A = (size_t)ROWS * KA * sizeof(double);
+  static constexpr size_t SMEM_B = (size_t)KC * D::NCS * sizeof(double);
+  static constexpr size_t SMEM = SMEM_A + 2 * SMEM_B;
 };
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
 template <int P>
 __global__ void __launch_bounds__(512, 1)
@@ -496,8 +508,9 @@ __global__ void __launch_bounds__(512, 1)
   using L = Layout<P>;
   using C = QmapCfg<P>;
   using QR = QRow<P>;
-  constexpr int K = D::K, KA = C::KA, TP = C::TP, NCS = D::NCS;
+  constexpr int K = D::K, KA = C::KA, TP = C::TP, NCS = D::NCS, KC = C::KC;
   extern __shared__ double sA_[];
+  double *sB = sA_ + C::SMEM_A / sizeof(double);    // [2][KC][NCS]
   const int64_t item = item0 + blockIdx.x;
   if (item >= item1) return;
   int64_t lo = 0, hi = n_patches;
@@ -508,30 +521,48 @@ __global__ void __launch_bounds__(512, 1)
   const int64_t Pp = lo;
   const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
+  const double *M = fit + Pp * (int64_t)L::STRIDE + L::MQ;
+  auto issue = [&](int ch) {
+    const double *src = M + (int64_t)ch * KC * NCS;
+    double *dst = sB + (ch & 1) * KC * NCS;
+    for (int i = threadIdx.x; i < KC * NCS / 2; i += blockDim.x) cp_async16(dst + 2 * i, src + 2 * i);
+    cp_async_commit();
+  };
+  issue(0);
   // stage A: row r < TP -> a-row of pair s0 + r; row TP + r -> b-row
   for (int i = threadIdx.x; i < C::ROWS * K; i += blockDim.x) {
     const int r = i / K, k = i % K, pr = r % TP, ab = r / TP;
     sA_[r * KA + k] = pr < cnt ? Arow[(s0 + pr - sA) * 2 * K + ab * K + k] : 0.0;
   }
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int mt = warp % C::MT, ns = warp / C::MT;
   const bool brows = mt >= C::MT / 2;
   const int ntiles = brows ? C::NTQ : C::NTALL;
-  const double *M = fit + Pp * (int64_t)L::STRIDE + L::MQ;
   double acc[C::NTW][2];
 #pragma unroll
   for (int t = 0; t < C::NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
   const double *arow = sA_ + (mt * 8 + (lane >> 2)) * KA + (lane & 3);
-  const double *bcol = M + (int64_t)(lane & 3) * NCS + (lane >> 2);
-  for (int k0 = 0; k0 < K; k0 += 4) {
-    const double a = arow[k0];
-    const double *bk = bcol + (int64_t)k0 * NCS;
-#pragma unroll
-    for (int t = 0; t < C::NTW; ++t) {
-      const int nt = ns + t * C::NSPLIT;
-      if (nt < ntiles) dmma(acc[t][0], acc[t][1], a, __ldg(bk + nt * 8));
+  const int bofs = (lane & 3) * NCS + (lane >> 2);
+  for (int ch = 0; ch < C::NCH; ++ch) {
+    if (ch + 1 < C::NCH) {
+      issue(ch + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();
+    const double *bb = sB + (ch & 1) * KC * NCS + bofs;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      const double a = arow[ch * KC + kk];
+      const double *bk = bb + kk * NCS;
+#pragma unroll
+      for (int t = 0; t < C::NTW; ++t) {
+        const int nt = ns + t * C::NSPLIT;
+        if (nt < ntiles) dmma(acc[t][0], acc[t][1], a, bk[nt * 8]);
+      }
+    }
+    __syncthreads();
   }
   // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]
   const int row = mt * 8 + (lane >> 2), pr = row % TP;

@@ -370,6 +370,266 @@ __global__ void __launch_bounds__(256) k_patch_fit(int64_t n_patches, const doub
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Fit operators, quaternion form.  The 4n x 4n_p real system of P:L729-735 is the real representation
+// of left multiplication by the n x n_p quaternion matrix F_{i,lm} = (0, grad H^{(l,m)}(x_i)) (eq qprule;
+// the block pattern [[0,-F1,-F2,-F3],[F1,0,-F3,F2],...] is exactly that representation), and the real
+// representation is a *-homomorphism, so A^+ = rep(F^+) with F^+ the quaternion Moore-Penrose inverse.
+// F^+ comes from a quaternion Householder QR (H = I - v v^H / beta, v_1 = u (|x_1| + ||x||),
+// u = x_1/|x_1|, H x = -u ||x|| e_1) held entirely in shared memory (4x fewer flops than the real QR),
+// then P_D[b n_p + lm][i] = (F^+_{lm,i})_b and P_Sp[b n_p + lm][i] = (F^+_{lm,i} (0, nu_i))_b.
+// The scalar system B = grad H . nu uses a real Householder QR in shared memory.
+// One CTA (256 threads) per patch, persistent over patches.
+// ------------------------------------------------------------------------------------------------
+struct qd {
+  double s, x, y, z;
+};
+__device__ __forceinline__ qd qmul_(qd a, qd b) {
+  return qd{a.s * b.s - a.x * b.x - a.y * b.y - a.z * b.z, a.s * b.x + b.s * a.x + a.y * b.z - a.z * b.y,
+            a.s * b.y + b.s * a.y + a.z * b.x - a.x * b.z, a.s * b.z + b.s * a.z + a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ qd qconjmul_(qd a, qd b) {   // conj(a) b
+  return qmul_(qd{a.s, -a.x, -a.y, -a.z}, b);
+}
+__device__ __forceinline__ qd qld(const double *p) { return qd{p[0], p[1], p[2], p[3]}; }
+__device__ __forceinline__ void qst(double *p, qd a) { p[0] = a.s; p[1] = a.x; p[2] = a.y; p[3] = a.z; }
+
+template <int P>
+struct FitCfg {
+  using D = Dims<P>;
+  static constexpr int N = D::N, NP = D::NP;
+  // shared: Fq [NP][N][4] | rd [NP][4] | beta [NP] | rdb [NP] | betab [NP] | xl,nl [N][3] | sh [64]
+  static constexpr size_t FQ = (size_t)NP * N * 4, RD = 4 * NP;
+  static constexpr size_t SMEM_D = FQ + RD + 3 * NP + 6 * N + 64;
+  static constexpr size_t SMEM = SMEM_D * sizeof(double);
+  // per-CTA global workspace (doubles): W [N][N][4] | Xs [N][N] | B [NP][N] | Hm [N][NP]
+  static constexpr int64_t WS = (int64_t)N * N * 4 + (int64_t)N * N + 2 * (int64_t)N * NP;
+};
+
+template <int P>
+__global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const double *__restrict__ nodes,
+                                                     const double *__restrict__ normals,
+                                                     const double *__restrict__ hc, double *__restrict__ fit,
+                                                     double *__restrict__ work, int32_t *__restrict__ status) {
+  using D = Dims<P>;
+  using L = Layout<P>;
+  using FC = FitCfg<P>;
+  constexpr int N = D::N, NP = D::NP;
+  extern __shared__ double fs[];
+  double *Fq = fs;                      // column lm: Fq[(lm N + i) 4 + comp]
+  double *rd = Fq + FC::FQ;             // [NP][4] diagonal of R
+  double *beta = rd + FC::RD;           // [NP]
+  double *rdb = beta + NP, *betab = rdb + NP;
+  double *xl = betab + NP, *nl = xl + 3 * N;
+  double *sh = nl + 3 * N;              // [32] reductions
+  double *W = work + blockIdx.x * FC::WS;       // [N][N][4]: Q^H e_c
+  double *Xs = W + (int64_t)N * N * 4;          // [N][N] real workspace (B system)
+  double *Bm = Xs + (int64_t)N * N;             // [NP][N] column-major real B
+  double *Hm = Bm + (int64_t)NP * N;            // [N][NP]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t Pp = blockIdx.x; Pp < n_patches; Pp += gridDim.x) {
+    double *blk = fit + Pp * (int64_t)L::STRIDE;
+    const double *o = blk + L::HDR + H_O, *Rm = blk + L::HDR + H_RM;
+    const double invh = 1.0 / blk[L::HDR + H_H];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double *x = nodes + (Pp * N + i) * 3, *nu = normals + (Pp * N + i) * 3;
+      const double d[3] = {x[0] - o[0], x[1] - o[1], x[2] - o[2]};
+      for (int r = 0; r < 3; ++r) {
+        xl[3 * i + r] = (Rm[3 * r] * d[0] + Rm[3 * r + 1] * d[1] + Rm[3 * r + 2] * d[2]) * invh;
+        nl[3 * i + r] = Rm[3 * r] * nu[0] + Rm[3 * r + 1] * nu[1] + Rm[3 * r + 2] * nu[2];
+      }
+    }
+    __syncthreads();
+    // F_{i,lm} = (0, grad H), H = sqrt2 Im S; B = grad H . nu; Hm = H(x_i)
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      cd R[D::NS];
+      r_table<P>(xl[3 * i + 1], xl[3 * i + 2], xl[3 * i], R, hc);
+      for (int l = 1; l <= P; ++l)
+        for (int m = 1; m <= l; ++m) {
+          cd g[3];
+          grad_fast(R, l, m, hc, g);
+          const int c = lmidx(l, m);
+          const double gx = 1.4142135623730950488 * g[0].y, gy = 1.4142135623730950488 * g[1].y,
+                       gz = 1.4142135623730950488 * g[2].y;
+          qst(Fq + ((size_t)c * N + i) * 4, qd{0.0, gx, gy, gz});
+          Bm[(size_t)c * N + i] = gx * nl[3 * i] + gy * nl[3 * i + 1] + gz * nl[3 * i + 2];
+          Hm[(size_t)i * NP + c] = 1.4142135623730950488 * R[sidx(l, m)].y;
+        }
+    }
+    __syncthreads();
+    // ---- quaternion Householder QR of Fq (N x NP)
+    for (int j = 0; j < NP; ++j) {
+      double s = 0;
+      for (int i = j + threadIdx.x; i < N; i += blockDim.x) {
+        const qd a = qld(Fq + ((size_t)j * N + i) * 4);
+        s += a.s * a.s + a.x * a.x + a.y * a.y + a.z * a.z;
+      }
+      s = warp_sum(s);
+      if (lane == 0) sh[warp] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double n2 = 0;
+        for (int w = 0; w < nw; ++w) n2 += sh[w];
+        const double nrm = sqrt(n2);
+        qd x1 = qld(Fq + ((size_t)j * N + j) * 4);
+        const double a = sqrt(x1.s * x1.s + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
+        const qd u = a > 0 ? qd{x1.s / a, x1.x / a, x1.y / a, x1.z / a} : qd{1, 0, 0, 0};
+        const double f = a + nrm;
+        qst(Fq + ((size_t)j * N + j) * 4, qd{u.s * f, u.x * f, u.y * f, u.z * f});
+        qst(rd + 4 * j, qd{-u.s * nrm, -u.x * nrm, -u.y * nrm, -u.z * nrm});
+        beta[j] = nrm * (nrm + a);
+      }
+      __syncthreads();
+      const double bj = beta[j];
+      if (bj > 0)
+        for (int c = j + 1 + warp; c < NP; c += nw) {
+          qd t = {0, 0, 0, 0};
+          for (int i = j + lane; i < N; i += 32) {
+            const qd p = qconjmul_(qld(Fq + ((size_t)j * N + i) * 4), qld(Fq + ((size_t)c * N + i) * 4));
+            t.s += p.s; t.x += p.x; t.y += p.y; t.z += p.z;
+          }
+          t.s = warp_sum(t.s) / bj; t.x = warp_sum(t.x) / bj; t.y = warp_sum(t.y) / bj; t.z = warp_sum(t.z) / bj;
+          for (int i = j + lane; i < N; i += 32) {
+            double *y = Fq + ((size_t)c * N + i) * 4;
+            const qd vt = qmul_(qld(Fq + ((size_t)j * N + i) * 4), t);
+            y[0] -= vt.s; y[1] -= vt.x; y[2] -= vt.y; y[3] -= vt.z;
+          }
+        }
+      __syncthreads();
+    }
+    // ---- Q^H e_c (warp per column c), first NP entries kept
+    for (int c = warp; c < N; c += nw) {
+      double *w = W + (size_t)c * N * 4;
+      for (int i = lane; i < N; i += 32) qst(w + 4 * i, qd{i == c ? 1.0 : 0.0, 0, 0, 0});
+      __syncwarp();
+      for (int j = 0; j < NP; ++j) {
+        const double bj = beta[j];
+        if (!(bj > 0)) continue;
+        qd t = {0, 0, 0, 0};
+        for (int i = j + lane; i < N; i += 32) {
+          const qd p = qconjmul_(qld(Fq + ((size_t)j * N + i) * 4), qld(w + 4 * i));
+          t.s += p.s; t.x += p.x; t.y += p.y; t.z += p.z;
+        }
+        t.s = warp_sum(t.s) / bj; t.x = warp_sum(t.x) / bj; t.y = warp_sum(t.y) / bj; t.z = warp_sum(t.z) / bj;
+        for (int i = j + lane; i < N; i += 32) {
+          const qd vt = qmul_(qld(Fq + ((size_t)j * N + i) * 4), t);
+          double *y = w + 4 * i;
+          y[0] -= vt.s; y[1] -= vt.x; y[2] -= vt.y; y[3] -= vt.z;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // ---- back substitution R x = (Q^H e_c)[0:NP], one thread per column c; x_r = rd_r^{-1}(w_r - sum R_rk x_k)
+    double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+      double *w = W + (size_t)c * N * 4;
+      const double n0 = nl[3 * c], n1 = nl[3 * c + 1], n2 = nl[3 * c + 2];
+      for (int r = NP - 1; r >= 0; --r) {
+        qd s = qld(w + 4 * r);
+        for (int k = r + 1; k < NP; ++k) {
+          const qd p = qmul_(qld(Fq + ((size_t)k * N + r) * 4), qld(w + 4 * k));
+          s.s -= p.s; s.x -= p.x; s.y -= p.y; s.z -= p.z;
+        }
+        const qd d = qld(rd + 4 * r);
+        const double dn = d.s * d.s + d.x * d.x + d.y * d.y + d.z * d.z;
+        const qd x = qconjmul_(d, s);
+        const qd xr = {x.s / dn, x.x / dn, x.y / dn, x.z / dn};
+        qst(w + 4 * r, xr);
+        // P_D (RHS (mu,0)) and P_Sp (RHS (0, sigma nu))
+        PD[(0 * NP + r) * N + c] = xr.s;
+        PD[(1 * NP + r) * N + c] = xr.x;
+        PD[(2 * NP + r) * N + c] = xr.y;
+        PD[(3 * NP + r) * N + c] = xr.z;
+        const qd sp = qmul_(xr, qd{0.0, n0, n1, n2});
+        PSp[(0 * NP + r) * N + c] = sp.s;
+        PSp[(1 * NP + r) * N + c] = sp.x;
+        PSp[(2 * NP + r) * N + c] = sp.y;
+        PSp[(3 * NP + r) * N + c] = sp.z;
+      }
+    }
+    __syncthreads();
+    // ---- real Householder QR of B (N x NP, column-major in Bm) -> P_Sd = B^+
+    for (int j = 0; j < NP; ++j) {
+      double s = 0;
+      for (int i = j + threadIdx.x; i < N; i += blockDim.x) s += Bm[(size_t)j * N + i] * Bm[(size_t)j * N + i];
+      s = warp_sum(s);
+      if (lane == 0) sh[warp] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double n2 = 0;
+        for (int w = 0; w < nw; ++w) n2 += sh[w];
+        const double nrm = sqrt(n2), ajj = Bm[(size_t)j * N + j];
+        const double alpha = ajj > 0 ? -nrm : nrm;
+        Bm[(size_t)j * N + j] = ajj - alpha;
+        rdb[j] = alpha;
+        betab[j] = nrm * (nrm + fabs(ajj));
+      }
+      __syncthreads();
+      const double bj = betab[j];
+      if (bj > 0)
+        for (int c = j + 1 + warp; c < NP; c += nw) {
+          double t = 0;
+          for (int i = j + lane; i < N; i += 32) t += Bm[(size_t)j * N + i] * Bm[(size_t)c * N + i];
+          t = warp_sum(t) / bj;
+          for (int i = j + lane; i < N; i += 32) Bm[(size_t)c * N + i] -= t * Bm[(size_t)j * N + i];
+        }
+      __syncthreads();
+    }
+    for (int c = warp; c < N; c += nw) {
+      double *w = Xs + (size_t)c * N;
+      for (int i = lane; i < N; i += 32) w[i] = i == c ? 1.0 : 0.0;
+      __syncwarp();
+      for (int j = 0; j < NP; ++j) {
+        const double bj = betab[j];
+        if (!(bj > 0)) continue;
+        double t = 0;
+        for (int i = j + lane; i < N; i += 32) t += Bm[(size_t)j * N + i] * w[i];
+        t = warp_sum(t) / bj;
+        for (int i = j + lane; i < N; i += 32) w[i] -= t * Bm[(size_t)j * N + i];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+      double *w = Xs + (size_t)c * N;
+      for (int r = NP - 1; r >= 0; --r) {
+        double s = w[r];
+        for (int k = r + 1; k < NP; ++k) s -= Bm[(size_t)k * N + r] * w[k];
+        w[r] = s / rdb[r];
+        PSd[r * N + c] = w[r];
+      }
+    }
+    __syncthreads();
+    // ---- P_Sg = P_D (Hm P_Sd); HP in the (now free) Fq space
+    double *HP = Fq;
+    for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
+      const int i = t / N, j = t % N;
+      double s = 0;
+      for (int c = 0; c < NP; ++c) s += Hm[(size_t)i * NP + c] * PSd[c * N + j];
+      HP[t] = s;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 4 * NP * N; t += blockDim.x) {
+      const int r = t / N, j = t % N;
+      double s = 0;
+      for (int i = 0; i < N; ++i) s += PD[r * N + i] * HP[(size_t)i * N + j];
+      PSg[t] = s;
+    }
+    if (threadIdx.x == 0 && status) {
+      double rmax = 0, rmin = 1e300, bmax = 0, bmin = 1e300;
+      for (int j = 0; j < NP; ++j) {
+        const qd d = qld(rd + 4 * j);
+        const double a = sqrt(d.s * d.s + d.x * d.x + d.y * d.y + d.z * d.z);
+        rmax = fmax(rmax, a); rmin = fmin(rmin, a);
+        bmax = fmax(bmax, fabs(rdb[j])); bmin = fmin(bmin, fabs(rdb[j]));
+      }
+      status[Pp] = (rmin <= 1e-13 * rmax || bmin <= 1e-13 * bmax) ? 1 : 0;
+    }
+    __syncthreads();
+  }
+}
+
 template <int P>
 constexpr int64_t fit_workspace_doubles() {
   using D = Dims<P>;

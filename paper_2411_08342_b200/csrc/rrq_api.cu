@@ -419,10 +419,15 @@ static rrq_status patch_fit_impl(rrq_ctx c, const rrq_surface *s, double *fit, i
   k_edge_tables<P><<<nblk(Pn * D::E, 128), 128, 0, st>>>(Pn, c->T.hc, fit);
   c->launches += 2;
   if ((r = cuda_check(c, "k_patch_geom/k_edge_tables"))) return r;
+  using FC = FitCfg<P>;
   int grid = (int)std::min<int64_t>(Pn, 2 * c->num_sms);
-  constexpr int64_t WS = fit_workspace_doubles<P>();
-  if (!ensure(c, c->fitwork, (size_t)grid * WS * sizeof(double))) return RRQ_ERR_CUDA;
-  k_patch_fit<P><<<grid, 256, 0, st>>>(Pn, s->nodes, s->normals, c->T.hc, fit, bp<double>(c->fitwork), status);
+  if (!ensure(c, c->fitwork, (size_t)grid * FC::WS * sizeof(double))) return RRQ_ERR_CUDA;
+  static bool fattr = false;
+  if (!fattr) {
+    cudaFuncSetAttribute(k_patch_fit_q<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM);
+    fattr = true;
+  }
+  k_patch_fit_q<P><<<grid, 256, FC::SMEM, st>>>(Pn, s->nodes, s->normals, c->T.hc, fit, bp<double>(c->fitwork), status);
   c->launches++;
   return cuda_check(c, "k_patch_fit");
 }
