@@ -738,7 +738,12 @@ struct ContractCfg {
   static constexpr int TP = P >= 10 ? 16 : 32, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 16;
   static constexpr int ZS = (D::NZS % 16 == 4) ? D::NZS : D::NZS + ((4 - D::NZS % 16) + 16) % 16;
   static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
-  static constexpr size_t SMEM = (size_t)TP * ZS * sizeof(double) + TP * 8 * sizeof(double) + TP * 16;
+  static constexpr int NB = (D::N % 16 == 8) ? D::N : D::N + ((8 - D::N % 16) + 16) % 16;   // B row stride
+  static constexpr int KC = (D::NP % 3 == 0) ? 12 : ((D::NP % 2 == 0) ? 8 : 4);            // k-rows per chunk
+  static constexpr int NCH = 4 * D::NP / KC;
+  static constexpr size_t SMEM_Z = (size_t)TP * ZS;
+  static constexpr size_t SMEM_B = 3 * (size_t)KC * NB;                                       // PD | PSp | PSg
+  static constexpr size_t SMEM = (SMEM_Z + 2 * SMEM_B + TP * 8) * sizeof(double) + TP * 16;
 };
 
 template <int P>
@@ -754,9 +759,10 @@ __global__ void __launch_bounds__(512, 1)
   using D = Dims<P>;
   using L = Layout<P>;
   using CC = ContractCfg<P>;
-  constexpr int N = D::N, NP = D::NP, TP = CC::TP, ZS = CC::ZS, NZS = D::NZS;
+  constexpr int N = D::N, NP = D::NP, TP = CC::TP, ZS = CC::ZS, NZS = D::NZS, NB = CC::NB, KC = CC::KC;
   extern __shared__ double sz[];
-  double *sT = sz + TP * ZS;                       // [TP][8] target x, nu'
+  double *sB = sz + CC::SMEM_Z;                    // [2][3][KC][NB]
+  double *sT = sB + 2 * CC::SMEM_B;                // [TP][8] target x, nu'
   int64_t *sK = reinterpret_cast<int64_t *>(sT + TP * 8);
   int *sSelf = reinterpret_cast<int *>(sK + TP);
   const int64_t item = item0 + blockIdx.x;
@@ -770,6 +776,19 @@ __global__ void __launch_bounds__(512, 1)
   const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *blk = fit + Pp * (int64_t)L::STRIDE;
+  const double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
+  // B chunk ch: rows [ch KC, (ch+1) KC) of P_D, P_Sp, P_Sg -> sB[(ch&1)][blk][row][NB] (cp.async, 16 B)
+  auto issue = [&](int ch) {
+    double *dst = sB + (ch & 1) * CC::SMEM_B;
+    const int per_row = N / 2, tot = 3 * KC * per_row;
+    for (int q = threadIdx.x; q < tot; q += blockDim.x) {
+      const int bk = q / (KC * per_row), rr = (q / per_row) % KC, cc = q % per_row;
+      const double *src = (bk == 0 ? PD : (bk == 1 ? PSp : PSg)) + (int64_t)(ch * KC + rr) * N + 2 * cc;
+      cp_async16(dst + (bk * KC + rr) * NB + 2 * cc, src);
+    }
+    cp_async_commit();
+  };
+  issue(0);
   for (int i = threadIdx.x; i < TP * NZS; i += blockDim.x) {
     const int r = i / NZS, c = i % NZS;
     sz[r * ZS + c] = r < cnt ? Zrow[(s0 + r - sA) * NZS + c] : 0.0;
@@ -792,38 +811,64 @@ __global__ void __launch_bounds__(512, 1)
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
   const double h = blk[L::HDR + H_H];
   const double inv4pi = 1.0 / (4.0 * kPi);
+  double acc[CC::TPW][8];
+#pragma unroll
+  for (int tw = 0; tw < CC::TPW; ++tw)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[tw][q] = 0.0;
+  // Theta . P_Sd (k over NP, straight from global; small)
+#pragma unroll
+  for (int tw = 0; tw < CC::TPW; ++tw) {
+    const int tile = warp + tw * CC::WARPS;
+    if (tile >= CC::TILES) break;
+    const int mt = tile % CC::MT, nt = tile / CC::MT, bn = nt * 8 + (lane >> 2);
+    const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3);
+    for (int k0 = 0; k0 < NP; k0 += 4) {
+      const int kk = k0 + (lane & 3);
+      const double bb = (bn < N && kk < NP) ? __ldg(PSd + kk * N + bn) : 0.0;
+      dmma(acc[tw][0], acc[tw][1], kk < NP ? zr[k0] : 0.0, bb);
+    }
+  }
+  // the 4 NP blocks, B double-buffered through shared memory
+  for (int ch = 0; ch < CC::NCH; ++ch) {
+    if (ch + 1 < CC::NCH) {
+      issue(ch + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double *bb = sB + (ch & 1) * CC::SMEM_B;
+#pragma unroll
+    for (int tw = 0; tw < CC::TPW; ++tw) {
+      const int tile = warp + tw * CC::WARPS;
+      if (tile >= CC::TILES) break;
+      const int mt = tile % CC::MT, nt = tile / CC::MT, bn = nt * 8 + (lane >> 2);
+      const bool bok = bn < N;
+      const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3) + ch * KC;
+#pragma unroll
+      for (int kk = 0; kk < KC; kk += 4) {
+        const int br = (kk + (lane & 3)) * NB + bn;
+        const double bd = bok ? bb[br] : 0.0, bsp = bok ? bb[KC * NB + br] : 0.0, bsg = bok ? bb[2 * KC * NB + br] : 0.0;
+        const double zw = zr[NP + kk], zdw = zr[5 * NP + kk], zs = zr[9 * NP + kk];
+        dmma(acc[tw][2], acc[tw][3], zw, bd);
+        dmma(acc[tw][6], acc[tw][7], zdw, bd);
+        dmma(acc[tw][4], acc[tw][5], zs, bsp);
+        dmma(acc[tw][0], acc[tw][1], zw, bsg);
+      }
+    }
+    __syncthreads();
+  }
 #pragma unroll 1
   for (int tw = 0; tw < CC::TPW; ++tw) {
     const int tile = warp + tw * CC::WARPS;
     if (tile >= CC::TILES) break;
     const int mt = tile % CC::MT, nt = tile / CC::MT;
-    const int bn = nt * 8 + (lane >> 2);           // B fragment column (node)
-    const bool bok = bn < N;
-    double aS0 = 0, aS1 = 0, aD0 = 0, aD1 = 0, aSp0 = 0, aSp1 = 0, aDp0 = 0, aDp1 = 0;
-    const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3);
-    // Theta . P_Sd  (k over NP, padded with zeros)
-    for (int k0 = 0; k0 < NP; k0 += 4) {
-      const int kk = k0 + (lane & 3);
-      const double b = (bok && kk < NP) ? __ldg(PSd + kk * N + bn) : 0.0;
-      const double a = kk < NP ? zr[k0] : 0.0;
-      dmma(aS0, aS1, a, b);
-    }
-    // the 4 NP blocks
-    for (int k0 = 0; k0 < 4 * NP; k0 += 4) {
-      const int kk = k0 + (lane & 3);
-      const double bd = bok ? __ldg(PD + kk * N + bn) : 0.0;
-      const double bsp = bok ? __ldg(PSp + kk * N + bn) : 0.0;
-      const double bsg = bok ? __ldg(PSg + kk * N + bn) : 0.0;
-      const double zw = zr[NP + k0], zdw = zr[5 * NP + k0], zs = zr[9 * NP + k0];
-      dmma(aD0, aD1, zw, bd);
-      dmma(aDp0, aDp1, zdw, bd);
-      dmma(aSp0, aSp1, zs, bsp);
-      dmma(aS0, aS1, zw, bsg);
-    }
-    // epilogue: C[row = lane/4][col = 2 (lane%4) + {0,1}]
+    const double aS0 = acc[tw][0], aS1 = acc[tw][1], aD0 = acc[tw][2], aD1 = acc[tw][3], aSp0 = acc[tw][4],
+                 aSp1 = acc[tw][5], aDp0 = acc[tw][6], aDp1 = acc[tw][7];
+  // epilogue: C[row = lane/4][col = 2 (lane%4) + {0,1}]
     const int row = mt * 8 + (lane >> 2);
     if (row >= cnt) continue;
     const double accS[2] = {aS0, aS1}, accD[2] = {aD0, aD1}, accSp[2] = {aSp0, aSp1}, accDp[2] = {aDp0, aDp1};
