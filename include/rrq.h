@@ -158,6 +158,10 @@ rrq_status rrq_reset_timing(rrq_ctx ctx);
  * c-layout.  At most max_pairs rows; returns the row count in *n_out. */
 rrq_status rrq_debug_zeta(rrq_ctx ctx, int64_t max_pairs, int64_t *perm, double *Z, int64_t *n_out);
 
+/* Profiling hook: SM cycles spent by k_pair_edge in each of its phases (harmonics, Newton + model
+ * integrals, weights, Omega_0 sinh rule, I[gamma]), summed over CTAs, into HOST out[8]; reset if set. */
+rrq_status rrq_debug_phase_cycles(rrq_ctx ctx, uint64_t out[8], int reset);
+
 #ifdef __cplusplus
 }
 #endif

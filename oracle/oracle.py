@@ -114,12 +114,13 @@ def model_integrals_direct(a, b, q):
     return I, J
 
 
-def find_t0(C, rp):
-    """C: [q,3] Legendre coefficients of an edge interpolant (reading A4'); rp target -> (t0, converged)."""
+def find_t0(C, rp, rho_stop=1e300):
+    """C: [q,3] Legendre coefficients of an edge interpolant (reading A4'); rp target -> (t0, converged).
+    rho_stop: early stop of reading A12' (default: never)."""
     C = _c(C, np.float64)
     re = ctypes.c_double(); im = ctypes.c_double()
-    conv = lib().orc_find_t0(_p(C), ctypes.c_int(C.shape[0]), _p(_c(rp, np.float64)), ctypes.byref(re),
-                             ctypes.byref(im))
+    conv = lib().orc_find_t0(_p(C), ctypes.c_int(C.shape[0]), _p(_c(rp, np.float64)), ctypes.c_double(rho_stop),
+                             ctypes.byref(re), ctypes.byref(im))
     return complex(re.value, im.value), bool(conv)
 
 

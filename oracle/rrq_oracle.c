@@ -593,9 +593,14 @@ static void edge_eval(const double *C, int q, cplx t, cplx *x, cplx *dx, cplx *d
   }
 }
 
+double orc_bernstein_rho(double re, double im);
+
 /* Reading A12: complex root t0 of sum_c (x_c(t) - r'_c)^2 = 0 (eq complexparameter).
- * Returns 1 if converged.  Im t0 >= 0. */
-int orc_find_t0(const double *C, int q, const double *rp, double *t0re, double *t0im) {
+ * Returns 1 if converged.  Im t0 >= 0.  Reading A12': the iteration also stops (as converged) once,
+ * after at least one complex step, the step is below 1e-3 |t| and rho(t) > rho_stop (= 2 rho0): the
+ * root is then certainly outside the swap ellipse, so the regime decision is already fixed and t0 is
+ * not used by the plain rule. */
+int orc_find_t0(const double *C, int q, const double *rp, double rho_stop, double *t0re, double *t0im) {
   cplx x[3], dx[3], ddx[3];
   /* chord projection */
   edge_eval(C, q, -1.0, x, dx, ddx);
@@ -639,6 +644,7 @@ int orc_find_t0(const double *C, int q, const double *rp, double *t0re, double *
     cplx dt = F / Fp;
     t -= dt;
     if (cabs(dt) < 1e-15 * (1.0 + cabs(t))) { conv = 1; break; }
+    if (it >= 1 && cabs(dt) < 1e-3 * cabs(t) && orc_bernstein_rho(creal(t), cimag(t)) > rho_stop) { conv = 1; break; }
   }
   if (cimag(t) < 0) t = conj(t);
   *t0re = creal(t);
@@ -726,7 +732,7 @@ static void edge_quadrature(const patch_t *P, const orc_params *pr, int e, const
   int q = P->q;
   const double *C = P->C + e * q * 3;
   double t0r, t0i;
-  int conv = orc_find_t0(C, q, rp, &t0r, &t0i);
+  int conv = orc_find_t0(C, q, rp, 2.0 * pr->rho0, &t0r, &t0i);
   E->t0re = t0r; E->t0im = t0i; E->conv = conv;
   E->swap = conv && (orc_bernstein_rho(t0r, t0i) < pr->rho0);
   double dn[64];

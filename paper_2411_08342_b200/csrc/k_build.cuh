@@ -61,6 +61,16 @@ __device__ __noinline__ void model_integrals(double a, double b, double *I, doub
   }
 }
 
+// Phase profiling of k_pair_edge (SM cycles between the CTA barriers, accumulated by thread 0 of each
+// CTA; read back with rrq_debug_phase_cycles).
+__device__ unsigned long long g_phase_cycles[8];
+#define RRQ_PHASE_MARK(ph)                                                         \
+  if (threadIdx.x == 0) {                                                          \
+    const long long now = clock64();                                               \
+    atomicAdd(&g_phase_cycles[ph], (unsigned long long)(now - ph_t));             \
+    ph_t = now;                                                                    \
+  }
+
 // Per-pair row of k_pair_edge's output for k_translate (doubles): S^{(l,m)}(r') and nu'.grad S for
 // m >= 0 (complex), the I[gamma] parts of W and dW ([4][NP], zeta sign convention NOT applied), the
 // S(r') Omega_0 part of Theta ([NP]), and nu' in the patch frame.
@@ -201,6 +211,7 @@ __global__ void __launch_bounds__(WPB * 32)
   // Phase-synchronous rounds: each warp takes one pair per round and all warps of the CTA step through
   // the phases together (__syncthreads between phases), so the SM's instruction working set is one
   // phase rather than the whole kernel (v1 was bound by instruction fetch, ncu "no instruction").
+  long long ph_t = clock64();
   for (int64_t base = sA + (int64_t)blockIdx.x * WPB; base < sB; base += (int64_t)gridDim.x * WPB) {
     const int64_t s = base + warp;
     const bool active = s < sB;
@@ -281,6 +292,7 @@ __global__ void __launch_bounds__(WPB * 32)
 
     }
     __syncthreads();
+    RRQ_PHASE_MARK(0);
     if (active) {
     // ---------------- Step 5: t0 per edge (reading A12), lanes (e, c) = (lane/3, lane%3)
     {
@@ -323,6 +335,8 @@ __global__ void __launch_bounds__(WPB * 32)
           cd dt = cdiv(F, Fp);
           tz = tz - dt;
           if (cabs_(dt) < 1e-15 * (1.0 + cabs_(tz))) conv = true;
+          else if (it >= 1 && cabs_(dt) < 1e-3 * cabs_(tz) && bernstein_rho(tz.x, tz.y) > 2.0 * rho0)
+            conv = true;   // reading A12': root certainly outside the swap ellipse
         }
         if (__all_sync(0xffffffffu, conv || lane >= 9)) break;
       }
@@ -367,6 +381,7 @@ __global__ void __launch_bounds__(WPB * 32)
 
     }
     __syncthreads();
+    RRQ_PHASE_MARK(1);
     if (active) {
     // ---------------- weights and the scalar line integrals (Step 6)
     for (int kap = lane; kap < E; kap += 32) {
@@ -406,6 +421,7 @@ __global__ void __launch_bounds__(WPB * 32)
     for (int i = 0; i < 8; ++i) om[i] = warp_sum(om[i]);
     }
     __syncthreads();
+    RRQ_PHASE_MARK(2);
     if (active) {
     // Omega_0 on swap edges: sinh-split Gauss-Legendre on the interpolated edge (reading A9)
     for (int e = 0; e < 3; ++e) {
@@ -434,6 +450,7 @@ __global__ void __launch_bounds__(WPB * 32)
 
     }
     __syncthreads();
+    RRQ_PHASE_MARK(3);
     if (active) {
     // ---------------- I[gamma]: (Omega_0, Omega)(0, grad S^{(l,m)}(r')), omega
     // first; its derivative.  W_gamma = -sqrt2 Im I[gamma], and the S(r') Omega_0 part of
@@ -466,6 +483,7 @@ __global__ void __launch_bounds__(WPB * 32)
     nswap += ws.swap[0] + ws.swap[1] + ws.swap[2];
     }
     __syncthreads();
+    RRQ_PHASE_MARK(4);
   }
   if (swapcnt && lane == 0 && nswap) atomicAdd(swapcnt, nswap);
 }

@@ -252,6 +252,17 @@ rrq_status rrq_debug_zeta(rrq_ctx c, int64_t max_pairs, int64_t *perm, double *Z
   return cuda_check(c, "rrq_debug_zeta");
 }
 
+rrq_status rrq_debug_phase_cycles(rrq_ctx c, uint64_t out[8], int reset) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  cudaDeviceSynchronize();
+  if (out) cudaMemcpyFromSymbol(out, g_phase_cycles, 8 * sizeof(uint64_t));
+  if (reset) {
+    uint64_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+  return cuda_check(c, "rrq_debug_phase_cycles");
+}
+
 rrq_status rrq_set_timing(rrq_ctx c, int enable) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   c->timing = enable != 0;
