@@ -87,17 +87,6 @@ struct QRow {
   static constexpr int Q = 0, DQ = D::NCQ, V = 2 * D::NCQ, STRIDE = (2 * D::NCQ + 2 * D::NV + 1) / 2 * 2;
 };
 
-template <int P>
-struct EdgeScratch {
-  using D = Dims<P>;
-  cd R[D::NS];        // R_l^m at (y', z', x'): S^{(l,m)}(r') for m >= 0
-  cd GS[D::NS][3];    // grad S^{(l,m)}(r')
-  cd HN[D::NS][3];    // Hess S^{(l,m)}(r') nu'
-  double I[3][D::Q], J[3][D::Q];
-  double t0[3][2];
-  double r13[2][kNDirect];
-  int swap[3], conv[3], direct[3];
-};
 
 // D = A B + C for one 8x8x4 fp64 tile (FP64 tensor core, SASS DMMA).  Fragments: a = A[lane/4][lane%4],
 // b = B[lane%4][lane/4], c/d = C[lane/4][2 (lane%4) + {0,1}].
@@ -168,6 +157,28 @@ __device__ __forceinline__ double tri_sum(double v, int base) {
   return a + b + c;
 }
 
+// Per-pair state of k_pair_edge (shared memory; one per pair of the CTA round).
+template <int P>
+struct PairState {
+  using D = Dims<P>;
+  cd R[D::NS];                 // R_l^m at (y', z', x'): S^{(l,m)}(r') for m >= 0
+  double I[3][D::Q], J[3][D::Q];
+  double t0[3][2];
+  double rp[3], nup[3], u3, om[8];
+  int64_t k, t;
+  int Pp, self_local, active, pad;
+  int swap[3], conv[3], direct[3];
+};
+// Per-warp scratch: gradient table and the direct-rule buffer.
+template <int P>
+struct WarpScr {
+  using D = Dims<P>;
+  cd GS[D::NS][3];
+  double r13[2][kNDirect];
+};
+
+constexpr int kPPW = 3;   // pairs per warp per round (the Newton phase packs 3 x 9 = 27 lanes)
+
 template <int P, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
     k_pair_edge(int64_t sA, int64_t sB, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt,
@@ -184,310 +195,325 @@ __global__ void __launch_bounds__(WPB * 32)
   double *sU = smem;                  // [Q][Q]
   double *stgl = sU + Q * Q, *swgl = stgl + Q;
   double *sxo = swgl + Q, *swo = sxo + n_omega;
-  double *ssqb = swo + n_omega;       // [(2P+1)][(2P+1)] sqrt binomials
-  double *sfac = ssqb + (2 * P + 1) * (2 * P + 1);  // [2P+2] factorials
-  constexpr int SQ = 2 * P + 1;
-  double *shc = sfac + (2 * P + 2);   // [HC_SIZE]
-  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + SQ * SQ + (2 * P + 2) + HC_SIZE;
+  double *shc = swo + n_omega;        // [HC_SIZE]
+  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + HC_SIZE;
   tab_doubles = (tab_doubles + 1) & ~1;
-  EdgeScratch<P> *wsall = reinterpret_cast<EdgeScratch<P> *>(smem + tab_doubles);
+  PairState<P> *pst = reinterpret_cast<PairState<P> *>(smem + tab_doubles);
+  WarpScr<P> *wscr = reinterpret_cast<WarpScr<P> *>(pst + WPB * kPPW);
   for (int i = threadIdx.x; i < HC_SIZE; i += blockDim.x) shc[i] = T.hc[i];
   for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) sU[i] = T.U[i];
   for (int i = threadIdx.x; i < Q; i += blockDim.x) { stgl[i] = T.tgl[i]; swgl[i] = T.wgl[i]; }
   for (int i = threadIdx.x; i < n_omega; i += blockDim.x) { sxo[i] = T.xo[i]; swo[i] = T.wo[i]; }
-  for (int i = threadIdx.x; i < SQ * SQ; i += blockDim.x) ssqb[i] = T.sqb[(i / SQ) * 41 + (i % SQ)];
-  if (threadIdx.x == 0) {
-    double f = 1;
-    sfac[0] = 1;
-    for (int i = 1; i < 2 * P + 2; ++i) { f *= i; sfac[i] = f; }
-  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  EdgeScratch<P> &ws = wsall[warp];
-  (void)ssqb; (void)sfac;
+  WarpScr<P> &wsc = wscr[warp];
+  PairState<P> *mine = pst + warp * kPPW;      // this warp's 3 pairs
   const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
   unsigned long long nswap = 0;
 
-  // Phase-synchronous rounds: each warp takes one pair per round and all warps of the CTA step through
-  // the phases together (__syncthreads between phases), so the SM's instruction working set is one
-  // phase rather than the whole kernel (v1 was bound by instruction fetch, ncu "no instruction").
+  // Phase-synchronous rounds of WPB * 3 pairs: all warps of the CTA step through the phases together
+  // (__syncthreads between phases), so the SM's instruction working set is one phase (v1 was bound by
+  // instruction fetch).  Phase 2 (Newton) packs the 3 pairs of a warp into 27 lanes.
   long long ph_t = clock64();
-  for (int64_t base = sA + (int64_t)blockIdx.x * WPB; base < sB; base += (int64_t)gridDim.x * WPB) {
-    const int64_t s = base + warp;
-    const bool active = s < sB;
-    int64_t k = 0, t = 0;
-    int Pp = 0;
-    double *X = Xrow, *Ar = Arow;
-    const double *blk = fit, *hd = fit;
-    double rp[3] = {0, 0, 0}, nup[3] = {0, 0, 0}, u[3] = {0, 0, 0};
-    int self_local = -1;
-    double om[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // Omega_0 Omega[3] dOmega_0 dOmega[3]
-    if (active) {
-    k = perm[s];
-    t = ptgt[k - kbase];
-    X = Xrow + (s - sA) * XR::STRIDE;
-    Ar = Arow + (s - sA) * 2 * K;
-    Pp = pair_patch[k];
-    blk = fit + (int64_t)Pp * L::STRIDE;
-    // ---------------- target in the patch frame (reading A2)
-    hd = blk + L::HDR;
-    {
-      double invh = 1.0 / hd[H_H];
-      double d[3] = {tx[3 * t] - hd[H_O], tx[3 * t + 1] - hd[H_O + 1], tx[3 * t + 2] - hd[H_O + 2]};
-      for (int r = 0; r < 3; ++r) rp[r] = (hd[H_RM + 3 * r] * d[0] + hd[H_RM + 3 * r + 1] * d[1] + hd[H_RM + 3 * r + 2] * d[2]) * invh;
-      if (tnorm) {
-        const double *nn = tnorm + 3 * t;
-        for (int r = 0; r < 3; ++r) nup[r] = hd[H_RM + 3 * r] * nn[0] + hd[H_RM + 3 * r + 1] * nn[1] + hd[H_RM + 3 * r + 2] * nn[2];
+  for (int64_t base = sA + (int64_t)blockIdx.x * WPB * kPPW; base < sB; base += (int64_t)gridDim.x * WPB * kPPW) {
+    // ---------------- phase 1: frame, gauge (A2, A8), harmonics at the target (Step 4)
+    for (int pp = 0; pp < kPPW; ++pp) {
+      PairState<P> &ps = mine[pp];
+      const int64_t s = base + warp * kPPW + pp;
+      const bool active = s < sB;
+      if (lane == 0) ps.active = active;
+      if (!active) continue;
+      const int64_t k = perm[s], t = ptgt[k - kbase];
+      const int Pp = pair_patch[k];
+      const double *hd = fit + (int64_t)Pp * L::STRIDE + L::HDR;
+      double rp[3], nup[3] = {0, 0, 0};
+      {
+        const double invh = 1.0 / hd[H_H];
+        const double d[3] = {tx[3 * t] - hd[H_O], tx[3 * t + 1] - hd[H_O + 1], tx[3 * t + 2] - hd[H_O + 2]};
+        for (int r = 0; r < 3; ++r) rp[r] = (hd[H_RM + 3 * r] * d[0] + hd[H_RM + 3 * r + 1] * d[1] + hd[H_RM + 3 * r + 2] * d[2]) * invh;
+        if (tnorm) {
+          const double *nn = tnorm + 3 * t;
+          for (int r = 0; r < 3; ++r) nup[r] = hd[H_RM + 3 * r] * nn[0] + hd[H_RM + 3 * r + 1] * nn[1] + hd[H_RM + 3 * r + 2] * nn[2];
+        }
       }
-    }
-    if (self_node) {
-      int64_t sn = self_node[t];
-      if (sn >= 0 && sn / D::N == Pp) self_local = (int)(sn % D::N);
-    }
-    const int sd = side ? (int)side[t] : 2;
-    // gauge sign (reading A8)
-    double sg;
-    {
-      double z = rp[2] - hd[H_VL + 2], zlo = hd[H_ZLO], zhi = hd[H_ZHI];
-      if (self_local >= 0) sg = -1.0;
-      else if (z > zhi + 0.1) sg = 1.0;
-      else if (z < zlo - 0.1) sg = -1.0;
-      else {
-        const double *va = hd + H_VL, *vb = hd + H_VL + 3, *vc = hd + H_VL + 6;
-        double det = (vb[0] - va[0]) * (vc[1] - va[1]) - (vc[0] - va[0]) * (vb[1] - va[1]);
-        double l1 = ((rp[0] - va[0]) * (vc[1] - va[1]) - (vc[0] - va[0]) * (rp[1] - va[1])) / det;
-        double l2 = ((vb[0] - va[0]) * (rp[1] - va[1]) - (rp[0] - va[0]) * (vb[1] - va[1])) / det;
-        double l0 = 1 - l1 - l2;
-        double mn = fmin(l0, fmin(l1, l2));
-        if (mn >= -0.25 && sd != 2) sg = sd > 0 ? 1.0 : -1.0;
-        else sg = (z - 0.5 * (zlo + zhi) > 0) ? 1.0 : -1.0;
+      int self_local = -1;
+      if (self_node) {
+        const int64_t sn = self_node[t];
+        if (sn >= 0 && sn / D::N == Pp) self_local = (int)(sn % D::N);
       }
-    }
-    u[2] = sg;
-
-    // ---------------- Step 4: harmonics at the target
-    if (lane <= P) r_column<P>(rp[1], rp[2], rp[0], lane, ws.R, shc);
-    __syncwarp();
-    for (int e = lane; e < NS; e += 32) {
-      int l = 0;
-      while (sidx(l + 1, 0) <= e) ++l;
-      const int m = e - sidx(l, 0);
-      cd g[3];
-      grad_fast(ws.R, l, m, shc, g);
-      cd ng = mk(0, 0);
-      for (int a = 0; a < 3; ++a) { ws.GS[e][a] = g[a]; ng = ng + nup[a] * g[a]; }
-      X[XR::R + 2 * e] = ws.R[e].x;
-      X[XR::R + 2 * e + 1] = ws.R[e].y;
-      X[XR::NG + 2 * e] = ng.x;
-      X[XR::NG + 2 * e + 1] = ng.y;
-    }
-    __syncwarp();
-    for (int e = lane; e < NS; e += 32) {   // Hess S nu' for m >= 1 (needed by d I[gamma])
-      int l = 0;
-      while (sidx(l + 1, 0) <= e) ++l;
-      const int m = e - sidx(l, 0);
-      if (m >= 1) hess_fast(ws.GS, l, m, nup, shc, ws.HN[e]);
-    }
-    if (lane < 3) X[XR::NU + lane] = nup[lane];
-
+      const int sd = side ? (int)side[t] : 2;
+      double sg;
+      {
+        const double z = rp[2] - hd[H_VL + 2], zlo = hd[H_ZLO], zhi = hd[H_ZHI];
+        if (self_local >= 0) sg = -1.0;
+        else if (z > zhi + 0.1) sg = 1.0;
+        else if (z < zlo - 0.1) sg = -1.0;
+        else {
+          const double *va = hd + H_VL, *vb = hd + H_VL + 3, *vc = hd + H_VL + 6;
+          const double det = (vb[0] - va[0]) * (vc[1] - va[1]) - (vc[0] - va[0]) * (vb[1] - va[1]);
+          const double l1 = ((rp[0] - va[0]) * (vc[1] - va[1]) - (vc[0] - va[0]) * (rp[1] - va[1])) / det;
+          const double l2 = ((vb[0] - va[0]) * (rp[1] - va[1]) - (rp[0] - va[0]) * (vb[1] - va[1])) / det;
+          const double l0 = 1 - l1 - l2;
+          const double mn = fmin(l0, fmin(l1, l2));
+          if (mn >= -0.25 && sd != 2) sg = sd > 0 ? 1.0 : -1.0;
+          else sg = (z - 0.5 * (zlo + zhi) > 0) ? 1.0 : -1.0;
+        }
+      }
+      if (lane == 0) {
+        ps.k = k; ps.t = t; ps.Pp = Pp; ps.self_local = self_local; ps.u3 = sg;
+        for (int a = 0; a < 3; ++a) { ps.rp[a] = rp[a]; ps.nup[a] = nup[a]; }
+      }
+      if (lane <= P) r_column<P>(rp[1], rp[2], rp[0], lane, ps.R, shc);
+      __syncwarp();
+      double *X = Xrow + (s - sA) * XR::STRIDE;
+      for (int e = lane; e < NS; e += 32) {
+        int l = 0;
+        while (sidx(l + 1, 0) <= e) ++l;
+        const int m = e - sidx(l, 0);
+        cd g[3];
+        grad_fast(ps.R, l, m, shc, g);
+        const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2];
+        X[XR::R + 2 * e] = ps.R[e].x;
+        X[XR::R + 2 * e + 1] = ps.R[e].y;
+        X[XR::NG + 2 * e] = ng.x;
+        X[XR::NG + 2 * e + 1] = ng.y;
+      }
+      if (lane < 3) X[XR::NU + lane] = nup[lane];
+      __syncwarp();
     }
     __syncthreads();
     RRQ_PHASE_MARK(0);
-    if (active) {
-    // ---------------- Step 5: t0 per edge (reading A12), lanes (e, c) = (lane/3, lane%3)
+    // ---------------- phase 2: t0 per edge (reading A12, A12'), lanes (pair, edge, comp) = 27 lanes
     {
-      const int e = lane < 9 ? lane / 3 : 2, c = lane < 9 ? lane % 3 : 2, base = 3 * e;
-      const double *C = blk + L::CM + e * Q * 3;
-      const double rc = rp[c];
+      const int L27 = lane < 27 ? lane : 26, pp = L27 / 9, e = (L27 % 9) / 3, c = L27 % 3, base3 = 9 * pp + 3 * e;
+      PairState<P> &ps = mine[pp];
+      const bool act = ps.active;
+      const double *C = fit + (int64_t)(act ? ps.Pp : 0) * L::STRIDE + L::CM + e * Q * 3;
+      const double rc = act ? ps.rp[c] : 0.0;
       double Cl[Q];
 #pragma unroll
-      for (int q = 0; q < Q; ++q) Cl[q] = C[q * 3 + c];
-      auto horner_r = [&](double tt, double &v, double &d1, double &d2) { leg_r<Q>(Cl, tt, v, d1, d2); };
-      // x(-1) = sum_j (-1)^j C_j, x(1) = sum_j C_j  (P_j(+-1) = (+-1)^j)
+      for (int q = 0; q < Q; ++q) Cl[q] = act ? C[q * 3 + c] : 0.0;
       double v = 0, A = 0;
 #pragma unroll
       for (int q = 0; q < Q; ++q) { v += Cl[q]; A += (q & 1) ? -Cl[q] : Cl[q]; }
       double d1, d2;
-      double ab = v - A, ar = rc - A;
-      double tc = -1.0 + 2.0 * tri_sum(ar * ab, base) / tri_sum(ab * ab, base);
+      const double ab = v - A, ar = rc - A;
+      const double abab = tri_sum(ab * ab, base3);
+      double tc = -1.0 + 2.0 * tri_sum(ar * ab, base3) / (abab > 0 ? abab : 1.0);
       bool go = true;
       for (int it = 0; it < 3; ++it) {
-        horner_r(tc, v, d1, d2);
-        double xr = v - rc;
-        double g = tri_sum(xr * d1, base), gp = tri_sum(d1 * d1 + xr * d2, base);
+        leg_r<Q>(Cl, tc, v, d1, d2);
+        const double xr = v - rc;
+        const double g = tri_sum(xr * d1, base3), gp = tri_sum(d1 * d1 + xr * d2, base3);
         go = go && (gp > 0);
         if (go) tc -= g / gp;
       }
-      horner_r(tc, v, d1, d2);
-      double xr = v - rc;
-      double f = tri_sum(xr * xr, base), dd = tri_sum(d1 * d1 + xr * d2, base), xp2 = tri_sum(d1 * d1, base);
+      leg_r<Q>(Cl, tc, v, d1, d2);
+      const double xr = v - rc;
+      const double f = tri_sum(xr * xr, base3), xp2 = tri_sum(d1 * d1, base3);
+      double dd = tri_sum(d1 * d1 + xr * d2, base3);
       if (!(dd > 0)) dd = xp2;
-      cd tz = mk(tc, sqrt(f / dd));
-      bool conv = false;
+      cd tz = mk(tc, sqrt(f / (dd > 0 ? dd : 1.0)));
+      bool conv = !act;
       for (int it = 0; it < 20; ++it) {
         cd xv, xd;
         leg_c<Q>(Cl, tz, xv, xd);
-        cd xrr = xv - mk(rc, 0);
-        cd sq = xrr * xrr, pr = xrr * xd;
-        cd F = mk(tri_sum(sq.x, base), tri_sum(sq.y, base));
-        cd Fp = 2.0 * mk(tri_sum(pr.x, base), tri_sum(pr.y, base));
+        const cd xrr = xv - mk(rc, 0);
+        const cd sq = xrr * xrr, pr = xrr * xd;
+        const cd F = mk(tri_sum(sq.x, base3), tri_sum(sq.y, base3));
+        const cd Fp = 2.0 * mk(tri_sum(pr.x, base3), tri_sum(pr.y, base3));
         if (!conv) {
-          cd dt = cdiv(F, Fp);
+          const cd dt = cdiv(F, Fp);
           tz = tz - dt;
           if (cabs_(dt) < 1e-15 * (1.0 + cabs_(tz))) conv = true;
           else if (it >= 1 && cabs_(dt) < 1e-3 * cabs_(tz) && bernstein_rho(tz.x, tz.y) > 2.0 * rho0)
             conv = true;   // reading A12': root certainly outside the swap ellipse
         }
-        if (__all_sync(0xffffffffu, conv || lane >= 9)) break;
+        if (__all_sync(0xffffffffu, conv || lane >= 27)) break;
       }
       if (tz.y < 0) tz.y = -tz.y;
       conv = conv && isfinite(tz.x) && isfinite(tz.y);
-      if (lane < 9 && c == 0) {
-        ws.t0[e][0] = tz.x;
-        ws.t0[e][1] = tz.y;
-        ws.conv[e] = conv;
-        double rho = bernstein_rho(tz.x, tz.y);
-        ws.swap[e] = conv && rho < rho0;
-        ws.direct[e] = rho >= kRhoDirect;
+      if (lane < 27 && c == 0 && act) {
+        ps.t0[e][0] = tz.x;
+        ps.t0[e][1] = tz.y;
+        ps.conv[e] = conv;
+        const double rho = bernstein_rho(tz.x, tz.y);
+        ps.swap[e] = conv && rho < rho0;
+        ps.direct[e] = rho >= kRhoDirect;
       }
     }
     __syncwarp();
-    // model integrals (reading A11 / A11'): recurrences inside rho = 1.6, a 48-point rule outside
-    if (lane < 3 && ws.swap[lane] && !ws.direct[lane])
-      model_integrals<Q>(ws.t0[lane][0], fabs(ws.t0[lane][1]), ws.I[lane], ws.J[lane]);
-    for (int e = 0; e < 3; ++e) {
-      if (!(ws.swap[e] && ws.direct[e])) continue;
-      const double a = ws.t0[e][0], b = fabs(ws.t0[e][1]);
+    // model integrals (reading A11 / A11'): recurrences inside rho = 1.6 (lanes (pair, edge)), a 48-point
+    // rule outside
+    if (lane < 9) {
+      PairState<P> &ps = mine[lane / 3];
+      const int e = lane % 3;
+      if (ps.active && ps.swap[e] && !ps.direct[e]) model_integrals<Q>(ps.t0[e][0], fabs(ps.t0[e][1]), ps.I[e], ps.J[e]);
+    }
+    for (int pe = 0; pe < 9; ++pe) {
+      PairState<P> &ps = mine[pe / 3];
+      const int e = pe % 3;
+      if (!(ps.active && ps.swap[e] && ps.direct[e])) continue;
+      const double a = ps.t0[e][0], b = fabs(ps.t0[e][1]);
       for (int j = lane; j < kNDirect; j += 32) {
-        double xj = T.xd[j], Qv = (xj - a) * (xj - a) + b * b;
-        double r1 = T.wd[j] / sqrt(Qv);
-        ws.r13[0][j] = r1;
-        ws.r13[1][j] = r1 / Qv;
+        const double xj = T.xd[j], Qv = (xj - a) * (xj - a) + b * b;
+        const double r1 = T.wd[j] / sqrt(Qv);
+        wsc.r13[0][j] = r1;
+        wsc.r13[1][j] = r1 / Qv;
       }
       __syncwarp();
       if (lane < Q) {
         double si = 0, sj = 0;
         for (int j = 0; j < kNDirect; ++j) {
-          double pw = __ldg(T.xdp + j * Q + lane);
-          si = fma(pw, ws.r13[0][j], si);
-          sj = fma(pw, ws.r13[1][j], sj);
+          const double pw = __ldg(T.xdp + j * Q + lane);
+          si = fma(pw, wsc.r13[0][j], si);
+          sj = fma(pw, wsc.r13[1][j], sj);
         }
-        ws.I[e][lane] = si;
-        ws.J[e][lane] = sj;
+        ps.I[e][lane] = si;
+        ps.J[e][lane] = sj;
       }
       __syncwarp();
     }
-    __syncwarp();
-
-    }
     __syncthreads();
     RRQ_PHASE_MARK(1);
-    if (active) {
-    // ---------------- weights and the scalar line integrals (Step 6)
-    for (int kap = lane; kap < E; kap += 32) {
-      const int e = kap / Q, kk = kap % Q;
-      const double *y = blk + L::YL + 3 * kap, *tau = blk + L::TL + 3 * kap;
-      double d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
-      double dn = sqrt(dot3(d, d));
-      double w1, w3;
-      if (ws.swap[e]) {
-        double mu1 = 0, mu3 = 0;
-        for (int c = 0; c < Q; ++c) {
-          mu1 = fma(ws.I[e][c], sU[c * Q + kk], mu1);
-          mu3 = fma(ws.J[e][c], sU[c * Q + kk], mu3);
+    // ---------------- phase 3: weights and the scalar line integrals (Step 6)
+    for (int pp = 0; pp < kPPW; ++pp) {
+      PairState<P> &ps = mine[pp];
+      if (!ps.active) continue;
+      const int64_t s = base + warp * kPPW + pp;
+      const double *blk = fit + (int64_t)ps.Pp * L::STRIDE;
+      double *Ar = Arow + (s - sA) * 2 * K;
+      const double rp[3] = {ps.rp[0], ps.rp[1], ps.rp[2]}, nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
+      const double u[3] = {0.0, 0.0, ps.u3};
+      double om[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // Omega_0(plain) Omega[3] dOmega_0 dOmega[3]
+      for (int kap = lane; kap < E; kap += 32) {
+        const int e = kap / Q, kk = kap % Q;
+        const double *y = blk + L::YL + 3 * kap, *tau = blk + L::TL + 3 * kap;
+        const double d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
+        const double dn = sqrt(dot3(d, d));
+        double w1, w3;
+        if (ps.swap[e]) {
+          double mu1 = 0, mu3 = 0;
+#pragma unroll 4
+          for (int c = 0; c < Q; ++c) {
+            mu1 = fma(ps.I[e][c], sU[c * Q + kk], mu1);
+            mu3 = fma(ps.J[e][c], sU[c * Q + kk], mu3);
+          }
+          const double ta = stgl[kk] - ps.t0[e][0], tb = ps.t0[e][1];
+          const double r1 = sqrt(ta * ta + tb * tb) / dn;
+          w1 = mu1 * r1;
+          w3 = mu3 * r1 * r1 * r1;
+        } else {
+          const double idn = 1.0 / dn;
+          w1 = swgl[kk] * idn;
+          w3 = w1 * idn * idn;
+          double dxu[3];
+          cross3(d, u, dxu);
+          om[0] += swgl[kk] * (-dot3(dxu, tau) / (dn * (dn + dot3(u, d))));
         }
-        double ta = stgl[kk] - ws.t0[e][0], tb = ws.t0[e][1];
-        double r1 = sqrt(ta * ta + tb * tb) / dn;
-        w1 = mu1 * r1;
-        w3 = mu3 * r1 * r1 * r1;
-      } else {
-        w1 = swgl[kk] / dn;
-        w3 = swgl[kk] / (dn * dn * dn);
-        double dxu[3];
-        cross3(d, u, dxu);
-        om[0] += swgl[kk] * (-dot3(dxu, tau) / (dn * (dn + dot3(u, d))));
+        const double nd = dot3(nup, d);
+        double txd[3];
+        cross3(tau, d, txd);
+        for (int a = 0; a < 3; ++a) {
+          Ar[3 * kap + a] = w1 * d[a];                        // GEMM row a (k = 3 kappa + axis)
+          Ar[K + 3 * kap + a] = w1 * nup[a] - w3 * nd * d[a];  // GEMM row b
+          om[1 + a] -= w1 * tau[a];
+          om[5 + a] += w3 * nd * tau[a];
+        }
+        om[4] += w3 * dot3(nup, txd);
       }
-      double nd = dot3(nup, d);
-      double txd[3];
-      cross3(tau, d, txd);
-      for (int a = 0; a < 3; ++a) {
-        Ar[3 * kap + a] = w1 * d[a];                       // GEMM row a (k = 3 kappa + axis)
-        Ar[K + 3 * kap + a] = w1 * nup[a] - w3 * nd * d[a]; // GEMM row b
-        om[1 + a] -= w1 * tau[a];
-        om[5 + a] += w3 * nd * tau[a];
-      }
-      om[4] += w3 * dot3(nup, txd);
-    }
-    for (int i = 0; i < 8; ++i) om[i] = warp_sum(om[i]);
+      for (int i = 0; i < 8; ++i) om[i] = warp_sum(om[i]);
+      if (lane == 0)
+        for (int i = 0; i < 8; ++i) ps.om[i] = om[i];
     }
     __syncthreads();
     RRQ_PHASE_MARK(2);
-    if (active) {
-    // Omega_0 on swap edges: sinh-split Gauss-Legendre on the interpolated edge (reading A9)
-    for (int e = 0; e < 3; ++e) {
-      if (!ws.swap[e]) continue;
-      double a = fmin(1.0, fmax(-1.0, ws.t0[e][0])), b = fabs(ws.t0[e][1]);
-      double sR = asinh((1 - a) / b), sL = asinh((-1 - a) / b);
-      const double *C = blk + L::CM + e * Q * 3;
-      double acc = 0;
-      for (int j = lane; j < 2 * n_omega; j += 32) {
-        int sdd = j / n_omega, jj = j % n_omega;
-        double lo = sdd ? 0.0 : sL, hi = sdd ? sR : 0.0;
-        if (!(hi > lo)) continue;
-        double sv = lo + (hi - lo) * (sxo[jj] + 1) * 0.5, W = (hi - lo) * 0.5 * swo[jj];
-        double tt = a + b * sinh(sv), dt = b * cosh(sv);
-        double x[3], dx[3];
-        leg_r3<Q>(C, tt, x, dx);
-        double d[3] = {rp[0] - x[0], rp[1] - x[1], rp[2] - x[2]};
-        double nd = sqrt(dot3(d, d)), dxu[3];
-        cross3(d, u, dxu);
-        acc += W * dt * (-dot3(dxu, dx) / (nd * (nd + dot3(u, d))));
+    // ---------------- phase 4: Omega_0 on swap edges: sinh-split Gauss-Legendre (reading A9)
+    for (int pp = 0; pp < kPPW; ++pp) {
+      PairState<P> &ps = mine[pp];
+      if (!ps.active) continue;
+      const double *blk = fit + (int64_t)ps.Pp * L::STRIDE;
+      const double rp[3] = {ps.rp[0], ps.rp[1], ps.rp[2]};
+      const double u[3] = {0.0, 0.0, ps.u3};
+      double add = 0;
+      for (int e = 0; e < 3; ++e) {
+        if (!ps.swap[e]) continue;
+        const double a = fmin(1.0, fmax(-1.0, ps.t0[e][0])), b = fabs(ps.t0[e][1]);
+        const double sR = asinh((1 - a) / b), sL = asinh((-1 - a) / b);
+        const double *C = blk + L::CM + e * Q * 3;
+        double acc = 0;
+        for (int j = lane; j < 2 * n_omega; j += 32) {
+          const int sdd = j / n_omega, jj = j % n_omega;
+          const double lo = sdd ? 0.0 : sL, hi = sdd ? sR : 0.0;
+          if (!(hi > lo)) continue;
+          const double sv = lo + (hi - lo) * (sxo[jj] + 1) * 0.5, W = (hi - lo) * 0.5 * swo[jj];
+          const double ex = exp(sv), iex = 1.0 / ex;
+          const double tt = a + b * 0.5 * (ex - iex), dt = b * 0.5 * (ex + iex);
+          double x[3], dx[3];
+          leg_r3<Q>(C, tt, x, dx);
+          const double d[3] = {rp[0] - x[0], rp[1] - x[1], rp[2] - x[2]};
+          const double nd = sqrt(dot3(d, d));
+          double dxu[3];
+          cross3(d, u, dxu);
+          acc += W * dt * (-dot3(dxu, dx) / (nd * (nd + dot3(u, d))));
+        }
+        add += warp_sum(acc);
       }
-      om[0] += warp_sum(acc);
-    }
-    if (self_local >= 0) om[0] -= 2.0 * kPi;   // principal value (reading A7)
-    __syncwarp();
-
+      if (lane == 0) ps.om[0] += add - (ps.self_local >= 0 ? 2.0 * kPi : 0.0);   // PV shift (reading A7)
     }
     __syncthreads();
     RRQ_PHASE_MARK(3);
-    if (active) {
-    // ---------------- I[gamma]: (Omega_0, Omega)(0, grad S^{(l,m)}(r')), omega
-    // first; its derivative.  W_gamma = -sqrt2 Im I[gamma], and the S(r') Omega_0 part of
-    // Theta (G2); k_translate adds the lambda_1 / theta_1 parts.
-    for (int c = lane; c < NP; c += 32) {
-      int l = 1;
-      while (lmidx(l + 1, 1) <= c) ++l;
-      const int m = c - lmidx(l, 1) + 1, hs = sidx(l, m);
-      const cd *g = ws.GS[hs], *hn = ws.HN[hs];
-      const double O0 = om[0], Ov[3] = {om[1], om[2], om[3]}, dO0 = om[4], dOv[3] = {om[5], om[6], om[7]};
-      double gs = 0, dgs = 0, gv[3], dgv[3];
-      for (int a = 0; a < 3; ++a) {
-        gs -= Ov[a] * g[a].y;
-        dgs -= dOv[a] * g[a].y + Ov[a] * hn[a].y;
-        const int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
-        gv[a] = O0 * g[a].y + (Ov[b1] * g[b2].y - Ov[b2] * g[b1].y);
-        dgv[a] = dO0 * g[a].y + (dOv[b1] * g[b2].y - dOv[b2] * g[b1].y) + O0 * hn[a].y +
-                 (Ov[b1] * hn[b2].y - Ov[b2] * hn[b1].y);
+    // ---------------- phase 5: I[gamma]: (Omega_0, Omega)(0, grad S(r')), omega
+    // first; its nu'-derivative with Hess S nu'; W_gamma = -sqrt2 Im I[gamma]; the
+    // S(r') Omega_0 part of Theta (G2).  k_translate adds the lambda_1 / theta_1 parts.
+    for (int pp = 0; pp < kPPW; ++pp) {
+      PairState<P> &ps = mine[pp];
+      if (!ps.active) continue;
+      const int64_t s = base + warp * kPPW + pp;
+      double *X = Xrow + (s - sA) * XR::STRIDE;
+      for (int e = lane; e < NS; e += 32) {
+        int l = 0;
+        while (sidx(l + 1, 0) <= e) ++l;
+        grad_fast(ps.R, l, e - sidx(l, 0), shc, wsc.GS[e]);
       }
-      const double f = -s2 * inv4pi;
-      X[XR::W + c] = f * gs;
-      X[XR::DW + c] = f * dgs;
-      for (int a = 0; a < 3; ++a) {
-        X[XR::W + (1 + a) * NP + c] = f * gv[a];
-        X[XR::DW + (1 + a) * NP + c] = f * dgv[a];
+      __syncwarp();
+      const double nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
+      const double O0 = ps.om[0], Ov[3] = {ps.om[1], ps.om[2], ps.om[3]}, dO0 = ps.om[4],
+                   dOv[3] = {ps.om[5], ps.om[6], ps.om[7]};
+      for (int c = lane; c < NP; c += 32) {
+        int l = 1;
+        while (lmidx(l + 1, 1) <= c) ++l;
+        const int m = c - lmidx(l, 1) + 1, hs = sidx(l, m);
+        const cd *g = wsc.GS[hs];
+        cd hn[3];
+        hess_fast(wsc.GS, l, m, nup, shc, hn);
+        double gs = 0, dgs = 0, gv[3], dgv[3];
+        for (int a = 0; a < 3; ++a) {
+          gs -= Ov[a] * g[a].y;
+          dgs -= dOv[a] * g[a].y + Ov[a] * hn[a].y;
+          const int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
+          gv[a] = O0 * g[a].y + (Ov[b1] * g[b2].y - Ov[b2] * g[b1].y);
+          dgv[a] = dO0 * g[a].y + (dOv[b1] * g[b2].y - dOv[b2] * g[b1].y) + O0 * hn[a].y +
+                   (Ov[b1] * hn[b2].y - Ov[b2] * hn[b1].y);
+        }
+        const double f = -s2 * inv4pi;
+        X[XR::W + c] = f * gs;
+        X[XR::DW + c] = f * dgs;
+        for (int a = 0; a < 3; ++a) {
+          X[XR::W + (1 + a) * NP + c] = f * gv[a];
+          X[XR::DW + (1 + a) * NP + c] = f * dgv[a];
+        }
+        X[XR::TH + c] = s2 * inv4pi * ps.R[hs].y * O0;
       }
-      X[XR::TH + c] = s2 * inv4pi * ws.R[hs].y * O0;
-    }
-    if (lane == 0 && pstat) pstat[k - obase] = (ws.conv[0] && ws.conv[1] && ws.conv[2]) ? 0 : 1;
-    nswap += ws.swap[0] + ws.swap[1] + ws.swap[2];
+      if (lane == 0 && pstat) pstat[ps.k - obase] = (ps.conv[0] && ps.conv[1] && ps.conv[2]) ? 0 : 1;
+      nswap += ps.swap[0] + ps.swap[1] + ps.swap[2];
+      __syncwarp();
     }
     __syncthreads();
     RRQ_PHASE_MARK(4);
   }
   if (swapcnt && lane == 0 && nswap) atomicAdd(swapcnt, nswap);
 }
-
 
 // ------------------------------------------------------------------------------------------------
 // k_qmap: line-integral maps (Step 6) as a DMMA GEMM per tile of TP pairs

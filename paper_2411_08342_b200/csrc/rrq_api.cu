@@ -463,9 +463,9 @@ constexpr int kWPB = 8;   // warps per CTA of k_pair_edge
 template <int P>
 static size_t edge_smem(int n_omega) {
   using D = Dims<P>;
-  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + (2 * P + 1) * (2 * P + 1) + (2 * P + 2) + HC_SIZE;
+  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + HC_SIZE;
   tab = (tab + 1) & ~1;
-  return (size_t)tab * sizeof(double) + kWPB * sizeof(EdgeScratch<P>);
+  return (size_t)tab * sizeof(double) + kWPB * kPPW * sizeof(PairState<P>) + kWPB * sizeof(WarpScr<P>);
 }
 template <int P>
 static size_t translate_smem() {
@@ -559,7 +559,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     const int64_t np_ = sB - sA;
     {
       TScope t1(c, 2, st);
-      unsigned grid = (unsigned)std::min<int64_t>((np_ + kWPB - 1) / kWPB, (int64_t)c->num_sms * 4);
+      unsigned grid = (unsigned)std::min<int64_t>((np_ + kWPB * kPPW - 1) / (kWPB * kPPW), (int64_t)c->num_sms * 4);
       k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), st>>>(
           sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
           tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, bp<double>(c->Arow), bp<double>(c->Xrow),
