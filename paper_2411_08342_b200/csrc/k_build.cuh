@@ -524,10 +524,11 @@ __global__ void __launch_bounds__(WPB * 32)
 template <int P>
 struct QmapCfg {
   using D = Dims<P>;
-  static constexpr int TP = P >= 10 ? 16 : 32, ROWS = 2 * TP, MT = ROWS / 8, WARPS = 16, NSPLIT = WARPS / MT;
+  static constexpr int TP = P >= 10 ? 16 : 32, ROWS = 2 * TP, WARPS = 16;
+  static constexpr int PG = TP / 8, NSPLIT = WARPS / PG;       // pair groups of 8; N splits per group
   static constexpr int KA = (D::K % 16 == 4) ? D::K : D::K + ((4 - D::K % 16) + 16) % 16;
-  static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8;
-  static constexpr int NTW = (NTALL + NSPLIT - 1) / NSPLIT;   // max N-tiles per warp
+  static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8, NTV = NTALL - NTQ;
+  static constexpr int NTQW = (NTQ + NSPLIT - 1) / NSPLIT, NTVW = (NTV + NSPLIT - 1) / NSPLIT;
   static constexpr int KC = 12, NCH = D::K / KC;              // B staged in chunks of KC k-rows
   static_assert(D::K % KC == 0, "K must be a multiple of the B chunk");
   static constexpr size_t SMEM_A = (size_t)ROWS * KA * sizeof(double);
@@ -579,13 +580,16 @@ __global__ void __launch_bounds__(512, 1)
     sA_[r * KA + k] = pr < cnt ? Arow[(s0 + pr - sA) * 2 * K + ab * K + k] : 0.0;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int mt = warp % C::MT, ns = warp / C::MT;
-  const bool brows = mt >= C::MT / 2;
-  const int ntiles = brows ? C::NTQ : C::NTALL;
-  double acc[C::NTW][2];
+  // warp = (pair group pg, N split ns): the a-row and b-row tiles of the same 8 pairs share every Q-column
+  // B fragment (2 DMMA per load); the V columns are needed for the a rows only.
+  const int pg = warp % C::PG, ns = warp / C::PG;
+  double accA[C::NTQW][2], accB[C::NTQW][2], accV[C::NTVW][2];
 #pragma unroll
-  for (int t = 0; t < C::NTW; ++t) acc[t][0] = acc[t][1] = 0.0;
-  const double *arow = sA_ + (mt * 8 + (lane >> 2)) * KA + (lane & 3);
+  for (int t = 0; t < C::NTQW; ++t) accA[t][0] = accA[t][1] = accB[t][0] = accB[t][1] = 0.0;
+#pragma unroll
+  for (int t = 0; t < C::NTVW; ++t) accV[t][0] = accV[t][1] = 0.0;
+  const double *arow = sA_ + (pg * 8 + (lane >> 2)) * KA + (lane & 3);
+  const double *brow = arow + TP * KA;
   const int bofs = (lane & 3) * NCS + (lane >> 2);
   for (int ch = 0; ch < C::NCH; ++ch) {
     if (ch + 1 < C::NCH) {
@@ -598,37 +602,46 @@ __global__ void __launch_bounds__(512, 1)
     const double *bb = sB + (ch & 1) * KC * NCS + bofs;
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
-      const double a = arow[ch * KC + kk];
+      const double a = arow[ch * KC + kk], b = brow[ch * KC + kk];
       const double *bk = bb + kk * NCS;
 #pragma unroll
-      for (int t = 0; t < C::NTW; ++t) {
+      for (int t = 0; t < C::NTQW; ++t) {
         const int nt = ns + t * C::NSPLIT;
-        if (nt < ntiles) dmma(acc[t][0], acc[t][1], a, bk[nt * 8]);
+        if (nt < C::NTQ) {
+          const double bq = bk[nt * 8];
+          dmma(accA[t][0], accA[t][1], a, bq);
+          dmma(accB[t][0], accB[t][1], b, bq);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < C::NTVW; ++t) {
+        const int nt = C::NTQ + ns + t * C::NSPLIT;
+        if (nt < C::NTALL) dmma(accV[t][0], accV[t][1], a, bk[nt * 8]);
       }
     }
     __syncthreads();
   }
   // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]
-  const int row = mt * 8 + (lane >> 2), pr = row % TP;
+  const int pr = pg * 8 + (lane >> 2);
   if (pr < cnt) {
     double *out = Qrow + (s0 + pr - sA) * QR::STRIDE;
 #pragma unroll
-    for (int t = 0; t < C::NTW; ++t) {
+    for (int t = 0; t < C::NTQW; ++t) {
       const int nt = ns + t * C::NSPLIT;
-      if (nt >= ntiles) continue;
+      if (nt >= C::NTQ) continue;
       const int col = nt * 8 + 2 * (lane & 3);
-      if (!brows) {
-        if (col < D::NCQ) {
-          out[QR::Q + col] = acc[t][0];
-          out[QR::Q + col + 1] = acc[t][1];
-        } else if (col - D::NCQ < 2 * D::NV) {
-          out[QR::V + col - D::NCQ] = acc[t][0];
-          if (col + 1 - D::NCQ < 2 * D::NV) out[QR::V + col + 1 - D::NCQ] = acc[t][1];
-        }
-      } else {
-        out[QR::DQ + col] = acc[t][0];
-        out[QR::DQ + col + 1] = acc[t][1];
-      }
+      out[QR::Q + col] = accA[t][0];
+      out[QR::Q + col + 1] = accA[t][1];
+      out[QR::DQ + col] = accB[t][0];
+      out[QR::DQ + col + 1] = accB[t][1];
+    }
+#pragma unroll
+    for (int t = 0; t < C::NTVW; ++t) {
+      const int nt = C::NTQ + ns + t * C::NSPLIT;
+      if (nt >= C::NTALL) continue;
+      const int col = nt * 8 + 2 * (lane & 3) - D::NCQ;
+      if (col < 2 * D::NV) out[QR::V + col] = accV[t][0];
+      if (col + 1 < 2 * D::NV) out[QR::V + col + 1] = accV[t][1];
     }
   }
 }
