@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(256)
 template <int P>
 struct ContractCfg {
   using D = Dims<P>;
-  static constexpr int TP = P >= 10 ? 16 : 32, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 16;
+  static constexpr int TP = 16, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 8;
   static constexpr int ZS = (D::NZS % 16 == 4) ? D::NZS : D::NZS + ((4 - D::NZS % 16) + 16) % 16;
   static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
   static constexpr int NB = (D::N % 16 == 8) ? D::N : D::N + ((8 - D::N % 16) + 16) % 16;   // B row stride
@@ -804,7 +804,7 @@ struct ContractCfg {
 };
 
 template <int P>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(256, 2)
     k_contract(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, int64_t n_patches,
                const int64_t *__restrict__ seg_ptr, int64_t sA, const int64_t *__restrict__ perm,
                const int64_t *__restrict__ ptgt, int64_t kbase, const double *__restrict__ fit,
@@ -879,7 +879,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
   for (int tw = 0; tw < CC::TPW; ++tw) {
     const int tile = warp + tw * CC::WARPS;
-    if (tile >= CC::TILES) break;
+    if (tile >= CC::TILES) continue;
     const int mt = tile % CC::MT, nt = tile / CC::MT, bn = nt * 8 + (lane >> 2);
     const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3);
     for (int k0 = 0; k0 < NP; k0 += 4) {
@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int tw = 0; tw < CC::TPW; ++tw) {
       const int tile = warp + tw * CC::WARPS;
-      if (tile >= CC::TILES) break;
+      if (tile >= CC::TILES) continue;
       const int mt = tile % CC::MT, nt = tile / CC::MT, bn = nt * 8 + (lane >> 2);
       const bool bok = bn < N;
       const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3) + ch * KC;
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 1
   for (int tw = 0; tw < CC::TPW; ++tw) {
     const int tile = warp + tw * CC::WARPS;
-    if (tile >= CC::TILES) break;
+    if (tile >= CC::TILES) continue;
     const int mt = tile % CC::MT, nt = tile / CC::MT;
     const double aS0 = acc[tw][0], aS1 = acc[tw][1], aD0 = acc[tw][2], aD1 = acc[tw][3], aSp0 = acc[tw][4],
                  aSp1 = acc[tw][5], aDp0 = acc[tw][6], aDp1 = acc[tw][7];
