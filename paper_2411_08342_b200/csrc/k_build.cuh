@@ -71,22 +71,63 @@ __device__ unsigned long long g_phase_cycles[8];
     ph_t = now;                                                                    \
   }
 
-// Per-pair row of k_pair_edge's output for k_translate (doubles): S^{(l,m)}(r') and nu'.grad S for
-// m >= 0 (complex), the I[gamma] parts of W and dW ([4][NP], zeta sign convention NOT applied), the
-// S(r') Omega_0 part of Theta ([NP]), and nu' in the patch frame.
+// Per-pair row of k_pair_edge's output for k_translate (doubles): the translation operands
+// S'^{(l',m')} = w(l',m') S^{(l',m')}(r') and NG' = w(l',m') nu'.grad S^{(l',m')} for l' < p, all m' (expanded
+// over m' < 0 by S^{(l,-m)} = (-1)^m conj S^{(l,m)}), stored per (l',m') at l'^2 + l' + m' as
+// (S'.y, S'.x, NG'.y, NG'.x); the I[gamma] parts of W and dW ([4][NP], zeta sign convention NOT applied);
+// the S(r') Omega_0 part of Theta ([NP]); nu' in the patch frame.
 template <int P>
 struct XRow {
   using D = Dims<P>;
-  static constexpr int R = 0, NG = 2 * D::NS, W = 4 * D::NS, DW = W + 4 * D::NP, TH = DW + 4 * D::NP,
-                       NU = TH + D::NP, STRIDE = (NU + 3 + 1) / 2 * 2;
+  static constexpr int SX = 0, W = 4 * P * P, DW = W + 4 * D::NP, TH = DW + 4 * D::NP, NU = TH + D::NP,
+                       G = W, GSZ = (9 * D::NP + 3 + 1) / 2 * 2, STRIDE = G + GSZ;
 };
-// Per-pair row of k_qmap's output: [Q (8 NQ) | dQ (8 NQ) | V (2 NV)] in the column convention of M.
+// Per-pair row of k_qmap's output: per (j, k >= 0), 2 <= j <= p, at EG qidx(j,k): [Q (4 quaternion comps,
+// re/im) | dQ (same)] scaled by v_lambda(j,k); then V [2 NV] scaled by v_theta(j,k) (TrCfg).  k_translate
+// stages the entries at stride EQ = 18 (144 B: 8 consecutive entries start in 8 different 16-B bank groups).
 template <int P>
 struct QRow {
   using D = Dims<P>;
-  static constexpr int Q = 0, DQ = D::NCQ, V = 2 * D::NCQ, STRIDE = (2 * D::NCQ + 2 * D::NV + 1) / 2 * 2;
+  static constexpr int EG = 16, EQ = 18;
+  static constexpr int V = EG * D::NQ, STRIDE = V + 2 * D::NV;
+  static constexpr int SV = EQ * D::NQ, SSZ = SV + 2 * D::NV;   // staged (shared-memory) layout
 };
 
+// k_translate's schedule (see k_translate): the j >= 2 translation terms of all c = (l, m).
+__host__ __device__ constexpr int tr_nterms(int P) {
+  int n = 0;
+  for (int l = 2; l <= P; ++l)
+    for (int m = 1; m <= l; ++m)
+      for (int j = 2; j <= l; ++j) {
+        const int lj = l - j;
+        const int kmin = (-j > m - lj) ? -j : m - lj, kmax = (j < m + lj) ? j : m + lj;
+        n += kmax - kmin + 1;
+      }
+  return n;
+}
+
+template <int P>
+struct TrCfg {
+  using D = Dims<P>;
+  static constexpr int NT = tr_nterms(P), STEPS = (NT + 31) / 32;
+  static constexpr int MAXSLOT = D::NP + 32, SLOTW = 9;
+  static constexpr int SXW = 6;                                  // smem (S'.y, S'.x, NG'.y, NG'.x | pad): 48 B
+  static constexpr int SXSZ = SXW * (P * P + 1);                 // + one zero entry for padding terms
+  static constexpr int QSZ = QRow<P>::SSZ, GSZ = XRow<P>::GSZ;
+  static constexpr int PER_WARP = (2 * QSZ + 2 * SXSZ + GSZ + SLOTW * MAXSLOT + 1) / 2 * 2;
+  // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 cinfo [NP] |
+  // f64 vlam [NQ], vth [NV], wS [P*P], olam [NP], oth [NP]
+  static constexpr int NWORD = STEPS * 32 + D::NP, TABW = (NWORD + 1) / 2;
+  static constexpr int VLAM = TABW, VTH = VLAM + D::NQ, WS = VTH + D::NV, OLAM = WS + P * P, OTH = OLAM + D::NP;
+  static constexpr int TAB_D = (OTH + D::NP + 1) / 2 * 2;
+  static constexpr int SMEM_MAX = 224 * 1024;
+  static constexpr int WPB_FIT = (SMEM_MAX / 8 - TAB_D) / PER_WARP;
+  static constexpr int WPB = WPB_FIT > 8 ? 8 : WPB_FIT;
+  static constexpr size_t SMEM = (size_t)(TAB_D + WPB * PER_WARP) * sizeof(double);
+  static constexpr uint32_t FA = 1u << 14, FB = 1u << 15, FLUSH = 1u << 16;   // code bits
+  static_assert(WPB >= 2, "translate smem");
+  static_assert(MAXSLOT < 2048 && D::NQ < 128 && P * P < 128, "translate code fields");
+};
 
 // D = A B + C for one 8x8x4 fp64 tile (FP64 tensor core, SASS DMMA).  Fragments: a = A[lane/4][lane%4],
 // b = B[lane%4][lane/4], c/d = C[lane/4][2 (lane%4) + {0,1}].
@@ -186,8 +227,9 @@ __global__ void __launch_bounds__(WPB * 32)
                 const double *__restrict__ tx, const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
                 const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Arow,
                 double *__restrict__ Xrow, int32_t *__restrict__ pstat, int64_t obase,
-                unsigned long long *__restrict__ swapcnt) {
+                unsigned long long *__restrict__ swapcnt, const double *__restrict__ trtab) {
   using D = Dims<P>;
+  const double *wS = trtab + TrCfg<P>::WS;
   using L = Layout<P>;
   using XR = XRow<P>;
   constexpr int Q = D::Q, E = D::E, NP = D::NP, NS = D::NS, K = D::K;
@@ -266,17 +308,27 @@ __global__ void __launch_bounds__(WPB * 32)
       if (lane <= P) r_column<P>(rp[1], rp[2], rp[0], lane, ps.R, shc);
       __syncwarp();
       double *X = Xrow + (s - sA) * XR::STRIDE;
-      for (int e = lane; e < NS; e += 32) {
+      for (int e = lane; e < sidx(P, 0); e += 32) {   // l' < p: the translation operands (XRow)
         int l = 0;
         while (sidx(l + 1, 0) <= e) ++l;
         const int m = e - sidx(l, 0);
         cd g[3];
         grad_fast(ps.R, l, m, shc, g);
-        const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2];
-        X[XR::R + 2 * e] = ps.R[e].x;
-        X[XR::R + 2 * e + 1] = ps.R[e].y;
-        X[XR::NG + 2 * e] = ng.x;
-        X[XR::NG + 2 * e + 1] = ng.y;
+        const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2], r = ps.R[e];
+        const double w = __ldg(wS + l * l + l + m);
+        double *o = X + XR::SX + 4 * (l * l + l + m);
+        o[0] = w * r.y;
+        o[1] = w * r.x;
+        o[2] = w * ng.y;
+        o[3] = w * ng.x;
+        if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
+          const double sg = (m & 1) ? -w : w;
+          o = X + XR::SX + 4 * (l * l + l - m);
+          o[0] = -sg * r.y;
+          o[1] = sg * r.x;
+          o[2] = -sg * ng.y;
+          o[3] = sg * ng.x;
+        }
       }
       if (lane < 3) X[XR::NU + lane] = nup[lane];
       __syncwarp();
@@ -548,7 +600,7 @@ template <int P>
 __global__ void __launch_bounds__(512, 1)
     k_qmap(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, int64_t n_patches,
            const int64_t *__restrict__ seg_ptr, int64_t sA, const double *__restrict__ fit,
-           const double *__restrict__ Arow, double *__restrict__ Qrow) {
+           const double *__restrict__ Arow, double *__restrict__ Qrow, const double *__restrict__ trtab) {
   using D = Dims<P>;
   using L = Layout<P>;
   using C = QmapCfg<P>;
@@ -629,19 +681,23 @@ __global__ void __launch_bounds__(512, 1)
     for (int t = 0; t < C::NTQW; ++t) {
       const int nt = ns + t * C::NSPLIT;
       if (nt >= C::NTQ) continue;
-      const int col = nt * 8 + 2 * (lane & 3);
-      out[QR::Q + col] = accA[t][0];
-      out[QR::Q + col + 1] = accA[t][1];
-      out[QR::DQ + col] = accB[t][0];
-      out[QR::DQ + col + 1] = accB[t][1];
+      const double sc = __ldg(trtab + TrCfg<P>::VLAM + nt);   // column block nt = entry qidx(j,k)
+      double *o = out + QR::EG * nt + 2 * (lane & 3);
+      o[0] = sc * accA[t][0];
+      o[1] = sc * accA[t][1];
+      o[8] = sc * accB[t][0];
+      o[9] = sc * accB[t][1];
     }
 #pragma unroll
     for (int t = 0; t < C::NTVW; ++t) {
       const int nt = C::NTQ + ns + t * C::NSPLIT;
       if (nt >= C::NTALL) continue;
       const int col = nt * 8 + 2 * (lane & 3) - D::NCQ;
-      if (col < 2 * D::NV) out[QR::V + col] = accV[t][0];
-      if (col + 1 < 2 * D::NV) out[QR::V + col + 1] = accV[t][1];
+      if (col < 2 * D::NV) {
+        const double sc = __ldg(trtab + TrCfg<P>::VTH + (col >> 1));
+        out[QR::V + col] = sc * accV[t][0];
+        out[QR::V + col + 1] = sc * accV[t][1];
+      }
     }
   }
 }
@@ -650,119 +706,151 @@ __global__ void __launch_bounds__(512, 1)
 // k_translate: Step 7 (P:L1263-1268 eq cdlp1dintegral): for each (l,m),
 // lambda_1, its nu'-derivative and theta_1 from Q^{(j,k)}, dQ^{(j,k)}, V^{(j,k)} and S(r'), plus the
 // gamma parts from k_pair_edge -> W, dW, Theta -> zeta = (Theta, zeta(W), zeta(dW), zeta_S).
-// One warp per pair; the pair's rows are staged in shared memory; lanes take (l,m) in a cost-balanced
-// order (heaviest first, the lightest four doubled up).
+//
+// The translation is a 2-D convolution  out(l,m) = sum_{j,k} c(l,m,j,k) A^{(j,k)} S^{(l-j,m-k)}  whose
+// coefficient factors as u(l,m) v(j,k) w(l-j,m-k) (T = F(l,m)/(F(j,k) F(l',m')), F(a,b) = sqrt((a+b)!(a-b)!),
+// and the factorial ratios of C_j, D_j split the same way).  k_qmap stores A = v A and k_pair_edge stores
+// S' = w S (expanded over m' < 0), so the inner loop is pure FMAs on the Im parts (only Im(lambda),
+// Im(theta) enter W, dW, Theta): Im(A S) = A.x S.y + A.y S.x, with A^{(j,-k)} = (-1)^k conj A^{(j,k)} folded
+// into sign flips of (S.y, S.x).
+// One warp per pair.  The j >= 2 terms (c-major) are split into 32 contiguous equal runs, one per lane
+// (host-built schedule, make_trtab in rrq_api.cu, ordered within each c to spread shared-memory banks), so
+// every lane executes the same STEPS steps; a c's partial sums are flushed to a slot where the lane's run
+// of that c ends, and the epilogue (lanes over c) sums a c's slots, adds the j = 1 theta terms and the
+// gamma parts and writes zeta.  Rows are prefetched with cp.async one pair ahead.
 // ------------------------------------------------------------------------------------------------
-template <int P>
-struct TransCfg {
-  using D = Dims<P>;
-  static constexpr int WPB = 8;
-  static constexpr int PER_WARP = XRow<P>::STRIDE + QRow<P>::STRIDE;
+__device__ __forceinline__ double flip_if(double x, uint32_t bit) {
+  return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)bit << 63));
+}
+
+struct TrOps {
+  double2 s, g, v, q[4], dq[4];
+  uint32_t cw;
 };
 
 template <int P>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     k_translate(int64_t sA, int64_t sB, const double *__restrict__ Xrow, const double *__restrict__ Qrow,
-                const double *__restrict__ sqb_g, double *__restrict__ Zrow) {
+                const double *__restrict__ trtab, double *__restrict__ Zrow) {
   using D = Dims<P>;
+  using C = TrCfg<P>;
   using XR = XRow<P>;
   using QR = QRow<P>;
-  constexpr int NP = D::NP, NZS = D::NZS, SQ = 2 * P + 1, WPB = TransCfg<P>::WPB;
-  extern __shared__ double sm[];
-  double *ssqb = sm;                         // [SQ][SQ]
-  double *sfac = ssqb + SQ * SQ;             // [2P+2]
-  int *order = reinterpret_cast<int *>(sfac + 2 * P + 2);   // [NP] cost-balanced task order
-  double *wsb = sfac + 2 * P + 2 + (NP + 1) / 2 + 1;
-  for (int i = threadIdx.x; i < SQ * SQ; i += blockDim.x) ssqb[i] = sqb_g[(i / SQ) * 41 + (i % SQ)];
-  if (threadIdx.x == 0) {
-    double f = 1;
-    sfac[0] = 1;
-    for (int i = 1; i < 2 * P + 2; ++i) { f *= i; sfac[i] = f; }
-    // cost of (l,m) ~ number of (j,k) terms; sort descending (selection sort, NP <= 55)
-    int cost[64];
-    for (int c = 0; c < NP; ++c) {
-      int l = 1;
-      while (lmidx(l + 1, 1) <= c) ++l;
-      const int m = c - lmidx(l, 1) + 1;
-      int n = 0;
-      for (int j = 1; j <= l; ++j) n += min(j, m + l - j) - max(-j, m - (l - j)) + 1;
-      cost[c] = n;
-      order[c] = c;
-    }
-    for (int i = 0; i < NP; ++i)
-      for (int j = i + 1; j < NP; ++j)
-        if (cost[order[j]] > cost[order[i]]) { int t = order[i]; order[i] = order[j]; order[j] = t; }
-    // tasks beyond 32 go to the lanes holding the lightest of the first 32 (reverse them)
-    if (NP > 32) {
-      int extra = NP - 32;
-      for (int i = 0; i < extra / 2; ++i) { int t = order[32 + i]; order[32 + i] = order[NP - 1 - i]; order[NP - 1 - i] = t; }
-    }
-  }
-  __syncthreads();
+  constexpr int NP = D::NP, NZS = D::NZS, WPB = C::WPB, EQ = QR::EQ, SXW = C::SXW;
+  extern __shared__ __align__(16) double sm[];
+  for (int i = threadIdx.x; i < C::TAB_D; i += blockDim.x) sm[i] = trtab[i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double *X = wsb + warp * TransCfg<P>::PER_WARP;
-  double *Qv = X + XR::STRIDE;
+  double *wb = sm + C::TAB_D + (size_t)warp * C::PER_WARP;
+  double *QB = wb, *SXB = QB + 2 * C::QSZ, *GB = SXB + 2 * C::SXSZ, *SL = GB + C::GSZ;
+  if (lane < 2 * SXW) SXB[(lane / SXW) * C::SXSZ + SXW * P * P + lane % SXW] = 0.0;   // zero entries
+  __syncthreads();
+  const uint32_t *code = reinterpret_cast<const uint32_t *>(sm);
+  const uint32_t *cinfo = code + C::STEPS * 32;
+  const double *olam = sm + C::OLAM, *oth = sm + C::OTH;
+  const int64_t stride = (int64_t)gridDim.x * WPB;
+
+  auto issue_qs = [&](int64_t s, int b) {   // Q row (linear) and the S'/NG' block (stride 4 -> SXW)
+    const double *qg = Qrow + (s - sA) * QR::STRIDE, *xg = Xrow + (s - sA) * XR::STRIDE + XR::SX;
+    double *qd = QB + b * C::QSZ, *sd = SXB + b * C::SXSZ;
+    for (int i = lane; i < 8 * D::NQ; i += 32) cp_async16(qd + EQ * (i >> 3) + 2 * (i & 7), qg + 2 * i);
+    for (int i = lane; i < D::NV; i += 32) cp_async16(qd + QR::SV + 2 * i, qg + QR::V + 2 * i);
+    for (int i = lane; i < 2 * P * P; i += 32) cp_async16(sd + SXW * (i >> 1) + 2 * (i & 1), xg + 2 * i);
+  };
+  auto issue_g = [&](int64_t s) {
+    const double *xg = Xrow + (s - sA) * XR::STRIDE + XR::G;
+    for (int i = lane; i < C::GSZ / 2; i += 32) cp_async16(GB + 2 * i, xg + 2 * i);
+  };
+
   const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
-  for (int64_t s = sA + (int64_t)blockIdx.x * WPB + warp; s < sB; s += (int64_t)gridDim.x * WPB) {
-    const double *xg = Xrow + (s - sA) * XR::STRIDE, *qg = Qrow + (s - sA) * QR::STRIDE;
-    for (int i = lane; i < XR::STRIDE; i += 32) X[i] = xg[i];
-    for (int i = lane; i < QR::STRIDE; i += 32) Qv[i] = qg[i];
+  int64_t s = sA + (int64_t)blockIdx.x * WPB + warp;
+  if (s < sB) {
+    issue_qs(s, 0);
+    issue_g(s);
+  }
+  cp_async_commit();
+  for (int it = 0; s < sB; s += stride, ++it) {
+    const int cb = it & 1;
+    if (s + stride < sB) issue_qs(s + stride, cb ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncwarp();
-    const cd *Rt = reinterpret_cast<const cd *>(X + XR::R), *NGt = reinterpret_cast<const cd *>(X + XR::NG);
-    const double nup[3] = {X[XR::NU], X[XR::NU + 1], X[XR::NU + 2]};
-    double *Z = Zrow + (s - sA) * NZS;
-    for (int ti = lane; ti < NP; ti += 32) {
-      const int c = order[ti];
-      int l = 1;
-      while (lmidx(l + 1, 1) <= c) ++l;
-      const int m = c - lmidx(l, 1) + 1;
-      cq lam = qzero(), dlam = qzero();
-      cd th = mk(0, 0);
-      for (int j = 1; j <= l; ++j) {
-        const int lj = l - j;
-        const int kmin = max(-j, m - lj), kmax = min(j, m + lj);
-        const double Dj = sfac[j - 1] * sfac[lj] / sfac[l];
-        const double Cj = j >= 2 ? sfac[j - 2] * sfac[lj] / sfac[l - 1] : 0.0;
-        for (int kk = kmin; kk <= kmax; ++kk) {
-          const double Tc = ssqb[(l + m) * SQ + (j + kk)] * ssqb[(l - m) * SQ + (j - kk)];
-          const int mk_ = m - kk;
-          const cd Sv = rget(Rt, lj, mk_);
-          cd NGv;
-          if (mk_ >= 0) NGv = NGt[sidx(lj, mk_)];
-          else NGv = (((-mk_) & 1) ? -1.0 : 1.0) * conj(NGt[sidx(lj, -mk_)]);
-          const int ak = kk < 0 ? -kk : kk;
-          const double sgn = (kk < 0 && (ak & 1)) ? -1.0 : 1.0;
-          const double cjs = kk < 0 ? -sgn : sgn;   // sign applied to the imaginary part
-          {  // theta_1: D_{j,l} T V^{(j,k)} S^{(l-j,m-k)}
-            const double *vv = Qv + QR::V + 2 * vidx(j, ak);
-            cfma(th, (Dj * Tc) * mk(sgn * vv[0], cjs * vv[1]), Sv);
-          }
-          if (j >= 2) {
-            const double cT = Cj * Tc;
-            const double *qv = Qv + QR::Q + 8 * qidx(j, ak), *dq = Qv + QR::DQ + 8 * qidx(j, ak);
-            const cd cS = cT * Sv, cN = cT * NGv;
+    const double *qb = QB + cb * C::QSZ, *sx = SXB + cb * C::SXSZ;
+    // main loop, software-pipelined one step ahead
+    auto load = [&](TrOps &o, uint32_t cw) {
+      o.cw = cw;
+      const int qe = cw & 127, se = (cw >> 7) & 127;
+      o.s = *reinterpret_cast<const double2 *>(sx + SXW * se);
+      o.g = *reinterpret_cast<const double2 *>(sx + SXW * se + 2);
+      o.v = *reinterpret_cast<const double2 *>(qb + QR::SV + 2 * (qe + 2));   // vidx(j,k) = qidx(j,k) + 2
+      const double *e = qb + EQ * qe;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-              const cd qb = mk(sgn * qv[2 * b], cjs * qv[2 * b + 1]);
-              const cd dqb = mk(sgn * dq[2 * b], cjs * dq[2 * b + 1]);
-              cd &L1 = b == 0 ? lam.s : lam.v[b - 1];
-              cd &L2 = b == 0 ? dlam.s : dlam.v[b - 1];
-              cfma(L1, qb, cS);
-              cfma(L2, dqb, cS);
-              cfma(L2, qb, cN);
-            }
-          }
+      for (int b = 0; b < 4; ++b) {
+        o.q[b] = *reinterpret_cast<const double2 *>(e + 2 * b);
+        o.dq[b] = *reinterpret_cast<const double2 *>(e + 8 + 2 * b);
+      }
+    };
+    double th = 0, lam[4] = {0, 0, 0, 0}, dla[4] = {0, 0, 0, 0}, dlb[4] = {0, 0, 0, 0};
+    TrOps cur, nxt;
+    load(cur, code[lane]);
+#pragma unroll 2
+    for (int t = 0; t < C::STEPS; ++t) {
+      if (t + 1 < C::STEPS) load(nxt, code[(t + 1) * 32 + lane]);
+      const uint32_t cw = cur.cw, fa = (cw >> 14) & 1, fb = (cw >> 15) & 1;
+      const double A = flip_if(cur.s.x, fa), B = flip_if(cur.s.y, fb);
+      const double An = flip_if(cur.g.x, fa), Bn = flip_if(cur.g.y, fb);
+      th = fma(cur.v.x, A, fma(cur.v.y, B, th));
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        lam[b] = fma(cur.q[b].x, A, fma(cur.q[b].y, B, lam[b]));
+        dla[b] = fma(cur.dq[b].x, A, fma(cur.dq[b].y, B, dla[b]));
+        dlb[b] = fma(cur.q[b].x, An, fma(cur.q[b].y, Bn, dlb[b]));
+      }
+      if (cw & C::FLUSH) {
+        double *d = SL + C::SLOTW * (cw >> 20);
+        d[0] = th;
+        th = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          d[1 + b] = lam[b];
+          d[5 + b] = dla[b] + dlb[b];
+          lam[b] = dla[b] = dlb[b] = 0;
         }
       }
-      const double f = -s2 * inv4pi;
-      double W[4], dW[4];
-      W[0] = f * lam.s.y + X[XR::W + c];
-      dW[0] = f * dlam.s.y + X[XR::DW + c];
-      for (int a = 0; a < 3; ++a) {
-        W[1 + a] = f * lam.v[a].y + X[XR::W + (1 + a) * NP + c];
-        dW[1 + a] = f * dlam.v[a].y + X[XR::DW + (1 + a) * NP + c];
+      cur = nxt;
+    }
+    __syncwarp();
+    // epilogue: lanes over c = (l, m); gamma parts from GB (W [4][NP], dW [4][NP], Theta [NP], nu')
+    const double nup[3] = {GB[9 * NP], GB[9 * NP + 1], GB[9 * NP + 2]};
+    double *Z = Zrow + (s - sA) * NZS;
+    for (int c = lane; c < NP; c += 32) {
+      const uint32_t ci = cinfo[c];
+      const int l = ci & 15, m = (ci >> 4) & 15, sb = (ci >> 8) & 2047, sc = ci >> 19;
+      double T = 0, L[4] = {0, 0, 0, 0}, DL[4] = {0, 0, 0, 0};
+      for (int q = 0; q < sc; ++q) {
+        const double *d = SL + C::SLOTW * (sb + q);
+        T += d[0];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          L[b] += d[1 + b];
+          DL[b] += d[5 + b];
+        }
       }
-      const double Th = s2 * inv4pi * th.y + X[XR::TH + c];
+      // j = 1 theta terms (no lambda part: C_1 = 0)
+      const int kmin = max(-1, m - (l - 1)), kmax = min(1, m + (l - 1));
+      for (int k = kmin; k <= kmax; ++k) {
+        const int lp = l - 1, se = lp * lp + lp + m - k;
+        const double *vv = qb + QR::SV + 2 * vidx(1, k < 0 ? -k : k);
+        const double A = k < 0 ? -sx[SXW * se] : sx[SXW * se], B = sx[SXW * se + 1];
+        T = fma(vv[0], A, fma(vv[1], B, T));
+      }
+      const double fo = -s2 * inv4pi * olam[c];
+      double W[4], dW[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        W[a] = fo * L[a] + GB[a * NP + c];
+        dW[a] = fo * DL[a] + GB[4 * NP + a * NP + c];
+      }
+      const double Th = s2 * inv4pi * oth[c] * T + GB[8 * NP + c];
       // zeta vectors (Step 8, App. A.7; reading G3 for S')
       double nxW[3];
       cross3(nup, W + 1, nxW);
@@ -780,7 +868,10 @@ __global__ void __launch_bounds__(256)
     }
     for (int i = D::NZ + lane; i < NZS; i += 32) Z[i] = 0.0;
     __syncwarp();
+    if (s + stride < sB) issue_g(s + stride);
+    cp_async_commit();
   }
+  cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -27,6 +27,7 @@ struct rrq_ctx_s {
   int num_sms = 148;
   // constant tables (device) + host copies
   double *d_tab = nullptr;
+  double *d_trtab = nullptr;   // k_translate schedule + scale tables (TrCfg<p>)
   Tables T;
   std::vector<double> h_t, h_w, h_U;
   // scratch
@@ -128,6 +129,118 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 
 // Exported functions get C linkage from their declarations in include/rrq.h.
 
+// k_translate's host-built table (TrCfg<P>): the j >= 2 translation terms of every c = (l, m) in c-major
+// order, split into 32 contiguous runs of equal length (one per lane), each term encoded as
+// qidx(j,|k|) | (l'^2 + l' + m') << 7 | sign flips of (S.y, S.x) for k < 0 | flush | slot << 20 (padding
+// terms point at the zero S' entry p^2); cinfo[c] = l | m << 4 | first slot << 8 | slot count << 19; and the
+// separable scale factors v_lambda(j,k) = (j-2)!/F(j,k), v_theta(j,k) = (j-1)!/F(j,k), w(l',m') = l'!/F(l',m'),
+// u_lambda(l,m) = F(l,m)/(l-1)!, u_theta(l,m) = F(l,m)/l!, F(a,b) = sqrt((a+b)! (a-b)!).
+// Within a run the order of terms is free; it is chosen greedily so that, at each step, the 8 lanes of a
+// quarter-warp read Q entries (16-B bank group qidx mod 8) and S' entries (3 se mod 8) in distinct groups.
+template <int P>
+static std::vector<double> make_trtab() {
+  using C = TrCfg<P>;
+  using D = Dims<P>;
+  struct Term { int c, l, m, j, k, qe, se; };
+  std::vector<Term> terms;
+  for (int l = 2; l <= P; ++l)
+    for (int m = 1; m <= l; ++m)
+      for (int j = 2; j <= l; ++j) {
+        const int lj = l - j;
+        for (int k = std::max(-j, m - lj); k <= std::min(j, m + lj); ++k)
+          terms.push_back({lmidx(l, m), l, m, j, k, qidx(j, std::abs(k)), lj * lj + lj + m - k});
+      }
+  const int NT = (int)terms.size();
+  std::vector<int> beg(33);
+  for (int L = 0; L <= 32; ++L) beg[L] = L * (NT / 32) + std::min(L, NT % 32);
+  // runs (lane, c) -> slots numbered in (c, lane) order so a c's slots are contiguous
+  struct Run { int c, lane, first, last; };
+  std::vector<Run> runs;
+  for (int L = 0; L < 32; ++L) {
+    int f = beg[L];
+    for (int i = beg[L]; i < beg[L + 1]; ++i)
+      if (i + 1 == beg[L + 1] || terms[i + 1].c != terms[i].c) {
+        runs.push_back({terms[i].c, L, f, i});
+        f = i + 1;
+      }
+  }
+  std::stable_sort(runs.begin(), runs.end(), [](const Run &a, const Run &b) { return a.c < b.c; });
+  std::vector<int> slot_of(NT, -1), run_of(NT, -1), sbeg(D::NP, 0), scnt(D::NP, 0);
+  for (int r = 0; r < (int)runs.size(); ++r) {
+    slot_of[runs[r].last] = r;
+    for (int i = runs[r].first; i <= runs[r].last; ++i) run_of[i] = r;
+    if (scnt[runs[r].c]++ == 0) sbeg[runs[r].c] = r;
+  }
+  // greedy bank-aware order within runs: pos -> term index
+  std::vector<int> order(NT);
+  std::vector<char> used(NT, 0);
+  for (int t = 0; t < C::STEPS; ++t)
+    for (int q = 0; q < 4; ++q) {
+      std::vector<int> qg, sg;   // (qe, group) and (se, group) chosen so far in this quarter at step t
+      for (int L = 8 * q; L < 8 * q + 8; ++L) {
+        const int pos = beg[L] + t;
+        if (pos >= beg[L + 1]) continue;
+        const Run &r = runs[run_of[pos]];
+        int best = -1, bc = 1 << 30;
+        for (int i = r.first; i <= r.last; ++i) {
+          if (used[i]) continue;
+          int cost = 0;
+          for (size_t a = 0; a < qg.size(); ++a)
+            if (qg[a] != terms[i].qe && (qg[a] - terms[i].qe) % 8 == 0) ++cost;
+          for (size_t a = 0; a < sg.size(); ++a)
+            if (sg[a] != terms[i].se && (sg[a] - terms[i].se) % 8 == 0) ++cost;
+          if (cost < bc) { bc = cost; best = i; }
+        }
+        used[best] = 1;
+        order[pos] = best;
+        qg.push_back(terms[best].qe);
+        sg.push_back(terms[best].se);
+      }
+    }
+  std::vector<uint32_t> w(C::STEPS * 32 + D::NP, (uint32_t)(P * P) << 7);   // padding: zero S' entry
+  for (int L = 0; L < 32; ++L)
+    for (int pos = beg[L]; pos < beg[L + 1]; ++pos) {
+      const Term &t = terms[order[pos]];
+      const int ak = std::abs(t.k);
+      uint32_t cw = (uint32_t)t.qe | (uint32_t)t.se << 7;
+      if (t.k < 0) cw |= (ak & 1) ? C::FA : C::FB;
+      if (slot_of[pos] >= 0) cw |= C::FLUSH | (uint32_t)slot_of[pos] << 20;
+      w[(pos - beg[L]) * 32 + L] = cw;
+    }
+  for (int l = 1; l <= P; ++l)
+    for (int m = 1; m <= l; ++m) {
+      const int c = lmidx(l, m);
+      w[C::STEPS * 32 + c] = (uint32_t)l | (uint32_t)m << 4 | (uint32_t)sbeg[c] << 8 | (uint32_t)scnt[c] << 19;
+    }
+  auto fact = [](int n) { long double f = 1; for (int i = 2; i <= n; ++i) f *= i; return f; };
+  auto F = [&](int a, int b) { const int ab = std::abs(b); return std::sqrt(fact(a + ab) * fact(a - ab)); };
+  std::vector<double> out(C::TAB_D, 0.0);
+  std::memcpy(out.data(), w.data(), w.size() * sizeof(uint32_t));
+  double *vlam = out.data() + C::VLAM, *vth = out.data() + C::VTH, *wS = out.data() + C::WS;
+  double *olam = out.data() + C::OLAM, *oth = out.data() + C::OTH;
+  for (int j = 2; j <= P; ++j)
+    for (int k = 0; k <= j; ++k) vlam[qidx(j, k)] = (double)(fact(j - 2) / F(j, k));
+  for (int j = 1; j <= P; ++j)
+    for (int k = 0; k <= j; ++k) vth[vidx(j, k)] = (double)(fact(j - 1) / F(j, k));
+  for (int lp = 0; lp < P; ++lp)
+    for (int mp = -lp; mp <= lp; ++mp) wS[lp * lp + lp + mp] = (double)(fact(lp) / F(lp, mp));
+  for (int l = 1; l <= P; ++l)
+    for (int m = 1; m <= l; ++m) {
+      olam[lmidx(l, m)] = (double)(F(l, m) / fact(l - 1));
+      oth[lmidx(l, m)] = (double)(F(l, m) / fact(l));
+    }
+  return out;
+}
+
+static std::vector<double> make_trtab_p(int p) {
+  switch (p) {
+    case 4: return make_trtab<4>();
+    case 6: return make_trtab<6>();
+    case 8: return make_trtab<8>();
+    default: return make_trtab<10>();
+  }
+}
+
 rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   if (!out) return fail(nullptr, RRQ_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
@@ -215,6 +328,11 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   c->T.wd = c->T.xd + kNDirect;
   c->T.xdp = c->T.wd + kNDirect;
   c->T.hc = c->T.xdp + kNDirect * q;
+  {
+    const std::vector<double> tt = make_trtab_p(p.p);
+    if (cudaMalloc(&c->d_trtab, tt.size() * sizeof(double)) == cudaSuccess)
+      cudaMemcpy(c->d_trtab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
   if (cuda_check(c, "rrq_create") != RRQ_OK) {
     g_create_err = c->err;
     rrq_destroy(c);
@@ -230,6 +348,7 @@ void rrq_destroy(rrq_ctx c) {
   for (auto e : c->pool) cudaEventDestroy(e);
   if (c->swapcnt.p) cudaFree(c->swapcnt.p);
   cudaFree(c->d_tab);
+  if (c->d_trtab) cudaFree(c->d_trtab);
   for (auto *b : {&c->Arow, &c->Xrow, &c->Qrow, &c->items4, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
                   &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
     if (b->p) cudaFree(b->p);
@@ -467,12 +586,6 @@ static size_t edge_smem(int n_omega) {
   tab = (tab + 1) & ~1;
   return (size_t)tab * sizeof(double) + kWPB * kPPW * sizeof(PairState<P>) + kWPB * sizeof(WarpScr<P>);
 }
-template <int P>
-static size_t translate_smem() {
-  using D = Dims<P>;
-  size_t tab = (2 * P + 1) * (2 * P + 1) + 2 * P + 2 + (D::NP + 1) / 2 + 1;
-  return (tab + TransCfg<P>::WPB * (size_t)TransCfg<P>::PER_WARP) * sizeof(double);
-}
 
 template <int P>
 static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets *tg, const int64_t *pair_ptr,
@@ -552,7 +665,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   if (!attr_set) {
     cudaFuncSetAttribute(k_pair_edge<P, kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_qmap<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_translate<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_translate<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM);
     cudaFuncSetAttribute(k_contract<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
@@ -568,21 +681,22 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
       k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), st>>>(
           sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
           tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, bp<double>(c->Arow), bp<double>(c->Xrow),
-          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr);
+          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab);
     }
     if ((r = cuda_check(c, "k_pair_edge"))) return r;
     {
       TScope t2(c, 3, st);
       k_qmap<P><<<(unsigned)(it1 - it0), 512, QC::SMEM, st>>>(it0, it1, bp<int64_t>(c->items), Pn,
                                                                 bp<int64_t>(c->seg), sA, fit, bp<double>(c->Arow),
-                                                                bp<double>(c->Qrow));
+                                                                bp<double>(c->Qrow), c->d_trtab);
     }
     if ((r = cuda_check(c, "k_qmap"))) return r;
     {
       TScope t3(c, 4, st);
-      unsigned grid = (unsigned)std::min<int64_t>((np_ + 7) / 8, (int64_t)c->num_sms * 8);
-      k_translate<P><<<grid, 256, translate_smem<P>(), st>>>(sA, sB, bp<double>(c->Xrow), bp<double>(c->Qrow),
-                                                              c->T.sqb, bp<double>(c->Z));
+      constexpr int WPB = TrCfg<P>::WPB;
+      unsigned grid = (unsigned)std::min<int64_t>((np_ + WPB - 1) / WPB, (int64_t)c->num_sms);
+      k_translate<P><<<grid, WPB * 32, TrCfg<P>::SMEM, st>>>(sA, sB, bp<double>(c->Xrow), bp<double>(c->Qrow),
+                                                              c->d_trtab, bp<double>(c->Z));
     }
     if ((r = cuda_check(c, "k_translate"))) return r;
     {
