@@ -5,7 +5,7 @@
 //   regime / model integrals / SSQ weights (Step 5), the GEMM rows a = omega1 d and
 //   b = omega1 nu' - omega3 (nu'.d) d, the scalar line integrals Omega, Omega_0 and derivatives
 //   (Step 6), and the I[gamma] part of W, dW and the S(r') Omega_0 part of Theta (Step 7).
-// k_qmap (CTA per tile of 32 pairs of one patch): the line-integral maps [Q | V](pair) = a M,
+// k_qmap (CTA per tile of 16 pairs of one patch): the line-integral maps [Q | V](pair) = a M,
 //   dQ(pair) = b M_Q as one FP64 tensor-core GEMM (mma.sync m8n8k4 f64 = DMMA) against the patch's
 //   operand M (built in k_edge_tables).
 // k_translate (warp per pair): translation (Step 7) -> W, dW, Theta -> contraction vectors zeta.
@@ -467,8 +467,8 @@ __global__ void __launch_bounds__(WPB * 32)
         double txd[3];
         cross3(tau, d, txd);
         for (int a = 0; a < 3; ++a) {
-          Ar[3 * kap + a] = w1 * d[a];                        // GEMM row a (k = 3 kappa + axis)
-          Ar[K + 3 * kap + a] = w1 * nup[a] - w3 * nd * d[a];  // GEMM row b
+          Ar[a * E + kap] = w1 * d[a];                          // GEMM row a (k = axis E + kappa)
+          Ar[K + a * E + kap] = w1 * nup[a] - w3 * nd * d[a];  // GEMM row b
           om[1 + a] -= w1 * tau[a];
           om[5 + a] += w3 * nd * tau[a];
         }
@@ -569,20 +569,26 @@ __global__ void __launch_bounds__(WPB * 32)
 
 // ------------------------------------------------------------------------------------------------
 // k_qmap: line-integral maps (Step 6) as a DMMA GEMM per tile of TP pairs
-// of one patch: rows [a(pairs) ; b(pairs)] x M (k_edge_tables).  Warp w owns M-tile (w % MT) and every
-// (W / MT)-th N-tile; the b-row M-tiles skip the V columns.  A tile staged in shared memory (row stride
-// == 4 mod 16 doubles: conflict-free fragments); B fragments straight from the patch operand (L1/L2).
+// of one patch: rows [a(pairs) ; b(pairs)] x M (k_edge_tables).  K runs axis-major (k = axis E + kappa) and
+// the Q columns component-major, so the structurally zero blocks of M (axis c-1 of vector component c, the
+// cross product) are skipped whole.  Warp = (pair group of 8, column split); the a- and b-row tiles share
+// every Q-column B fragment (2 DMMA per load), the V columns need the a rows only.  A staged in shared
+// memory by cp.async (row stride == 4 mod 16 doubles), M streamed in KC-row chunks (double buffered,
+// row stride == 8 mod 16).  Two CTAs per SM so one's staging / stores overlap the other's DMMA loop.
+// The epilogue scales by v_lambda / v_theta (TrCfg) and stores the QRow layout for k_translate.
 // ------------------------------------------------------------------------------------------------
 template <int P>
 struct QmapCfg {
   using D = Dims<P>;
-  static constexpr int TP = P >= 10 ? 16 : 32, ROWS = 2 * TP, WARPS = 16;
-  static constexpr int PG = TP / 8, NSPLIT = WARPS / PG;       // pair groups of 8; N splits per group
+  static constexpr int TP = 16, ROWS = 2 * TP, WARPS = 8;
+  static constexpr int PG = TP / 8, GPW = 1;                   // pair groups of 8 per tile / per warp
+  static constexpr int NSPLIT = WARPS / (PG / GPW);              // N splits
   static constexpr int KA = (D::K % 16 == 4) ? D::K : D::K + ((4 - D::K % 16) + 16) % 16;
+  static constexpr int TQC = D::CQP / 8;                      // tiles per quaternion component
   static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8, NTV = NTALL - NTQ;
   static constexpr int NTQW = (NTQ + NSPLIT - 1) / NSPLIT, NTVW = (NTV + NSPLIT - 1) / NSPLIT;
-  static constexpr int KC = 12, NCH = D::K / KC;              // B staged in chunks of KC k-rows
-  static_assert(D::K % KC == 0, "K must be a multiple of the B chunk");
+  static constexpr int KC = (D::E % 8 == 0) ? 8 : 12, NCH = D::K / KC, CPA = D::E / KC;   // chunks per axis
+  static_assert(D::E % KC == 0, "a B chunk must lie within one axis block");
   static constexpr size_t SMEM_A = (size_t)ROWS * KA * sizeof(double);
   static constexpr size_t SMEM_B = (size_t)KC * D::NCS * sizeof(double);
   static constexpr size_t SMEM = SMEM_A + 2 * SMEM_B;
@@ -596,9 +602,33 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
+// 1-D bulk copies (TMA engine) completing on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
 template <int P>
-__global__ void __launch_bounds__(512, 1)
-    k_qmap(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, int64_t n_patches,
+__global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, 2)
+    k_qmap(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, const int32_t *__restrict__ item_patch,
            const int64_t *__restrict__ seg_ptr, int64_t sA, const double *__restrict__ fit,
            const double *__restrict__ Arow, double *__restrict__ Qrow, const double *__restrict__ trtab) {
   using D = Dims<P>;
@@ -606,87 +636,109 @@ __global__ void __launch_bounds__(512, 1)
   using C = QmapCfg<P>;
   using QR = QRow<P>;
   constexpr int K = D::K, KA = C::KA, TP = C::TP, NCS = D::NCS, KC = C::KC;
-  extern __shared__ double sA_[];
+  extern __shared__ __align__(16) double sA_[];
   double *sB = sA_ + C::SMEM_A / sizeof(double);    // [2][KC][NCS]
   const int64_t item = item0 + blockIdx.x;
   if (item >= item1) return;
-  int64_t lo = 0, hi = n_patches;
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (item_ptr[mid] <= item) lo = mid; else hi = mid;
-  }
-  const int64_t Pp = lo;
+  const int64_t Pp = item_patch[item];
   const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *M = fit + Pp * (int64_t)L::STRIDE + L::MQ;
-  auto issue = [&](int ch) {
-    const double *src = M + (int64_t)ch * KC * NCS;
-    double *dst = sB + (ch & 1) * KC * NCS;
-    for (int i = threadIdx.x; i < KC * NCS / 2; i += blockDim.x) cp_async16(dst + 2 * i, src + 2 * i);
-    cp_async_commit();
-  };
-  issue(0);
-  // stage A: row r < TP -> a-row of pair s0 + r; row TP + r -> b-row
-  for (int i = threadIdx.x; i < C::ROWS * K; i += blockDim.x) {
-    const int r = i / K, k = i % K, pr = r % TP, ab = r / TP;
-    sA_[r * KA + k] = pr < cnt ? Arow[(s0 + pr - sA) * 2 * K + ab * K + k] : 0.0;
-  }
+  __shared__ uint64_t bar[2];
+  constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ROWB = (unsigned)(K * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // warp = (pair group pg, N split ns): the a-row and b-row tiles of the same 8 pairs share every Q-column
-  // B fragment (2 DMMA per load); the V columns are needed for the a rows only.
-  const int pg = warp % C::PG, ns = warp / C::PG;
-  double accA[C::NTQW][2], accB[C::NTQW][2], accV[C::NTVW][2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  // rows of absent pairs are zero
+  for (int i = threadIdx.x; i < C::ROWS * K; i += blockDim.x) {
+    const int r = i / K;
+    if (r % TP >= cnt) sA_[r * KA + i % K] = 0.0;
+  }
+  __syncthreads();
+  // stage A (row r < TP -> a-row of pair s0 + r; row TP + r -> b-row) and chunk 0 of M on bar[0]
+  if (warp == 0) {
+    if (lane == 0) mbar_expect_tx(&bar[0], 2u * cnt * ROWB + CHB);
+    __syncwarp();
+    for (int r = lane; r < 2 * TP; r += 32)
+      if (r % TP < cnt) bulk_g2s(sA_ + r * KA, Arow + (s0 + r % TP - sA) * 2 * K + (r / TP) * K, ROWB, &bar[0]);
+    if (lane == 0) bulk_g2s(sB, M, CHB, &bar[0]);
+  }
+  const int ns = warp / (C::PG / C::GPW), g0 = (warp % (C::PG / C::GPW)) * C::GPW;
+  __shared__ double ssc[D::NQ + D::NV];   // v_lambda | v_theta
+  for (int i = threadIdx.x; i < D::NQ + D::NV; i += blockDim.x) ssc[i] = trtab[TrCfg<P>::VLAM + i];
+  double accA[C::GPW][C::NTQW][2], accB[C::GPW][C::NTQW][2], accV[C::GPW][C::NTVW][2];
 #pragma unroll
-  for (int t = 0; t < C::NTQW; ++t) accA[t][0] = accA[t][1] = accB[t][0] = accB[t][1] = 0.0;
+  for (int g = 0; g < C::GPW; ++g) {
 #pragma unroll
-  for (int t = 0; t < C::NTVW; ++t) accV[t][0] = accV[t][1] = 0.0;
-  const double *arow = sA_ + (pg * 8 + (lane >> 2)) * KA + (lane & 3);
-  const double *brow = arow + TP * KA;
+    for (int t = 0; t < C::NTQW; ++t) accA[g][t][0] = accA[g][t][1] = accB[g][t][0] = accB[g][t][1] = 0.0;
+#pragma unroll
+    for (int t = 0; t < C::NTVW; ++t) accV[g][t][0] = accV[g][t][1] = 0.0;
+  }
+  const double *arow = sA_ + (g0 * 8 + (lane >> 2)) * KA + (lane & 3);   // group g0 + g: + 8 g KA; b: + TP KA
   const int bofs = (lane & 3) * NCS + (lane >> 2);
   for (int ch = 0; ch < C::NCH; ++ch) {
-    if (ch + 1 < C::NCH) {
-      issue(ch + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    if (threadIdx.x == 0 && ch + 1 < C::NCH) {   // buffer (ch+1)&1 was released by the barrier ending ch-1
+      fence_proxy_async();
+      mbar_expect_tx(&bar[(ch + 1) & 1], CHB);
+      bulk_g2s(sB + ((ch + 1) & 1) * KC * NCS, M + (int64_t)(ch + 1) * KC * NCS, CHB, &bar[(ch + 1) & 1]);
     }
-    __syncthreads();
+    mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
+    const int zc = ch / C::CPA + 1;   // quaternion component whose block is zero in this axis
     const double *bb = sB + (ch & 1) * KC * NCS + bofs;
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
-      const double a = arow[ch * KC + kk], b = brow[ch * KC + kk];
+      double a[C::GPW], b[C::GPW];
+#pragma unroll
+      for (int g = 0; g < C::GPW; ++g) {
+        a[g] = arow[g * 8 * KA + ch * KC + kk];
+        b[g] = arow[(TP + g * 8) * KA + ch * KC + kk];
+      }
       const double *bk = bb + kk * NCS;
 #pragma unroll
       for (int t = 0; t < C::NTQW; ++t) {
         const int nt = ns + t * C::NSPLIT;
-        if (nt < C::NTQ) {
+        if (nt < C::NTQ && nt / C::TQC != zc) {
           const double bq = bk[nt * 8];
-          dmma(accA[t][0], accA[t][1], a, bq);
-          dmma(accB[t][0], accB[t][1], b, bq);
+#pragma unroll
+          for (int g = 0; g < C::GPW; ++g) {
+            dmma(accA[g][t][0], accA[g][t][1], a[g], bq);
+            dmma(accB[g][t][0], accB[g][t][1], b[g], bq);
+          }
         }
       }
 #pragma unroll
       for (int t = 0; t < C::NTVW; ++t) {
         const int nt = C::NTQ + ns + t * C::NSPLIT;
-        if (nt < C::NTALL) dmma(accV[t][0], accV[t][1], a, bk[nt * 8]);
+        if (nt < C::NTALL) {
+          const double bv = bk[nt * 8];
+#pragma unroll
+          for (int g = 0; g < C::GPW; ++g) dmma(accV[g][t][0], accV[g][t][1], a[g], bv);
+        }
       }
     }
     __syncthreads();
   }
   // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]
-  const int pr = pg * 8 + (lane >> 2);
-  if (pr < cnt) {
+#pragma unroll
+  for (int g = 0; g < C::GPW; ++g) {
+    const int pr = (g0 + g) * 8 + (lane >> 2);
+    if (pr >= cnt) continue;
     double *out = Qrow + (s0 + pr - sA) * QR::STRIDE;
 #pragma unroll
     for (int t = 0; t < C::NTQW; ++t) {
       const int nt = ns + t * C::NSPLIT;
       if (nt >= C::NTQ) continue;
-      const double sc = __ldg(trtab + TrCfg<P>::VLAM + nt);   // column block nt = entry qidx(j,k)
-      double *o = out + QR::EG * nt + 2 * (lane & 3);
-      o[0] = sc * accA[t][0];
-      o[1] = sc * accA[t][1];
-      o[8] = sc * accB[t][0];
-      o[9] = sc * accB[t][1];
+      const int comp = nt / C::TQC, e = (nt - comp * C::TQC) * 4 + (lane & 3);   // entry qidx(j,k)
+      if (e >= D::NQ) continue;
+      const double sc = ssc[e];
+      double *o = out + QR::EG * e + 2 * comp;
+      o[0] = sc * accA[g][t][0];
+      o[1] = sc * accA[g][t][1];
+      o[8] = sc * accB[g][t][0];
+      o[9] = sc * accB[g][t][1];
     }
 #pragma unroll
     for (int t = 0; t < C::NTVW; ++t) {
@@ -694,9 +746,9 @@ __global__ void __launch_bounds__(512, 1)
       if (nt >= C::NTALL) continue;
       const int col = nt * 8 + 2 * (lane & 3) - D::NCQ;
       if (col < 2 * D::NV) {
-        const double sc = __ldg(trtab + TrCfg<P>::VTH + (col >> 1));
-        out[QR::V + col] = sc * accV[t][0];
-        out[QR::V + col + 1] = sc * accV[t][1];
+        const double sc = ssc[D::NQ + (col >> 1)];
+        out[QR::V + col] = sc * accV[g][t][0];
+        out[QR::V + col + 1] = sc * accV[g][t][1];
       }
     }
   }
@@ -886,7 +938,7 @@ struct ContractCfg {
   static constexpr int TP = 16, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 8;
   static constexpr int ZS = (D::NZS % 16 == 4) ? D::NZS : D::NZS + ((4 - D::NZS % 16) + 16) % 16;
   static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
-  static constexpr int NB = (D::N % 16 == 8) ? D::N : D::N + ((8 - D::N % 16) + 16) % 16;   // B row stride
+  static constexpr int NB = (D::N % 16 == 4) ? D::N : D::N + ((4 - D::N % 16) + 16) % 16;   // B row stride
   static constexpr int KC = (D::NP % 3 == 0) ? 12 : ((D::NP % 2 == 0) ? 8 : 4);            // k-rows per chunk
   static constexpr int NCH = 4 * D::NP / KC;
   static constexpr size_t SMEM_Z = (size_t)TP * ZS;
@@ -896,7 +948,7 @@ struct ContractCfg {
 
 template <int P>
 __global__ void __launch_bounds__(256, 2)
-    k_contract(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, int64_t n_patches,
+    k_contract(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, const int32_t *__restrict__ item_patch,
                const int64_t *__restrict__ seg_ptr, int64_t sA, const int64_t *__restrict__ perm,
                const int64_t *__restrict__ ptgt, int64_t kbase, const double *__restrict__ fit,
                const double *__restrict__ Zrow, const double *__restrict__ nodes,
@@ -915,12 +967,7 @@ __global__ void __launch_bounds__(256, 2)
   int *sSelf = reinterpret_cast<int *>(sK + TP);
   const int64_t item = item0 + blockIdx.x;
   if (item >= item1) return;
-  int64_t lo = 0, hi = n_patches;
-  while (hi - lo > 1) {
-    int64_t mid = (lo + hi) >> 1;
-    if (item_ptr[mid] <= item) lo = mid; else hi = mid;
-  }
-  const int64_t Pp = lo;
+  const int64_t Pp = item_patch[item];
   const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *blk = fit + Pp * (int64_t)L::STRIDE;
@@ -1091,6 +1138,13 @@ __global__ void k_items(int64_t n_patches, const int64_t *__restrict__ seg_ptr, 
   if (P >= n_patches) return;
   int64_t c = seg_ptr[P + 1] - seg_ptr[P];
   items[P] = (c + tile - 1) / tile;
+}
+
+// item -> patch map for the tile kernels (items of patch P are [items[P], items[P+1])).
+__global__ void k_item_patch(int64_t n_patches, const int64_t *__restrict__ items, int32_t *__restrict__ item_patch) {
+  int64_t P = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (P >= n_patches) return;
+  for (int64_t i = items[P]; i < items[P + 1]; ++i) item_patch[i] = (int32_t)P;
 }
 
 __global__ void k_copy_i64(int64_t n, const int64_t *__restrict__ a, int64_t *__restrict__ b) {

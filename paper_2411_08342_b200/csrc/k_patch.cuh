@@ -156,30 +156,33 @@ __global__ void k_edge_tables(int64_t n_patches, const double *__restrict__ hc, 
   cd GS[D::NS][3];
   for (int j = 0; j <= P; ++j)
     for (int k = 0; k <= j; ++k) grad_fast(R, j, k, hc, GS[sidx(j, k)]);
-  double *M0 = blk + L::MQ + (int64_t)(3 * kap) * D::NCS;   // rows for axis 0, 1, 2 at stride NCS
-  for (int c = 0; c < D::NCS; ++c) { M0[c] = 0; M0[D::NCS + c] = 0; M0[2 * D::NCS + c] = 0; }
+  // rows k = axis E + kappa; columns: Q component-major (comp CQP + 2 qidx + re/im), then V (2 vidx + re/im)
+  double *M0 = blk + L::MQ + (int64_t)kap * D::NCS;
+  constexpr int64_t AX = (int64_t)D::E * D::NCS;   // axis stride
+  for (int c = 0; c < D::NCS; ++c) { M0[c] = 0; M0[AX + c] = 0; M0[2 * AX + c] = 0; }
   for (int j = 1; j <= P; ++j)
     for (int k = 0; k <= j; ++k) {
       const cd *g = GS[sidx(j, k)];
       cd e[3] = {g[1] * mk(t[2], 0) - g[2] * mk(t[1], 0), g[2] * mk(t[0], 0) - g[0] * mk(t[2], 0),
                  g[0] * mk(t[1], 0) - g[1] * mk(t[0], 0)};
       const int vc = D::NCQ + 2 * vidx(j, k);
-      for (int a = 0; a < 3; ++a) { M0[a * D::NCS + vc] = e[a].x; M0[a * D::NCS + vc + 1] = e[a].y; }
+      for (int a = 0; a < 3; ++a) { M0[a * AX + vc] = e[a].x; M0[a * AX + vc + 1] = e[a].y; }
       if (j >= 2) {
         cd h[3];
         hess_fast(GS, j, k, t, hc, h);
-        const int qc = 8 * qidx(j, k);
+        const int qc = 2 * qidx(j, k);
+        constexpr int S = D::CQP;
         for (int ri = 0; ri < 2; ++ri) {
           double hv[3] = {ri ? h[0].y : h[0].x, ri ? h[1].y : h[1].x, ri ? h[2].y : h[2].x};
           // scalar part: -a.g
-          for (int a = 0; a < 3; ++a) M0[a * D::NCS + qc + ri] = -hv[a];
-          // x: a_y g_z - a_z g_y ; y: a_z g_x - a_x g_z ; z: a_x g_y - a_y g_x
-          M0[1 * D::NCS + qc + 2 + ri] = hv[2];
-          M0[2 * D::NCS + qc + 2 + ri] = -hv[1];
-          M0[2 * D::NCS + qc + 4 + ri] = hv[0];
-          M0[0 * D::NCS + qc + 4 + ri] = -hv[2];
-          M0[0 * D::NCS + qc + 6 + ri] = hv[1];
-          M0[1 * D::NCS + qc + 6 + ri] = -hv[0];
+          for (int a = 0; a < 3; ++a) M0[a * AX + qc + ri] = -hv[a];
+          // x: a_y g_z - a_z g_y ; y: a_z g_x - a_x g_z ; z: a_x g_y - a_y g_x  (axis c-1 of component c is zero)
+          M0[1 * AX + S + qc + ri] = hv[2];
+          M0[2 * AX + S + qc + ri] = -hv[1];
+          M0[2 * AX + 2 * S + qc + ri] = hv[0];
+          M0[0 * AX + 2 * S + qc + ri] = -hv[2];
+          M0[0 * AX + 3 * S + qc + ri] = hv[1];
+          M0[1 * AX + 3 * S + qc + ri] = -hv[0];
         }
       }
     }

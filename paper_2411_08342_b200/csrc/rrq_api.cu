@@ -36,7 +36,7 @@ struct rrq_ctx_s {
     size_t n = 0;
   };
   int64_t last_np = 0, last_nz = 0, last_nzs = 0, last_sA = 0;
-  Buf Arow, Xrow, Qrow, items4;
+  Buf Arow, Xrow, Qrow, ipatch;
   Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one, swapcnt;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
@@ -349,7 +349,7 @@ void rrq_destroy(rrq_ctx c) {
   if (c->swapcnt.p) cudaFree(c->swapcnt.p);
   cudaFree(c->d_tab);
   if (c->d_trtab) cudaFree(c->d_trtab);
-  for (auto *b : {&c->Arow, &c->Xrow, &c->Qrow, &c->items4, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
+  for (auto *b : {&c->Arow, &c->Xrow, &c->Qrow, &c->ipatch, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
                   &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
     if (b->p) cudaFree(b->p);
   delete c;
@@ -595,7 +595,8 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   using D = Dims<P>;
   using QC = QmapCfg<P>;
   using CC = ContractCfg<P>;
-  constexpr int TP = QC::TP, TP4 = CC::TP;
+  constexpr int TP = QC::TP;
+  static_assert(QC::TP == CC::TP, "k_qmap and k_contract share the work items");
   const int64_t Pn = s->n_patches;
   const int raw = (mask & RRQ_RAW) ? 1 : 0;
   int64_t b[2];
@@ -616,11 +617,11 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   }
   if (!ensure(c, c->ptgt, total * sizeof(int64_t)) || !ensure(c, c->perm, total * sizeof(int64_t)) ||
       !ensure(c, c->seg, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->cursor, (Pn + 1) * sizeof(int64_t)) ||
-      !ensure(c, c->items, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->items4, (Pn + 1) * sizeof(int64_t)) ||
+      !ensure(c, c->items, (Pn + 1) * sizeof(int64_t)) || !ensure(c, c->ipatch, (total / TP + Pn + 1) * sizeof(int32_t)) ||
       !ensure(c, c->one, 64))
     return RRQ_ERR_CUDA;
   // ---- plumbing over the whole call: pair -> target, patch-major permutation, work items
-  std::vector<int64_t> hseg(Pn + 1), hitem(Pn + 1), hitem4(Pn + 1);
+  std::vector<int64_t> hseg(Pn + 1), hitem(Pn + 1);
   {
     TScope tsp(c, 6, st);
     k_pair_targets<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase,
@@ -634,13 +635,10 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     k_items<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<int64_t>(c->seg), TP, bp<int64_t>(c->items));
     cudaMemsetAsync(bp<int64_t>(c->items) + Pn, 0, sizeof(int64_t), st);
     k_scan_i64<<<1, 1024, 0, st>>>(Pn + 1, bp<int64_t>(c->items), bp<int64_t>(c->one) + 1);
-    k_items<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<int64_t>(c->seg), TP4, bp<int64_t>(c->items4));
-    cudaMemsetAsync(bp<int64_t>(c->items4) + Pn, 0, sizeof(int64_t), st);
-    k_scan_i64<<<1, 1024, 0, st>>>(Pn + 1, bp<int64_t>(c->items4), bp<int64_t>(c->one) + 2);
-    c->launches += 8;
+    k_item_patch<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<int64_t>(c->items), bp<int32_t>(c->ipatch));
+    c->launches += 7;
     cudaMemcpyAsync(hseg.data(), c->seg.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(hitem.data(), c->items.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(hitem4.data(), c->items4.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   }
   cudaStreamSynchronize(st);
   hseg[Pn] = total;
@@ -673,7 +671,6 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   for (auto &sr : subs) {
     const int64_t sA = hseg[sr.first], sB = hseg[sr.second];
     const int64_t it0 = hitem[sr.first], it1 = hitem[sr.second];
-    const int64_t iu0 = hitem4[sr.first], iu1 = hitem4[sr.second];
     const int64_t np_ = sB - sA;
     {
       TScope t1(c, 2, st);
@@ -686,7 +683,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     if ((r = cuda_check(c, "k_pair_edge"))) return r;
     {
       TScope t2(c, 3, st);
-      k_qmap<P><<<(unsigned)(it1 - it0), 512, QC::SMEM, st>>>(it0, it1, bp<int64_t>(c->items), Pn,
+      k_qmap<P><<<(unsigned)(it1 - it0), QC::WARPS * 32, QC::SMEM, st>>>(it0, it1, bp<int64_t>(c->items), bp<int32_t>(c->ipatch),
                                                                 bp<int64_t>(c->seg), sA, fit, bp<double>(c->Arow),
                                                                 bp<double>(c->Qrow), c->d_trtab);
     }
@@ -701,8 +698,8 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     if ((r = cuda_check(c, "k_translate"))) return r;
     {
       TScope t4(c, 5, st);
-      k_contract<P><<<(unsigned)(iu1 - iu0), CC::WARPS * 32, CC::SMEM, st>>>(
-          iu0, iu1, bp<int64_t>(c->items4), Pn, bp<int64_t>(c->seg), sA, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt),
+      k_contract<P><<<(unsigned)(it1 - it0), CC::WARPS * 32, CC::SMEM, st>>>(
+          it0, it1, bp<int64_t>(c->items), bp<int32_t>(c->ipatch), bp<int64_t>(c->seg), sA, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt),
           obase, fit, bp<double>(c->Z), s->nodes, s->normals, s->weights, tg->x, tg->normal, tg->self_node, mask, raw,
           obase, col_idx, vals[0], vals[1], vals[2], vals[3], pstat);
     }

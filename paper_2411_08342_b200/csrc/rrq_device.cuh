@@ -39,12 +39,12 @@ struct Dims {
   static constexpr int NQ = NS - 3;               // (j, k >= 0), 2 <= j <= p
   static constexpr int NV = NS - 1;               // (j, k >= 0), 1 <= j <= p
   static constexpr int NZ = 13 * NP;              // per-pair contraction vector
-  static constexpr int K = 3 * E;                 // GEMM depth of the line-integral maps: (kappa, axis)
-  static constexpr int NCQ = 8 * NQ;              // Q columns: (jk, quaternion comp, re/im)
-  static constexpr int NC = 8 * NQ + 2 * NV;      // + V columns (jk, re/im)
-  static constexpr int NCP = (NC + 7) / 8 * 8;    // padded to whole 8-wide DMMA tiles
-  static constexpr int NCS = NCP % 16 == 8 ? NCP : NCP + 8;   // row stride == 8 (mod 16): conflict-free B frags
-  static constexpr int NV8 = (2 * NV + 7) / 8 * 8;           // V columns padded
+  static constexpr int K = 3 * E;                 // GEMM depth of the line-integral maps: k = axis E + kappa
+  static constexpr int CQP = (2 * NQ + 7) / 8 * 8;// Q columns of one quaternion component (jk, re/im), padded
+  static constexpr int NCQ = 4 * CQP;             // Q columns, component-major (scalar, x, y, z)
+  static constexpr int NV8 = (2 * NV + 7) / 8 * 8;// V columns (jk, re/im), padded
+  static constexpr int NCP = NCQ + NV8;           // whole 8-wide DMMA tiles
+  static constexpr int NCS = NCP + ((4 - NCP % 16) + 16) % 16; // row stride == 4 (mod 16): conflict-free B frags
   static constexpr int NZS = (NZ + 3) / 4 * 4;    // Z row stride (k-steps of 4)
 };
 

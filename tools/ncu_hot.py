@@ -12,7 +12,9 @@ nl = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 
 
 def run(*a):
-    return subprocess.run(["ncu", "-i", rep, *a], capture_output=True, text=True).stdout
+    import os
+    flt = ["-k", "regex:" + os.environ["KERNEL"]] if os.environ.get("KERNEL") else []
+    return subprocess.run(["ncu", "-i", rep, *flt, *a], capture_output=True, text=True).stdout
 
 
 raw = list(csv.reader(io.StringIO(run("--page", "raw", "--csv"))))
@@ -59,3 +61,24 @@ if os.environ.get("RANGES"):
         a, b = (int(x, 16) for x in rg.split(":"))
         sel = [r for r in rows if a <= int(r[4], 16) - base < b]
         print(f"{a:6x}-{b:6x}: samples {100 * sum(r[0] for r in sel) / ts:5.1f}%  inst {100 * sum(r[1] for r in sel) / ti:5.1f}%")
+
+# per-region stall reasons: REGIONS=0:1700,1700:2300 (hex offsets)
+if os.environ.get("REGIONS"):
+    reasons = [c for c in hh if c.startswith("stall_") and "Not Issued" not in c]
+    idx = {c: hh.index(c) for c in reasons}
+    allrows = []
+    prev = -1
+    for r in src[2:]:
+        if not r[ia].startswith("0x"):
+            continue
+        a = int(r[ia], 16) - base
+        if a < prev:
+            break
+        prev = a
+        allrows.append((a, r))
+    for rg in os.environ["REGIONS"].split(","):
+        a0, b0 = (int(x, 16) for x in rg.split(":"))
+        tot = {c: sum(int(r[idx[c]] or 0) for a, r in allrows if a0 <= a < b0) for c in reasons}
+        s_ = sum(tot.values())
+        top = sorted(tot.items(), key=lambda x: -x[1])[:6]
+        print(f"{a0:6x}-{b0:6x} {100 * s_ / ts:5.1f}%: " + ", ".join(f"{c[6:]} {100 * v / max(s_, 1):.0f}%" for c, v in top))
