@@ -205,20 +205,20 @@ struct PairState {
   cd R[D::NS];                 // R_l^m at (y', z', x'): S^{(l,m)}(r') for m >= 0
   double I[3][D::Q], J[3][D::Q];
   double t0[3][2];
-  double rp[3], nup[3], u3, om[8];
+  double rp[3], nup[3], u3, om[8], o0e[3];
   int64_t k, t;
   int Pp, self_local, active, pad;
   int swap[3], conv[3], direct[3];
 };
-// Per-warp scratch: gradient table and the direct-rule buffer.
+constexpr int kPPW = 3;   // pairs per warp per round (the Newton phase packs 3 x 9 = 27 lanes)
+
+// Per-warp scratch: gradient tables of the warp's pairs (phase 1 -> phase 5) and the direct-rule buffer.
 template <int P>
 struct WarpScr {
   using D = Dims<P>;
-  cd GS[D::NS][3];
+  cd GS[kPPW][D::NS][3];
   double r13[2][kNDirect];
 };
-
-constexpr int kPPW = 3;   // pairs per warp per round (the Newton phase packs 3 x 9 = 27 lanes)
 
 template <int P, int WPB>
 __global__ void __launch_bounds__(WPB * 32)
@@ -249,6 +249,8 @@ __global__ void __launch_bounds__(WPB * 32)
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpScr<P> &wsc = wscr[warp];
+  __shared__ int nsw;                          // swap edges of the round (CTA-wide list for phase 4)
+  __shared__ int swl[WPB * kPPW * 3];
   PairState<P> *mine = pst + warp * kPPW;      // this warp's 3 pairs
   const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
   unsigned long long nswap = 0;
@@ -259,80 +261,96 @@ __global__ void __launch_bounds__(WPB * 32)
   long long ph_t = clock64();
   for (int64_t base = sA + (int64_t)blockIdx.x * WPB * kPPW; base < sB; base += (int64_t)gridDim.x * WPB * kPPW) {
     // ---------------- phase 1: frame, gauge (A2, A8), harmonics at the target (Step 4)
-    for (int pp = 0; pp < kPPW; ++pp) {
+    if (lane < kPPW) {   // one lane per pair: the index / header loads of the 3 pairs overlap
+      const int pp = lane;
       PairState<P> &ps = mine[pp];
       const int64_t s = base + warp * kPPW + pp;
       const bool active = s < sB;
-      if (lane == 0) ps.active = active;
-      if (!active) continue;
-      const int64_t k = perm[s], t = ptgt[k - kbase];
-      const int Pp = pair_patch[k];
-      const double *hd = fit + (int64_t)Pp * L::STRIDE + L::HDR;
-      double rp[3], nup[3] = {0, 0, 0};
-      {
-        const double invh = 1.0 / hd[H_H];
-        const double d[3] = {tx[3 * t] - hd[H_O], tx[3 * t + 1] - hd[H_O + 1], tx[3 * t + 2] - hd[H_O + 2]};
-        for (int r = 0; r < 3; ++r) rp[r] = (hd[H_RM + 3 * r] * d[0] + hd[H_RM + 3 * r + 1] * d[1] + hd[H_RM + 3 * r + 2] * d[2]) * invh;
-        if (tnorm) {
-          const double *nn = tnorm + 3 * t;
-          for (int r = 0; r < 3; ++r) nup[r] = hd[H_RM + 3 * r] * nn[0] + hd[H_RM + 3 * r + 1] * nn[1] + hd[H_RM + 3 * r + 2] * nn[2];
+      ps.active = active;
+      if (active) {
+        const int64_t k = perm[s], t = ptgt[k - kbase];
+        const int Pp = pair_patch[k];
+        const double *hd = fit + (int64_t)Pp * L::STRIDE + L::HDR;
+        double rp[3], nup[3] = {0, 0, 0};
+        {
+          const double invh = 1.0 / hd[H_H];
+          const double d[3] = {tx[3 * t] - hd[H_O], tx[3 * t + 1] - hd[H_O + 1], tx[3 * t + 2] - hd[H_O + 2]};
+          for (int r = 0; r < 3; ++r) rp[r] = (hd[H_RM + 3 * r] * d[0] + hd[H_RM + 3 * r + 1] * d[1] + hd[H_RM + 3 * r + 2] * d[2]) * invh;
+          if (tnorm) {
+            const double *nn = tnorm + 3 * t;
+            for (int r = 0; r < 3; ++r) nup[r] = hd[H_RM + 3 * r] * nn[0] + hd[H_RM + 3 * r + 1] * nn[1] + hd[H_RM + 3 * r + 2] * nn[2];
+          }
         }
-      }
-      int self_local = -1;
-      if (self_node) {
-        const int64_t sn = self_node[t];
-        if (sn >= 0 && sn / D::N == Pp) self_local = (int)(sn % D::N);
-      }
-      const int sd = side ? (int)side[t] : 2;
-      double sg;
-      {
-        const double z = rp[2] - hd[H_VL + 2], zlo = hd[H_ZLO], zhi = hd[H_ZHI];
-        if (self_local >= 0) sg = -1.0;
-        else if (z > zhi + 0.1) sg = 1.0;
-        else if (z < zlo - 0.1) sg = -1.0;
-        else {
-          const double *va = hd + H_VL, *vb = hd + H_VL + 3, *vc = hd + H_VL + 6;
-          const double det = (vb[0] - va[0]) * (vc[1] - va[1]) - (vc[0] - va[0]) * (vb[1] - va[1]);
-          const double l1 = ((rp[0] - va[0]) * (vc[1] - va[1]) - (vc[0] - va[0]) * (rp[1] - va[1])) / det;
-          const double l2 = ((vb[0] - va[0]) * (rp[1] - va[1]) - (rp[0] - va[0]) * (vb[1] - va[1])) / det;
-          const double l0 = 1 - l1 - l2;
-          const double mn = fmin(l0, fmin(l1, l2));
-          if (mn >= -0.25 && sd != 2) sg = sd > 0 ? 1.0 : -1.0;
-          else sg = (z - 0.5 * (zlo + zhi) > 0) ? 1.0 : -1.0;
+        int self_local = -1;
+        if (self_node) {
+          const int64_t sn = self_node[t];
+          if (sn >= 0 && sn / D::N == Pp) self_local = (int)(sn % D::N);
         }
-      }
-      if (lane == 0) {
+        const int sd = side ? (int)side[t] : 2;
+        double sg;
+        {
+          const double z = rp[2] - hd[H_VL + 2], zlo = hd[H_ZLO], zhi = hd[H_ZHI];
+          if (self_local >= 0) sg = -1.0;
+          else if (z > zhi + 0.1) sg = 1.0;
+          else if (z < zlo - 0.1) sg = -1.0;
+          else {
+            const double *va = hd + H_VL, *vb = hd + H_VL + 3, *vc = hd + H_VL + 6;
+            const double det = (vb[0] - va[0]) * (vc[1] - va[1]) - (vc[0] - va[0]) * (vb[1] - va[1]);
+            const double l1 = ((rp[0] - va[0]) * (vc[1] - va[1]) - (vc[0] - va[0]) * (rp[1] - va[1])) / det;
+            const double l2 = ((vb[0] - va[0]) * (rp[1] - va[1]) - (rp[0] - va[0]) * (vb[1] - va[1])) / det;
+            const double l0 = 1 - l1 - l2;
+            const double mn = fmin(l0, fmin(l1, l2));
+            if (mn >= -0.25 && sd != 2) sg = sd > 0 ? 1.0 : -1.0;
+            else sg = (z - 0.5 * (zlo + zhi) > 0) ? 1.0 : -1.0;
+          }
+        }
         ps.k = k; ps.t = t; ps.Pp = Pp; ps.self_local = self_local; ps.u3 = sg;
         for (int a = 0; a < 3; ++a) { ps.rp[a] = rp[a]; ps.nup[a] = nup[a]; }
       }
-      if (lane <= P) r_column<P>(rp[1], rp[2], rp[0], lane, ps.R, shc);
-      __syncwarp();
-      double *X = Xrow + (s - sA) * XR::STRIDE;
-      for (int e = lane; e < sidx(P, 0); e += 32) {   // l' < p: the translation operands (XRow)
-        int l = 0;
-        while (sidx(l + 1, 0) <= e) ++l;
-        const int m = e - sidx(l, 0);
-        cd g[3];
-        grad_fast(ps.R, l, m, shc, g);
-        const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2], r = ps.R[e];
-        const double w = __ldg(wS + l * l + l + m);
-        double *o = X + XR::SX + 4 * (l * l + l + m);
-        o[0] = w * r.y;
-        o[1] = w * r.x;
-        o[2] = w * ng.y;
-        o[3] = w * ng.x;
-        if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
-          const double sg = (m & 1) ? -w : w;
-          o = X + XR::SX + 4 * (l * l + l - m);
-          o[0] = -sg * r.y;
-          o[1] = sg * r.x;
-          o[2] = -sg * ng.y;
-          o[3] = sg * ng.x;
-        }
-      }
-      if (lane < 3) X[XR::NU + lane] = nup[lane];
-      __syncwarp();
     }
+    __syncwarp();
+    // solid harmonics of the warp's pairs: lanes (pair, column m)
+    for (int i = lane; i < kPPW * (P + 1); i += 32) {
+      PairState<P> &ps = mine[i / (P + 1)];
+      if (ps.active) r_column<P>(ps.rp[1], ps.rp[2], ps.rp[0], i % (P + 1), ps.R, shc);
+    }
+    __syncwarp();
+    // gradient tables (kept for phase 5), then the translation operands S', NG' (XRow): flat over pairs
+    for (int i = lane; i < kPPW * NS; i += 32) {
+      const int pp = i / NS, e = i % NS;
+      if (!mine[pp].active) continue;
+      int l = 0;
+      while (sidx(l + 1, 0) <= e) ++l;
+      grad_fast(mine[pp].R, l, e - sidx(l, 0), shc, wsc.GS[pp][e]);
+    }
+    __syncwarp();
+    constexpr int NSX = sidx(P, 0);   // l' < p
+    for (int i = lane; i < kPPW * NSX; i += 32) {
+      const int pp = i / NSX, e = i % NSX;
+      PairState<P> &ps = mine[pp];
+      if (!ps.active) continue;
+      int l = 0;
+      while (sidx(l + 1, 0) <= e) ++l;
+      const int m = e - sidx(l, 0);
+      const cd *g = wsc.GS[pp][e];
+      const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
+      const double w = __ldg(wS + l * l + l + m);
+      double *o = Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m);
+      o[0] = w * r.y;
+      o[1] = w * r.x;
+      o[2] = w * ng.y;
+      o[3] = w * ng.x;
+      if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
+        const double sg = (m & 1) ? -w : w;
+        o -= 8 * m;
+        o[0] = -sg * r.y;
+        o[1] = sg * r.x;
+        o[2] = -sg * ng.y;
+        o[3] = sg * ng.x;
+      }
+    }
+    if (lane < 3 * kPPW && mine[lane / 3].active)
+      Xrow[(base + warp * kPPW + lane / 3 - sA) * XR::STRIDE + XR::NU + lane % 3] = mine[lane / 3].nup[lane % 3];
     __syncthreads();
     RRQ_PHASE_MARK(0);
     // ---------------- phase 2: t0 per edge (reading A12, A12'), lanes (pair, edge, comp) = 27 lanes
@@ -426,9 +444,14 @@ __global__ void __launch_bounds__(WPB * 32)
       }
       __syncwarp();
     }
+    if (threadIdx.x == 0) nsw = 0;
     __syncthreads();
     RRQ_PHASE_MARK(1);
     // ---------------- phase 3: weights and the scalar line integrals (Step 6)
+    if (lane < 3 * kPPW) {
+      const PairState<P> &ps = mine[lane / 3];
+      if (ps.active && ps.swap[lane % 3]) swl[atomicAdd(&nsw, 1)] = warp * 3 * kPPW + lane;
+    }
     for (int pp = 0; pp < kPPW; ++pp) {
       PairState<P> &ps = mine[pp];
       if (!ps.active) continue;
@@ -480,91 +503,95 @@ __global__ void __launch_bounds__(WPB * 32)
     }
     __syncthreads();
     RRQ_PHASE_MARK(2);
-    // ---------------- phase 4: Omega_0 on swap edges: sinh-split Gauss-Legendre (reading A9)
-    for (int pp = 0; pp < kPPW; ++pp) {
-      PairState<P> &ps = mine[pp];
-      if (!ps.active) continue;
+    // ---------------- phase 4: Omega_0 on swap edges: sinh-split Gauss-Legendre (reading A9); the round's
+    // swap edges are spread over all warps of the CTA (warp per edge)
+    for (int q = warp; q < nsw; q += WPB) {
+      const int code = swl[q], e = code % 3;
+      PairState<P> &ps = pst[code / 3];
       const double *blk = fit + (int64_t)ps.Pp * L::STRIDE;
       const double rp[3] = {ps.rp[0], ps.rp[1], ps.rp[2]};
       const double u[3] = {0.0, 0.0, ps.u3};
-      double add = 0;
-      for (int e = 0; e < 3; ++e) {
-        if (!ps.swap[e]) continue;
-        const double a = fmin(1.0, fmax(-1.0, ps.t0[e][0])), b = fabs(ps.t0[e][1]);
-        const double sR = asinh((1 - a) / b), sL = asinh((-1 - a) / b);
-        const double *C = blk + L::CM + e * Q * 3;
-        double acc = 0;
-        for (int j = lane; j < 2 * n_omega; j += 32) {
-          const int sdd = j / n_omega, jj = j % n_omega;
-          const double lo = sdd ? 0.0 : sL, hi = sdd ? sR : 0.0;
-          if (!(hi > lo)) continue;
-          const double sv = lo + (hi - lo) * (sxo[jj] + 1) * 0.5, W = (hi - lo) * 0.5 * swo[jj];
-          const double ex = exp(sv), iex = 1.0 / ex;
-          const double tt = a + b * 0.5 * (ex - iex), dt = b * 0.5 * (ex + iex);
-          double x[3], dx[3];
-          leg_r3<Q>(C, tt, x, dx);
-          const double d[3] = {rp[0] - x[0], rp[1] - x[1], rp[2] - x[2]};
-          const double nd = sqrt(dot3(d, d));
-          double dxu[3];
-          cross3(d, u, dxu);
-          acc += W * dt * (-dot3(dxu, dx) / (nd * (nd + dot3(u, d))));
-        }
-        add += warp_sum(acc);
+      const double a = fmin(1.0, fmax(-1.0, ps.t0[e][0])), b = fabs(ps.t0[e][1]);
+      const double sR = asinh((1 - a) / b), sL = asinh((-1 - a) / b);
+      const double *C = blk + L::CM + e * Q * 3;
+      double acc = 0;
+      for (int j = lane; j < 2 * n_omega; j += 32) {
+        const int sdd = j / n_omega, jj = j % n_omega;
+        const double lo = sdd ? 0.0 : sL, hi = sdd ? sR : 0.0;
+        if (!(hi > lo)) continue;
+        const double sv = lo + (hi - lo) * (sxo[jj] + 1) * 0.5, W = (hi - lo) * 0.5 * swo[jj];
+        const double ex = exp(sv), iex = 1.0 / ex;
+        const double tt = a + b * 0.5 * (ex - iex), dt = b * 0.5 * (ex + iex);
+        double x[3], dx[3];
+        leg_r3<Q>(C, tt, x, dx);
+        const double d[3] = {rp[0] - x[0], rp[1] - x[1], rp[2] - x[2]};
+        const double nd = sqrt(dot3(d, d));
+        double dxu[3];
+        cross3(d, u, dxu);
+        acc += W * dt * (-dot3(dxu, dx) / (nd * (nd + dot3(u, d))));
       }
-      if (lane == 0) ps.om[0] += add - (ps.self_local >= 0 ? 2.0 * kPi : 0.0);   // PV shift (reading A7)
+      acc = warp_sum(acc);
+      if (lane == 0) ps.o0e[e] = acc;
     }
     __syncthreads();
     RRQ_PHASE_MARK(3);
     // ---------------- phase 5: I[gamma]: (Omega_0, Omega)(0, grad S(r')), omega
     // first; its nu'-derivative with Hess S nu'; W_gamma = -sqrt2 Im I[gamma]; the
     // S(r') Omega_0 part of Theta (G2).  k_translate adds the lambda_1 / theta_1 parts.
-    for (int pp = 0; pp < kPPW; ++pp) {
+    if (lane < kPPW) {
+      PairState<P> &ps = mine[lane];
+      if (ps.active) {
+        double add = 0;
+        for (int e = 0; e < 3; ++e)
+          if (ps.swap[e]) add += ps.o0e[e];
+        ps.om[0] += add - (ps.self_local >= 0 ? 2.0 * kPi : 0.0);   // PV shift (reading A7)
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < kPPW * NP; i += 32) {
+      const int pp = i / NP, c = i % NP;
       PairState<P> &ps = mine[pp];
       if (!ps.active) continue;
-      const int64_t s = base + warp * kPPW + pp;
-      double *X = Xrow + (s - sA) * XR::STRIDE;
-      for (int e = lane; e < NS; e += 32) {
-        int l = 0;
-        while (sidx(l + 1, 0) <= e) ++l;
-        grad_fast(ps.R, l, e - sidx(l, 0), shc, wsc.GS[e]);
-      }
-      __syncwarp();
+      double *X = Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE;
       const double nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
       const double O0 = ps.om[0], Ov[3] = {ps.om[1], ps.om[2], ps.om[3]}, dO0 = ps.om[4],
                    dOv[3] = {ps.om[5], ps.om[6], ps.om[7]};
-      for (int c = lane; c < NP; c += 32) {
-        int l = 1;
-        while (lmidx(l + 1, 1) <= c) ++l;
-        const int m = c - lmidx(l, 1) + 1, hs = sidx(l, m);
-        const cd *g = wsc.GS[hs];
-        cd hn[3];
-        hess_fast(wsc.GS, l, m, nup, shc, hn);
-        double gs = 0, dgs = 0, gv[3], dgv[3];
-        for (int a = 0; a < 3; ++a) {
-          gs -= Ov[a] * g[a].y;
-          dgs -= dOv[a] * g[a].y + Ov[a] * hn[a].y;
-          const int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
-          gv[a] = O0 * g[a].y + (Ov[b1] * g[b2].y - Ov[b2] * g[b1].y);
-          dgv[a] = dO0 * g[a].y + (dOv[b1] * g[b2].y - dOv[b2] * g[b1].y) + O0 * hn[a].y +
-                   (Ov[b1] * hn[b2].y - Ov[b2] * hn[b1].y);
-        }
-        const double f = -s2 * inv4pi;
-        X[XR::W + c] = f * gs;
-        X[XR::DW + c] = f * dgs;
-        for (int a = 0; a < 3; ++a) {
-          X[XR::W + (1 + a) * NP + c] = f * gv[a];
-          X[XR::DW + (1 + a) * NP + c] = f * dgv[a];
-        }
-        X[XR::TH + c] = s2 * inv4pi * ps.R[hs].y * O0;
+      int l = 1;
+      while (lmidx(l + 1, 1) <= c) ++l;
+      const int m = c - lmidx(l, 1) + 1, hs = sidx(l, m);
+      const cd *g = wsc.GS[pp][hs];
+      cd hn[3];
+      hess_fast(wsc.GS[pp], l, m, nup, shc, hn);
+      double gs = 0, dgs = 0, gv[3], dgv[3];
+      for (int a = 0; a < 3; ++a) {
+        gs -= Ov[a] * g[a].y;
+        dgs -= dOv[a] * g[a].y + Ov[a] * hn[a].y;
+        const int b1 = (a + 1) % 3, b2 = (a + 2) % 3;
+        gv[a] = O0 * g[a].y + (Ov[b1] * g[b2].y - Ov[b2] * g[b1].y);
+        dgv[a] = dO0 * g[a].y + (dOv[b1] * g[b2].y - dOv[b2] * g[b1].y) + O0 * hn[a].y +
+                 (Ov[b1] * hn[b2].y - Ov[b2] * hn[b1].y);
       }
-      if (lane == 0 && pstat) pstat[ps.k - obase] = (ps.conv[0] && ps.conv[1] && ps.conv[2]) ? 0 : 1;
-      nswap += ps.swap[0] + ps.swap[1] + ps.swap[2];
-      __syncwarp();
+      const double f = -s2 * inv4pi;
+      X[XR::W + c] = f * gs;
+      X[XR::DW + c] = f * dgs;
+      for (int a = 0; a < 3; ++a) {
+        X[XR::W + (1 + a) * NP + c] = f * gv[a];
+        X[XR::DW + (1 + a) * NP + c] = f * dgv[a];
+      }
+      X[XR::TH + c] = s2 * inv4pi * ps.R[hs].y * O0;
     }
+    if (lane < kPPW) {
+      PairState<P> &ps = mine[lane];
+      if (ps.active) {
+        if (pstat) pstat[ps.k - obase] = (ps.conv[0] && ps.conv[1] && ps.conv[2]) ? 0 : 1;
+        nswap += ps.swap[0] + ps.swap[1] + ps.swap[2];
+      }
+    }
+    __syncwarp();
     __syncthreads();
     RRQ_PHASE_MARK(4);
   }
-  if (swapcnt && lane == 0 && nswap) atomicAdd(swapcnt, nswap);
+  if (swapcnt && nswap) atomicAdd(swapcnt, nswap);
 }
 
 // ------------------------------------------------------------------------------------------------
