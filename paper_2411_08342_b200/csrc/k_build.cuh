@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(256, 2)
   using L = Layout<P>;
   using CC = ContractCfg<P>;
   constexpr int N = D::N, NP = D::NP, TP = CC::TP, ZS = CC::ZS, NZS = D::NZS, NB = CC::NB, KC = CC::KC;
-  extern __shared__ double sz[];
+  extern __shared__ __align__(16) double sz[];
   double *sB = sz + CC::SMEM_Z;                    // [2][3][KC][NB]
   double *sT = sB + 2 * CC::SMEM_B;                // [TP][8] target x, nu'
   int64_t *sK = reinterpret_cast<int64_t *>(sT + TP * 8);
@@ -999,21 +999,35 @@ __global__ void __launch_bounds__(256, 2)
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *blk = fit + Pp * (int64_t)L::STRIDE;
   const double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
-  // B chunk ch: rows [ch KC, (ch+1) KC) of P_D, P_Sp, P_Sg -> sB[(ch&1)][blk][row][NB] (cp.async, 16 B)
-  auto issue = [&](int ch) {
+  // B chunk ch: rows [ch KC, (ch+1) KC) of P_D, P_Sp, P_Sg -> sB[(ch&1)][blk][row][NB]; the Z tile (rows of
+  // NZS doubles, contiguous in global and in shared memory since ZS == NZS) rides on chunk 0's barrier.
+  // 1-D bulk copies (TMA) issued by warp 0 on mbarriers.
+  static_assert(ZS == NZS, "Z tile staged as one bulk copy");
+  __shared__ uint64_t bar[2];
+  constexpr unsigned ROWB = (unsigned)(N * sizeof(double));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  for (int i = cnt * ZS + threadIdx.x; i < TP * ZS; i += blockDim.x) sz[i] = 0.0;   // absent pairs
+  __syncthreads();
+  auto issue = [&](int ch, unsigned extra) {
+    uint64_t *br = &bar[ch & 1];
+    if (lane == 0) mbar_expect_tx(br, 3u * KC * ROWB + extra);
+    __syncwarp();
     double *dst = sB + (ch & 1) * CC::SMEM_B;
-    const int per_row = N / 2, tot = 3 * KC * per_row;
-    for (int q = threadIdx.x; q < tot; q += blockDim.x) {
-      const int bk = q / (KC * per_row), rr = (q / per_row) % KC, cc = q % per_row;
-      const double *src = (bk == 0 ? PD : (bk == 1 ? PSp : PSg)) + (int64_t)(ch * KC + rr) * N + 2 * cc;
-      cp_async16(dst + (bk * KC + rr) * NB + 2 * cc, src);
+    for (int q = lane; q < 3 * KC; q += 32) {
+      const int bk = q / KC, rr = q % KC;
+      const double *src = (bk == 0 ? PD : (bk == 1 ? PSp : PSg)) + (int64_t)(ch * KC + rr) * N;
+      bulk_g2s(dst + (bk * KC + rr) * NB, src, ROWB, br);
     }
-    cp_async_commit();
   };
-  issue(0);
-  for (int i = threadIdx.x; i < TP * NZS; i += blockDim.x) {
-    const int r = i / NZS, c = i % NZS;
-    sz[r * ZS + c] = r < cnt ? Zrow[(s0 + r - sA) * NZS + c] : 0.0;
+  if (warp == 0) {
+    const unsigned zb = (unsigned)(cnt * NZS * sizeof(double));
+    issue(0, zb);
+    if (lane == 0) bulk_g2s(sz, Zrow + (s0 - sA) * NZS, zb, &bar[0]);
   }
   for (int r = threadIdx.x; r < TP; r += blockDim.x) {
     if (r < cnt) {
@@ -1032,7 +1046,7 @@ __global__ void __launch_bounds__(256, 2)
     }
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  mbar_wait(&bar[0], 0);   // Z tile (and chunk 0)
   const double h = blk[L::HDR + H_H];
   const double inv4pi = 1.0 / (4.0 * kPi);
   double acc[CC::TPW][8];
@@ -1055,13 +1069,11 @@ __global__ void __launch_bounds__(256, 2)
   }
   // the 4 NP blocks, B double-buffered through shared memory
   for (int ch = 0; ch < CC::NCH; ++ch) {
-    if (ch + 1 < CC::NCH) {
-      issue(ch + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    if (warp == 0 && ch + 1 < CC::NCH) {   // buffer (ch+1)&1 was released by the barrier ending ch-1
+      fence_proxy_async();
+      issue(ch + 1, 0);
     }
-    __syncthreads();
+    mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
     const double *bb = sB + (ch & 1) * CC::SMEM_B;
 #pragma unroll
     for (int tw = 0; tw < CC::TPW; ++tw) {

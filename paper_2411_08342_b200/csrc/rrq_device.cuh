@@ -45,7 +45,7 @@ struct Dims {
   static constexpr int NV8 = (2 * NV + 7) / 8 * 8;// V columns (jk, re/im), padded
   static constexpr int NCP = NCQ + NV8;           // whole 8-wide DMMA tiles
   static constexpr int NCS = NCP + ((4 - NCP % 16) + 16) % 16; // row stride == 4 (mod 16): conflict-free B frags
-  static constexpr int NZS = (NZ + 3) / 4 * 4;    // Z row stride (k-steps of 4)
+  static constexpr int NZS = NZ + ((4 - NZ % 16) + 16) % 16;   // Z row stride == 4 (mod 16): conflict-free A frags
 };
 
 // (l, m >= 0) -> flat index
