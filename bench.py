@@ -35,6 +35,26 @@ sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.1      # measured: DMMA m8n8k4 f64, 148 SMs @1965 MHz (profiles/r01_fp64_peak.txt)
 FP64_PEAK_SRC = "measured FP64 peak (DMMA m8n8k4 microbenchmark, profiles/r01_fp64_peak.txt; DFMA chains 34.2)"
+FP64_DFMA_TFLOPS = 34.2      # measured: independent DFMA chains, 8 CTAs/SM (same file)
+# per kernel: which FP64 unit bounds it
+KERNEL_BOUND = {"pair_edge": ("alu", FP64_DFMA_TFLOPS, "measured FP64 DFMA peak (profiles/r01_fp64_peak.txt)"),
+                "translate": ("alu", FP64_DFMA_TFLOPS, "measured FP64 DFMA peak (profiles/r01_fp64_peak.txt)"),
+                "qmap": ("tensor", FP64_PEAK_TFLOPS, "measured FP64 DMMA peak (profiles/r01_fp64_peak.txt)"),
+                "contract": ("tensor", FP64_PEAK_TFLOPS, "measured FP64 DMMA peak (profiles/r01_fp64_peak.txt)")}
+
+
+def traffic_per_launch(kernel, pairs, launches):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (bytes per pair measured
+    there x this run's average pairs per launch), or None."""
+    import json as _j
+    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
+    try:
+        rec = _j.load(open(f)).get("k_" + kernel)
+    except (OSError, ValueError):
+        return None, None
+    if not rec or not launches:
+        return None, None
+    return rec["dram_bytes_per_pair"] * pairs / launches, rec["source"]
 METRIC = "near-correction weights/s (fp64, S/D/S'/D') on 1 B200"
 UNIT = "weights/s"
 
@@ -269,6 +289,10 @@ def run_ours(args, ws, rank):
                   for k, v in kflops.items()}
     dom = max(kflops, key=lambda k: tim["ms"][k])
     achieved = per_kernel[dom]["tflops"]
+    traffic, traffic_src = traffic_per_launch(dom, pairs_t, tim["launches"][dom])
+    for k in per_kernel:
+        per_kernel[k]["bound"], per_kernel[k]["peak"] = KERNEL_BOUND[k][0], KERNEL_BOUND[k][1]
+        per_kernel[k]["frac"] = (per_kernel[k]["tflops"] or 0) / KERNEL_BOUND[k][1]
     build_ms = sum(tim["ms"][k] for k in ("pair_edge", "qmap", "translate", "contract", "plumbing"))
     build_tflops = sum(kflops.values()) / (build_ms / 1e3) / 1e12
     res = {
@@ -277,9 +301,10 @@ def run_ours(args, ws, rank):
         "dtype": "f64", "data": "synthetic (seeded generator synth/configs.py; BASELINE.json configs[3] shape)",
         "config": dict(cfg_desc(cfg, npairs, R.T), parallelism=f"replicas{ws}" if ws > 1 else "single",
                        step="near_list+patch_fit+build(all rows, chunked)", chunk_pairs=args.chunk_pairs),
-        "roofline": {"bound": "alu", "kernel": "k_" + dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                     "peak_source": FP64_PEAK_SRC,
+        "roofline": {"bound": KERNEL_BOUND[dom][0], "kernel": "k_" + dom, "achieved": achieved,
+                     "peak": KERNEL_BOUND[dom][1], "unit": "TFLOP/s", "frac": achieved / KERNEL_BOUND[dom][1],
+                     "traffic": traffic, "traffic_unit": "bytes/launch", "traffic_source": traffic_src,
+                     "peak_source": KERNEL_BOUND[dom][2],
                      "flops_per_pair": kflops[dom] / pairs_t, "launches": tim["launches"][dom],
                      "build_stage_tflops": build_tflops, "build_stage_frac": build_tflops / FP64_PEAK_TFLOPS,
                      "per_kernel": per_kernel},

@@ -93,16 +93,24 @@ struct QRow {
   static constexpr int SV = EQ * D::NQ, SSZ = SV + 2 * D::NV;   // staged (shared-memory) layout
 };
 
-// k_translate's schedule (see k_translate): the j >= 2 translation terms of all c = (l, m).
+// k_translate's schedule (see k_translate): tasks = pairs of outputs (l, m0), (l, m0 + 1) (or a single
+// (l, l)); a task's terms are the (j, k), j >= 2, in the union of the two outputs' k ranges.
 __host__ __device__ constexpr int tr_nterms(int P) {
   int n = 0;
   for (int l = 2; l <= P; ++l)
-    for (int m = 1; m <= l; ++m)
+    for (int m = 1; m <= l; m += 2) {
+      const int m1 = m + 1 <= l ? m + 1 : m;
       for (int j = 2; j <= l; ++j) {
         const int lj = l - j;
-        const int kmin = (-j > m - lj) ? -j : m - lj, kmax = (j < m + lj) ? j : m + lj;
+        const int kmin = (-j > m - lj) ? -j : m - lj, kmax = (j < m1 + lj) ? j : m1 + lj;
         n += kmax - kmin + 1;
       }
+    }
+  return n;
+}
+__host__ __device__ constexpr int tr_ntasks(int P) {
+  int n = 0;
+  for (int l = 2; l <= P; ++l) n += (l + 1) / 2;
   return n;
 }
 
@@ -110,9 +118,9 @@ template <int P>
 struct TrCfg {
   using D = Dims<P>;
   static constexpr int NT = tr_nterms(P), STEPS = (NT + 31) / 32;
-  static constexpr int MAXSLOT = D::NP + 32, SLOTW = 9;
+  static constexpr int MAXSLOT = tr_ntasks(P) + 32, SLOTW = 18;  // slot: 2 outputs x (theta, lambda[4], dlambda[4])
   static constexpr int SXW = 6;                                  // smem (S'.y, S'.x, NG'.y, NG'.x | pad): 48 B
-  static constexpr int SXSZ = SXW * (P * P + 1);                 // + one zero entry for padding terms
+  static constexpr int SXSZ = SXW * (P * P + 1);                 // + one zero entry for absent outputs / padding
   static constexpr int QSZ = QRow<P>::SSZ, GSZ = XRow<P>::GSZ;
   static constexpr int PER_WARP = (2 * QSZ + 2 * SXSZ + GSZ + SLOTW * MAXSLOT + 1) / 2 * 2;
   // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 cinfo [NP] |
@@ -124,9 +132,10 @@ struct TrCfg {
   static constexpr int WPB_FIT = (SMEM_MAX / 8 - TAB_D) / PER_WARP;
   static constexpr int WPB = WPB_FIT > 8 ? 8 : WPB_FIT;
   static constexpr size_t SMEM = (size_t)(TAB_D + WPB * PER_WARP) * sizeof(double);
-  static constexpr uint32_t FA = 1u << 14, FB = 1u << 15, FLUSH = 1u << 16;   // code bits
+  // code: qidx(j,|k|) | se0 << 7 | se1 << 14 | FA | FB | FLUSH | slot << 24
+  static constexpr uint32_t FA = 1u << 21, FB = 1u << 22, FLUSH = 1u << 23;
   static_assert(WPB >= 2, "translate smem");
-  static_assert(MAXSLOT < 2048 && D::NQ < 128 && P * P < 128, "translate code fields");
+  static_assert(MAXSLOT < 256 && D::NQ < 128 && P * P < 128, "translate code fields");
 };
 
 // D = A B + C for one 8x8x4 fp64 tile (FP64 tensor core, SASS DMMA).  Fragments: a = A[lane/4][lane%4],
@@ -792,18 +801,21 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, 2)
 // S' = w S (expanded over m' < 0), so the inner loop is pure FMAs on the Im parts (only Im(lambda),
 // Im(theta) enter W, dW, Theta): Im(A S) = A.x S.y + A.y S.x, with A^{(j,-k)} = (-1)^k conj A^{(j,k)} folded
 // into sign flips of (S.y, S.x).
-// One warp per pair.  The j >= 2 terms (c-major) are split into 32 contiguous equal runs, one per lane
-// (host-built schedule, make_trtab in rrq_api.cu, ordered within each c to spread shared-memory banks), so
-// every lane executes the same STEPS steps; a c's partial sums are flushed to a slot where the lane's run
-// of that c ends, and the epilogue (lanes over c) sums a c's slots, adds the j = 1 theta terms and the
-// gamma parts and writes zeta.  Rows are prefetched with cp.async one pair ahead.
+// One warp per pair.  The outputs are taken in pairs (l, m0), (l, m0 + 1) (tasks) so that every Q / dQ / V
+// entry loaded from shared memory feeds two outputs (shared-memory bandwidth is this kernel's bound); a
+// task's terms (j, k), j >= 2, span the union of its outputs' k ranges (an output outside its range reads
+// the zero S' entry).  The terms (task-major) are split into 32 contiguous equal runs, one per lane
+// (host-built schedule, make_trtab in rrq_api.cu, ordered within each task to spread shared-memory banks),
+// so every lane executes the same STEPS steps; a task's partial sums are flushed to a slot where the
+// lane's run of it ends, and the epilogue (lanes over c) sums a c's slots, adds the j = 1 theta terms and
+// the gamma parts and writes zeta.  Rows are prefetched with cp.async one pair ahead.
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ double flip_if(double x, uint32_t bit) {
   return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)bit << 63));
 }
 
 struct TrOps {
-  double2 s, g, v, q[4], dq[4];
+  double2 s0, g0, s1, g1, v, q[4], dq[4];
   uint32_t cw;
 };
 
@@ -828,7 +840,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   const double *olam = sm + C::OLAM, *oth = sm + C::OTH;
   const int64_t stride = (int64_t)gridDim.x * WPB;
 
-  auto issue_qs = [&](int64_t s, int b) {   // Q row (linear) and the S'/NG' block (stride 4 -> SXW)
+  auto issue_qs = [&](int64_t s, int b) {   // Q row (entries re-strided to EQ) and the S'/NG' block (4 -> SXW)
     const double *qg = Qrow + (s - sA) * QR::STRIDE, *xg = Xrow + (s - sA) * XR::STRIDE + XR::SX;
     double *qd = QB + b * C::QSZ, *sd = SXB + b * C::SXSZ;
     for (int i = lane; i < 8 * D::NQ; i += 32) cp_async16(qd + EQ * (i >> 3) + 2 * (i & 7), qg + 2 * i);
@@ -854,12 +866,14 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     cp_async_wait<1>();
     __syncwarp();
     const double *qb = QB + cb * C::QSZ, *sx = SXB + cb * C::SXSZ;
-    // main loop, software-pipelined one step ahead
+    // main loop: each step one (j, k) term of this lane's task for both of its outputs; software-pipelined
     auto load = [&](TrOps &o, uint32_t cw) {
       o.cw = cw;
-      const int qe = cw & 127, se = (cw >> 7) & 127;
-      o.s = *reinterpret_cast<const double2 *>(sx + SXW * se);
-      o.g = *reinterpret_cast<const double2 *>(sx + SXW * se + 2);
+      const int qe = cw & 127, e0 = (cw >> 7) & 127, e1 = (cw >> 14) & 127;
+      o.s0 = *reinterpret_cast<const double2 *>(sx + SXW * e0);
+      o.g0 = *reinterpret_cast<const double2 *>(sx + SXW * e0 + 2);
+      o.s1 = *reinterpret_cast<const double2 *>(sx + SXW * e1);
+      o.g1 = *reinterpret_cast<const double2 *>(sx + SXW * e1 + 2);
       o.v = *reinterpret_cast<const double2 *>(qb + QR::SV + 2 * (qe + 2));   // vidx(j,k) = qidx(j,k) + 2
       const double *e = qb + EQ * qe;
 #pragma unroll
@@ -868,34 +882,41 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
         o.dq[b] = *reinterpret_cast<const double2 *>(e + 8 + 2 * b);
       }
     };
-    double th = 0, lam[4] = {0, 0, 0, 0}, dla[4] = {0, 0, 0, 0}, dlb[4] = {0, 0, 0, 0};
+    double th[2] = {0, 0}, lam[2][4] = {}, dla[2][4] = {}, dlb[2][4] = {};
     TrOps cur, nxt;
     load(cur, code[lane]);
-#pragma unroll 2
+#pragma unroll
     for (int t = 0; t < C::STEPS; ++t) {
       if (t + 1 < C::STEPS) load(nxt, code[(t + 1) * 32 + lane]);
-      const uint32_t cw = cur.cw, fa = (cw >> 14) & 1, fb = (cw >> 15) & 1;
-      const double A = flip_if(cur.s.x, fa), B = flip_if(cur.s.y, fb);
-      const double An = flip_if(cur.g.x, fa), Bn = flip_if(cur.g.y, fb);
-      th = fma(cur.v.x, A, fma(cur.v.y, B, th));
+      const uint32_t cw = cur.cw, fa = (cw >> 21) & 1, fb = (cw >> 22) & 1;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        lam[b] = fma(cur.q[b].x, A, fma(cur.q[b].y, B, lam[b]));
-        dla[b] = fma(cur.dq[b].x, A, fma(cur.dq[b].y, B, dla[b]));
-        dlb[b] = fma(cur.q[b].x, An, fma(cur.q[b].y, Bn, dlb[b]));
-      }
-      if (cw & C::FLUSH) {
-        double *d = SL + C::SLOTW * (cw >> 20);
-        d[0] = th;
-        th = 0;
+      for (int o = 0; o < 2; ++o) {
+        const double2 sv = o ? cur.s1 : cur.s0, gv = o ? cur.g1 : cur.g0;
+        const double A = flip_if(sv.x, fa), B = flip_if(sv.y, fb);
+        const double An = flip_if(gv.x, fa), Bn = flip_if(gv.y, fb);
+        th[o] = fma(cur.v.x, A, fma(cur.v.y, B, th[o]));
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          d[1 + b] = lam[b];
-          d[5 + b] = dla[b] + dlb[b];
-          lam[b] = dla[b] = dlb[b] = 0;
+          lam[o][b] = fma(cur.q[b].x, A, fma(cur.q[b].y, B, lam[o][b]));
+          dla[o][b] = fma(cur.dq[b].x, A, fma(cur.dq[b].y, B, dla[o][b]));
+          dlb[o][b] = fma(cur.q[b].x, An, fma(cur.q[b].y, Bn, dlb[o][b]));
         }
       }
-      cur = nxt;
+      if (cw & C::FLUSH) {
+        double *d = SL + C::SLOTW * (cw >> 24);
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          d[9 * o] = th[o];
+          th[o] = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            d[9 * o + 1 + b] = lam[o][b];
+            d[9 * o + 5 + b] = dla[o][b] + dlb[o][b];
+            lam[o][b] = dla[o][b] = dlb[o][b] = 0;
+          }
+        }
+      }
+      if (t + 1 < C::STEPS) cur = nxt;
     }
     __syncwarp();
     // epilogue: lanes over c = (l, m); gamma parts from GB (W [4][NP], dW [4][NP], Theta [NP], nu')
@@ -903,10 +924,10 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     double *Z = Zrow + (s - sA) * NZS;
     for (int c = lane; c < NP; c += 32) {
       const uint32_t ci = cinfo[c];
-      const int l = ci & 15, m = (ci >> 4) & 15, sb = (ci >> 8) & 2047, sc = ci >> 19;
+      const int l = ci & 15, m = (ci >> 4) & 15, sb = (ci >> 8) & 255, sc = (ci >> 16) & 255, hf = (ci >> 24) & 1;
       double T = 0, L[4] = {0, 0, 0, 0}, DL[4] = {0, 0, 0, 0};
       for (int q = 0; q < sc; ++q) {
-        const double *d = SL + C::SLOTW * (sb + q);
+        const double *d = SL + C::SLOTW * (sb + q) + 9 * hf;
         T += d[0];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {

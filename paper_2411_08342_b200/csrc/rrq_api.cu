@@ -129,11 +129,13 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 
 // Exported functions get C linkage from their declarations in include/rrq.h.
 
-// k_translate's host-built table (TrCfg<P>): the j >= 2 translation terms of every c = (l, m) in c-major
-// order, split into 32 contiguous runs of equal length (one per lane), each term encoded as
-// qidx(j,|k|) | (l'^2 + l' + m') << 7 | sign flips of (S.y, S.x) for k < 0 | flush | slot << 20 (padding
-// terms point at the zero S' entry p^2); cinfo[c] = l | m << 4 | first slot << 8 | slot count << 19; and the
-// separable scale factors v_lambda(j,k) = (j-2)!/F(j,k), v_theta(j,k) = (j-1)!/F(j,k), w(l',m') = l'!/F(l',m'),
+// k_translate's host-built table (TrCfg<P>): tasks = output pairs (l, m0), (l, m0 + 1) (a single (l, l)
+// when l is odd), task-major, each task's j >= 2 terms over the union of its outputs' k ranges; the term
+// list is split into 32 contiguous runs of equal length (one per lane).  A term is encoded as
+// qidx(j,|k|) | se0 << 7 | se1 << 14 | sign flips of (S.y, S.x) for k < 0 | flush | slot << 24, se = l'^2 + l' + m'
+// of the S' entry of each output (p^2 = the zero entry when the output does not take the term; padding
+// terms are all-zero-entry).  cinfo[c] = l | m << 4 | first slot << 8 | slot count << 16 | half << 24.
+// Scale factors: v_lambda(j,k) = (j-2)!/F(j,k), v_theta(j,k) = (j-1)!/F(j,k), w(l',m') = l'!/F(l',m'),
 // u_lambda(l,m) = F(l,m)/(l-1)!, u_theta(l,m) = F(l,m)/l!, F(a,b) = sqrt((a+b)! (a-b)!).
 // Within a run the order of terms is free; it is chosen greedily so that, at each step, the 8 lanes of a
 // quarter-warp read Q entries (16-B bank group qidx mod 8) and S' entries (3 se mod 8) in distinct groups.
@@ -141,42 +143,50 @@ template <int P>
 static std::vector<double> make_trtab() {
   using C = TrCfg<P>;
   using D = Dims<P>;
-  struct Term { int c, l, m, j, k, qe, se; };
+  constexpr int ZE = P * P;
+  struct Term { int task, qe, se0, se1, k; };
+  struct Task { int l, m0, m1; };
   std::vector<Term> terms;
+  std::vector<Task> tasks;
+  auto sidx2 = [](int lp, int mp) { return (mp < -lp || mp > lp) ? ZE : lp * lp + lp + mp; };
   for (int l = 2; l <= P; ++l)
-    for (int m = 1; m <= l; ++m)
+    for (int m = 1; m <= l; m += 2) {
+      const int m1 = m + 1 <= l ? m + 1 : -1, tk = (int)tasks.size();
+      tasks.push_back({l, m, m1});
       for (int j = 2; j <= l; ++j) {
-        const int lj = l - j;
-        for (int k = std::max(-j, m - lj); k <= std::min(j, m + lj); ++k)
-          terms.push_back({lmidx(l, m), l, m, j, k, qidx(j, std::abs(k)), lj * lj + lj + m - k});
+        const int lj = l - j, mh = m1 > 0 ? m1 : m;
+        for (int k = std::max(-j, m - lj); k <= std::min(j, mh + lj); ++k)
+          terms.push_back({tk, qidx(j, std::abs(k)), sidx2(lj, m - k), m1 > 0 ? sidx2(lj, m1 - k) : ZE, k});
       }
+    }
   const int NT = (int)terms.size();
   std::vector<int> beg(33);
   for (int L = 0; L <= 32; ++L) beg[L] = L * (NT / 32) + std::min(L, NT % 32);
-  // runs (lane, c) -> slots numbered in (c, lane) order so a c's slots are contiguous
-  struct Run { int c, lane, first, last; };
+  // runs (lane, task) -> slots numbered in (task, lane) order so a task's slots are contiguous
+  struct Run { int task, lane, first, last; };
   std::vector<Run> runs;
   for (int L = 0; L < 32; ++L) {
     int f = beg[L];
     for (int i = beg[L]; i < beg[L + 1]; ++i)
-      if (i + 1 == beg[L + 1] || terms[i + 1].c != terms[i].c) {
-        runs.push_back({terms[i].c, L, f, i});
+      if (i + 1 == beg[L + 1] || terms[i + 1].task != terms[i].task) {
+        runs.push_back({terms[i].task, L, f, i});
         f = i + 1;
       }
   }
-  std::stable_sort(runs.begin(), runs.end(), [](const Run &a, const Run &b) { return a.c < b.c; });
-  std::vector<int> slot_of(NT, -1), run_of(NT, -1), sbeg(D::NP, 0), scnt(D::NP, 0);
+  std::stable_sort(runs.begin(), runs.end(), [](const Run &a, const Run &b) { return a.task < b.task; });
+  const int NTK = (int)tasks.size();
+  std::vector<int> slot_of(NT, -1), run_of(NT, -1), sbeg(NTK, 0), scnt(NTK, 0);
   for (int r = 0; r < (int)runs.size(); ++r) {
     slot_of[runs[r].last] = r;
     for (int i = runs[r].first; i <= runs[r].last; ++i) run_of[i] = r;
-    if (scnt[runs[r].c]++ == 0) sbeg[runs[r].c] = r;
+    if (scnt[runs[r].task]++ == 0) sbeg[runs[r].task] = r;
   }
   // greedy bank-aware order within runs: pos -> term index
   std::vector<int> order(NT);
   std::vector<char> used(NT, 0);
   for (int t = 0; t < C::STEPS; ++t)
     for (int q = 0; q < 4; ++q) {
-      std::vector<int> qg, sg;   // (qe, group) and (se, group) chosen so far in this quarter at step t
+      std::vector<int> qg, sg;   // entries chosen so far in this quarter at step t
       for (int L = 8 * q; L < 8 * q + 8; ++L) {
         const int pos = beg[L] + t;
         if (pos >= beg[L + 1]) continue;
@@ -185,33 +195,40 @@ static std::vector<double> make_trtab() {
         for (int i = r.first; i <= r.last; ++i) {
           if (used[i]) continue;
           int cost = 0;
-          for (size_t a = 0; a < qg.size(); ++a)
-            if (qg[a] != terms[i].qe && (qg[a] - terms[i].qe) % 8 == 0) ++cost;
-          for (size_t a = 0; a < sg.size(); ++a)
-            if (sg[a] != terms[i].se && (sg[a] - terms[i].se) % 8 == 0) ++cost;
+          for (int a : qg)
+            if (a != terms[i].qe && (a - terms[i].qe) % 8 == 0) ++cost;
+          for (int a : sg) {
+            if (a != terms[i].se0 && (a - terms[i].se0) % 8 == 0) ++cost;
+            if (a != terms[i].se1 && (a - terms[i].se1) % 8 == 0) ++cost;
+          }
           if (cost < bc) { bc = cost; best = i; }
         }
         used[best] = 1;
         order[pos] = best;
         qg.push_back(terms[best].qe);
-        sg.push_back(terms[best].se);
+        sg.push_back(terms[best].se0);
+        sg.push_back(terms[best].se1);
       }
     }
-  std::vector<uint32_t> w(C::STEPS * 32 + D::NP, (uint32_t)(P * P) << 7);   // padding: zero S' entry
+  std::vector<uint32_t> w(C::STEPS * 32 + D::NP, (uint32_t)ZE << 7 | (uint32_t)ZE << 14);   // padding terms
   for (int L = 0; L < 32; ++L)
     for (int pos = beg[L]; pos < beg[L + 1]; ++pos) {
       const Term &t = terms[order[pos]];
       const int ak = std::abs(t.k);
-      uint32_t cw = (uint32_t)t.qe | (uint32_t)t.se << 7;
+      uint32_t cw = (uint32_t)t.qe | (uint32_t)t.se0 << 7 | (uint32_t)t.se1 << 14;
       if (t.k < 0) cw |= (ak & 1) ? C::FA : C::FB;
-      if (slot_of[pos] >= 0) cw |= C::FLUSH | (uint32_t)slot_of[pos] << 20;
+      if (slot_of[pos] >= 0) cw |= C::FLUSH | (uint32_t)slot_of[pos] << 24;
       w[(pos - beg[L]) * 32 + L] = cw;
     }
-  for (int l = 1; l <= P; ++l)
-    for (int m = 1; m <= l; ++m) {
-      const int c = lmidx(l, m);
-      w[C::STEPS * 32 + c] = (uint32_t)l | (uint32_t)m << 4 | (uint32_t)sbeg[c] << 8 | (uint32_t)scnt[c] << 19;
+  for (int tk = 0; tk < NTK; ++tk)
+    for (int hf = 0; hf < 2; ++hf) {
+      const int m = hf ? tasks[tk].m1 : tasks[tk].m0;
+      if (m < 0) continue;
+      const int l = tasks[tk].l;
+      w[C::STEPS * 32 + lmidx(l, m)] = (uint32_t)l | (uint32_t)m << 4 | (uint32_t)sbeg[tk] << 8 |
+                                       (uint32_t)scnt[tk] << 16 | (uint32_t)hf << 24;
     }
+  w[C::STEPS * 32 + lmidx(1, 1)] = 1u | 1u << 4;   // (1,1): j = 1 terms only (no slots)
   auto fact = [](int n) { long double f = 1; for (int i = 2; i <= n; ++i) f *= i; return f; };
   auto F = [&](int a, int b) { const int ab = std::abs(b); return std::sqrt(fact(a + ab) * fact(a - ab)); };
   std::vector<double> out(C::TAB_D, 0.0);
