@@ -695,12 +695,12 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, 2)
   }
   __syncthreads();
   // stage A (row r < TP -> a-row of pair s0 + r; row TP + r -> b-row) and chunk 0 of M on bar[0]
-  if (warp == 0) {
-    if (lane == 0) mbar_expect_tx(&bar[0], 2u * cnt * ROWB + CHB);
-    __syncwarp();
-    for (int r = lane; r < 2 * TP; r += 32)
+  // (a bulk copy takes uniform operands: one issuing lane per warp, rows spread over the warps)
+  if (threadIdx.x == 0) mbar_expect_tx(&bar[0], 2u * cnt * ROWB + CHB);
+  if (lane == 0) {
+    for (int r = warp; r < 2 * TP; r += C::WARPS)
       if (r % TP < cnt) bulk_g2s(sA_ + r * KA, Arow + (s0 + r % TP - sA) * 2 * K + (r / TP) * K, ROWB, &bar[0]);
-    if (lane == 0) bulk_g2s(sB, M, CHB, &bar[0]);
+    if (warp == C::WARPS - 1) bulk_g2s(sB, M, CHB, &bar[0]);
   }
   const int ns = warp / (C::PG / C::GPW), g0 = (warp % (C::PG / C::GPW)) * C::GPW;
   __shared__ double ssc[D::NQ + D::NV];   // v_lambda | v_theta
@@ -1034,21 +1034,24 @@ __global__ void __launch_bounds__(256, 2)
   }
   for (int i = cnt * ZS + threadIdx.x; i < TP * ZS; i += blockDim.x) sz[i] = 0.0;   // absent pairs
   __syncthreads();
+  // called by every warp: lane 0 of warp w issues rows w, w + WARPS, ... (a bulk copy takes uniform operands,
+  // so one issuing lane per warp; spreading the rows keeps any one warp from stalling the barrier)
   auto issue = [&](int ch, unsigned extra) {
     uint64_t *br = &bar[ch & 1];
-    if (lane == 0) mbar_expect_tx(br, 3u * KC * ROWB + extra);
-    __syncwarp();
-    double *dst = sB + (ch & 1) * CC::SMEM_B;
-    for (int q = lane; q < 3 * KC; q += 32) {
-      const int bk = q / KC, rr = q % KC;
-      const double *src = (bk == 0 ? PD : (bk == 1 ? PSp : PSg)) + (int64_t)(ch * KC + rr) * N;
-      bulk_g2s(dst + (bk * KC + rr) * NB, src, ROWB, br);
+    if (threadIdx.x == 0) mbar_expect_tx(br, 3u * KC * ROWB + extra);
+    if (lane == 0) {
+      double *dst = sB + (ch & 1) * CC::SMEM_B;
+      for (int q = warp; q < 3 * KC; q += CC::WARPS) {
+        const int bk = q / KC, rr = q % KC;
+        const double *src = (bk == 0 ? PD : (bk == 1 ? PSp : PSg)) + (int64_t)(ch * KC + rr) * N;
+        bulk_g2s(dst + (bk * KC + rr) * NB, src, ROWB, br);
+      }
     }
   };
-  if (warp == 0) {
+  {
     const unsigned zb = (unsigned)(cnt * NZS * sizeof(double));
     issue(0, zb);
-    if (lane == 0) bulk_g2s(sz, Zrow + (s0 - sA) * NZS, zb, &bar[0]);
+    if (threadIdx.x == 32) bulk_g2s(sz, Zrow + (s0 - sA) * NZS, zb, &bar[0]);
   }
   for (int r = threadIdx.x; r < TP; r += blockDim.x) {
     if (r < cnt) {
@@ -1082,16 +1085,23 @@ __global__ void __launch_bounds__(256, 2)
     if (tile >= CC::TILES) continue;
     const int mt = tile % CC::MT, nt = tile / CC::MT, bn = nt * 8 + (lane >> 2);
     const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3);
-    for (int k0 = 0; k0 < NP; k0 += 4) {
-      const int kk = k0 + (lane & 3);
-      const double bb = (bn < N && kk < NP) ? __ldg(PSd + kk * N + bn) : 0.0;
-      dmma(acc[tw][0], acc[tw][1], kk < NP ? zr[k0] : 0.0, bb);
+    constexpr int NK = (NP + 3) / 4;
+    double bq[NK];
+#pragma unroll
+    for (int q = 0; q < NK; ++q) {   // all loads first (latency overlapped), then the DMMAs
+      const int kk = 4 * q + (lane & 3);
+      bq[q] = (bn < N && kk < NP) ? __ldg(PSd + kk * N + bn) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < NK; ++q) {
+      const int kk = 4 * q + (lane & 3);
+      dmma(acc[tw][0], acc[tw][1], kk < NP ? zr[4 * q] : 0.0, bq[q]);
     }
   }
   // the 4 NP blocks, B double-buffered through shared memory
   for (int ch = 0; ch < CC::NCH; ++ch) {
-    if (warp == 0 && ch + 1 < CC::NCH) {   // buffer (ch+1)&1 was released by the barrier ending ch-1
-      fence_proxy_async();
+    if (ch + 1 < CC::NCH) {   // buffer (ch+1)&1 was released by the barrier ending ch-1
+      if (lane == 0) fence_proxy_async();
       issue(ch + 1, 0);
     }
     mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
