@@ -119,10 +119,12 @@ struct TrCfg {
   using D = Dims<P>;
   static constexpr int NT = tr_nterms(P), STEPS = (NT + 31) / 32;
   static constexpr int MAXSLOT = tr_ntasks(P) + 32, SLOTW = 18;  // slot: 2 outputs x (theta, lambda[4], dlambda[4])
+  static constexpr int SMAX = P <= 4 ? 10 : (P <= 6 ? 8 : (P <= 8 ? 5 : 4));   // max slots of a task (host-checked)
+  static constexpr int ZSLOT = MAXSLOT;                          // an all-zero slot
   static constexpr int SXW = 6;                                  // smem (S'.y, S'.x, NG'.y, NG'.x | pad): 48 B
   static constexpr int SXSZ = SXW * (P * P + 1);                 // + one zero entry for absent outputs / padding
   static constexpr int QSZ = QRow<P>::SSZ, GSZ = XRow<P>::GSZ;
-  static constexpr int PER_WARP = (2 * QSZ + 2 * SXSZ + GSZ + SLOTW * MAXSLOT + 1) / 2 * 2;
+  static constexpr int PER_WARP = (2 * QSZ + 2 * SXSZ + GSZ + SLOTW * (MAXSLOT + 1) + 1) / 2 * 2;
   // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 cinfo [NP] |
   // f64 vlam [NQ], vth [NV], wS [P*P], olam [NP], oth [NP]
   static constexpr int NWORD = STEPS * 32 + D::NP, TABW = (NWORD + 1) / 2;
@@ -834,6 +836,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   double *wb = sm + C::TAB_D + (size_t)warp * C::PER_WARP;
   double *QB = wb, *SXB = QB + 2 * C::QSZ, *GB = SXB + 2 * C::SXSZ, *SL = GB + C::GSZ;
   if (lane < 2 * SXW) SXB[(lane / SXW) * C::SXSZ + SXW * P * P + lane % SXW] = 0.0;   // zero entries
+  if (lane < C::SLOTW) SL[C::SLOTW * C::ZSLOT + lane] = 0.0;                          // zero slot
   __syncthreads();
   const uint32_t *code = reinterpret_cast<const uint32_t *>(sm);
   const uint32_t *cinfo = code + C::STEPS * 32;
@@ -926,8 +929,9 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
       const uint32_t ci = cinfo[c];
       const int l = ci & 15, m = (ci >> 4) & 15, sb = (ci >> 8) & 255, sc = (ci >> 16) & 255, hf = (ci >> 24) & 1;
       double T = 0, L[4] = {0, 0, 0, 0}, DL[4] = {0, 0, 0, 0};
-      for (int q = 0; q < sc; ++q) {
-        const double *d = SL + C::SLOTW * (sb + q) + 9 * hf;
+#pragma unroll
+      for (int q = 0; q < C::SMAX; ++q) {   // uniform trip count (absent slots read the zero slot)
+        const double *d = SL + C::SLOTW * (q < sc ? sb + q : C::ZSLOT) + 9 * hf;
         T += d[0];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -935,10 +939,11 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
           DL[b] += d[5 + b];
         }
       }
-      // j = 1 theta terms (no lambda part: C_1 = 0)
-      const int kmin = max(-1, m - (l - 1)), kmax = min(1, m + (l - 1));
-      for (int k = kmin; k <= kmax; ++k) {
-        const int lp = l - 1, se = lp * lp + lp + m - k;
+      // j = 1 theta terms (no lambda part: C_1 = 0); |m - k| > l - 1 reads the zero S' entry
+#pragma unroll
+      for (int k = -1; k <= 1; ++k) {
+        const int lp = l - 1, mp = m - k;
+        const int se = (mp >= -lp && mp <= lp) ? lp * lp + lp + mp : P * P;
         const double *vv = qb + QR::SV + 2 * vidx(1, k < 0 ? -k : k);
         const double A = k < 0 ? -sx[SXW * se] : sx[SXW * se], B = sx[SXW * se + 1];
         T = fma(vv[0], A, fma(vv[1], B, T));

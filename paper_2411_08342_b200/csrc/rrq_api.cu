@@ -181,6 +181,11 @@ static std::vector<double> make_trtab() {
     for (int i = runs[r].first; i <= runs[r].last; ++i) run_of[i] = r;
     if (scnt[runs[r].task]++ == 0) sbeg[runs[r].task] = r;
   }
+  for (int tk = 0; tk < NTK; ++tk)
+    if (scnt[tk] > C::SMAX) {
+      std::fprintf(stderr, "rrq: translate schedule needs %d slots per task > SMAX %d\n", scnt[tk], C::SMAX);
+      std::abort();
+    }
   // greedy bank-aware order within runs: pos -> term index
   std::vector<int> order(NT);
   std::vector<char> used(NT, 0);
