@@ -125,9 +125,10 @@ struct TrCfg {
   static constexpr int SXSZ = SXW * (P * P + 1);                 // + one zero entry for absent outputs / padding
   static constexpr int QSZ = QRow<P>::SSZ, GSZ = XRow<P>::GSZ;
   static constexpr int PER_WARP = (2 * QSZ + 2 * SXSZ + GSZ + SLOTW * (MAXSLOT + 1) + 1) / 2 * 2;
-  // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 cinfo [NP] |
+  // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 cinfo [NP], u8 shared-memory
+  // positions of the Q entries [NQ] and of the S' entries [P*P] |
   // f64 vlam [NQ], vth [NV], wS [P*P], olam [NP], oth [NP]
-  static constexpr int NWORD = STEPS * 32 + D::NP, TABW = (NWORD + 1) / 2;
+  static constexpr int NWORD = STEPS * 32 + D::NP + (D::NQ + P * P + 3) / 4, TABW = (NWORD + 1) / 2;
   static constexpr int VLAM = TABW, VTH = VLAM + D::NQ, WS = VTH + D::NV, OLAM = WS + P * P, OTH = OLAM + D::NP;
   static constexpr int TAB_D = (OTH + D::NP + 1) / 2 * 2;
   static constexpr int SMEM_MAX = 224 * 1024;
@@ -840,15 +841,20 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   __syncthreads();
   const uint32_t *code = reinterpret_cast<const uint32_t *>(sm);
   const uint32_t *cinfo = code + C::STEPS * 32;
+  const uint8_t *posq = reinterpret_cast<const uint8_t *>(cinfo + NP), *poss = posq + D::NQ;
   const double *olam = sm + C::OLAM, *oth = sm + C::OTH;
   const int64_t stride = (int64_t)gridDim.x * WPB;
 
-  auto issue_qs = [&](int64_t s, int b) {   // Q row (entries re-strided to EQ) and the S'/NG' block (4 -> SXW)
+  // Q row (entry e -> position posq[e] at stride EQ; V of (j >= 2, k) next to it) and the S'/NG' block
+  // (entry e -> position poss[e] at stride SXW): positions chosen by the host to spread the main loop's
+  // shared-memory banks
+  auto issue_qs = [&](int64_t s, int b) {
     const double *qg = Qrow + (s - sA) * QR::STRIDE, *xg = Xrow + (s - sA) * XR::STRIDE + XR::SX;
     double *qd = QB + b * C::QSZ, *sd = SXB + b * C::SXSZ;
-    for (int i = lane; i < 8 * D::NQ; i += 32) cp_async16(qd + EQ * (i >> 3) + 2 * (i & 7), qg + 2 * i);
-    for (int i = lane; i < D::NV; i += 32) cp_async16(qd + QR::SV + 2 * i, qg + QR::V + 2 * i);
-    for (int i = lane; i < 2 * P * P; i += 32) cp_async16(sd + SXW * (i >> 1) + 2 * (i & 1), xg + 2 * i);
+    for (int i = lane; i < 8 * D::NQ; i += 32) cp_async16(qd + EQ * posq[i >> 3] + 2 * (i & 7), qg + 2 * i);
+    for (int i = lane; i < D::NV; i += 32)
+      cp_async16(qd + QR::SV + 2 * (i < 2 ? i : posq[i - 2] + 2), qg + QR::V + 2 * i);
+    for (int i = lane; i < 2 * P * P; i += 32) cp_async16(sd + SXW * poss[i >> 1] + 2 * (i & 1), xg + 2 * i);
   };
   auto issue_g = [&](int64_t s) {
     const double *xg = Xrow + (s - sA) * XR::STRIDE + XR::G;
@@ -905,18 +911,22 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
           dlb[o][b] = fma(cur.q[b].x, An, fma(cur.q[b].y, Bn, dlb[o][b]));
         }
       }
-      if (cw & C::FLUSH) {
-        double *d = SL + C::SLOTW * (cw >> 24);
+      if (cw & C::FLUSH) {   // slot = [th0 lam0[4] dl0[4] | th1 lam1[4] dl1[4]], 16-B stores
+        double2 *d = reinterpret_cast<double2 *>(SL + C::SLOTW * (cw >> 24));
+        d[0] = make_double2(th[0], lam[0][0]);
+        d[1] = make_double2(lam[0][1], lam[0][2]);
+        d[2] = make_double2(lam[0][3], dla[0][0] + dlb[0][0]);
+        d[3] = make_double2(dla[0][1] + dlb[0][1], dla[0][2] + dlb[0][2]);
+        d[4] = make_double2(dla[0][3] + dlb[0][3], th[1]);
+        d[5] = make_double2(lam[1][0], lam[1][1]);
+        d[6] = make_double2(lam[1][2], lam[1][3]);
+        d[7] = make_double2(dla[1][0] + dlb[1][0], dla[1][1] + dlb[1][1]);
+        d[8] = make_double2(dla[1][2] + dlb[1][2], dla[1][3] + dlb[1][3]);
 #pragma unroll
         for (int o = 0; o < 2; ++o) {
-          d[9 * o] = th[o];
           th[o] = 0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            d[9 * o + 1 + b] = lam[o][b];
-            d[9 * o + 5 + b] = dla[o][b] + dlb[o][b];
-            lam[o][b] = dla[o][b] = dlb[o][b] = 0;
-          }
+          for (int b = 0; b < 4; ++b) lam[o][b] = dla[o][b] = dlb[o][b] = 0;
         }
       }
       if (t + 1 < C::STEPS) cur = nxt;
@@ -943,7 +953,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 #pragma unroll
       for (int k = -1; k <= 1; ++k) {
         const int lp = l - 1, mp = m - k;
-        const int se = (mp >= -lp && mp <= lp) ? lp * lp + lp + mp : P * P;
+        const int se = (mp >= -lp && mp <= lp) ? poss[lp * lp + lp + mp] : P * P;
         const double *vv = qb + QR::SV + 2 * vidx(1, k < 0 ? -k : k);
         const double A = k < 0 ? -sx[SXW * se] : sx[SXW * se], B = sx[SXW * se + 1];
         T = fma(vv[0], A, fma(vv[1], B, T));

@@ -186,41 +186,102 @@ static std::vector<double> make_trtab() {
       std::fprintf(stderr, "rrq: translate schedule needs %d slots per task > SMAX %d\n", scnt[tk], C::SMAX);
       std::abort();
     }
-  // greedy bank-aware order within runs: pos -> term index
+  // Shared-memory wavefronts of one step (quarter-warp model: 8 lanes per wavefront of 16-B accesses,
+  // verified by tools/lds_banks.cu).  Q / dQ / V loads hit 16-B group (pq[qe] + c) mod 8, S' loads
+  // (3 ps[se] + c) mod 8; a quarter costs the largest number of DISTINCT entries sharing one group.
+  // The schedule (order of terms within runs) and the shared-memory positions pq (Q entries) and ps
+  // (S' entries) are chosen together: greedy ordering, then annealing on the positions, alternated.
+  std::vector<int> pq(D::NQ), ps(ZE + 1);
+  for (int e = 0; e < D::NQ; ++e) pq[e] = e;
+  for (int e = 0; e <= ZE; ++e) ps[e] = e;
+  auto mult = [](const int *ent, const int *grp, int n) {   // max over groups of the distinct entries in it
+    uint64_t m[8][2] = {};
+    for (int i = 0; i < n; ++i) m[grp[i]][ent[i] >> 6] |= 1ull << (ent[i] & 63);
+    int best = 1;
+    for (int g = 0; g < 8; ++g) best = std::max(best, __builtin_popcountll(m[g][0]) + __builtin_popcountll(m[g][1]));
+    return best;
+  };
   std::vector<int> order(NT);
-  std::vector<char> used(NT, 0);
-  for (int t = 0; t < C::STEPS; ++t)
-    for (int q = 0; q < 4; ++q) {
-      std::vector<int> qg, sg;   // entries chosen so far in this quarter at step t
-      for (int L = 8 * q; L < 8 * q + 8; ++L) {
-        const int pos = beg[L] + t;
-        if (pos >= beg[L + 1]) continue;
-        const Run &r = runs[run_of[pos]];
-        int best = -1, bc = 1 << 30;
-        for (int i = r.first; i <= r.last; ++i) {
-          if (used[i]) continue;
-          int cost = 0;
-          for (int a : qg)
-            if (a != terms[i].qe && (a - terms[i].qe) % 8 == 0) ++cost;
-          for (int a : sg) {
-            if (a != terms[i].se0 && (a - terms[i].se0) % 8 == 0) ++cost;
-            if (a != terms[i].se1 && (a - terms[i].se1) % 8 == 0) ++cost;
+  auto greedy = [&]() {
+    std::vector<char> used(NT, 0);
+    for (int t = 0; t < C::STEPS; ++t)
+      for (int q = 0; q < 4; ++q) {
+        std::vector<int> qg, sg;   // entries chosen so far in this quarter at step t
+        for (int L = 8 * q; L < 8 * q + 8; ++L) {
+          const int pos = beg[L] + t;
+          if (pos >= beg[L + 1]) continue;
+          const Run &r = runs[run_of[pos]];
+          int best = -1, bc = 1 << 30;
+          for (int i = r.first; i <= r.last; ++i) {
+            if (used[i]) continue;
+            int cost = 0;
+            for (int a : qg)
+              if (a != terms[i].qe && ((pq[a] - pq[terms[i].qe]) & 7) == 0) cost += 9;
+            for (int a : sg) {
+              if (a != terms[i].se0 && ((ps[a] - ps[terms[i].se0]) & 7) == 0) cost += 2;
+              if (a != terms[i].se1 && ((ps[a] - ps[terms[i].se1]) & 7) == 0) cost += 2;
+            }
+            if (cost < bc) { bc = cost; best = i; }
           }
-          if (cost < bc) { bc = cost; best = i; }
+          used[best] = 1;
+          order[pos] = best;
+          qg.push_back(terms[best].qe);
+          sg.push_back(terms[best].se0);
+          sg.push_back(terms[best].se1);
         }
-        used[best] = 1;
-        order[pos] = best;
-        qg.push_back(terms[best].qe);
-        sg.push_back(terms[best].se0);
-        sg.push_back(terms[best].se1);
       }
+  };
+  auto cost = [&]() {
+    int tot = 0;
+    for (int t = 0; t < C::STEPS; ++t)
+      for (int q = 0; q < 4; ++q) {
+        int eq[8], gq[8], e0[8], g0[8], e1[8], g1[8], n = 0;
+        for (int L = 8 * q; L < 8 * q + 8; ++L) {
+          const int pos = beg[L] + t;
+          if (pos >= beg[L + 1]) continue;
+          const Term &tm = terms[order[pos]];
+          eq[n] = tm.qe; gq[n] = pq[tm.qe] & 7;
+          e0[n] = tm.se0; g0[n] = (3 * ps[tm.se0]) & 7;
+          e1[n] = tm.se1; g1[n] = (3 * ps[tm.se1]) & 7;
+          ++n;
+        }
+        tot += 9 * mult(eq, gq, n) + 2 * mult(e0, g0, n) + 2 * mult(e1, g1, n);
+      }
+    return tot;
+  };
+  greedy();
+  int cur = cost();
+  std::vector<int> best_order = order, best_pq = pq, best_ps = ps;
+  int best = cur;
+  uint64_t rng = 0x9E3779B97F4A7C15ull;
+  auto rnd = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
+  double T = 3.0;
+  for (int round = 0; round < 8; ++round) {
+    for (int it = 0; it < 3000; ++it) {
+      const bool onq = (rnd() & 1) != 0;
+      std::vector<int> &v = onq ? pq : ps;
+      const int n = onq ? D::NQ : ZE;   // ps[ZE] (the zero entry) stays last
+      const int a = (int)(rnd() % n), b2 = (int)(rnd() % n);
+      if (a == b2) continue;
+      std::swap(v[a], v[b2]);
+      const int c = cost();
+      const double u = (double)(rnd() >> 11) * (1.0 / 9007199254740992.0);
+      if (c <= cur || u < std::exp((cur - c) / T)) cur = c;
+      else std::swap(v[a], v[b2]);
+      T = std::max(0.05, T * 0.9996);
     }
-  std::vector<uint32_t> w(C::STEPS * 32 + D::NP, (uint32_t)ZE << 7 | (uint32_t)ZE << 14);   // padding terms
+    greedy();
+    cur = cost();
+    if (cur < best) { best = cur; best_order = order; best_pq = pq; best_ps = ps; }
+  }
+  order = best_order; pq = best_pq; ps = best_ps;
+  std::vector<uint32_t> w(C::NWORD, 0u);
+  for (int i = 0; i < C::STEPS * 32; ++i) w[i] = (uint32_t)ZE << 7 | (uint32_t)ZE << 14;   // padding terms
   for (int L = 0; L < 32; ++L)
     for (int pos = beg[L]; pos < beg[L + 1]; ++pos) {
       const Term &t = terms[order[pos]];
       const int ak = std::abs(t.k);
-      uint32_t cw = (uint32_t)t.qe | (uint32_t)t.se0 << 7 | (uint32_t)t.se1 << 14;
+      uint32_t cw = (uint32_t)pq[t.qe] | (uint32_t)ps[t.se0] << 7 | (uint32_t)ps[t.se1] << 14;
       if (t.k < 0) cw |= (ak & 1) ? C::FA : C::FB;
       if (slot_of[pos] >= 0) cw |= C::FLUSH | (uint32_t)slot_of[pos] << 24;
       w[(pos - beg[L]) * 32 + L] = cw;
@@ -234,6 +295,11 @@ static std::vector<double> make_trtab() {
                                        (uint32_t)scnt[tk] << 16 | (uint32_t)hf << 24;
     }
   w[C::STEPS * 32 + lmidx(1, 1)] = 1u | 1u << 4;   // (1,1): j = 1 terms only (no slots)
+  {   // shared-memory positions of the Q entries and S' entries (bytes)
+    uint8_t *pb = reinterpret_cast<uint8_t *>(w.data() + C::STEPS * 32 + D::NP);
+    for (int e = 0; e < D::NQ; ++e) pb[e] = (uint8_t)pq[e];
+    for (int e = 0; e < ZE; ++e) pb[D::NQ + e] = (uint8_t)ps[e];
+  }
   auto fact = [](int n) { long double f = 1; for (int i = 2; i <= n; ++i) f *= i; return f; };
   auto F = [&](int a, int b) { const int ab = std::abs(b); return std::sqrt(fact(a + ab) * fact(a - ab)); };
   std::vector<double> out(C::TAB_D, 0.0);
