@@ -620,18 +620,53 @@ template <int P>
 struct QmapCfg {
   using D = Dims<P>;
   static constexpr int TP = 16, ROWS = 2 * TP, WARPS = 8;
-  static constexpr int PG = TP / 8, GPW = 1;                   // pair groups of 8 per tile / per warp
-  static constexpr int NSPLIT = WARPS / (PG / GPW);              // N splits
+  static constexpr int PG = TP / 8, NSPLIT = WARPS / PG;        // warp = (pair group of 8, column split)
   static constexpr int KA = (D::K % 16 == 4) ? D::K : D::K + ((4 - D::K % 16) + 16) % 16;
   static constexpr int TQC = D::CQP / 8;                      // tiles per quaternion component
   static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8, NTV = NTALL - NTQ;
-  static constexpr int NTQW = (NTQ + NSPLIT - 1) / NSPLIT, NTVW = (NTV + NSPLIT - 1) / NSPLIT;
+  static constexpr int UQ = (TQC + NSPLIT - 1) / NSPLIT;       // a warp's tiles per component
+  static constexpr int UV = (NTV + NSPLIT - 1) / NSPLIT;       // a warp's V tiles
   static constexpr int KC = (D::E % 8 == 0) ? 8 : 12, NCH = D::K / KC, CPA = D::E / KC;   // chunks per axis
   static_assert(D::E % KC == 0, "a B chunk must lie within one axis block");
+  static constexpr int MINB = P <= 8 ? 2 : 1;                 // CTAs per SM (register budget)
   static constexpr size_t SMEM_A = (size_t)ROWS * KA * sizeof(double);
   static constexpr size_t SMEM_B = (size_t)KC * D::NCS * sizeof(double);
   static constexpr size_t SMEM = SMEM_A + 2 * SMEM_B;
 };
+
+// One KC-row chunk of the k_qmap GEMM for a warp; ZC = the quaternion component whose M block is zero in
+// this chunk's axis (compile time, so the skipped tiles cost nothing).  Tiles: component c, u-th of the
+// warp: column tile c TQC + ns + NSPLIT u; V: NTQ + ns + NSPLIT u.
+template <int P, int ZC>
+__device__ __forceinline__ void qmap_chunk(const double *arow, const double *brow, const double *bb, int ns,
+                                           double (&accA)[4][QmapCfg<P>::UQ][2], double (&accB)[4][QmapCfg<P>::UQ][2],
+                                           double (&accV)[QmapCfg<P>::UV][2]) {
+  using C = QmapCfg<P>;
+  constexpr int NCS = Dims<P>::NCS;
+#pragma unroll
+  for (int kk = 0; kk < C::KC; kk += 4) {
+    const double a = arow[kk], b = brow[kk];
+    const double *bk = bb + kk * NCS;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c == ZC) continue;
+#pragma unroll
+      for (int u = 0; u < C::UQ; ++u) {
+        const int tl = ns + u * C::NSPLIT;
+        if (u + 1 < C::UQ || tl < C::TQC) {
+          const double bq = bk[(c * C::TQC + tl) * 8];
+          dmma(accA[c][u][0], accA[c][u][1], a, bq);
+          dmma(accB[c][u][0], accB[c][u][1], b, bq);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < C::UV; ++u) {
+      const int tl = ns + u * C::NSPLIT;
+      if (u + 1 < C::UV || tl < C::NTV) dmma(accV[u][0], accV[u][1], a, bk[(C::NTQ + tl) * 8]);
+    }
+  }
+}
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -657,6 +692,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
@@ -666,7 +704,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, 2)
+__global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     k_qmap(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, const int32_t *__restrict__ item_patch,
            const int64_t *__restrict__ seg_ptr, int64_t sA, const double *__restrict__ fit,
            const double *__restrict__ Arow, double *__restrict__ Qrow, const double *__restrict__ trtab) {
@@ -683,12 +721,17 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, 2)
   const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *M = fit + Pp * (int64_t)L::STRIDE + L::MQ;
-  __shared__ uint64_t bar[2];
+  // pipeline: bar[b] = "chunk in buffer b landed" (bulk-copy transactions), emp[b] = "all warps done with
+  // buffer b" (one arrival per warp); no CTA-wide barrier inside the K loop
+  __shared__ uint64_t bar[2], emp[2];
+  __shared__ double ssc[D::NQ + D::NV];   // v_lambda | v_theta
   constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ROWB = (unsigned)(K * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&emp[0], C::WARPS);
+    mbar_init(&emp[1], C::WARPS);
     mbar_fence_init();
   }
   // rows of absent pairs are zero
@@ -696,6 +739,7 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, 2)
     const int r = i / K;
     if (r % TP >= cnt) sA_[r * KA + i % K] = 0.0;
   }
+  for (int i = threadIdx.x; i < D::NQ + D::NV; i += blockDim.x) ssc[i] = trtab[TrCfg<P>::VLAM + i];
   __syncthreads();
   // stage A (row r < TP -> a-row of pair s0 + r; row TP + r -> b-row) and chunk 0 of M on bar[0]
   // (a bulk copy takes uniform operands: one issuing lane per warp, rows spread over the warps)
@@ -705,89 +749,62 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, 2)
       if (r % TP < cnt) bulk_g2s(sA_ + r * KA, Arow + (s0 + r % TP - sA) * 2 * K + (r / TP) * K, ROWB, &bar[0]);
     if (warp == C::WARPS - 1) bulk_g2s(sB, M, CHB, &bar[0]);
   }
-  const int ns = warp / (C::PG / C::GPW), g0 = (warp % (C::PG / C::GPW)) * C::GPW;
-  __shared__ double ssc[D::NQ + D::NV];   // v_lambda | v_theta
-  for (int i = threadIdx.x; i < D::NQ + D::NV; i += blockDim.x) ssc[i] = trtab[TrCfg<P>::VLAM + i];
-  double accA[C::GPW][C::NTQW][2], accB[C::GPW][C::NTQW][2], accV[C::GPW][C::NTVW][2];
+  const int ns = warp / C::PG, pg = warp % C::PG;
+  double accA[4][C::UQ][2], accB[4][C::UQ][2], accV[C::UV][2];
 #pragma unroll
-  for (int g = 0; g < C::GPW; ++g) {
+  for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int t = 0; t < C::NTQW; ++t) accA[g][t][0] = accA[g][t][1] = accB[g][t][0] = accB[g][t][1] = 0.0;
+    for (int u = 0; u < C::UQ; ++u) accA[c][u][0] = accA[c][u][1] = accB[c][u][0] = accB[c][u][1] = 0.0;
 #pragma unroll
-    for (int t = 0; t < C::NTVW; ++t) accV[g][t][0] = accV[g][t][1] = 0.0;
-  }
-  const double *arow = sA_ + (g0 * 8 + (lane >> 2)) * KA + (lane & 3);   // group g0 + g: + 8 g KA; b: + TP KA
+  for (int u = 0; u < C::UV; ++u) accV[u][0] = accV[u][1] = 0.0;
+  const double *arow = sA_ + (pg * 8 + (lane >> 2)) * KA + (lane & 3), *brow = arow + TP * KA;
   const int bofs = (lane & 3) * NCS + (lane >> 2);
   for (int ch = 0; ch < C::NCH; ++ch) {
-    if (threadIdx.x == 0 && ch + 1 < C::NCH) {   // buffer (ch+1)&1 was released by the barrier ending ch-1
+    if (threadIdx.x == 0 && ch + 1 < C::NCH) {   // refill the other buffer once every warp has left chunk ch-1
+      const int b = (ch + 1) & 1;
+      if (ch >= 1) mbar_wait(&emp[b], ((ch - 1) >> 1) & 1);
       fence_proxy_async();
-      mbar_expect_tx(&bar[(ch + 1) & 1], CHB);
-      bulk_g2s(sB + ((ch + 1) & 1) * KC * NCS, M + (int64_t)(ch + 1) * KC * NCS, CHB, &bar[(ch + 1) & 1]);
+      mbar_expect_tx(&bar[b], CHB);
+      bulk_g2s(sB + b * KC * NCS, M + (int64_t)(ch + 1) * KC * NCS, CHB, &bar[b]);
     }
     mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
-    const int zc = ch / C::CPA + 1;   // quaternion component whose block is zero in this axis
     const double *bb = sB + (ch & 1) * KC * NCS + bofs;
-#pragma unroll
-    for (int kk = 0; kk < KC; kk += 4) {
-      double a[C::GPW], b[C::GPW];
-#pragma unroll
-      for (int g = 0; g < C::GPW; ++g) {
-        a[g] = arow[g * 8 * KA + ch * KC + kk];
-        b[g] = arow[(TP + g * 8) * KA + ch * KC + kk];
-      }
-      const double *bk = bb + kk * NCS;
-#pragma unroll
-      for (int t = 0; t < C::NTQW; ++t) {
-        const int nt = ns + t * C::NSPLIT;
-        if (nt < C::NTQ && nt / C::TQC != zc) {
-          const double bq = bk[nt * 8];
-#pragma unroll
-          for (int g = 0; g < C::GPW; ++g) {
-            dmma(accA[g][t][0], accA[g][t][1], a[g], bq);
-            dmma(accB[g][t][0], accB[g][t][1], b[g], bq);
-          }
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < C::NTVW; ++t) {
-        const int nt = C::NTQ + ns + t * C::NSPLIT;
-        if (nt < C::NTALL) {
-          const double bv = bk[nt * 8];
-#pragma unroll
-          for (int g = 0; g < C::GPW; ++g) dmma(accV[g][t][0], accV[g][t][1], a[g], bv);
-        }
-      }
+    switch (ch / C::CPA) {   // axis of this chunk: component axis + 1 has a zero block
+      case 0: qmap_chunk<P, 1>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
+      case 1: qmap_chunk<P, 2>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
+      default: qmap_chunk<P, 3>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
     }
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&emp[ch & 1]);
   }
   // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]
-#pragma unroll
-  for (int g = 0; g < C::GPW; ++g) {
-    const int pr = (g0 + g) * 8 + (lane >> 2);
-    if (pr >= cnt) continue;
+  const int pr = pg * 8 + (lane >> 2);
+  if (pr < cnt) {
     double *out = Qrow + (s0 + pr - sA) * QR::STRIDE;
 #pragma unroll
-    for (int t = 0; t < C::NTQW; ++t) {
-      const int nt = ns + t * C::NSPLIT;
-      if (nt >= C::NTQ) continue;
-      const int comp = nt / C::TQC, e = (nt - comp * C::TQC) * 4 + (lane & 3);   // entry qidx(j,k)
-      if (e >= D::NQ) continue;
-      const double sc = ssc[e];
-      double *o = out + QR::EG * e + 2 * comp;
-      o[0] = sc * accA[g][t][0];
-      o[1] = sc * accA[g][t][1];
-      o[8] = sc * accB[g][t][0];
-      o[9] = sc * accB[g][t][1];
-    }
+    for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int t = 0; t < C::NTVW; ++t) {
-      const int nt = C::NTQ + ns + t * C::NSPLIT;
-      if (nt >= C::NTALL) continue;
-      const int col = nt * 8 + 2 * (lane & 3) - D::NCQ;
+      for (int u = 0; u < C::UQ; ++u) {
+        const int tl = ns + u * C::NSPLIT;
+        if (tl >= C::TQC) continue;
+        const int e = tl * 4 + (lane & 3);   // entry qidx(j,k)
+        if (e >= D::NQ) continue;
+        const double sc = ssc[e];
+        double *o = out + QR::EG * e + 2 * c;
+        o[0] = sc * accA[c][u][0];
+        o[1] = sc * accA[c][u][1];
+        o[8] = sc * accB[c][u][0];
+        o[9] = sc * accB[c][u][1];
+      }
+#pragma unroll
+    for (int u = 0; u < C::UV; ++u) {
+      const int tl = ns + u * C::NSPLIT;
+      if (tl >= C::NTV) continue;
+      const int col = tl * 8 + 2 * (lane & 3);
       if (col < 2 * D::NV) {
         const double sc = ssc[D::NQ + (col >> 1)];
-        out[QR::V + col] = sc * accV[g][t][0];
-        out[QR::V + col + 1] = sc * accV[g][t][1];
+        out[QR::V + col] = sc * accV[u][0];
+        out[QR::V + col + 1] = sc * accV[u][1];
       }
     }
   }
