@@ -627,11 +627,12 @@ struct QmapCfg {
   static constexpr int UQ = (TQC + NSPLIT - 1) / NSPLIT;       // a warp's tiles per component
   static constexpr int UV = (NTV + NSPLIT - 1) / NSPLIT;       // a warp's V tiles
   static constexpr int KC = (D::E % 8 == 0) ? 8 : 12, NCH = D::K / KC, CPA = D::E / KC;   // chunks per axis
+  static constexpr int NST = 2;                                    // pipeline stages (chunks in flight)
   static_assert(D::E % KC == 0, "a B chunk must lie within one axis block");
   static constexpr int MINB = P <= 8 ? 2 : 1;                 // CTAs per SM (register budget)
   static constexpr size_t SMEM_A = (size_t)ROWS * KA * sizeof(double);
   static constexpr size_t SMEM_B = (size_t)KC * D::NCS * sizeof(double);
-  static constexpr size_t SMEM = SMEM_A + 2 * SMEM_B;
+  static constexpr size_t SMEM = SMEM_A + NST * SMEM_B;
 };
 
 // One KC-row chunk of the k_qmap GEMM for a warp; ZC = the quaternion component whose M block is zero in
@@ -723,15 +724,15 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
   const double *M = fit + Pp * (int64_t)L::STRIDE + L::MQ;
   // pipeline: bar[b] = "chunk in buffer b landed" (bulk-copy transactions), emp[b] = "all warps done with
   // buffer b" (one arrival per warp); no CTA-wide barrier inside the K loop
-  __shared__ uint64_t bar[2], emp[2];
+  __shared__ uint64_t bar[C::NST], emp[C::NST];
   __shared__ double ssc[D::NQ + D::NV];   // v_lambda | v_theta
   constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ROWB = (unsigned)(K * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&emp[0], C::WARPS);
-    mbar_init(&emp[1], C::WARPS);
+    for (int i = 0; i < C::NST; ++i) {
+      mbar_init(&bar[i], 1);
+      mbar_init(&emp[i], C::WARPS);
+    }
     mbar_fence_init();
   }
   // rows of absent pairs are zero
@@ -749,6 +750,11 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
       if (r % TP < cnt) bulk_g2s(sA_ + r * KA, Arow + (s0 + r % TP - sA) * 2 * K + (r / TP) * K, ROWB, &bar[0]);
     if (warp == C::WARPS - 1) bulk_g2s(sB, M, CHB, &bar[0]);
   }
+  if (threadIdx.x == 0)   // chunks 1 .. NST-2 in flight from the start
+    for (int ch = 1; ch < C::NST - 1 && ch < C::NCH; ++ch) {
+      mbar_expect_tx(&bar[ch], CHB);
+      bulk_g2s(sB + ch * KC * NCS, M + (int64_t)ch * KC * NCS, CHB, &bar[ch]);
+    }
   const int ns = warp / C::PG, pg = warp % C::PG;
   double accA[4][C::UQ][2], accB[4][C::UQ][2], accV[C::UV][2];
 #pragma unroll
@@ -760,22 +766,23 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
   const double *arow = sA_ + (pg * 8 + (lane >> 2)) * KA + (lane & 3), *brow = arow + TP * KA;
   const int bofs = (lane & 3) * NCS + (lane >> 2);
   for (int ch = 0; ch < C::NCH; ++ch) {
-    if (threadIdx.x == 0 && ch + 1 < C::NCH) {   // refill the other buffer once every warp has left chunk ch-1
-      const int b = (ch + 1) & 1;
-      if (ch >= 1) mbar_wait(&emp[b], ((ch - 1) >> 1) & 1);
+    const int nx = ch + C::NST - 1;   // chunk to issue now, into the buffer chunk ch-1 used
+    if (threadIdx.x == 0 && nx < C::NCH) {
+      const int b = nx % C::NST;
+      if (ch >= 1) mbar_wait(&emp[b], ((ch - 1) / C::NST) & 1);
       fence_proxy_async();
       mbar_expect_tx(&bar[b], CHB);
-      bulk_g2s(sB + b * KC * NCS, M + (int64_t)(ch + 1) * KC * NCS, CHB, &bar[b]);
+      bulk_g2s(sB + b * KC * NCS, M + (int64_t)nx * KC * NCS, CHB, &bar[b]);
     }
-    mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
-    const double *bb = sB + (ch & 1) * KC * NCS + bofs;
+    mbar_wait(&bar[ch % C::NST], (ch / C::NST) & 1);
+    const double *bb = sB + (ch % C::NST) * KC * NCS + bofs;
     switch (ch / C::CPA) {   // axis of this chunk: component axis + 1 has a zero block
       case 0: qmap_chunk<P, 1>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
       case 1: qmap_chunk<P, 2>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
       default: qmap_chunk<P, 3>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&emp[ch & 1]);
+    if (lane == 0) mbar_arrive(&emp[ch % C::NST]);
   }
   // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]
   const int pr = pg * 8 + (lane >> 2);
