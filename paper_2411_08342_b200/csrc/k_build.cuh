@@ -1025,7 +1025,7 @@ struct ContractCfg {
   static constexpr int TP = 16, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 8;
   static constexpr int ZS = (D::NZS % 16 == 4) ? D::NZS : D::NZS + ((4 - D::NZS % 16) + 16) % 16;
   static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
-  static constexpr int NB = (D::N % 16 == 4) ? D::N : D::N + ((4 - D::N % 16) + 16) % 16;   // B row stride
+  static constexpr int NB = Layout<P>::NF;   // B row stride (== the fit operators' row stride)
   static constexpr int KC = (D::NP % 3 == 0) ? 12 : ((D::NP % 2 == 0) ? 8 : 4);            // k-rows per chunk
   static constexpr int NCH = 4 * D::NP / KC;
   static constexpr size_t SMEM_Z = (size_t)TP * ZS;
@@ -1058,13 +1058,13 @@ __global__ void __launch_bounds__(256, 2)
   const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *blk = fit + Pp * (int64_t)L::STRIDE;
-  const double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
+  const double *PD = blk + L::FIT, *PSp = PD + 4 * NP * NB, *PSd = PD + 8 * NP * NB, *PSg = PD + 9 * NP * NB;
   // B chunk ch: rows [ch KC, (ch+1) KC) of P_D, P_Sp, P_Sg -> sB[(ch&1)][blk][row][NB]; the Z tile (rows of
   // NZS doubles, contiguous in global and in shared memory since ZS == NZS) rides on chunk 0's barrier.
   // 1-D bulk copies (TMA) issued by warp 0 on mbarriers.
   static_assert(ZS == NZS, "Z tile staged as one bulk copy");
   __shared__ uint64_t bar[2];
-  constexpr unsigned ROWB = (unsigned)(N * sizeof(double));
+  constexpr unsigned ROWB = (unsigned)(NB * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -1073,18 +1073,15 @@ __global__ void __launch_bounds__(256, 2)
   }
   for (int i = cnt * ZS + threadIdx.x; i < TP * ZS; i += blockDim.x) sz[i] = 0.0;   // absent pairs
   __syncthreads();
-  // called by every warp: lane 0 of warp w issues rows w, w + WARPS, ... (a bulk copy takes uniform operands,
-  // so one issuing lane per warp; spreading the rows keeps any one warp from stalling the barrier)
+  // the fit operators are stored with the padded row stride NB, so a chunk of each is one contiguous copy
   auto issue = [&](int ch, unsigned extra) {
     uint64_t *br = &bar[ch & 1];
-    if (threadIdx.x == 0) mbar_expect_tx(br, 3u * KC * ROWB + extra);
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(br, 3u * KC * ROWB + extra);
       double *dst = sB + (ch & 1) * CC::SMEM_B;
-      for (int q = warp; q < 3 * KC; q += CC::WARPS) {
-        const int bk = q / KC, rr = q % KC;
-        const double *src = (bk == 0 ? PD : (bk == 1 ? PSp : PSg)) + (int64_t)(ch * KC + rr) * N;
-        bulk_g2s(dst + (bk * KC + rr) * NB, src, ROWB, br);
-      }
+      bulk_g2s(dst, PD + (int64_t)ch * KC * NB, KC * ROWB, br);
+      bulk_g2s(dst + KC * NB, PSp + (int64_t)ch * KC * NB, KC * ROWB, br);
+      bulk_g2s(dst + 2 * KC * NB, PSg + (int64_t)ch * KC * NB, KC * ROWB, br);
     }
   };
   {
@@ -1129,7 +1126,7 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
     for (int q = 0; q < NK; ++q) {   // all loads first (latency overlapped), then the DMMAs
       const int kk = 4 * q + (lane & 3);
-      bq[q] = (bn < N && kk < NP) ? __ldg(PSd + kk * N + bn) : 0.0;
+      bq[q] = (bn < N && kk < NP) ? __ldg(PSd + kk * NB + bn) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < NK; ++q) {
@@ -1140,7 +1137,7 @@ __global__ void __launch_bounds__(256, 2)
   // the 4 NP blocks, B double-buffered through shared memory
   for (int ch = 0; ch < CC::NCH; ++ch) {
     if (ch + 1 < CC::NCH) {   // buffer (ch+1)&1 was released by the barrier ending ch-1
-      if (lane == 0) fence_proxy_async();
+      if (threadIdx.x == 0) fence_proxy_async();
       issue(ch + 1, 0);
     }
     mbar_wait(&bar[ch & 1], (ch >> 1) & 1);

@@ -189,191 +189,6 @@ __global__ void k_edge_tables(int64_t n_patches, const double *__restrict__ hc, 
 }
 
 // ------------------------------------------------------------------------------------------------
-// Fit operators.  One CTA (256 threads = 8 warps) per patch, persistent over patches; workspace per
-// CTA in global memory.  Householder QR (column-major, warp per column), Q^T formed on the identity,
-// back substitution -> A^+ (reading A1).
-// ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ double block_sum(double v, double *sh) {
-  v = warp_sum(v);
-  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) sh[w] = v;
-  __syncthreads();
-  double s = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sh[i];
-  return s;
-}
-
-// In-place pseudo-inverse of the m x k column-major matrix A (m >= k): writes X = A^+ (k x m,
-// column-major, ld = k) into Xo.  W: workspace m*m doubles (holds Q^T applied to I), rd: k doubles,
-// beta: k doubles.  Returns 1 if rank deficient (|R_jj| <= 1e-13 max|R_jj|).
-__device__ int cta_pinv(int m, int k, double *A, double *W, double *Xo, double *rd, double *beta, double *sh) {
-  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = 0; j < k; ++j) {
-    double *col = A + (int64_t)j * m;
-    double s = 0;
-    for (int i = j + threadIdx.x; i < m; i += blockDim.x) s += col[i] * col[i];
-    double nrm = sqrt(block_sum(s, sh));
-    double ajj = col[j];
-    double alpha = ajj > 0 ? -nrm : nrm;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      col[j] = ajj - alpha;               // v_j (v stored in place, v_i = A_ij for i > j)
-      rd[j] = alpha;                      // R_jj
-      beta[j] = nrm * (nrm + fabs(ajj));  // v.v / 2
-    }
-    __syncthreads();
-    double bj = beta[j];
-    if (bj > 0)
-      for (int c = j + 1 + warp; c < k; c += nw) {
-        double *cc = A + (int64_t)c * m;
-        double d = 0;
-        for (int i = j + lane; i < m; i += 32) d += col[i] * cc[i];
-        d = warp_sum(d) / bj;
-        for (int i = j + lane; i < m; i += 32) cc[i] -= d * col[i];
-      }
-    __syncthreads();
-  }
-  // Q^T applied to the m unit vectors (W column-major m x m): only the first k rows are needed.
-  for (int c = warp; c < m; c += nw) {
-    double *w = W + (int64_t)c * m;
-    for (int i = lane; i < m; i += 32) w[i] = (i == c) ? 1.0 : 0.0;
-    __syncwarp();
-    for (int j = 0; j < k; ++j) {
-      double bj = beta[j];
-      if (!(bj > 0)) continue;
-      const double *col = A + (int64_t)j * m;
-      double d = 0;
-      for (int i = j + lane; i < m; i += 32) d += col[i] * w[i];
-      d = warp_sum(d) / bj;
-      for (int i = j + lane; i < m; i += 32) w[i] -= d * col[i];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  // back substitution R x = (Q^T e_c)[0:k], one thread per right-hand side c (R_jj = rd[j],
-  // R_ji (i > j) = A[i*m + j], read by all threads in lockstep: broadcast)
-  for (int c = threadIdx.x; c < m; c += blockDim.x) {
-    double *w = W + (int64_t)c * m;
-    for (int r = k - 1; r >= 0; --r) {
-      double s0 = w[r], s1 = 0, s2 = 0, s3 = 0;
-      int cc = r + 1;
-      for (; cc + 3 < k; cc += 4) {
-        s0 -= A[(int64_t)cc * m + r] * w[cc];
-        s1 -= A[(int64_t)(cc + 1) * m + r] * w[cc + 1];
-        s2 -= A[(int64_t)(cc + 2) * m + r] * w[cc + 2];
-        s3 -= A[(int64_t)(cc + 3) * m + r] * w[cc + 3];
-      }
-      for (; cc < k; ++cc) s0 -= A[(int64_t)cc * m + r] * w[cc];
-      w[r] = ((s0 + s1) + (s2 + s3)) / rd[r];
-    }
-    for (int r = 0; r < k; ++r) Xo[(int64_t)c * k + r] = w[r];
-  }
-  __syncthreads();
-  double rmax = 0;
-  for (int j = 0; j < k; ++j) rmax = fmax(rmax, fabs(rd[j]));
-  int def = 0;
-  for (int j = 0; j < k; ++j) def |= fabs(rd[j]) <= 1e-13 * rmax;
-  return def;
-}
-
-template <int P>
-__global__ void __launch_bounds__(256) k_patch_fit(int64_t n_patches, const double *__restrict__ nodes,
-                                                   const double *__restrict__ normals, const double *__restrict__ hc,
-                                                   double *__restrict__ fit, double *__restrict__ work,
-                                                   int32_t *__restrict__ status) {
-  using D = Dims<P>;
-  using L = Layout<P>;
-  constexpr int N = D::N, NP = D::NP, M4 = 4 * N, K4 = 4 * NP;
-  constexpr int64_t WS = (int64_t)M4 * K4 + (int64_t)M4 * M4 + (int64_t)K4 * M4 + 3 * N * NP + N * NP + 2 * N * N;
-  double *A = work + blockIdx.x * WS;
-  double *W = A + (int64_t)M4 * K4;
-  double *X = W + (int64_t)M4 * M4;
-  double *F = X + (int64_t)K4 * M4;   // [3][N][NP]
-  double *Hm = F + 3 * N * NP;        // [N][NP]
-  double *HP = Hm + N * NP;           // [N][N]
-  __shared__ double sh[32], rd[4 * 55], beta[4 * 55], xl[3 * 100], nl[3 * 100];
-  for (int64_t Pp = blockIdx.x; Pp < n_patches; Pp += gridDim.x) {
-    double *blk = fit + Pp * (int64_t)L::STRIDE;
-    const double *o = blk + L::HDR + H_O, *Rm = blk + L::HDR + H_RM;
-    double invh = 1.0 / blk[L::HDR + H_H];
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      const double *x = nodes + (Pp * N + i) * 3, *nu = normals + (Pp * N + i) * 3;
-      double d[3] = {x[0] - o[0], x[1] - o[1], x[2] - o[2]};
-      for (int r = 0; r < 3; ++r) {
-        xl[3 * i + r] = (Rm[3 * r] * d[0] + Rm[3 * r + 1] * d[1] + Rm[3 * r + 2] * d[2]) * invh;
-        nl[3 * i + r] = Rm[3 * r] * nu[0] + Rm[3 * r + 1] * nu[1] + Rm[3 * r + 2] * nu[2];
-      }
-    }
-    __syncthreads();
-    // F_{a,i,lm} = d_a H^{(l,m)}(x_i), Hm_{i,lm} = H^{(l,m)}(x_i), H = sqrt2 Im S
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      cd R[D::NS];
-      r_table<P>(xl[3 * i + 1], xl[3 * i + 2], xl[3 * i], R, hc);
-      for (int l = 1; l <= P; ++l)
-        for (int m = 1; m <= l; ++m) {
-          cd g[3];
-          grad_fast(R, l, m, hc, g);
-          int c = lmidx(l, m);
-          for (int a = 0; a < 3; ++a) F[(a * N + i) * NP + c] = 1.4142135623730950488 * g[a].y;
-          Hm[i * NP + c] = 1.4142135623730950488 * R[sidx(l, m)].y;
-        }
-    }
-    __syncthreads();
-    // A (M4 x K4, column-major): blocks [[0,-F1,-F2,-F3],[F1,0,-F3,F2],[F2,F3,0,-F1],[F3,-F2,F1,0]]
-    const int blkmap[4][4] = {{0, -1, -2, -3}, {1, 0, -3, 2}, {2, 3, 0, -1}, {3, -2, 1, 0}};
-    for (int64_t t = threadIdx.x; t < (int64_t)M4 * K4; t += blockDim.x) {
-      int col = t / M4, row = t % M4;
-      int br = row / N, i = row % N, bc = col / NP, c = col % NP;
-      int s = blkmap[br][bc];
-      A[t] = s == 0 ? 0.0 : (s > 0 ? 1.0 : -1.0) * F[((abs(s) - 1) * N + i) * NP + c];
-    }
-    __syncthreads();
-    int st = cta_pinv(M4, K4, A, W, X, rd, beta, sh);
-    // X = A^+ column-major (K4 x M4): X[c * K4 + r].  P_D[r][i] = X[i][r]; P_Sp[r][i] = sum_a nu_a X[(a+1)N+i][r]
-    double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
-    for (int t = threadIdx.x; t < K4 * N; t += blockDim.x) {
-      int r = t / N, i = t % N;
-      PD[t] = X[(int64_t)i * K4 + r];
-      double s = 0;
-      for (int a = 0; a < 3; ++a) s += nl[3 * i + a] * X[(int64_t)((a + 1) * N + i) * K4 + r];
-      PSp[t] = s;
-    }
-    __syncthreads();
-    // B (N x NP) = F . nu -> P_Sd = B^+ 
-    for (int t = threadIdx.x; t < N * NP; t += blockDim.x) {
-      int c = t / N, i = t % N;
-      double s = 0;
-      for (int a = 0; a < 3; ++a) s += F[(a * N + i) * NP + c] * nl[3 * i + a];
-      A[t] = s;   // column-major (N x NP)
-    }
-    __syncthreads();
-    st |= cta_pinv(N, NP, A, W, X, rd, beta, sh);
-    for (int t = threadIdx.x; t < NP * N; t += blockDim.x) {
-      int r = t / N, i = t % N;
-      PSd[t] = X[(int64_t)i * NP + r];
-    }
-    __syncthreads();
-    // P_Sg = P_D (Hm P_Sd)
-    for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
-      int i = t / N, j = t % N;
-      double s = 0;
-      for (int c = 0; c < NP; ++c) s += Hm[i * NP + c] * PSd[c * N + j];
-      HP[t] = s;
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < K4 * N; t += blockDim.x) {
-      int r = t / N, j = t % N;
-      double s = 0;
-      for (int i = 0; i < N; ++i) s += PD[r * N + i] * HP[i * N + j];
-      PSg[t] = s;
-    }
-    if (threadIdx.x == 0 && status) status[Pp] = st;
-    __syncthreads();
-  }
-}
-
-// ------------------------------------------------------------------------------------------------
 // Fit operators, quaternion form.  The 4n x 4n_p real system of P:L729-735 is the real representation
 // of left multiplication by the n x n_p quaternion matrix F_{i,lm} = (0, grad H^{(l,m)}(x_i)) (eq qprule;
 // the block pattern [[0,-F1,-F2,-F3],[F1,0,-F3,F2],...] is exactly that representation), and the real
@@ -524,7 +339,8 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
     }
     __syncthreads();
     // ---- back substitution R x = (Q^H e_c)[0:NP], one thread per column c; x_r = rd_r^{-1}(w_r - sum R_rk x_k)
-    double *PD = blk + L::FIT, *PSp = PD + 4 * NP * N, *PSd = PD + 8 * NP * N, *PSg = PD + 9 * NP * N;
+    constexpr int NF = L::NF;   // row stride of the fit operators
+    double *PD = blk + L::FIT, *PSp = PD + 4 * NP * NF, *PSd = PD + 8 * NP * NF, *PSg = PD + 9 * NP * NF;
     for (int c = threadIdx.x; c < N; c += blockDim.x) {
       double *w = W + (size_t)c * N * 4;
       const double n0 = nl[3 * c], n1 = nl[3 * c + 1], n2 = nl[3 * c + 2];
@@ -540,15 +356,15 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
         const qd xr = {x.s / dn, x.x / dn, x.y / dn, x.z / dn};
         qst(w + 4 * r, xr);
         // P_D (RHS (mu,0)) and P_Sp (RHS (0, sigma nu))
-        PD[(0 * NP + r) * N + c] = xr.s;
-        PD[(1 * NP + r) * N + c] = xr.x;
-        PD[(2 * NP + r) * N + c] = xr.y;
-        PD[(3 * NP + r) * N + c] = xr.z;
+        PD[(0 * NP + r) * NF + c] = xr.s;
+        PD[(1 * NP + r) * NF + c] = xr.x;
+        PD[(2 * NP + r) * NF + c] = xr.y;
+        PD[(3 * NP + r) * NF + c] = xr.z;
         const qd sp = qmul_(xr, qd{0.0, n0, n1, n2});
-        PSp[(0 * NP + r) * N + c] = sp.s;
-        PSp[(1 * NP + r) * N + c] = sp.x;
-        PSp[(2 * NP + r) * N + c] = sp.y;
-        PSp[(3 * NP + r) * N + c] = sp.z;
+        PSp[(0 * NP + r) * NF + c] = sp.s;
+        PSp[(1 * NP + r) * NF + c] = sp.x;
+        PSp[(2 * NP + r) * NF + c] = sp.y;
+        PSp[(3 * NP + r) * NF + c] = sp.z;
       }
     }
     __syncthreads();
@@ -600,7 +416,7 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
         double s = w[r];
         for (int k = r + 1; k < NP; ++k) s -= Bm[(size_t)k * N + r] * w[k];
         w[r] = s / rdb[r];
-        PSd[r * N + c] = w[r];
+        PSd[r * NF + c] = w[r];
       }
     }
     __syncthreads();
@@ -609,15 +425,15 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
     for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
       const int i = t / N, j = t % N;
       double s = 0;
-      for (int c = 0; c < NP; ++c) s += Hm[(size_t)i * NP + c] * PSd[c * N + j];
+      for (int c = 0; c < NP; ++c) s += Hm[(size_t)i * NP + c] * PSd[c * NF + j];
       HP[t] = s;
     }
     __syncthreads();
     for (int t = threadIdx.x; t < 4 * NP * N; t += blockDim.x) {
       const int r = t / N, j = t % N;
       double s = 0;
-      for (int i = 0; i < N; ++i) s += PD[r * N + i] * HP[(size_t)i * N + j];
-      PSg[t] = s;
+      for (int i = 0; i < N; ++i) s += PD[r * NF + i] * HP[(size_t)i * N + j];
+      PSg[r * NF + j] = s;
     }
     if (threadIdx.x == 0 && status) {
       double rmax = 0, rmin = 1e300, bmax = 0, bmin = 1e300;

@@ -63,8 +63,9 @@ struct Layout {
   static constexpr int YL = 32;       // [E][3] local scaled edge samples
   static constexpr int TL = YL + 3 * D::E;   // [E][3] local scaled tangents
   static constexpr int CM = TL + 3 * D::E;   // [3][Q][3] monomial coefficients of the edge interpolants
-  static constexpr int FIT = CM + 9 * D::Q;  // [13 NP][N]: P_D (4NP) P_Sp (4NP) P_Sd (NP) P_Sg (4NP)
-  static constexpr int MQ = (FIT + 13 * D::NP * D::N + 3) / 4 * 4;   // [K][NCS]: GEMM operand of the Q / V maps
+  static constexpr int NF = D::N + ((4 - D::N % 16) + 16) % 16;   // fit-operator row stride == 4 (mod 16)
+  static constexpr int FIT = CM + 9 * D::Q;  // [13 NP][NF]: P_D (4NP) P_Sp (4NP) P_Sd (NP) P_Sg (4NP)
+  static constexpr int MQ = (FIT + 13 * D::NP * NF + 3) / 4 * 4;   // [K][NCS]: GEMM operand of the Q / V maps
   static constexpr int END = MQ + D::K * D::NCS;
   static constexpr int STRIDE = (END + 31) / 32 * 32;
 };
