@@ -1063,12 +1063,14 @@ __global__ void __launch_bounds__(256, 2)
   // NZS doubles, contiguous in global and in shared memory since ZS == NZS) rides on chunk 0's barrier.
   // 1-D bulk copies (TMA) issued by warp 0 on mbarriers.
   static_assert(ZS == NZS, "Z tile staged as one bulk copy");
-  __shared__ uint64_t bar[2];
+  __shared__ uint64_t bar[2], emp[2];
   constexpr unsigned ROWB = (unsigned)(NB * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&emp[0], CC::WARPS);
+    mbar_init(&emp[1], CC::WARPS);
     mbar_fence_init();
   }
   for (int i = cnt * ZS + threadIdx.x; i < TP * ZS; i += blockDim.x) sz[i] = 0.0;   // absent pairs
@@ -1134,33 +1136,39 @@ __global__ void __launch_bounds__(256, 2)
       dmma(acc[tw][0], acc[tw][1], kk < NP ? zr[4 * q] : 0.0, bq[q]);
     }
   }
-  // the 4 NP blocks, B double-buffered through shared memory
+  // the 4 NP blocks, B double-buffered through shared memory; emp[b] = "every warp is done with buffer b"
+  // (no CTA-wide barrier in the K loop).  A warp's tiles share the M-tile (tile = warp + WARPS tw).
+  static_assert(CC::WARPS % CC::MT == 0, "a warp's tiles share one M-tile");
+  const int mtw = warp % CC::MT;
+  const double *zr0 = sz + (mtw * 8 + (lane >> 2)) * ZS + (lane & 3);
   for (int ch = 0; ch < CC::NCH; ++ch) {
-    if (ch + 1 < CC::NCH) {   // buffer (ch+1)&1 was released by the barrier ending ch-1
-      if (threadIdx.x == 0) fence_proxy_async();
+    if (ch + 1 < CC::NCH && threadIdx.x == 0) {   // refill buffer (ch+1)&1 once every warp has left chunk ch-1
+      if (ch >= 1) mbar_wait(&emp[(ch + 1) & 1], ((ch - 1) >> 1) & 1);
+      fence_proxy_async();
       issue(ch + 1, 0);
     }
     mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
     const double *bb = sB + (ch & 1) * CC::SMEM_B;
+    const double *zr = zr0 + ch * KC;
 #pragma unroll
-    for (int tw = 0; tw < CC::TPW; ++tw) {
-      const int tile = warp + tw * CC::WARPS;
-      if (tile >= CC::TILES) continue;
-      const int mt = tile % CC::MT, nt = tile / CC::MT, bn = nt * 8 + (lane >> 2);
-      const bool bok = bn < N;
-      const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3) + ch * KC;
+    for (int kk = 0; kk < KC; kk += 4) {
+      const double zw = zr[NP + kk], zdw = zr[5 * NP + kk], zs = zr[9 * NP + kk];
 #pragma unroll
-      for (int kk = 0; kk < KC; kk += 4) {
+      for (int tw = 0; tw < CC::TPW; ++tw) {
+        const int tile = warp + tw * CC::WARPS;
+        if (tile >= CC::TILES) continue;
+        const int bn = (tile / CC::MT) * 8 + (lane >> 2);
+        const bool bok = bn < N;
         const int br = (kk + (lane & 3)) * NB + bn;
         const double bd = bok ? bb[br] : 0.0, bsp = bok ? bb[KC * NB + br] : 0.0, bsg = bok ? bb[2 * KC * NB + br] : 0.0;
-        const double zw = zr[NP + kk], zdw = zr[5 * NP + kk], zs = zr[9 * NP + kk];
         dmma(acc[tw][2], acc[tw][3], zw, bd);
         dmma(acc[tw][6], acc[tw][7], zdw, bd);
         dmma(acc[tw][4], acc[tw][5], zs, bsp);
         dmma(acc[tw][0], acc[tw][1], zw, bsg);
       }
     }
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&emp[ch & 1]);
   }
 #pragma unroll 1
   for (int tw = 0; tw < CC::TPW; ++tw) {
