@@ -210,76 +210,24 @@ __device__ __forceinline__ double tri_sum(double v, int base) {
   return a + b + c;
 }
 
-// Per-pair state of k_pair_edge (shared memory; one per pair of the CTA round).
-template <int P>
-struct PairState {
-  using D = Dims<P>;
-  cd R[D::NS];                 // R_l^m at (y', z', x'): S^{(l,m)}(r') for m >= 0
-  double I[3][D::Q], J[3][D::Q];
-  double t0[3][2];
-  double rp[3], nup[3], u3, om[8], o0e[3];
-  int64_t k, t;
-  int Pp, self_local, active, pad;
-  int swap[3], conv[3], direct[3];
-};
-constexpr int kPPW = 3;   // pairs per warp per round (the Newton phase packs 3 x 9 = 27 lanes)
-
-// Per-warp scratch: gradient tables of the warp's pairs (phase 1 -> phase 5) and the direct-rule buffer.
-template <int P>
-struct WarpScr {
-  using D = Dims<P>;
-  cd GS[kPPW][D::NS][3];
-  double r13[2][kNDirect];
+// Per-pair setup (thread per pair; latency-bound index chasing done with full occupancy): the target in
+// the patch frame (A2: origin, rotation, scale 1/h), nu' in the frame, the self node, the gauge sign (A8).
+struct PairSetup {
+  double rp[3], nup[3], u3;
+  int64_t k;
+  int32_t Pp, self_local;
 };
 
-template <int P, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
-    k_pair_edge(int64_t sA, int64_t sB, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt,
-                int64_t kbase, const int32_t *__restrict__ pair_patch, const double *__restrict__ fit,
-                const double *__restrict__ tx, const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
-                const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Arow,
-                double *__restrict__ Xrow, int32_t *__restrict__ pstat, int64_t obase,
-                unsigned long long *__restrict__ swapcnt, const double *__restrict__ trtab) {
+template <int P>
+__global__ void k_pair_setup(int64_t sA, int64_t sB, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt,
+                             int64_t kbase, const int32_t *__restrict__ pair_patch, const double *__restrict__ fit,
+                             const double *__restrict__ tx, const double *__restrict__ tnorm,
+                             const int64_t *__restrict__ self_node, const int8_t *__restrict__ side,
+                             PairSetup *__restrict__ setup) {
   using D = Dims<P>;
-  const double *wS = trtab + TrCfg<P>::WS;
   using L = Layout<P>;
-  using XR = XRow<P>;
-  constexpr int Q = D::Q, E = D::E, NP = D::NP, NS = D::NS, K = D::K;
-  extern __shared__ double smem[];
-  double *sU = smem;                  // [Q][Q]
-  double *stgl = sU + Q * Q, *swgl = stgl + Q;
-  double *sxo = swgl + Q, *swo = sxo + n_omega;
-  double *shc = swo + n_omega;        // [HC_SIZE]
-  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + HC_SIZE;
-  tab_doubles = (tab_doubles + 1) & ~1;
-  PairState<P> *pst = reinterpret_cast<PairState<P> *>(smem + tab_doubles);
-  WarpScr<P> *wscr = reinterpret_cast<WarpScr<P> *>(pst + WPB * kPPW);
-  for (int i = threadIdx.x; i < HC_SIZE; i += blockDim.x) shc[i] = T.hc[i];
-  for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) sU[i] = T.U[i];
-  for (int i = threadIdx.x; i < Q; i += blockDim.x) { stgl[i] = T.tgl[i]; swgl[i] = T.wgl[i]; }
-  for (int i = threadIdx.x; i < n_omega; i += blockDim.x) { sxo[i] = T.xo[i]; swo[i] = T.wo[i]; }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpScr<P> &wsc = wscr[warp];
-  __shared__ int nsw;                          // swap edges of the round (CTA-wide list for phase 4)
-  __shared__ int swl[WPB * kPPW * 3];
-  PairState<P> *mine = pst + warp * kPPW;      // this warp's 3 pairs
-  const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
-  unsigned long long nswap = 0;
-
-  // Phase-synchronous rounds of WPB * 3 pairs: all warps of the CTA step through the phases together
-  // (__syncthreads between phases), so the SM's instruction working set is one phase (v1 was bound by
-  // instruction fetch).  Phase 2 (Newton) packs the 3 pairs of a warp into 27 lanes.
-  long long ph_t = clock64();
-  for (int64_t base = sA + (int64_t)blockIdx.x * WPB * kPPW; base < sB; base += (int64_t)gridDim.x * WPB * kPPW) {
-    // ---------------- phase 1: frame, gauge (A2, A8), harmonics at the target (Step 4, P:L1448-1451)
-    if (lane < kPPW) {   // one lane per pair: the index / header loads of the 3 pairs overlap
-      const int pp = lane;
-      PairState<P> &ps = mine[pp];
-      const int64_t s = base + warp * kPPW + pp;
-      const bool active = s < sB;
-      ps.active = active;
-      if (active) {
+  const int64_t s = sA + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= sB) return;
         const int64_t k = perm[s], t = ptgt[k - kbase];
         const int Pp = pair_patch[k];
         const double *hd = fit + (int64_t)Pp * L::STRIDE + L::HDR;
@@ -316,8 +264,85 @@ __global__ void __launch_bounds__(WPB * 32)
             else sg = (z - 0.5 * (zlo + zhi) > 0) ? 1.0 : -1.0;
           }
         }
-        ps.k = k; ps.t = t; ps.Pp = Pp; ps.self_local = self_local; ps.u3 = sg;
-        for (int a = 0; a < 3; ++a) { ps.rp[a] = rp[a]; ps.nup[a] = nup[a]; }
+        PairSetup &q = setup[s - sA];
+        q.k = k; q.Pp = Pp; q.self_local = self_local; q.u3 = sg;
+        for (int a = 0; a < 3; ++a) { q.rp[a] = rp[a]; q.nup[a] = nup[a]; }
+}
+
+// Per-pair state of k_pair_edge (shared memory; one per pair of the CTA round).
+template <int P>
+struct PairState {
+  using D = Dims<P>;
+  cd R[D::NS];                 // R_l^m at (y', z', x'): S^{(l,m)}(r') for m >= 0
+  double I[3][D::Q], J[3][D::Q];
+  double t0[3][2];
+  double rp[3], nup[3], u3, om[8], o0e[3];
+  int64_t k, t;
+  int Pp, self_local, active, pad;
+  int swap[3], conv[3], direct[3];
+};
+constexpr int kPPW = 3;   // pairs per warp per round (the Newton phase packs 3 x 9 = 27 lanes)
+
+// Per-warp scratch: gradient tables of the warp's pairs (phase 1 -> phase 5) and the direct-rule buffer.
+template <int P>
+struct WarpScr {
+  using D = Dims<P>;
+  cd GS[kPPW][D::NS][3];
+  double r13[2][kNDirect];
+};
+
+template <int P, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    k_pair_edge(int64_t sA, int64_t sB, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt,
+                int64_t kbase, const int32_t *__restrict__ pair_patch, const double *__restrict__ fit,
+                const double *__restrict__ tx, const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
+                const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Arow,
+                double *__restrict__ Xrow, int32_t *__restrict__ pstat, int64_t obase,
+                unsigned long long *__restrict__ swapcnt, const double *__restrict__ trtab,
+                const PairSetup *__restrict__ setup) {
+  using D = Dims<P>;
+  const double *wS = trtab + TrCfg<P>::WS;
+  using L = Layout<P>;
+  using XR = XRow<P>;
+  constexpr int Q = D::Q, E = D::E, NP = D::NP, NS = D::NS, K = D::K;
+  extern __shared__ double smem[];
+  double *sU = smem;                  // [Q][Q]
+  double *stgl = sU + Q * Q, *swgl = stgl + Q;
+  double *sxo = swgl + Q, *swo = sxo + n_omega;
+  double *shc = swo + n_omega;        // [HC_SIZE]
+  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + HC_SIZE;
+  tab_doubles = (tab_doubles + 1) & ~1;
+  PairState<P> *pst = reinterpret_cast<PairState<P> *>(smem + tab_doubles);
+  WarpScr<P> *wscr = reinterpret_cast<WarpScr<P> *>(pst + WPB * kPPW);
+  for (int i = threadIdx.x; i < HC_SIZE; i += blockDim.x) shc[i] = T.hc[i];
+  for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) sU[i] = T.U[i];
+  for (int i = threadIdx.x; i < Q; i += blockDim.x) { stgl[i] = T.tgl[i]; swgl[i] = T.wgl[i]; }
+  for (int i = threadIdx.x; i < n_omega; i += blockDim.x) { sxo[i] = T.xo[i]; swo[i] = T.wo[i]; }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpScr<P> &wsc = wscr[warp];
+  __shared__ int nsw;                          // swap edges of the round (CTA-wide list for phase 4)
+  __shared__ int swl[WPB * kPPW * 3];
+  PairState<P> *mine = pst + warp * kPPW;      // this warp's 3 pairs
+  const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
+  unsigned long long nswap = 0;
+
+  // Phase-synchronous rounds of WPB * 3 pairs: all warps of the CTA step through the phases together
+  // (__syncthreads between phases), so the SM's instruction working set is one phase (v1 was bound by
+  // instruction fetch).  Phase 2 (Newton) packs the 3 pairs of a warp into 27 lanes.
+  long long ph_t = clock64();
+  for (int64_t base = sA + (int64_t)blockIdx.x * WPB * kPPW; base < sB; base += (int64_t)gridDim.x * WPB * kPPW) {
+    // ---------------- phase 1: frame, gauge (A2, A8), harmonics at the target (Step 4, P:L1448-1451)
+    if (lane < kPPW) {   // one lane per pair: the per-pair setup from k_pair_setup
+      const int pp = lane;
+      PairState<P> &ps = mine[pp];
+      const int64_t s = base + warp * kPPW + pp;
+      const bool active = s < sB;
+      ps.active = active;
+      if (active) {
+        const PairSetup &q = setup[s - sA];
+        ps.k = q.k; ps.Pp = q.Pp; ps.self_local = q.self_local; ps.u3 = q.u3;
+        for (int a = 0; a < 3; ++a) { ps.rp[a] = q.rp[a]; ps.nup[a] = q.nup[a]; }
       }
     }
     __syncwarp();

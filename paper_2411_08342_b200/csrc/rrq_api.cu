@@ -36,7 +36,7 @@ struct rrq_ctx_s {
     size_t n = 0;
   };
   int64_t last_np = 0, last_nz = 0, last_nzs = 0, last_sA = 0;
-  Buf Arow, Xrow, Qrow, ipatch;
+  Buf Arow, Xrow, Qrow, ipatch, psetup;
   Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one, swapcnt;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
@@ -437,7 +437,7 @@ void rrq_destroy(rrq_ctx c) {
   if (c->swapcnt.p) cudaFree(c->swapcnt.p);
   cudaFree(c->d_tab);
   if (c->d_trtab) cudaFree(c->d_trtab);
-  for (auto *b : {&c->Arow, &c->Xrow, &c->Qrow, &c->ipatch, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
+  for (auto *b : {&c->Arow, &c->Xrow, &c->Qrow, &c->ipatch, &c->psetup, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
                   &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
     if (b->p) cudaFree(b->p);
   delete c;
@@ -745,7 +745,8 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     P0 = P1;
   }
   if (!ensure(c, c->Arow, (size_t)maxsub * 2 * D::K * 8) || !ensure(c, c->Xrow, (size_t)maxsub * XRow<P>::STRIDE * 8) ||
-      !ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxsub * D::NZS * 8))
+      !ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxsub * D::NZS * 8) ||
+      !ensure(c, c->psetup, (size_t)maxsub * sizeof(PairSetup)))
     return RRQ_ERR_CUDA;
   static bool attr_set = false;
   if (!attr_set) {
@@ -762,11 +763,14 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     const int64_t np_ = sB - sA;
     {
       TScope t1(c, 2, st);
+      k_pair_setup<P><<<nblk(np_, 256), 256, 0, st>>>(sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase,
+                                                       pair_patch, fit, tg->x, tg->normal, tg->self_node, tg->side,
+                                                       bp<PairSetup>(c->psetup));
       unsigned grid = (unsigned)std::min<int64_t>((np_ + kWPB * kPPW - 1) / (kWPB * kPPW), (int64_t)c->num_sms * 4);
       k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), st>>>(
           sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
           tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, bp<double>(c->Arow), bp<double>(c->Xrow),
-          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab);
+          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, bp<PairSetup>(c->psetup));
     }
     if ((r = cuda_check(c, "k_pair_edge"))) return r;
     {
@@ -792,7 +796,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
           obase, col_idx, vals[0], vals[1], vals[2], vals[3], pstat);
     }
     if ((r = cuda_check(c, "k_contract"))) return r;
-    c->launches += 4;
+    c->launches += 5;
     c->last_sA = sA;
     c->last_np = np_;
   }
