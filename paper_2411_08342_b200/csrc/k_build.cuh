@@ -897,13 +897,36 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   // Q row (entry e -> position posq[e] at stride EQ; V of (j >= 2, k) next to it) and the S'/NG' block
   // (entry e -> position poss[e] at stride SXW): positions chosen by the host to spread the main loop's
   // shared-memory banks
+  // destinations of this lane's 16-B chunks, fixed for every pair: computed once (registers)
+  constexpr int NCQ_ = 8 * D::NQ, NLQ = (NCQ_ + 31) / 32, NLV = (D::NV + 31) / 32, NLS = (2 * P * P + 31) / 32;
+  int dq[NLQ], dv[NLV], ds[NLS];
+#pragma unroll
+  for (int u = 0; u < NLQ; ++u) {
+    const int i = lane + 32 * u;
+    dq[u] = i < NCQ_ ? EQ * posq[i >> 3] + 2 * (i & 7) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < NLV; ++u) {
+    const int i = lane + 32 * u;
+    dv[u] = i < D::NV ? QR::SV + 2 * (i < 2 ? i : posq[i - 2] + 2) : 0;
+  }
+#pragma unroll
+  for (int u = 0; u < NLS; ++u) {
+    const int i = lane + 32 * u;
+    ds[u] = i < 2 * P * P ? SXW * poss[i >> 1] + 2 * (i & 1) : 0;
+  }
   auto issue_qs = [&](int64_t s, int b) {
     const double *qg = Qrow + (s - sA) * QR::STRIDE, *xg = Xrow + (s - sA) * XR::STRIDE + XR::SX;
     double *qd = QB + b * C::QSZ, *sd = SXB + b * C::SXSZ;
-    for (int i = lane; i < 8 * D::NQ; i += 32) cp_async16(qd + EQ * posq[i >> 3] + 2 * (i & 7), qg + 2 * i);
-    for (int i = lane; i < D::NV; i += 32)
-      cp_async16(qd + QR::SV + 2 * (i < 2 ? i : posq[i - 2] + 2), qg + QR::V + 2 * i);
-    for (int i = lane; i < 2 * P * P; i += 32) cp_async16(sd + SXW * poss[i >> 1] + 2 * (i & 1), xg + 2 * i);
+#pragma unroll
+    for (int u = 0; u < NLQ; ++u)
+      if (lane + 32 * u < NCQ_) cp_async16(qd + dq[u], qg + 2 * (lane + 32 * u));
+#pragma unroll
+    for (int u = 0; u < NLV; ++u)
+      if (lane + 32 * u < D::NV) cp_async16(qd + dv[u], qg + QR::V + 2 * (lane + 32 * u));
+#pragma unroll
+    for (int u = 0; u < NLS; ++u)
+      if (lane + 32 * u < 2 * P * P) cp_async16(sd + ds[u], xg + 2 * (lane + 32 * u));
   };
   auto issue_g = [&](int64_t s) {
     const double *xg = Xrow + (s - sA) * XR::STRIDE + XR::G;
