@@ -310,19 +310,22 @@ __global__ void __launch_bounds__(WPB * 32)
   double *stgl = sU + Q * Q, *swgl = stgl + Q;
   double *sxo = swgl + Q, *swo = sxo + n_omega;
   double *shc = swo + n_omega;        // [HC_SIZE]
-  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + HC_SIZE;
+  double *sxdp = shc + HC_SIZE;       // [kNDirect][Q] powers of the direct-rule nodes (reading A11')
+  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + HC_SIZE + kNDirect * Q;
   tab_doubles = (tab_doubles + 1) & ~1;
   PairState<P> *pst = reinterpret_cast<PairState<P> *>(smem + tab_doubles);
+  __shared__ int nsw;                          // swap edges of the round (CTA-wide list, phases 2b and 4)
+  __shared__ int swl[WPB * kPPW * 3];
   WarpScr<P> *wscr = reinterpret_cast<WarpScr<P> *>(pst + WPB * kPPW);
   for (int i = threadIdx.x; i < HC_SIZE; i += blockDim.x) shc[i] = T.hc[i];
   for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) sU[i] = T.U[i];
   for (int i = threadIdx.x; i < Q; i += blockDim.x) { stgl[i] = T.tgl[i]; swgl[i] = T.wgl[i]; }
   for (int i = threadIdx.x; i < n_omega; i += blockDim.x) { sxo[i] = T.xo[i]; swo[i] = T.wo[i]; }
+  for (int i = threadIdx.x; i < kNDirect * Q; i += blockDim.x) sxdp[i] = T.xdp[i];
+  if (threadIdx.x == 0) nsw = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpScr<P> &wsc = wscr[warp];
-  __shared__ int nsw;                          // swap edges of the round (CTA-wide list for phase 4)
-  __shared__ int swl[WPB * kPPW * 3];
   PairState<P> *mine = pst + warp * kPPW;      // this warp's 3 pairs
   const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
   unsigned long long nswap = 0;
@@ -450,17 +453,24 @@ __global__ void __launch_bounds__(WPB * 32)
       }
     }
     __syncwarp();
-    // model integrals (reading A11 / A11'): recurrences inside rho = 1.6 (lanes (pair, edge)), a 48-point
-    // rule outside
-    if (lane < 9) {
-      PairState<P> &ps = mine[lane / 3];
-      const int e = lane % 3;
-      if (ps.active && ps.swap[e] && !ps.direct[e]) model_integrals<Q>(ps.t0[e][0], fabs(ps.t0[e][1]), ps.I[e], ps.J[e]);
+    // the round's swap edges -> CTA-wide list (phases 2b and 4)
+    __syncwarp();
+    if (lane < 3 * kPPW) {
+      const PairState<P> &ps = mine[lane / 3];
+      if (ps.active && ps.swap[lane % 3]) swl[atomicAdd(&nsw, 1)] = warp * 3 * kPPW + lane;
     }
-    for (int pe = 0; pe < 9; ++pe) {
-      PairState<P> &ps = mine[pe / 3];
-      const int e = pe % 3;
-      if (!(ps.active && ps.swap[e] && ps.direct[e])) continue;
+    __syncthreads();
+    // phase 2b, model integrals (reading A11 / A11'): recurrences inside rho = 1.6 (one thread per swap
+    // edge of the CTA), a 48-point rule outside (one warp per edge)
+    for (int q = threadIdx.x; q < nsw; q += blockDim.x) {
+      PairState<P> &ps = pst[swl[q] / 3];
+      const int e = swl[q] % 3;
+      if (!ps.direct[e]) model_integrals<Q>(ps.t0[e][0], fabs(ps.t0[e][1]), ps.I[e], ps.J[e]);
+    }
+    for (int q = warp; q < nsw; q += WPB) {
+      PairState<P> &ps = pst[swl[q] / 3];
+      const int e = swl[q] % 3;
+      if (!ps.direct[e]) continue;
       const double a = ps.t0[e][0], b = fabs(ps.t0[e][1]);
       for (int j = lane; j < kNDirect; j += 32) {
         const double xj = T.xd[j], Qv = (xj - a) * (xj - a) + b * b;
@@ -472,7 +482,7 @@ __global__ void __launch_bounds__(WPB * 32)
       if (lane < Q) {
         double si = 0, sj = 0;
         for (int j = 0; j < kNDirect; ++j) {
-          const double pw = __ldg(T.xdp + j * Q + lane);
+          const double pw = sxdp[j * Q + lane];
           si = fma(pw, wsc.r13[0][j], si);
           sj = fma(pw, wsc.r13[1][j], sj);
         }
@@ -481,14 +491,9 @@ __global__ void __launch_bounds__(WPB * 32)
       }
       __syncwarp();
     }
-    if (threadIdx.x == 0) nsw = 0;
     __syncthreads();
     RRQ_PHASE_MARK(1);
     // ---------------- phase 3: weights and the scalar line integrals (Step 6)
-    if (lane < 3 * kPPW) {
-      const PairState<P> &ps = mine[lane / 3];
-      if (ps.active && ps.swap[lane % 3]) swl[atomicAdd(&nsw, 1)] = warp * 3 * kPPW + lane;
-    }
     for (int pp = 0; pp < kPPW; ++pp) {
       PairState<P> &ps = mine[pp];
       if (!ps.active) continue;
@@ -625,6 +630,7 @@ __global__ void __launch_bounds__(WPB * 32)
       }
     }
     __syncwarp();
+    if (threadIdx.x == 0) nsw = 0;   // the list was last read in phase 4
     __syncthreads();
     RRQ_PHASE_MARK(4);
   }

@@ -670,7 +670,7 @@ constexpr int kWPB = 8;   // warps per CTA of k_pair_edge
 template <int P>
 static size_t edge_smem(int n_omega) {
   using D = Dims<P>;
-  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + HC_SIZE;
+  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + HC_SIZE + kNDirect * D::Q;
   tab = (tab + 1) & ~1;
   return (size_t)tab * sizeof(double) + kWPB * kPPW * sizeof(PairState<P>) + kWPB * sizeof(WarpScr<P>);
 }
