@@ -1162,7 +1162,18 @@ __global__ void __launch_bounds__(256, 2)
     }
   }
   __syncthreads();
-  mbar_wait(&bar[0], 0);   // Z tile (and chunk 0)
+  // P_Sd fragments for Theta . P_Sd straight from global, issued before waiting for the Z tile
+  constexpr int NK = (NP + 3) / 4;
+  double bq[CC::TPW][NK];
+#pragma unroll
+  for (int tw = 0; tw < CC::TPW; ++tw) {
+    const int tile = warp + tw * CC::WARPS, bn = (tile / CC::MT) * 8 + (lane >> 2);
+#pragma unroll
+    for (int q = 0; q < NK; ++q) {
+      const int kk = 4 * q + (lane & 3);
+      bq[tw][q] = (tile < CC::TILES && bn < N && kk < NP) ? __ldg(PSd + kk * NB + bn) : 0.0;
+    }
+  }
   const double h = blk[L::HDR + H_H];
   const double inv4pi = 1.0 / (4.0 * kPi);
   double acc[CC::TPW][8];
@@ -1170,24 +1181,16 @@ __global__ void __launch_bounds__(256, 2)
   for (int tw = 0; tw < CC::TPW; ++tw)
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[tw][q] = 0.0;
-  // Theta . P_Sd (k over NP, straight from global; small)
+  mbar_wait(&bar[0], 0);   // Z tile (and chunk 0)
 #pragma unroll
   for (int tw = 0; tw < CC::TPW; ++tw) {
     const int tile = warp + tw * CC::WARPS;
     if (tile >= CC::TILES) continue;
-    const int mt = tile % CC::MT, nt = tile / CC::MT, bn = nt * 8 + (lane >> 2);
-    const double *zr = sz + (mt * 8 + (lane >> 2)) * ZS + (lane & 3);
-    constexpr int NK = (NP + 3) / 4;
-    double bq[NK];
-#pragma unroll
-    for (int q = 0; q < NK; ++q) {   // all loads first (latency overlapped), then the DMMAs
-      const int kk = 4 * q + (lane & 3);
-      bq[q] = (bn < N && kk < NP) ? __ldg(PSd + kk * NB + bn) : 0.0;
-    }
+    const double *zr = sz + ((tile % CC::MT) * 8 + (lane >> 2)) * ZS + (lane & 3);
 #pragma unroll
     for (int q = 0; q < NK; ++q) {
       const int kk = 4 * q + (lane & 3);
-      dmma(acc[tw][0], acc[tw][1], kk < NP ? zr[4 * q] : 0.0, bq[q]);
+      dmma(acc[tw][0], acc[tw][1], kk < NP ? zr[4 * q] : 0.0, bq[tw][q]);
     }
   }
   // the 4 NP blocks, B double-buffered through shared memory; emp[b] = "every warp is done with buffer b"
