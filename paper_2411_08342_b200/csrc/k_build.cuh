@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(WPB * 32)
     }
     if (lane < 3 * kPPW && mine[lane / 3].active)
       Xrow[(base + warp * kPPW + lane / 3 - sA) * XR::STRIDE + XR::NU + lane % 3] = mine[lane / 3].nup[lane % 3];
-    __syncthreads();
+    __syncwarp();   // next phase only reads this warp's pairs
     RRQ_PHASE_MARK(0);
     // ---------------- phase 2: t0 per edge (reading A12, A12'), lanes (pair, edge, comp) = 27 lanes
     {
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(WPB * 32)
       if (lane == 0)
         for (int i = 0; i < 8; ++i) ps.om[i] = om[i];
     }
-    __syncthreads();
+    __syncwarp();   // next phase only reads this warp's pairs
     RRQ_PHASE_MARK(2);
     // ---------------- phase 4: Omega_0 on swap edges: sinh-split Gauss-Legendre (reading A9); the round's
     // swap edges are spread over all warps of the CTA (warp per edge)
