@@ -123,7 +123,9 @@ rrq_status rrq_patch_fit(rrq_ctx ctx, const rrq_surface *surf, void *fit, int32_
  *   pair_status [pairs of the chunk] int32 or NULL: bit0 Newton fallback on some edge, bit1
  *               nonfinite weight.
  * fit is the buffer written by rrq_patch_fit.  Nodes of a row are in patch-local order, patches
- * ascending.  Weights are in global units (S rows scale with h_P, D' rows with 1/h_P). */
+ * ascending.  Weights are in global units (S rows scale with h_P, D' rows with 1/h_P).
+ * Alignment: surf->nodes, normals, weights and vals[k] 16-byte aligned, col_idx 8-byte aligned
+ * (RRQ_ERR_INVALID_ARG otherwise); cudaMalloc / torch allocations satisfy this. */
 rrq_status rrq_build_correction(rrq_ctx ctx, const rrq_surface *surf, const rrq_targets *tgt,
                                 const int64_t *pair_ptr, const int32_t *pair_patch, int64_t n_pairs,
                                 int64_t row_begin, int64_t row_end, const void *fit, uint32_t kernel_mask,

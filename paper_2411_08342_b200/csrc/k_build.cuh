@@ -1084,7 +1084,8 @@ struct ContractCfg {
   static constexpr int NCH = 4 * D::NP / KC;
   static constexpr size_t SMEM_Z = (size_t)TP * ZS;
   static constexpr size_t SMEM_B = 3 * (size_t)KC * NB;                                       // PD | PSp | PSg
-  static constexpr size_t SMEM = (SMEM_Z + 2 * SMEM_B + TP * 8) * sizeof(double) + TP * 16;
+  static constexpr size_t SNODE = (7 * D::N + 1) / 2 * 2;   // the patch's nodes [N][3], normals [N][3], weights [N]
+  static constexpr size_t SMEM = (SMEM_Z + 2 * SMEM_B + SNODE + TP * 8) * sizeof(double) + TP * 16;
 };
 
 template <int P>
@@ -1103,7 +1104,8 @@ __global__ void __launch_bounds__(256, 2)
   constexpr int N = D::N, NP = D::NP, TP = CC::TP, ZS = CC::ZS, NZS = D::NZS, NB = CC::NB, KC = CC::KC;
   extern __shared__ __align__(16) double sz[];
   double *sB = sz + CC::SMEM_Z;                    // [2][3][KC][NB]
-  double *sT = sB + 2 * CC::SMEM_B;                // [TP][8] target x, nu'
+  double *sN = sB + 2 * CC::SMEM_B;                // nodes [N][3] | normals [N][3] | weights [N] of the patch
+  double *sT = sN + CC::SNODE;                     // [TP][8] target x, nu'
   int64_t *sK = reinterpret_cast<int64_t *>(sT + TP * 8);
   int *sSelf = reinterpret_cast<int *>(sK + TP);
   const int64_t item = item0 + blockIdx.x;
@@ -1141,9 +1143,15 @@ __global__ void __launch_bounds__(256, 2)
     }
   };
   {
-    const unsigned zb = (unsigned)(cnt * NZS * sizeof(double));
-    issue(0, zb);
-    if (threadIdx.x == 32) bulk_g2s(sz, Zrow + (s0 - sA) * NZS, zb, &bar[0]);
+    const unsigned zb = (unsigned)(cnt * NZS * sizeof(double)), nb3 = (unsigned)(3 * N * sizeof(double)),
+                   nb1 = (unsigned)(N * sizeof(double));
+    issue(0, zb + 2 * nb3 + nb1);
+    if (threadIdx.x == 32) {
+      bulk_g2s(sz, Zrow + (s0 - sA) * NZS, zb, &bar[0]);
+      bulk_g2s(sN, nodes + Pp * N * 3, nb3, &bar[0]);
+      bulk_g2s(sN + 3 * N, normals + Pp * N * 3, nb3, &bar[0]);
+      bulk_g2s(sN + 6 * N, weights + Pp * N, nb1, &bar[0]);
+    }
   }
   for (int r = threadIdx.x; r < TP; r += blockDim.x) {
     if (r < cnt) {
@@ -1238,13 +1246,16 @@ __global__ void __launch_bounds__(256, 2)
     const int row = mt * 8 + (lane >> 2);
     if (row >= cnt) continue;
     const double accS[2] = {aS0, aS1}, accD[2] = {aD0, aD1}, accSp[2] = {aSp0, aSp1}, accDp[2] = {aDp0, aDp1};
+    double oS[2], oD[2], oSp[2], oDp[2];
+    bool bad = false;
+    const int i0 = nt * 8 + 2 * (lane & 3);
+#pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const int i = nt * 8 + 2 * (lane & 3) + q;
-      if (i >= N) continue;
+      const int i = i0 + q;
       double S = accS[q] * h, Dv = accD[q], Sp = accSp[q], Dp = accDp[q] / h;
-      if (!raw && sSelf[row] != i) {
-        const double *xi = nodes + (Pp * N + i) * 3, *ni = normals + (Pp * N + i) * 3;
-        const double wi = weights[Pp * N + i];
+      if (!raw && i < N && sSelf[row] != i) {
+        const double *xi = sN + 3 * i, *ni = sN + 3 * N + 3 * i;
+        const double wi = sN[6 * N + i];
         const double d0 = sT[row * 8] - xi[0], d1 = sT[row * 8 + 1] - xi[1], d2 = sT[row * 8 + 2] - xi[2];
         const double r2 = d0 * d0 + d1 * d1 + d2 * d2;
         double ir = rsqrt(r2);
@@ -1258,15 +1269,27 @@ __global__ void __launch_bounds__(256, 2)
         Sp += inv4pi * dnp * ir3 * wi;
         Dp -= inv4pi * (nn * ir3 - 3.0 * dn * dnp * ir3 * ir * ir) * wi;
       }
-      const int64_t o = (sK[row] - obase) * N + i;
-      if (col_idx) col_idx[o] = (int32_t)(Pp * N + i);
-      bool bad = false;
-      if (vS) { vS[o] = (mask & 1) ? S : 0.0; bad |= !isfinite(S); }
-      if (vD) { vD[o] = (mask & 2) ? Dv : 0.0; bad |= !isfinite(Dv); }
-      if (vSp) { vSp[o] = (mask & 4) ? Sp : 0.0; bad |= !isfinite(Sp); }
-      if (vDp) { vDp[o] = (mask & 8) ? Dp : 0.0; bad |= !isfinite(Dp); }
-      if (bad && pstat) atomicOr(pstat + (sK[row] - obase), 2);
+      oS[q] = (mask & 1) ? S : 0.0;
+      oD[q] = (mask & 2) ? Dv : 0.0;
+      oSp[q] = (mask & 4) ? Sp : 0.0;
+      oDp[q] = (mask & 8) ? Dp : 0.0;
+      if (i < N) bad |= !isfinite(S) || !isfinite(Dv) || !isfinite(Sp) || !isfinite(Dp);
     }
+    const int64_t o = (sK[row] - obase) * N + i0;
+    if (i0 + 1 < N) {   // the usual case: both columns, 16-B stores
+      if (col_idx) *reinterpret_cast<int2 *>(col_idx + o) = make_int2((int32_t)(Pp * N + i0), (int32_t)(Pp * N + i0 + 1));
+      if (vS) *reinterpret_cast<double2 *>(vS + o) = make_double2(oS[0], oS[1]);
+      if (vD) *reinterpret_cast<double2 *>(vD + o) = make_double2(oD[0], oD[1]);
+      if (vSp) *reinterpret_cast<double2 *>(vSp + o) = make_double2(oSp[0], oSp[1]);
+      if (vDp) *reinterpret_cast<double2 *>(vDp + o) = make_double2(oDp[0], oDp[1]);
+    } else if (i0 < N) {
+      if (col_idx) col_idx[o] = (int32_t)(Pp * N + i0);
+      if (vS) vS[o] = oS[0];
+      if (vD) vD[o] = oD[0];
+      if (vSp) vSp[o] = oSp[0];
+      if (vDp) vDp[o] = oDp[0];
+    }
+    if (bad && pstat) atomicOr(pstat + (sK[row] - obase), 2);
   }
 }
 

@@ -829,6 +829,12 @@ rrq_status rrq_build_correction(rrq_ctx c, const rrq_surface *s, const rrq_targe
   if (n_pairs < 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_pairs < 0");
   if ((mask & (RRQ_SP | RRQ_DP)) && !tg->normal) return fail(c, RRQ_ERR_INVALID_ARG, "S' and D' need target normals");
   if ((mask & RRQ_ALL) == 0) return fail(c, RRQ_ERR_INVALID_ARG, "kernel_mask selects no kernel");
+  {   // the contraction stores weight pairs with 16-B (8-B index) stores and stages the patch's nodes by bulk copies
+    auto al = [](const void *q, uintptr_t a) { return q == nullptr || ((uintptr_t)q % a) == 0; };
+    if (!al(s->nodes, 16) || !al(s->normals, 16) || !al(s->weights, 16) || !al(col_idx, 8) || !al(vals[0], 16) ||
+        !al(vals[1], 16) || !al(vals[2], 16) || !al(vals[3], 16))
+      return fail(c, RRQ_ERR_INVALID_ARG, "nodes/normals/weights/vals must be 16-byte aligned, col_idx 8-byte aligned");
+  }
   if (row_end == row_begin) return RRQ_OK;
   cudaStream_t st = (cudaStream_t)stream;
   switch (c->prm.p) {
