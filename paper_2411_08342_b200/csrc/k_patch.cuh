@@ -368,19 +368,26 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
       }
     }
     __syncthreads();
-    // ---- real Householder QR of B (N x NP, column-major in Bm) -> P_Sd = B^+
+    // ---- the real part runs in shared memory (the Fq space is free now): B, then Xs, Hm (then HP over Xs)
+    double *const sBm = Fq, *const sXs = Fq + (size_t)NP * N, *const sHm = sXs + (size_t)N * N;
+    for (int i = threadIdx.x; i < NP * N; i += blockDim.x) {
+      sBm[i] = Bm[i];
+      sHm[i] = Hm[i];
+    }
+    __syncthreads();
+    // ---- real Householder QR of B (N x NP, column-major in sBm) -> P_Sd = B^+
     for (int j = 0; j < NP; ++j) {
       double s = 0;
-      for (int i = j + threadIdx.x; i < N; i += blockDim.x) s += Bm[(size_t)j * N + i] * Bm[(size_t)j * N + i];
+      for (int i = j + threadIdx.x; i < N; i += blockDim.x) s += sBm[(size_t)j * N + i] * sBm[(size_t)j * N + i];
       s = warp_sum(s);
       if (lane == 0) sh[warp] = s;
       __syncthreads();
       if (threadIdx.x == 0) {
         double n2 = 0;
         for (int w = 0; w < nw; ++w) n2 += sh[w];
-        const double nrm = sqrt(n2), ajj = Bm[(size_t)j * N + j];
+        const double nrm = sqrt(n2), ajj = sBm[(size_t)j * N + j];
         const double alpha = ajj > 0 ? -nrm : nrm;
-        Bm[(size_t)j * N + j] = ajj - alpha;
+        sBm[(size_t)j * N + j] = ajj - alpha;
         rdb[j] = alpha;
         betab[j] = nrm * (nrm + fabs(ajj));
       }
@@ -389,43 +396,43 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
       if (bj > 0)
         for (int c = j + 1 + warp; c < NP; c += nw) {
           double t = 0;
-          for (int i = j + lane; i < N; i += 32) t += Bm[(size_t)j * N + i] * Bm[(size_t)c * N + i];
+          for (int i = j + lane; i < N; i += 32) t += sBm[(size_t)j * N + i] * sBm[(size_t)c * N + i];
           t = warp_sum(t) / bj;
-          for (int i = j + lane; i < N; i += 32) Bm[(size_t)c * N + i] -= t * Bm[(size_t)j * N + i];
+          for (int i = j + lane; i < N; i += 32) sBm[(size_t)c * N + i] -= t * sBm[(size_t)j * N + i];
         }
       __syncthreads();
     }
     for (int c = warp; c < N; c += nw) {
-      double *w = Xs + (size_t)c * N;
+      double *w = sXs + (size_t)c * N;
       for (int i = lane; i < N; i += 32) w[i] = i == c ? 1.0 : 0.0;
       __syncwarp();
       for (int j = 0; j < NP; ++j) {
         const double bj = betab[j];
         if (!(bj > 0)) continue;
         double t = 0;
-        for (int i = j + lane; i < N; i += 32) t += Bm[(size_t)j * N + i] * w[i];
+        for (int i = j + lane; i < N; i += 32) t += sBm[(size_t)j * N + i] * w[i];
         t = warp_sum(t) / bj;
-        for (int i = j + lane; i < N; i += 32) w[i] -= t * Bm[(size_t)j * N + i];
+        for (int i = j + lane; i < N; i += 32) w[i] -= t * sBm[(size_t)j * N + i];
         __syncwarp();
       }
     }
     __syncthreads();
     for (int c = threadIdx.x; c < N; c += blockDim.x) {
-      double *w = Xs + (size_t)c * N;
+      double *w = sXs + (size_t)c * N;
       for (int r = NP - 1; r >= 0; --r) {
         double s = w[r];
-        for (int k = r + 1; k < NP; ++k) s -= Bm[(size_t)k * N + r] * w[k];
+        for (int k = r + 1; k < NP; ++k) s -= sBm[(size_t)k * N + r] * w[k];
         w[r] = s / rdb[r];
         PSd[r * NF + c] = w[r];
       }
     }
     __syncthreads();
-    // ---- P_Sg = P_D (Hm P_Sd); HP in the (now free) Fq space
-    double *HP = Fq;
+    // ---- P_Sg = P_D (sHm P_Sd); HP over the (now dead) Xs
+    double *HP = sXs;
     for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
       const int i = t / N, j = t % N;
       double s = 0;
-      for (int c = 0; c < NP; ++c) s += Hm[(size_t)i * NP + c] * PSd[c * NF + j];
+      for (int c = 0; c < NP; ++c) s += sHm[(size_t)i * NP + c] * PSd[c * NF + j];
       HP[t] = s;
     }
     __syncthreads();
