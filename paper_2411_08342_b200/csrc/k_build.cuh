@@ -47,17 +47,26 @@ __device__ __noinline__ void model_integrals(double a, double b, double *I, doub
     I[0] = log((u + su) / (v + sv));
     J[0] = 4 * aa / (su * sv * (u * sv + v * su));
   }
-  double a2b2 = a * a + b * b, is1 = 1.0 / s1, ism = 1.0 / sm;
-  for (int k = 1; k < Q; ++k) {
-    double sg = ((k - 1) & 1) ? -1.0 : 1.0;
-    double beta = s1 - sg * sm, gam = is1 - sg * ism;
-    if (k == 1) {
-      I[1] = beta + a * I[0];
-      J[1] = a * J[0] - gam;
-    } else {
-      I[k] = (beta + (2 * k - 1) * a * I[k - 1] - (k - 1) * a2b2 * I[k - 2]) / k;
-      J[k] = a * J[k - 1] - gam + (k - 1) * I[k - 2];
-    }
+  // the recurrence runs in registers (fully unrolled; /k as a multiplication by the constant 1/k)
+  const double a2b2 = a * a + b * b, is1 = 1.0 / s1, ism = 1.0 / sm;
+  const double be = s1 - sm, bo = s1 + sm, ge = is1 - ism, go = is1 + ism;   // k-1 even / odd
+  double Im2 = I[0], Jm1 = J[0];
+  double Im1 = (s1 - sm) + a * Im2;   // k = 1 (k-1 = 0 even)
+  double J1 = a * Jm1 - (is1 - ism);
+  I[1] = Im1;
+  J[1] = J1;
+  Jm1 = J1;
+#pragma unroll
+  for (int k = 2; k < Q; ++k) {
+    const bool odd = ((k - 1) & 1) != 0;
+    const double beta = odd ? bo : be, gam = odd ? go : ge;
+    const double Ik = (beta + (2 * k - 1) * a * Im1 - (k - 1) * a2b2 * Im2) * (1.0 / k);
+    const double Jk = a * Jm1 - gam + (k - 1) * Im2;
+    I[k] = Ik;
+    J[k] = Jk;
+    Im2 = Im1;
+    Im1 = Ik;
+    Jm1 = Jk;
   }
 }
 
