@@ -482,21 +482,24 @@ __global__ void __launch_bounds__(WPB * 32)
       if (!ps.direct[e]) continue;
       const double a = ps.t0[e][0], b = fabs(ps.t0[e][1]);
       for (int j = lane; j < kNDirect; j += 32) {
-        const double xj = T.xd[j], Qv = (xj - a) * (xj - a) + b * b;
-        const double r1 = T.wd[j] / sqrt(Qv);
+        const double xj = T.xd[j], Qv = (xj - a) * (xj - a) + b * b, rs = rsqrt(Qv);
+        const double r1 = T.wd[j] * rs;
         wsc.r13[0][j] = r1;
-        wsc.r13[1][j] = r1 / Qv;
+        wsc.r13[1][j] = r1 * rs * rs;
       }
       __syncwarp();
-      if (lane < Q) {
-        double si = 0, sj = 0;
-        for (int j = 0; j < kNDirect; ++j) {
-          const double pw = sxdp[j * Q + lane];
-          si = fma(pw, wsc.r13[0][j], si);
-          sj = fma(pw, wsc.r13[1][j], sj);
+      if (lane < Q) {   // two interleaved partial sums (shorter dependency chains)
+        double si0 = 0, sj0 = 0, si1 = 0, sj1 = 0;
+#pragma unroll 4
+        for (int j = 0; j < kNDirect; j += 2) {
+          const double pw0 = sxdp[j * Q + lane], pw1 = sxdp[(j + 1) * Q + lane];
+          si0 = fma(pw0, wsc.r13[0][j], si0);
+          sj0 = fma(pw0, wsc.r13[1][j], sj0);
+          si1 = fma(pw1, wsc.r13[0][j + 1], si1);
+          sj1 = fma(pw1, wsc.r13[1][j + 1], sj1);
         }
-        ps.I[e][lane] = si;
-        ps.J[e][lane] = sj;
+        ps.I[e][lane] = si0 + si1;
+        ps.J[e][lane] = sj0 + sj1;
       }
       __syncwarp();
     }
