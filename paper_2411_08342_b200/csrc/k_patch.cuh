@@ -315,26 +315,53 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
         }
       __syncthreads();
     }
-    // ---- Q^H e_c (warp per column c), first NP entries kept
-    for (int c = warp; c < N; c += nw) {
-      double *w = W + (size_t)c * N * 4;
-      for (int i = lane; i < N; i += 32) qst(w + 4 * i, qd{i == c ? 1.0 : 0.0, 0, 0, 0});
-      __syncwarp();
-      for (int j = 0; j < NP; ++j) {
-        const double bj = beta[j];
-        if (!(bj > 0)) continue;
-        qd t = {0, 0, 0, 0};
-        for (int i = j + lane; i < N; i += 32) {
-          const qd p = qconjmul_(qld(Fq + ((size_t)j * N + i) * 4), qld(w + 4 * i));
-          t.s += p.s; t.x += p.x; t.y += p.y; t.z += p.z;
+    // ---- Q^H e_c (warp per pair of columns, the columns in registers: entry i = lane + 32 u), the first
+    // NP entries stored for the back substitution
+    {
+      constexpr int NU = (N + 31) / 32;
+      for (int c0 = 2 * warp; c0 < N; c0 += 2 * nw) {
+        qd y[2][NU];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int u = 0; u < NU; ++u) y[h][u] = qd{lane + 32 * u == c0 + h ? 1.0 : 0.0, 0, 0, 0};
+        for (int j = 0; j < NP; ++j) {
+          const double bj = beta[j];
+          if (!(bj > 0)) continue;
+          qd v[NU];
+          qd t[2] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            const int i = lane + 32 * u;
+            v[u] = (i >= j && i < N) ? qld(Fq + ((size_t)j * N + i) * 4) : qd{0, 0, 0, 0};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const qd p = qconjmul_(v[u], y[h][u]);
+              t[h].s += p.s; t[h].x += p.x; t[h].y += p.y; t[h].z += p.z;
+            }
+          }
+          const double ib = 1.0 / bj;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            t[h].s = warp_sum(t[h].s) * ib; t[h].x = warp_sum(t[h].x) * ib;
+            t[h].y = warp_sum(t[h].y) * ib; t[h].z = warp_sum(t[h].z) * ib;
+          }
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const qd vt = qmul_(v[u], t[h]);
+              y[h][u].s -= vt.s; y[h][u].x -= vt.x; y[h][u].y -= vt.y; y[h][u].z -= vt.z;
+            }
         }
-        t.s = warp_sum(t.s) / bj; t.x = warp_sum(t.x) / bj; t.y = warp_sum(t.y) / bj; t.z = warp_sum(t.z) / bj;
-        for (int i = j + lane; i < N; i += 32) {
-          const qd vt = qmul_(qld(Fq + ((size_t)j * N + i) * 4), t);
-          double *y = w + 4 * i;
-          y[0] -= vt.s; y[1] -= vt.x; y[2] -= vt.y; y[3] -= vt.z;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (c0 + h >= N) continue;
+          double *w = W + (size_t)(c0 + h) * N * 4;
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+            if (lane + 32 * u < NP) qst(w + 4 * (lane + 32 * u), y[h][u]);
         }
-        __syncwarp();
       }
     }
     __syncthreads();
