@@ -429,18 +429,43 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
         }
       __syncthreads();
     }
-    for (int c = warp; c < N; c += nw) {
-      double *w = sXs + (size_t)c * N;
-      for (int i = lane; i < N; i += 32) w[i] = i == c ? 1.0 : 0.0;
-      __syncwarp();
-      for (int j = 0; j < NP; ++j) {
-        const double bj = betab[j];
-        if (!(bj > 0)) continue;
-        double t = 0;
-        for (int i = j + lane; i < N; i += 32) t += sBm[(size_t)j * N + i] * w[i];
-        t = warp_sum(t) / bj;
-        for (int i = j + lane; i < N; i += 32) w[i] -= t * sBm[(size_t)j * N + i];
-        __syncwarp();
+    {   // Q_B^T e_c, four columns per warp in registers (entry i = lane + 32 u)
+      constexpr int NU = (N + 31) / 32, CW = 4;
+      for (int c0 = CW * warp; c0 < N; c0 += CW * nw) {
+        double y[CW][NU];
+#pragma unroll
+        for (int h = 0; h < CW; ++h)
+#pragma unroll
+          for (int u = 0; u < NU; ++u) y[h][u] = lane + 32 * u == c0 + h ? 1.0 : 0.0;
+        for (int j = 0; j < NP; ++j) {
+          const double bj = betab[j];
+          if (!(bj > 0)) continue;
+          double v[NU], t[CW];
+#pragma unroll
+          for (int h = 0; h < CW; ++h) t[h] = 0;
+#pragma unroll
+          for (int u = 0; u < NU; ++u) {
+            const int i = lane + 32 * u;
+            v[u] = (i >= j && i < N) ? sBm[(size_t)j * N + i] : 0.0;
+#pragma unroll
+            for (int h = 0; h < CW; ++h) t[h] = fma(v[u], y[h][u], t[h]);
+          }
+          const double ib = 1.0 / bj;
+#pragma unroll
+          for (int h = 0; h < CW; ++h) t[h] = warp_sum(t[h]) * ib;
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int h = 0; h < CW; ++h) y[h][u] = fma(-t[h], v[u], y[h][u]);
+        }
+#pragma unroll
+        for (int h = 0; h < CW; ++h) {
+          if (c0 + h >= N) continue;
+          double *w = sXs + (size_t)(c0 + h) * N;
+#pragma unroll
+          for (int u = 0; u < NU; ++u)
+            if (lane + 32 * u < N) w[lane + 32 * u] = y[h][u];
+        }
       }
     }
     __syncthreads();
