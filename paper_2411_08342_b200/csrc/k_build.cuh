@@ -92,62 +92,76 @@ struct XRow {
                        G = W, GSZ = (9 * D::NP + 3 + 1) / 2 * 2, STRIDE = G + GSZ;
 };
 // Per-pair row of k_qmap's output: per (j, k >= 0), 2 <= j <= p, at EG qidx(j,k): [Q (4 quaternion comps,
-// re/im) | dQ (same)] scaled by v_lambda(j,k); then V [2 NV] scaled by v_theta(j,k) (TrCfg).  k_translate
-// stages the entries at stride EQ = 18 (144 B: 8 consecutive entries start in 8 different 16-B bank groups).
+// re/im) | dQ (same)] scaled by v_lambda(j,k); then V [2 NV] scaled by v_theta(j,k) (TrCfg).
 template <int P>
 struct QRow {
   using D = Dims<P>;
-  static constexpr int EG = 16, EQ = 18;
+  static constexpr int EG = 16;
   static constexpr int V = EG * D::NQ, STRIDE = V + 2 * D::NV;
-  static constexpr int SV = EQ * D::NQ, SSZ = SV + 2 * D::NV;   // staged (shared-memory) layout
 };
 
-// k_translate's schedule (see k_translate): tasks = pairs of outputs (l, m0), (l, m0 + 1) (or a single
-// (l, l)); a task's terms are the (j, k), j >= 2, in the union of the two outputs' k ranges.
-__host__ __device__ constexpr int tr_nterms(int P) {
+// k_translate's schedule (see k_translate).  Outputs (l, m), m = 1..l, are grouped in blocks of WD
+// consecutive m (l, m0 .. m0 + WD - 1); a block's work is, for each j = 2..l, a sweep over k of the terms
+// Q^{(j,k)} S'^{(l-j, m-k)} of all WD outputs at once (k from the smallest to the largest k any output of
+// the block takes).  Along the sweep output m0 + i needs S'^{(l-j, m0+i-k)}, i.e. the entry output m0 took
+// i steps earlier: a window of WD S' entries in registers, one new entry per step.
+__host__ __device__ constexpr int tr_wd(int P) { return P <= 4 ? 4 : (P <= 6 ? 3 : (P <= 8 ? 4 : 5)); }
+__host__ __device__ constexpr int tr_block_len(int l, int m0, int wd) {
   int n = 0;
-  for (int l = 2; l <= P; ++l)
-    for (int m = 1; m <= l; m += 2) {
-      const int m1 = m + 1 <= l ? m + 1 : m;
-      for (int j = 2; j <= l; ++j) {
-        const int lj = l - j;
-        const int kmin = (-j > m - lj) ? -j : m - lj, kmax = (j < m1 + lj) ? j : m1 + lj;
-        n += kmax - kmin + 1;
-      }
-    }
+  const int m1 = (m0 + wd - 1 < l) ? m0 + wd - 1 : l;
+  for (int j = 2; j <= l; ++j) {
+    const int lp = l - j;
+    const int lo = (-j > m0 - lp) ? -j : m0 - lp, hi = (j < m1 + lp) ? j : m1 + lp;
+    n += hi - lo + 1;
+  }
   return n;
 }
-__host__ __device__ constexpr int tr_ntasks(int P) {
+// lanes needed when every block is split into contiguous pieces of at most st steps
+__host__ __device__ constexpr int tr_lanes(int P, int st) {
   int n = 0;
-  for (int l = 2; l <= P; ++l) n += (l + 1) / 2;
+  for (int l = 2; l <= P; ++l)
+    for (int m0 = 1; m0 <= l; m0 += tr_wd(P)) n += (tr_block_len(l, m0, tr_wd(P)) + st - 1) / st;
   return n;
+}
+__host__ __device__ constexpr int tr_steps(int P) {
+  int st = 1;
+  while (tr_lanes(P, st) > 32) ++st;
+  return st;
 }
 
 template <int P>
 struct TrCfg {
   using D = Dims<P>;
-  static constexpr int NT = tr_nterms(P), STEPS = (NT + 31) / 32;
-  static constexpr int MAXSLOT = tr_ntasks(P) + 32, SLOTW = 18;  // slot: 2 outputs x (theta, lambda[4], dlambda[4])
-  static constexpr int SMAX = P <= 4 ? 10 : (P <= 6 ? 8 : (P <= 8 ? 5 : 4));   // max slots of a task (host-checked)
-  static constexpr int ZSLOT = MAXSLOT;                          // an all-zero slot
+  static constexpr int WD = tr_wd(P), STEPS = tr_steps(P);
+  // a lane's flush slot: WD x (theta, lambda[4], dlambda[4]), an odd number of 16-B groups (conflict-free stores)
+  static constexpr int SLW0 = (9 * WD + 1) / 2 * 2, SLW = (SLW0 / 2) % 2 ? SLW0 : SLW0 + 2;
   static constexpr int SXW = 6;                                  // smem (S'.y, S'.x, NG'.y, NG'.x | pad): 48 B
-  static constexpr int SXSZ = SXW * (P * P + 1);                 // + one zero entry for absent outputs / padding
-  static constexpr int QSZ = QRow<P>::SSZ, GSZ = XRow<P>::GSZ;
-  static constexpr int PER_WARP = (2 * QSZ + 2 * SXSZ + GSZ + SLOTW * (MAXSLOT + 1) + 1) / 2 * 2;
-  // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 cinfo [NP], u8 shared-memory
-  // positions of the Q entries [NQ] and of the S' entries [P*P] |
+  static constexpr int SXSZ = SXW * (P * P + 1);                 // + one zero entry (out-of-range S', padding)
+  // staged Q block: NQ entries + a zero entry at stride EQ = 18 doubles (144 B: entries whose positions
+  // differ mod 8 start in different 16-B bank groups), then V at SV + 2 vpos: j = 1 at 0, 1, the entry at
+  // position pos at pos + 2 (the zero entry's V at NQ + 2)
+  static constexpr int EQ = 18, ZQ = D::NQ, SV = EQ * (D::NQ + 1), QSZ = SV + 2 * (D::NQ + 3);
+  // a staging buffer = [Q block | S' block]; after the sweep the current buffer holds the 32 flush slots
+  static constexpr int BUF = QSZ + SXSZ > 32 * SLW ? QSZ + SXSZ : 32 * SLW;
+  static_assert(QSZ % 2 == 0 && BUF % 2 == 0, "translate buffer");
+  static constexpr int GSZ = XRow<P>::GSZ;
+  static constexpr int PER_WARP = (2 * BUF + GSZ + 1) / 2 * 2;
+  // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 prime codes [STEPS][32],
+  // u32 cinfo [NP], u8 shared-memory positions of the Q entries [NQ] and of the S' entries [P*P] |
   // f64 vlam [NQ], vth [NV], wS [P*P], olam [NP], oth [NP]
-  static constexpr int NWORD = STEPS * 32 + D::NP + (D::NQ + P * P + 3) / 4, TABW = (NWORD + 1) / 2;
+  static constexpr int NWORD = 2 * STEPS * 32 + D::NP + (D::NQ + P * P + 3) / 4, TABW = (NWORD + 1) / 2;
+  static constexpr int POSQ_BYTE = 4 * (2 * STEPS * 32 + D::NP), POSS_BYTE = POSQ_BYTE + D::NQ;
   static constexpr int VLAM = TABW, VTH = VLAM + D::NQ, WS = VTH + D::NV, OLAM = WS + P * P, OTH = OLAM + D::NP;
   static constexpr int TAB_D = (OTH + D::NP + 1) / 2 * 2;
   static constexpr int SMEM_MAX = 224 * 1024;
   static constexpr int WPB_FIT = (SMEM_MAX / 8 - TAB_D) / PER_WARP;
   static constexpr int WPB = WPB_FIT > 8 ? 8 : WPB_FIT;
   static constexpr size_t SMEM = (size_t)(TAB_D + WPB * PER_WARP) * sizeof(double);
-  // code: qidx(j,|k|) | se0 << 7 | se1 << 14 | FA | FB | FLUSH | slot << 24
-  static constexpr uint32_t FA = 1u << 21, FB = 1u << 22, FLUSH = 1u << 23;
+  // code: Q position | new S' position << 7 | FA | FB | PRIME;  prime code: S' positions of window
+  // entries 1 .. WD-1, 7 bits each.  cinfo: l | m << 4 | i << 8 | first lane << 12 | lanes << 20.
+  static constexpr uint32_t FA = 1u << 14, FB = 1u << 15, PRIME = 1u << 17;
   static_assert(WPB >= 2, "translate smem");
-  static_assert(MAXSLOT < 256 && D::NQ < 128 && P * P < 128, "translate code fields");
+  static_assert(D::NQ < 127 && P * P < 128 && WD <= 5, "translate code fields");
 };
 
 // D = A B + C for one 8x8x4 fp64 tile (FP64 tensor core, SASS DMMA).  Fragments: a = A[lane/4][lane%4],
@@ -871,23 +885,20 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
 // S' = w S (expanded over m' < 0), so the inner loop is pure FMAs on the Im parts (only Im(lambda),
 // Im(theta) enter W, dW, Theta): Im(A S) = A.x S.y + A.y S.x, with A^{(j,-k)} = (-1)^k conj A^{(j,k)} folded
 // into sign flips of (S.y, S.x).
-// One warp per pair.  The outputs are taken in pairs (l, m0), (l, m0 + 1) (tasks) so that every Q / dQ / V
-// entry loaded from shared memory feeds two outputs (shared-memory bandwidth is this kernel's bound); a
-// task's terms (j, k), j >= 2, span the union of its outputs' k ranges (an output outside its range reads
-// the zero S' entry).  The terms (task-major) are split into 32 contiguous equal runs, one per lane
-// (host-built schedule, make_trtab in rrq_api.cu, ordered within each task to spread shared-memory banks),
-// so every lane executes the same STEPS steps; a task's partial sums are flushed to a slot where the
-// lane's run of it ends, and the epilogue (lanes over c) sums a c's slots, adds the j = 1 theta terms and
-// the gamma parts and writes zeta.  Rows are prefetched with cp.async one pair ahead.
+// One warp per pair; shared memory bandwidth is the bound, so every operand is loaded once per use by
+// as many outputs as possible: a lane works on one block of WD outputs (l, m0 .. m0+WD-1) (TrCfg) and
+// sweeps k for each j, loading per step one Q / dQ / V entry (used by all WD outputs) and ONE new S'
+// entry (the S' window of the WD outputs slides by one entry per step, in registers).  A block's steps
+// are split into contiguous pieces over several lanes so that every lane runs the same STEPS steps
+// (host-built codes, make_trtab in rrq_api.cu); a piece starts by loading the whole window (PRIME), a new
+// j starts from an all-zero window (RESET; PRIME where the sweep is clipped at k = -j).  Each lane
+// writes its WD partial outputs to its slot once, after the sweep; the epilogue (lanes over c) sums the
+// slots of a c's block, adds the j = 1 theta terms and the gamma parts and writes zeta.  Rows are
+// prefetched with cp.async one pair ahead.
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ double flip_if(double x, uint32_t bit) {
   return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)bit << 63));
 }
-
-struct TrOps {
-  double2 s0, g0, s1, g1, v, q[4], dq[4];
-  uint32_t cw;
-};
 
 template <int P>
 __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
@@ -897,25 +908,31 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   using C = TrCfg<P>;
   using XR = XRow<P>;
   using QR = QRow<P>;
-  constexpr int NP = D::NP, NZS = D::NZS, WPB = C::WPB, EQ = QR::EQ, SXW = C::SXW;
+  constexpr int NP = D::NP, NZS = D::NZS, WPB = C::WPB, EQ = C::EQ, SXW = C::SXW, WD = C::WD;
   extern __shared__ __align__(16) double sm[];
   for (int i = threadIdx.x; i < C::TAB_D; i += blockDim.x) sm[i] = trtab[i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double *wb = sm + C::TAB_D + (size_t)warp * C::PER_WARP;
-  double *QB = wb, *SXB = QB + 2 * C::QSZ, *GB = SXB + 2 * C::SXSZ, *SL = GB + C::GSZ;
-  if (lane < 2 * SXW) SXB[(lane / SXW) * C::SXSZ + SXW * P * P + lane % SXW] = 0.0;   // zero entries
-  if (lane < C::SLOTW) SL[C::SLOTW * C::ZSLOT + lane] = 0.0;                          // zero slot
+  double *GB = wb + 2 * C::BUF;   // buffer b: wb + b BUF = [Q block | S' block]
+  auto zero_entries = [&](int b) {  // the zero Q entry (+ its V) and the zero S' entry (never staged)
+    double *qd = wb + b * C::BUF;
+    if (lane < 16) qd[EQ * C::ZQ + lane] = 0.0;
+    else if (lane < 18) qd[C::SV + 2 * (C::ZQ + 2) + lane - 16] = 0.0;
+    else if (lane < 22) qd[C::QSZ + SXW * P * P + lane - 18] = 0.0;
+  };
+  zero_entries(0);
+  zero_entries(1);
   __syncthreads();
   const uint32_t *code = reinterpret_cast<const uint32_t *>(sm);
-  const uint32_t *cinfo = code + C::STEPS * 32;
+  const uint32_t *pcode = code + C::STEPS * 32;
+  const uint32_t *cinfo = pcode + C::STEPS * 32;
   const uint8_t *posq = reinterpret_cast<const uint8_t *>(cinfo + NP), *poss = posq + D::NQ;
   const double *olam = sm + C::OLAM, *oth = sm + C::OTH;
   const int64_t stride = (int64_t)gridDim.x * WPB;
 
   // Q row (entry e -> position posq[e] at stride EQ; V of (j >= 2, k) next to it) and the S'/NG' block
   // (entry e -> position poss[e] at stride SXW): positions chosen by the host to spread the main loop's
-  // shared-memory banks
-  // destinations of this lane's 16-B chunks, fixed for every pair: computed once (registers)
+  // shared-memory banks.  Destinations of this lane's 16-B chunks, fixed for every pair (registers).
   constexpr int NCQ_ = 8 * D::NQ, NLQ = (NCQ_ + 31) / 32, NLV = (D::NV + 31) / 32, NLS = (2 * P * P + 31) / 32;
   int dq[NLQ], dv[NLV], ds[NLS];
 #pragma unroll
@@ -926,16 +943,16 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 #pragma unroll
   for (int u = 0; u < NLV; ++u) {
     const int i = lane + 32 * u;
-    dv[u] = i < D::NV ? QR::SV + 2 * (i < 2 ? i : posq[i - 2] + 2) : 0;
+    dv[u] = i < D::NV ? C::SV + 2 * (i < 2 ? i : posq[i - 2] + 2) : 0;
   }
 #pragma unroll
   for (int u = 0; u < NLS; ++u) {
     const int i = lane + 32 * u;
-    ds[u] = i < 2 * P * P ? SXW * poss[i >> 1] + 2 * (i & 1) : 0;
+    ds[u] = i < 2 * P * P ? C::QSZ + SXW * poss[i >> 1] + 2 * (i & 1) : 0;
   }
   auto issue_qs = [&](int64_t s, int b) {
     const double *qg = Qrow + (s - sA) * QR::STRIDE, *xg = Xrow + (s - sA) * XR::STRIDE + XR::SX;
-    double *qd = QB + b * C::QSZ, *sd = SXB + b * C::SXSZ;
+    double *qd = wb + b * C::BUF;
 #pragma unroll
     for (int u = 0; u < NLQ; ++u)
       if (lane + 32 * u < NCQ_) cp_async16(qd + dq[u], qg + 2 * (lane + 32 * u));
@@ -944,7 +961,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
       if (lane + 32 * u < D::NV) cp_async16(qd + dv[u], qg + QR::V + 2 * (lane + 32 * u));
 #pragma unroll
     for (int u = 0; u < NLS; ++u)
-      if (lane + 32 * u < 2 * P * P) cp_async16(sd + ds[u], xg + 2 * (lane + 32 * u));
+      if (lane + 32 * u < 2 * P * P) cp_async16(qd + ds[u], xg + 2 * (lane + 32 * u));
   };
   auto issue_g = [&](int64_t s) {
     const double *xg = Xrow + (s - sA) * XR::STRIDE + XR::G;
@@ -964,89 +981,109 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
-    const double *qb = QB + cb * C::QSZ, *sx = SXB + cb * C::SXSZ;
-    // main loop: each step one (j, k) term of this lane's task for both of its outputs; software-pipelined
-    auto load = [&](TrOps &o, uint32_t cw) {
-      o.cw = cw;
-      const int qe = cw & 127, e0 = (cw >> 7) & 127, e1 = (cw >> 14) & 127;
-      o.s0 = *reinterpret_cast<const double2 *>(sx + SXW * e0);
-      o.g0 = *reinterpret_cast<const double2 *>(sx + SXW * e0 + 2);
-      o.s1 = *reinterpret_cast<const double2 *>(sx + SXW * e1);
-      o.g1 = *reinterpret_cast<const double2 *>(sx + SXW * e1 + 2);
-      o.v = *reinterpret_cast<const double2 *>(qb + QR::SV + 2 * (qe + 2));   // vidx(j,k) = qidx(j,k) + 2
-      const double *e = qb + EQ * qe;
+    double *qbw = wb + cb * C::BUF;
+    const double *qb = qbw, *sx = qbw + C::QSZ;
+    // main loop: the window w[i] = (S'.y, S'.x, NG'.y, NG'.x) of output m0 + i
+    double th[WD], lam[WD][4], dl[WD][4];
+    double2 ws[WD], wg[WD];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        o.q[b] = *reinterpret_cast<const double2 *>(e + 2 * b);
-        o.dq[b] = *reinterpret_cast<const double2 *>(e + 8 + 2 * b);
-      }
-    };
-    double th[2] = {0, 0}, lam[2][4] = {}, dla[2][4] = {}, dlb[2][4] = {};
-    TrOps cur, nxt;
-    load(cur, code[lane]);
+    for (int i = 0; i < WD; ++i) {
+      th[i] = 0;
+      ws[i] = wg[i] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) lam[i][b] = dl[i][b] = 0;
+    }
 #pragma unroll
     for (int t = 0; t < C::STEPS; ++t) {
-      if (t + 1 < C::STEPS) load(nxt, code[(t + 1) * 32 + lane]);
-      const uint32_t cw = cur.cw, fa = (cw >> 21) & 1, fb = (cw >> 22) & 1;
+      const uint32_t cw = code[t * 32 + lane];
+      const int qe = cw & 127, se = (cw >> 7) & 127;
 #pragma unroll
-      for (int o = 0; o < 2; ++o) {
-        const double2 sv = o ? cur.s1 : cur.s0, gv = o ? cur.g1 : cur.g0;
-        const double A = flip_if(sv.x, fa), B = flip_if(sv.y, fb);
-        const double An = flip_if(gv.x, fa), Bn = flip_if(gv.y, fb);
-        th[o] = fma(cur.v.x, A, fma(cur.v.y, B, th[o]));
+      for (int i = WD - 1; i >= 1; --i) {
+        ws[i] = ws[i - 1];
+        wg[i] = wg[i - 1];
+      }
+      ws[0] = *reinterpret_cast<const double2 *>(sx + SXW * se);
+      wg[0] = *reinterpret_cast<const double2 *>(sx + SXW * se + 2);
+      if (t == 0 || (cw & C::PRIME)) {   // every piece starts with a PRIME (step 0: all lanes together)
+        const uint32_t pw = pcode[t * 32 + lane];
+#pragma unroll
+        for (int i = 1; i < WD; ++i) {
+          const int pe = (pw >> (7 * (i - 1))) & 127;
+          ws[i] = *reinterpret_cast<const double2 *>(sx + SXW * pe);
+          wg[i] = *reinterpret_cast<const double2 *>(sx + SXW * pe + 2);
+        }
+      }
+      const double *e = qb + EQ * qe;
+      double2 q[4], dq[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        q[b] = *reinterpret_cast<const double2 *>(e + 2 * b);
+        dq[b] = *reinterpret_cast<const double2 *>(e + 8 + 2 * b);
+      }
+      const double2 v = *reinterpret_cast<const double2 *>(qb + C::SV + 2 * (qe + 2));
+      const uint32_t fa = (cw >> 14) & 1, fb = (cw >> 15) & 1;
+#pragma unroll
+      for (int i = 0; i < WD; ++i) {
+        const double A = flip_if(ws[i].x, fa), B = flip_if(ws[i].y, fb);
+        const double An = flip_if(wg[i].x, fa), Bn = flip_if(wg[i].y, fb);
+        th[i] = fma(v.x, A, fma(v.y, B, th[i]));
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
-          lam[o][b] = fma(cur.q[b].x, A, fma(cur.q[b].y, B, lam[o][b]));
-          dla[o][b] = fma(cur.dq[b].x, A, fma(cur.dq[b].y, B, dla[o][b]));
-          dlb[o][b] = fma(cur.q[b].x, An, fma(cur.q[b].y, Bn, dlb[o][b]));
+          lam[i][b] = fma(q[b].x, A, fma(q[b].y, B, lam[i][b]));
+          dl[i][b] = fma(dq[b].x, A, fma(dq[b].y, B, fma(q[b].x, An, fma(q[b].y, Bn, dl[i][b]))));
         }
       }
-      if (cw & C::FLUSH) {   // slot = [th0 lam0[4] dl0[4] | th1 lam1[4] dl1[4]], 16-B stores
-        double2 *d = reinterpret_cast<double2 *>(SL + C::SLOTW * (cw >> 24));
-        d[0] = make_double2(th[0], lam[0][0]);
-        d[1] = make_double2(lam[0][1], lam[0][2]);
-        d[2] = make_double2(lam[0][3], dla[0][0] + dlb[0][0]);
-        d[3] = make_double2(dla[0][1] + dlb[0][1], dla[0][2] + dlb[0][2]);
-        d[4] = make_double2(dla[0][3] + dlb[0][3], th[1]);
-        d[5] = make_double2(lam[1][0], lam[1][1]);
-        d[6] = make_double2(lam[1][2], lam[1][3]);
-        d[7] = make_double2(dla[1][0] + dlb[1][0], dla[1][1] + dlb[1][1]);
-        d[8] = make_double2(dla[1][2] + dlb[1][2], dla[1][3] + dlb[1][3]);
+    }
+    // j = 1 theta terms of this lane's outputs c = lane, lane + 32 (no lambda part: C_1 = 0; |m - k| > l - 1
+    // reads the zero S' entry), taken before the slots overwrite the buffer
+    double T1[2] = {0, 0};
 #pragma unroll
-        for (int o = 0; o < 2; ++o) {
-          th[o] = 0;
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c >= NP) continue;
+      const uint32_t ci = cinfo[c];
+      const int l = ci & 15, m = (ci >> 4) & 15;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) lam[o][b] = dla[o][b] = dlb[o][b] = 0;
+      for (int k = -1; k <= 1; ++k) {
+        const int lp = l - 1, mp = m - k;
+        const int se = (mp >= -lp && mp <= lp) ? poss[lp * lp + lp + mp] : P * P;
+        const double *vv = qb + C::SV + 2 * vidx(1, k < 0 ? -k : k);
+        const double A = k < 0 ? -sx[SXW * se] : sx[SXW * se], B = sx[SXW * se + 1];
+        T1[h] = fma(vv[0], A, fma(vv[1], B, T1[h]));
+      }
+    }
+    __syncwarp();
+    {   // this lane's slot (in the current buffer): WD x (theta, lambda[4], dlambda[4])
+      double *d = qbw + C::SLW * lane;
+#pragma unroll
+      for (int i = 0; i < WD; ++i) {
+        d[9 * i] = th[i];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          d[9 * i + 1 + b] = lam[i][b];
+          d[9 * i + 5 + b] = dl[i][b];
         }
       }
-      if (t + 1 < C::STEPS) cur = nxt;
     }
     __syncwarp();
     // epilogue: lanes over c = (l, m); gamma parts from GB (W [4][NP], dW [4][NP], Theta [NP], nu')
     const double nup[3] = {GB[9 * NP], GB[9 * NP + 1], GB[9 * NP + 2]};
     double *Z = Zrow + (s - sA) * NZS;
-    for (int c = lane; c < NP; c += 32) {
-      const uint32_t ci = cinfo[c];
-      const int l = ci & 15, m = (ci >> 4) & 15, sb = (ci >> 8) & 255, sc = (ci >> 16) & 255, hf = (ci >> 24) & 1;
-      double T = 0, L[4] = {0, 0, 0, 0}, DL[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int q = 0; q < C::SMAX; ++q) {   // uniform trip count (absent slots read the zero slot)
-        const double *d = SL + C::SLOTW * (q < sc ? sb + q : C::ZSLOT) + 9 * hf;
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c >= NP) continue;
+      const uint32_t ci = cinfo[c];
+      const int ib = (ci >> 8) & 15, fl = (ci >> 12) & 255, nl = (ci >> 20) & 63;
+      double T = T1[h], L[4] = {0, 0, 0, 0}, DL[4] = {0, 0, 0, 0};
+      for (int q = 0; q < nl; ++q) {
+        const double *d = qbw + C::SLW * (fl + q) + 9 * ib;
         T += d[0];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           L[b] += d[1 + b];
           DL[b] += d[5 + b];
         }
-      }
-      // j = 1 theta terms (no lambda part: C_1 = 0); |m - k| > l - 1 reads the zero S' entry
-#pragma unroll
-      for (int k = -1; k <= 1; ++k) {
-        const int lp = l - 1, mp = m - k;
-        const int se = (mp >= -lp && mp <= lp) ? poss[lp * lp + lp + mp] : P * P;
-        const double *vv = qb + QR::SV + 2 * vidx(1, k < 0 ? -k : k);
-        const double A = k < 0 ? -sx[SXW * se] : sx[SXW * se], B = sx[SXW * se + 1];
-        T = fma(vv[0], A, fma(vv[1], B, T));
       }
       const double fo = -s2 * inv4pi * olam[c];
       double W[4], dW[4];
@@ -1073,6 +1110,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     }
     for (int i = D::NZ + lane; i < NZS; i += 32) Z[i] = 0.0;
     __syncwarp();
+    zero_entries(cb);   // the slots overwrote them
     if (s + stride < sB) issue_g(s + stride);
     cp_async_commit();
   }

@@ -129,174 +129,138 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 
 // Exported functions get C linkage from their declarations in include/rrq.h.
 
-// k_translate's host-built table (TrCfg<P>): tasks = output pairs (l, m0), (l, m0 + 1) (a single (l, l)
-// when l is odd), task-major, each task's j >= 2 terms over the union of its outputs' k ranges; the term
-// list is split into 32 contiguous runs of equal length (one per lane).  A term is encoded as
-// qidx(j,|k|) | se0 << 7 | se1 << 14 | sign flips of (S.y, S.x) for k < 0 | flush | slot << 24, se = l'^2 + l' + m'
-// of the S' entry of each output (p^2 = the zero entry when the output does not take the term; padding
-// terms are all-zero-entry).  cinfo[c] = l | m << 4 | first slot << 8 | slot count << 16 | half << 24.
+// k_translate's host-built table (TrCfg<P>).  Blocks of WD outputs (l, m0 .. m0 + WD - 1), l-major; a block's
+// steps are its j = 2..l sweeps over k (from the smallest to the largest k any output of the block takes),
+// each step = the Q entry (j, |k|) (sign flips of (S.y, S.x) for k < 0: FA for odd k, FB for even k) and the
+// new window entry S'^{(l-j, m0-k)} (the zero entry ZE outside |m'| <= l').  A block is split into
+// ceil(len / STEPS) contiguous pieces of near-equal length, one lane each (lanes in block order); a piece's
+// first step and every sweep's first step carry PRIME: window entries 1 .. WD-1 (S'^{(l-j, m0+i-k)}, mostly
+// the zero entry) are loaded.  Padding steps read the zero Q entry ZQ.  cinfo[c] = l | m << 4 | i << 8 |
+// first lane << 12 | lanes << 20 (i = m - m0).
 // Scale factors: v_lambda(j,k) = (j-2)!/F(j,k), v_theta(j,k) = (j-1)!/F(j,k), w(l',m') = l'!/F(l',m'),
 // u_lambda(l,m) = F(l,m)/(l-1)!, u_theta(l,m) = F(l,m)/l!, F(a,b) = sqrt((a+b)! (a-b)!).
-// Within a run the order of terms is free; it is chosen greedily so that, at each step, the 8 lanes of a
-// quarter-warp read Q entries (16-B bank group qidx mod 8) and S' entries (3 se mod 8) in distinct groups.
+// The shared-memory positions of the Q entries (pq) and of the S' entries (ps) are chosen by annealing so
+// that at each step the 8 lanes of a quarter-warp read entries in distinct 16-B bank groups.
 template <int P>
 static std::vector<double> make_trtab() {
   using C = TrCfg<P>;
   using D = Dims<P>;
-  constexpr int ZE = P * P;
-  struct Term { int task, qe, se0, se1, k; };
-  struct Task { int l, m0, m1; };
-  std::vector<Term> terms;
-  std::vector<Task> tasks;
+  constexpr int ZE = P * P, WD = C::WD, ST = C::STEPS, ZQ = C::ZQ;
+  struct Step { int qe, se, k, flags, pe[4]; };
   auto sidx2 = [](int lp, int mp) { return (mp < -lp || mp > lp) ? ZE : lp * lp + lp + mp; };
+  struct Blk { int l, m0; std::vector<Step> st; };
+  std::vector<Blk> blks;
   for (int l = 2; l <= P; ++l)
-    for (int m = 1; m <= l; m += 2) {
-      const int m1 = m + 1 <= l ? m + 1 : -1, tk = (int)tasks.size();
-      tasks.push_back({l, m, m1});
+    for (int m0 = 1; m0 <= l; m0 += WD) {
+      Blk B{l, m0, {}};
+      const int m1 = std::min(m0 + WD - 1, l);
       for (int j = 2; j <= l; ++j) {
-        const int lj = l - j, mh = m1 > 0 ? m1 : m;
-        for (int k = std::max(-j, m - lj); k <= std::min(j, mh + lj); ++k)
-          terms.push_back({tk, qidx(j, std::abs(k)), sidx2(lj, m - k), m1 > 0 ? sidx2(lj, m1 - k) : ZE, k});
+        const int lp = l - j, lo = std::max(-j, m0 - lp), hi = std::min(j, m1 + lp);
+        for (int k = lo; k <= hi; ++k) {
+          Step t{qidx(j, std::abs(k)), sidx2(lp, m0 - k), k, 0, {ZE, ZE, ZE, ZE}};
+          for (int i = 1; i < WD; ++i) t.pe[i - 1] = (m0 + i <= l) ? sidx2(lp, m0 + i - k) : ZE;
+          if (k < 0) t.flags |= (std::abs(k) & 1) ? C::FA : C::FB;
+          if (k == lo && j > 2) t.flags |= C::PRIME;   // a new sweep: window entries 1 .. WD-1 reloaded
+          B.st.push_back(t);
+        }
+      }
+      if ((int)B.st.size() != tr_block_len(l, m0, WD)) { std::fprintf(stderr, "rrq: translate block length\n"); std::abort(); }
+      blks.push_back(B);
+    }
+  // lanes: pieces of each block; per lane the list of steps (padded to ST)
+  std::vector<std::vector<Step>> lanes(32);
+  std::vector<int> bfirst(blks.size()), bcnt(blks.size());
+  int L = 0;
+  for (size_t b = 0; b < blks.size(); ++b) {
+    const int len = (int)blks[b].st.size(), n = (len + ST - 1) / ST;
+    bfirst[b] = L;
+    bcnt[b] = n;
+    for (int q = 0; q < n; ++q, ++L) {
+      if (L >= 32) { std::fprintf(stderr, "rrq: translate schedule needs more than 32 lanes\n"); std::abort(); }
+      const int f = (int)((int64_t)q * len / n), e = (int)((int64_t)(q + 1) * len / n);
+      for (int i = f; i < e; ++i) {
+        Step t = blks[b].st[i];
+        if (i == f) t.flags = (t.flags & (C::FA | C::FB)) | C::PRIME;
+        lanes[L].push_back(t);
       }
     }
-  const int NT = (int)terms.size();
-  std::vector<int> beg(33);
-  for (int L = 0; L <= 32; ++L) beg[L] = L * (NT / 32) + std::min(L, NT % 32);
-  // runs (lane, task) -> slots numbered in (task, lane) order so a task's slots are contiguous
-  struct Run { int task, lane, first, last; };
-  std::vector<Run> runs;
-  for (int L = 0; L < 32; ++L) {
-    int f = beg[L];
-    for (int i = beg[L]; i < beg[L + 1]; ++i)
-      if (i + 1 == beg[L + 1] || terms[i + 1].task != terms[i].task) {
-        runs.push_back({terms[i].task, L, f, i});
-        f = i + 1;
-      }
   }
-  std::stable_sort(runs.begin(), runs.end(), [](const Run &a, const Run &b) { return a.task < b.task; });
-  const int NTK = (int)tasks.size();
-  std::vector<int> slot_of(NT, -1), run_of(NT, -1), sbeg(NTK, 0), scnt(NTK, 0);
-  for (int r = 0; r < (int)runs.size(); ++r) {
-    slot_of[runs[r].last] = r;
-    for (int i = runs[r].first; i <= runs[r].last; ++i) run_of[i] = r;
-    if (scnt[runs[r].task]++ == 0) sbeg[runs[r].task] = r;
+  for (int l2 = 0; l2 < 32; ++l2) {
+    if ((int)lanes[l2].size() > ST) { std::fprintf(stderr, "rrq: translate piece too long\n"); std::abort(); }
+    while ((int)lanes[l2].size() < ST) lanes[l2].push_back(Step{ZQ, ZE, 0, lanes[l2].empty() ? (int)C::PRIME : 0, {ZE, ZE, ZE, ZE}});
   }
-  for (int tk = 0; tk < NTK; ++tk)
-    if (scnt[tk] > C::SMAX) {
-      std::fprintf(stderr, "rrq: translate schedule needs %d slots per task > SMAX %d\n", scnt[tk], C::SMAX);
-      std::abort();
-    }
-  // Shared-memory wavefronts of one step (quarter-warp model: 8 lanes per wavefront of 16-B accesses,
-  // verified by tools/lds_banks.cu).  Q / dQ / V loads hit 16-B group (pq[qe] + c) mod 8, S' loads
-  // (3 ps[se] + c) mod 8; a quarter costs the largest number of DISTINCT entries sharing one group.
-  // The schedule (order of terms within runs) and the shared-memory positions pq (Q entries) and ps
-  // (S' entries) are chosen together: greedy ordering, then annealing on the positions, alternated.
-  std::vector<int> pq(D::NQ), ps(ZE + 1);
-  for (int e = 0; e < D::NQ; ++e) pq[e] = e;
+  // Bank model (quarter-warp: 8 lanes per wavefront of 16-B accesses, tools/lds_banks.cu): a Q entry at
+  // position x starts in 16-B group x mod 8 (stride 144 B) and its 8 chunks and V follow; an S' entry at
+  // position y starts in group 3y mod 8 (stride 48 B).  Cost of a quarter = 9 x (max distinct Q entries in
+  // one group) + 2 x (same for the new S' entries) (+ the PRIME loads, which all lanes issue at step 0).
+  std::vector<int> pq(D::NQ + 1), ps(ZE + 1);
+  for (int e = 0; e <= D::NQ; ++e) pq[e] = e;
   for (int e = 0; e <= ZE; ++e) ps[e] = e;
-  auto mult = [](const int *ent, const int *grp, int n) {   // max over groups of the distinct entries in it
+  auto mult = [](const int *ent, const int *grp, int n) {
     uint64_t m[8][2] = {};
     for (int i = 0; i < n; ++i) m[grp[i]][ent[i] >> 6] |= 1ull << (ent[i] & 63);
     int best = 1;
     for (int g = 0; g < 8; ++g) best = std::max(best, __builtin_popcountll(m[g][0]) + __builtin_popcountll(m[g][1]));
     return best;
   };
-  std::vector<int> order(NT);
-  auto greedy = [&]() {
-    std::vector<char> used(NT, 0);
-    for (int t = 0; t < C::STEPS; ++t)
-      for (int q = 0; q < 4; ++q) {
-        std::vector<int> qg, sg;   // entries chosen so far in this quarter at step t
-        for (int L = 8 * q; L < 8 * q + 8; ++L) {
-          const int pos = beg[L] + t;
-          if (pos >= beg[L + 1]) continue;
-          const Run &r = runs[run_of[pos]];
-          int best = -1, bc = 1 << 30;
-          for (int i = r.first; i <= r.last; ++i) {
-            if (used[i]) continue;
-            int cost = 0;
-            for (int a : qg)
-              if (a != terms[i].qe && ((pq[a] - pq[terms[i].qe]) & 7) == 0) cost += 9;
-            for (int a : sg) {
-              if (a != terms[i].se0 && ((ps[a] - ps[terms[i].se0]) & 7) == 0) cost += 2;
-              if (a != terms[i].se1 && ((ps[a] - ps[terms[i].se1]) & 7) == 0) cost += 2;
-            }
-            if (cost < bc) { bc = cost; best = i; }
-          }
-          used[best] = 1;
-          order[pos] = best;
-          qg.push_back(terms[best].qe);
-          sg.push_back(terms[best].se0);
-          sg.push_back(terms[best].se1);
-        }
-      }
-  };
   auto cost = [&]() {
     int tot = 0;
-    for (int t = 0; t < C::STEPS; ++t)
+    for (int t = 0; t < ST; ++t)
       for (int q = 0; q < 4; ++q) {
-        int eq[8], gq[8], e0[8], g0[8], e1[8], g1[8], n = 0;
-        for (int L = 8 * q; L < 8 * q + 8; ++L) {
-          const int pos = beg[L] + t;
-          if (pos >= beg[L + 1]) continue;
-          const Term &tm = terms[order[pos]];
-          eq[n] = tm.qe; gq[n] = pq[tm.qe] & 7;
-          e0[n] = tm.se0; g0[n] = (3 * ps[tm.se0]) & 7;
-          e1[n] = tm.se1; g1[n] = (3 * ps[tm.se1]) & 7;
-          ++n;
+        int eq[8], gq[8], es[8], gs[8];
+        for (int i = 0; i < 8; ++i) {
+          const Step &s = lanes[8 * q + i][t];
+          eq[i] = s.qe; gq[i] = pq[s.qe] & 7;
+          es[i] = s.se; gs[i] = (3 * ps[s.se]) & 7;
         }
-        tot += 9 * mult(eq, gq, n) + 2 * mult(e0, g0, n) + 2 * mult(e1, g1, n);
+        tot += 9 * mult(eq, gq, 8) + 2 * mult(es, gs, 8);
+        if (t == 0)
+          for (int w = 0; w < WD - 1; ++w) {
+            for (int i = 0; i < 8; ++i) { es[i] = lanes[8 * q + i][0].pe[w]; gs[i] = (3 * ps[es[i]]) & 7; }
+            tot += 2 * mult(es, gs, 8);
+          }
       }
     return tot;
   };
-  greedy();
-  int cur = cost();
-  std::vector<int> best_order = order, best_pq = pq, best_ps = ps;
-  int best = cur;
+  int cur = cost(), best = cur;
+  std::vector<int> best_pq = pq, best_ps = ps;
   uint64_t rng = 0x9E3779B97F4A7C15ull;
   auto rnd = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
   double T = 3.0;
-  for (int round = 0; round < 8; ++round) {
-    for (int it = 0; it < 3000; ++it) {
-      const bool onq = (rnd() & 1) != 0;
-      std::vector<int> &v = onq ? pq : ps;
-      const int n = onq ? D::NQ : ZE;   // ps[ZE] (the zero entry) stays last
-      const int a = (int)(rnd() % n), b2 = (int)(rnd() % n);
-      if (a == b2) continue;
-      std::swap(v[a], v[b2]);
-      const int c = cost();
-      const double u = (double)(rnd() >> 11) * (1.0 / 9007199254740992.0);
-      if (c <= cur || u < std::exp((cur - c) / T)) cur = c;
-      else std::swap(v[a], v[b2]);
-      T = std::max(0.05, T * 0.9996);
-    }
-    greedy();
-    cur = cost();
-    if (cur < best) { best = cur; best_order = order; best_pq = pq; best_ps = ps; }
+  for (int it = 0; it < 24000; ++it) {
+    const bool onq = (rnd() & 1) != 0;
+    std::vector<int> &v = onq ? pq : ps;
+    const int n = onq ? D::NQ : ZE;   // the zero entries keep the last positions
+    const int a = (int)(rnd() % n), b2 = (int)(rnd() % n);
+    if (a == b2) continue;
+    std::swap(v[a], v[b2]);
+    const int c = cost();
+    const double u = (double)(rnd() >> 11) * (1.0 / 9007199254740992.0);
+    if (c <= cur || u < std::exp((cur - c) / T)) cur = c;
+    else std::swap(v[a], v[b2]);
+    if (cur < best) { best = cur; best_pq = pq; best_ps = ps; }
+    T = std::max(0.05, T * 0.9997);
   }
-  order = best_order; pq = best_pq; ps = best_ps;
+  pq = best_pq; ps = best_ps;
   std::vector<uint32_t> w(C::NWORD, 0u);
-  for (int i = 0; i < C::STEPS * 32; ++i) w[i] = (uint32_t)ZE << 7 | (uint32_t)ZE << 14;   // padding terms
-  for (int L = 0; L < 32; ++L)
-    for (int pos = beg[L]; pos < beg[L + 1]; ++pos) {
-      const Term &t = terms[order[pos]];
-      const int ak = std::abs(t.k);
-      uint32_t cw = (uint32_t)pq[t.qe] | (uint32_t)ps[t.se0] << 7 | (uint32_t)ps[t.se1] << 14;
-      if (t.k < 0) cw |= (ak & 1) ? C::FA : C::FB;
-      if (slot_of[pos] >= 0) cw |= C::FLUSH | (uint32_t)slot_of[pos] << 24;
-      w[(pos - beg[L]) * 32 + L] = cw;
+  for (int l2 = 0; l2 < 32; ++l2)
+    for (int t = 0; t < ST; ++t) {
+      const Step &s = lanes[l2][t];
+      w[t * 32 + l2] = (uint32_t)pq[s.qe] | (uint32_t)ps[s.se] << 7 | (uint32_t)s.flags;
+      uint32_t pw = 0;
+      for (int i = 0; i < WD - 1; ++i) pw |= (uint32_t)ps[s.pe[i]] << (7 * i);
+      w[ST * 32 + t * 32 + l2] = pw;
     }
-  for (int tk = 0; tk < NTK; ++tk)
-    for (int hf = 0; hf < 2; ++hf) {
-      const int m = hf ? tasks[tk].m1 : tasks[tk].m0;
-      if (m < 0) continue;
-      const int l = tasks[tk].l;
-      w[C::STEPS * 32 + lmidx(l, m)] = (uint32_t)l | (uint32_t)m << 4 | (uint32_t)sbeg[tk] << 8 |
-                                       (uint32_t)scnt[tk] << 16 | (uint32_t)hf << 24;
+  uint32_t *ci = w.data() + 2 * ST * 32;
+  for (size_t b = 0; b < blks.size(); ++b)
+    for (int i = 0; i < WD && blks[b].m0 + i <= blks[b].l; ++i) {
+      const int l = blks[b].l, m = blks[b].m0 + i;
+      ci[lmidx(l, m)] = (uint32_t)l | (uint32_t)m << 4 | (uint32_t)i << 8 | (uint32_t)bfirst[b] << 12 |
+                        (uint32_t)bcnt[b] << 20;
     }
-  w[C::STEPS * 32 + lmidx(1, 1)] = 1u | 1u << 4;   // (1,1): j = 1 terms only (no slots)
-  {   // shared-memory positions of the Q entries and S' entries (bytes)
-    uint8_t *pb = reinterpret_cast<uint8_t *>(w.data() + C::STEPS * 32 + D::NP);
+  ci[lmidx(1, 1)] = 1u | 1u << 4;   // (1,1): j = 1 terms only (no slots)
+  {   // shared-memory positions of the Q entries and S' entries
+    uint8_t *pb = reinterpret_cast<uint8_t *>(ci + D::NP);
     for (int e = 0; e < D::NQ; ++e) pb[e] = (uint8_t)pq[e];
     for (int e = 0; e < ZE; ++e) pb[D::NQ + e] = (uint8_t)ps[e];
   }
