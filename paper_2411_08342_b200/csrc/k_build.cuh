@@ -133,8 +133,9 @@ template <int P>
 struct TrCfg {
   using D = Dims<P>;
   static constexpr int WD = tr_wd(P), STEPS = tr_steps(P);
-  // a lane's flush slot: WD x (theta, lambda[4], dlambda[4]), an odd number of 16-B groups (conflict-free stores)
-  static constexpr int SLW0 = (9 * WD + 1) / 2 * 2, SLW = (SLW0 / 2) % 2 ? SLW0 : SLW0 + 2;
+  // a lane's flush slot: WD x (theta, lambda[4], dlambda[4], pad) (16-B aligned per output), an odd number
+  // of 16-B groups per slot (conflict-free stores)
+  static constexpr int SLW = 10 * WD + (WD % 2 ? 0 : 2);
   static constexpr int SXW = 6;                                  // smem (S'.y, S'.x, NG'.y, NG'.x | pad): 48 B
   static constexpr int SXSZ = SXW * (P * P + 1);                 // + one zero entry (out-of-range S', padding)
   // staged Q block: NQ entries + a zero entry at stride EQ = 18 doubles (144 B: entries whose positions
@@ -884,7 +885,7 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
 // and the factorial ratios of C_j, D_j split the same way).  k_qmap stores A = v A and k_pair_edge stores
 // S' = w S (expanded over m' < 0), so the inner loop is pure FMAs on the Im parts (only Im(lambda),
 // Im(theta) enter W, dW, Theta): Im(A S) = A.x S.y + A.y S.x, with A^{(j,-k)} = (-1)^k conj A^{(j,k)} folded
-// into sign flips of (S.y, S.x).
+// into sign flips of (A.x, A.y).
 // One warp per pair; shared memory bandwidth is the bound, so every operand is loaded once per use by
 // as many outputs as possible: a lane works on one block of WD outputs (l, m0 .. m0+WD-1) (TrCfg) and
 // sweeps k for each j, loading per step one Q / dQ / V entry (used by all WD outputs) and ONE new S'
@@ -983,7 +984,9 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     __syncwarp();
     double *qbw = wb + cb * C::BUF;
     const double *qb = qbw, *sx = qbw + C::QSZ;
-    // main loop: the window w[i] = (S'.y, S'.x, NG'.y, NG'.x) of output m0 + i
+    // main loop: a ring of WD S' entries (S'.y, S'.x, NG'.y, NG'.x); the entry loaded at step t sits in
+    // ring slot t mod WD, and output m0 + i at step t uses the one loaded at step t - i (static indices in
+    // the unrolled loop: no register moves)
     double th[WD], lam[WD][4], dl[WD][4];
     double2 ws[WD], wg[WD];
 #pragma unroll
@@ -997,20 +1000,15 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     for (int t = 0; t < C::STEPS; ++t) {
       const uint32_t cw = code[t * 32 + lane];
       const int qe = cw & 127, se = (cw >> 7) & 127;
-#pragma unroll
-      for (int i = WD - 1; i >= 1; --i) {
-        ws[i] = ws[i - 1];
-        wg[i] = wg[i - 1];
-      }
-      ws[0] = *reinterpret_cast<const double2 *>(sx + SXW * se);
-      wg[0] = *reinterpret_cast<const double2 *>(sx + SXW * se + 2);
-      if (t == 0 || (cw & C::PRIME)) {   // every piece starts with a PRIME (step 0: all lanes together)
+      ws[t % WD] = *reinterpret_cast<const double2 *>(sx + SXW * se);
+      wg[t % WD] = *reinterpret_cast<const double2 *>(sx + SXW * se + 2);
+      if (t == 0 || (cw & C::PRIME)) {   // every piece and every sweep starts with a PRIME
         const uint32_t pw = pcode[t * 32 + lane];
 #pragma unroll
         for (int i = 1; i < WD; ++i) {
           const int pe = (pw >> (7 * (i - 1))) & 127;
-          ws[i] = *reinterpret_cast<const double2 *>(sx + SXW * pe);
-          wg[i] = *reinterpret_cast<const double2 *>(sx + SXW * pe + 2);
+          ws[(t - i + WD * C::STEPS) % WD] = *reinterpret_cast<const double2 *>(sx + SXW * pe);
+          wg[(t - i + WD * C::STEPS) % WD] = *reinterpret_cast<const double2 *>(sx + SXW * pe + 2);
         }
       }
       const double *e = qb + EQ * qe;
@@ -1020,12 +1018,23 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
         q[b] = *reinterpret_cast<const double2 *>(e + 2 * b);
         dq[b] = *reinterpret_cast<const double2 *>(e + 8 + 2 * b);
       }
-      const double2 v = *reinterpret_cast<const double2 *>(qb + C::SV + 2 * (qe + 2));
+      double2 v = *reinterpret_cast<const double2 *>(qb + C::SV + 2 * (qe + 2));
+      // k < 0: A^{(j,-k)} = (-1)^k conj A^{(j,k)}, so Im(A S) = A.x S.y + A.y S.x takes -A.x (odd k, FA) or
+      // -A.y (even k, FB): flipped in place on this step's Q operands (used by all WD outputs)
       const uint32_t fa = (cw >> 14) & 1, fb = (cw >> 15) & 1;
+      v.x = flip_if(v.x, fa);
+      v.y = flip_if(v.y, fb);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        q[b].x = flip_if(q[b].x, fa);
+        q[b].y = flip_if(q[b].y, fb);
+        dq[b].x = flip_if(dq[b].x, fa);
+        dq[b].y = flip_if(dq[b].y, fb);
+      }
 #pragma unroll
       for (int i = 0; i < WD; ++i) {
-        const double A = flip_if(ws[i].x, fa), B = flip_if(ws[i].y, fb);
-        const double An = flip_if(wg[i].x, fa), Bn = flip_if(wg[i].y, fb);
+        const int r = (t - i + WD * C::STEPS) % WD;
+        const double A = ws[r].x, B = ws[r].y, An = wg[r].x, Bn = wg[r].y;
         th[i] = fma(v.x, A, fma(v.y, B, th[i]));
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
@@ -1053,16 +1062,15 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
       }
     }
     __syncwarp();
-    {   // this lane's slot (in the current buffer): WD x (theta, lambda[4], dlambda[4])
-      double *d = qbw + C::SLW * lane;
+    {   // this lane's slot (in the current buffer): WD x (theta, lambda[4], dlambda[4], pad)
+      double2 *d = reinterpret_cast<double2 *>(qbw + C::SLW * lane);
 #pragma unroll
       for (int i = 0; i < WD; ++i) {
-        d[9 * i] = th[i];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          d[9 * i + 1 + b] = lam[i][b];
-          d[9 * i + 5 + b] = dl[i][b];
-        }
+        d[5 * i] = make_double2(th[i], lam[i][0]);
+        d[5 * i + 1] = make_double2(lam[i][1], lam[i][2]);
+        d[5 * i + 2] = make_double2(lam[i][3], dl[i][0]);
+        d[5 * i + 3] = make_double2(dl[i][1], dl[i][2]);
+        d[5 * i + 4] = make_double2(dl[i][3], 0.0);
       }
     }
     __syncwarp();
@@ -1077,13 +1085,11 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
       const int ib = (ci >> 8) & 15, fl = (ci >> 12) & 255, nl = (ci >> 20) & 63;
       double T = T1[h], L[4] = {0, 0, 0, 0}, DL[4] = {0, 0, 0, 0};
       for (int q = 0; q < nl; ++q) {
-        const double *d = qbw + C::SLW * (fl + q) + 9 * ib;
-        T += d[0];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          L[b] += d[1 + b];
-          DL[b] += d[5 + b];
-        }
+        const double2 *d = reinterpret_cast<const double2 *>(qbw + C::SLW * (fl + q) + 10 * ib);
+        const double2 d0 = d[0], d1 = d[1], d2 = d[2], d3 = d[3], d4 = d[4];
+        T += d0.x;
+        L[0] += d0.y; L[1] += d1.x; L[2] += d1.y; L[3] += d2.x;
+        DL[0] += d2.y; DL[1] += d3.x; DL[2] += d3.y; DL[3] += d4.x;
       }
       const double fo = -s2 * inv4pi * olam[c];
       double W[4], dW[4];

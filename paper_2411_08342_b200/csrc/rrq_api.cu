@@ -131,7 +131,7 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 
 // k_translate's host-built table (TrCfg<P>).  Blocks of WD outputs (l, m0 .. m0 + WD - 1), l-major; a block's
 // steps are its j = 2..l sweeps over k (from the smallest to the largest k any output of the block takes),
-// each step = the Q entry (j, |k|) (sign flips of (S.y, S.x) for k < 0: FA for odd k, FB for even k) and the
+// each step = the Q entry (j, |k|) (k < 0: the sign of Q.x flipped for odd k (FA), of Q.y for even k (FB)) and the
 // new window entry S'^{(l-j, m0-k)} (the zero entry ZE outside |m'| <= l').  A block is split into
 // ceil(len / STEPS) contiguous pieces of near-equal length, one lane each (lanes in block order); a piece's
 // first step and every sweep's first step carry PRIME: window entries 1 .. WD-1 (S'^{(l-j, m0+i-k)}, mostly
