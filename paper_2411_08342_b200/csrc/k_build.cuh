@@ -682,26 +682,37 @@ struct QmapCfg {
   static constexpr int KA = (D::K % 16 == 4) ? D::K : D::K + ((4 - D::K % 16) + 16) % 16;
   static constexpr int TQC = D::CQP / 8;                      // tiles per quaternion component
   static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8, NTV = NTALL - NTQ;
-  static constexpr int UQ = (TQC + NSPLIT - 1) / NSPLIT;       // a warp's tiles per component
-  static constexpr int UV = (NTV + NSPLIT - 1) / NSPLIT;       // a warp's V tiles
+  static constexpr int UQ = (TQC + NSPLIT - 1) / NSPLIT;       // a warp's tiles per component (at most)
+  // Work balance.  Column split ns takes the Q tiles tl = ns + NSPLIT u < TQC (2 DMMA each: a and b rows)
+  // and a contiguous range of V tiles (1 DMMA each), sized so that the two SM sub-partitions' loads match:
+  // warp w = ns PG + pg runs on sub-partition w % 4, so splits {0, 2} share one pair of sub-partitions and
+  // {1, 3} the other.  Counts are compile-time per split (no predicated-off DMMA).
+  __host__ __device__ static constexpr int nq(int ns) { return (TQC - ns + NSPLIT - 1) / NSPLIT; }
+  static constexpr int VA0 = (NTV + 6 * (nq(1) + nq(3)) - 6 * (nq(0) + nq(2)) + 1) / 2;
+  static constexpr int VA = VA0 < 0 ? 0 : (VA0 > NTV ? NTV : VA0), VB = NTV - VA;
+  __host__ __device__ static constexpr int vcount(int ns) { return ns == 0 ? (VA + 1) / 2 : ns == 2 ? VA / 2 : ns == 1 ? (VB + 1) / 2 : VB / 2; }
+  __host__ __device__ static constexpr int vstart(int ns) { return ns == 0 ? 0 : ns == 1 ? vcount(0) : ns == 2 ? vcount(0) + vcount(1) : vcount(0) + vcount(1) + vcount(2); }
+  static constexpr int UV = vcount(0) > vcount(1) ? (vcount(0) > vcount(2) ? (vcount(0) > vcount(3) ? vcount(0) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)))
+                                                  : (vcount(1) > vcount(2) ? (vcount(1) > vcount(3) ? vcount(1) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)));
   static constexpr int KC = (D::E % 8 == 0) ? 8 : 12, NCH = D::K / KC, CPA = D::E / KC;   // chunks per axis
   static constexpr int NST = 2;                                    // pipeline stages (chunks in flight)
   static_assert(D::E % KC == 0, "a B chunk must lie within one axis block");
+  static_assert(NSPLIT == 4 && PG == 2, "sub-partition balance assumes 4 column splits x 2 pair groups");
   static constexpr int MINB = P <= 8 ? 2 : 1;                 // CTAs per SM (register budget)
   static constexpr size_t SMEM_A = (size_t)ROWS * KA * sizeof(double);
   static constexpr size_t SMEM_B = (size_t)KC * D::NCS * sizeof(double);
   static constexpr size_t SMEM = SMEM_A + NST * SMEM_B;
 };
 
-// One KC-row chunk of the k_qmap GEMM for a warp; ZC = the quaternion component whose M block is zero in
-// this chunk's axis (compile time, so the skipped tiles cost nothing).  Tiles: component c, u-th of the
-// warp: column tile c TQC + ns + NSPLIT u; V: NTQ + ns + NSPLIT u.
-template <int P, int ZC>
-__device__ __forceinline__ void qmap_chunk(const double *arow, const double *brow, const double *bb, int ns,
+// One KC-row chunk of the k_qmap GEMM for a warp of column split NS; ZC = the quaternion component whose M
+// block is zero in this chunk's axis (compile time, so the skipped tiles cost nothing).  Tiles: component
+// c, u-th of the warp: column tile c TQC + NS + NSPLIT u; V: NTQ + vstart(NS) + u.
+template <int P, int ZC, int NS>
+__device__ __forceinline__ void qmap_chunk(const double *arow, const double *brow, const double *bb,
                                            double (&accA)[4][QmapCfg<P>::UQ][2], double (&accB)[4][QmapCfg<P>::UQ][2],
                                            double (&accV)[QmapCfg<P>::UV][2]) {
   using C = QmapCfg<P>;
-  constexpr int NCS = Dims<P>::NCS;
+  constexpr int NCS = Dims<P>::NCS, NQT = C::nq(NS), NVT = C::vcount(NS), V0 = C::vstart(NS);
 #pragma unroll
   for (int kk = 0; kk < C::KC; kk += 4) {
     const double a = arow[kk], b = brow[kk];
@@ -710,20 +721,14 @@ __device__ __forceinline__ void qmap_chunk(const double *arow, const double *bro
     for (int c = 0; c < 4; ++c) {
       if (c == ZC) continue;
 #pragma unroll
-      for (int u = 0; u < C::UQ; ++u) {
-        const int tl = ns + u * C::NSPLIT;
-        if (u + 1 < C::UQ || tl < C::TQC) {
-          const double bq = bk[(c * C::TQC + tl) * 8];
-          dmma(accA[c][u][0], accA[c][u][1], a, bq);
-          dmma(accB[c][u][0], accB[c][u][1], b, bq);
-        }
+      for (int u = 0; u < NQT; ++u) {
+        const double bq = bk[(c * C::TQC + NS + u * C::NSPLIT) * 8];
+        dmma(accA[c][u][0], accA[c][u][1], a, bq);
+        dmma(accB[c][u][0], accB[c][u][1], b, bq);
       }
     }
 #pragma unroll
-    for (int u = 0; u < C::UV; ++u) {
-      const int tl = ns + u * C::NSPLIT;
-      if (u + 1 < C::UV || tl < C::NTV) dmma(accV[u][0], accV[u][1], a, bk[(C::NTQ + tl) * 8]);
-    }
+    for (int u = 0; u < NVT; ++u) dmma(accV[u][0], accV[u][1], a, bk[(C::NTQ + V0 + u) * 8]);
   }
 }
 
@@ -834,11 +839,17 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     }
     mbar_wait(&bar[ch % C::NST], (ch / C::NST) & 1);
     const double *bb = sB + (ch % C::NST) * KC * NCS + bofs;
-    switch (ch / C::CPA) {   // axis of this chunk: component axis + 1 has a zero block
-      case 0: qmap_chunk<P, 1>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
-      case 1: qmap_chunk<P, 2>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
-      default: qmap_chunk<P, 3>(arow + ch * KC, brow + ch * KC, bb, ns, accA, accB, accV); break;
+    const int zc = 1 + ch / C::CPA;   // axis of this chunk: component axis + 1 has a zero block
+#define RRQ_QCHUNK(Z, N) qmap_chunk<P, Z, N>(arow + ch * KC, brow + ch * KC, bb, accA, accB, accV)
+#define RRQ_QNS(N) (zc == 1 ? RRQ_QCHUNK(1, N) : zc == 2 ? RRQ_QCHUNK(2, N) : RRQ_QCHUNK(3, N))
+    switch (ns) {
+      case 0: RRQ_QNS(0); break;
+      case 1: RRQ_QNS(1); break;
+      case 2: RRQ_QNS(2); break;
+      default: RRQ_QNS(3); break;
     }
+#undef RRQ_QNS
+#undef RRQ_QCHUNK
     __syncwarp();
     if (lane == 0) mbar_arrive(&emp[ch % C::NST]);
   }
@@ -851,7 +862,7 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
 #pragma unroll
       for (int u = 0; u < C::UQ; ++u) {
         const int tl = ns + u * C::NSPLIT;
-        if (tl >= C::TQC) continue;
+        if (tl >= C::TQC) continue;   // == u < nq(ns)
         const int e = tl * 4 + (lane & 3);   // entry qidx(j,k)
         if (e >= D::NQ) continue;
         const double sc = ssc[e];
@@ -861,11 +872,12 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
         o[8] = sc * accB[c][u][0];
         o[9] = sc * accB[c][u][1];
       }
+    const int v0 = ns == 0 ? C::vstart(0) : ns == 1 ? C::vstart(1) : ns == 2 ? C::vstart(2) : C::vstart(3);
+    const int nv = ns == 0 ? C::vcount(0) : ns == 1 ? C::vcount(1) : ns == 2 ? C::vcount(2) : C::vcount(3);
 #pragma unroll
     for (int u = 0; u < C::UV; ++u) {
-      const int tl = ns + u * C::NSPLIT;
-      if (tl >= C::NTV) continue;
-      const int col = tl * 8 + 2 * (lane & 3);
+      if (u >= nv) continue;
+      const int col = (v0 + u) * 8 + 2 * (lane & 3);
       if (col < 2 * D::NV) {
         const double sc = ssc[D::NQ + (col >> 1)];
         out[QR::V + col] = sc * accV[u][0];
