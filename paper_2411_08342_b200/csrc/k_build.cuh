@@ -241,13 +241,21 @@ struct PairSetup {
   int64_t k;
   int32_t Pp, self_local;
 };
+// What k_contract's epilogue needs of a pair (global target position and normal, pair index, self node),
+// written by k_pair_setup in the sub-chunk's patch-major order so a tile's entries are one bulk copy.
+struct ContractPair {
+  double x[3], n[3];
+  int64_t k;
+  int32_t self_local, pad;
+};
+static_assert(sizeof(ContractPair) == 64, "ContractPair layout");
 
 template <int P>
 __global__ void k_pair_setup(int64_t sA, int64_t sB, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt,
                              int64_t kbase, const int32_t *__restrict__ pair_patch, const double *__restrict__ fit,
                              const double *__restrict__ tx, const double *__restrict__ tnorm,
                              const int64_t *__restrict__ self_node, const int8_t *__restrict__ side,
-                             PairSetup *__restrict__ setup) {
+                             PairSetup *__restrict__ setup, ContractPair *__restrict__ cpair) {
   using D = Dims<P>;
   using L = Layout<P>;
   const int64_t s = sA + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -291,6 +299,14 @@ __global__ void k_pair_setup(int64_t sA, int64_t sB, const int64_t *__restrict__
         PairSetup &q = setup[s - sA];
         q.k = k; q.Pp = Pp; q.self_local = self_local; q.u3 = sg;
         for (int a = 0; a < 3; ++a) { q.rp[a] = rp[a]; q.nup[a] = nup[a]; }
+        ContractPair &cp = cpair[s - sA];
+        for (int a = 0; a < 3; ++a) {
+          cp.x[a] = tx[3 * t + a];
+          cp.n[a] = tnorm ? tnorm[3 * t + a] : 0.0;
+        }
+        cp.k = k;
+        cp.self_local = self_local;
+        cp.pad = 0;
 }
 
 // Per-pair state of k_pair_edge (shared memory; one per pair of the CTA round).
@@ -1153,18 +1169,15 @@ struct ContractCfg {
   static constexpr size_t SMEM_Z = (size_t)TP * ZS;
   static constexpr size_t SMEM_B = 3 * (size_t)KC * NB;                                       // PD | PSp | PSg
   static constexpr size_t SNODE = (7 * D::N + 1) / 2 * 2;   // the patch's nodes [N][3], normals [N][3], weights [N]
-  static constexpr size_t SMEM = (SMEM_Z + 2 * SMEM_B + SNODE + TP * 8) * sizeof(double) + TP * 16;
+  static constexpr size_t SMEM = (SMEM_Z + 2 * SMEM_B + SNODE + TP * 8) * sizeof(double);   // + ContractPair[TP]
 };
 
 template <int P>
 __global__ void __launch_bounds__(256, 2)
     k_contract(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, const int32_t *__restrict__ item_patch,
-               const int64_t *__restrict__ seg_ptr, int64_t sA, const int64_t *__restrict__ perm,
-               const int64_t *__restrict__ ptgt, int64_t kbase, const double *__restrict__ fit,
-               const double *__restrict__ Zrow, const double *__restrict__ nodes,
-               const double *__restrict__ normals, const double *__restrict__ weights,
-               const double *__restrict__ tx, const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
-               uint32_t mask, int raw, int64_t obase, int32_t *__restrict__ col_idx, double *vS, double *vD,
+               const int64_t *__restrict__ seg_ptr, int64_t sA, const ContractPair *__restrict__ cpair,
+               const double *__restrict__ fit, const double *__restrict__ Zrow, const double *__restrict__ nodes,
+               const double *__restrict__ normals, const double *__restrict__ weights, uint32_t mask, int raw, int64_t obase, int32_t *__restrict__ col_idx, double *vS, double *vD,
                double *vSp, double *vDp, int32_t *__restrict__ pstat) {
   using D = Dims<P>;
   using L = Layout<P>;
@@ -1173,9 +1186,7 @@ __global__ void __launch_bounds__(256, 2)
   extern __shared__ __align__(16) double sz[];
   double *sB = sz + CC::SMEM_Z;                    // [2][3][KC][NB]
   double *sN = sB + 2 * CC::SMEM_B;                // nodes [N][3] | normals [N][3] | weights [N] of the patch
-  double *sT = sN + CC::SNODE;                     // [TP][8] target x, nu'
-  int64_t *sK = reinterpret_cast<int64_t *>(sT + TP * 8);
-  int *sSelf = reinterpret_cast<int *>(sK + TP);
+  ContractPair *sC = reinterpret_cast<ContractPair *>(sN + CC::SNODE);   // [TP] the tile's pairs
   const int64_t item = item0 + blockIdx.x;
   if (item >= item1) return;
   const int64_t Pp = item_patch[item];
@@ -1212,32 +1223,16 @@ __global__ void __launch_bounds__(256, 2)
   };
   {
     const unsigned zb = (unsigned)(cnt * NZS * sizeof(double)), nb3 = (unsigned)(3 * N * sizeof(double)),
-                   nb1 = (unsigned)(N * sizeof(double));
-    issue(0, zb + 2 * nb3 + nb1);
+                   nb1 = (unsigned)(N * sizeof(double)), cb = (unsigned)(cnt * sizeof(ContractPair));
+    issue(0, zb + 2 * nb3 + nb1 + cb);
     if (threadIdx.x == 32) {
       bulk_g2s(sz, Zrow + (s0 - sA) * NZS, zb, &bar[0]);
       bulk_g2s(sN, nodes + Pp * N * 3, nb3, &bar[0]);
       bulk_g2s(sN + 3 * N, normals + Pp * N * 3, nb3, &bar[0]);
       bulk_g2s(sN + 6 * N, weights + Pp * N, nb1, &bar[0]);
+      bulk_g2s(sC, cpair + (s0 - sA), cb, &bar[0]);
     }
   }
-  for (int r = threadIdx.x; r < TP; r += blockDim.x) {
-    if (r < cnt) {
-      const int64_t k = perm[s0 + r], t = ptgt[k - kbase];
-      sK[r] = k;
-      for (int a = 0; a < 3; ++a) {
-        sT[r * 8 + a] = tx[3 * t + a];
-        sT[r * 8 + 3 + a] = tnorm ? tnorm[3 * t + a] : 0.0;
-      }
-      int sl = -1;
-      if (self_node) {
-        const int64_t sn = self_node[t];
-        if (sn >= 0 && sn / N == Pp) sl = (int)(sn % N);
-      }
-      sSelf[r] = sl;
-    }
-  }
-  __syncthreads();
   // P_Sd fragments for Theta . P_Sd straight from global, issued before waiting for the Z tile
   constexpr int NK = (NP + 3) / 4;
   double bq[CC::TPW][NK];
@@ -1321,17 +1316,18 @@ __global__ void __launch_bounds__(256, 2)
     for (int q = 0; q < 2; ++q) {
       const int i = i0 + q;
       double S = accS[q] * h, Dv = accD[q], Sp = accSp[q], Dp = accDp[q] / h;
-      if (!raw && i < N && sSelf[row] != i) {
+      if (!raw && i < N && sC[row].self_local != i) {
         const double *xi = sN + 3 * i, *ni = sN + 3 * N + 3 * i;
         const double wi = sN[6 * N + i];
-        const double d0 = sT[row * 8] - xi[0], d1 = sT[row * 8 + 1] - xi[1], d2 = sT[row * 8 + 2] - xi[2];
+        const double *tr = sC[row].x, *tn = sC[row].n;
+        const double d0 = tr[0] - xi[0], d1 = tr[1] - xi[1], d2 = tr[2] - xi[2];
         const double r2 = d0 * d0 + d1 * d1 + d2 * d2;
         double ir = rsqrt(r2);
         ir = ir * (1.5 - 0.5 * r2 * ir * ir);
         const double ir3 = ir * ir * ir;
         const double dn = d0 * ni[0] + d1 * ni[1] + d2 * ni[2];
-        const double dnp = d0 * sT[row * 8 + 3] + d1 * sT[row * 8 + 4] + d2 * sT[row * 8 + 5];
-        const double nn = ni[0] * sT[row * 8 + 3] + ni[1] * sT[row * 8 + 4] + ni[2] * sT[row * 8 + 5];
+        const double dnp = d0 * tn[0] + d1 * tn[1] + d2 * tn[2];
+        const double nn = ni[0] * tn[0] + ni[1] * tn[1] + ni[2] * tn[2];
         S -= inv4pi * ir * wi;
         Dv -= inv4pi * dn * ir3 * wi;
         Sp += inv4pi * dnp * ir3 * wi;
@@ -1343,7 +1339,7 @@ __global__ void __launch_bounds__(256, 2)
       oDp[q] = (mask & 8) ? Dp : 0.0;
       if (i < N) bad |= !isfinite(S) || !isfinite(Dv) || !isfinite(Sp) || !isfinite(Dp);
     }
-    const int64_t o = (sK[row] - obase) * N + i0;
+    const int64_t o = (sC[row].k - obase) * N + i0;
     if (i0 + 1 < N) {   // the usual case: both columns, 16-B stores
       if (col_idx) *reinterpret_cast<int2 *>(col_idx + o) = make_int2((int32_t)(Pp * N + i0), (int32_t)(Pp * N + i0 + 1));
       if (vS) *reinterpret_cast<double2 *>(vS + o) = make_double2(oS[0], oS[1]);
@@ -1357,7 +1353,7 @@ __global__ void __launch_bounds__(256, 2)
       if (vSp) vSp[o] = oSp[0];
       if (vDp) vDp[o] = oDp[0];
     }
-    if (bad && pstat) atomicOr(pstat + (sK[row] - obase), 2);
+    if (bad && pstat) atomicOr(pstat + (sC[row].k - obase), 2);
   }
 }
 

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -36,12 +37,18 @@ struct rrq_ctx_s {
     size_t n = 0;
   };
   int64_t last_np = 0, last_nz = 0, last_nzs = 0, last_sA = 0;
-  Buf Arow, Xrow, Qrow, ipatch, psetup;
+  // k_pair_edge's outputs are double-buffered (set = sub-chunk parity) so that the producer stream (k_pair_setup,
+  // k_pair_edge of sub-chunk i+1) runs concurrently with the consumer stream (k_qmap, k_translate, k_contract of
+  // sub-chunk i): the edge kernel is FP64-latency bound and the GEMM kernels leave the FP64 pipe ~40 % idle.
+  Buf Arow[2], Xrow[2], psetup[2], cpair[2], Qrow, ipatch;
+  cudaStream_t st2 = nullptr;                      // producer stream (created on first use)
+  cudaEvent_t ev_edge[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_fork = nullptr, ev_join = nullptr;
+  bool overlap = true;                             // RRQ_NO_OVERLAP=1 runs everything on the caller's stream
   Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one, swapcnt;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
-  double t_ms[7] = {0, 0, 0, 0, 0, 0, 0};
-  int64_t t_n[7] = {0, 0, 0, 0, 0, 0, 0};
+  double t_ms[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t t_n[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0};
   int64_t stats[2] = {0, 0};
   struct Pend {
     int stage;
@@ -310,6 +317,10 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  {
+    const char *e = std::getenv("RRQ_NO_OVERLAP");
+    c->overlap = !(e && std::atoi(e) != 0);
+  }
   int q = p.p_edge, no = p.n_omega;
   c->h_t.resize(q);
   c->h_w.resize(q);
@@ -401,7 +412,11 @@ void rrq_destroy(rrq_ctx c) {
   if (c->swapcnt.p) cudaFree(c->swapcnt.p);
   cudaFree(c->d_tab);
   if (c->d_trtab) cudaFree(c->d_trtab);
-  for (auto *b : {&c->Arow, &c->Xrow, &c->Qrow, &c->ipatch, &c->psetup, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
+  if (c->st2) cudaStreamDestroy(c->st2);
+  for (cudaEvent_t e : {c->ev_edge[0], c->ev_edge[1], c->ev_free[0], c->ev_free[1], c->ev_fork, c->ev_join})
+    if (e) cudaEventDestroy(e);
+  for (auto *b : {&c->Arow[0], &c->Arow[1], &c->Xrow[0], &c->Xrow[1], &c->psetup[0], &c->psetup[1], &c->cpair[0],
+                  &c->cpair[1], &c->Qrow, &c->ipatch, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
                   &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
     if (b->p) cudaFree(b->p);
   delete c;
@@ -448,10 +463,10 @@ rrq_status rrq_reset_timing(rrq_ctx c) {
   return RRQ_OK;
 }
 
-rrq_status rrq_get_timing(rrq_ctx c, double ms[7], int64_t launches[7], int64_t stats[2]) {
+rrq_status rrq_get_timing(rrq_ctx c, double ms[RRQ_NSTAGES], int64_t launches[RRQ_NSTAGES], int64_t stats[2]) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   t_flush(c);
-  for (int i = 0; i < 7; ++i) {
+  for (int i = 0; i < RRQ_NSTAGES; ++i) {
     if (ms) ms[i] = c->t_ms[i];
     if (launches) launches[i] = c->t_n[i];
   }
@@ -674,6 +689,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     return RRQ_ERR_CUDA;
   // ---- plumbing over the whole call: pair -> target, patch-major permutation, work items
   std::vector<int64_t> hseg(Pn + 1), hitem(Pn + 1);
+  TScope tbuild(c, 7, st);   // the whole call (device time on the caller's stream)
   {
     TScope tsp(c, 6, st);
     k_pair_targets<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase,
@@ -694,9 +710,11 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   }
   cudaStreamSynchronize(st);
   hseg[Pn] = total;
-  // ---- sub-chunks: ranges of whole patches with at most `cap` pairs (scratch ~16 KB per pair at p = 8)
-  const int64_t per_pair = (int64_t)(2 * D::K + XRow<P>::STRIDE + QRow<P>::STRIDE + D::NZS) * 8;
-  const int64_t cap = std::max<int64_t>(4096, (int64_t)(20e9 / per_pair));
+  // ---- sub-chunks: ranges of whole patches with at most `cap` pairs (scratch ~24 KB per pair at p = 8:
+  // the double-buffered pair_edge outputs plus the Q and Z rows)
+  const int64_t per_pair = (int64_t)(2 * (2 * D::K + XRow<P>::STRIDE) + QRow<P>::STRIDE + D::NZS) * 8 +
+                           2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair));
+  const int64_t cap = std::max<int64_t>(4096, (int64_t)(24e9 / per_pair));
   std::vector<std::pair<int64_t, int64_t>> subs;
   int64_t maxsub = 0;
   for (int64_t P0 = 0; P0 < Pn;) {
@@ -708,9 +726,13 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     }
     P0 = P1;
   }
-  if (!ensure(c, c->Arow, (size_t)maxsub * 2 * D::K * 8) || !ensure(c, c->Xrow, (size_t)maxsub * XRow<P>::STRIDE * 8) ||
-      !ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxsub * D::NZS * 8) ||
-      !ensure(c, c->psetup, (size_t)maxsub * sizeof(PairSetup)))
+  const int nset = (c->overlap && subs.size() > 1) ? 2 : 1;
+  for (int b = 0; b < nset; ++b)
+    if (!ensure(c, c->Arow[b], (size_t)maxsub * 2 * D::K * 8) || !ensure(c, c->Xrow[b], (size_t)maxsub * XRow<P>::STRIDE * 8) ||
+        !ensure(c, c->psetup[b], (size_t)maxsub * sizeof(PairSetup)) ||
+        !ensure(c, c->cpair[b], (size_t)maxsub * sizeof(ContractPair)))
+      return RRQ_ERR_CUDA;
+  if (!ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxsub * D::NZS * 8))
     return RRQ_ERR_CUDA;
   static bool attr_set = false;
   if (!attr_set) {
@@ -720,49 +742,76 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     cudaFuncSetAttribute(k_contract<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
+  // producer stream: a second stream when overlapping, else the caller's
+  cudaStream_t sp = st;
+  if (nset == 2) {
+    if (!c->st2) {
+      if (cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(c, RRQ_ERR_CUDA, "stream creation failed");
+      for (cudaEvent_t *e : {&c->ev_edge[0], &c->ev_edge[1], &c->ev_free[0], &c->ev_free[1], &c->ev_fork, &c->ev_join})
+        cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    }
+    sp = c->st2;
+    cudaEventRecord(c->ev_fork, st);   // the producer sees the plumbing above (perm, items, ...)
+    cudaStreamWaitEvent(sp, c->ev_fork, 0);
+  }
   rrq_status r;
-  for (auto &sr : subs) {
+  for (size_t i = 0; i < subs.size(); ++i) {
+    const auto &sr = subs[i];
+    const int b = (int)(i % nset);
     const int64_t sA = hseg[sr.first], sB = hseg[sr.second];
     const int64_t it0 = hitem[sr.first], it1 = hitem[sr.second];
     const int64_t np_ = sB - sA;
+    double *Ar = bp<double>(c->Arow[b]), *Xr = bp<double>(c->Xrow[b]);
+    PairSetup *ps = bp<PairSetup>(c->psetup[b]);
+    ContractPair *cp = bp<ContractPair>(c->cpair[b]);
+    // ---- producer: Steps 4-5 (+ scalar line integrals, gamma parts) into set b
+    if (nset == 2 && i >= 2) cudaStreamWaitEvent(sp, c->ev_free[b], 0);   // sub-chunk i-2 is done with set b
     {
-      TScope t1(c, 2, st);
-      k_pair_setup<P><<<nblk(np_, 256), 256, 0, st>>>(sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase,
-                                                       pair_patch, fit, tg->x, tg->normal, tg->self_node, tg->side,
-                                                       bp<PairSetup>(c->psetup));
+      TScope t1(c, 2, sp);
+      k_pair_setup<P><<<nblk(np_, 256), 256, 0, sp>>>(sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase,
+                                                       pair_patch, fit, tg->x, tg->normal, tg->self_node, tg->side, ps, cp);
       unsigned grid = (unsigned)std::min<int64_t>((np_ + kWPB * kPPW - 1) / (kWPB * kPPW), (int64_t)c->num_sms * 4);
-      k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), st>>>(
+      k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), sp>>>(
           sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
-          tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, bp<double>(c->Arow), bp<double>(c->Xrow),
-          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, bp<PairSetup>(c->psetup));
+          tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, Ar, Xr,
+          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, ps);
     }
     if ((r = cuda_check(c, "k_pair_edge"))) return r;
+    if (nset == 2) {
+      cudaEventRecord(c->ev_edge[b], sp);
+      cudaStreamWaitEvent(st, c->ev_edge[b], 0);
+    }
+    // ---- consumer: Steps 6-8
     {
       TScope t2(c, 3, st);
       k_qmap<P><<<(unsigned)(it1 - it0), QC::WARPS * 32, QC::SMEM, st>>>(it0, it1, bp<int64_t>(c->items), bp<int32_t>(c->ipatch),
-                                                                bp<int64_t>(c->seg), sA, fit, bp<double>(c->Arow),
-                                                                bp<double>(c->Qrow), c->d_trtab);
+                                                                bp<int64_t>(c->seg), sA, fit, Ar, bp<double>(c->Qrow), c->d_trtab);
     }
     if ((r = cuda_check(c, "k_qmap"))) return r;
     {
       TScope t3(c, 4, st);
       constexpr int WPB = TrCfg<P>::WPB;
       unsigned grid = (unsigned)std::min<int64_t>((np_ + WPB - 1) / WPB, (int64_t)c->num_sms);
-      k_translate<P><<<grid, WPB * 32, TrCfg<P>::SMEM, st>>>(sA, sB, bp<double>(c->Xrow), bp<double>(c->Qrow),
-                                                              c->d_trtab, bp<double>(c->Z));
+      k_translate<P><<<grid, WPB * 32, TrCfg<P>::SMEM, st>>>(sA, sB, Xr, bp<double>(c->Qrow), c->d_trtab, bp<double>(c->Z));
     }
     if ((r = cuda_check(c, "k_translate"))) return r;
     {
       TScope t4(c, 5, st);
       k_contract<P><<<(unsigned)(it1 - it0), CC::WARPS * 32, CC::SMEM, st>>>(
-          it0, it1, bp<int64_t>(c->items), bp<int32_t>(c->ipatch), bp<int64_t>(c->seg), sA, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt),
-          obase, fit, bp<double>(c->Z), s->nodes, s->normals, s->weights, tg->x, tg->normal, tg->self_node, mask, raw,
-          obase, col_idx, vals[0], vals[1], vals[2], vals[3], pstat);
+          it0, it1, bp<int64_t>(c->items), bp<int32_t>(c->ipatch), bp<int64_t>(c->seg), sA, cp,
+          fit, bp<double>(c->Z), s->nodes, s->normals, s->weights, mask, raw, obase, col_idx, vals[0], vals[1], vals[2],
+          vals[3], pstat);
     }
     if ((r = cuda_check(c, "k_contract"))) return r;
+    if (nset == 2) cudaEventRecord(c->ev_free[b], st);
     c->launches += 5;
     c->last_sA = sA;
     c->last_np = np_;
+  }
+  if (nset == 2) {   // join the producer stream
+    cudaEventRecord(c->ev_join, sp);
+    cudaStreamWaitEvent(st, c->ev_join, 0);
   }
   if (row_ptr) {
     k_row_ptr<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase, row_ptr, D::N);

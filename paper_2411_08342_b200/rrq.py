@@ -162,7 +162,7 @@ class RRQ:
     def launch_count(self):
         return int(self.lib.rrq_launch_count(self.h))
 
-    STAGES = ("near_list", "patch_fit", "pair_edge", "qmap", "translate", "contract", "plumbing")
+    STAGES = ("near_list", "patch_fit", "pair_edge", "qmap", "translate", "contract", "plumbing", "build")
 
     def set_timing(self, on=True):
         self._check(self.lib.rrq_set_timing(self.h, int(on)), "rrq_set_timing")
@@ -173,7 +173,7 @@ class RRQ:
     def timing(self):
         """Accumulated device ms and launch counts per stage + (pairs, swap edges)."""
         import numpy as np
-        ms = np.zeros(7); n = np.zeros(7, np.int64); st = np.zeros(2, np.int64)
+        ms = np.zeros(len(self.STAGES)); n = np.zeros(len(self.STAGES), np.int64); st = np.zeros(2, np.int64)
         self._check(self.lib.rrq_get_timing(self.h, ms.ctypes.data, n.ctypes.data, st.ctypes.data), "rrq_get_timing")
         return dict(ms=dict(zip(self.STAGES, ms.tolist())), launches=dict(zip(self.STAGES, n.tolist())),
                     pairs=int(st[0]), swap_edges=int(st[1]))
