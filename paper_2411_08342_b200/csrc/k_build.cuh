@@ -97,7 +97,7 @@ template <int P>
 struct QRow {
   using D = Dims<P>;
   static constexpr int EG = 16;
-  static constexpr int V = EG * D::NQ, STRIDE = V + 2 * D::NV;
+  static constexpr int V = EG * D::NQ, STRIDE = (V + 2 * D::NV + 15) / 16 * 16;   // rows 128-B aligned
 };
 
 // k_translate's schedule (see k_translate).  Outputs (l, m), m = 1..l, are grouped in blocks of WD
@@ -804,7 +804,6 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
   // pipeline: bar[b] = "chunk in buffer b landed" (bulk-copy transactions), emp[b] = "all warps done with
   // buffer b" (one arrival per warp); no CTA-wide barrier inside the K loop
   __shared__ uint64_t bar[C::NST], emp[C::NST];
-  __shared__ double ssc[D::NQ + D::NV];   // v_lambda | v_theta
   constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ROWB = (unsigned)(K * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -819,7 +818,6 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     const int r = i / K;
     if (r % TP >= cnt) sA_[r * KA + i % K] = 0.0;
   }
-  for (int i = threadIdx.x; i < D::NQ + D::NV; i += blockDim.x) ssc[i] = trtab[TrCfg<P>::VLAM + i];
   __syncthreads();
   // stage A (row r < TP -> a-row of pair s0 + r; row TP + r -> b-row) and chunk 0 of M on bar[0]
   // (a bulk copy takes uniform operands: one issuing lane per warp, rows spread over the warps)
@@ -869,36 +867,32 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     __syncwarp();
     if (lane == 0) mbar_arrive(&emp[ch % C::NST]);
   }
-  // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]
+  // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]; a lane owns whole entries (all 4 components of Q and
+  // dQ of entry e over its c loop): 16-B stores filling the entry's 128-B line (rows are 128-B aligned).
+  // M's columns carry v_lambda / v_theta (k_edge_tables), so no scaling here.
   const int pr = pg * 8 + (lane >> 2);
   if (pr < cnt) {
     double *out = Qrow + (s0 + pr - sA) * QR::STRIDE;
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int u = 0; u < C::UQ; ++u) {
+      const int tl = ns + u * C::NSPLIT;
+      if (tl >= C::TQC) continue;   // == u < nq(ns)
+      const int e = tl * 4 + (lane & 3);   // entry qidx(j,k)
+      if (e >= D::NQ) continue;
+      double2 *o = reinterpret_cast<double2 *>(out + QR::EG * e);
 #pragma unroll
-      for (int u = 0; u < C::UQ; ++u) {
-        const int tl = ns + u * C::NSPLIT;
-        if (tl >= C::TQC) continue;   // == u < nq(ns)
-        const int e = tl * 4 + (lane & 3);   // entry qidx(j,k)
-        if (e >= D::NQ) continue;
-        const double sc = ssc[e];
-        double *o = out + QR::EG * e + 2 * c;
-        o[0] = sc * accA[c][u][0];
-        o[1] = sc * accA[c][u][1];
-        o[8] = sc * accB[c][u][0];
-        o[9] = sc * accB[c][u][1];
+      for (int c = 0; c < 4; ++c) {
+        o[c] = make_double2(accA[c][u][0], accA[c][u][1]);
+        o[4 + c] = make_double2(accB[c][u][0], accB[c][u][1]);
       }
+    }
     const int v0 = ns == 0 ? C::vstart(0) : ns == 1 ? C::vstart(1) : ns == 2 ? C::vstart(2) : C::vstart(3);
     const int nv = ns == 0 ? C::vcount(0) : ns == 1 ? C::vcount(1) : ns == 2 ? C::vcount(2) : C::vcount(3);
 #pragma unroll
     for (int u = 0; u < C::UV; ++u) {
       if (u >= nv) continue;
       const int col = (v0 + u) * 8 + 2 * (lane & 3);
-      if (col < 2 * D::NV) {
-        const double sc = ssc[D::NQ + (col >> 1)];
-        out[QR::V + col] = sc * accV[u][0];
-        out[QR::V + col + 1] = sc * accV[u][1];
-      }
+      if (col < 2 * D::NV) *reinterpret_cast<double2 *>(out + QR::V + col) = make_double2(accV[u][0], accV[u][1]);
     }
   }
 }

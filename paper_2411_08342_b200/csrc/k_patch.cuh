@@ -139,9 +139,12 @@ __global__ void k_patch_geom(int64_t n_patches, const double *__restrict__ nodes
 // so that [Q | V](pair) = a(pair) M with a = (omega1_kappa d_kappa) flattened (k = 3 kappa + axis), and
 // dQ(pair) = b(pair) M[:, Q cols] with b = omega1 nu' - omega3 (nu'.d) d.
 // Columns: Q block 8 jk + 2 comp + re/im (comp 0..3 = scalar, x, y, z), then V block 8 NQ + 2 jk + re/im.
+// The columns of (j,k) carry k_translate's operand scaling v_lambda(j,k) (Q) / v_theta(j,k) (V) (TrCfg), so
+// k_qmap stores its accumulators as they are.
 // One thread per (patch, edge node); it owns rows 3 kappa .. 3 kappa + 2.
 template <int P>
-__global__ void k_edge_tables(int64_t n_patches, const double *__restrict__ hc, double *__restrict__ fit) {
+__global__ void k_edge_tables(int64_t n_patches, const double *__restrict__ hc, const double *__restrict__ vlam,
+                              const double *__restrict__ vth, double *__restrict__ fit) {
   using D = Dims<P>;
   using L = Layout<P>;
   int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -166,14 +169,16 @@ __global__ void k_edge_tables(int64_t n_patches, const double *__restrict__ hc, 
       cd e[3] = {g[1] * mk(t[2], 0) - g[2] * mk(t[1], 0), g[2] * mk(t[0], 0) - g[0] * mk(t[2], 0),
                  g[0] * mk(t[1], 0) - g[1] * mk(t[0], 0)};
       const int vc = D::NCQ + 2 * vidx(j, k);
-      for (int a = 0; a < 3; ++a) { M0[a * AX + vc] = e[a].x; M0[a * AX + vc + 1] = e[a].y; }
+      const double sv = vth[vidx(j, k)];   // k_translate's pre-scaling of V (TrCfg)
+      for (int a = 0; a < 3; ++a) { M0[a * AX + vc] = sv * e[a].x; M0[a * AX + vc + 1] = sv * e[a].y; }
       if (j >= 2) {
         cd h[3];
         hess_fast(GS, j, k, t, hc, h);
         const int qc = 2 * qidx(j, k);
         constexpr int S = D::CQP;
         for (int ri = 0; ri < 2; ++ri) {
-          double hv[3] = {ri ? h[0].y : h[0].x, ri ? h[1].y : h[1].x, ri ? h[2].y : h[2].x};
+          const double sq = vlam[qidx(j, k)];   // k_translate's pre-scaling of Q, dQ (TrCfg)
+          double hv[3] = {sq * (ri ? h[0].y : h[0].x), sq * (ri ? h[1].y : h[1].x), sq * (ri ? h[2].y : h[2].x)};
           // scalar part: -a.g
           for (int a = 0; a < 3; ++a) M0[a * AX + qc + ri] = -hv[a];
           // x: a_y g_z - a_z g_y ; y: a_z g_x - a_x g_z ; z: a_x g_y - a_y g_x  (axis c-1 of component c is zero)
