@@ -89,7 +89,7 @@ template <int P>
 struct XRow {
   using D = Dims<P>;
   static constexpr int SX = 0, W = 4 * P * P, DW = W + 4 * D::NP, TH = DW + 4 * D::NP, NU = TH + D::NP,
-                       G = W, GSZ = (9 * D::NP + 3 + 1) / 2 * 2, STRIDE = G + GSZ;
+                       G = W, GSZ = (9 * D::NP + 3 + 1) / 2 * 2, STRIDE = (G + GSZ + 15) / 16 * 16;   // rows 128-B aligned
 };
 // Per-pair row of k_qmap's output: per (j, k >= 0), 2 <= j <= p, at EG qidx(j,k): [Q (4 quaternion comps,
 // re/im) | dQ (same)] scaled by v_lambda(j,k); then V [2 NV] scaled by v_theta(j,k) (TrCfg).
@@ -415,18 +415,14 @@ __global__ void __launch_bounds__(WPB * 32)
       const cd *g = wsc.GS[pp][e];
       const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
       const double w = __ldg(wS + l * l + l + m);
-      double *o = Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m);
-      o[0] = w * r.y;
-      o[1] = w * r.x;
-      o[2] = w * ng.y;
-      o[3] = w * ng.x;
+      double2 *o = reinterpret_cast<double2 *>(Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m));
+      o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
+      o[1] = make_double2(w * ng.y, w * ng.x);
       if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
         const double sg = (m & 1) ? -w : w;
-        o -= 8 * m;
-        o[0] = -sg * r.y;
-        o[1] = sg * r.x;
-        o[2] = -sg * ng.y;
-        o[3] = sg * ng.x;
+        o -= 4 * m;
+        o[0] = make_double2(-sg * r.y, sg * r.x);
+        o[1] = make_double2(-sg * ng.y, sg * ng.x);
       }
     }
     if (lane < 3 * kPPW && mine[lane / 3].active)
