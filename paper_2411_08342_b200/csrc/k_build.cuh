@@ -236,14 +236,15 @@ __device__ __forceinline__ double tri_sum(double v, int base) {
 
 // Per-pair setup (thread per pair; latency-bound index chasing done with full occupancy): the target in
 // the patch frame (A2: origin, rotation, scale 1/h), nu' in the frame, the self node, the gauge sign (A8).
-struct PairSetup {
+struct __align__(16) PairSetup {
   double rp[3], nup[3], u3;
-  int64_t k;
   int32_t Pp, self_local;
+  int64_t k, pad;
 };
+static_assert(sizeof(PairSetup) == 80, "PairSetup layout");
 // What k_contract's epilogue needs of a pair (global target position and normal, pair index, self node),
 // written by k_pair_setup in the sub-chunk's patch-major order so a tile's entries are one bulk copy.
-struct ContractPair {
+struct __align__(16) ContractPair {
   double x[3], n[3];
   int64_t k;
   int32_t self_local, pad;
@@ -296,17 +297,20 @@ __global__ void k_pair_setup(int64_t sA, int64_t sB, const int64_t *__restrict__
             else sg = (z - 0.5 * (zlo + zhi) > 0) ? 1.0 : -1.0;
           }
         }
-        PairSetup &q = setup[s - sA];
-        q.k = k; q.Pp = Pp; q.self_local = self_local; q.u3 = sg;
-        for (int a = 0; a < 3; ++a) { q.rp[a] = rp[a]; q.nup[a] = nup[a]; }
-        ContractPair &cp = cpair[s - sA];
-        for (int a = 0; a < 3; ++a) {
-          cp.x[a] = tx[3 * t + a];
-          cp.n[a] = tnorm ? tnorm[3 * t + a] : 0.0;
-        }
-        cp.k = k;
-        cp.self_local = self_local;
-        cp.pad = 0;
+        // whole records with 16-B stores
+        double2 *q = reinterpret_cast<double2 *>(setup + (s - sA));
+        q[0] = make_double2(rp[0], rp[1]);
+        q[1] = make_double2(rp[2], nup[0]);
+        q[2] = make_double2(nup[1], nup[2]);
+        q[3] = make_double2(sg, __longlong_as_double((long long)(uint32_t)Pp | ((long long)self_local << 32)));
+        q[4] = make_double2(__longlong_as_double(k), 0.0);
+        const double x0 = tx[3 * t], x1 = tx[3 * t + 1], x2 = tx[3 * t + 2];
+        const double n0 = tnorm ? tnorm[3 * t] : 0.0, n1 = tnorm ? tnorm[3 * t + 1] : 0.0, n2 = tnorm ? tnorm[3 * t + 2] : 0.0;
+        double2 *cp = reinterpret_cast<double2 *>(cpair + (s - sA));
+        cp[0] = make_double2(x0, x1);
+        cp[1] = make_double2(x2, n0);
+        cp[2] = make_double2(n1, n2);
+        cp[3] = make_double2(__longlong_as_double(k), __longlong_as_double((long long)(uint32_t)self_local));
 }
 
 // Per-pair state of k_pair_edge (shared memory; one per pair of the CTA round).
