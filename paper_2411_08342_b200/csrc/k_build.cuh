@@ -234,12 +234,48 @@ __device__ __forceinline__ double tri_sum(double v, int base) {
   return a + b + c;
 }
 
+// k_qmap's tile configuration (see k_qmap); k_pair_edge writes the A rows in its tile-chunked layout.
+template <int P>
+struct QmapCfg {
+  using D = Dims<P>;
+  static constexpr int TP = 16, ROWS = 2 * TP, WARPS = 8;
+  static constexpr int PG = TP / 8, NSPLIT = WARPS / PG;        // warp = (pair group of 8, column split)
+  static constexpr int TQC = D::CQP / 8;                      // tiles per quaternion component
+  static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8, NTV = NTALL - NTQ;
+  static constexpr int UQ = (TQC + NSPLIT - 1) / NSPLIT;       // a warp's tiles per component (at most)
+  // Work balance.  Column split ns takes the Q tiles tl = ns + NSPLIT u < TQC (2 DMMA each: a and b rows)
+  // and a contiguous range of V tiles (1 DMMA each), sized so that the two SM sub-partitions' loads match:
+  // warp w = ns PG + pg runs on sub-partition w % 4, so splits {0, 2} share one pair of sub-partitions and
+  // {1, 3} the other.  Counts are compile-time per split (no predicated-off DMMA).
+  __host__ __device__ static constexpr int nq(int ns) { return (TQC - ns + NSPLIT - 1) / NSPLIT; }
+  static constexpr int VA0 = (NTV + 6 * (nq(1) + nq(3)) - 6 * (nq(0) + nq(2)) + 1) / 2;
+  static constexpr int VA = VA0 < 0 ? 0 : (VA0 > NTV ? NTV : VA0), VB = NTV - VA;
+  __host__ __device__ static constexpr int vcount(int ns) { return ns == 0 ? (VA + 1) / 2 : ns == 2 ? VA / 2 : ns == 1 ? (VB + 1) / 2 : VB / 2; }
+  __host__ __device__ static constexpr int vstart(int ns) { return ns == 0 ? 0 : ns == 1 ? vcount(0) : ns == 2 ? vcount(0) + vcount(1) : vcount(0) + vcount(1) + vcount(2); }
+  static constexpr int UV = vcount(0) > vcount(1) ? (vcount(0) > vcount(2) ? (vcount(0) > vcount(3) ? vcount(0) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)))
+                                                  : (vcount(1) > vcount(2) ? (vcount(1) > vcount(3) ? vcount(1) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)));
+  static constexpr int KC = (D::E % 8 == 0) ? 8 : 12, NCH = D::K / KC, CPA = D::E / KC;   // chunks per axis
+  static constexpr int NST = 3;                                    // pipeline stages (chunks in flight)
+  // A (the tile's 32 GEMM rows) is stored tile-chunked by k_pair_edge: chunk ch = [32 rows][KC] (ACH doubles,
+  // rows 0..15 = a-rows of the tile's pairs, 16..31 = b-rows), so a stage = [A chunk | B chunk] is two bulk
+  // copies and A needs no resident shared memory.  KC = 8: the halves of rows with (r >> 1) odd are swapped
+  // (k ^ 4) so a quarter-warp's A fragments fall in distinct banks.
+  static constexpr int ACH = ROWS * KC, ABLK = NCH * ACH, STG = ACH + KC * D::NCS;
+  static_assert(D::E % KC == 0, "a B chunk must lie within one axis block");
+  static_assert(NSPLIT == 4 && PG == 2, "sub-partition balance assumes 4 column splits x 2 pair groups");
+  static constexpr int MINB = P <= 8 ? 2 : 1;                 // CTAs per SM (register budget)
+  static constexpr size_t SMEM = (size_t)NST * STG * sizeof(double);
+  __host__ __device__ static constexpr int swz(int r) { return KC == 8 ? ((r >> 1) & 1) << 2 : 0; }
+  // offset of A element (row r, k) in a tile block
+  __host__ __device__ static constexpr int aoff(int r, int k) { return (k / KC) * ACH + r * KC + ((k % KC) ^ swz(r)); }
+};
+
 // Per-pair setup (thread per pair; latency-bound index chasing done with full occupancy): the target in
 // the patch frame (A2: origin, rotation, scale 1/h), nu' in the frame, the self node, the gauge sign (A8).
 struct __align__(16) PairSetup {
   double rp[3], nup[3], u3;
   int32_t Pp, self_local;
-  int64_t k, pad;
+  int64_t k, aslot;   // aslot = (k_qmap tile of the pair within the sub-chunk) << 5 | row in the tile
 };
 static_assert(sizeof(PairSetup) == 80, "PairSetup layout");
 // What k_contract's epilogue needs of a pair (global target position and normal, pair index, self node),
@@ -256,6 +292,7 @@ __global__ void k_pair_setup(int64_t sA, int64_t sB, const int64_t *__restrict__
                              int64_t kbase, const int32_t *__restrict__ pair_patch, const double *__restrict__ fit,
                              const double *__restrict__ tx, const double *__restrict__ tnorm,
                              const int64_t *__restrict__ self_node, const int8_t *__restrict__ side,
+                             const int64_t *__restrict__ seg_ptr, const int64_t *__restrict__ item_ptr, int64_t it0,
                              PairSetup *__restrict__ setup, ContractPair *__restrict__ cpair) {
   using D = Dims<P>;
   using L = Layout<P>;
@@ -303,7 +340,8 @@ __global__ void k_pair_setup(int64_t sA, int64_t sB, const int64_t *__restrict__
         q[1] = make_double2(rp[2], nup[0]);
         q[2] = make_double2(nup[1], nup[2]);
         q[3] = make_double2(sg, __longlong_as_double((long long)(uint32_t)Pp | ((long long)self_local << 32)));
-        q[4] = make_double2(__longlong_as_double(k), 0.0);
+        const int64_t pos = s - seg_ptr[Pp], tile = item_ptr[Pp] + pos / QmapCfg<P>::TP - it0;
+        q[4] = make_double2(__longlong_as_double(k), __longlong_as_double(tile << 5 | (pos % QmapCfg<P>::TP)));
         const double x0 = tx[3 * t], x1 = tx[3 * t + 1], x2 = tx[3 * t + 2];
         const double n0 = tnorm ? tnorm[3 * t] : 0.0, n1 = tnorm ? tnorm[3 * t + 1] : 0.0, n2 = tnorm ? tnorm[3 * t + 2] : 0.0;
         double2 *cp = reinterpret_cast<double2 *>(cpair + (s - sA));
@@ -322,6 +360,7 @@ struct PairState {
   double t0[3][2];
   double rp[3], nup[3], u3, om[8], o0e[3];
   int64_t k, t;
+  int64_t aslot;               // PairSetup::aslot
   int Pp, self_local, active, pad;
   int swap[3], conv[3], direct[3];
 };
@@ -388,7 +427,7 @@ __global__ void __launch_bounds__(WPB * 32)
       ps.active = active;
       if (active) {
         const PairSetup &q = setup[s - sA];
-        ps.k = q.k; ps.Pp = q.Pp; ps.self_local = q.self_local; ps.u3 = q.u3;
+        ps.k = q.k; ps.Pp = q.Pp; ps.self_local = q.self_local; ps.u3 = q.u3; ps.aslot = q.aslot;
         for (int a = 0; a < 3; ++a) { ps.rp[a] = q.rp[a]; ps.nup[a] = q.nup[a]; }
       }
     }
@@ -542,7 +581,10 @@ __global__ void __launch_bounds__(WPB * 32)
       if (!ps.active) continue;
       const int64_t s = base + warp * kPPW + pp;
       const double *blk = fit + (int64_t)ps.Pp * L::STRIDE;
-      double *Ar = Arow + (s - sA) * 2 * K;
+      using QC = QmapCfg<P>;
+      double *Ar = Arow + (ps.aslot >> 5) * QC::ABLK;   // k_qmap's tile block (tile-chunked rows)
+      const int arow_ = (int)(ps.aslot & 31);
+      (void)s;
       const double rp[3] = {ps.rp[0], ps.rp[1], ps.rp[2]}, nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
       const double u[3] = {0.0, 0.0, ps.u3};
       double om[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // Omega_0(plain) Omega[3] dOmega_0 dOmega[3]
@@ -575,8 +617,8 @@ __global__ void __launch_bounds__(WPB * 32)
         double txd[3];
         cross3(tau, d, txd);
         for (int a = 0; a < 3; ++a) {
-          Ar[a * E + kap] = w1 * d[a];                          // GEMM row a (k = axis E + kappa)
-          Ar[K + a * E + kap] = w1 * nup[a] - w3 * nd * d[a];  // GEMM row b
+          Ar[QC::aoff(arow_, a * E + kap)] = w1 * d[a];                                 // row a (k = axis E + kappa)
+          Ar[QC::aoff(QC::TP + arow_, a * E + kap)] = w1 * nup[a] - w3 * nd * d[a];     // row b
           om[1 + a] -= w1 * tau[a];
           om[5 + a] += w3 * nd * tau[a];
         }
@@ -690,48 +732,19 @@ __global__ void __launch_bounds__(WPB * 32)
 // row stride == 8 mod 16).  Two CTAs per SM so one's staging / stores overlap the other's DMMA loop.
 // The epilogue scales by v_lambda / v_theta (TrCfg) and stores the QRow layout for k_translate.
 // ------------------------------------------------------------------------------------------------
-template <int P>
-struct QmapCfg {
-  using D = Dims<P>;
-  static constexpr int TP = 16, ROWS = 2 * TP, WARPS = 8;
-  static constexpr int PG = TP / 8, NSPLIT = WARPS / PG;        // warp = (pair group of 8, column split)
-  static constexpr int KA = (D::K % 16 == 4) ? D::K : D::K + ((4 - D::K % 16) + 16) % 16;
-  static constexpr int TQC = D::CQP / 8;                      // tiles per quaternion component
-  static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8, NTV = NTALL - NTQ;
-  static constexpr int UQ = (TQC + NSPLIT - 1) / NSPLIT;       // a warp's tiles per component (at most)
-  // Work balance.  Column split ns takes the Q tiles tl = ns + NSPLIT u < TQC (2 DMMA each: a and b rows)
-  // and a contiguous range of V tiles (1 DMMA each), sized so that the two SM sub-partitions' loads match:
-  // warp w = ns PG + pg runs on sub-partition w % 4, so splits {0, 2} share one pair of sub-partitions and
-  // {1, 3} the other.  Counts are compile-time per split (no predicated-off DMMA).
-  __host__ __device__ static constexpr int nq(int ns) { return (TQC - ns + NSPLIT - 1) / NSPLIT; }
-  static constexpr int VA0 = (NTV + 6 * (nq(1) + nq(3)) - 6 * (nq(0) + nq(2)) + 1) / 2;
-  static constexpr int VA = VA0 < 0 ? 0 : (VA0 > NTV ? NTV : VA0), VB = NTV - VA;
-  __host__ __device__ static constexpr int vcount(int ns) { return ns == 0 ? (VA + 1) / 2 : ns == 2 ? VA / 2 : ns == 1 ? (VB + 1) / 2 : VB / 2; }
-  __host__ __device__ static constexpr int vstart(int ns) { return ns == 0 ? 0 : ns == 1 ? vcount(0) : ns == 2 ? vcount(0) + vcount(1) : vcount(0) + vcount(1) + vcount(2); }
-  static constexpr int UV = vcount(0) > vcount(1) ? (vcount(0) > vcount(2) ? (vcount(0) > vcount(3) ? vcount(0) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)))
-                                                  : (vcount(1) > vcount(2) ? (vcount(1) > vcount(3) ? vcount(1) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)));
-  static constexpr int KC = (D::E % 8 == 0) ? 8 : 12, NCH = D::K / KC, CPA = D::E / KC;   // chunks per axis
-  static constexpr int NST = 2;                                    // pipeline stages (chunks in flight)
-  static_assert(D::E % KC == 0, "a B chunk must lie within one axis block");
-  static_assert(NSPLIT == 4 && PG == 2, "sub-partition balance assumes 4 column splits x 2 pair groups");
-  static constexpr int MINB = P <= 8 ? 2 : 1;                 // CTAs per SM (register budget)
-  static constexpr size_t SMEM_A = (size_t)ROWS * KA * sizeof(double);
-  static constexpr size_t SMEM_B = (size_t)KC * D::NCS * sizeof(double);
-  static constexpr size_t SMEM = SMEM_A + NST * SMEM_B;
-};
 
 // One KC-row chunk of the k_qmap GEMM for a warp of column split NS; ZC = the quaternion component whose M
 // block is zero in this chunk's axis (compile time, so the skipped tiles cost nothing).  Tiles: component
 // c, u-th of the warp: column tile c TQC + NS + NSPLIT u; V: NTQ + vstart(NS) + u.
 template <int P, int ZC, int NS>
-__device__ __forceinline__ void qmap_chunk(const double *arow, const double *brow, const double *bb,
+__device__ __forceinline__ void qmap_chunk(const double *arow, const double *brow, int sw, const double *bb,
                                            double (&accA)[4][QmapCfg<P>::UQ][2], double (&accB)[4][QmapCfg<P>::UQ][2],
                                            double (&accV)[QmapCfg<P>::UV][2]) {
   using C = QmapCfg<P>;
   constexpr int NCS = Dims<P>::NCS, NQT = C::nq(NS), NVT = C::vcount(NS), V0 = C::vstart(NS);
 #pragma unroll
   for (int kk = 0; kk < C::KC; kk += 4) {
-    const double a = arow[kk], b = brow[kk];
+    const double a = arow[kk ^ sw], b = brow[kk ^ sw];
     const double *bk = bb + kk * NCS;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -792,19 +805,19 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
   using L = Layout<P>;
   using C = QmapCfg<P>;
   using QR = QRow<P>;
-  constexpr int K = D::K, KA = C::KA, TP = C::TP, NCS = D::NCS, KC = C::KC;
-  extern __shared__ __align__(16) double sA_[];
-  double *sB = sA_ + C::SMEM_A / sizeof(double);    // [2][KC][NCS]
+  constexpr int TP = C::TP, NCS = D::NCS, KC = C::KC;
+  extern __shared__ __align__(16) double sst[];   // [NST][A chunk | B chunk]
   const int64_t item = item0 + blockIdx.x;
   if (item >= item1) return;
   const int64_t Pp = item_patch[item];
   const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *M = fit + Pp * (int64_t)L::STRIDE + L::MQ;
-  // pipeline: bar[b] = "chunk in buffer b landed" (bulk-copy transactions), emp[b] = "all warps done with
-  // buffer b" (one arrival per warp); no CTA-wide barrier inside the K loop
+  const double *Ablk = Arow + (item - item0) * (int64_t)C::ABLK;   // rows of absent pairs: never read back
+  // pipeline: bar[b] = "stage b landed" (bulk-copy transactions), emp[b] = "all warps done with stage b" (one
+  // arrival per warp); no CTA-wide barrier inside the K loop
   __shared__ uint64_t bar[C::NST], emp[C::NST];
-  constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ROWB = (unsigned)(K * sizeof(double));
+  constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ACHB = (unsigned)(C::ACH * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NST; ++i) {
@@ -813,25 +826,16 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     }
     mbar_fence_init();
   }
-  // rows of absent pairs are zero
-  for (int i = threadIdx.x; i < C::ROWS * K; i += blockDim.x) {
-    const int r = i / K;
-    if (r % TP >= cnt) sA_[r * KA + i % K] = 0.0;
-  }
   __syncthreads();
-  // stage A (row r < TP -> a-row of pair s0 + r; row TP + r -> b-row) and chunk 0 of M on bar[0]
-  // (a bulk copy takes uniform operands: one issuing lane per warp, rows spread over the warps)
-  if (threadIdx.x == 0) mbar_expect_tx(&bar[0], 2u * cnt * ROWB + CHB);
-  if (lane == 0) {
-    for (int r = warp; r < 2 * TP; r += C::WARPS)
-      if (r % TP < cnt) bulk_g2s(sA_ + r * KA, Arow + (s0 + r % TP - sA) * 2 * K + (r / TP) * K, ROWB, &bar[0]);
-    if (warp == C::WARPS - 1) bulk_g2s(sB, M, CHB, &bar[0]);
-  }
-  if (threadIdx.x == 0)   // chunks 1 .. NST-2 in flight from the start
-    for (int ch = 1; ch < C::NST - 1 && ch < C::NCH; ++ch) {
-      mbar_expect_tx(&bar[ch], CHB);
-      bulk_g2s(sB + ch * KC * NCS, M + (int64_t)ch * KC * NCS, CHB, &bar[ch]);
-    }
+  auto issue = [&](int ch) {   // thread 0
+    const int b = ch % C::NST;
+    double *st = sst + b * C::STG;
+    mbar_expect_tx(&bar[b], ACHB + CHB);
+    bulk_g2s(st, Ablk + (int64_t)ch * C::ACH, ACHB, &bar[b]);
+    bulk_g2s(st + C::ACH, M + (int64_t)ch * KC * NCS, CHB, &bar[b]);
+  };
+  if (threadIdx.x == 0)   // chunks 0 .. NST-2 in flight from the start
+    for (int ch = 0; ch < C::NST - 1 && ch < C::NCH; ++ch) issue(ch);
   const int ns = warp / C::PG, pg = warp % C::PG;
   double accA[4][C::UQ][2], accB[4][C::UQ][2], accV[C::UV][2];
 #pragma unroll
@@ -840,21 +844,20 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     for (int u = 0; u < C::UQ; ++u) accA[c][u][0] = accA[c][u][1] = accB[c][u][0] = accB[c][u][1] = 0.0;
 #pragma unroll
   for (int u = 0; u < C::UV; ++u) accV[u][0] = accV[u][1] = 0.0;
-  const double *arow = sA_ + (pg * 8 + (lane >> 2)) * KA + (lane & 3), *brow = arow + TP * KA;
-  const int bofs = (lane & 3) * NCS + (lane >> 2);
+  const int ar = pg * 8 + (lane >> 2), sw = C::swz(ar);
+  const int aofs = ar * KC + (lane & 3), bofs = C::ACH + (lane & 3) * NCS + (lane >> 2);
   for (int ch = 0; ch < C::NCH; ++ch) {
-    const int nx = ch + C::NST - 1;   // chunk to issue now, into the buffer chunk ch-1 used
+    const int nx = ch + C::NST - 1;   // chunk to issue now, into the stage chunk ch-1 used
     if (threadIdx.x == 0 && nx < C::NCH) {
-      const int b = nx % C::NST;
-      if (ch >= 1) mbar_wait(&emp[b], ((ch - 1) / C::NST) & 1);
+      if (ch >= 1) mbar_wait(&emp[nx % C::NST], ((ch - 1) / C::NST) & 1);
       fence_proxy_async();
-      mbar_expect_tx(&bar[b], CHB);
-      bulk_g2s(sB + b * KC * NCS, M + (int64_t)nx * KC * NCS, CHB, &bar[b]);
+      issue(nx);
     }
     mbar_wait(&bar[ch % C::NST], (ch / C::NST) & 1);
-    const double *bb = sB + (ch % C::NST) * KC * NCS + bofs;
+    const double *stg = sst + (ch % C::NST) * C::STG;
+    const double *arow = stg + aofs, *brow = arow + TP * KC, *bb = stg + bofs;
     const int zc = 1 + ch / C::CPA;   // axis of this chunk: component axis + 1 has a zero block
-#define RRQ_QCHUNK(Z, N) qmap_chunk<P, Z, N>(arow + ch * KC, brow + ch * KC, bb, accA, accB, accV)
+#define RRQ_QCHUNK(Z, N) qmap_chunk<P, Z, N>(arow, brow, sw, bb, accA, accB, accV)
 #define RRQ_QNS(N) (zc == 1 ? RRQ_QCHUNK(1, N) : zc == 2 ? RRQ_QCHUNK(2, N) : RRQ_QCHUNK(3, N))
     switch (ns) {
       case 0: RRQ_QNS(0); break;

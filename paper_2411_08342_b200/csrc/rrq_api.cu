@@ -717,19 +717,20 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
                            2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair));
   const int64_t cap = std::max<int64_t>(4096, (int64_t)(24e9 / per_pair));
   std::vector<std::pair<int64_t, int64_t>> subs;
-  int64_t maxsub = 0;
+  int64_t maxsub = 0, maxitems = 0;
   for (int64_t P0 = 0; P0 < Pn;) {
     int64_t P1 = P0 + 1;
     while (P1 < Pn && hseg[P1 + 1] - hseg[P0] <= cap) ++P1;
     if (hseg[P1] > hseg[P0]) {
       subs.push_back({P0, P1});
       maxsub = std::max(maxsub, hseg[P1] - hseg[P0]);
+      maxitems = std::max(maxitems, hitem[P1] - hitem[P0]);
     }
     P0 = P1;
   }
   const int nset = (c->overlap && subs.size() > 1) ? 2 : 1;
   for (int b = 0; b < nset; ++b)
-    if (!ensure(c, c->Arow[b], (size_t)maxsub * 2 * D::K * 8) || !ensure(c, c->Xrow[b], (size_t)maxsub * XRow<P>::STRIDE * 8) ||
+    if (!ensure(c, c->Arow[b], (size_t)maxitems * QC::ABLK * 8) || !ensure(c, c->Xrow[b], (size_t)maxsub * XRow<P>::STRIDE * 8) ||
         !ensure(c, c->psetup[b], (size_t)maxsub * sizeof(PairSetup)) ||
         !ensure(c, c->cpair[b], (size_t)maxsub * sizeof(ContractPair)))
       return RRQ_ERR_CUDA;
@@ -771,7 +772,8 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     {
       TScope t1(c, 2, sp);
       k_pair_setup<P><<<nblk(np_, 256), 256, 0, sp>>>(sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase,
-                                                       pair_patch, fit, tg->x, tg->normal, tg->self_node, tg->side, ps, cp);
+                                                       pair_patch, fit, tg->x, tg->normal, tg->self_node, tg->side,
+                                                       bp<int64_t>(c->seg), bp<int64_t>(c->items), it0, ps, cp);
       unsigned grid = (unsigned)std::min<int64_t>((np_ + kWPB * kPPW - 1) / (kWPB * kPPW), (int64_t)c->num_sms * 4);
       k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), sp>>>(
           sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
