@@ -514,8 +514,11 @@ __global__ void __launch_bounds__(WPB * 32)
         if (!conv) {
           const cd dt = cdiv(F, Fp);
           tz = tz - dt;
-          if (cabs_(dt) < 1e-15 * (1.0 + cabs_(tz))) conv = true;
-          else if (it >= 1 && cabs_(dt) < 1e-3 * cabs_(tz) && bernstein_rho(tz.x, tz.y) > 2.0 * rho0)
+          // |dt| < 1e-15 (1 + |t|) and |dt| < 1e-3 |t| compared as squares (no hypot)
+          const double dt2 = dt.x * dt.x + dt.y * dt.y, tz2 = tz.x * tz.x + tz.y * tz.y;
+          const double tza = tz2 > 0 ? tz2 * rsqrt_nr(tz2) : 0.0;
+          if (dt2 < 1e-30 * (1.0 + tza) * (1.0 + tza)) conv = true;
+          else if (it >= 1 && dt2 < 1e-6 * tz2 && bernstein_rho(tz.x, tz.y) > 2.0 * rho0)
             conv = true;   // reading A12': root certainly outside the swap ellipse
         }
         if (__all_sync(0xffffffffu, conv || lane >= 27)) break;
@@ -592,7 +595,7 @@ __global__ void __launch_bounds__(WPB * 32)
         const int e = kap / Q, kk = kap % Q;
         const double *y = blk + L::YL + 3 * kap, *tau = blk + L::TL + 3 * kap;
         const double d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
-        const double dn = sqrt(dot3(d, d));
+        const double d2 = dot3(d, d), idn = rsqrt_nr(d2), dn = d2 * idn;   // |d| > 0: targets are off the edges
         double w1, w3;
         if (ps.swap[e]) {
           double mu1 = 0, mu3 = 0;
@@ -602,16 +605,15 @@ __global__ void __launch_bounds__(WPB * 32)
             mu3 = fma(ps.J[e][c], sU[c * Q + kk], mu3);
           }
           const double ta = stgl[kk] - ps.t0[e][0], tb = ps.t0[e][1];
-          const double r1 = sqrt(ta * ta + tb * tb) / dn;
+          const double tt2 = ta * ta + tb * tb, r1 = tt2 * rsqrt_nr(tt2) * idn;
           w1 = mu1 * r1;
           w3 = mu3 * r1 * r1 * r1;
         } else {
-          const double idn = 1.0 / dn;
           w1 = swgl[kk] * idn;
           w3 = w1 * idn * idn;
           double dxu[3];
           cross3(d, u, dxu);
-          om[0] += swgl[kk] * (-dot3(dxu, tau) / (dn * (dn + dot3(u, d))));
+          om[0] += swgl[kk] * (-dot3(dxu, tau) * rcp_nr(dn * (dn + dot3(u, d))));
         }
         const double nd = dot3(nup, d);
         double txd[3];
@@ -647,15 +649,15 @@ __global__ void __launch_bounds__(WPB * 32)
         const double lo = sdd ? 0.0 : sL, hi = sdd ? sR : 0.0;
         if (!(hi > lo)) continue;
         const double sv = lo + (hi - lo) * (sxo[jj] + 1) * 0.5, W = (hi - lo) * 0.5 * swo[jj];
-        const double ex = exp(sv), iex = 1.0 / ex;
+        const double ex = exp(sv), iex = rcp_nr(ex);
         const double tt = a + b * 0.5 * (ex - iex), dt = b * 0.5 * (ex + iex);
         double x[3], dx[3];
         leg_r3<Q>(C, tt, x, dx);
         const double d[3] = {rp[0] - x[0], rp[1] - x[1], rp[2] - x[2]};
-        const double nd = sqrt(dot3(d, d));
+        const double nd2 = dot3(d, d), nd = nd2 * rsqrt_nr(nd2);
         double dxu[3];
         cross3(d, u, dxu);
-        acc += W * dt * (-dot3(dxu, dx) / (nd * (nd + dot3(u, d))));
+        acc += W * dt * (-dot3(dxu, dx) * rcp_nr(nd * (nd + dot3(u, d))));
       }
       acc = warp_sum(acc);
       if (lane == 0) ps.o0e[e] = acc;
@@ -1319,8 +1321,7 @@ __global__ void __launch_bounds__(256, 2)
         const double *tr = sC[row].x, *tn = sC[row].n;
         const double d0 = tr[0] - xi[0], d1 = tr[1] - xi[1], d2 = tr[2] - xi[2];
         const double r2 = d0 * d0 + d1 * d1 + d2 * d2;
-        double ir = rsqrt(r2);
-        ir = ir * (1.5 - 0.5 * r2 * ir * ir);
+        const double ir = rsqrt_nr(r2);
         const double ir3 = ir * ir * ir;
         const double dn = d0 * ni[0] + d1 * ni[1] + d2 * ni[2];
         const double dnp = d0 * tn[0] + d1 * tn[1] + d2 * tn[2];

@@ -18,8 +18,24 @@ __device__ __forceinline__ cd operator-(cd a, cd b) { return cd{a.x - b.x, a.y -
 __device__ __forceinline__ cd operator*(cd a, cd b) { return cd{a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
 __device__ __forceinline__ cd operator*(double s, cd a) { return cd{s * a.x, s * a.y}; }
 __device__ __forceinline__ cd conj(cd a) { return cd{a.x, -a.y}; }
+// 1/sqrt(x) and 1/x for finite x > 0 (resp. x != 0): the SFU's 64-bit seed (MUFU.RSQ64H / RCP64H, ~2^-22)
+// and two Newton steps (error ~2^-80 before the final rounding): a few DFMAs instead of the IEEE library
+// routines with their slow-path calls.  Results are within 1 ulp of the correctly rounded value.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-x, y, 2.0);
+  return y * fma(-x, y, 2.0);
+}
 __device__ __forceinline__ cd cdiv(cd a, cd b) {
-  double s = 1.0 / (b.x * b.x + b.y * b.y);
+  double s = rcp_nr(b.x * b.x + b.y * b.y);
   return cd{(a.x * b.x + a.y * b.y) * s, (a.y * b.x - a.x * b.y) * s};
 }
 __device__ __forceinline__ double cabs_(cd a) { return hypot(a.x, a.y); }
