@@ -16,21 +16,13 @@
 
 namespace rrq {
 
-__device__ __forceinline__ cd csqrt_(cd z) {
-  double r = hypot(z.x, z.y);
-  if (r == 0) return mk(0, 0);
-  double a = sqrt(0.5 * (r + fabs(z.x)));
-  double b = 0.5 * z.y / a;
-  if (z.x >= 0) return mk(a, b);
-  return mk(fabs(b), z.y >= 0 ? a : -a);
-}
-
-// Bernstein ellipse parameter (reading A5)
+// Bernstein ellipse parameter (reading A5): rho(t) = a + sqrt(a^2 - 1) with a = (|t - 1| + |t + 1|) / 2 the
+// semi-major axis of the confocal ellipse through t (= max |t +- sqrt(t^2 - 1)|), by rsqrt_nr.
+__device__ __forceinline__ double sqrt_nn(double x) { return x > 0 ? x * rsqrt_nr(x) : 0.0; }
 __device__ __forceinline__ double bernstein_rho(double re, double im) {
-  cd t = mk(re, im);
-  cd s = csqrt_(t * t - mk(1.0, 0.0));
-  double r1 = cabs_(t + s), r2 = cabs_(t - s);
-  return fmax(r1, r2);
+  const double y2 = im * im;
+  const double a = 0.5 * (sqrt_nn((re - 1) * (re - 1) + y2) + sqrt_nn((re + 1) * (re + 1) + y2));
+  return a + sqrt_nn(a * a - 1.0);
 }
 
 // Model integrals I_k, J_k (reading A11): upward recurrences, cancellation-free I_0, J_0.
@@ -495,14 +487,14 @@ __global__ void __launch_bounds__(WPB * 32)
         const double xr = v - rc;
         const double g = tri_sum(xr * d1, base3), gp = tri_sum(d1 * d1 + xr * d2, base3);
         go = go && (gp > 0);
-        if (go) tc -= g / gp;
+        if (go) tc -= g * rcp_nr(gp);
       }
       leg_r<Q>(Cl, tc, v, d1, d2);
       const double xr = v - rc;
       const double f = tri_sum(xr * xr, base3), xp2 = tri_sum(d1 * d1, base3);
       double dd = tri_sum(d1 * d1 + xr * d2, base3);
       if (!(dd > 0)) dd = xp2;
-      cd tz = mk(tc, sqrt(f / (dd > 0 ? dd : 1.0)));
+      cd tz = mk(tc, sqrt_nn(f * rcp_nr(dd > 0 ? dd : 1.0)));
       bool conv = !act;
       for (int it = 0; it < 20; ++it) {
         cd xv, xd;
