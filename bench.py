@@ -56,6 +56,11 @@ def traffic_per_launch(kernel, pairs, launches):
         return None, None
     return rec["dram_bytes_per_pair"] * pairs / launches, rec["source"]
 METRIC = "near-correction weights/s (fp64, S/D/S'/D') on 1 B200"
+# BASELINE.md 1a (Table 3): rows/s/core of the paper's RRQ correction build, S and D separately
+PAPER_TABLE3 = {p: {"rows_per_s_per_core_S": s_, "rows_per_s_per_core_D": d_, "hardware": "1 core, AMD EPYC 9474F 3.60 GHz",
+                    "source": "PAPER.md Table 3 (P:L1921-1938)"}
+                for p, s_, d_ in ((4, 21285, 27212), (6, 15065, 21376), (8, 9921, 15017), (10, 6621, 10449),
+                                  (12, 4324, 6845), (14, 2907, 4534))}
 UNIT = "weights/s"
 
 
@@ -317,6 +322,10 @@ def run_ours(args, ws, rank):
         "pairs_per_s": npairs * args.steps / (ms_max / 1e3) * ws,
         "rows_per_s": R.T * args.steps / (ms_max / 1e3) * ws,
         "swap_edges_per_pair": swap_per_pair,
+        # context, not the target: the paper's correction-build throughput for this p (Table 3, P:L1921-1938;
+        # one core of a 3.60 GHz AMD EPYC 9474F, Fortran; on-surface targets of a stellarator; S and D
+        # built separately) in points (rows) per second per core
+        "paper_context": PAPER_TABLE3.get(R.S.p),
         "clocks": clocks,
         "gpu_launches": int(launches),
         "gen_s": gen_s,
@@ -437,10 +446,28 @@ def cpu_baseline(cfg, args, R=None, steps=1):
         O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa)
     el = (time.time() - t0) / steps
     w = tg.shape[0] * S.n * 4
-    return {"value": w / el, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{tg.shape[0]} pairs = all near pairs of {npatch} random patches of {cfg['name']} "
-                      f"(Steps 1-8 incl. per-patch fit, all 4 kernels), {el:.1f} s on {cores} OpenMP threads",
-            "seconds": el, "pairs": int(tg.shape[0])}
+    res = {"value": w / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{tg.shape[0]} pairs = all near pairs of {npatch} random patches of {cfg['name']} "
+                     f"(Steps 1-8 incl. per-patch fit, all 4 kernels), {el:.1f} s on {cores} OpenMP threads",
+           "seconds": el, "pairs": int(tg.shape[0])}
+    # like-for-like with the paper's single-core numbers: the first patch's pairs on one thread
+    try:
+        import ctypes
+        gomp = ctypes.CDLL("libgomp.so.1")
+        n1 = min(3000, len(pa))
+        gomp.omp_set_num_threads(1)
+        t1 = time.time()
+        O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg[:n1], pa[:n1])
+        e1 = time.time() - t1
+        gomp.omp_set_num_threads(cores)
+        rows1 = np.unique(tg[:n1]).size
+        res["one_core"] = {"value": n1 * S.n * 4 / e1, "unit": UNIT, "pairs": n1, "seconds": e1,
+                           "pairs_per_s": n1 / e1,
+                           "rows_per_s_equiv": n1 / e1 / (tg.shape[0] / max(np.unique(tg).size, 1)),
+                           "sample": f"first {n1} pairs of the sample ({rows1} distinct targets), 1 OpenMP thread"}
+    except OSError as ex:
+        res["one_core"] = {"error": repr(ex)}
+    return res
 
 
 def run_reference(args, ws, rank):
