@@ -72,7 +72,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n-off", type=int, default=None, help="override off-surface target count (debug)")
-    ap.add_argument("--freq", type=int, default=None, help="override icosphere frequency (debug)")
+    ap.add_argument("--freq", type=str, default=None,
+                    help="override the mesh: icosphere frequency (configs 2, 4), or NTHxNPH / NUxNV (configs 3, 6)")
     ap.add_argument("--chunk-pairs", type=int, default=16_000_000)
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
@@ -175,7 +176,7 @@ def make_inputs(args, rank):
     if args.n_off is not None:
         kw["n_off"] = args.n_off
     if args.freq is not None:
-        kw["freq"] = args.freq
+        kw["freq"] = tuple(int(v) for v in args.freq.split("x")) if "x" in args.freq else int(args.freq)
     return make_config(args.config, seed_offset=rank, **kw)
 
 
@@ -183,7 +184,16 @@ def cfg_desc(cfg, npairs, T):
     S = cfg["surface"]
     return {"workload": cfg["name"], "patches": int(S.n_patches), "p": int(S.p), "p_edge": int(S.q),
             "nodes": int(S.n_patches * S.n), "targets": int(T), "pairs": int(npairs) if npairs is not None else None, "eta": cfg["eta"],
-            "kernels": "S,D,Sp,Dp", "l2": "inputs+outputs > L2 (fit 22 GB, CSR ~300 GB per step): no flush needed"}
+            "kernels": "S,D,Sp,Dp", "l2": _l2_note(S, npairs)}
+
+
+def _l2_note(S, npairs):
+    """Inputs/outputs against the 126 MB L2: the bench never flushes, so say whether it needs to."""
+    fit_gb = S.n_patches * 8.0 * (13 * S.p * (S.p + 1) // 2 * S.n + 9 * 2 * S.p * 12 * S.p * (S.p + 1)) / 1e9
+    csr_gb = (npairs or 0) * S.n * 36 / 1e9
+    big = fit_gb + csr_gb > 0.5
+    return (f"inputs+outputs > L2 (fit ~{fit_gb:.1f} GB, CSR ~{csr_gb:.0f} GB per step): no flush needed" if big
+            else f"small workload (fit ~{fit_gb:.2f} GB, CSR ~{csr_gb:.2f} GB): L2-resident, not a bench config")
 
 
 class Runner:

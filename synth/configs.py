@@ -8,10 +8,10 @@ import math
 import numpy as np
 import torch
 
-from .geometry import (make_sphere_surface, make_torus_surface, make_cap_surface,
+from .geometry import (make_sphere_surface, make_torus_surface, make_cap_surface, make_stellarator_surface,
                        bumpy_radius_fn, _eval_map, _radial_map)
 
-CONFIG_SEEDS = {c: 2411083420 + c for c in range(1, 6)}
+CONFIG_SEEDS = {c: 2411083420 + c for c in range(1, 7)}
 
 
 def patch_h(S):
@@ -146,4 +146,16 @@ def make_config(cfg, n_off=None, include_nodes=True, freq=None, p=None, seed_off
         x = qd * (1.0 + sides * d)[:, None]
         parts = [(x, qd.copy(), np.full(cnt, -1, np.int64), sides.astype(np.int8))]
         return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=float("inf"), all_pairs=True, name="cfg5-cap-p10"))
+    if cfg == 6:
+        # SURVEY §8(f) NEXT(1), the paper's solve-phase throughput workload (E3): the
+        # stellarator of eq (stellarator), n_u x n_v rectangles halved, on-surface node targets only
+        # (Table 3's X_RRQ = N / T_RRQ counts all discretisation points); n_off adds off-surface targets
+        pp = p or 8
+        nu_, nv_ = (16, 48) if freq is None else freq
+        S = make_stellarator_surface(nu_, nv_, pp, 2 * pp)
+        parts = [node_targets(S)] if include_nodes else []
+        if n_off:
+            parts.append(offsurface_normal_targets(S, rng, n_off, lambda r, c: r.uniform(-12.0, 0.0, c)))
+        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False,
+                                        name=f"cfg6-stellarator{S.n_patches}-p{pp}"))
     raise ValueError(cfg)

@@ -245,6 +245,45 @@ def make_torus_surface(R, r, n_theta, n_phi, p, q):
     return S
 
 
+# Stellarator of PAPER eq (stellarator): r(u, v) = sum_{i=-1..2} sum_{j=-1..1} delta_ij
+# [cos v cos((1-i)u + jv), sin v cos((1-i)u + jv), sin((1-i)u + jv)], (u, v) in [0, 2 pi]^2.
+STELLARATOR_DELTA = {(-1, -1): 0.17, (-1, 0): 0.11, (0, 0): 1.0, (1, 0): 4.5, (2, 0): -0.25, (0, 1): 0.07,
+                     (2, 1): -0.45}
+
+
+def make_stellarator_surface(n_u, n_v, p, q):
+    """The paper's stellarator, the parameter square split into n_u x n_v equal rectangles, each halved
+    (P:L1856-1858).  v is the toroidal (major) angle, u the poloidal one; parameter order (v, u) makes
+    X_v x X_u the outward normal (checked by tests/test_oracle_stellarator.py: enclosed volume > 0)."""
+    dv = 2 * np.pi / n_v
+    du = 2 * np.pi / n_u
+    pd = []
+    for i in range(n_v):
+        for j in range(n_u):
+            LL = (i * dv, j * du)
+            LR = ((i + 1) * dv, j * du)
+            UR = ((i + 1) * dv, (j + 1) * du)
+            UL = (i * dv, (j + 1) * du)
+            pd.append(LL + LR + UR)
+            pd.append(LL + UR + UL)
+    pdata = torch.as_tensor(np.array(pd, dtype=np.float64))
+
+    def fmap(pdt, s, t):
+        P0, P1, P2 = pdt[:, 0:2], pdt[:, 2:4], pdt[:, 4:6]
+        ab = P0 + s[:, None] * (P1 - P0) + t[:, None] * (P2 - P0)
+        v, u = ab[:, 0], ab[:, 1]
+        x = torch.zeros_like(v); y = torch.zeros_like(v); z = torch.zeros_like(v)
+        for (i, j), d in STELLARATOR_DELTA.items():
+            ang = (1 - i) * u + j * v
+            c = torch.cos(ang)
+            x = x + d * torch.cos(v) * c
+            y = y + d * torch.sin(v) * c
+            z = z + d * torch.sin(ang)
+        return torch.stack([x, y, z], 1)
+
+    return build_surface(fmap, pdata, p, q, kind="stellarator")
+
+
 def make_flat_surface(tris, p, q):
     """Flat triangles [P,3,3] with the affine map (test geometry)."""
     pdata = torch.as_tensor(np.asarray(tris, np.float64).reshape(-1, 9))
