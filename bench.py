@@ -249,6 +249,7 @@ class Runner:
             if on_chunk is not None:
                 on_chunk("after", i, o, int(hptr[r1] - hptr[r0]))
         self.npairs = int(hptr[-1])
+        self.n_close = int((np.diff(hptr) > 0).sum())   # targets with at least one near patch
         self.fit = fit
         return self.npairs
 
@@ -331,6 +332,9 @@ def run_ours(args, ws, rank):
         "stages_ms_per_step": {k: v / args.steps for k, v in tim["ms"].items()},
         "pairs_per_s": npairs * args.steps / (ms_max / 1e3) * ws,
         "rows_per_s": R.T * args.steps / (ms_max / 1e3) * ws,
+        # the paper's throughput unit for the evaluation phase: close targets (rows with a correction) per
+        # second, X_RRQ = N_T^c / T_RRQ
+        "close_rows_per_s": R.n_close * args.steps / (ms_max / 1e3) * ws,
         "swap_edges_per_pair": swap_per_pair,
         # context, not the target: the paper's correction-build throughput for this p (Table 3, P:L1921-1938;
         # one core of a 3.60 GHz AMD EPYC 9474F, Fortran; on-surface targets of a stellarator; S and D

@@ -9,9 +9,10 @@ import numpy as np
 import torch
 
 from .geometry import (make_sphere_surface, make_torus_surface, make_cap_surface, make_stellarator_surface,
+                       make_interlocked_tori, inside_interlocked_tori,
                        bumpy_radius_fn, _eval_map, _radial_map)
 
-CONFIG_SEEDS = {c: 2411083420 + c for c in range(1, 7)}
+CONFIG_SEEDS = {c: 2411083420 + c for c in range(1, 8)}
 
 
 def patch_h(S):
@@ -158,4 +159,21 @@ def make_config(cfg, n_off=None, include_nodes=True, freq=None, p=None, seed_off
             parts.append(offsurface_normal_targets(S, rng, n_off, lambda r, c: r.uniform(-12.0, 0.0, c)))
         return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False,
                                         name=f"cfg6-stellarator{S.n_patches}-p{pp}"))
+    if cfg == 7:
+        # SURVEY §8(f) NEXT(2), the paper's evaluation-phase workload (E4): four interlocking
+        # tori (a = 3, b = 0.5, 4.95 apart), each n_theta x n_phi rectangles halved, and the exterior points
+        # of a uniform G^3 grid over the box [-5,20] x [-6,6]^2 with G = 1 + 100 n_theta / 6 (the paper's
+        # pairing 6x36 <-> 101^3 ... 24x144 <-> 401^3).  No target normals (u itself: S and D; S', D' rows are
+        # then zero).  Close targets are those the near rule (A6) pairs with some patch.
+        pp = p or 8
+        nth, nph = (6, 36) if freq is None else freq
+        S = make_interlocked_tori(nth, nph, pp, 2 * pp)
+        G = int(round(1 + 100 * nth / 6)) if n_off is None else int(n_off)
+        gx = np.linspace(-5.0, 20.0, G); gy = np.linspace(-6.0, 6.0, G)
+        X = np.stack(np.meshgrid(gx, gy, gy, indexing="ij"), -1).reshape(-1, 3)
+        X = X[~inside_interlocked_tori(X)]
+        cnt = X.shape[0]
+        parts = [(X, np.zeros_like(X), np.full(cnt, -1, np.int64), np.ones(cnt, np.int8))]
+        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False,
+                                        name=f"cfg7-tori{S.n_patches}-grid{G}-p{pp}"))
     raise ValueError(cfg)

@@ -284,6 +284,53 @@ def make_stellarator_surface(n_u, n_v, p, q):
     return build_surface(fmap, pdata, p, q, kind="stellarator")
 
 
+def make_interlocked_tori(n_theta, n_phi, p, q, count=4, a=3.0, b=0.5, shift=4.95):
+    """The evaluation-phase boundary of PAPER §5: `count` copies of the torus eq (eq:torus)
+    with a = 3, b = 0.5 (omega_c = 0), torus k translated by k * shift along x and, for odd k, rotated by
+    90 degrees about the x axis, so adjacent tori interlock with a 0.05 gap (shift 4.95).  Each torus is
+    n_theta x n_phi rectangles halved (the same split as make_torus_surface)."""
+    dphi = 2 * np.pi / n_phi
+    dth = 2 * np.pi / n_theta
+    pd = []
+    for k in range(count):
+        for i in range(n_phi):
+            for j in range(n_theta):
+                LL = (i * dphi, j * dth)
+                LR = ((i + 1) * dphi, j * dth)
+                UR = ((i + 1) * dphi, (j + 1) * dth)
+                UL = (i * dphi, (j + 1) * dth)
+                pd.append(LL + LR + UR + (k,))
+                pd.append(LL + UR + UL + (k,))
+    pdata = torch.as_tensor(np.array(pd, dtype=np.float64))
+
+    def fmap(pdt, s, t):
+        P0, P1, P2 = pdt[:, 0:2], pdt[:, 2:4], pdt[:, 4:6]
+        ab = P0 + s[:, None] * (P1 - P0) + t[:, None] * (P2 - P0)
+        ph, th = ab[:, 0], ab[:, 1]
+        rho = a + b * torch.cos(th)
+        x, y, z = rho * torch.cos(ph), rho * torch.sin(ph), b * torch.sin(th)
+        odd = (pdt[:, 6] % 2) == 1
+        # rotation by +90 degrees about x for odd k: (x, y, z) -> (x, -z, y)
+        y2 = torch.where(odd, -z, y)
+        z2 = torch.where(odd, y, z)
+        return torch.stack([x + shift * pdt[:, 6], y2, z2], 1)
+
+    return build_surface(fmap, pdata, p, q, kind="tori")
+
+
+def inside_interlocked_tori(x, count=4, a=3.0, b=0.5, shift=4.95):
+    """True where x lies inside (or on) one of the tori of make_interlocked_tori."""
+    x = np.asarray(x, np.float64)
+    inside = np.zeros(x.shape[0], bool)
+    for k in range(count):
+        px, py, pz = x[:, 0] - shift * k, x[:, 1], x[:, 2]
+        if k % 2 == 1:   # undo the rotation: (x, y, z) = (x0, -z0, y0) -> z0 = -y, y0 = z
+            py, pz = pz, -py
+        dc = np.sqrt(px ** 2 + py ** 2) - a
+        inside |= dc ** 2 + pz ** 2 <= b * b
+    return inside
+
+
 def make_flat_surface(tris, p, q):
     """Flat triangles [P,3,3] with the affine map (test geometry)."""
     pdata = torch.as_tensor(np.asarray(tris, np.float64).reshape(-1, 9))
