@@ -137,6 +137,16 @@ rrq_status rrq_build_correction(rrq_ctx ctx, const rrq_surface *surf, const rrq_
 rrq_status rrq_apply_correction(rrq_ctx ctx, int64_t n_rows, const int64_t *row_ptr, const int32_t *col_idx,
                                 const double *vals, const double *density, double *y, rrq_stream_t stream);
 
+/* y[t] += alpha S_smooth[density](x_t) + beta D_smooth[density](x_t): the smooth rule of the splitting
+ * over all surface nodes j except self_node[t] (reading A14),
+ *   S_smooth = sum_j w_j density_j / (4 pi |x_t - x_j|),  D_smooth = sum_j w_j density_j (x_t - x_j).n_j / (4 pi |x_t - x_j|^3),
+ * so that smooth + correction (rrq_apply_correction) is the discretised operator (used by the
+ * combined-field solve).  Direct sum, O(n_targets x nodes) (no FMM).  tx [n_targets][3] and
+ * self_node [n_targets] (or NULL) device arrays; density [nodes], y [n_targets] device fp64 (y accumulated). */
+rrq_status rrq_apply_smooth(rrq_ctx ctx, int64_t n_targets, const double *tx, const int64_t *self_node,
+                            const rrq_surface *surf, double alpha, double beta, const double *density, double *y,
+                            rrq_stream_t stream);
+
 /* Test hook: copy the host-built constant tables (GL nodes t[q], weights w[q], U[q][q] row-major)
  * into HOST arrays.  Lets tests check they are bit-identical to the oracle's. */
 rrq_status rrq_get_tables(rrq_ctx ctx, double *t, double *w, double *U);

@@ -9,7 +9,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librrq.so")
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(CSRC, f) for f in ("rrq_api.cu", "rrq_tables.cpp", "rrq_device.cuh", "k_build.cuh",
-                                           "k_near.cuh", "k_patch.cuh")] + [os.path.join(ROOT, "include", "rrq.h")]
+                                           "k_near.cuh", "k_patch.cuh", "k_smooth.cuh")] + [os.path.join(ROOT, "include", "rrq.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -97,7 +97,7 @@ struct QRow {
 // Q^{(j,k)} S'^{(l-j, m-k)} of all WD outputs at once (k from the smallest to the largest k any output of
 // the block takes).  Along the sweep output m0 + i needs S'^{(l-j, m0+i-k)}, i.e. the entry output m0 took
 // i steps earlier: a window of WD S' entries in registers, one new entry per step.
-__host__ __device__ constexpr int tr_wd(int P) { return P <= 4 ? 4 : (P <= 6 ? 3 : (P <= 8 ? 4 : 5)); }
+__host__ __device__ constexpr int tr_wd(int P) { return P <= 4 ? 4 : (P <= 6 ? 3 : (P <= 8 ? 3 : 5)); }
 __host__ __device__ constexpr int tr_block_len(int l, int m0, int wd) {
   int n = 0;
   const int m1 = (m0 + wd - 1 < l) ? m0 + wd - 1 : l;

@@ -13,6 +13,7 @@
 #include "k_build.cuh"
 #include "k_near.cuh"
 #include "k_patch.cuh"
+#include "k_smooth.cuh"
 
 namespace rrq_host {
 void gauss_legendre(int n, double *x, double *w);
@@ -839,7 +840,8 @@ rrq_status rrq_build_correction(rrq_ctx c, const rrq_surface *s, const rrq_targe
   if (!c) return RRQ_ERR_INVALID_ARG;
   rrq_status r;
   if ((r = check_surface(c, s)) || (r = check_targets(c, tg))) return r;
-  if (!pair_ptr || !pair_patch || !fit || !vals) return fail(c, RRQ_ERR_INVALID_ARG, "pair_ptr, pair_patch, fit, vals must be non-NULL");
+  if (!pair_ptr || (!pair_patch && n_pairs > 0) || !fit || !vals)
+    return fail(c, RRQ_ERR_INVALID_ARG, "pair_ptr, pair_patch (unless n_pairs == 0), fit, vals must be non-NULL");
   if (row_begin < 0 || row_end < row_begin || row_end > tg->n_targets)
     return fail(c, RRQ_ERR_INVALID_ARG, "row range must satisfy 0 <= row_begin <= row_end <= n_targets");
   if (n_pairs < 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_pairs < 0");
@@ -860,6 +862,23 @@ rrq_status rrq_build_correction(rrq_ctx c, const rrq_surface *s, const rrq_targe
     case 10: return build_impl<10>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
   }
   return RRQ_ERR_NOT_IMPLEMENTED;
+}
+
+rrq_status rrq_apply_smooth(rrq_ctx c, int64_t n_targets, const double *tx, const int64_t *self_node,
+                            const rrq_surface *s, double alpha, double beta, const double *density, double *y,
+                            rrq_stream_t stream) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  rrq_status r;
+  if ((r = check_surface(c, s))) return r;
+  if (n_targets < 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_targets < 0");
+  if (n_targets == 0) return RRQ_OK;
+  if (!tx || !density || !y) return fail(c, RRQ_ERR_INVALID_ARG, "NULL array");
+  const int64_t ns = s->n_patches * (int64_t)c->prm.n_nodes;
+  k_smooth_apply<<<nblk(n_targets, 256), 256, 0, (cudaStream_t)stream>>>(n_targets, tx, self_node, ns, s->nodes,
+                                                                          s->normals, s->weights, density, alpha,
+                                                                          beta, y);
+  c->launches++;
+  return cuda_check(c, "rrq_apply_smooth");
 }
 
 rrq_status rrq_apply_correction(rrq_ctx c, int64_t n_rows, const int64_t *row_ptr, const int32_t *col_idx,

@@ -64,6 +64,9 @@ def load_library():
     lib.rrq_build_correction.restype = ctypes.c_int
     lib.rrq_apply_correction.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
     lib.rrq_apply_correction.restype = ctypes.c_int
+    lib.rrq_apply_smooth.argtypes = [vp, i64, vp, vp, ctypes.POINTER(_Surface), ctypes.c_double, ctypes.c_double,
+                                     vp, vp, vp]
+    lib.rrq_apply_smooth.restype = ctypes.c_int
     lib.rrq_get_tables.argtypes = [vp, vp, vp, vp]
     lib.rrq_get_tables.restype = ctypes.c_int
     lib.rrq_launch_count.argtypes = [vp]
@@ -242,6 +245,15 @@ class RRQ:
             _ptr(out["col_idx"]) if out.get("col_idx") is not None else None, ctypes.byref(vp4),
             _ptr(out["status"]) if out.get("status") is not None else None, _stream()), "rrq_build_correction")
         return out
+
+    def apply_smooth(self, surf, tx, self_node, density, y, alpha=1.0, beta=0.0):
+        """y += alpha S_smooth[density] + beta D_smooth[density] at targets tx (self node skipped)."""
+        self._check(self.lib.rrq_apply_smooth(self.h, tx.shape[0], _ptr(tx, torch.float64, "tx"),
+                                              _ptr(self_node, torch.int64, "self_node"), ctypes.byref(surf.c),
+                                              float(alpha), float(beta), _ptr(density, torch.float64, "density"),
+                                              _ptr(y, torch.float64, "y"), _stream()),
+                    "rrq_apply_smooth")
+        return y
 
     def apply_correction(self, row_ptr, col_idx, vals, density, y):
         self._check(self.lib.rrq_apply_correction(self.h, row_ptr.numel() - 1, _ptr(row_ptr, torch.int64),
