@@ -424,40 +424,99 @@ __global__ void __launch_bounds__(WPB * 32)
       }
     }
     __syncwarp();
-    // solid harmonics of the warp's pairs: lanes (pair, column m)
-    for (int i = lane; i < kPPW * (P + 1); i += 32) {
-      PairState<P> &ps = mine[i / (P + 1)];
-      if (ps.active) r_column<P>(ps.rp[1], ps.rp[2], ps.rp[0], i % (P + 1), ps.R, shc);
-    }
-    __syncwarp();
-    // gradient tables (kept for phase 5), then the translation operands S', NG' (XRow): flat over pairs
-    for (int i = lane; i < kPPW * NS; i += 32) {
-      const int pp = i / NS, e = i % NS;
-      if (!mine[pp].active) continue;
-      int l = 0;
-      while (sidx(l + 1, 0) <= e) ++l;
-      grad_fast(mine[pp].R, l, e - sidx(l, 0), shc, wsc.GS[pp][e]);
-    }
-    __syncwarp();
-    constexpr int NSX = sidx(P, 0);   // l' < p
-    for (int i = lane; i < kPPW * NSX; i += 32) {
-      const int pp = i / NSX, e = i % NSX;
+    if constexpr (kPPW * (P + 1) <= 32) {
+      // lane = (pair, column m): R_l^m of its column in registers (the r_column recurrence), the
+      // neighbour columns m +- 1 by shuffles for grad S^{(l,m)} (grad_fast's rules), then straight away the
+      // translation operands S', NG' of (l, +-m) (XRow) and the R / grad tables phase 5 reads
+      const int pp = lane / (P + 1) < kPPW ? lane / (P + 1) : kPPW - 1, m = lane % (P + 1);
+      const bool in = lane < kPPW * (P + 1);
       PairState<P> &ps = mine[pp];
-      if (!ps.active) continue;
-      int l = 0;
-      while (sidx(l + 1, 0) <= e) ++l;
-      const int m = e - sidx(l, 0);
-      const cd *g = wsc.GS[pp][e];
-      const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
-      const double w = __ldg(wS + l * l + l + m);
-      double2 *o = reinterpret_cast<double2 *>(Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m));
-      o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
-      o[1] = make_double2(w * ng.y, w * ng.x);
-      if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
-        const double sg = (m & 1) ? -w : w;
-        o -= 4 * m;
-        o[0] = make_double2(-sg * r.y, sg * r.x);
-        o[1] = make_double2(-sg * ng.y, sg * ng.x);
+      const bool act = in && ps.active;
+      const double X = ps.rp[1], Y = ps.rp[2], Z = ps.rp[0], r2 = X * X + Y * Y + Z * Z;
+      cd rmm = mk(1.0, 0.0);
+      for (int k = 1; k <= m; ++k) rmm = shc[HC_DG + k] * (mk(X, Y) * rmm);
+      cd Rc[P + 1];
+#pragma unroll
+      for (int l = 0; l <= P; ++l) {
+        cd v = mk(0.0, 0.0);
+        if (l == m) v = rmm;
+        else if (l == m + 1) v = shc[HC_SB + m] * Z * rmm;
+        else if (l > m + 1)
+          v = (shc[HC_RA + sidx(l - 1, m)] * Z) * Rc[l - 1] - (shc[HC_RB + sidx(l - 1, m)] * r2) * Rc[l - 2];
+        Rc[l] = act ? v : mk(0.0, 0.0);
+        if (act && l >= m) ps.R[sidx(l, m)] = Rc[l];
+      }
+      const double nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
+      double2 *xo = reinterpret_cast<double2 *>(Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE + XR::SX);
+      const bool last = m == P;
+#pragma unroll
+      for (int l = 0; l <= P; ++l) {
+        cd g[3] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
+        if (l >= 1) {
+          const cd r0 = Rc[l - 1];
+          cd rp = mk(__shfl_down_sync(0xffffffffu, r0.x, 1), __shfl_down_sync(0xffffffffu, r0.y, 1));
+          cd rm = mk(__shfl_up_sync(0xffffffffu, r0.x, 1), __shfl_up_sync(0xffffffffu, r0.y, 1));
+          if (last) rp = mk(0.0, 0.0);               // R^{m+1} with m + 1 > l - 1
+          if (m == 0) rm = mk(-rp.x, rp.y);          // R_{l-1}^{-1} = -conj R_{l-1}^{1}
+          const double *dc = shc + HC_DC + 3 * (l * l + l + m);
+          g[0] = dc[0] * r0;
+          g[1] = 0.5 * (dc[2] * rm - dc[1] * rp);
+          const cd t = 0.5 * (dc[1] * rp + dc[2] * rm);
+          g[2] = mk(-t.y, t.x);
+        }
+        if (!act || l < m) continue;
+        cd *gs = wsc.GS[pp][sidx(l, m)];
+        gs[0] = g[0]; gs[1] = g[1]; gs[2] = g[2];
+        if (l < P) {   // translation operands, l' < p
+          const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2], r = Rc[l];
+          const double w = __ldg(wS + l * l + l + m);
+          double2 *o = xo + 2 * (l * l + l + m);
+          o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
+          o[1] = make_double2(w * ng.y, w * ng.x);
+          if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
+            const double sg = (m & 1) ? -w : w;
+            o -= 4 * m;
+            o[0] = make_double2(-sg * r.y, sg * r.x);
+            o[1] = make_double2(-sg * ng.y, sg * ng.x);
+          }
+        }
+      }
+    } else {
+      // solid harmonics of the warp's pairs: lanes (pair, column m)
+      for (int i = lane; i < kPPW * (P + 1); i += 32) {
+        PairState<P> &ps = mine[i / (P + 1)];
+        if (ps.active) r_column<P>(ps.rp[1], ps.rp[2], ps.rp[0], i % (P + 1), ps.R, shc);
+      }
+      __syncwarp();
+      // gradient tables (kept for phase 5), then the translation operands S', NG' (XRow): flat over pairs
+      for (int i = lane; i < kPPW * NS; i += 32) {
+        const int pp = i / NS, e = i % NS;
+        if (!mine[pp].active) continue;
+        int l = 0;
+        while (sidx(l + 1, 0) <= e) ++l;
+        grad_fast(mine[pp].R, l, e - sidx(l, 0), shc, wsc.GS[pp][e]);
+      }
+      __syncwarp();
+      constexpr int NSX = sidx(P, 0);   // l' < p
+      for (int i = lane; i < kPPW * NSX; i += 32) {
+        const int pp = i / NSX, e = i % NSX;
+        PairState<P> &ps = mine[pp];
+        if (!ps.active) continue;
+        int l = 0;
+        while (sidx(l + 1, 0) <= e) ++l;
+        const int m = e - sidx(l, 0);
+        const cd *g = wsc.GS[pp][e];
+        const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
+        const double w = __ldg(wS + l * l + l + m);
+        double2 *o = reinterpret_cast<double2 *>(Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m));
+        o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
+        o[1] = make_double2(w * ng.y, w * ng.x);
+        if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
+          const double sg = (m & 1) ? -w : w;
+          o -= 4 * m;
+          o[0] = make_double2(-sg * r.y, sg * r.x);
+          o[1] = make_double2(-sg * ng.y, sg * ng.x);
+        }
       }
     }
     if (lane < 3 * kPPW && mine[lane / 3].active)
