@@ -599,7 +599,9 @@ double orc_bernstein_rho(double re, double im);
  * Returns 1 if converged.  Im t0 >= 0.  Reading A12': the iteration also stops (as converged) once,
  * after at least one complex step, the step is below 1e-3 |t| and rho(t) > rho_stop (= 2 rho0): the
  * root is then certainly outside the swap ellipse, so the regime decision is already fixed and t0 is
- * not used by the plain rule. */
+ * not used by the plain rule.  Reading A12'': it also stops once the iteration is in its quadratic
+ * regime (|dt| < 0.1 |dt_prev|) and the predicted next step C |dt|^2, C ~ |dt| / |dt_prev|^2, is below the
+ * tolerance 1e-15 (1 + |t|): the updated t is then already converged (Newton's quadratic convergence). */
 int orc_find_t0(const double *C, int q, const double *rp, double rho_stop, double *t0re, double *t0im) {
   cplx x[3], dx[3], ddx[3];
   /* chord projection */
@@ -633,6 +635,7 @@ int orc_find_t0(const double *C, int q, const double *rp, double rho_stop, doubl
   if (!(dd > 0)) dd = xp2;
   cplx t = tc + I * sqrt(f / dd);
   int conv = 0;
+  double dprev = 0.0;
   for (int it = 0; it < 20; ++it) {
     edge_eval(C, q, t, x, dx, ddx);
     cplx F = 0, Fp = 0;
@@ -643,8 +646,11 @@ int orc_find_t0(const double *C, int q, const double *rp, double rho_stop, doubl
     }
     cplx dt = F / Fp;
     t -= dt;
-    if (cabs(dt) < 1e-15 * (1.0 + cabs(t))) { conv = 1; break; }
-    if (it >= 1 && cabs(dt) < 1e-3 * cabs(t) && orc_bernstein_rho(creal(t), cimag(t)) > rho_stop) { conv = 1; break; }
+    const double ad = cabs(dt), tol = 1e-15 * (1.0 + cabs(t));
+    if (ad < tol) { conv = 1; break; }
+    if (dprev > 0 && ad < 0.1 * dprev && ad * ad * ad < tol * dprev * dprev) { conv = 1; break; }   /* A12'' */
+    if (it >= 1 && ad < 1e-3 * cabs(t) && orc_bernstein_rho(creal(t), cimag(t)) > rho_stop) { conv = 1; break; }
+    dprev = ad;
   }
   if (cimag(t) < 0) t = conj(t);
   *t0re = creal(t);

@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(WPB * 32)
       if (!(dd > 0)) dd = xp2;
       cd tz = mk(tc, sqrt_nn(f * rcp_nr(dd > 0 ? dd : 1.0)));
       bool conv = !act;
+      double dt2_prev = 0.0;
       for (int it = 0; it < 20; ++it) {
         cd xv, xd;
         leg_c<Q>(Cl, tz, xv, xd);
@@ -568,9 +569,15 @@ __global__ void __launch_bounds__(WPB * 32)
           // |dt| < 1e-15 (1 + |t|) and |dt| < 1e-3 |t| compared as squares (no hypot)
           const double dt2 = dt.x * dt.x + dt.y * dt.y, tz2 = tz.x * tz.x + tz.y * tz.y;
           const double tza = tz2 > 0 ? tz2 * rsqrt_nr(tz2) : 0.0;
-          if (dt2 < 1e-30 * (1.0 + tza) * (1.0 + tza)) conv = true;
+          const double tol2 = 1e-30 * (1.0 + tza) * (1.0 + tza);
+          if (dt2 < tol2) conv = true;
+          // quadratic convergence: the step after this one is ~C |dt|^2 with C ~ |dt| / |dt_prev|^2, so
+          // once (|dt|^3 / |dt_prev|^2)^2 < tol^2 the updated t is already within the tolerance (saves the
+          // confirming iteration; t agrees with the full iteration to rounding)
+          else if (dt2_prev > 0 && dt2 < 1e-2 * dt2_prev && dt2 * dt2 * dt2 < tol2 * dt2_prev * dt2_prev) conv = true;
           else if (it >= 1 && dt2 < 1e-6 * tz2 && bernstein_rho(tz.x, tz.y) > 2.0 * rho0)
             conv = true;   // reading A12': root certainly outside the swap ellipse
+          dt2_prev = dt2;
         }
         if (__all_sync(0xffffffffu, conv || lane >= 27)) break;
       }
