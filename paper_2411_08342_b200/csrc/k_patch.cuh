@@ -143,54 +143,98 @@ __global__ void k_patch_geom(int64_t n_patches, const double *__restrict__ nodes
 // k_qmap stores its accumulators as they are.
 // One thread per (patch, edge node); it owns rows 3 kappa .. 3 kappa + 2.
 template <int P>
-__global__ void k_edge_tables(int64_t n_patches, const double *__restrict__ hc, const double *__restrict__ vlam,
-                              const double *__restrict__ vth, double *__restrict__ fit) {
+struct EdgeTabCfg {
+  using D = Dims<P>;
+  static constexpr int NB = 8;                                   // edge nodes per round
+  static constexpr int THREADS = 128;
+  // shared: per node of the round: R [NS] | GS [NS][3] | H [NQ][3] | EV [NV][3] (complex), y, tau
+  static constexpr int NODE = (D::NS + 3 * D::NS + 3 * D::NQ + 3 * D::NV) * 2 + 6;
+  static constexpr size_t SMEM = (size_t)NB * NODE * sizeof(double);
+};
+
+// CTA per patch, rounds of NB edge nodes: thread per node builds R (r_table) and the gradient table in
+// shared memory, threads over (node, (j,k)) build g = Hess S tau and e = grad S x tau, then the CTA writes
+// the NB x 3 rows of M column-fastest (coalesced whole rows; zero blocks and padding included).
+template <int P>
+__global__ void __launch_bounds__(EdgeTabCfg<P>::THREADS) k_edge_tables(int64_t n_patches, const double *__restrict__ hc,
+                                                                        const double *__restrict__ vlam,
+                                                                        const double *__restrict__ vth,
+                                                                        double *__restrict__ fit) {
   using D = Dims<P>;
   using L = Layout<P>;
-  int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= n_patches * D::E) return;
-  int64_t Pp = gid / D::E;
-  int kap = gid % D::E;
+  using C = EdgeTabCfg<P>;
+  constexpr int NS = D::NS, NQ = D::NQ, NV = D::NV, E = D::E, NB = C::NB, NCS = D::NCS, CQP = D::CQP;
+  extern __shared__ __align__(16) double es[];
+  const int64_t Pp = blockIdx.x;
+  if (Pp >= n_patches) return;
   double *blk = fit + Pp * (int64_t)L::STRIDE;
-  double y[3], t[3];
-  for (int a = 0; a < 3; ++a) { y[a] = blk[L::YL + 3 * kap + a]; t[a] = blk[L::TL + 3 * kap + a]; }
-  cd R[D::NS];
-  r_table<P>(y[1], y[2], y[0], R, hc);
-  cd GS[D::NS][3];
-  for (int j = 0; j <= P; ++j)
-    for (int k = 0; k <= j; ++k) grad_fast(R, j, k, hc, GS[sidx(j, k)]);
-  // rows k = axis E + kappa; columns: Q component-major (comp CQP + 2 qidx + re/im), then V (2 vidx + re/im)
-  double *M0 = blk + L::MQ + (int64_t)kap * D::NCS;
-  constexpr int64_t AX = (int64_t)D::E * D::NCS;   // axis stride
-  for (int c = 0; c < D::NCS; ++c) { M0[c] = 0; M0[AX + c] = 0; M0[2 * AX + c] = 0; }
-  for (int j = 1; j <= P; ++j)
-    for (int k = 0; k <= j; ++k) {
+  double *M = blk + L::MQ;
+  for (int n0 = 0; n0 < E; n0 += NB) {
+    const int nb = E - n0 < NB ? E - n0 : NB;   // nodes in this round
+    __syncthreads();
+    // thread per node: R and grad tables (written to shared memory directly)
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      double *nd = es + i * C::NODE;
+      cd *R = reinterpret_cast<cd *>(nd), *GS = R + NS;
+      double *yt = nd + C::NODE - 6;
+      const int kap = n0 + i;
+      for (int a = 0; a < 3; ++a) { yt[a] = blk[L::YL + 3 * kap + a]; yt[3 + a] = blk[L::TL + 3 * kap + a]; }
+      r_table<P>(yt[1], yt[2], yt[0], R, hc);
+      for (int j = 0; j <= P; ++j)
+        for (int k = 0; k <= j; ++k) grad_fast(R, j, k, hc, reinterpret_cast<cd(*)[3]>(GS)[sidx(j, k)]);
+    }
+    __syncthreads();
+    // threads over (node, (j,k)): hessian along tau (j >= 2) and grad x tau, pre-scaled by v_lambda / v_theta
+    for (int w = threadIdx.x; w < nb * NV; w += blockDim.x) {
+      const int i = w / NV, v = w % NV;
+      double *nd = es + i * C::NODE;
+      const cd(*GS)[3] = reinterpret_cast<const cd(*)[3]>(reinterpret_cast<cd *>(nd) + NS);
+      cd *H = reinterpret_cast<cd *>(nd) + 4 * NS, *EV = H + 3 * NQ;
+      const double *t = nd + C::NODE - 3;
+      int j = 1;
+      while (vidx(j + 1, 0) <= v) ++j;
+      const int k = v - vidx(j, 0);
       const cd *g = GS[sidx(j, k)];
-      cd e[3] = {g[1] * mk(t[2], 0) - g[2] * mk(t[1], 0), g[2] * mk(t[0], 0) - g[0] * mk(t[2], 0),
-                 g[0] * mk(t[1], 0) - g[1] * mk(t[0], 0)};
-      const int vc = D::NCQ + 2 * vidx(j, k);
-      const double sv = vth[vidx(j, k)];   // k_translate's pre-scaling of V (TrCfg)
-      for (int a = 0; a < 3; ++a) { M0[a * AX + vc] = sv * e[a].x; M0[a * AX + vc + 1] = sv * e[a].y; }
+      const double sv = vth[v];
+      EV[3 * v + 0] = sv * (g[1] * mk(t[2], 0) - g[2] * mk(t[1], 0));
+      EV[3 * v + 1] = sv * (g[2] * mk(t[0], 0) - g[0] * mk(t[2], 0));
+      EV[3 * v + 2] = sv * (g[0] * mk(t[1], 0) - g[1] * mk(t[0], 0));
       if (j >= 2) {
         cd h[3];
         hess_fast(GS, j, k, t, hc, h);
-        const int qc = 2 * qidx(j, k);
-        constexpr int S = D::CQP;
-        for (int ri = 0; ri < 2; ++ri) {
-          const double sq = vlam[qidx(j, k)];   // k_translate's pre-scaling of Q, dQ (TrCfg)
-          double hv[3] = {sq * (ri ? h[0].y : h[0].x), sq * (ri ? h[1].y : h[1].x), sq * (ri ? h[2].y : h[2].x)};
-          // scalar part: -a.g
-          for (int a = 0; a < 3; ++a) M0[a * AX + qc + ri] = -hv[a];
-          // x: a_y g_z - a_z g_y ; y: a_z g_x - a_x g_z ; z: a_x g_y - a_y g_x  (axis c-1 of component c is zero)
-          M0[1 * AX + S + qc + ri] = hv[2];
-          M0[2 * AX + S + qc + ri] = -hv[1];
-          M0[2 * AX + 2 * S + qc + ri] = hv[0];
-          M0[0 * AX + 2 * S + qc + ri] = -hv[2];
-          M0[0 * AX + 3 * S + qc + ri] = hv[1];
-          M0[1 * AX + 3 * S + qc + ri] = -hv[0];
-        }
+        const int q = qidx(j, k);
+        const double sq = vlam[q];
+        for (int a = 0; a < 3; ++a) H[3 * q + a] = sq * h[a];
       }
     }
+    __syncthreads();
+    // rows k = axis E + kappa of M (row stride NCS), column-fastest over the round's NB x 3 rows
+    for (int w = threadIdx.x; w < 3 * nb * NCS; w += blockDim.x) {
+      const int r = w / NCS, col = w % NCS, axis = r / nb, i = r % nb;
+      const cd *H = reinterpret_cast<const cd *>(es + i * C::NODE) + 4 * NS, *EV = H + 3 * NQ;
+      double val = 0.0;
+      if (col < D::NCQ) {
+        // Q columns: component c = col / CQP, entry q, re/im.  Scalar part -a.g; vector parts a x g with
+        // the zero block (axis c-1 of component c)
+        const int c = col / CQP, wq = col % CQP, q = wq >> 1, ri = wq & 1;
+        if (q < NQ) {
+          const cd *h = H + 3 * q;
+          auto hv = [&](int b) { return ri ? h[b].y : h[b].x; };
+          if (c == 0) val = -hv(axis);
+          else {
+            // component c = 1..3 (x, y, z), cc = c - 1: (a x g)_cc = a_{cc+1} g_{cc+2} - a_{cc+2} g_{cc+1}
+            const int cc = c - 1, p1 = (cc + 1) % 3, p2 = (cc + 2) % 3;
+            if (axis == p1) val = hv(p2);
+            else if (axis == p2) val = -hv(p1);
+          }
+        }
+      } else {
+        const int wv = col - D::NCQ, v = wv >> 1, ri = wv & 1;
+        if (v < NV) val = ri ? EV[3 * v + axis].y : EV[3 * v + axis].x;
+      }
+      M[(int64_t)(axis * E + n0 + i) * NCS + col] = val;
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -614,8 +614,16 @@ static rrq_status patch_fit_impl(rrq_ctx c, const rrq_surface *s, double *fit, i
   TScope ts(c, 1, st);
   if ((r = compute_balls(c, s, st))) return r;
   k_patch_geom<P><<<(unsigned)Pn, 128, 0, st>>>(Pn, s->nodes, s->verts, s->edge_x, s->edge_dx, bp<double>(c->balls), c->T, fit);
-  k_edge_tables<P><<<nblk(Pn * D::E, 128), 128, 0, st>>>(Pn, c->T.hc, c->d_trtab + TrCfg<P>::VLAM,
-                                                          c->d_trtab + TrCfg<P>::VTH, fit);
+  {
+    using EC = EdgeTabCfg<P>;
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(k_edge_tables<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EC::SMEM);
+      set = true;
+    }
+    k_edge_tables<P><<<(unsigned)Pn, EC::THREADS, EC::SMEM, st>>>(Pn, c->T.hc, c->d_trtab + TrCfg<P>::VLAM,
+                                                                  c->d_trtab + TrCfg<P>::VTH, fit);
+  }
   c->launches += 2;
   if ((r = cuda_check(c, "k_patch_geom/k_edge_tables"))) return r;
   using FC = FitCfg<P>;
