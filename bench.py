@@ -189,7 +189,10 @@ def cfg_desc(cfg, npairs, T):
 
 def _l2_note(S, npairs):
     """Inputs/outputs against the 126 MB L2: the bench never flushes, so say whether it needs to."""
-    fit_gb = S.n_patches * 8.0 * (13 * S.p * (S.p + 1) // 2 * S.n + 9 * 2 * S.p * 12 * S.p * (S.p + 1)) / 1e9
+    p_, n_p = S.p, S.p * (S.p + 1) // 2
+    nq, nv = sum(j + 1 for j in range(2, p_ + 1)), sum(j + 1 for j in range(1, p_ + 1))
+    # fit block: the 13 n_p x n fit operators + the K x (8 n_Q + 2 n_V) operand M of the line-integral maps
+    fit_gb = S.n_patches * 8.0 * (13 * n_p * S.n + 18 * p_ * (8 * nq + 2 * nv)) / 1e9
     csr_gb = (npairs or 0) * S.n * 36 / 1e9
     big = fit_gb + csr_gb > 0.5
     return (f"inputs+outputs > L2 (fit ~{fit_gb:.1f} GB, CSR ~{csr_gb:.0f} GB per step): no flush needed" if big

@@ -397,3 +397,63 @@ def test_cfg7_tori_volume_grid():
     r = resid.abs().cpu().numpy() / np.abs(Uh).max()
     print(f"cfg7 Green representation over {close.size} close targets: E_inf {r.max():.3e}, median {np.median(r):.3e}")
     assert r.max() < 3e-5
+
+
+def test_cfg4_bench_launch_configuration_sampled():
+    """The full BASELINE.json config 4 (50,000 patches, p = 8, 4.2M targets, 143M pairs) built exactly as
+    bench.py times it (Runner.step: row chunks of 16M pairs, producer/consumer overlap, reused output
+    buffers); every near pair of 6 random patches is compared with the oracle element by element."""
+    import types
+    import bench
+    cfg = make_config(4)
+    S = cfg["surface"]
+    args = types.SimpleNamespace(chunk_pairs=16_000_000)
+    R = bench.Runner(cfg, args)
+    R.bufs = [R.alloc_out(args.chunk_pairs)]
+    rng = np.random.default_rng(3)
+    patches = rng.choice(S.n_patches, size=6, replace=False)
+    tg, pa = O.near_pairs_for_patches(S, cfg["tx"], cfg["self_node"], cfg["eta"], patches)
+    n = S.n
+    got = {k: np.zeros((tg.size, n)) for k in range(4)}
+    state = {}
+
+    def on_chunk(when, i, o, npairs=None):
+        if when == "before":
+            return
+        hptr = state["hptr"]
+        r0, r1 = state["chunks"][i]
+        sel = np.where((tg >= r0) & (tg < r1))[0]
+        if sel.size == 0:
+            return
+        pat = state["pat"]
+        rows = []
+        for s_ in sel:
+            t = tg[s_]
+            seg = pat[hptr[t]:hptr[t + 1]]
+            j = int(np.searchsorted(seg, pa[s_]))
+            assert seg[j] == pa[s_]
+            rows.append(hptr[t] - hptr[r0] + j)
+        idx = torch.as_tensor(np.asarray(rows, np.int64), device="cuda")
+        for k in range(4):   # gather only the sampled rows on the device
+            v = o["vals"][k][: npairs * n].view(npairs, n).index_select(0, idx).cpu().numpy()
+            got[k][sel] = v
+
+    ptr, pat = R.ctx.near_list(R.ds, R.dt)
+    state["hptr"] = ptr.cpu().numpy(); state["pat"] = pat.cpu().numpy()
+    state["chunks"] = R.chunks(state["hptr"], args.chunk_pairs)
+    assert len(state["chunks"]) > 1
+    R.step(on_chunk=on_chunk)
+    assert R.npairs == state["hptr"][-1]
+    vo, sto, kap = O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa, kappa=True)
+    band = _band_for_pairs(S, cfg["tx"], tg, pa)
+    inv = np.unique(tg, return_inverse=True)[1]
+    rb = np.ones(inv.max() + 1); np.maximum.at(rb, inv, band)
+    worst = []
+    for k in range(4):
+        st = {}
+        w, _ = U.compare_rows(got[k].reshape(-1), vo[k], inv, n, REL, ABS, rb[inv], kap[k], st,
+                              U.KAPPA_REL_DP if k == 3 else U.KAPPA_REL)
+        worst.append(w)
+        print("cfg4 bench-config", "S D Sp Dp".split()[k], st, "worst", w)
+    print(f"cfg4 bench launch configuration: {tg.size} pairs of {len(patches)} patches, worst {worst}")
+    assert max(worst) <= 1.0, worst
