@@ -453,6 +453,64 @@ def sample_pairs(cfg, budget, seed=7):
     return np.concatenate(tg), np.concatenate(pa), len(chosen)
 
 
+def parity_sample(R, tg, pa, vo, kap):
+    """One more full step (untimed) gathering the CSR rows of the oracle's sampled pairs on the device;
+    per kernel the largest per-row relative error max_i |g_i - o_i| / max_i |o_i|, the fraction of rows
+    within the strict 1e-11, the largest |g_i - o_i| / kappa_i, and the fraction of rows within the parity
+    bar of tests/ (per weight max(1e-11 max_row|o|, 1e-13, 1e-10 kappa_i), 3e-10 kappa_i for
+    D').  A correction weight is the difference of the RRQ weight and the smooth-rule weight (A14), which
+    nearly cancel for far pairs; kappa_i carries that scale, so the strict per-row figure is small there."""
+    import torch
+    n = R.n
+    ptr, pat = R.ctx.near_list(R.ds, R.dt)
+    hptr, hpat = ptr.cpu().numpy(), pat.cpu().numpy()
+    ch = R.chunks(hptr, R.args.chunk_pairs)
+    pos = np.empty(tg.size, np.int64)
+    for i, (t, q) in enumerate(zip(tg, pa)):
+        seg = hpat[hptr[t]:hptr[t + 1]]
+        j = int(np.searchsorted(seg, q))
+        if j >= seg.size or seg[j] != q:
+            raise RuntimeError("sampled pair missing from the GPU near list")
+        pos[i] = hptr[t] + j
+    got = np.zeros((4, tg.size, n))
+
+    def on_chunk(when, i, o, npairs=None):
+        if when == "before":
+            return
+        r0, r1 = ch[i]
+        sel = np.where((pos >= hptr[r0]) & (pos < hptr[r1]))[0]
+        if sel.size == 0:
+            return
+        idx = torch.as_tensor(pos[sel] - hptr[r0], device="cuda")
+        for k in range(4):
+            got[k, sel] = o["vals"][k][: npairs * n].view(npairs, n).index_select(0, idx).cpu().numpy()
+
+    R.step(on_chunk=on_chunk)
+    out = {"pairs": int(tg.size), "rows": int(np.unique(tg).size)}
+    for k, name in enumerate(("S", "D", "Sp", "Dp")):
+        o = vo[k].reshape(tg.size, n)
+        rowmax = {}
+        for t, m in zip(tg, np.abs(o).max(1)):
+            rowmax[t] = max(rowmax.get(t, 0.0), m)
+        rm = np.array([max(rowmax[t], 1e-300) for t in tg])
+        rel = np.abs(got[k] - o).max(1) / rm
+        worst_row = {}
+        for t, r in zip(tg, rel):
+            worst_row[t] = max(worst_row.get(t, 0.0), r)
+        wr = np.array(list(worst_row.values()))
+        kr = (3e-10 if name == "Dp" else 1e-10) * kap[k].reshape(tg.size, n)
+        tol = np.maximum(np.maximum(1e-11 * rm[:, None], 1e-13), kr)
+        ok_pair = (np.abs(got[k] - o) <= tol).all(1)
+        ok_row = {}
+        for t, ok in zip(tg, ok_pair):
+            ok_row[t] = ok_row.get(t, True) and bool(ok)
+        out[name] = {"max_rel_err_per_row": float(wr.max()), "median": float(np.median(wr)),
+                     "rows_within_1e-11": float((wr <= 1e-11).mean()),
+                     "max_err_over_kappa": float((np.abs(got[k] - o) / np.maximum(kap[k].reshape(tg.size, n), 1e-300)).max()),
+                     "rows_within_bar": float(np.mean(list(ok_row.values())))}
+    return out
+
+
 def cpu_baseline(cfg, args, R=None, steps=1):
     from oracle import oracle as O
     S = cfg["surface"]
@@ -460,13 +518,19 @@ def cpu_baseline(cfg, args, R=None, steps=1):
     cores = os.cpu_count()
     t0 = time.time()
     for _ in range(steps):
-        O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa)
+        vo, _ = O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa)
     el = (time.time() - t0) / steps
     w = tg.shape[0] * S.n * 4
     res = {"value": w / el, "unit": UNIT, "cores": cores, "kind": "oracle",
            "sample": f"{tg.shape[0]} pairs = all near pairs of {npatch} random patches of {cfg['name']} "
                      f"(Steps 1-8 incl. per-patch fit, all 4 kernels), {el:.1f} s on {cores} OpenMP threads",
            "seconds": el, "pairs": int(tg.shape[0])}
+    if R is not None:   # the same pairs out of a full-size build in the timed launch configuration
+        try:
+            _, _, kap = O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa, kappa=True)
+            res["parity_sample"] = parity_sample(R, tg, pa, vo, kap)
+        except Exception as ex:  # report, never hide
+            res["parity_sample"] = {"error": repr(ex)}
     # like-for-like with the paper's single-core numbers: the first patch's pairs on one thread
     try:
         import ctypes

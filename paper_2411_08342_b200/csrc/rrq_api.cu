@@ -725,17 +725,37 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   const int64_t per_pair = (int64_t)(2 * (2 * D::K + XRow<P>::STRIDE) + QRow<P>::STRIDE + D::NZS) * 8 +
                            2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair));
   const int64_t cap = std::max<int64_t>(4096, (int64_t)(24e9 / per_pair));
-  std::vector<std::pair<int64_t, int64_t>> subs;
+  // sub-chunks = contiguous ranges of work items (tiles of TP pairs of one patch): whole patches while they
+  // fit, a patch with more than `cap` pairs (config 5: one patch, 10M targets) split at tile boundaries
+  struct Sub { int64_t it0, it1, sA, sB; };
+  std::vector<Sub> subs;
   int64_t maxsub = 0, maxitems = 0;
-  for (int64_t P0 = 0; P0 < Pn;) {
-    int64_t P1 = P0 + 1;
-    while (P1 < Pn && hseg[P1 + 1] - hseg[P0] <= cap) ++P1;
-    if (hseg[P1] > hseg[P0]) {
-      subs.push_back({P0, P1});
-      maxsub = std::max(maxsub, hseg[P1] - hseg[P0]);
-      maxitems = std::max(maxitems, hitem[P1] - hitem[P0]);
+  {
+    const int64_t capI = std::max<int64_t>(1, cap / TP);
+    int64_t cur_it0 = -1, cur_sA = 0;
+    auto flush = [&](int64_t it1, int64_t sB) {
+      if (cur_it0 >= 0 && sB > cur_sA) subs.push_back({cur_it0, it1, cur_sA, sB});
+      cur_it0 = -1;
+    };
+    for (int64_t P0 = 0; P0 < Pn; ++P0) {
+      const int64_t np0 = hseg[P0 + 1] - hseg[P0];
+      if (np0 == 0) continue;
+      if (cur_it0 >= 0 && hseg[P0 + 1] - cur_sA > cap) flush(hitem[P0], hseg[P0]);
+      if (np0 > cap) {
+        for (int64_t it = hitem[P0]; it < hitem[P0 + 1]; it += capI) {
+          const int64_t ie = std::min(it + capI, hitem[P0 + 1]);
+          subs.push_back({it, ie, hseg[P0] + (it - hitem[P0]) * TP,
+                          ie == hitem[P0 + 1] ? hseg[P0 + 1] : hseg[P0] + (ie - hitem[P0]) * TP});
+        }
+        continue;
+      }
+      if (cur_it0 < 0) { cur_it0 = hitem[P0]; cur_sA = hseg[P0]; }
     }
-    P0 = P1;
+    flush(hitem[Pn], hseg[Pn]);
+    for (const Sub &u : subs) {
+      maxsub = std::max(maxsub, u.sB - u.sA);
+      maxitems = std::max(maxitems, u.it1 - u.it0);
+    }
   }
   const int nset = (c->overlap && subs.size() > 1) ? 2 : 1;
   for (int b = 0; b < nset; ++b)
@@ -768,10 +788,9 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   }
   rrq_status r;
   for (size_t i = 0; i < subs.size(); ++i) {
-    const auto &sr = subs[i];
+    const Sub &sr = subs[i];
     const int b = (int)(i % nset);
-    const int64_t sA = hseg[sr.first], sB = hseg[sr.second];
-    const int64_t it0 = hitem[sr.first], it1 = hitem[sr.second];
+    const int64_t sA = sr.sA, sB = sr.sB, it0 = sr.it0, it1 = sr.it1;
     const int64_t np_ = sB - sA;
     double *Ar = bp<double>(c->Arow[b]), *Xr = bp<double>(c->Xrow[b]);
     PairSetup *ps = bp<PairSetup>(c->psetup[b]);
