@@ -138,7 +138,10 @@ struct TrCfg {
   static constexpr int BUF = QSZ + SXSZ > 32 * SLW ? QSZ + SXSZ : 32 * SLW;
   static_assert(QSZ % 2 == 0 && BUF % 2 == 0, "translate buffer");
   static constexpr int GSZ = XRow<P>::GSZ;
-  static constexpr int PER_WARP = (2 * BUF + GSZ + 1) / 2 * 2;
+  // NBUF = 1: a warp stages its next pair after the current one's epilogue (the load latency is covered by
+  // the other warps); the smaller footprint buys more warps per SM than double buffering (NBUF = 2)
+  static constexpr int NBUF = 1, WMAX = P >= 10 ? 8 : 12;
+  static constexpr int PER_WARP = (NBUF * BUF + GSZ + 1) / 2 * 2;
   // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 prime codes [STEPS][32],
   // u32 cinfo [NP], u8 shared-memory positions of the Q entries [NQ] and of the S' entries [P*P] |
   // f64 vlam [NQ], vth [NV], wS [P*P], olam [NP], oth [NP]
@@ -148,7 +151,7 @@ struct TrCfg {
   static constexpr int TAB_D = (OTH + D::NP + 1) / 2 * 2;
   static constexpr int SMEM_MAX = 224 * 1024;
   static constexpr int WPB_FIT = (SMEM_MAX / 8 - TAB_D) / PER_WARP;
-  static constexpr int WPB = WPB_FIT > 8 ? 8 : WPB_FIT;
+  static constexpr int WPB = WPB_FIT > WMAX ? WMAX : WPB_FIT;
   static constexpr size_t SMEM = (size_t)(TAB_D + WPB * PER_WARP) * sizeof(double);
   // code: Q position | new S' position << 7 | FA | FB | PRIME;  prime code: S' positions of window
   // entries 1 .. WD-1, 7 bits each.  cinfo: l | m << 4 | i << 8 | first lane << 12 | lanes << 20.
@@ -999,15 +1002,14 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   for (int i = threadIdx.x; i < C::TAB_D; i += blockDim.x) sm[i] = trtab[i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double *wb = sm + C::TAB_D + (size_t)warp * C::PER_WARP;
-  double *GB = wb + 2 * C::BUF;   // buffer b: wb + b BUF = [Q block | S' block]
+  double *GB = wb + C::NBUF * C::BUF;   // buffer b: wb + b BUF = [Q block | S' block]
   auto zero_entries = [&](int b) {  // the zero Q entry (+ its V) and the zero S' entry (never staged)
     double *qd = wb + b * C::BUF;
     if (lane < 16) qd[EQ * C::ZQ + lane] = 0.0;
     else if (lane < 18) qd[C::SV + 2 * (C::ZQ + 2) + lane - 16] = 0.0;
     else if (lane < 22) qd[C::QSZ + SXW * P * P + lane - 18] = 0.0;
   };
-  zero_entries(0);
-  zero_entries(1);
+  for (int b = 0; b < C::NBUF; ++b) zero_entries(b);
   __syncthreads();
   const uint32_t *code = reinterpret_cast<const uint32_t *>(sm);
   const uint32_t *pcode = code + C::STEPS * 32;
@@ -1062,10 +1064,14 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   }
   cp_async_commit();
   for (int it = 0; s < sB; s += stride, ++it) {
-    const int cb = it & 1;
-    if (s + stride < sB) issue_qs(s + stride, cb ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
+    const int cb = C::NBUF == 2 ? (it & 1) : 0;
+    if constexpr (C::NBUF == 2) {
+      if (s + stride < sB) issue_qs(s + stride, cb ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncwarp();
     double *qbw = wb + cb * C::BUF;
     const double *qb = qbw, *sx = qbw + C::QSZ;
@@ -1202,7 +1208,11 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     for (int i = D::NZ + lane; i < NZS; i += 32) Z[i] = 0.0;
     __syncwarp();
     zero_entries(cb);   // the slots overwrote them
-    if (s + stride < sB) issue_g(s + stride);
+    __syncwarp();
+    if (s + stride < sB) {
+      if constexpr (C::NBUF == 1) issue_qs(s + stride, 0);
+      issue_g(s + stride);
+    }
     cp_async_commit();
   }
   cp_async_wait<0>();
