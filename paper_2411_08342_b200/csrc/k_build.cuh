@@ -140,7 +140,7 @@ struct TrCfg {
   static constexpr int GSZ = XRow<P>::GSZ;
   // NBUF = 1: a warp stages its next pair after the current one's epilogue (the load latency is covered by
   // the other warps); the smaller footprint buys more warps per SM than double buffering (NBUF = 2)
-  static constexpr int NBUF = 1, WMAX = P >= 10 ? 8 : 12;
+  static constexpr int NBUF = 1, WMAX = P >= 10 ? 8 : 16;
   static constexpr int PER_WARP = (NBUF * BUF + GSZ + 1) / 2 * 2;
   // per-CTA table (host-built, rrq_api.cu make_trtab): u32 codes [STEPS][32], u32 prime codes [STEPS][32],
   // u32 cinfo [NP], u8 shared-memory positions of the Q entries [NQ] and of the S' entries [P*P] |
