@@ -162,7 +162,9 @@ int64_t rrq_launch_count(rrq_ctx ctx);
  * store), [6] build plumbing (pair permutation, work items), [7] whole rrq_build_correction calls
  * (caller's stream).  rrq_build_correction runs stage [2] of sub-chunk i+1 on an internal stream
  * concurrently with stages [3]-[5] of sub-chunk i (unless the environment sets RRQ_NO_OVERLAP=1),
- * so stages [2]-[6] may overlap; [7] is the build's device time.  stats[0] = pairs built, stats[1] =
+ * so stages [2]-[6] may overlap; [7] is the build's device time.  The build works in sub-chunks of
+ * whole patches (or tile ranges of one patch) within a scratch budget of 24 GB (RRQ_SCRATCH_BYTES
+ * overrides it; a test hook).  stats[0] = pairs built, stats[1] =
  * swap-regime edges (reading A5).  The build synchronises the stream before the events are read. */
 #define RRQ_NSTAGES 8
 rrq_status rrq_set_timing(rrq_ctx ctx, int enable);

@@ -45,6 +45,7 @@ struct rrq_ctx_s {
   cudaStream_t st2 = nullptr;                      // producer stream (created on first use)
   cudaEvent_t ev_edge[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_fork = nullptr, ev_join = nullptr;
   bool overlap = true;                             // RRQ_NO_OVERLAP=1 runs everything on the caller's stream
+  double scratch_bytes = 24e9;                     // sub-chunk scratch budget (RRQ_SCRATCH_BYTES: test hook)
   Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one, swapcnt;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
@@ -321,6 +322,8 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   {
     const char *e = std::getenv("RRQ_NO_OVERLAP");
     c->overlap = !(e && std::atoi(e) != 0);
+    const char *sb = std::getenv("RRQ_SCRATCH_BYTES");
+    if (sb && std::atof(sb) > 0) c->scratch_bytes = std::atof(sb);
   }
   int q = p.p_edge, no = p.n_omega;
   c->h_t.resize(q);
@@ -724,7 +727,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   // the double-buffered pair_edge outputs plus the Q and Z rows)
   const int64_t per_pair = (int64_t)(2 * (2 * D::K + XRow<P>::STRIDE) + QRow<P>::STRIDE + D::NZS) * 8 +
                            2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair));
-  const int64_t cap = std::max<int64_t>(4096, (int64_t)(24e9 / per_pair));
+  const int64_t cap = std::max<int64_t>(2 * TP, (int64_t)(c->scratch_bytes / per_pair));
   // sub-chunks = contiguous ranges of work items (tiles of TP pairs of one patch): whole patches while they
   // fit, a patch with more than `cap` pairs (config 5: one patch, 10M targets) split at tile boundaries
   struct Sub { int64_t it0, it1, sA, sB; };

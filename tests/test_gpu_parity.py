@@ -457,3 +457,34 @@ def test_cfg4_bench_launch_configuration_sampled():
         print("cfg4 bench-config", "S D Sp Dp".split()[k], st, "worst", w)
     print(f"cfg4 bench launch configuration: {tg.size} pairs of {len(patches)} patches, worst {worst}")
     assert max(worst) <= 1.0, worst
+
+
+def _build_with_env(cfg, env):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    try:
+        os.environ.update(env)
+        res = U.gpu_build(cfg, cfg["surface"], (cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"]))
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return res
+
+
+def test_schedule_independence_bit_exact():
+    """The build's internal schedule does not change a single bit of the output: producer/consumer overlap on
+    or off (RRQ_NO_OVERLAP), and sub-chunks of whole patches or tile ranges of one patch (a scratch budget
+    small enough to split config 5's single patch and config 1's patches)."""
+    for cfgid, kw in ((1, dict(n_off=300)), (5, dict(n_off=2000))):
+        cfg = make_config(cfgid, **kw)
+        ref = _build_with_env(cfg, {"RRQ_NO_OVERLAP": "1", "RRQ_SCRATCH_BYTES": "1e12"})
+        for env in ({"RRQ_NO_OVERLAP": "0", "RRQ_SCRATCH_BYTES": "1e12"},
+                    {"RRQ_NO_OVERLAP": "0", "RRQ_SCRATCH_BYTES": "3e6"},
+                    {"RRQ_NO_OVERLAP": "1", "RRQ_SCRATCH_BYTES": "3e6"}):
+            got = _build_with_env(cfg, env)
+            for k in range(4):
+                assert np.array_equal(got["vals"][k], ref["vals"][k]), (cfgid, env, k)
+            assert np.array_equal(got["col"], ref["col"]) and np.array_equal(got["status"], ref["status"])
