@@ -81,7 +81,7 @@ template <int P>
 struct XRow {
   using D = Dims<P>;
   static constexpr int SX = 0, W = 4 * P * P, DW = W + 4 * D::NP, TH = DW + 4 * D::NP, NU = TH + D::NP,
-                       G = W, GSZ = (9 * D::NP + 3 + 1) / 2 * 2, STRIDE = (G + GSZ + 15) / 16 * 16;   // rows 128-B aligned
+                       G = W, GSZ = (9 * D::NP + 4 + 1) / 2 * 2, STRIDE = (G + GSZ + 15) / 16 * 16;   // rows 128-B aligned
 };
 // Per-pair row of k_qmap's output: per (j, k >= 0), 2 <= j <= p, at EG qidx(j,k): [Q (4 quaternion comps,
 // re/im) | dQ (same)] scaled by v_lambda(j,k); then V [2 NV] scaled by v_theta(j,k) (TrCfg).
@@ -524,6 +524,8 @@ __global__ void __launch_bounds__(WPB * 32)
     }
     if (lane < 3 * kPPW && mine[lane / 3].active)
       Xrow[(base + warp * kPPW + lane / 3 - sA) * XR::STRIDE + XR::NU + lane % 3] = mine[lane / 3].nup[lane % 3];
+    if (lane < kPPW && mine[lane].active)   // k_contract tile slot (k_translate writes zeta there)
+      Xrow[(base + warp * kPPW + lane - sA) * XR::STRIDE + XR::NU + 3] = __longlong_as_double(mine[lane].aslot);
     __syncwarp();   // next phase only reads this warp's pairs
     RRQ_PHASE_MARK(0);
     // ---------------- phase 2: t0 per edge (reading A12, A12'), lanes (pair, edge, comp) = 27 lanes
@@ -963,6 +965,36 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
   }
 }
 
+// k_contract's tile configuration (see k_contract); k_translate writes zeta in its tile-chunked layout.
+template <int P>
+struct ContractCfg {
+  using D = Dims<P>;
+  static constexpr int TP = 16, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 8;
+  static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
+  static constexpr int NB = Layout<P>::NF;   // B row stride (== the fit operators' row stride)
+  static constexpr int KC = (D::NP % 3 == 0) ? 12 : ((D::NP % 2 == 0) ? 8 : 4);            // k-rows per chunk
+  static constexpr int NCH = 4 * D::NP / KC;
+  // Z is stored tile-chunked by k_translate (a tile's block of ZBLK doubles): the Theta part [TP][ZTS]
+  // (ZTS == 4 mod 16: conflict-free A fragments), then per K chunk ch the W | dW | S slices [3][TP][KC]
+  // (k = component NP + c of zeta(W), zeta(dW), zeta_S).  A pipeline stage = [B chunk | Z chunk], two
+  // bulk copies; the small footprint lets 3 CTAs share an SM.  KC = 8: the halves of rows with bit 1 set
+  // are swapped (conflict-free fragments).
+  static constexpr int ZTS = D::NP + ((4 - D::NP % 16) + 16) % 16, ZT = TP * ZTS, ZCH = 3 * TP * KC;
+  static constexpr int64_t ZBLK = (int64_t)ZT + (int64_t)NCH * ZCH;
+  static constexpr size_t SMEM_B = 3 * (size_t)KC * NB;                                       // PD | PSp | PSg
+  static constexpr size_t STG = SMEM_B + ZCH;
+  static constexpr size_t SNODE = (7 * D::N + 1) / 2 * 2;   // the patch's nodes [N][3], normals [N][3], weights [N]
+  static constexpr size_t SMEM = (ZT + 2 * STG + SNODE) * sizeof(double) + TP * 64;   // + ContractPair[TP]
+  static constexpr int MINB = (P <= 8 && SMEM * 3 <= 225 * 1024) ? 3 : 2;   // p = 10: registers (TPW = 4)
+  __host__ __device__ static constexpr int swz(int r) { return KC == 8 ? ((r >> 1) & 1) << 2 : 0; }
+  // position of zeta entry (block b = 0 Theta, 1..4 zeta(W), 5..8 zeta(dW), 9..12 zeta_S; c = (l,m)) of tile row r
+  __host__ __device__ static constexpr int64_t zoff(int b, int r, int c) {
+    return b == 0 ? (int64_t)r * ZTS + c
+                  : (int64_t)ZT + (int64_t)((((b - 1) & 3) * D::NP + c) / KC) * ZCH + (int64_t)((b - 1) >> 2) * TP * KC +
+                        r * KC + (((((b - 1) & 3) * D::NP + c) % KC) ^ swz(r));
+  }
+};
+
 // ------------------------------------------------------------------------------------------------
 // k_translate: Step 7 (P:L1263-1268 eq cdlp1dintegral): for each (l,m),
 // lambda_1, its nu'-derivative and theta_1 from Q^{(j,k)}, dQ^{(j,k)}, V^{(j,k)} and S(r'), plus the
@@ -997,7 +1029,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   using C = TrCfg<P>;
   using XR = XRow<P>;
   using QR = QRow<P>;
-  constexpr int NP = D::NP, NZS = D::NZS, WPB = C::WPB, EQ = C::EQ, SXW = C::SXW, WD = C::WD;
+  constexpr int NP = D::NP, WPB = C::WPB, EQ = C::EQ, SXW = C::SXW, WD = C::WD;
   extern __shared__ __align__(16) double sm[];
   for (int i = threadIdx.x; i < C::TAB_D; i += blockDim.x) sm[i] = trtab[i];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1167,7 +1199,10 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     __syncwarp();
     // epilogue: lanes over c = (l, m); gamma parts from GB (W [4][NP], dW [4][NP], Theta [NP], nu')
     const double nup[3] = {GB[9 * NP], GB[9 * NP + 1], GB[9 * NP + 2]};
-    double *Z = Zrow + (s - sA) * NZS;
+    using CC = ContractCfg<P>;   // Z in k_contract's tile-chunked layout; the tile slot rides in the G block
+    const int64_t aslot = __double_as_longlong(GB[9 * NP + 3]);
+    double *Zt = Zrow + (aslot >> 5) * CC::ZBLK;
+    const int zr = (int)(aslot & 31);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = lane + 32 * h;
@@ -1193,19 +1228,18 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
       // zeta vectors (Step 8, App. A.7; reading G3 for S')
       double nxW[3];
       cross3(nup, W + 1, nxW);
-      Z[c] = Th;
-      Z[NP + c] = W[0];
-      Z[2 * NP + c] = -W[1];
-      Z[3 * NP + c] = -W[2];
-      Z[4 * NP + c] = -W[3];
-      Z[5 * NP + c] = dW[0];
-      Z[6 * NP + c] = -dW[1];
-      Z[7 * NP + c] = -dW[2];
-      Z[8 * NP + c] = -dW[3];
-      Z[9 * NP + c] = -dot3(nup, W + 1);
-      for (int a = 0; a < 3; ++a) Z[10 * NP + a * NP + c] = -W[0] * nup[a] - nxW[a];
+      Zt[CC::zoff(0, zr, c)] = Th;
+      Zt[CC::zoff(1, zr, c)] = W[0];
+      Zt[CC::zoff(2, zr, c)] = -W[1];
+      Zt[CC::zoff(3, zr, c)] = -W[2];
+      Zt[CC::zoff(4, zr, c)] = -W[3];
+      Zt[CC::zoff(5, zr, c)] = dW[0];
+      Zt[CC::zoff(6, zr, c)] = -dW[1];
+      Zt[CC::zoff(7, zr, c)] = -dW[2];
+      Zt[CC::zoff(8, zr, c)] = -dW[3];
+      Zt[CC::zoff(9, zr, c)] = -dot3(nup, W + 1);
+      for (int a = 0; a < 3; ++a) Zt[CC::zoff(10 + a, zr, c)] = -W[0] * nup[a] - nxW[a];
     }
-    for (int i = D::NZ + lane; i < NZS; i += 32) Z[i] = 0.0;
     __syncwarp();
     zero_entries(cb);   // the slots overwrote them
     __syncwarp();
@@ -1224,23 +1258,9 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 // units (A2), the smooth-rule subtraction (A14) and the CSR store.  Warp w owns the (M-tile, N-tile)
 // pairs w, w + 16, ...; 4 accumulator tiles (S, D, S', D') each.  Z tile staged in shared memory.
 // ------------------------------------------------------------------------------------------------
-template <int P>
-struct ContractCfg {
-  using D = Dims<P>;
-  static constexpr int TP = 16, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 8;
-  static constexpr int ZS = (D::NZS % 16 == 4) ? D::NZS : D::NZS + ((4 - D::NZS % 16) + 16) % 16;
-  static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
-  static constexpr int NB = Layout<P>::NF;   // B row stride (== the fit operators' row stride)
-  static constexpr int KC = (D::NP % 3 == 0) ? 12 : ((D::NP % 2 == 0) ? 8 : 4);            // k-rows per chunk
-  static constexpr int NCH = 4 * D::NP / KC;
-  static constexpr size_t SMEM_Z = (size_t)TP * ZS;
-  static constexpr size_t SMEM_B = 3 * (size_t)KC * NB;                                       // PD | PSp | PSg
-  static constexpr size_t SNODE = (7 * D::N + 1) / 2 * 2;   // the patch's nodes [N][3], normals [N][3], weights [N]
-  static constexpr size_t SMEM = (SMEM_Z + 2 * SMEM_B + SNODE + TP * 8) * sizeof(double);   // + ContractPair[TP]
-};
 
 template <int P>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
     k_contract(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, const int32_t *__restrict__ item_patch,
                const int64_t *__restrict__ seg_ptr, int64_t sA, const ContractPair *__restrict__ cpair,
                const double *__restrict__ fit, const double *__restrict__ Zrow, const double *__restrict__ nodes,
@@ -1249,10 +1269,10 @@ __global__ void __launch_bounds__(256, 2)
   using D = Dims<P>;
   using L = Layout<P>;
   using CC = ContractCfg<P>;
-  constexpr int N = D::N, NP = D::NP, TP = CC::TP, ZS = CC::ZS, NZS = D::NZS, NB = CC::NB, KC = CC::KC;
+  constexpr int N = D::N, NP = D::NP, TP = CC::TP, ZTS = CC::ZTS, NB = CC::NB, KC = CC::KC;
   extern __shared__ __align__(16) double sz[];
-  double *sB = sz + CC::SMEM_Z;                    // [2][3][KC][NB]
-  double *sN = sB + 2 * CC::SMEM_B;                // nodes [N][3] | normals [N][3] | weights [N] of the patch
+  double *sB = sz + CC::ZT;                        // [2][B chunk: 3][KC][NB | Z chunk: 3][TP][KC]
+  double *sN = sB + 2 * CC::STG;                   // nodes [N][3] | normals [N][3] | weights [N] of the patch
   ContractPair *sC = reinterpret_cast<ContractPair *>(sN + CC::SNODE);   // [TP] the tile's pairs
   const int64_t item = item0 + blockIdx.x;
   if (item >= item1) return;
@@ -1261,12 +1281,12 @@ __global__ void __launch_bounds__(256, 2)
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
   const double *blk = fit + Pp * (int64_t)L::STRIDE;
   const double *PD = blk + L::FIT, *PSp = PD + 4 * NP * NB, *PSd = PD + 8 * NP * NB, *PSg = PD + 9 * NP * NB;
-  // B chunk ch: rows [ch KC, (ch+1) KC) of P_D, P_Sp, P_Sg -> sB[(ch&1)][blk][row][NB]; the Z tile (rows of
-  // NZS doubles, contiguous in global and in shared memory since ZS == NZS) rides on chunk 0's barrier.
-  // 1-D bulk copies (TMA) issued by warp 0 on mbarriers.
-  static_assert(ZS == NZS, "Z tile staged as one bulk copy");
+  const double *Zblk = Zrow + (item - item0) * CC::ZBLK;   // rows of absent pairs: never read back
+  // stage ch & 1: rows [ch KC, (ch+1) KC) of P_D, P_Sp, P_Sg and the tile's Z chunk ch; the Theta part,
+  // the patch's nodes and the tile's pair records ride on chunk 0's barrier.  1-D bulk copies (TMA) on
+  // mbarriers, issued by thread 0 (and 32 for the prologue extras).
   __shared__ uint64_t bar[2], emp[2];
-  constexpr unsigned ROWB = (unsigned)(NB * sizeof(double));
+  constexpr unsigned ROWB = (unsigned)(NB * sizeof(double)), ZCB = (unsigned)(CC::ZCH * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -1275,25 +1295,25 @@ __global__ void __launch_bounds__(256, 2)
     mbar_init(&emp[1], CC::WARPS);
     mbar_fence_init();
   }
-  for (int i = cnt * ZS + threadIdx.x; i < TP * ZS; i += blockDim.x) sz[i] = 0.0;   // absent pairs
   __syncthreads();
   // the fit operators are stored with the padded row stride NB, so a chunk of each is one contiguous copy
   auto issue = [&](int ch, unsigned extra) {
     uint64_t *br = &bar[ch & 1];
     if (threadIdx.x == 0) {
-      mbar_expect_tx(br, 3u * KC * ROWB + extra);
-      double *dst = sB + (ch & 1) * CC::SMEM_B;
+      mbar_expect_tx(br, 3u * KC * ROWB + ZCB + extra);
+      double *dst = sB + (ch & 1) * CC::STG;
       bulk_g2s(dst, PD + (int64_t)ch * KC * NB, KC * ROWB, br);
       bulk_g2s(dst + KC * NB, PSp + (int64_t)ch * KC * NB, KC * ROWB, br);
       bulk_g2s(dst + 2 * KC * NB, PSg + (int64_t)ch * KC * NB, KC * ROWB, br);
+      bulk_g2s(dst + CC::SMEM_B, Zblk + CC::ZT + (int64_t)ch * CC::ZCH, ZCB, br);
     }
   };
   {
-    const unsigned zb = (unsigned)(cnt * NZS * sizeof(double)), nb3 = (unsigned)(3 * N * sizeof(double)),
+    const unsigned zb = (unsigned)(CC::ZT * sizeof(double)), nb3 = (unsigned)(3 * N * sizeof(double)),
                    nb1 = (unsigned)(N * sizeof(double)), cb = (unsigned)(cnt * sizeof(ContractPair));
     issue(0, zb + 2 * nb3 + nb1 + cb);
     if (threadIdx.x == 32) {
-      bulk_g2s(sz, Zrow + (s0 - sA) * NZS, zb, &bar[0]);
+      bulk_g2s(sz, Zblk, zb, &bar[0]);
       bulk_g2s(sN, nodes + Pp * N * 3, nb3, &bar[0]);
       bulk_g2s(sN + 3 * N, normals + Pp * N * 3, nb3, &bar[0]);
       bulk_g2s(sN + 6 * N, weights + Pp * N, nb1, &bar[0]);
@@ -1324,7 +1344,7 @@ __global__ void __launch_bounds__(256, 2)
   for (int tw = 0; tw < CC::TPW; ++tw) {
     const int tile = warp + tw * CC::WARPS;
     if (tile >= CC::TILES) continue;
-    const double *zr = sz + ((tile % CC::MT) * 8 + (lane >> 2)) * ZS + (lane & 3);
+    const double *zr = sz + ((tile % CC::MT) * 8 + (lane >> 2)) * ZTS + (lane & 3);
 #pragma unroll
     for (int q = 0; q < NK; ++q) {
       const int kk = 4 * q + (lane & 3);
@@ -1335,7 +1355,8 @@ __global__ void __launch_bounds__(256, 2)
   // (no CTA-wide barrier in the K loop).  A warp's tiles share the M-tile (tile = warp + WARPS tw).
   static_assert(CC::WARPS % CC::MT == 0, "a warp's tiles share one M-tile");
   const int mtw = warp % CC::MT;
-  const double *zr0 = sz + (mtw * 8 + (lane >> 2)) * ZS + (lane & 3);
+  const int zrow = mtw * 8 + (lane >> 2), zsw = CC::swz(zrow);
+  const int zofs = zrow * KC + (lane & 3);
   for (int ch = 0; ch < CC::NCH; ++ch) {
     if (ch + 1 < CC::NCH && threadIdx.x == 0) {   // refill buffer (ch+1)&1 once every warp has left chunk ch-1
       if (ch >= 1) mbar_wait(&emp[(ch + 1) & 1], ((ch - 1) >> 1) & 1);
@@ -1343,11 +1364,11 @@ __global__ void __launch_bounds__(256, 2)
       issue(ch + 1, 0);
     }
     mbar_wait(&bar[ch & 1], (ch >> 1) & 1);
-    const double *bb = sB + (ch & 1) * CC::SMEM_B;
-    const double *zr = zr0 + ch * KC;
+    const double *bb = sB + (ch & 1) * CC::STG;
+    const double *zr = bb + CC::SMEM_B + zofs;
 #pragma unroll
     for (int kk = 0; kk < KC; kk += 4) {
-      const double zw = zr[NP + kk], zdw = zr[5 * NP + kk], zs = zr[9 * NP + kk];
+      const double zw = zr[kk ^ zsw], zdw = zr[TP * KC + (kk ^ zsw)], zs = zr[2 * TP * KC + (kk ^ zsw)];
 #pragma unroll
       for (int tw = 0; tw < CC::TPW; ++tw) {
         const int tile = warp + tw * CC::WARPS;
@@ -1477,6 +1498,20 @@ __global__ void k_copy_i64(int64_t n, const int64_t *__restrict__ a, int64_t *__
 }
 
 // CSR SpMV: warp per row.
+// Test hook (rrq_debug_zeta): zeta rows of the last sub-chunk, in pair order, out of the tile-chunked layout.
+template <int P>
+__global__ void k_debug_zeta(int64_t np_, const PairSetup *__restrict__ setup, const double *__restrict__ Z,
+                             double *__restrict__ out) {
+  using CC = ContractCfg<P>;
+  constexpr int NP = Dims<P>::NP;
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= np_ * 13 * NP) return;
+  const int64_t i = w / (13 * NP);
+  const int bc = (int)(w % (13 * NP)), b = bc / NP, c = bc % NP;
+  const int64_t a = setup[i].aslot;
+  out[w] = Z[(a >> 5) * CC::ZBLK + CC::zoff(b, (int)(a & 31), c)];
+}
+
 __global__ void k_apply(int64_t n_rows, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                         const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y) {
   int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;

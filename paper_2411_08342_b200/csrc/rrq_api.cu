@@ -37,7 +37,8 @@ struct rrq_ctx_s {
     void *p = nullptr;
     size_t n = 0;
   };
-  int64_t last_np = 0, last_nz = 0, last_nzs = 0, last_sA = 0;
+  int64_t last_np = 0, last_nz = 0, last_sA = 0;
+  int last_set = 0;
   // k_pair_edge's outputs are double-buffered (set = sub-chunk parity) so that the producer stream (k_pair_setup,
   // k_pair_edge of sub-chunk i+1) runs concurrently with the consumer stream (k_qmap, k_translate, k_contract of
   // sub-chunk i): the edge kernel is FP64-latency bound and the GEMM kernels leave the FP64 pipe ~40 % idle.
@@ -435,9 +436,21 @@ rrq_status rrq_debug_zeta(rrq_ctx c, int64_t max_pairs, int64_t *perm, double *Z
   cudaDeviceSynchronize();
   int64_t n = std::min(max_pairs, c->last_np);
   if (perm && n > 0) cudaMemcpy(perm, bp<int64_t>(c->perm) + c->last_sA, n * sizeof(int64_t), cudaMemcpyDeviceToHost);
-  if (Z && n > 0)
-    cudaMemcpy2D(Z, c->last_nz * sizeof(double), c->Z.p, c->last_nzs * sizeof(double), c->last_nz * sizeof(double), n,
-                 cudaMemcpyDeviceToHost);
+  if (Z && n > 0) {   // gather the rows out of k_contract's tile-chunked layout
+    double *tmp = nullptr;
+    if (cudaMalloc(&tmp, (size_t)n * c->last_nz * sizeof(double)) != cudaSuccess) return fail(c, RRQ_ERR_CUDA, "debug buffer");
+    const PairSetup *su = bp<PairSetup>(c->psetup[c->last_set]);
+    const double *zb = bp<double>(c->Z);
+    const unsigned g = nblk(n * c->last_nz, 256);
+    switch (c->prm.p) {
+      case 4: k_debug_zeta<4><<<g, 256>>>(n, su, zb, tmp); break;
+      case 6: k_debug_zeta<6><<<g, 256>>>(n, su, zb, tmp); break;
+      case 8: k_debug_zeta<8><<<g, 256>>>(n, su, zb, tmp); break;
+      default: k_debug_zeta<10><<<g, 256>>>(n, su, zb, tmp); break;
+    }
+    cudaMemcpy(Z, tmp, (size_t)n * c->last_nz * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+  }
   *n_out = n;
   return cuda_check(c, "rrq_debug_zeta");
 }
@@ -725,7 +738,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   hseg[Pn] = total;
   // ---- sub-chunks: ranges of whole patches with at most `cap` pairs (scratch ~24 KB per pair at p = 8:
   // the double-buffered pair_edge outputs plus the Q and Z rows)
-  const int64_t per_pair = (int64_t)(2 * (2 * D::K + XRow<P>::STRIDE) + QRow<P>::STRIDE + D::NZS) * 8 +
+  const int64_t per_pair = (int64_t)(2 * (2 * D::K + XRow<P>::STRIDE) + QRow<P>::STRIDE + CC::ZBLK / CC::TP) * 8 +
                            2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair));
   const int64_t cap = std::max<int64_t>(2 * TP, (int64_t)(c->scratch_bytes / per_pair));
   // sub-chunks = contiguous ranges of work items (tiles of TP pairs of one patch): whole patches while they
@@ -766,7 +779,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
         !ensure(c, c->psetup[b], (size_t)maxsub * sizeof(PairSetup)) ||
         !ensure(c, c->cpair[b], (size_t)maxsub * sizeof(ContractPair)))
       return RRQ_ERR_CUDA;
-  if (!ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxsub * D::NZS * 8))
+  if (!ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxitems * CC::ZBLK * 8))
     return RRQ_ERR_CUDA;
   static bool attr_set = false;
   if (!attr_set) {
@@ -842,6 +855,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     c->launches += 5;
     c->last_sA = sA;
     c->last_np = np_;
+    c->last_set = b;
   }
   if (nset == 2) {   // join the producer stream
     cudaEventRecord(c->ev_join, sp);
@@ -852,7 +866,6 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     c->launches++;
   }
   c->last_nz = D::NZ;
-  c->last_nzs = D::NZS;
   if (c->timing) {
     unsigned long long sw = 0;
     cudaMemcpyAsync(&sw, c->swapcnt.p, 8, cudaMemcpyDeviceToHost, st);
