@@ -972,13 +972,14 @@ struct ContractCfg {
   static constexpr int TP = 16, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 8;
   static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
   static constexpr int NB = Layout<P>::NF;   // B row stride (== the fit operators' row stride)
-  static constexpr int KC = (D::NP % 3 == 0) ? 12 : ((D::NP % 2 == 0) ? 8 : 4);            // k-rows per chunk
+  // k-rows per chunk: 16 where it divides 4 NP (a Z chunk row is then one 128-B line), else 12, 8, 4
+  static constexpr int KC = (D::NP % 4 == 0) ? 16 : (D::NP % 3 == 0) ? 12 : ((D::NP % 2 == 0) ? 8 : 4);
   static constexpr int NCH = 4 * D::NP / KC;
   // Z is stored tile-chunked by k_translate (a tile's block of ZBLK doubles): the Theta part [TP][ZTS]
   // (ZTS == 4 mod 16: conflict-free A fragments), then per K chunk ch the W | dW | S slices [3][TP][KC]
   // (k = component NP + c of zeta(W), zeta(dW), zeta_S).  A pipeline stage = [B chunk | Z chunk], two
-  // bulk copies; the small footprint lets 3 CTAs share an SM.  KC = 8: the halves of rows with bit 1 set
-  // are swapped (conflict-free fragments).
+  // bulk copies; the small footprint lets 3 CTAs share an SM.  Rows are XOR-swizzled in 4-column groups
+  // (KC = 16: by r mod 4; KC = 8: by bit 1 of r) so a half-warp's A fragments hit distinct banks.
   static constexpr int ZTS = D::NP + ((4 - D::NP % 16) + 16) % 16, ZT = TP * ZTS, ZCH = 3 * TP * KC;
   static constexpr int64_t ZBLK = (int64_t)ZT + (int64_t)NCH * ZCH;
   static constexpr size_t SMEM_B = 3 * (size_t)KC * NB;                                       // PD | PSp | PSg
@@ -986,7 +987,7 @@ struct ContractCfg {
   static constexpr size_t SNODE = (7 * D::N + 1) / 2 * 2;   // the patch's nodes [N][3], normals [N][3], weights [N]
   static constexpr size_t SMEM = (ZT + 2 * STG + SNODE) * sizeof(double) + TP * 64;   // + ContractPair[TP]
   static constexpr int MINB = (P <= 8 && SMEM * 3 <= 225 * 1024) ? 3 : 2;   // p = 10: registers (TPW = 4)
-  __host__ __device__ static constexpr int swz(int r) { return KC == 8 ? ((r >> 1) & 1) << 2 : 0; }
+  __host__ __device__ static constexpr int swz(int r) { return KC == 16 ? (r & 3) << 2 : KC == 8 ? ((r >> 1) & 1) << 2 : 0; }
   // position of zeta entry (block b = 0 Theta, 1..4 zeta(W), 5..8 zeta(dW), 9..12 zeta_S; c = (l,m)) of tile row r
   __host__ __device__ static constexpr int64_t zoff(int b, int r, int c) {
     return b == 0 ? (int64_t)r * ZTS + c
