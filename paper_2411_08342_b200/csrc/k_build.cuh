@@ -1,15 +1,17 @@
 // The per-pair hot path, Steps 4-8 + smooth-rule subtraction (A14), as
 // four kernels over a sub-chunk of pairs in patch-major order (s = position in the permutation):
 //
-// k_pair_edge (warp per pair): target frame, harmonics at the target (Step 4), per-edge Newton /
-//   regime / model integrals / SSQ weights (Step 5), the GEMM rows a = omega1 d and
-//   b = omega1 nu' - omega3 (nu'.d) d, the scalar line integrals Omega, Omega_0 and derivatives
-//   (Step 6), and the I[gamma] part of W, dW and the S(r') Omega_0 part of Theta (Step 7).
+// k_pair_setup (thread per pair) + k_pair_edge (warp per 3 pairs, phase-synchronous): target frame,
+//   harmonics at the target (Step 4), per-edge Newton / regime / model integrals / SSQ weights (Step 5),
+//   the GEMM rows a = omega1 d and b = omega1 nu' - omega3 (nu'.d) d (tile-chunked for k_qmap), the scalar
+//   line integrals Omega, Omega_0 and derivatives (Step 6), and the I[gamma] part of W, dW and the
+//   S(r') Omega_0 part of Theta (Step 7).  Runs on a producer stream one sub-chunk ahead of the others.
 // k_qmap (CTA per tile of 16 pairs of one patch): the line-integral maps [Q | V](pair) = a M,
 //   dQ(pair) = b M_Q as one FP64 tensor-core GEMM (mma.sync m8n8k4 f64 = DMMA) against the patch's
 //   operand M (built in k_edge_tables).
-// k_translate (warp per pair): translation (Step 7) -> W, dW, Theta -> contraction vectors zeta.
-// k_contract (CTA per tile of 32 pairs of one patch): Step 8 in matrix mode as DMMA GEMMs
+// k_translate (warp per pair): translation (Step 7) -> W, dW, Theta -> contraction vectors zeta (written
+//   tile-chunked for k_contract).
+// k_contract (CTA per tile of 16 pairs of one patch): Step 8 in matrix mode as DMMA GEMMs
 //   zeta^T [P_D | P_Sp | P_Sd | P_Sg], then smooth subtraction, scaling and the CSR store.
 #pragma once
 #include "rrq_device.cuh"
