@@ -217,6 +217,23 @@ def test_row_chunks_and_masks():
     e = DeviceTargets(dt.x[:0], dt.normal[:0], dt.self_node[:0], dt.side[:0])
     p0, q0 = ctx.near_list(ds, e)
     assert p0.numel() == 1 and q0.numel() == 0
+    # targets with no near patch: empty rows, zero pairs through the whole build
+    far = DeviceTargets((dt.x[:5] * 50.0).contiguous(), dt.normal[:5].contiguous(), None, dt.side[:5].contiguous())
+    pf, qf = ctx.near_list(ds, far)
+    assert int(pf[-1]) == 0 and qf.numel() == 0
+    out = ctx.build_correction(ds, far, pf, qf, fit)
+    assert torch.equal(out["row_ptr"], torch.zeros(6, dtype=torch.int64, device="cuda"))
+    # a row range without pairs inside a non-empty build
+    mix = DeviceTargets(torch.cat([dt.x[:3] * 50.0, dt.x[3:6]]).contiguous(), torch.cat([dt.normal[:3], dt.normal[3:6]]).contiguous(),
+                        torch.cat([torch.full((3,), -1, dtype=torch.int64, device="cuda"), dt.self_node[3:6]]).contiguous(),
+                        torch.cat([dt.side[:3], dt.side[3:6]]).contiguous())
+    pm, qm = ctx.near_list(ds, mix)
+    assert int(pm[3]) == 0 and int(pm[-1]) > 0
+    out0 = ctx.build_correction(ds, mix, pm, qm, fit, row_begin=0, row_end=3)
+    assert torch.equal(out0["row_ptr"], torch.zeros(4, dtype=torch.int64, device="cuda"))
+    out1 = ctx.build_correction(ds, mix, pm, qm, fit)
+    for k in range(4):
+        assert torch.equal(out1["vals"][k][: int(pm[-1]) * n], full["vals"][k][hp[3] * n: hp[6] * n])
 
 
 def test_apply_correction_spmv():
