@@ -691,9 +691,8 @@ __global__ void __launch_bounds__(WPB * 32)
         }
         om[4] += w3 * dot3(nup, txd);
       }
-      for (int i = 0; i < 8; ++i) om[i] = warp_sum(om[i]);
-      if (lane == 0)
-        for (int i = 0; i < 8; ++i) ps.om[i] = om[i];
+      const double red = warp_sum8(om, lane);
+      if ((lane & 3) == 0) ps.om[(lane >> 2) & 7] = red;   // value index 4 b4 + 2 b3 + b2 = (lane >> 2) & 7
     }
     __syncwarp();   // next phase only reads this warp's pairs
     RRQ_PHASE_MARK(2);

@@ -264,5 +264,26 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// Warp sums of 8 values at once by a reduce-scatter butterfly (9 shuffles instead of 8 x 5): on return
+// lane L holds the sum of value 4 b4 + 2 b3 + b2 (b = bits of L), i.e. value (L >> 2) & 7 ... for L in 0..31
+// the value index is ((L >> 4) & 1) * 4 + ((L >> 3) & 1) * 2 + ((L >> 2) & 1).
+__device__ __forceinline__ double warp_sum8(const double (&v)[8], int lane) {
+  const bool b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+  double w[4], x[2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double keep = b4 ? v[4 + j] : v[j], send = b4 ? v[j] : v[4 + j];
+    w[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const double keep = b3 ? w[2 + j] : w[j], send = b3 ? w[j] : w[2 + j];
+    x[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double y = (b2 ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, b2 ? x[0] : x[1], 4);
+  y += __shfl_xor_sync(0xffffffffu, y, 2);
+  y += __shfl_xor_sync(0xffffffffu, y, 1);
+  return y;
+}
 
 }  // namespace rrq
