@@ -38,7 +38,6 @@ __device__ __forceinline__ cd cdiv(cd a, cd b) {
   double s = rcp_nr(b.x * b.x + b.y * b.y);
   return cd{(a.x * b.x + a.y * b.y) * s, (a.y * b.x - a.x * b.y) * s};
 }
-__device__ __forceinline__ double cabs_(cd a) { return hypot(a.x, a.y); }
 // acc += a * b
 __device__ __forceinline__ void cfma(cd &acc, cd a, cd b) {
   acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
@@ -61,7 +60,6 @@ struct Dims {
   static constexpr int NV8 = (2 * NV + 7) / 8 * 8;// V columns (jk, re/im), padded
   static constexpr int NCP = NCQ + NV8;           // whole 8-wide DMMA tiles
   static constexpr int NCS = NCP + ((4 - NCP % 16) + 16) % 16; // row stride == 4 (mod 16): conflict-free B frags
-  static constexpr int NZS = NZ + ((4 - NZ % 16) + 16) % 16;   // Z row stride == 4 (mod 16): conflict-free A frags
 };
 
 // (l, m >= 0) -> flat index
