@@ -1258,7 +1258,9 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 // k_contract: Step 8 in matrix mode (App. A.7) as DMMA GEMMs per tile of TP pairs of one
 // patch: D = zeta(W) P_D, D' = zeta(dW) P_D, S' = zeta_S P_Sp, S = Theta P_Sd + zeta(W) P_Sg, then global
 // units (A2), the smooth-rule subtraction (A14) and the CSR store.  Warp w owns the (M-tile, N-tile)
-// pairs w, w + 16, ...; 4 accumulator tiles (S, D, S', D') each.  Z tile staged in shared memory.
+// pairs w, w + WARPS, ...; 4 accumulator tiles (S, D, S', D') each.  The Theta part of the tile's zeta
+// and, per K chunk, the fit-operator rows with the matching zeta chunk are staged by bulk copies
+// (ContractCfg: tile-chunked zeta written by k_translate), two stages, 3 CTAs per SM at p <= 8.
 // ------------------------------------------------------------------------------------------------
 
 template <int P>
