@@ -497,8 +497,7 @@ __global__ void __launch_bounds__(WPB * 32)
       for (int i = lane; i < kPPW * NS; i += 32) {
         const int pp = i / NS, e = i % NS;
         if (!mine[pp].active) continue;
-        int l = 0;
-        while (sidx(l + 1, 0) <= e) ++l;
+        const int l = tri_inv(e);   // sidx(l, 0) <= e < sidx(l + 1, 0)
         grad_fast(mine[pp].R, l, e - sidx(l, 0), shc, wsc.GS[pp][e]);
       }
       __syncwarp();
@@ -507,8 +506,7 @@ __global__ void __launch_bounds__(WPB * 32)
         const int pp = i / NSX, e = i % NSX;
         PairState<P> &ps = mine[pp];
         if (!ps.active) continue;
-        int l = 0;
-        while (sidx(l + 1, 0) <= e) ++l;
+        const int l = tri_inv(e);   // sidx(l, 0) <= e < sidx(l + 1, 0)
         const int m = e - sidx(l, 0);
         const cd *g = wsc.GS[pp][e];
         const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
@@ -749,8 +747,7 @@ __global__ void __launch_bounds__(WPB * 32)
       const double nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
       const double O0 = ps.om[0], Ov[3] = {ps.om[1], ps.om[2], ps.om[3]}, dO0 = ps.om[4],
                    dOv[3] = {ps.om[5], ps.om[6], ps.om[7]};
-      int l = 1;
-      while (lmidx(l + 1, 1) <= c) ++l;
+      const int l = tri_inv(c) + 1;   // lmidx(l, 1) <= c < lmidx(l + 1, 1)
       const int m = c - lmidx(l, 1) + 1, hs = sidx(l, m);
       const cd *g = wsc.GS[pp][hs];
       cd hn[3];

@@ -257,6 +257,10 @@ __device__ __forceinline__ void cross3(const double *a, const double *b, double 
   c[2] = a[0] * b[1] - a[1] * b[0];
 }
 
+// Inverse of the triangular index t(l) = l (l + 1) / 2: the l with t(l) <= e < t(l + 1) (e < 2^20; the float
+// square root is exact on the perfect squares 8 t(l) + 1 = (2l + 1)^2 that decide the floor).
+__device__ __forceinline__ int tri_inv(int e) { return (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
