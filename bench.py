@@ -318,6 +318,20 @@ def run_ours(args, ws, rank):
     # the build stage's device time: whole rrq_build_correction calls on the caller's stream (k_pair_edge of
     # the next sub-chunk runs concurrently with the GEMM kernels of the current one, so per-kernel times overlap)
     build_ms = tim["ms"].get("build") or sum(tim["ms"][k] for k in ("pair_edge", "qmap", "translate", "contract", "plumbing"))
+    # the kernels' own device times: one extra (untimed) step with the overlap off
+    R.ctx.set_overlap(False)
+    R.ctx.reset_timing()
+    R.ctx.set_timing(True)
+    R.step()
+    torch.cuda.synchronize()
+    tser = R.ctx.timing()
+    R.ctx.set_timing(False)
+    R.ctx.set_overlap(True)
+    for k in per_kernel:
+        ms_k = tser["ms"][k]
+        per_kernel[k]["serial_ms_per_step"] = ms_k
+        per_kernel[k]["serial_tflops"] = kflops[k] / args.steps / (ms_k / 1e3) / 1e12 if ms_k > 0 else None
+        per_kernel[k]["serial_frac"] = (per_kernel[k]["serial_tflops"] or 0) / KERNEL_BOUND[k][1]
     build_tflops = sum(kflops.values()) / (build_ms / 1e3) / 1e12
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -331,7 +345,10 @@ def run_ours(args, ws, rank):
                      "peak_source": KERNEL_BOUND[dom][2],
                      "flops_per_pair": kflops[dom] / pairs_t, "launches": tim["launches"][dom],
                      "build_stage_tflops": build_tflops, "build_stage_frac": build_tflops / FP64_PEAK_TFLOPS,
-                     "per_kernel": per_kernel},
+                     "per_kernel": per_kernel,
+                     "per_kernel_note": "ms_per_step/tflops/frac: timed steps, overlap on (k_pair_edge of sub-chunk i+1 "
+                                        "co-runs with k_qmap/k_translate/k_contract of sub-chunk i); serial_*: one extra "
+                                        "untimed step with the overlap off (the kernels' own device times)"},
         "stages_ms_per_step": {k: v / args.steps for k, v in tim["ms"].items()},
         "pairs_per_s": npairs * args.steps / (ms_max / 1e3) * ws,
         "rows_per_s": R.T * args.steps / (ms_max / 1e3) * ws,

@@ -171,6 +171,11 @@ rrq_status rrq_set_timing(rrq_ctx ctx, int enable);
 rrq_status rrq_get_timing(rrq_ctx ctx, double ms[RRQ_NSTAGES], int64_t launches[RRQ_NSTAGES], int64_t stats[2]);
 rrq_status rrq_reset_timing(rrq_ctx ctx);
 
+/* Producer/consumer overlap of rrq_build_correction (see above) on (1, the default unless the environment
+ * sets RRQ_NO_OVERLAP=1) or off (0: every kernel on the caller's stream, so stages [2]-[5] are the
+ * kernels' own device times).  Results are bit-identical either way. */
+rrq_status rrq_set_overlap(rrq_ctx ctx, int enable);
+
 /* Test hook: copy the internal per-pair contraction vectors of the LAST build sub-chunk to HOST
  * arrays: perm[i] = global pair id of row i, Z[i][13 n_p] = (Theta, zeta(W), zeta(dW), zeta_S) in
  * c-layout.  At most max_pairs rows; returns the row count in *n_out. */

@@ -472,6 +472,12 @@ rrq_status rrq_set_timing(rrq_ctx c, int enable) {
   return RRQ_OK;
 }
 
+rrq_status rrq_set_overlap(rrq_ctx c, int enable) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  c->overlap = enable != 0;
+  return RRQ_OK;
+}
+
 rrq_status rrq_reset_timing(rrq_ctx c) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   t_flush(c);

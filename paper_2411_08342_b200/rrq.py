@@ -73,6 +73,8 @@ def load_library():
     lib.rrq_launch_count.restype = ctypes.c_int64
     lib.rrq_set_timing.argtypes = [vp, ctypes.c_int]
     lib.rrq_set_timing.restype = ctypes.c_int
+    lib.rrq_set_overlap.argtypes = [vp, ctypes.c_int]
+    lib.rrq_set_overlap.restype = ctypes.c_int
     lib.rrq_reset_timing.argtypes = [vp]
     lib.rrq_reset_timing.restype = ctypes.c_int
     lib.rrq_get_timing.argtypes = [vp, vp, vp, vp]
@@ -169,6 +171,9 @@ class RRQ:
 
     def set_timing(self, on=True):
         self._check(self.lib.rrq_set_timing(self.h, int(on)), "rrq_set_timing")
+
+    def set_overlap(self, on=True):
+        self._check(self.lib.rrq_set_overlap(self.h, int(on)), "rrq_set_overlap")
 
     def reset_timing(self):
         self._check(self.lib.rrq_reset_timing(self.h), "rrq_reset_timing")
