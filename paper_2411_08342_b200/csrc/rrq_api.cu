@@ -499,11 +499,9 @@ rrq_status rrq_get_timing(rrq_ctx c, double ms[RRQ_NSTAGES], int64_t launches[RR
 
 rrq_status rrq_get_tables(rrq_ctx c, double *t, double *w, double *U) {
   if (!c) return RRQ_ERR_INVALID_ARG;
-  int q = c->prm.p_edge;
   if (t) std::copy(c->h_t.begin(), c->h_t.end(), t);
   if (w) std::copy(c->h_w.begin(), c->h_w.end(), w);
   if (U) std::copy(c->h_U.begin(), c->h_U.end(), U);
-  (void)q;
   return RRQ_OK;
 }
 
