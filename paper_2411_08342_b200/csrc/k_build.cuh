@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(WPB * 32)
   const double *wS = trtab + TrCfg<P>::WS;
   using L = Layout<P>;
   using XR = XRow<P>;
-  constexpr int Q = D::Q, E = D::E, NP = D::NP, NS = D::NS, K = D::K;
+  constexpr int Q = D::Q, E = D::E, NP = D::NP, NS = D::NS;
   extern __shared__ double smem[];
   double *sU = smem;                  // [Q][Q]
   double *stgl = sU + Q * Q, *swgl = stgl + Q;
