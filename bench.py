@@ -391,21 +391,22 @@ def run_e2e(R, cfg, args, ws):
                 self_node=pin(cfg["self_node"], torch.int64), side=pin(cfg["side"], torch.int8))
     d_in = {k: torch.empty(v.shape, dtype=v.dtype, device="cuda") for k, v in h_in.items()}
     h2d = sum(v.numel() * v.element_size() for v in h_in.values())
-    cap = min(args.chunk_pairs, 4_000_000)
+    cap = min(args.chunk_pairs, int(os.environ.get("RRQ_E2E_CAP", "4000000")))
+    nset = int(os.environ.get("RRQ_E2E_SETS", "2"))
     old_cap = args.chunk_pairs
     args.chunk_pairs = cap
-    sets = [R.alloc_out(cap), R.alloc_out(cap)]
+    sets = [R.alloc_out(cap) for _ in range(nset)]
     n = R.n
     h_out = [dict(col=torch.empty(cap * n, dtype=torch.int32).pin_memory(),
-                  vals=[torch.empty(cap * n, dtype=torch.float64).pin_memory() for _ in range(4)]) for _ in range(2)]
+                  vals=[torch.empty(cap * n, dtype=torch.float64).pin_memory() for _ in range(4)]) for _ in range(nset)]
     copy_stream = torch.cuda.Stream()
     main = torch.cuda.current_stream()
-    done = [torch.cuda.Event(), torch.cuda.Event()]
+    done = [torch.cuda.Event() for _ in range(nset)]
     d2h_bytes = [0]
     slot_of = {}
 
     def on_chunk(when, i, o, np_=0):
-        k = i % 2
+        k = i % nset
         if when == "before":
             main.wait_event(done[k])          # the copy of this buffer's previous chunk has finished
             return

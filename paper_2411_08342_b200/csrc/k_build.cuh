@@ -1493,6 +1493,14 @@ __global__ void k_item_patch(int64_t n_patches, const int64_t *__restrict__ item
   for (int64_t i = items[P]; i < items[P + 1]; ++i) item_patch[i] = (int32_t)P;
 }
 
+// The pair range [pair_ptr[row_begin], pair_ptr[row_end]) of a build call, written to mapped host memory.
+__global__ void k_pair_range(const int64_t *__restrict__ pair_ptr, int64_t row_begin, int64_t row_end, int64_t *out) {
+  if (threadIdx.x == 0) {
+    out[0] = pair_ptr[row_begin];
+    out[1] = pair_ptr[row_end];
+  }
+}
+
 __global__ void k_copy_i64(int64_t n, const int64_t *__restrict__ a, int64_t *__restrict__ b) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = a[i];

@@ -48,6 +48,12 @@ struct rrq_ctx_s {
   bool overlap = true;                             // RRQ_NO_OVERLAP=1 runs everything on the caller's stream
   double scratch_bytes = 24e9;                     // sub-chunk scratch budget (RRQ_SCRATCH_BYTES: test hook)
   Buf balls, cell_cnt, cell_items, patch_cell, tcnt, ptgt, perm, seg, cursor, items, Z, fitwork, one, swapcnt;
+  // Small device->host reads inside rrq_build_correction (the pair range, the per-patch segment and item offsets)
+  // go through mapped pinned memory written by a kernel, not cudaMemcpyAsync: a D2H memcpy queues behind
+  // whatever the caller's own D2H copies hold on the copy engine (an e2e loop copying the previous chunk's
+  // weights out), which would stall this call's host-side planning for the length of that copy.
+  int64_t *hmap = nullptr;
+  size_t hmap_n = 0;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
   double t_ms[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -129,6 +135,20 @@ static bool ensure(rrq_ctx c, rrq_ctx_s::Buf &b, size_t bytes) {
     return false;
   }
   b.n = bytes;
+  return true;
+}
+
+static bool ensure_hmap(rrq_ctx c, size_t n) {
+  if (c->hmap_n >= n) return true;
+  if (c->hmap) cudaFreeHost(c->hmap);
+  c->hmap = nullptr;
+  c->hmap_n = 0;
+  if (cudaHostAlloc((void **)&c->hmap, n * sizeof(int64_t), cudaHostAllocMapped) != cudaSuccess) {
+    cudaGetLastError();
+    c->err = "mapped host allocation of " + std::to_string(n * sizeof(int64_t)) + " bytes failed";
+    return false;
+  }
+  c->hmap_n = n;
   return true;
 }
 
@@ -415,6 +435,7 @@ void rrq_destroy(rrq_ctx c) {
   t_flush(c);
   for (auto e : c->pool) cudaEventDestroy(e);
   if (c->swapcnt.p) cudaFree(c->swapcnt.p);
+  if (c->hmap) cudaFreeHost(c->hmap);
   cudaFree(c->d_tab);
   if (c->d_trtab) cudaFree(c->d_trtab);
   if (c->st2) cudaStreamDestroy(c->st2);
@@ -696,11 +717,11 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   static_assert(QC::TP == CC::TP, "k_qmap and k_contract share the work items");
   const int64_t Pn = s->n_patches;
   const int raw = (mask & RRQ_RAW) ? 1 : 0;
-  int64_t b[2];
-  cudaMemcpyAsync(&b[0], pair_ptr + row_begin, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&b[1], pair_ptr + row_end, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if (!ensure_hmap(c, 2 * (size_t)(Pn + 2))) return RRQ_ERR_CUDA;
+  k_pair_range<<<1, 32, 0, st>>>(pair_ptr, row_begin, row_end, c->hmap);
+  c->launches++;
   cudaStreamSynchronize(st);
-  const int64_t obase = b[0], total = b[1] - b[0];
+  const int64_t obase = c->hmap[0], total = c->hmap[1] - c->hmap[0];
   if (total == 0) {
     if (row_ptr) {
       k_row_ptr<<<nblk(row_end - row_begin + 1, 256), 256, 0, st>>>(row_begin, row_end, pair_ptr, obase, row_ptr, D::N);
@@ -734,11 +755,13 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     cudaMemsetAsync(bp<int64_t>(c->items) + Pn, 0, sizeof(int64_t), st);
     k_scan_i64<<<1, 1024, 0, st>>>(Pn + 1, bp<int64_t>(c->items), bp<int64_t>(c->one) + 1);
     k_item_patch<<<nblk(Pn, 256), 256, 0, st>>>(Pn, bp<int64_t>(c->items), bp<int32_t>(c->ipatch));
-    c->launches += 7;
-    cudaMemcpyAsync(hseg.data(), c->seg.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(hitem.data(), c->items.p, (Pn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    k_copy_i64<<<nblk(Pn + 1, 256), 256, 0, st>>>(Pn + 1, bp<int64_t>(c->seg), c->hmap);
+    k_copy_i64<<<nblk(Pn + 1, 256), 256, 0, st>>>(Pn + 1, bp<int64_t>(c->items), c->hmap + Pn + 1);
+    c->launches += 9;
   }
   cudaStreamSynchronize(st);
+  std::memcpy(hseg.data(), c->hmap, (Pn + 1) * sizeof(int64_t));
+  std::memcpy(hitem.data(), c->hmap + Pn + 1, (Pn + 1) * sizeof(int64_t));
   hseg[Pn] = total;
   // ---- sub-chunks: ranges of whole patches with at most `cap` pairs (scratch ~24 KB per pair at p = 8:
   // the double-buffered pair_edge outputs plus the Q and Z rows)
