@@ -185,6 +185,11 @@ rrq_status rrq_debug_zeta(rrq_ctx ctx, int64_t max_pairs, int64_t *perm, double 
  * integrals, weights, Omega_0 sinh rule, I[gamma]), summed over CTAs, into HOST out[8]; reset if set. */
 rrq_status rrq_debug_phase_cycles(rrq_ctx ctx, uint64_t out[8], int reset);
 
+/* Profiling hook: SM cycles spent by k_patch_fit_q in its phases (node tables, quaternion QR, Q^H e_c,
+ * quaternion back substitution, real QR, Q_B^T e_c, real back substitution, P_Sg), summed over CTAs,
+ * into HOST out[8]; reset if set. */
+rrq_status rrq_debug_fit_cycles(rrq_ctx ctx, uint64_t out[8], int reset);
+
 #ifdef __cplusplus
 }
 #endif

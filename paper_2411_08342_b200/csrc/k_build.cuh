@@ -65,8 +65,8 @@ __device__ __noinline__ void model_integrals(double a, double b, double *I, doub
 }
 
 // Phase profiling of k_pair_edge (SM cycles between the CTA barriers, accumulated by thread 0 of each
-// CTA; read back with rrq_debug_phase_cycles).
-__device__ unsigned long long g_phase_cycles[8];
+// CTA; read back with rrq_debug_phase_cycles); slots 8-15: k_patch_fit_q's phases (rrq_debug_fit_cycles).
+__device__ unsigned long long g_phase_cycles[16];
 #define RRQ_PHASE_MARK(ph)                                                         \
   if (threadIdx.x == 0) {                                                          \
     const long long now = clock64();                                               \

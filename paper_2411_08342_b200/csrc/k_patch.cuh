@@ -265,16 +265,18 @@ template <int P>
 struct FitCfg {
   using D = Dims<P>;
   static constexpr int N = D::N, NP = D::NP;
-  // shared: Fq [NP][N][4] | rd [NP][4] | beta [NP] | rdb [NP] | betab [NP] | xl,nl [N][3] | sh [64]
+  // shared: Fq [NP][N][4] | rd [NP][4] | beta [NP] | rdb [NP] | betab [NP] | xl,nl [N][3] | sh [64] |
+  // vd [NP][4] | cn2 [NP + 1]
   static constexpr size_t FQ = (size_t)NP * N * 4, RD = 4 * NP;
-  static constexpr size_t SMEM_D = FQ + RD + 3 * NP + 6 * N + 64;
+  static constexpr size_t SMEM_D = FQ + RD + 3 * NP + 6 * N + 64 + 4 * NP + NP + 1;
   static constexpr size_t SMEM = SMEM_D * sizeof(double);
+  static constexpr int MINB = 2 * SMEM <= 227 * 1024 ? 2 : 1;   // CTAs per SM the shared memory allows
   // per-CTA global workspace (doubles): W [N][N][4] | Xs [N][N] | B [NP][N] | Hm [N][NP]
   static constexpr int64_t WS = (int64_t)N * N * 4 + (int64_t)N * N + 2 * (int64_t)N * NP;
 };
 
 template <int P>
-__global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const double *__restrict__ nodes,
+__global__ void __launch_bounds__(256, FitCfg<P>::MINB) k_patch_fit_q(int64_t n_patches, const double *__restrict__ nodes,
                                                      const double *__restrict__ normals,
                                                      const double *__restrict__ hc, double *__restrict__ fit,
                                                      double *__restrict__ work, int32_t *__restrict__ status) {
@@ -289,11 +291,13 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
   double *rdb = beta + NP, *betab = rdb + NP;
   double *xl = betab + NP, *nl = xl + 3 * N;
   double *sh = nl + 3 * N;              // [32] reductions
+  double *vd = sh + 64, *cn2 = vd + 4 * NP;   // QR pivots v_j, squared column norms
   double *W = work + blockIdx.x * FC::WS;       // [N][N][4]: Q^H e_c
   double *Xs = W + (int64_t)N * N * 4;          // [N][N] real workspace (B system)
   double *Bm = Xs + (int64_t)N * N;             // [NP][N] column-major real B
   double *Hm = Bm + (int64_t)NP * N;            // [N][NP]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  long long ph_t = clock64();
   for (int64_t Pp = blockIdx.x; Pp < n_patches; Pp += gridDim.x) {
     double *blk = fit + Pp * (int64_t)L::STRIDE;
     const double *o = blk + L::HDR + H_O, *Rm = blk + L::HDR + H_RM;
@@ -324,87 +328,127 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
         }
     }
     __syncthreads();
-    // ---- quaternion Householder QR of Fq (N x NP)
+    RRQ_PHASE_MARK(8);
+    // ---- quaternion Householder QR of Fq (N x NP), one barrier per column: every thread derives column j's
+    // reflector (u, |x_1|, ||x||) itself from the squared norm cn2[j] that warp 0 left when it updated column
+    // j in step j - 1; the pivot entry v_j = u (|x_1| + ||x||) is kept in registers during the step and
+    // written back (vd) after the loop
+    if (warp == 0) {
+      double s2 = 0;
+      for (int i = lane; i < N; i += 32) {
+        const qd a = qld(Fq + (size_t)i * 4);
+        s2 += a.s * a.s + a.x * a.x + a.y * a.y + a.z * a.z;
+      }
+      s2 = warp_sum(s2);
+      if (lane == 0) cn2[0] = s2;
+    }
+    __syncthreads();
     for (int j = 0; j < NP; ++j) {
-      double s = 0;
-      for (int i = j + threadIdx.x; i < N; i += blockDim.x) {
-        const qd a = qld(Fq + ((size_t)j * N + i) * 4);
-        s += a.s * a.s + a.x * a.x + a.y * a.y + a.z * a.z;
-      }
-      s = warp_sum(s);
-      if (lane == 0) sh[warp] = s;
-      __syncthreads();
+      const double nrm = sqrt(cn2[j]);
+      const qd x1 = qld(Fq + ((size_t)j * N + j) * 4);
+      const double a = sqrt(x1.s * x1.s + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
+      const qd u = a > 0 ? qd{x1.s / a, x1.x / a, x1.y / a, x1.z / a} : qd{1, 0, 0, 0};
+      const double f = a + nrm;
+      const qd vj = {u.s * f, u.x * f, u.y * f, u.z * f};
+      const double bj = nrm * (nrm + a);
       if (threadIdx.x == 0) {
-        double n2 = 0;
-        for (int w = 0; w < nw; ++w) n2 += sh[w];
-        const double nrm = sqrt(n2);
-        qd x1 = qld(Fq + ((size_t)j * N + j) * 4);
-        const double a = sqrt(x1.s * x1.s + x1.x * x1.x + x1.y * x1.y + x1.z * x1.z);
-        const qd u = a > 0 ? qd{x1.s / a, x1.x / a, x1.y / a, x1.z / a} : qd{1, 0, 0, 0};
-        const double f = a + nrm;
-        qst(Fq + ((size_t)j * N + j) * 4, qd{u.s * f, u.x * f, u.y * f, u.z * f});
+        qst(vd + 4 * j, vj);
         qst(rd + 4 * j, qd{-u.s * nrm, -u.x * nrm, -u.y * nrm, -u.z * nrm});
-        beta[j] = nrm * (nrm + a);
+        beta[j] = bj;
       }
-      __syncthreads();
-      const double bj = beta[j];
-      if (bj > 0)
-        for (int c = j + 1 + warp; c < NP; c += nw) {
-          qd t = {0, 0, 0, 0};
+      // two columns per warp per pass (c0 and c0 + nw) so their reductions interleave
+      for (int c0 = j + 1 + warp; c0 < NP; c0 += 2 * nw) {
+        const int c1 = c0 + nw;
+        const bool two = c1 < NP;
+        double s2 = 0;
+        if (bj > 0) {
+          qd t0 = {0, 0, 0, 0}, t1 = {0, 0, 0, 0};
           for (int i = j + lane; i < N; i += 32) {
-            const qd p = qconjmul_(qld(Fq + ((size_t)j * N + i) * 4), qld(Fq + ((size_t)c * N + i) * 4));
-            t.s += p.s; t.x += p.x; t.y += p.y; t.z += p.z;
+            const qd vi = i == j ? vj : qld(Fq + ((size_t)j * N + i) * 4);
+            const qd p0 = qconjmul_(vi, qld(Fq + ((size_t)c0 * N + i) * 4));
+            t0.s += p0.s; t0.x += p0.x; t0.y += p0.y; t0.z += p0.z;
+            if (two) {
+              const qd p1 = qconjmul_(vi, qld(Fq + ((size_t)c1 * N + i) * 4));
+              t1.s += p1.s; t1.x += p1.x; t1.y += p1.y; t1.z += p1.z;
+            }
           }
-          t.s = warp_sum(t.s) / bj; t.x = warp_sum(t.x) / bj; t.y = warp_sum(t.y) / bj; t.z = warp_sum(t.z) / bj;
+          const double ib = 1.0 / bj;
+          t0.s = warp_sum(t0.s) * ib; t0.x = warp_sum(t0.x) * ib; t0.y = warp_sum(t0.y) * ib; t0.z = warp_sum(t0.z) * ib;
+          if (two) {
+            t1.s = warp_sum(t1.s) * ib; t1.x = warp_sum(t1.x) * ib; t1.y = warp_sum(t1.y) * ib; t1.z = warp_sum(t1.z) * ib;
+          }
           for (int i = j + lane; i < N; i += 32) {
-            double *y = Fq + ((size_t)c * N + i) * 4;
-            const qd vt = qmul_(qld(Fq + ((size_t)j * N + i) * 4), t);
-            y[0] -= vt.s; y[1] -= vt.x; y[2] -= vt.y; y[3] -= vt.z;
+            const qd vi = i == j ? vj : qld(Fq + ((size_t)j * N + i) * 4);
+            double *y = Fq + ((size_t)c0 * N + i) * 4;
+            const qd vt = qmul_(vi, t0);
+            const qd yn = {y[0] - vt.s, y[1] - vt.x, y[2] - vt.y, y[3] - vt.z};
+            qst(y, yn);
+            if (c0 == j + 1 && i > j) s2 += yn.s * yn.s + yn.x * yn.x + yn.y * yn.y + yn.z * yn.z;
+            if (two) {
+              double *y1 = Fq + ((size_t)c1 * N + i) * 4;
+              const qd vt1 = qmul_(vi, t1);
+              qst(y1, qd{y1[0] - vt1.s, y1[1] - vt1.x, y1[2] - vt1.y, y1[3] - vt1.z});
+            }
+          }
+        } else if (c0 == j + 1) {
+          for (int i = j + 1 + lane; i < N; i += 32) {
+            const qd yn = qld(Fq + ((size_t)c0 * N + i) * 4);
+            s2 += yn.s * yn.s + yn.x * yn.x + yn.y * yn.y + yn.z * yn.z;
           }
         }
+        if (c0 == j + 1) {
+          s2 = warp_sum(s2);
+          if (lane == 0) cn2[j + 1] = s2;
+        }
+      }
       __syncthreads();
     }
-    // ---- Q^H e_c (warp per pair of columns, the columns in registers: entry i = lane + 32 u), the first
+    for (int j = threadIdx.x; j < NP; j += blockDim.x) qst(Fq + ((size_t)j * N + j) * 4, qld(vd + 4 * j));
+    __syncthreads();
+    RRQ_PHASE_MARK(9);
+    // ---- Q^H e_c (warp per four columns, the columns in registers: entry i = lane + 32 u), the first
     // NP entries stored for the back substitution
     {
-      constexpr int NU = (N + 31) / 32;
-      for (int c0 = 2 * warp; c0 < N; c0 += 2 * nw) {
-        qd y[2][NU];
+      constexpr int NU = (N + 31) / 32, CW = 4;
+      for (int c0 = CW * warp; c0 < N; c0 += CW * nw) {
+        qd y[CW][NU];
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < CW; ++h)
 #pragma unroll
           for (int u = 0; u < NU; ++u) y[h][u] = qd{lane + 32 * u == c0 + h ? 1.0 : 0.0, 0, 0, 0};
         for (int j = 0; j < NP; ++j) {
           const double bj = beta[j];
           if (!(bj > 0)) continue;
           qd v[NU];
-          qd t[2] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+          qd t[CW];
+#pragma unroll
+          for (int h = 0; h < CW; ++h) t[h] = qd{0, 0, 0, 0};
 #pragma unroll
           for (int u = 0; u < NU; ++u) {
             const int i = lane + 32 * u;
             v[u] = (i >= j && i < N) ? qld(Fq + ((size_t)j * N + i) * 4) : qd{0, 0, 0, 0};
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < CW; ++h) {
               const qd p = qconjmul_(v[u], y[h][u]);
               t[h].s += p.s; t[h].x += p.x; t[h].y += p.y; t[h].z += p.z;
             }
           }
           const double ib = 1.0 / bj;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < CW; ++h) {
             t[h].s = warp_sum(t[h].s) * ib; t[h].x = warp_sum(t[h].x) * ib;
             t[h].y = warp_sum(t[h].y) * ib; t[h].z = warp_sum(t[h].z) * ib;
           }
 #pragma unroll
           for (int u = 0; u < NU; ++u)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < CW; ++h) {
               const qd vt = qmul_(v[u], t[h]);
               y[h][u].s -= vt.s; y[h][u].x -= vt.x; y[h][u].y -= vt.y; y[h][u].z -= vt.z;
             }
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < CW; ++h) {
           if (c0 + h >= N) continue;
           double *w = W + (size_t)(c0 + h) * N * 4;
 #pragma unroll
@@ -414,36 +458,64 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
       }
     }
     __syncthreads();
-    // ---- back substitution R x = (Q^H e_c)[0:NP], one thread per column c; x_r = rd_r^{-1}(w_r - sum R_rk x_k)
+    RRQ_PHASE_MARK(10);
+    // ---- back substitution R x = (Q^H e_c)[0:NP], column-oriented with four threads per column c: thread g
+    // keeps s_k (k = g mod 4) in registers; for r = NP-1 .. 0 the owner of r forms x_r = rd_r^{-1} s_r,
+    // broadcasts it to the column's threads, and each subtracts R_kr x_r from its s_k, k < r
     constexpr int NF = L::NF;   // row stride of the fit operators
     double *PD = blk + L::FIT, *PSp = PD + 4 * NP * NF, *PSd = PD + 8 * NP * NF, *PSg = PD + 9 * NP * NF;
-    for (int c = threadIdx.x; c < N; c += blockDim.x) {
-      double *w = W + (size_t)c * N * 4;
-      const double n0 = nl[3 * c], n1 = nl[3 * c + 1], n2 = nl[3 * c + 2];
-      for (int r = NP - 1; r >= 0; --r) {
-        qd s = qld(w + 4 * r);
-        for (int k = r + 1; k < NP; ++k) {
-          const qd p = qmul_(qld(Fq + ((size_t)k * N + r) * 4), qld(w + 4 * k));
-          s.s -= p.s; s.x -= p.x; s.y -= p.y; s.z -= p.z;
+    {
+      constexpr int G = 4, NR = (NP + G - 1) / G;
+      const int g = threadIdx.x & (G - 1), cpb = blockDim.x / G;
+      for (int cb = 0; cb < N; cb += cpb) {
+        const int c = cb + threadIdx.x / G;
+        const bool ok = c < N;
+        const double *w = W + (size_t)(ok ? c : 0) * N * 4;
+        qd sk[NR];
+#pragma unroll
+        for (int u = 0; u < NR; ++u) {
+          const int k = g + G * u;
+          sk[u] = (ok && k < NP) ? qld(w + 4 * k) : qd{0, 0, 0, 0};
         }
-        const qd d = qld(rd + 4 * r);
-        const double dn = d.s * d.s + d.x * d.x + d.y * d.y + d.z * d.z;
-        const qd x = qconjmul_(d, s);
-        const qd xr = {x.s / dn, x.x / dn, x.y / dn, x.z / dn};
-        qst(w + 4 * r, xr);
-        // P_D (RHS (mu,0)) and P_Sp (RHS (0, sigma nu))
-        PD[(0 * NP + r) * NF + c] = xr.s;
-        PD[(1 * NP + r) * NF + c] = xr.x;
-        PD[(2 * NP + r) * NF + c] = xr.y;
-        PD[(3 * NP + r) * NF + c] = xr.z;
-        const qd sp = qmul_(xr, qd{0.0, n0, n1, n2});
-        PSp[(0 * NP + r) * NF + c] = sp.s;
-        PSp[(1 * NP + r) * NF + c] = sp.x;
-        PSp[(2 * NP + r) * NF + c] = sp.y;
-        PSp[(3 * NP + r) * NF + c] = sp.z;
+        const double n0 = ok ? nl[3 * c] : 0.0, n1 = ok ? nl[3 * c + 1] : 0.0, n2 = ok ? nl[3 * c + 2] : 0.0;
+#pragma unroll
+        for (int r = NP - 1; r >= 0; --r) {
+          const int ow = r % G, ur = r / G;
+          qd x = {0, 0, 0, 0};
+          if (g == ow) {
+            const qd d = qld(rd + 4 * r);
+            const double idn = 1.0 / (d.s * d.s + d.x * d.x + d.y * d.y + d.z * d.z);
+            const qd q = qconjmul_(d, sk[ur]);
+            x = qd{q.s * idn, q.x * idn, q.y * idn, q.z * idn};
+            if (ok) {
+              // P_D (RHS (mu,0)) and P_Sp (RHS (0, sigma nu))
+              PD[(0 * NP + r) * NF + c] = x.s;
+              PD[(1 * NP + r) * NF + c] = x.x;
+              PD[(2 * NP + r) * NF + c] = x.y;
+              PD[(3 * NP + r) * NF + c] = x.z;
+              const qd sp = qmul_(x, qd{0.0, n0, n1, n2});
+              PSp[(0 * NP + r) * NF + c] = sp.s;
+              PSp[(1 * NP + r) * NF + c] = sp.x;
+              PSp[(2 * NP + r) * NF + c] = sp.y;
+              PSp[(3 * NP + r) * NF + c] = sp.z;
+            }
+          }
+          const int src = (lane & ~(G - 1)) | ow;
+          x.s = __shfl_sync(0xffffffffu, x.s, src); x.x = __shfl_sync(0xffffffffu, x.x, src);
+          x.y = __shfl_sync(0xffffffffu, x.y, src); x.z = __shfl_sync(0xffffffffu, x.z, src);
+#pragma unroll
+          for (int u = 0; u < NR; ++u) {
+            const int k = g + G * u;
+            if (G * u < r && k < r) {
+              const qd p = qmul_(qld(Fq + ((size_t)r * N + k) * 4), x);
+              sk[u].s -= p.s; sk[u].x -= p.x; sk[u].y -= p.y; sk[u].z -= p.z;
+            }
+          }
+        }
       }
     }
     __syncthreads();
+    RRQ_PHASE_MARK(11);
     // ---- the real part runs in shared memory (the Fq space is free now): B, then Xs, Hm (then HP over Xs)
     double *const sBm = Fq, *const sXs = Fq + (size_t)NP * N, *const sHm = sXs + (size_t)N * N;
     for (int i = threadIdx.x; i < NP * N; i += blockDim.x) {
@@ -451,33 +523,48 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
       sHm[i] = Hm[i];
     }
     __syncthreads();
-    // ---- real Householder QR of B (N x NP, column-major in sBm) -> P_Sd = B^+
+    // ---- real Householder QR of B (N x NP, column-major in sBm) -> P_Sd = B^+; one barrier per column as
+    // in the quaternion QR (cn2: squared norms from warp 0, pivots kept in registers, written back after)
+    if (warp == 0) {
+      double s2 = 0;
+      for (int i = lane; i < N; i += 32) s2 += sBm[i] * sBm[i];
+      s2 = warp_sum(s2);
+      if (lane == 0) cn2[0] = s2;
+    }
+    __syncthreads();
     for (int j = 0; j < NP; ++j) {
-      double s = 0;
-      for (int i = j + threadIdx.x; i < N; i += blockDim.x) s += sBm[(size_t)j * N + i] * sBm[(size_t)j * N + i];
-      s = warp_sum(s);
-      if (lane == 0) sh[warp] = s;
-      __syncthreads();
+      const double nrm = sqrt(cn2[j]), ajj = sBm[(size_t)j * N + j];
+      const double alpha = ajj > 0 ? -nrm : nrm;
+      const double vj = ajj - alpha, bj = nrm * (nrm + fabs(ajj));
       if (threadIdx.x == 0) {
-        double n2 = 0;
-        for (int w = 0; w < nw; ++w) n2 += sh[w];
-        const double nrm = sqrt(n2), ajj = sBm[(size_t)j * N + j];
-        const double alpha = ajj > 0 ? -nrm : nrm;
-        sBm[(size_t)j * N + j] = ajj - alpha;
+        vd[j] = vj;
         rdb[j] = alpha;
-        betab[j] = nrm * (nrm + fabs(ajj));
+        betab[j] = bj;
+      }
+      for (int c = j + 1 + warp; c < NP; c += nw) {
+        double s2 = 0;
+        if (bj > 0) {
+          double t = 0;
+          for (int i = j + lane; i < N; i += 32) t += (i == j ? vj : sBm[(size_t)j * N + i]) * sBm[(size_t)c * N + i];
+          t = warp_sum(t) / bj;
+          for (int i = j + lane; i < N; i += 32) {
+            const double yn = sBm[(size_t)c * N + i] - t * (i == j ? vj : sBm[(size_t)j * N + i]);
+            sBm[(size_t)c * N + i] = yn;
+            if (c == j + 1 && i > j) s2 += yn * yn;
+          }
+        } else if (c == j + 1) {
+          for (int i = j + 1 + lane; i < N; i += 32) s2 += sBm[(size_t)c * N + i] * sBm[(size_t)c * N + i];
+        }
+        if (c == j + 1) {
+          s2 = warp_sum(s2);
+          if (lane == 0) cn2[j + 1] = s2;
+        }
       }
       __syncthreads();
-      const double bj = betab[j];
-      if (bj > 0)
-        for (int c = j + 1 + warp; c < NP; c += nw) {
-          double t = 0;
-          for (int i = j + lane; i < N; i += 32) t += sBm[(size_t)j * N + i] * sBm[(size_t)c * N + i];
-          t = warp_sum(t) / bj;
-          for (int i = j + lane; i < N; i += 32) sBm[(size_t)c * N + i] -= t * sBm[(size_t)j * N + i];
-        }
-      __syncthreads();
     }
+    for (int j = threadIdx.x; j < NP; j += blockDim.x) sBm[(size_t)j * N + j] = vd[j];
+    __syncthreads();
+    RRQ_PHASE_MARK(12);
     {   // Q_B^T e_c, four columns per warp in registers (entry i = lane + 32 u)
       constexpr int NU = (N + 31) / 32, CW = 4;
       for (int c0 = CW * warp; c0 < N; c0 += CW * nw) {
@@ -518,6 +605,7 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
       }
     }
     __syncthreads();
+    RRQ_PHASE_MARK(13);
     for (int c = threadIdx.x; c < N; c += blockDim.x) {
       double *w = sXs + (size_t)c * N;
       for (int r = NP - 1; r >= 0; --r) {
@@ -528,6 +616,7 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
       }
     }
     __syncthreads();
+    RRQ_PHASE_MARK(14);
     // ---- P_Sg = P_D (sHm P_Sd); HP over the (now dead) Xs
     double *HP = sXs;
     for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
@@ -554,6 +643,7 @@ __global__ void __launch_bounds__(256) k_patch_fit_q(int64_t n_patches, const do
       status[Pp] = (rmin <= 1e-13 * rmax || bmin <= 1e-13 * bmax) ? 1 : 0;
     }
     __syncthreads();
+    RRQ_PHASE_MARK(15);
   }
 }
 

@@ -487,6 +487,17 @@ rrq_status rrq_debug_phase_cycles(rrq_ctx c, uint64_t out[8], int reset) {
   return cuda_check(c, "rrq_debug_phase_cycles");
 }
 
+rrq_status rrq_debug_fit_cycles(rrq_ctx c, uint64_t out[8], int reset) {
+  if (!c) return RRQ_ERR_INVALID_ARG;
+  cudaDeviceSynchronize();
+  if (out) cudaMemcpyFromSymbol(out, g_phase_cycles, 8 * sizeof(uint64_t), 8 * sizeof(uint64_t));
+  if (reset) {
+    uint64_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z), 8 * sizeof(uint64_t));
+  }
+  return cuda_check(c, "rrq_debug_fit_cycles");
+}
+
 rrq_status rrq_set_timing(rrq_ctx c, int enable) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   c->timing = enable != 0;
