@@ -406,10 +406,10 @@ __global__ void __launch_bounds__(256, FitCfg<P>::MINB) k_patch_fit_q(int64_t n_
     for (int j = threadIdx.x; j < NP; j += blockDim.x) qst(Fq + ((size_t)j * N + j) * 4, qld(vd + 4 * j));
     __syncthreads();
     RRQ_PHASE_MARK(9);
-    // ---- Q^H e_c (warp per four columns, the columns in registers: entry i = lane + 32 u), the first
+    // ---- Q^H e_c (warp per two or four columns, the columns in registers: entry i = lane + 32 u), the first
     // NP entries stored for the back substitution
     {
-      constexpr int NU = (N + 31) / 32, CW = 4;
+      constexpr int NU = (N + 31) / 32, CW = FC::MINB == 2 ? 2 : 4;   // 2 under the 128-register bound
       for (int c0 = CW * warp; c0 < N; c0 += CW * nw) {
         qd y[CW][NU];
 #pragma unroll

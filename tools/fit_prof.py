@@ -13,5 +13,5 @@ lib.rrq_debug_fit_cycles(res['ctx'].h, out.ctypes.data, 1)
 tot = out.sum()
 names = ['node tables', 'quaternion QR', 'Q^H e_c', 'quat backsub', 'real QR', 'Q_B^T e_c', 'real backsub', 'HP + P_Sg']
 for i, n in enumerate(names):
-    print('%-14s %5.1f%%' % (n, 100 * out[i] / tot))
+    print('%-14s %5.1f%%  %8.1f kcycles/patch-CTA' % (n, 100 * out[i] / tot, out[i] / 1e3 / cfg['surface'].n_patches))
 print('patches', cfg['surface'].n_patches)
