@@ -541,21 +541,30 @@ __global__ void __launch_bounds__(256, FitCfg<P>::MINB) k_patch_fit_q(int64_t n_
         rdb[j] = alpha;
         betab[j] = bj;
       }
-      for (int c = j + 1 + warp; c < NP; c += nw) {
+      for (int c0 = j + 1 + warp; c0 < NP; c0 += 2 * nw) {   // two columns per pass, as above
+        const int c1 = c0 + nw;
+        const bool two = c1 < NP;
         double s2 = 0;
         if (bj > 0) {
-          double t = 0;
-          for (int i = j + lane; i < N; i += 32) t += (i == j ? vj : sBm[(size_t)j * N + i]) * sBm[(size_t)c * N + i];
-          t = warp_sum(t) / bj;
+          double t0 = 0, t1 = 0;
           for (int i = j + lane; i < N; i += 32) {
-            const double yn = sBm[(size_t)c * N + i] - t * (i == j ? vj : sBm[(size_t)j * N + i]);
-            sBm[(size_t)c * N + i] = yn;
-            if (c == j + 1 && i > j) s2 += yn * yn;
+            const double vi = i == j ? vj : sBm[(size_t)j * N + i];
+            t0 += vi * sBm[(size_t)c0 * N + i];
+            if (two) t1 += vi * sBm[(size_t)c1 * N + i];
           }
-        } else if (c == j + 1) {
-          for (int i = j + 1 + lane; i < N; i += 32) s2 += sBm[(size_t)c * N + i] * sBm[(size_t)c * N + i];
+          t0 = warp_sum(t0) / bj;
+          if (two) t1 = warp_sum(t1) / bj;
+          for (int i = j + lane; i < N; i += 32) {
+            const double vi = i == j ? vj : sBm[(size_t)j * N + i];
+            const double yn = sBm[(size_t)c0 * N + i] - t0 * vi;
+            sBm[(size_t)c0 * N + i] = yn;
+            if (c0 == j + 1 && i > j) s2 += yn * yn;
+            if (two) sBm[(size_t)c1 * N + i] -= t1 * vi;
+          }
+        } else if (c0 == j + 1) {
+          for (int i = j + 1 + lane; i < N; i += 32) s2 += sBm[(size_t)c0 * N + i] * sBm[(size_t)c0 * N + i];
         }
-        if (c == j + 1) {
+        if (c0 == j + 1) {
           s2 = warp_sum(s2);
           if (lane == 0) cn2[j + 1] = s2;
         }
