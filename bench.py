@@ -79,6 +79,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-pairs", type=int, default=48000)
+    ap.add_argument("--mask", type=int, default=None,
+                    help="kernel mask (1 S, 2 D, 4 S', 8 D'); default all four, S|D for config 7 (no target normals)")
     return ap.parse_args()
 
 
@@ -180,11 +182,13 @@ def make_inputs(args, rank):
     return make_config(args.config, seed_offset=rank, **kw)
 
 
-def cfg_desc(cfg, npairs, T):
+def cfg_desc(cfg, npairs, T, mask=None):
     S = cfg["surface"]
+    mask = cfg.get("mask", 15) if mask is None else mask
     return {"workload": cfg["name"], "patches": int(S.n_patches), "p": int(S.p), "p_edge": int(S.q),
             "nodes": int(S.n_patches * S.n), "targets": int(T), "pairs": int(npairs) if npairs is not None else None, "eta": cfg["eta"],
-            "kernels": "S,D,Sp,Dp", "l2": _l2_note(S, npairs)}
+            "kernels": ",".join(k for i, k in enumerate(("S", "D", "Sp", "Dp")) if (mask >> i) & 1),
+            "l2": _l2_note(S, npairs)}
 
 
 def _l2_note(S, npairs):
@@ -212,6 +216,9 @@ class Runner:
         self.ds = DeviceSurface.from_numpy(S)
         self.dt = DeviceTargets.from_numpy(cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
         self.T = self.dt.n_targets
+        m = getattr(args, "mask", None)
+        self.mask = m if m is not None else cfg.get("mask", 15)
+        self.nk = bin(self.mask).count("1")
         self.bufs = None
         self.stream = torch.cuda.current_stream()
 
@@ -220,7 +227,8 @@ class Runner:
         n = self.n
         return dict(row_ptr=t.empty(self.T + 1, dtype=t.int64, device="cuda"),
                     col_idx=t.empty(cap * n, dtype=t.int32, device="cuda"),
-                    vals=[t.empty(cap * n, dtype=t.float64, device="cuda") for _ in range(4)],
+                    vals=[t.empty(cap * n, dtype=t.float64, device="cuda") if (self.mask >> k) & 1 else None
+                          for k in range(4)],
                     status=t.empty(cap, dtype=t.int32, device="cuda"))
 
     def chunks(self, hptr, cap):
@@ -237,6 +245,8 @@ class Runner:
     def step(self, out_sets=None, on_chunk=None):
         """One pass: near list, patch fit, build over all row chunks."""
         ptr, pat = self.ctx.near_list(self.ds, self.dt)
+        if on_chunk is not None:
+            on_chunk("near", -1, (ptr, pat))
         fit, fst = self.ctx.patch_fit(self.ds)
         hptr = ptr.cpu().numpy()
         cap = self.args.chunk_pairs
@@ -247,7 +257,7 @@ class Runner:
             if on_chunk is not None:
                 on_chunk("before", i, o)
             rp = o["row_ptr"][: r1 - r0 + 1]
-            self.ctx.build_correction(self.ds, self.dt, ptr, pat, fit, row_begin=r0, row_end=r1,
+            self.ctx.build_correction(self.ds, self.dt, ptr, pat, fit, mask=self.mask, row_begin=r0, row_end=r1,
                                       out=dict(row_ptr=rp, col_idx=o["col_idx"], vals=o["vals"], status=o["status"]))
             if on_chunk is not None:
                 on_chunk("after", i, o, int(hptr[r1] - hptr[r0]))
@@ -270,7 +280,7 @@ def run_ours(args, ws, rank):
         R.step()
     torch.cuda.synchronize()
     npairs = R.npairs
-    weights_per_step = npairs * R.n * 4
+    weights_per_step = npairs * R.n * R.nk
     # timed region
     clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     R.ctx.reset_timing()
@@ -337,7 +347,7 @@ def run_ours(args, ws, rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generator synth/configs.py; BASELINE.json configs[3] shape)",
-        "config": dict(cfg_desc(cfg, npairs, R.T), parallelism=f"replicas{ws}" if ws > 1 else "single",
+        "config": dict(cfg_desc(cfg, npairs, R.T, R.mask), parallelism=f"replicas{ws}" if ws > 1 else "single",
                        step="near_list+patch_fit+build(all rows, chunked)", chunk_pairs=args.chunk_pairs),
         "roofline": {"bound": KERNEL_BOUND[dom][0], "kernel": "k_" + dom, "achieved": achieved,
                      "peak": KERNEL_BOUND[dom][1], "unit": "TFLOP/s", "frac": achieved / KERNEL_BOUND[dom][1],
@@ -378,8 +388,11 @@ def run_ours(args, ws, rank):
 
 
 def run_e2e(R, cfg, args, ws):
-    """Same metric with host buffers: pinned host inputs copied H2D each step, every chunk's CSR copied
-    D2H (overlapped on a copy stream, double-buffered device outputs)."""
+    """Same metric with host buffers: pinned host inputs copied H2D each step; the host receives the CSR as
+    (pair_ptr, pair_patch, values): pair_ptr (read by the step itself for the row chunking) and pair_patch once
+    per step, every chunk's masked value arrays D2H (overlapped on a copy stream, double-buffered device
+    outputs).  col_idx and row_ptr are implied (col = patch * n + local, row_ptr = pair_ptr * n; include/rrq.h)
+    and are not shipped."""
     import torch
     from paper_2411_08342_b200 import DeviceSurface, DeviceTargets
     S = cfg["surface"]
@@ -397,15 +410,24 @@ def run_e2e(R, cfg, args, ws):
     args.chunk_pairs = cap
     sets = [R.alloc_out(cap) for _ in range(nset)]
     n = R.n
-    h_out = [dict(col=torch.empty(cap * n, dtype=torch.int32).pin_memory(),
-                  vals=[torch.empty(cap * n, dtype=torch.float64).pin_memory() for _ in range(4)]) for _ in range(nset)]
+    h_out = [dict(vals=[torch.empty(cap * n, dtype=torch.float64).pin_memory() if (R.mask >> j) & 1 else None
+                        for j in range(4)]) for _ in range(nset)]
+    h_pat = torch.empty(max(R.npairs, 1), dtype=torch.int32).pin_memory()
     copy_stream = torch.cuda.Stream()
     main = torch.cuda.current_stream()
     done = [torch.cuda.Event() for _ in range(nset)]
     d2h_bytes = [0]
-    slot_of = {}
 
     def on_chunk(when, i, o, np_=0):
+        if when == "near":
+            ptr, pat = o
+            ev = torch.cuda.Event()
+            ev.record(main)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(ev)
+                h_pat[: pat.numel()].copy_(pat, non_blocking=True)
+            d2h_bytes[0] += pat.numel() * 4 + ptr.numel() * 8     # pair_patch here, pair_ptr by the step's .cpu()
+            return
         k = i % nset
         if when == "before":
             main.wait_event(done[k])          # the copy of this buffer's previous chunk has finished
@@ -415,11 +437,11 @@ def run_e2e(R, cfg, args, ws):
         with torch.cuda.stream(copy_stream):
             copy_stream.wait_event(ev)
             m = np_ * n
-            h_out[k]["col"][:m].copy_(o["col_idx"][:m], non_blocking=True)
             for j in range(4):
-                h_out[k]["vals"][j][:m].copy_(o["vals"][j][:m], non_blocking=True)
+                if h_out[k]["vals"][j] is not None:
+                    h_out[k]["vals"][j][:m].copy_(o["vals"][j][:m], non_blocking=True)
             done[k].record(copy_stream)
-        d2h_bytes[0] += m * (4 + 4 * 8)
+        d2h_bytes[0] += m * 8 * R.nk
 
     def one_step():
         for k, v in h_in.items():
@@ -444,10 +466,11 @@ def run_e2e(R, cfg, args, ws):
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), ws)
     args.chunk_pairs = old_cap
-    w = sum_over_ranks(R.npairs * n * 4 * args.e2e_steps, ws)
+    w = sum_over_ranks(R.npairs * n * R.nk * args.e2e_steps, ws)
     return {"value": w / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h_bytes[0] / args.e2e_steps), "steps": args.e2e_steps,
-            "ms_per_step": ms / args.e2e_steps}
+            "ms_per_step": ms / args.e2e_steps,
+            "host_csr": "pair_ptr + pair_patch + value arrays (col_idx = patch*n + local, row_ptr = pair_ptr*n implied)"}
 
 
 def sample_pairs(cfg, budget, seed=7):
@@ -471,15 +494,19 @@ def sample_pairs(cfg, budget, seed=7):
     return np.concatenate(tg), np.concatenate(pa), len(chosen)
 
 
-def parity_sample(R, tg, pa, vo, kap):
-    """One more full step (untimed) gathering the CSR rows of the oracle's sampled pairs on the device;
-    per kernel the largest per-row relative error max_i |g_i - o_i| / max_i |o_i|, the fraction of rows
-    within the strict 1e-11, the largest |g_i - o_i| / kappa_i, and the fraction of rows within the parity
-    bar of tests/ (per weight max(1e-11 max_row|o|, 1e-13, 1e-10 kappa_i), 3e-10 kappa_i for
-    D').  A correction weight is the difference of the RRQ weight and the smooth-rule weight (A14), which
-    nearly cancel for far pairs; kappa_i carries that scale, so the strict per-row figure is small there."""
+def parity_sample(R, tg, pa, max_pairs=1500, seed=11):
+    """One more full step (untimed) in the timed launch configuration, gathering the CSR rows of a seeded
+    subsample of the oracle's sampled pairs on the device; per kernel the GPU's and the fp64 oracle's row
+    errors against the binary128 truth (median / 90th percentile / max of max_i |x_i - t_i| / max_i |t_i|,
+    rows within 1e-11) and the parity bar of tests/parity_util.py."""
     import torch
-    n = R.n
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import parity_util as U
+    rng = np.random.default_rng(seed)
+    if tg.size > max_pairs:
+        sel = np.sort(rng.choice(tg.size, max_pairs, replace=False))
+        tg, pa = tg[sel], pa[sel]
+    cfg, n = R.cfg, R.n
     ptr, pat = R.ctx.near_list(R.ds, R.dt)
     hptr, hpat = ptr.cpu().numpy(), pat.cpu().numpy()
     ch = R.chunks(hptr, R.args.chunk_pairs)
@@ -493,7 +520,7 @@ def parity_sample(R, tg, pa, vo, kap):
     got = np.zeros((4, tg.size, n))
 
     def on_chunk(when, i, o, npairs=None):
-        if when == "before":
+        if when != "after":
             return
         r0, r1 = ch[i]
         sel = np.where((pos >= hptr[r0]) & (pos < hptr[r1]))[0]
@@ -501,31 +528,23 @@ def parity_sample(R, tg, pa, vo, kap):
             return
         idx = torch.as_tensor(pos[sel] - hptr[r0], device="cuda")
         for k in range(4):
-            got[k, sel] = o["vals"][k][: npairs * n].view(npairs, n).index_select(0, idx).cpu().numpy()
+            if o["vals"][k] is not None:
+                got[k, sel] = o["vals"][k][: npairs * n].view(npairs, n).index_select(0, idx).cpu().numpy()
 
     R.step(on_chunk=on_chunk)
-    out = {"pairs": int(tg.size), "rows": int(np.unique(tg).size)}
+    t0 = time.time()
+    tgs = (cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
+    ref = U.reference(cfg["surface"], tgs, tg, pa, mask=R.mask)
+    inv = np.unique(tg, return_inverse=True)[1]
+    out = {"pairs": int(tg.size), "rows": int(inv.max() + 1), "truth": "oracle in IEEE binary128 (liboracle_q.so)",
+           "truth_seconds": time.time() - t0,
+           "bar": f"per row e_g <= {U.ROW_FACTOR:g} x fp64 rounding envelope + 1e-11 rowmax; median/p90 within "
+                  f"{U.Q_FACTOR:g}x, max within {U.MAX_FACTOR:g}x of the fp64 oracle's"}
     for k, name in enumerate(("S", "D", "Sp", "Dp")):
-        o = vo[k].reshape(tg.size, n)
-        rowmax = {}
-        for t, m in zip(tg, np.abs(o).max(1)):
-            rowmax[t] = max(rowmax.get(t, 0.0), m)
-        rm = np.array([max(rowmax[t], 1e-300) for t in tg])
-        rel = np.abs(got[k] - o).max(1) / rm
-        worst_row = {}
-        for t, r in zip(tg, rel):
-            worst_row[t] = max(worst_row.get(t, 0.0), r)
-        wr = np.array(list(worst_row.values()))
-        kr = (3e-10 if name == "Dp" else 1e-10) * kap[k].reshape(tg.size, n)
-        tol = np.maximum(np.maximum(1e-11 * rm[:, None], 1e-13), kr)
-        ok_pair = (np.abs(got[k] - o) <= tol).all(1)
-        ok_row = {}
-        for t, ok in zip(tg, ok_pair):
-            ok_row[t] = ok_row.get(t, True) and bool(ok)
-        out[name] = {"max_rel_err_per_row": float(wr.max()), "median": float(np.median(wr)),
-                     "rows_within_1e-11": float((wr <= 1e-11).mean()),
-                     "max_err_over_kappa": float((np.abs(got[k] - o) / np.maximum(kap[k].reshape(tg.size, n), 1e-300)).max()),
-                     "rows_within_bar": float(np.mean(list(ok_row.values())))}
+        if not (R.mask >> k) & 1:
+            continue
+        ok, st = U.gate_rows(got[k], ref, k, inv)
+        out[name] = dict(st, passes=bool(ok))
     return out
 
 
@@ -543,10 +562,9 @@ def cpu_baseline(cfg, args, R=None, steps=1):
            "sample": f"{tg.shape[0]} pairs = all near pairs of {npatch} random patches of {cfg['name']} "
                      f"(Steps 1-8 incl. per-patch fit, all 4 kernels), {el:.1f} s on {cores} OpenMP threads",
            "seconds": el, "pairs": int(tg.shape[0])}
-    if R is not None:   # the same pairs out of a full-size build in the timed launch configuration
+    if R is not None:   # a subsample of the same pairs out of a full-size build in the timed launch configuration
         try:
-            _, _, kap = O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa, kappa=True)
-            res["parity_sample"] = parity_sample(R, tg, pa, vo, kap)
+            res["parity_sample"] = parity_sample(R, tg, pa)
         except Exception as ex:  # report, never hide
             res["parity_sample"] = {"error": repr(ex)}
     # like-for-like with the paper's single-core numbers: the first patch's pairs on one thread
@@ -560,9 +578,13 @@ def cpu_baseline(cfg, args, R=None, steps=1):
         e1 = time.time() - t1
         gomp.omp_set_num_threads(cores)
         rows1 = np.unique(tg[:n1]).size
+        # a CSR row of the full workload holds npairs / n_close pairs (near patches per close target), so one
+        # core's rows/s equivalent is its pairs/s divided by that (the sample's own pairs-per-target is ~1:
+        # it takes all pairs of a few patches)
+        ppr = (R.npairs / max(R.n_close, 1)) if R is not None else None
         res["one_core"] = {"value": n1 * S.n * 4 / e1, "unit": UNIT, "pairs": n1, "seconds": e1,
-                           "pairs_per_s": n1 / e1,
-                           "rows_per_s_equiv": n1 / e1 / (tg.shape[0] / max(np.unique(tg).size, 1)),
+                           "pairs_per_s": n1 / e1, "pairs_per_row_full_workload": ppr,
+                           "rows_per_s_equiv": (n1 / e1 / ppr) if ppr else None,
                            "sample": f"first {n1} pairs of the sample ({rows1} distinct targets), 1 OpenMP thread"}
     except OSError as ex:
         res["one_core"] = {"error": repr(ex)}

@@ -1,4 +1,4 @@
-"""ctypes binding of the CPU fp64 oracle (oracle/rrq_oracle.c).
+"""ctypes binding of the CPU oracle (oracle/rrq_oracle.c): fp64, plus long-double and quad builds.
 
 TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline and
 `--impl reference` legs may import this module.  It imports nothing from paper_2411_08342_b200/.
@@ -12,29 +12,50 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "rrq_oracle.c")
-_LIB = os.path.join(_HERE, "liboracle.so")
+
+# The oracle in four builds of the same source (rrq_oracle.c header):
+#   "d"    fp64, no FMA contraction: THE oracle (its rows are what "oracle" means in the tests);
+#   "fma"  fp64 with FMA contraction (-mfma -ffp-contract=fast): a second, equally correct fp64 rounding;
+#   "ld"   x87 long double (64-bit significand);
+#   "q"    IEEE binary128: the truth reference (same algorithm, same fp64 inputs, ~34 digits).
+_BUILDS = {
+    "d": ("liboracle.so", ["-frounding-math", "-ffp-contract=off"]),
+    "fma": ("liboracle_fma.so", ["-frounding-math", "-mfma", "-ffp-contract=fast"]),
+    "ld": ("liboracle_ld.so", ["-DORC_REAL_LD"]),
+    "q": ("liboracle_q.so", ["-DORC_REAL_QUAD"]),
+}
+PRECISIONS = tuple(_BUILDS)
+ROUNDING = {"nearest": 0, "up": 1, "down": 2, "zero": 3}
 
 
-def build(force=False):
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC,
-                               "-lquadmath", "-lm"])
-    return _LIB
+def build(force=False, prec=None):
+    """Compile the oracle library of precision `prec` (all four if None); returns the path (or the
+    fp64 path when building all)."""
+    out = None
+    for k in (PRECISIONS if prec is None else (prec,)):
+        name, flags = _BUILDS[k]
+        lib_path = os.path.join(_HERE, name)
+        if force or not os.path.exists(lib_path) or os.path.getmtime(lib_path) < os.path.getmtime(_SRC):
+            tmp = lib_path + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", "-O2", *flags, "-fopenmp", "-fPIC", "-shared", "-Wl,-Bsymbolic",
+                                   "-o", tmp, _SRC, "-lquadmath", "-lm"])
+            os.replace(tmp, lib_path)
+        out = lib_path if out is None or k == "d" else out
+    return out
 
 
 class OrcParams(ctypes.Structure):
     _fields_ = [("p", ctypes.c_int), ("q", ctypes.c_int), ("n_omega", ctypes.c_int),
-                ("rho0", ctypes.c_double)]
+                ("rho0", ctypes.c_double), ("rounding", ctypes.c_int)]
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        _lib = ctypes.CDLL(build())
-    return _lib
+def lib(prec="d"):
+    if prec not in _libs:
+        _libs[prec] = ctypes.CDLL(build(prec=prec))
+    return _libs[prec]
 
 
 def _p(a):
@@ -131,20 +152,30 @@ def bernstein_rho(t0):
 
 # ------------------------------------------------------------------ whole-path entry points
 
-def params(p, q=None, n_omega=32, rho0=3.0):
-    return OrcParams(p, q if q is not None else 2 * p, n_omega, rho0)
+def params(p, q=None, n_omega=32, rho0=3.0, rounding="nearest"):
+    return OrcParams(p, q if q is not None else 2 * p, n_omega, rho0, ROUNDING[rounding])
 
 
-def patch_fit(S):
+def patch_fit(S, prec="d", rounding="nearest"):
     P, n = S.nodes.shape[:2]
     p, q = S.p, S.q
     np_ = p * (p + 1) // 2
     fit = np.zeros((P, 13 * np_, n))
     st = np.zeros(P, np.int32)
-    lib().orc_patch_fit(ctypes.c_int64(P), ctypes.c_int(p), ctypes.c_int(q), _p(_c(S.nodes, np.float64)),
-                        _p(_c(S.normals, np.float64)), _p(_c(S.verts, np.float64)),
-                        _p(_c(S.edge_x, np.float64)), _p(_c(S.edge_dx, np.float64)), _p(fit), _p(st))
+    lib(prec).orc_patch_fit(ctypes.c_int64(P), ctypes.c_int(p), ctypes.c_int(q), _p(_c(S.nodes, np.float64)),
+                            _p(_c(S.normals, np.float64)), _p(_c(S.verts, np.float64)),
+                            _p(_c(S.edge_x, np.float64)), _p(_c(S.edge_dx, np.float64)), _p(fit), _p(st),
+                            ctypes.c_int(ROUNDING[rounding]))
     return fit, st
+
+
+def near_balls(S):
+    """(c_P, R_P, h_P) of every patch (reading A6) -> [P, 5]."""
+    ball = np.zeros((S.n_patches, 5))
+    lib().orc_near_balls(ctypes.c_int64(S.n_patches), ctypes.c_int(S.p), ctypes.c_int(S.q),
+                         _p(_c(S.nodes, np.float64)), _p(_c(S.weights, np.float64)), _p(_c(S.verts, np.float64)),
+                         _p(_c(S.edge_x, np.float64)), _p(ball))
+    return ball
 
 
 def near_list(S, tx, self_node, eta, all_pairs=False):
@@ -163,35 +194,37 @@ def near_list(S, tx, self_node, eta, all_pairs=False):
 
 
 def build_rows(S, tx, tnormal, self_node, side, pair_target, pair_patch, mask=15, raw=False, n_omega=32,
-               rho0=3.0, kappa=False):
-    """-> vals [4, n_pairs, n] (S, D, S', D'), status [n_pairs] (, kappa [4, n_pairs, n] if kappa=True:
-    the scale of the terms entering each weight, ||zeta||_inf sum_c |P_ci| + |smooth_i|)."""
+               rho0=3.0, prec="d", rounding="nearest", zeta=False):
+    """-> vals [4, n_pairs, n] (S, D, S', D'), status [n_pairs] (, zeta [n_pairs, 9 np] if zeta: the Step 4-7
+    outputs Theta [np] | W [np, 4] | dW [np, 4] per pair).  prec: "d" (the fp64 oracle), "fma", "ld" or "q"
+    (truth); rounding: IEEE rounding mode of the whole evaluation ("nearest", "up", "down", "zero")."""
     n = S.n
     npairs = int(pair_target.shape[0])
     vals = np.zeros((4, npairs, n))
     st = np.zeros(npairs, np.int32)
-    kap = np.zeros((4, npairs, n)) if kappa else None
-    pr = params(S.p, S.q, n_omega, rho0)
-    lib().orc_build_rows2(ctypes.byref(pr), ctypes.c_int64(S.n_patches), _p(_c(S.nodes, np.float64)),
-                         _p(_c(S.normals, np.float64)), _p(_c(S.weights, np.float64)),
-                         _p(_c(S.verts, np.float64)), _p(_c(S.edge_x, np.float64)),
-                         _p(_c(S.edge_dx, np.float64)), _p(_c(tx, np.float64)),
-                         _p(_c(tnormal, np.float64)) if tnormal is not None else None,
-                         _p(_c(self_node, np.int64)) if self_node is not None else None,
-                         _p(_c(side, np.int8)) if side is not None else None,
-                         ctypes.c_int64(npairs), _p(_c(pair_target, np.int64)), _p(_c(pair_patch, np.int32)),
-                         ctypes.c_uint32(mask), ctypes.c_int(int(raw)), _p(vals), _p(st), _p(kap))
-    return (vals, st, kap) if kappa else (vals, st)
+    npb = S.p * (S.p + 1) // 2
+    z = np.zeros((npairs, 9 * npb)) if zeta else None
+    pr = params(S.p, S.q, n_omega, rho0, rounding)
+    lib(prec).orc_build_rows(ctypes.byref(pr), ctypes.c_int64(S.n_patches), _p(_c(S.nodes, np.float64)),
+                             _p(_c(S.normals, np.float64)), _p(_c(S.weights, np.float64)),
+                             _p(_c(S.verts, np.float64)), _p(_c(S.edge_x, np.float64)),
+                             _p(_c(S.edge_dx, np.float64)), _p(_c(tx, np.float64)),
+                             _p(_c(tnormal, np.float64)) if tnormal is not None else None,
+                             _p(_c(self_node, np.int64)) if self_node is not None else None,
+                             _p(_c(side, np.int8)) if side is not None else None,
+                             ctypes.c_int64(npairs), _p(_c(pair_target, np.int64)), _p(_c(pair_patch, np.int32)),
+                             ctypes.c_uint32(mask), ctypes.c_int(int(raw)), _p(vals), _p(st), _p(z))
+    return (vals, st, z) if zeta else (vals, st)
 
 
-def pair_debug(S, P, x, nu, self_local=-1, side=2, raw=True, n_omega=32, rho0=3.0):
+def pair_debug(S, P, x, nu, self_local=-1, side=2, raw=True, n_omega=32, rho0=3.0, prec="d", rounding="nearest"):
     """Intermediates of one pair on patch P.  Returns dict."""
     p, n = S.p, S.n
     np_ = p * (p + 1) // 2
     rows = np.zeros((4, n)); scal = np.zeros(20); W = np.zeros((np_, 4)); dW = np.zeros((np_, 4))
     Th = np.zeros(np_); frame = np.zeros(13)
-    pr = params(p, S.q, n_omega, rho0)
-    st = lib().orc_pair_debug(ctypes.byref(pr), _p(_c(S.nodes[P], np.float64)), _p(_c(S.normals[P], np.float64)),
+    pr = params(p, S.q, n_omega, rho0, rounding)
+    st = lib(prec).orc_pair_debug(ctypes.byref(pr), _p(_c(S.nodes[P], np.float64)), _p(_c(S.normals[P], np.float64)),
                               _p(_c(S.weights[P], np.float64)), _p(_c(S.verts[P], np.float64)),
                               _p(_c(S.edge_x[P], np.float64)), _p(_c(S.edge_dx[P], np.float64)),
                               _p(_c(x, np.float64)), _p(_c(nu, np.float64)) if nu is not None else None,

@@ -1,6 +1,6 @@
 /*
- * rrq_oracle.c -- plain, slow, CPU fp64 ORACLE of the recursive reduction quadrature (RRQ) near
- * correction build of Jiang & Zhu, arXiv 2411.08342 ("PAPER.md").
+ * rrq_oracle.c -- plain, slow, CPU ORACLE of the recursive reduction quadrature (RRQ) near correction
+ * build of Jiang & Zhu, arXiv 2411.08342 ("PAPER.md").
  *
  * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
  * --impl reference legs may load this library.  It shares no code, header, table generator or
@@ -13,6 +13,17 @@
  * it follows.  Plain loops, no blocking, fusion or reordering beyond what the paper states; the
  * negative-k line integrals are computed directly (no conjugate-symmetry shortcut).
  *
+ * PRECISION.  The arithmetic type `real` is chosen at compile time:
+ *   default        fp64 ("the oracle", liboracle.so; also liboracle_fma.so built with FMA contraction)
+ *   ORC_REAL_LD    x87 80-bit long double (liboracle_ld.so)
+ *   ORC_REAL_QUAD  IEEE binary128 __float128 (liboracle_q.so): the TRUTH reference of the parity tests,
+ *                  i.e. the same algorithm on the same fp64 inputs with ~34-digit arithmetic, constant
+ *                  tables (Gauss-Legendre nodes/weights, U = V^{-1}) kept in quad and the Newton
+ *                  tolerance scaled to the working precision.
+ * Inputs and outputs at the C interface are always fp64 (the outputs are the real results rounded once).
+ * The fp64 build can also run under any IEEE rounding mode (orc_params.rounding): the spread of those
+ * runs around the truth measures what an fp64 evaluation of this formulation can attain.
+ *
  * Citation key: P:Lnnn = /root/reference/PAPER.md line nnn (not read at run time).
  *
  * Pins (tests/test_oracle_*.py, all `-m "not gpu"`): Legendre vs scipy (textbook), solid harmonics
@@ -20,37 +31,98 @@
  * model integrals vs adaptive quadrature and closed forms, t0 closed form on straight edges,
  * Omega_0 vs Van Oosterom-Strackee, per-(l,m) W / Theta vs brute-force 2-form surface integrals
  * (Thm 3.4 / 3.5), D' vs finite differences, fit vs an independent least-squares solve, full
- * operator on the sphere (Gauss law, Y_l^m eigenrelations, Green's identity).  Parity unpinned:
+ * operator on the sphere (Gauss law, Y_l^m eigenrelations, Green's identity), close evaluation
+ * against closed forms and adaptive quadrature down to 1e-14 h (tests/test_oracle_close.py), and the
+ * precision ladder fp64 -> long double -> quad (tests/test_oracle_precision.py).  Parity unpinned:
  * none.
  */
 #include <complex.h>
+#include <fenv.h>
 #include <math.h>
 #include <quadmath.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
+/* ------------------------------------------------------------------------------------------------
+ * The working precision.
+ * ----------------------------------------------------------------------------------------------*/
+#if defined(ORC_REAL_QUAD)
+typedef __float128 real;
+typedef __complex128 cplx;
+#define RF(f) f##q
+#define ISFIN(x) finiteq(x)
+#define NEWTON_TOL 1e-32Q   /* ~ 50 ulp of binary128 */
+#define NEWTON_MAXIT 30
+#elif defined(ORC_REAL_LD)
+typedef long double real;
+typedef long double complex cplx;
+#define RF(f) f##l
+#define ISFIN(x) isfinite(x)
+#define NEWTON_TOL 1e-18L   /* ~ 10 ulp of the 64-bit significand */
+#define NEWTON_MAXIT 30
+#else
+typedef double real;
 typedef double complex cplx;
+#define RF(f) f
+#define ISFIN(x) isfinite(x)
+#define NEWTON_TOL 1e-15    /* reading A12 */
+#define NEWTON_MAXIT 20
+#endif
+#define SQRT RF(sqrt)
+#define FABS RF(fabs)
+#define LOG RF(log)
+#define ASINH RF(asinh)
+#define SINH RF(sinh)
+#define COSH RF(cosh)
+#define COS RF(cos)
+#define SIN RF(sin)
+#define ATAN2 RF(atan2)
+#define ACOS RF(acos)
+#define POW RF(pow)
+#define CABS RF(cabs)
+#define CSQRT RF(csqrt)
+#define CONJ RF(conj)
+#define CRE(z) (__real__(z))
+#define CIM(z) (__imag__(z))
 
-#define ORC_PI 3.14159265358979323846264338327950288
+static inline cplx mkc(real re, real im) {
+  cplx z;
+  __real__ z = re;
+  __imag__ z = im;
+  return z;
+}
+static inline real rmax2(real a, real b) { return a > b ? a : b; }
+#define R_PI (ACOS((real)-1))
 
 /* ------------------------------------------------------------------------------------------------
  * Parameters of one run (the discrete choices of DESIGN.md §2: p~ = 2p (A4), rho0 = 3 (A5),
- * n_Omega = 32 (A9), eta (A6)).
+ * n_Omega = 32 (A9), eta (A6)); `rounding`: IEEE rounding mode of the run (0 nearest, 1 upward,
+ * 2 downward, 3 toward zero).
  * ----------------------------------------------------------------------------------------------*/
 typedef struct {
   int p;          /* harmonic order */
   int q;          /* p~: edge Gauss-Legendre nodes per edge */
   int n_omega;    /* Gauss-Legendre nodes per side of the sinh split (A9) */
   double rho0;    /* Bernstein-ellipse threshold of the swap regime (A5) */
+  int rounding;   /* IEEE rounding mode of the whole evaluation */
 } orc_params;
+
+static int fe_mode(int r) {
+  switch (r) {
+    case 1: return FE_UPWARD;
+    case 2: return FE_DOWNWARD;
+    case 3: return FE_TOWARDZERO;
+    default: return FE_TONEAREST;
+  }
+}
 
 /* ------------------------------------------------------------------------------------------------
  * Quad-precision constant tables.  Gauss-Legendre nodes ("the p~ Gauss-Legendre
- * nodes") and U = V^{-1} are computed in __float128 and rounded once to double, so
- * they are correctly rounded (A4).
+ * nodes") and U = V^{-1} are computed in __float128 and rounded once to the working
+ * precision (correctly rounded in fp64: DESIGN.md §2, A4).
  * ----------------------------------------------------------------------------------------------*/
-void orc_gauss_legendre(int n, double *x, double *w) {
+static void gl_real(int n, real *x, real *w) {
   for (int i = 0; i < n; ++i) {
     __float128 t = cosq(M_PIq * (n - i - 0.25Q) / (n + 0.5Q)); /* ascending order */
     __float128 dp = 0;
@@ -76,15 +148,22 @@ void orc_gauss_legendre(int n, double *x, double *w) {
       }
       dp = n * (t * p1 - p0) / (t * t - 1);
     }
-    x[i] = (double)t;
-    w[i] = (double)(2 / ((1 - t * t) * dp * dp));
+    x[i] = (real)t;
+    w[i] = (real)(2 / ((1 - t * t) * dp * dp));
   }
 }
 
+void orc_gauss_legendre(int n, double *x, double *w) {
+  real *xr = malloc(sizeof(real) * n), *wr = malloc(sizeof(real) * n);
+  gl_real(n, xr, wr);
+  for (int i = 0; i < n; ++i) { x[i] = (double)xr[i]; w[i] = (double)wr[i]; }
+  free(xr); free(wr);
+}
+
 /* U = V^{-1}, V_{kq} = t_k^q: Gauss-Jordan with partial pivoting in __float128 on the
- * double nodes t (so V is exactly the Vandermonde of the nodes actually used).  U is row-major
- * [q][k]: c~_q = sum_k U[q][k] F_k. */
-void orc_vandermonde_inverse(int n, const double *t, double *U) {
+ * working-precision nodes t (so V is exactly the Vandermonde of the nodes actually used).  U is
+ * row-major [q][k]: c~_q = sum_k U[q][k] F_k. */
+static void vandermonde_inverse_real(int n, const real *t, real *U) {
   __float128 *M = malloc(sizeof(__float128) * n * 2 * n);
   for (int k = 0; k < n; ++k) {
     __float128 tp = 1;
@@ -115,21 +194,29 @@ void orc_vandermonde_inverse(int n, const double *t, double *U) {
   }
   /* M = [I | V^{-1}] with V^{-1}[q][k]: row q of V^{-1} maps samples F_k to coefficient q. */
   for (int q = 0; q < n; ++q)
-    for (int k = 0; k < n; ++k) U[q * n + k] = (double)M[q * 2 * n + n + k];
+    for (int k = 0; k < n; ++k) U[q * n + k] = (real)M[q * 2 * n + n + k];
   free(M);
+}
+
+void orc_vandermonde_inverse(int n, const double *t, double *U) {
+  real *tr = calloc(n, sizeof(real)), *Ur = calloc((size_t)n * n, sizeof(real));
+  for (int i = 0; i < n; ++i) tr[i] = t[i];
+  vandermonde_inverse_real(n, tr, Ur);
+  for (int i = 0; i < n * n; ++i) U[i] = (double)Ur[i];
+  free(tr); free(Ur);
 }
 
 /* ------------------------------------------------------------------------------------------------
  * Harmonic polynomials.
  * ----------------------------------------------------------------------------------------------*/
-static double fact(int n) {
-  double f = 1;
+static real fact(int n) {
+  real f = 1;
   for (int i = 2; i <= n; ++i) f *= i;
   return f;
 }
 
-static double binom(int n, int k) {
-  if (n < 0 || k < 0 || k > n) return 0.0;
+static real binom(int n, int k) {
+  if (n < 0 || k < 0 || k > n) return 0;
   return fact(n) / (fact(k) * fact(n - k));
 }
 
@@ -137,7 +224,7 @@ static double binom(int n, int k) {
  * associatelegendrerecurrence) with the diagonal sign of the Rodrigues formula P:L333 (no
  * Condon-Shortley phase, reading G5): P_{l+1}^{l+1} = +(2l+1) sqrt(1-x^2) P_l^l.  `s` is
  * sqrt(1-x^2), passed in so it can be formed accurately.  P[l*(p+1)+m]. */
-void orc_legendre(int p, double x, double s, double *P) {
+static void legendre_real(int p, real x, real s, real *P) {
   int L = p + 1;
   for (int i = 0; i < L * L; ++i) P[i] = 0;
   P[0] = 1;
@@ -150,31 +237,48 @@ void orc_legendre(int p, double x, double s, double *P) {
       P[(l + 1) * L + m] = ((2 * l + 1) * x * P[l * L + m] - (l + m) * P[(l - 1) * L + m]) / (l - m + 1);
 }
 
+void orc_legendre(int p, double x, double s, double *P) {
+  int L = (p + 1) * (p + 1);
+  real *Pr = malloc(sizeof(real) * L);
+  legendre_real(p, x, s, Pr);
+  for (int i = 0; i < L; ++i) P[i] = (double)Pr[i];
+  free(Pr);
+}
+
 static inline int hidx(int l, int m) { return l * l + l + m; }
 
 /* Regular solid harmonics R_l^m(X,Y,Z) = sqrt((l-m)!/(l+m)!) r^l P_l^m(cos theta) e^{i m phi}
  * (eqs ylmdef, rlmdef), 0<=l<=p, m>=0, and R_l^{-m} := (-1)^m conj(R_l^m) (reading G5).
  * Output R[hidx(l,m)], -l<=m<=l. */
-void orc_solid_R(int p, double X, double Y, double Z, cplx *R) {
+static void solid_R_real(int p, real X, real Y, real Z, cplx *R) {
   int L = p + 1;
   for (int i = 0; i < L * L; ++i) R[i] = 0;
   R[0] = 1;
-  double rho = sqrt(X * X + Y * Y);
-  double r = sqrt(X * X + Y * Y + Z * Z);
+  real rho = SQRT(X * X + Y * Y);
+  real r = SQRT(X * X + Y * Y + Z * Z);
   if (r == 0) return;
-  double ct = Z / r, st = rho / r, phi = atan2(Y, X);
-  double *P = malloc(sizeof(double) * L * L);
-  orc_legendre(p, ct, st, P);
+  real ct = Z / r, st = rho / r, phi = ATAN2(Y, X);
+  real *P = malloc(sizeof(real) * L * L);
+  legendre_real(p, ct, st, P);
   for (int l = 0; l <= p; ++l) {
-    double rl = pow(r, l);
+    real rl = POW(r, (real)l);
     for (int m = 0; m <= l; ++m) {
-      double N = sqrt(fact(l - m) / fact(l + m));
-      cplx v = N * rl * P[l * L + m] * cexp(I * (m * phi));
+      real N = SQRT(fact(l - m) / fact(l + m));
+      real a = N * rl * P[l * L + m];
+      cplx v = mkc(a * COS(m * phi), a * SIN(m * phi));
       R[hidx(l, m)] = v;
-      if (m > 0) R[hidx(l, -m)] = ((m & 1) ? -1.0 : 1.0) * conj(v);
+      if (m > 0) R[hidx(l, -m)] = ((m & 1) ? -1 : 1) * CONJ(v);
     }
   }
   free(P);
+}
+
+void orc_solid_R(int p, double X, double Y, double Z, double *out) {
+  int L = (p + 1) * (p + 1);
+  cplx *R = malloc(sizeof(cplx) * L);
+  solid_R_real(p, X, Y, Z, R);
+  for (int k = 0; k < L; ++k) { out[2 * k] = (double)CRE(R[k]); out[2 * k + 1] = (double)CIM(R[k]); }
+  free(R);
 }
 
 static inline cplx Rget(const cplx *R, int l, int m) {
@@ -188,20 +292,20 @@ static inline cplx Rget(const cplx *R, int l, int m) {
 typedef struct { cplx c; int l, m; } term_t;
 
 static int dR_terms(int l, int m, int a, term_t *t) {
-  double cp = (l - m) * (double)(l - m - 1) > 0 ? sqrt((l - m) * (double)(l - m - 1)) : 0.0;
-  double cm = (l + m) * (double)(l + m - 1) > 0 ? sqrt((l + m) * (double)(l + m - 1)) : 0.0;
+  real cp = (l - m) * (real)(l - m - 1) > 0 ? SQRT((l - m) * (real)(l - m - 1)) : 0;
+  real cm = (l + m) * (real)(l + m - 1) > 0 ? SQRT((l + m) * (real)(l + m - 1)) : 0;
   if (a == 2) {
-    double cz = (l - m) * (double)(l + m) > 0 ? sqrt((l - m) * (double)(l + m)) : 0.0;
+    real cz = (l - m) * (real)(l + m) > 0 ? SQRT((l - m) * (real)(l + m)) : 0;
     t[0].c = cz; t[0].l = l - 1; t[0].m = m;
     return 1;
   }
   /* D+ = -cp R_{l-1}^{m+1}, D- = cm R_{l-1}^{m-1};  dX = (D+ + D-)/2, dY = (D+ - D-)/(2i) */
   if (a == 0) {
-    t[0].c = -0.5 * cp; t[0].l = l - 1; t[0].m = m + 1;
-    t[1].c = 0.5 * cm;  t[1].l = l - 1; t[1].m = m - 1;
+    t[0].c = -cp / 2; t[0].l = l - 1; t[0].m = m + 1;
+    t[1].c = cm / 2;  t[1].l = l - 1; t[1].m = m - 1;
   } else {
-    t[0].c = -cp / (2.0 * I); t[0].l = l - 1; t[0].m = m + 1;
-    t[1].c = -cm / (2.0 * I); t[1].l = l - 1; t[1].m = m - 1;
+    t[0].c = mkc(0, cp / 2); t[0].l = l - 1; t[0].m = m + 1;   /* -cp/(2i) = i cp/2 */
+    t[1].c = mkc(0, cm / 2); t[1].l = l - 1; t[1].m = m - 1;   /* -cm/(2i) = i cm/2 */
   }
   return 2;
 }
@@ -243,10 +347,10 @@ static void htab_alloc(htab_t *h, int p, int with_hess) {
 }
 static void htab_free(htab_t *h) { free(h->S); free(h->G); free(h->H); }
 
-static void htab_eval(htab_t *h, double x, double y, double z) {
+static void htab_eval(htab_t *h, real x, real y, real z) {
   int p = h->p;
   cplx *R = malloc(sizeof(cplx) * (p + 1) * (p + 1));
-  orc_solid_R(p, y, z, x, R);
+  solid_R_real(p, y, z, x, R);
   for (int l = 0; l <= p; ++l)
     for (int m = -l; m <= l; ++m) {
       int k = hidx(l, m);
@@ -266,19 +370,19 @@ void orc_harmonics_S(int p, double x, double y, double z, double *S, double *G, 
   htab_eval(&h, x, y, z);
   int L = (p + 1) * (p + 1);
   for (int k = 0; k < L; ++k) {
-    S[2 * k] = creal(h.S[k]); S[2 * k + 1] = cimag(h.S[k]);
-    for (int a = 0; a < 3; ++a) { G[6 * k + 2 * a] = creal(h.G[3 * k + a]); G[6 * k + 2 * a + 1] = cimag(h.G[3 * k + a]); }
+    S[2 * k] = (double)CRE(h.S[k]); S[2 * k + 1] = (double)CIM(h.S[k]);
+    for (int a = 0; a < 3; ++a) { G[6 * k + 2 * a] = (double)CRE(h.G[3 * k + a]); G[6 * k + 2 * a + 1] = (double)CIM(h.G[3 * k + a]); }
     if (Hs)
-      for (int a = 0; a < 9; ++a) { Hs[18 * k + 2 * a] = creal(h.H[9 * k + a]); Hs[18 * k + 2 * a + 1] = cimag(h.H[9 * k + a]); }
+      for (int a = 0; a < 9; ++a) { Hs[18 * k + 2 * a] = (double)CRE(h.H[9 * k + a]); Hs[18 * k + 2 * a + 1] = (double)CIM(h.H[9 * k + a]); }
   }
   htab_free(&h);
 }
 
 /* T_{jk,lm} = C(l+m, j+k)^{1/2} C(l-m, j-k)^{1/2} (eq tjklmdef), zero out of range. */
-static double Tjklm(int j, int k, int l, int m) { return sqrt(binom(l + m, j + k) * binom(l - m, j - k)); }
+static real Tjklm(int j, int k, int l, int m) { return SQRT(binom(l + m, j + k) * binom(l - m, j - k)); }
 /* C_{j,l} = (j-2)!(l-j)!/(l-1)! and D_{j,l} = (j-1)!(l-j)!/l!. */
-static double Cjl(int j, int l) { return fact(j - 2) * fact(l - j) / fact(l - 1); }
-static double Djl(int j, int l) { return fact(j - 1) * fact(l - j) / fact(l); }
+static real Cjl(int j, int l) { return fact(j - 2) * fact(l - j) / fact(l - 1); }
+static real Djl(int j, int l) { return fact(j - 1) * fact(l - j) / fact(l); }
 
 /* (l,m), 1<=m<=l<=p -> basis index (P:L465-466 enumerates l=1..p, m=1..l). */
 static inline int lmidx(int l, int m) { return l * (l - 1) / 2 + (m - 1); }
@@ -304,55 +408,55 @@ static quat qadd(quat f, quat g) { quat r; r.s = f.s + g.s; for (int i = 0; i < 
 void orc_qmul(const double *f, const double *g, double *out) {
   quat a = {f[0], {f[1], f[2], f[3]}}, b = {g[0], {g[1], g[2], g[3]}};
   quat r = qmul(a, b);
-  out[0] = creal(r.s);
-  for (int i = 0; i < 3; ++i) out[1 + i] = creal(r.v[i]);
+  out[0] = (double)CRE(r.s);
+  for (int i = 0; i < 3; ++i) out[1 + i] = (double)CRE(r.v[i]);
 }
 
 /* ------------------------------------------------------------------------------------------------
  * Dense least squares: Moore-Penrose pseudo-inverse by Householder QR (reading A1).
  * A is m x k row-major (m >= k), Aplus is k x m row-major.  Returns 1 if rank deficient.
  * ----------------------------------------------------------------------------------------------*/
-int orc_pinv_qr(int m, int k, const double *A, double *Aplus) {
-  double *W = malloc(sizeof(double) * m * k);
-  double *V = calloc((size_t)m * k, sizeof(double)); /* reflector vectors, column j in V[:,j] */
-  double *beta = calloc(k, sizeof(double));
-  memcpy(W, A, sizeof(double) * m * k);
+static int pinv_qr_real(int m, int k, const real *A, real *Aplus) {
+  real *W = malloc(sizeof(real) * m * k);
+  real *V = calloc((size_t)m * k, sizeof(real)); /* reflector vectors, column j in V[:,j] */
+  real *beta = calloc(k, sizeof(real));
+  memcpy(W, A, sizeof(real) * m * k);
   int deficient = 0;
-  double rmax = 0;
+  real rmax = 0;
   for (int j = 0; j < k; ++j) {
-    double nrm = 0;
+    real nrm = 0;
     for (int i = j; i < m; ++i) nrm += W[i * k + j] * W[i * k + j];
-    nrm = sqrt(nrm);
-    double alpha = (W[j * k + j] > 0) ? -nrm : nrm;
+    nrm = SQRT(nrm);
+    real alpha = (W[j * k + j] > 0) ? -nrm : nrm;
     for (int i = j; i < m; ++i) V[i * k + j] = W[i * k + j];
     V[j * k + j] -= alpha;
-    double b = 0;
+    real b = 0;
     for (int i = j; i < m; ++i) b += V[i * k + j] * V[i * k + j];
     beta[j] = b;
     if (b > 0)
       for (int c = j; c < k; ++c) {
-        double s = 0;
+        real s = 0;
         for (int i = j; i < m; ++i) s += V[i * k + j] * W[i * k + c];
         s = 2 * s / b;
         for (int i = j; i < m; ++i) W[i * k + c] -= s * V[i * k + j];
       }
-    if (fabs(W[j * k + j]) > rmax) rmax = fabs(W[j * k + j]);
+    if (FABS(W[j * k + j]) > rmax) rmax = FABS(W[j * k + j]);
   }
   for (int j = 0; j < k; ++j)
-    if (fabs(W[j * k + j]) <= 1e-13 * rmax) deficient = 1;
+    if (!(FABS(W[j * k + j]) > (real)1e-13 * rmax)) deficient = 1;
   /* Q^T e_c for each column c, first k rows; then R^{-1} by back substitution. */
-  double *e = malloc(sizeof(double) * m);
+  real *e = malloc(sizeof(real) * m);
   for (int c = 0; c < m; ++c) {
     for (int i = 0; i < m; ++i) e[i] = (i == c);
     for (int j = 0; j < k; ++j) {
       if (beta[j] <= 0) continue;
-      double s = 0;
+      real s = 0;
       for (int i = j; i < m; ++i) s += V[i * k + j] * e[i];
       s = 2 * s / beta[j];
       for (int i = j; i < m; ++i) e[i] -= s * V[i * k + j];
     }
     for (int r = k - 1; r >= 0; --r) {
-      double s = e[r];
+      real s = e[r];
       for (int cc = r + 1; cc < k; ++cc) s -= W[r * k + cc] * e[cc];
       e[r] = s / W[r * k + r];
     }
@@ -362,72 +466,82 @@ int orc_pinv_qr(int m, int k, const double *A, double *Aplus) {
   return deficient;
 }
 
+int orc_pinv_qr(int m, int k, const double *A, double *Aplus) {
+  real *Ar = calloc((size_t)m * k, sizeof(real)), *Pr = calloc((size_t)m * k, sizeof(real));
+  for (int i = 0; i < m * k; ++i) Ar[i] = A[i];
+  int st = pinv_qr_real(m, k, Ar, Pr);
+  for (int i = 0; i < m * k; ++i) Aplus[i] = (double)Pr[i];
+  free(Ar); free(Pr);
+  return st;
+}
+
 /* ------------------------------------------------------------------------------------------------
  * Patch: local frame (reading A2), fit operators (Steps 1-2 in matrix mode, reading A1; P:L715-746,
  * P:L846-865), edge tables (Step 3).
  * ----------------------------------------------------------------------------------------------*/
 typedef struct {
   int p, q, n, np;
-  double o[3], Rm[3][3], h;   /* local = Rm (x - o) / h */
-  double *xl, *nl;            /* [n][3] local nodes, normals */
-  double vl[3][3];            /* local vertices */
-  double *yl, *tl;            /* [3q][3] local edge samples, tangents d y / d t */
-  double *C;                  /* [3][q][3] Legendre coefficients of each edge interpolant (A4, A4') */
-  double zlo, zhi;
+  real o[3], Rm[3][3], h;     /* local = Rm (x - o) / h */
+  real *xl, *nl;              /* [n][3] local nodes, normals */
+  real vl[3][3];              /* local vertices */
+  real *yl, *tl;              /* [3q][3] local edge samples, tangents d y / d t */
+  real *C;                    /* [3][q][3] Legendre coefficients of each edge interpolant (A4, A4') */
+  real zlo, zhi;
   cplx *g;                    /* [3q][(p+1)^2][3] Hess S^{(j,k)}(y) tau */
   cplx *e;                    /* [3q][(p+1)^2][3] grad S^{(j,k)}(y) x tau */
-  double *fit;                /* [13 np][n]: P_D (4np), P_Sp (4np), P_Sd (np), P_Sg (4np) */
+  real *fit;                  /* [13 np][n]: P_D (4np), P_Sp (4np), P_Sd (np), P_Sg (4np) */
   int status;
 } patch_t;
 
-static void cross3(const double *a, const double *b, double *c) {
+static void cross3(const real *a, const real *b, real *c) {
   c[0] = a[1] * b[2] - a[2] * b[1];
   c[1] = a[2] * b[0] - a[0] * b[2];
   c[2] = a[0] * b[1] - a[1] * b[0];
 }
-static double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
-static double norm3(const double *a) { return sqrt(dot3(a, a)); }
+static real dot3(const real *a, const real *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+static real norm3(const real *a) { return SQRT(dot3(a, a)); }
 
 /* Reading A2: origin = vertex centroid, z = normalise((v1-v0) x (v2-v0)), e1 = normalise(v1-v0),
  * e2 = z x e1, coordinates scaled by 1/h_P (h_P = max vertex chord, A6). */
-static void patch_frame(const double *verts, double o[3], double Rm[3][3], double *h) {
-  const double *v0 = verts, *v1 = verts + 3, *v2 = verts + 6;
-  double a[3], b[3], z[3], e1[3], e2[3];
+static void patch_frame(const double *verts, real o[3], real Rm[3][3], real *h) {
+  real v0[3], v1[3], v2[3];
+  for (int i = 0; i < 3; ++i) { v0[i] = verts[i]; v1[i] = verts[3 + i]; v2[i] = verts[6 + i]; }
+  real a[3], b[3], z[3], e1[3], e2[3];
   for (int i = 0; i < 3; ++i) { o[i] = (v0[i] + v1[i] + v2[i]) / 3; a[i] = v1[i] - v0[i]; b[i] = v2[i] - v0[i]; }
   cross3(a, b, z);
-  double nz = norm3(z), na = norm3(a);
+  real nz = norm3(z), na = norm3(a);
   for (int i = 0; i < 3; ++i) { z[i] /= nz; e1[i] = a[i] / na; }
   cross3(z, e1, e2);
   for (int i = 0; i < 3; ++i) { Rm[0][i] = e1[i]; Rm[1][i] = e2[i]; Rm[2][i] = z[i]; }
-  double c[3] = {0, 0, 0};
+  real c = 0;
   for (int e = 0; e < 3; ++e) {
-    double d[3];
-    for (int i = 0; i < 3; ++i) d[i] = verts[3 * ((e + 1) % 3) + i] - verts[3 * e + i];
-    double l = norm3(d);
-    if (l > c[0]) c[0] = l;
+    real d[3];
+    for (int i = 0; i < 3; ++i) d[i] = (real)verts[3 * ((e + 1) % 3) + i] - (real)verts[3 * e + i];
+    real l = norm3(d);
+    if (l > c) c = l;
   }
-  *h = c[0];
+  *h = c;
 }
 
-static void to_local(const patch_t *P, const double *x, double *y) {
-  double d[3] = {x[0] - P->o[0], x[1] - P->o[1], x[2] - P->o[2]};
+static void to_local(const patch_t *P, const double *x, real *y) {
+  real d[3] = {(real)x[0] - P->o[0], (real)x[1] - P->o[1], (real)x[2] - P->o[2]};
   for (int r = 0; r < 3; ++r) y[r] = dot3(P->Rm[r], d) / P->h;
 }
-static void rot_local(const patch_t *P, const double *v, double *y) {
-  for (int r = 0; r < 3; ++r) y[r] = dot3(P->Rm[r], v);
+static void rot_local(const patch_t *P, const double *v, real *y) {
+  real vr[3] = {v[0], v[1], v[2]};
+  for (int r = 0; r < 3; ++r) y[r] = dot3(P->Rm[r], vr);
 }
 
 static void patch_build(patch_t *P, const orc_params *pr, const double *nodes, const double *normals,
-                        const double *verts, const double *edge_x, const double *edge_dx, const double *U,
-                        int want_fit) {
+                        const double *verts, const double *edge_x, const double *edge_dx, int want_fit) {
   int p = pr->p, q = pr->q, n = p * p, np = p * (p + 1) / 2, L = (p + 1) * (p + 1);
   P->p = p; P->q = q; P->n = n; P->np = np;
   patch_frame(verts, P->o, P->Rm, &P->h);
-  P->xl = malloc(sizeof(double) * n * 3);
-  P->nl = malloc(sizeof(double) * n * 3);
-  P->yl = malloc(sizeof(double) * 3 * q * 3);
-  P->tl = malloc(sizeof(double) * 3 * q * 3);
-  P->C = malloc(sizeof(double) * 3 * q * 3);
+  P->xl = malloc(sizeof(real) * n * 3);
+  P->nl = malloc(sizeof(real) * n * 3);
+  P->yl = malloc(sizeof(real) * 3 * q * 3);
+  P->tl = malloc(sizeof(real) * 3 * q * 3);
+  P->C = malloc(sizeof(real) * 3 * q * 3);
   for (int i = 0; i < n; ++i) { to_local(P, nodes + 3 * i, P->xl + 3 * i); rot_local(P, normals + 3 * i, P->nl + 3 * i); }
   for (int v = 0; v < 3; ++v) to_local(P, verts + 3 * v, P->vl[v]);
   for (int k = 0; k < 3 * q; ++k) {
@@ -440,27 +554,27 @@ static void patch_build(patch_t *P, const orc_params *pr, const double *nodes, c
    * P:L1231, but evaluated without the cond(V) amplification of monomials).  Gauss-Legendre exactness
    * gives the discrete transform C_j = (2j+1)/2 sum_k W_k P_j(t_k) y_k. */
   {
-    double tg[64], wg[64];
-    orc_gauss_legendre(q, tg, wg);
+    real tg[64], wg[64];
+    gl_real(q, tg, wg);
     for (int e = 0; e < 3; ++e)
       for (int a = 0; a < 3; ++a)
         for (int j = 0; j < q; ++j) P->C[(e * q + j) * 3 + a] = 0;
     for (int k = 0; k < q; ++k) {
-      double Pj[64];
+      real Pj[64];
       Pj[0] = 1;
       if (q > 1) Pj[1] = tg[k];
       for (int j = 1; j + 1 < q; ++j) Pj[j + 1] = ((2 * j + 1) * tg[k] * Pj[j] - j * Pj[j - 1]) / (j + 1);
       for (int e = 0; e < 3; ++e)
         for (int j = 0; j < q; ++j)
           for (int a = 0; a < 3; ++a)
-            P->C[(e * q + j) * 3 + a] += 0.5 * (2 * j + 1) * wg[k] * Pj[j] * P->yl[3 * (e * q + k) + a];
+            P->C[(e * q + j) * 3 + a] += (real)0.5 * (2 * j + 1) * wg[k] * Pj[j] * P->yl[3 * (e * q + k) + a];
     }
   }
   /* height range of nodes, vertices, edge samples (reading A8) */
   P->zlo = 1e300; P->zhi = -1e300;
-  for (int i = 0; i < n; ++i) { double z = P->xl[3 * i + 2]; if (z < P->zlo) P->zlo = z; if (z > P->zhi) P->zhi = z; }
-  for (int v = 0; v < 3; ++v) { double z = P->vl[v][2]; if (z < P->zlo) P->zlo = z; if (z > P->zhi) P->zhi = z; }
-  for (int k = 0; k < 3 * q; ++k) { double z = P->yl[3 * k + 2]; if (z < P->zlo) P->zlo = z; if (z > P->zhi) P->zhi = z; }
+  for (int i = 0; i < n; ++i) { real z = P->xl[3 * i + 2]; if (z < P->zlo) P->zlo = z; if (z > P->zhi) P->zhi = z; }
+  for (int v = 0; v < 3; ++v) { real z = P->vl[v][2]; if (z < P->zlo) P->zlo = z; if (z > P->zhi) P->zhi = z; }
+  for (int k = 0; k < 3 * q; ++k) { real z = P->yl[3 * k + 2]; if (z < P->zlo) P->zlo = z; if (z > P->zhi) P->zhi = z; }
 
   /* Step 3: harmonics at the 3 p~ edge nodes. */
   P->g = malloc(sizeof(cplx) * 3 * q * L * 3);
@@ -469,7 +583,7 @@ static void patch_build(patch_t *P, const orc_params *pr, const double *nodes, c
   htab_alloc(&ht, p, 1);
   for (int k = 0; k < 3 * q; ++k) {
     htab_eval(&ht, P->yl[3 * k], P->yl[3 * k + 1], P->yl[3 * k + 2]);
-    const double *t = P->tl + 3 * k;
+    const real *t = P->tl + 3 * k;
     for (int j = 0; j <= p; ++j)
       for (int kk = -j; kk <= j; ++kk) {
         int hk = hidx(j, kk);
@@ -490,8 +604,9 @@ static void patch_build(patch_t *P, const orc_params *pr, const double *nodes, c
   P->status = 0;
   if (!want_fit) return;
   /* Steps 1-2: F_{i,lm} = grad H^{(l,m)}(x_i), H^{(l,m)} = sqrt(2) Im S^{(l,m)} (G5). */
-  double *F = malloc(sizeof(double) * 3 * n * np);  /* F[a][i][lm] */
-  double *Hm = malloc(sizeof(double) * n * np);
+  const real s2 = SQRT((real)2);
+  real *F = malloc(sizeof(real) * 3 * n * np);  /* F[a][i][lm] */
+  real *Hm = malloc(sizeof(real) * n * np);
   htab_t hn;
   htab_alloc(&hn, p, 0);
   for (int i = 0; i < n; ++i) {
@@ -499,14 +614,14 @@ static void patch_build(patch_t *P, const orc_params *pr, const double *nodes, c
     for (int l = 1; l <= p; ++l)
       for (int m = 1; m <= l; ++m) {
         int c = lmidx(l, m), hk = hidx(l, m);
-        for (int a = 0; a < 3; ++a) F[(a * n + i) * np + c] = sqrt(2.0) * cimag(hn.G[3 * hk + a]);
-        Hm[i * np + c] = sqrt(2.0) * cimag(hn.S[hk]);
+        for (int a = 0; a < 3; ++a) F[(a * n + i) * np + c] = s2 * CIM(hn.G[3 * hk + a]);
+        Hm[i * np + c] = s2 * CIM(hn.S[hk]);
       }
   }
   htab_free(&hn);
   /* A: 4n x 4np block matrix of P:L729-735 (eq dlpdensitylinearsystem2). */
   int M4 = 4 * n, K4 = 4 * np;
-  double *A = calloc((size_t)M4 * K4, sizeof(double));
+  real *A = calloc((size_t)M4 * K4, sizeof(real));
   /* block (r, c) of [[0,-F1,-F2,-F3],[F1,0,-F3,F2],[F2,F3,0,-F1],[F3,-F2,F1,0]] */
   const int blk[4][4] = {{0, -1, -2, -3}, {1, 0, -3, 2}, {2, 3, 0, -1}, {3, -2, 1, 0}};
   for (int br = 0; br < 4; ++br)
@@ -514,27 +629,27 @@ static void patch_build(patch_t *P, const orc_params *pr, const double *nodes, c
       int s = blk[br][bc];
       if (s == 0) continue;
       int a = abs(s) - 1;
-      double sg = s > 0 ? 1.0 : -1.0;
+      real sg = s > 0 ? 1 : -1;
       for (int i = 0; i < n; ++i)
         for (int c = 0; c < np; ++c) A[(size_t)(br * n + i) * K4 + bc * np + c] = sg * F[(a * n + i) * np + c];
     }
-  double *Ap = malloc(sizeof(double) * K4 * M4);
-  int st = orc_pinv_qr(M4, K4, A, Ap);
+  real *Ap = malloc(sizeof(real) * K4 * M4);
+  int st = pinv_qr_real(M4, K4, A, Ap);
   /* B_{i,lm} = grad H^{(l,m)}(x_i) . nu_i */
-  double *B = malloc(sizeof(double) * n * np), *Bp = malloc(sizeof(double) * np * n);
+  real *B = malloc(sizeof(real) * n * np), *Bp = malloc(sizeof(real) * np * n);
   for (int i = 0; i < n; ++i)
     for (int c = 0; c < np; ++c) {
-      double s = 0;
+      real s = 0;
       for (int a = 0; a < 3; ++a) s += F[(a * n + i) * np + c] * P->nl[3 * i + a];
       B[i * np + c] = s;
     }
-  st |= orc_pinv_qr(n, np, B, Bp);
-  double *fit = calloc((size_t)13 * np * n, sizeof(double));
-  double *PD = fit, *PSp = fit + 4 * np * n, *PSd = fit + 8 * np * n, *PSg = fit + 9 * np * n;
+  st |= pinv_qr_real(n, np, B, Bp);
+  real *fit = calloc((size_t)13 * np * n, sizeof(real));
+  real *PD = fit, *PSp = fit + 4 * np * n, *PSd = fit + 8 * np * n, *PSg = fit + 9 * np * n;
   for (int r = 0; r < K4; ++r)
     for (int i = 0; i < n; ++i) {
       PD[r * n + i] = Ap[r * M4 + i];  /* RHS (mu, 0, 0, 0) */
-      double s = 0;                     /* RHS (0, sigma nu) */
+      real s = 0;                       /* RHS (0, sigma nu) */
       for (int a = 0; a < 3; ++a) s += P->nl[3 * i + a] * Ap[r * M4 + (a + 1) * n + i];
       PSp[r * n + i] = s;
     }
@@ -542,16 +657,16 @@ static void patch_build(patch_t *P, const orc_params *pr, const double *nodes, c
     for (int i = 0; i < n; ++i) PSd[r * n + i] = Bp[r * n + i];
   /* P_Sg = P_D Hm P_Sd : rho = sum_lm H d at the nodes, then the quaternion fit of (rho, 0)
    * (P:L857-865). */
-  double *HP = malloc(sizeof(double) * n * n);
+  real *HP = malloc(sizeof(real) * n * n);
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) {
-      double s = 0;
+      real s = 0;
       for (int c = 0; c < np; ++c) s += Hm[i * np + c] * PSd[c * n + j];
       HP[i * n + j] = s;
     }
   for (int r = 0; r < K4; ++r)
     for (int j = 0; j < n; ++j) {
-      double s = 0;
+      real s = 0;
       for (int i = 0; i < n; ++i) s += PD[r * n + i] * HP[i * n + j];
       PSg[r * n + j] = s;
     }
@@ -570,7 +685,7 @@ static void patch_free(patch_t *P) {
 /* x(t), x'(t), x''(t) of the Legendre series C (reading A4'), complex t: Bonnet's recurrence
  * (j+1)P_{j+1} = (2j+1) t P_j - j P_{j-1} and P'_{j+1} = P'_{j-1} + (2j+1) P_j,
  * P''_{j+1} = P''_{j-1} + (2j+1) P'_j. */
-static void edge_eval(const double *C, int q, cplx t, cplx *x, cplx *dx, cplx *ddx) {
+static void edge_eval(const real *C, int q, cplx t, cplx *x, cplx *dx, cplx *ddx) {
   cplx P0 = 1, P1 = t, d0 = 0, d1 = 1, e0 = 0, e1 = 0;
   for (int a = 0; a < 3; ++a) {
     x[a] = C[a] * P0;
@@ -580,11 +695,11 @@ static void edge_eval(const double *C, int q, cplx t, cplx *x, cplx *dx, cplx *d
   if (q > 1)
     for (int a = 0; a < 3; ++a) { x[a] += C[3 + a] * P1; dx[a] += C[3 + a] * d1; }
   for (int j = 1; j + 1 < q; ++j) {
-    cplx P2 = ((2 * j + 1) * t * P1 - j * P0) / (j + 1.0);
+    cplx P2 = ((2 * j + 1) * t * P1 - j * P0) / (real)(j + 1);
     cplx d2 = d0 + (2 * j + 1) * P1;
     cplx e2 = e0 + (2 * j + 1) * d1;
     for (int a = 0; a < 3; ++a) {
-      double c = C[(j + 1) * 3 + a];
+      real c = C[(j + 1) * 3 + a];
       x[a] += c * P2;
       dx[a] += c * d2;
       ddx[a] += c * e2;
@@ -593,7 +708,15 @@ static void edge_eval(const double *C, int q, cplx t, cplx *x, cplx *dx, cplx *d
   }
 }
 
-double orc_bernstein_rho(double re, double im);
+/* Bernstein ellipse parameter rho(t0) = |t0 + sqrt(t0^2 - 1)|, branch with rho >= 1 (reading A5). */
+static real bernstein_rho_real(real re, real im) {
+  cplx t = mkc(re, im);
+  cplx s = CSQRT(t * t - 1);
+  real r1 = CABS(t + s), r2 = CABS(t - s);
+  return r1 > r2 ? r1 : r2;
+}
+
+double orc_bernstein_rho(double re, double im) { return (double)bernstein_rho_real(re, im); }
 
 /* Reading A12: complex root t0 of sum_c (x_c(t) - r'_c)^2 = 0 (eq complexparameter).
  * Returns 1 if converged.  Im t0 >= 0.  Reading A12': the iteration also stops (as converged) once,
@@ -601,94 +724,96 @@ double orc_bernstein_rho(double re, double im);
  * root is then certainly outside the swap ellipse, so the regime decision is already fixed and t0 is
  * not used by the plain rule.  Reading A12'': it also stops once the iteration is in its quadratic
  * regime (|dt| < 0.1 |dt_prev|) and the predicted next step C |dt|^2, C ~ |dt| / |dt_prev|^2, is below the
- * tolerance 1e-15 (1 + |t|): the updated t is then already converged (Newton's quadratic convergence). */
-int orc_find_t0(const double *C, int q, const double *rp, double rho_stop, double *t0re, double *t0im) {
+ * tolerance NEWTON_TOL (1 + |t|): the updated t is then already converged (Newton's quadratic
+ * convergence).  NEWTON_TOL = 1e-15 in fp64 (A12), scaled to the working precision otherwise. */
+static int find_t0_real(const real *C, int q, const real *rp, real rho_stop, real *t0re, real *t0im) {
   cplx x[3], dx[3], ddx[3];
   /* chord projection */
-  edge_eval(C, q, -1.0, x, dx, ddx);
-  double A[3] = {creal(x[0]), creal(x[1]), creal(x[2])};
-  edge_eval(C, q, 1.0, x, dx, ddx);
-  double Bv[3] = {creal(x[0]), creal(x[1]), creal(x[2])};
-  double ab[3] = {Bv[0] - A[0], Bv[1] - A[1], Bv[2] - A[2]}, ar[3] = {rp[0] - A[0], rp[1] - A[1], rp[2] - A[2]};
-  double tc = -1.0 + 2.0 * dot3(ar, ab) / dot3(ab, ab);
+  edge_eval(C, q, -1, x, dx, ddx);
+  real A[3] = {CRE(x[0]), CRE(x[1]), CRE(x[2])};
+  edge_eval(C, q, 1, x, dx, ddx);
+  real Bv[3] = {CRE(x[0]), CRE(x[1]), CRE(x[2])};
+  real ab[3] = {Bv[0] - A[0], Bv[1] - A[1], Bv[2] - A[2]}, ar[3] = {rp[0] - A[0], rp[1] - A[1], rp[2] - A[2]};
+  real tc = -1 + 2 * dot3(ar, ab) / dot3(ab, ab);
   /* 3 real Newton steps on g(t) = (x(t) - r').x'(t) */
   for (int it = 0; it < 3; ++it) {
     edge_eval(C, q, tc, x, dx, ddx);
-    double g = 0, gp = 0;
+    real g = 0, gp = 0;
     for (int a = 0; a < 3; ++a) {
-      double xr = creal(x[a]) - rp[a];
-      g += xr * creal(dx[a]);
-      gp += creal(dx[a]) * creal(dx[a]) + xr * creal(ddx[a]);
+      real xr = CRE(x[a]) - rp[a];
+      g += xr * CRE(dx[a]);
+      gp += CRE(dx[a]) * CRE(dx[a]) + xr * CRE(ddx[a]);
     }
     if (!(gp > 0)) break;
     tc -= g / gp;
   }
   /* quadratic-model guess t_c + i sqrt(2 f / f''), f = |x - r'|^2, f'' = 2 (|x'|^2 + (x-r').x'') */
   edge_eval(C, q, tc, x, dx, ddx);
-  double f = 0, dd = 0, xp2 = 0;
+  real f = 0, dd = 0, xp2 = 0;
   for (int a = 0; a < 3; ++a) {
-    double xr = creal(x[a]) - rp[a];
+    real xr = CRE(x[a]) - rp[a];
     f += xr * xr;
-    dd += creal(dx[a]) * creal(dx[a]) + xr * creal(ddx[a]);
-    xp2 += creal(dx[a]) * creal(dx[a]);
+    dd += CRE(dx[a]) * CRE(dx[a]) + xr * CRE(ddx[a]);
+    xp2 += CRE(dx[a]) * CRE(dx[a]);
   }
   if (!(dd > 0)) dd = xp2;
-  cplx t = tc + I * sqrt(f / dd);
+  cplx t = mkc(tc, SQRT(f / dd));
   int conv = 0;
-  double dprev = 0.0;
-  for (int it = 0; it < 20; ++it) {
+  real dprev = 0;
+  for (int it = 0; it < NEWTON_MAXIT; ++it) {
     edge_eval(C, q, t, x, dx, ddx);
     cplx F = 0, Fp = 0;
     for (int a = 0; a < 3; ++a) {
       cplx xr = x[a] - rp[a];
       F += xr * xr;
-      Fp += 2.0 * xr * dx[a];
+      Fp += 2 * xr * dx[a];
     }
     cplx dt = F / Fp;
     t -= dt;
-    const double ad = cabs(dt), tol = 1e-15 * (1.0 + cabs(t));
+    const real ad = CABS(dt), tol = NEWTON_TOL * (1 + CABS(t));
     if (ad < tol) { conv = 1; break; }
-    if (dprev > 0 && ad < 0.1 * dprev && ad * ad * ad < tol * dprev * dprev) { conv = 1; break; }   /* A12'' */
-    if (it >= 1 && ad < 1e-3 * cabs(t) && orc_bernstein_rho(creal(t), cimag(t)) > rho_stop) { conv = 1; break; }
+    if (dprev > 0 && ad < (real)0.1 * dprev && ad * ad * ad < tol * dprev * dprev) { conv = 1; break; }   /* A12'' */
+    if (it >= 1 && ad < (real)1e-3 * CABS(t) && bernstein_rho_real(CRE(t), CIM(t)) > rho_stop) { conv = 1; break; }
     dprev = ad;
   }
-  if (cimag(t) < 0) t = conj(t);
-  *t0re = creal(t);
-  *t0im = cimag(t);
-  return conv && isfinite(creal(t)) && isfinite(cimag(t));
+  if (CIM(t) < 0) t = CONJ(t);
+  *t0re = CRE(t);
+  *t0im = CIM(t);
+  return conv && ISFIN(CRE(t)) && ISFIN(CIM(t));
 }
 
-/* Bernstein ellipse parameter rho(t0) = |t0 + sqrt(t0^2 - 1)|, branch with rho >= 1 (reading A5). */
-double orc_bernstein_rho(double re, double im) {
-  cplx t = re + I * im;
-  cplx s = csqrt(t * t - 1.0);
-  double r1 = cabs(t + s), r2 = cabs(t - s);
-  return r1 > r2 ? r1 : r2;
+int orc_find_t0(const double *C, int q, const double *rp, double rho_stop, double *t0re, double *t0im) {
+  real Cr[64 * 3], rr[3] = {rp[0], rp[1], rp[2]}, a, b;
+  for (int i = 0; i < 3 * q; ++i) Cr[i] = C[i];
+  int conv = find_t0_real(Cr, q, rr, rho_stop, &a, &b);
+  *t0re = (double)a;
+  *t0im = (double)b;
+  return conv;
 }
 
 /* Model integrals (reading A11, App. A.4): with a = Re t0, b = |Im t0|, Q(t) = (t-a)^2 + b^2,
  * I_k = int_{-1}^{1} t^k Q^{-1/2} dt, J_k = int t^k Q^{-3/2} dt, k = 0..q-1, by upward recurrences
  * ("calculated by a recurrence relation").  I_0 and J_0 in cancellation-free form. */
-void orc_model_integrals(double a, double b, int q, double *Iv, double *Jv) {
-  double Q1 = (1 - a) * (1 - a) + b * b, Qm = (1 + a) * (1 + a) + b * b;
-  double s1 = sqrt(Q1), sm = sqrt(Qm);
-  double I0, J0;
-  if (fabs(a) <= 1.0) {
-    I0 = asinh((1 - a) / b) + asinh((1 + a) / b);
+static void model_integrals_real(real a, real b, int q, real *Iv, real *Jv) {
+  real Q1 = (1 - a) * (1 - a) + b * b, Qm = (1 + a) * (1 + a) + b * b;
+  real s1 = SQRT(Q1), sm = SQRT(Qm);
+  real I0, J0;
+  if (FABS(a) <= 1) {
+    I0 = ASINH((1 - a) / b) + ASINH((1 + a) / b);
     J0 = ((1 - a) / s1 + (1 + a) / sm) / (b * b);
   } else {
-    double aa = fabs(a), u = aa + 1, v = aa - 1;
-    double su = sqrt(u * u + b * b), sv = sqrt(v * v + b * b);
-    I0 = log((u + su) / (v + sv));
+    real aa = FABS(a), u = aa + 1, v = aa - 1;
+    real su = SQRT(u * u + b * b), sv = SQRT(v * v + b * b);
+    I0 = LOG((u + su) / (v + sv));
     J0 = 4 * aa / (su * sv * (u * sv + v * su));
   }
   Iv[0] = I0;
   Jv[0] = J0;
-  double a2b2 = a * a + b * b;
+  real a2b2 = a * a + b * b;
   for (int k = 1; k < q; ++k) {
-    double sgn = ((k - 1) & 1) ? -1.0 : 1.0;          /* (-1)^{k-1} */
-    double beta = s1 - sgn * sm;                       /* [t^{k-1} sqrt(Q)]_{-1}^{1} */
-    double gam = 1.0 / s1 - sgn / sm;                  /* [t^{k-1} Q^{-1/2}]_{-1}^{1} */
+    real sgn = ((k - 1) & 1) ? -1 : 1;                 /* (-1)^{k-1} */
+    real beta = s1 - sgn * sm;                         /* [t^{k-1} sqrt(Q)]_{-1}^{1} */
+    real gam = 1 / s1 - sgn / sm;                      /* [t^{k-1} Q^{-1/2}]_{-1}^{1} */
     if (k == 1) {
       Iv[1] = beta + a * Iv[0];
       Jv[1] = a * Jv[0] - gam;
@@ -699,6 +824,12 @@ void orc_model_integrals(double a, double b, int q, double *Iv, double *Jv) {
   }
 }
 
+void orc_model_integrals(double a, double b, int q, double *Iv, double *Jv) {
+  real Ir[64], Jr[64];
+  model_integrals_real(a, b, q, Ir, Jr);
+  for (int k = 0; k < q; ++k) { Iv[k] = (double)Ir[k]; Jv[k] = (double)Jr[k]; }
+}
+
 /* Reading A11': where t0 lies outside the Bernstein ellipse rho = RHO_DIRECT the upward recurrences
  * amplify rounding (App. B.8: 1e-10..2e-7 near rho0 = 3 at p~ = 20), while the model integrands
  * t^k |t - t0|^{-m} are analytic inside that ellipse; there the same integrals are evaluated by an
@@ -706,13 +837,11 @@ void orc_model_integrals(double a, double b, int q, double *Iv, double *Jv) {
  * (accurate to ~1e-14 for |t0| <~ 1.1) are used. */
 #define RHO_DIRECT 1.6
 #define N_DIRECT 48
-void orc_model_integrals_direct(double a, double b, int q, double *Iv, double *Jv) {
-  double x[N_DIRECT], w[N_DIRECT];
-  orc_gauss_legendre(N_DIRECT, x, w);
+static void model_integrals_direct_real(real a, real b, int q, const real *x, const real *w, real *Iv, real *Jv) {
   for (int k = 0; k < q; ++k) { Iv[k] = 0; Jv[k] = 0; }
   for (int j = 0; j < N_DIRECT; ++j) {
-    double Qv = (x[j] - a) * (x[j] - a) + b * b;
-    double r1 = w[j] / sqrt(Qv), r3 = r1 / Qv, tk = 1;
+    real Qv = (x[j] - a) * (x[j] - a) + b * b;
+    real r1 = w[j] / SQRT(Qv), r3 = r1 / Qv, tk = 1;
     for (int k = 0; k < q; ++k) {
       Iv[k] += tk * r1;
       Jv[k] += tk * r3;
@@ -721,96 +850,115 @@ void orc_model_integrals_direct(double a, double b, int q, double *Iv, double *J
   }
 }
 
+void orc_model_integrals_direct(double a, double b, int q, double *Iv, double *Jv) {
+  real Ir[64], Jr[64], x[N_DIRECT], w[N_DIRECT];
+  gl_real(N_DIRECT, x, w);
+  model_integrals_direct_real(a, b, q, x, w, Ir, Jr);
+  for (int k = 0; k < q; ++k) { Iv[k] = (double)Ir[k]; Jv[k] = (double)Jr[k]; }
+}
+
 /* Per-edge quadrature data for one target. */
 typedef struct {
-  double w1[64], w3[64];   /* omega^{(1)}_k, omega^{(3)}_k (q <= 64) */
-  double om0;              /* this edge's contribution to Omega_0 */
-  double t0re, t0im;
+  real w1[64], w3[64];     /* omega^{(1)}_k, omega^{(3)}_k (q <= 64) */
+  real om0;                /* this edge's contribution to Omega_0 */
+  real t0re, t0im;
   int swap, conv;
 } edgeq_t;
+
+/* Constant tables of one run, in the working precision. */
+typedef struct {
+  real tgl[64], wgl[64], U[64 * 64], xo[256], wo[256], xd[N_DIRECT], wd[N_DIRECT];
+} tables_t;
+
+static void tables_init(tables_t *T, const orc_params *pr) {
+  gl_real(pr->q, T->tgl, T->wgl);
+  vandermonde_inverse_real(pr->q, T->tgl, T->U);
+  gl_real(pr->n_omega, T->xo, T->wo);
+  gl_real(N_DIRECT, T->xd, T->wd);
+}
 
 /* Step 5 for edge e: regime, t0, weights omega^{(m)}_k = [M^T U]_k |t_k - t0|^m / |d_k|^m
  * in the swap regime, w_k / |d_k|^m in the plain regime (readings A4, A5); and Omega_0's edge
  * integral by the sinh-split rule (reading A9) or plain Gauss-Legendre. */
-static void edge_quadrature(const patch_t *P, const orc_params *pr, int e, const double *rp, const double *u,
-                            const double *tgl, const double *wgl, const double *U, const double *xo,
-                            const double *wo, edgeq_t *E) {
+static void edge_quadrature(const patch_t *P, const orc_params *pr, const tables_t *T, int e, const real *rp,
+                            const real *u, edgeq_t *E) {
   int q = P->q;
-  const double *C = P->C + e * q * 3;
-  double t0r, t0i;
-  int conv = orc_find_t0(C, q, rp, 2.0 * pr->rho0, &t0r, &t0i);
+  const real *C = P->C + e * q * 3;
+  const real rho0 = pr->rho0;
+  real t0r, t0i;
+  int conv = find_t0_real(C, q, rp, 2 * rho0, &t0r, &t0i);
   E->t0re = t0r; E->t0im = t0i; E->conv = conv;
-  E->swap = conv && (orc_bernstein_rho(t0r, t0i) < pr->rho0);
-  double dn[64];
+  E->swap = conv && (bernstein_rho_real(t0r, t0i) < rho0);
+  real dn[64];
   for (int k = 0; k < q; ++k) {
-    const double *y = P->yl + 3 * (e * q + k);
-    double d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
+    const real *y = P->yl + 3 * (e * q + k);
+    real d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
     dn[k] = norm3(d);
   }
   if (E->swap) {
-    double Iv[64], Jv[64];
-    if (orc_bernstein_rho(t0r, t0i) >= RHO_DIRECT) orc_model_integrals_direct(t0r, fabs(t0i), q, Iv, Jv);
-    else orc_model_integrals(t0r, fabs(t0i), q, Iv, Jv);
+    real Iv[64], Jv[64];
+    if (bernstein_rho_real(t0r, t0i) >= (real)RHO_DIRECT) model_integrals_direct_real(t0r, FABS(t0i), q, T->xd, T->wd, Iv, Jv);
+    else model_integrals_real(t0r, FABS(t0i), q, Iv, Jv);
     for (int k = 0; k < q; ++k) {
-      double mu1 = 0, mu3 = 0;
-      for (int c = 0; c < q; ++c) { mu1 += Iv[c] * U[c * q + k]; mu3 += Jv[c] * U[c * q + k]; }
-      double tt = sqrt((tgl[k] - t0r) * (tgl[k] - t0r) + t0i * t0i);
-      double r1 = tt / dn[k];
+      real mu1 = 0, mu3 = 0;
+      for (int c = 0; c < q; ++c) { mu1 += Iv[c] * T->U[c * q + k]; mu3 += Jv[c] * T->U[c * q + k]; }
+      real tt = SQRT((T->tgl[k] - t0r) * (T->tgl[k] - t0r) + t0i * t0i);
+      real r1 = tt / dn[k];
       E->w1[k] = mu1 * r1;
       E->w3[k] = mu3 * r1 * r1 * r1;
     }
     /* Omega_0 on this edge: t = a + b sinh(s), n_Omega GL nodes on each side of a (reading A9) */
-    double a = t0r < -1 ? -1 : (t0r > 1 ? 1 : t0r), b = fabs(t0i);
-    double sR = asinh((1 - a) / b), sL = asinh((-1 - a) / b);
-    double acc = 0;
+    real a = t0r < -1 ? -1 : (t0r > 1 ? 1 : t0r), b = FABS(t0i);
+    real sR = ASINH((1 - a) / b), sL = ASINH((-1 - a) / b);
+    real acc = 0;
     for (int side = 0; side < 2; ++side) {
-      double lo = side ? 0.0 : sL, hi = side ? sR : 0.0;
+      real lo = side ? 0 : sL, hi = side ? sR : 0;
       if (hi <= lo) continue;
       for (int j = 0; j < pr->n_omega; ++j) {
-        double s = lo + (hi - lo) * (xo[j] + 1) / 2, W = (hi - lo) / 2 * wo[j];
-        double t = a + b * sinh(s), dt = b * cosh(s);
+        real s = lo + (hi - lo) * (T->xo[j] + 1) / 2, W = (hi - lo) / 2 * T->wo[j];
+        real t = a + b * SINH(s), dt = b * COSH(s);
         cplx x[3], dx[3], ddx[3];
         edge_eval(C, q, t, x, dx, ddx);
-        double d[3] = {rp[0] - creal(x[0]), rp[1] - creal(x[1]), rp[2] - creal(x[2])};
-        double tau[3] = {creal(dx[0]), creal(dx[1]), creal(dx[2])};
-        double dxu[3];
+        real d[3] = {rp[0] - CRE(x[0]), rp[1] - CRE(x[1]), rp[2] - CRE(x[2])};
+        real tau[3] = {CRE(dx[0]), CRE(dx[1]), CRE(dx[2])};
+        real dxu[3];
         cross3(d, u, dxu);
-        double nd = norm3(d);
+        real nd = norm3(d);
         acc += W * dt * (-(dot3(dxu, tau)) / (nd * (nd + dot3(u, d))));
       }
     }
     E->om0 = acc;
   } else {
-    double acc = 0;
+    real acc = 0;
     for (int k = 0; k < q; ++k) {
-      E->w1[k] = wgl[k] / dn[k];
-      E->w3[k] = wgl[k] / (dn[k] * dn[k] * dn[k]);
-      const double *y = P->yl + 3 * (e * q + k), *tau = P->tl + 3 * (e * q + k);
-      double d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]}, dxu[3];
+      E->w1[k] = T->wgl[k] / dn[k];
+      E->w3[k] = T->wgl[k] / (dn[k] * dn[k] * dn[k]);
+      const real *y = P->yl + 3 * (e * q + k), *tau = P->tl + 3 * (e * q + k);
+      real d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]}, dxu[3];
       cross3(d, u, dxu);
-      acc += wgl[k] * (-(dot3(dxu, tau)) / (dn[k] * (dn[k] + dot3(u, d))));
+      acc += T->wgl[k] * (-(dot3(dxu, tau)) / (dn[k] * (dn[k] + dot3(u, d))));
     }
     E->om0 = acc;
   }
 }
 
 /* Reading A8: gauge u = sigma_P z (local frame), Dirac string r' + s u (s > 0) must miss P. */
-static double gauge_sign(const patch_t *P, const double *rp, int side, int is_self) {
-  if (is_self) return -1.0;
-  double z = rp[2] - P->vl[0][2];
-  if (z > P->zhi + 0.1) return 1.0;   /* h_P = 1 in local scaled units */
-  if (z < P->zlo - 0.1) return -1.0;
+static real gauge_sign(const patch_t *P, const real *rp, int side, int is_self) {
+  if (is_self) return -1;
+  real z = rp[2] - P->vl[0][2];
+  if (z > P->zhi + (real)0.1) return 1;   /* h_P = 1 in local scaled units */
+  if (z < P->zlo - (real)0.1) return -1;
   /* barycentric coordinates of the projection in the vertex triangle */
-  const double *a = P->vl[0], *b = P->vl[1], *c = P->vl[2];
-  double det = (b[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (b[1] - a[1]);
-  double l1 = ((rp[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (rp[1] - a[1])) / det;
-  double l2 = ((b[0] - a[0]) * (rp[1] - a[1]) - (rp[0] - a[0]) * (b[1] - a[1])) / det;
-  double l0 = 1 - l1 - l2;
-  double mn = l0 < l1 ? l0 : l1;
+  const real *a = P->vl[0], *b = P->vl[1], *c = P->vl[2];
+  real det = (b[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (b[1] - a[1]);
+  real l1 = ((rp[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (rp[1] - a[1])) / det;
+  real l2 = ((b[0] - a[0]) * (rp[1] - a[1]) - (rp[0] - a[0]) * (b[1] - a[1])) / det;
+  real l0 = 1 - l1 - l2;
+  real mn = l0 < l1 ? l0 : l1;
   if (l2 < mn) mn = l2;
-  if (mn >= -0.25 && side != 2) return side > 0 ? 1.0 : -1.0;  /* side == 2: flag absent */
-  double mid = 0.5 * (P->zlo + P->zhi);
-  return (z - mid > 0) ? 1.0 : -1.0;
+  if (mn >= (real)-0.25 && side != 2) return side > 0 ? 1 : -1;  /* side == 2: flag absent */
+  real mid = (P->zlo + P->zhi) / 2;
+  return (z - mid > 0) ? 1 : -1;
 }
 
 /* ------------------------------------------------------------------------------------------------
@@ -818,21 +966,20 @@ static double gauge_sign(const patch_t *P, const double *rp, int side, int is_se
  * rows[4][n] (S, D, S', D') in GLOBAL units; dbg (optional) receives intermediates.
  * ----------------------------------------------------------------------------------------------*/
 typedef struct {
-  double om0, om[3], dom0, dom[3];
-  double t0[3][2];
+  real om0, om[3], dom0, dom[3];
+  real t0[3][2];
   int swap[3], conv[3];
-  double *W, *dW, *Th;     /* [np][4], [np][4], [np] */
+  double *W, *dW, *Th;     /* [np][4], [np][4], [np] (rounded to fp64) */
 } pair_dbg;
 
-static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, const double *tgl, const double *wgl,
-                     const double *xo, const double *wo, const double *x_glob, const double *nu_glob, int self_local,
-                     int side, unsigned mask, int raw, const double *nodes_glob, const double *normals_glob,
-                     const double *weights_glob, double *rows, pair_dbg *dbg, double *kap) {
+static int pair_rows(const patch_t *P, const orc_params *pr, const tables_t *T, const double *x_glob,
+                     const double *nu_glob, int self_local, int side, unsigned mask, int raw, const double *nodes_glob,
+                     const double *normals_glob, const double *weights_glob, real *rows, pair_dbg *dbg) {
   int p = P->p, q = P->q, n = P->n, np = P->np, L = (p + 1) * (p + 1);
-  const double inv4pi = 1.0 / (4.0 * ORC_PI), s2 = sqrt(2.0);
+  const real inv4pi = 1 / (4 * R_PI), s2 = SQRT((real)2);
   int is_self = self_local >= 0;
   int status = 0;
-  double rp[3], nup[3] = {0, 0, 0};
+  real rp[3], nup[3] = {0, 0, 0};
   to_local(P, x_glob, rp);
   if (nu_glob) rot_local(P, nu_glob, nup);
 
@@ -842,16 +989,16 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
   htab_eval(&ht, rp[0], rp[1], rp[2]);
 
   /* gauge (A8) and Step 5 per edge */
-  double sg = gauge_sign(P, rp, side, is_self);
-  double u[3] = {0, 0, sg};
+  real sg = gauge_sign(P, rp, side, is_self);
+  real u[3] = {0, 0, sg};
   edgeq_t E[3];
   for (int e = 0; e < 3; ++e) {
-    edge_quadrature(P, pr, e, rp, u, tgl, wgl, U, xo, wo, &E[e]);
+    edge_quadrature(P, pr, T, e, rp, u, &E[e]);
     if (!E[e].conv) status |= 1;
   }
 
   /* Step 6: line integrals (P:L1196-1211 eq lineintegrals, P:L1362-1376 eq dprimelineintegrals). */
-  double Om0 = 0, Om[3] = {0, 0, 0}, dOm0 = 0, dOm[3] = {0, 0, 0};
+  real Om0 = 0, Om[3] = {0, 0, 0}, dOm0 = 0, dOm[3] = {0, 0, 0};
   quat *Qt = malloc(sizeof(quat) * L), *dQt = malloc(sizeof(quat) * L);
   cplx *Vt = malloc(sizeof(cplx) * L);
   for (int k = 0; k < L; ++k) { Qt[k] = qzero(); dQt[k] = qzero(); Vt[k] = 0; }
@@ -859,15 +1006,15 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
     Om0 += E[e].om0;
     for (int kk = 0; kk < q; ++kk) {
       int kap = e * q + kk;
-      const double *y = P->yl + 3 * kap, *tau = P->tl + 3 * kap;
-      double d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
-      double w1 = E[e].w1[kk], w3 = E[e].w3[kk];
-      double nd = dot3(nup, d);
+      const real *y = P->yl + 3 * kap, *tau = P->tl + 3 * kap;
+      real d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
+      real w1 = E[e].w1[kk], w3 = E[e].w3[kk];
+      real nd = dot3(nup, d);
       for (int a = 0; a < 3; ++a) {
         Om[a] -= w1 * tau[a];            /* Omega = - int dr / |r' - r| */
         dOm[a] += w3 * nd * tau[a];      /* dOmega/dnu' = int (nu'.(r'-r)) dr / |r'-r|^3 */
       }
-      double txd[3];
+      real txd[3];
       cross3(tau, d, txd);
       dOm0 += w3 * dot3(nup, txd);       /* Biot-Savart form of dOmega_0/dnu' (reading A10) */
       quat qd = qvec(d[0], d[1], d[2]);
@@ -890,10 +1037,10 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
   }
   /* reading G1: Omega_0 := solid angle = - sum of the printed omega_0 (the sign is folded into the
    * edge integrand above).  Reading A7: self targets use u = -z and the principal value shift. */
-  if (is_self) Om0 -= 2.0 * ORC_PI;
+  if (is_self) Om0 -= 2 * R_PI;
 
   /* Step 7: translation (P:L1263-1268 eq cdlp1dintegral, reading G2). */
-  double *Wr = calloc(np * 4, sizeof(double)), *dWr = calloc(np * 4, sizeof(double)), *Th = calloc(np, sizeof(double));
+  real *Wr = calloc(np * 4, sizeof(real)), *dWr = calloc(np * 4, sizeof(real)), *Th = calloc(np, sizeof(real));
   quat Omq = {Om0, {Om[0], Om[1], Om[2]}}, dOmq = {dOm0, {dOm[0], dOm[1], dOm[2]}};
   for (int l = 1; l <= p; ++l)
     for (int m = 1; m <= l; ++m) {
@@ -903,17 +1050,17 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
         for (int k = -j; k <= j; ++k) {
           int mk = m - k, lj = l - j;
           if (mk > lj || mk < -lj) continue;
-          double T = Tjklm(j, k, l, m);
-          if (T == 0) continue;
+          real Tv = Tjklm(j, k, l, m);
+          if (Tv == 0) continue;
           int hk = hidx(j, k), hs = hidx(lj, mk);
           cplx Sv = ht.S[hs];
           cplx nuGS = nup[0] * ht.G[3 * hs] + nup[1] * ht.G[3 * hs + 1] + nup[2] * ht.G[3 * hs + 2];
           if (j >= 2) {
-            double cT = Cjl(j, l) * T;
+            real cT = Cjl(j, l) * Tv;
             lam = qadd(lam, qscale(Qt[hk], cT * Sv));
             dlam = qadd(dlam, qadd(qscale(dQt[hk], cT * Sv), qscale(Qt[hk], cT * nuGS)));
           }
-          th += Djl(j, l) * T * Vt[hk] * Sv;
+          th += Djl(j, l) * Tv * Vt[hk] * Sv;
         }
       int hl = hidx(l, m);
       const cplx *GS = ht.G + 3 * hl, *HS = ht.H + 9 * hl;
@@ -926,27 +1073,27 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
       quat tot = qscale(qadd(lam, gam), inv4pi), dtot = qscale(qadd(dlam, dgam), inv4pi);
       int c = lmidx(l, m);
       /* W = -sqrt(2) Im(I[lambda_1] + I[gamma]) (eq wlmdef) */
-      Wr[4 * c] = -s2 * cimag(tot.s);
-      dWr[4 * c] = -s2 * cimag(dtot.s);
-      for (int a = 0; a < 3; ++a) { Wr[4 * c + 1 + a] = -s2 * cimag(tot.v[a]); dWr[4 * c + 1 + a] = -s2 * cimag(dtot.v[a]); }
+      Wr[4 * c] = -s2 * CIM(tot.s);
+      dWr[4 * c] = -s2 * CIM(dtot.s);
+      for (int a = 0; a < 3; ++a) { Wr[4 * c + 1 + a] = -s2 * CIM(tot.v[a]); dWr[4 * c + 1 + a] = -s2 * CIM(dtot.v[a]); }
       /* Theta = sqrt(2) Im I[theta_1],  I[theta_1] = (1/4pi)[sum D T V S + S(r') Omega_0] (G2) */
-      Th[c] = s2 * cimag(inv4pi * (th + ht.S[hl] * Om0));
+      Th[c] = s2 * CIM(inv4pi * (th + ht.S[hl] * Om0));
     }
 
   /* Step 8, matrix mode (reading G3 for S'; Thm 3.3 for S). */
-  const double *PD = P->fit, *PSp = P->fit + 4 * np * n, *PSd = P->fit + 8 * np * n, *PSg = P->fit + 9 * np * n;
-  double *rS = rows, *rD = rows + n, *rSp = rows + 2 * n, *rDp = rows + 3 * n;
+  const real *PD = P->fit, *PSp = P->fit + 4 * np * n, *PSd = P->fit + 8 * np * n, *PSg = P->fit + 9 * np * n;
+  real *rS = rows, *rD = rows + n, *rSp = rows + 2 * n, *rDp = rows + 3 * n;
   for (int i = 0; i < 4 * n; ++i) rows[i] = 0;
   for (int c = 0; c < np; ++c) {
-    double zW[4] = {Wr[4 * c], -Wr[4 * c + 1], -Wr[4 * c + 2], -Wr[4 * c + 3]};
-    double zdW[4] = {dWr[4 * c], -dWr[4 * c + 1], -dWr[4 * c + 2], -dWr[4 * c + 3]};
-    const double *Wv = Wr + 4 * c + 1;
-    double nxW[3];
+    real zW[4] = {Wr[4 * c], -Wr[4 * c + 1], -Wr[4 * c + 2], -Wr[4 * c + 3]};
+    real zdW[4] = {dWr[4 * c], -dWr[4 * c + 1], -dWr[4 * c + 2], -dWr[4 * c + 3]};
+    const real *Wv = Wr + 4 * c + 1;
+    real nxW[3];
     cross3(nup, Wv, nxW);
-    double zS[4] = {-dot3(nup, Wv), -Wr[4 * c] * nup[0] - nxW[0], -Wr[4 * c] * nup[1] - nxW[1],
-                    -Wr[4 * c] * nup[2] - nxW[2]};
+    real zS[4] = {-dot3(nup, Wv), -Wr[4 * c] * nup[0] - nxW[0], -Wr[4 * c] * nup[1] - nxW[1],
+                  -Wr[4 * c] * nup[2] - nxW[2]};
     for (int b = 0; b < 4; ++b) {
-      const double *pd = PD + (b * np + c) * n, *psp = PSp + (b * np + c) * n, *psg = PSg + (b * np + c) * n;
+      const real *pd = PD + (b * np + c) * n, *psp = PSp + (b * np + c) * n, *psg = PSg + (b * np + c) * n;
       for (int i = 0; i < n; ++i) {
         rD[i] += zW[b] * pd[i];
         rDp[i] += zdW[b] * pd[i];
@@ -958,56 +1105,23 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
   }
   /* back to global units (reading A2): S rows scale with h, D' rows with 1/h */
   for (int i = 0; i < n; ++i) { rS[i] *= P->h; rDp[i] /= P->h; }
-  /* Optional: kappa_i = ||zeta||_inf * sum_c |P_{c,i}|, the forward-error scale of weight i of the
-   * Step-8 contraction when its input vector zeta is known to a relative accuracy (DESIGN.md §5
-   * parity bar).  Test instrumentation only. */
-  if (kap) {
-    double *kS = kap, *kD = kap + n, *kSp = kap + 2 * n, *kDp = kap + 3 * n;
-    double zW = 0, zdW = 0, zS = 0, zT = 0;
-    for (int c = 0; c < np; ++c) {
-      const double *Wv = Wr + 4 * c + 1;
-      double nxW[3];
-      cross3(nup, Wv, nxW);
-      double s4[4] = {fabs(dot3(nup, Wv)), fabs(Wr[4 * c] * nup[0] + nxW[0]), fabs(Wr[4 * c] * nup[1] + nxW[1]),
-                      fabs(Wr[4 * c] * nup[2] + nxW[2])};
-      for (int b = 0; b < 4; ++b) {
-        zW = fmax(zW, fabs(Wr[4 * c + b]));
-        zdW = fmax(zdW, fabs(dWr[4 * c + b]));
-        zS = fmax(zS, s4[b]);
-      }
-      zT = fmax(zT, fabs(Th[c]));
-    }
-    for (int i = 0; i < n; ++i) {
-      double aD = 0, aSp = 0, aSg = 0, aSd = 0;
-      for (int r = 0; r < 4 * np; ++r) { aD += fabs(PD[r * n + i]); aSp += fabs(PSp[r * n + i]); aSg += fabs(PSg[r * n + i]); }
-      for (int r = 0; r < np; ++r) aSd += fabs(PSd[r * n + i]);
-      kD[i] = zW * aD;
-      kDp[i] = zdW * aD;
-      kSp[i] = zS * aSp;
-      kS[i] = fmax(zW, zT) * (aSg + aSd);
-    }
-    for (int i = 0; i < n; ++i) { kS[i] *= P->h; kDp[i] /= P->h; }
-  }
 
   /* smooth-rule subtraction (reading A14), skipping the self node */
   if (!raw)
     for (int i = 0; i < n; ++i) {
       if (i == self_local) continue;
       const double *x = nodes_glob + 3 * i, *nu = normals_glob + 3 * i;
-      double d[3] = {x_glob[0] - x[0], x_glob[1] - x[1], x_glob[2] - x[2]};
-      double r = norm3(d), r3 = r * r * r, w = weights_glob[i];
-      double dn = dot3(d, nu);
+      real d[3] = {(real)x_glob[0] - x[0], (real)x_glob[1] - x[1], (real)x_glob[2] - x[2]};
+      real nur[3] = {nu[0], nu[1], nu[2]};
+      real r = norm3(d), r3 = r * r * r, w = weights_glob[i];
+      real dn = dot3(d, nur);
       rS[i] -= inv4pi / r * w;
       rD[i] -= inv4pi * dn / r3 * w;
-      if (kap) { kap[i] += fabs(inv4pi / r * w); kap[n + i] += fabs(inv4pi * dn / r3 * w); }
       if (nu_glob) {
-        double dnp = dot3(d, nu_glob);
+        real nug[3] = {nu_glob[0], nu_glob[1], nu_glob[2]};
+        real dnp = dot3(d, nug);
         rSp[i] -= -inv4pi * dnp / r3 * w;
-        rDp[i] -= inv4pi * (dot3(nu, nu_glob) / r3 - 3.0 * dn * dnp / (r3 * r * r)) * w;
-        if (kap) {
-          kap[2 * n + i] += fabs(inv4pi * dnp / r3 * w);
-          kap[3 * n + i] += inv4pi * (fabs(dot3(nu, nu_glob) / r3) + fabs(3.0 * dn * dnp / (r3 * r * r))) * w;
-        }
+        rDp[i] -= inv4pi * (dot3(nur, nug) / r3 - 3 * dn * dnp / (r3 * r * r)) * w;
       }
     }
   if (!(mask & 1)) for (int i = 0; i < n; ++i) rS[i] = 0;
@@ -1015,15 +1129,15 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
   if (!(mask & 4)) for (int i = 0; i < n; ++i) rSp[i] = 0;
   if (!(mask & 8)) for (int i = 0; i < n; ++i) rDp[i] = 0;
   for (int i = 0; i < 4 * n; ++i)
-    if (!isfinite(rows[i])) status |= 2;
+    if (!ISFIN(rows[i])) status |= 2;
 
   if (dbg) {
     dbg->om0 = Om0; dbg->dom0 = dOm0;
     for (int a = 0; a < 3; ++a) { dbg->om[a] = Om[a]; dbg->dom[a] = dOm[a]; }
     for (int e = 0; e < 3; ++e) { dbg->t0[e][0] = E[e].t0re; dbg->t0[e][1] = E[e].t0im; dbg->swap[e] = E[e].swap; dbg->conv[e] = E[e].conv; }
-    if (dbg->W) memcpy(dbg->W, Wr, sizeof(double) * 4 * np);
-    if (dbg->dW) memcpy(dbg->dW, dWr, sizeof(double) * 4 * np);
-    if (dbg->Th) memcpy(dbg->Th, Th, sizeof(double) * np);
+    if (dbg->W) for (int i = 0; i < 4 * np; ++i) dbg->W[i] = (double)Wr[i];
+    if (dbg->dW) for (int i = 0; i < 4 * np; ++i) dbg->dW[i] = (double)dWr[i];
+    if (dbg->Th) for (int i = 0; i < np; ++i) dbg->Th[i] = (double)Th[i];
   }
   free(Qt); free(dQt); free(Vt); free(Wr); free(dWr); free(Th);
   htab_free(&ht);
@@ -1031,45 +1145,42 @@ static int pair_rows(const patch_t *P, const orc_params *pr, const double *U, co
 }
 
 /* ------------------------------------------------------------------------------------------------
- * Public oracle entry points (called from tests via ctypes).
+ * Public oracle entry points (called from tests via ctypes).  Inputs and outputs are fp64.
  * ----------------------------------------------------------------------------------------------*/
-typedef struct {
-  double tgl[64], wgl[64], U[64 * 64], xo[256], wo[256];
-} tables_t;
-
-static void tables_init(tables_t *T, const orc_params *pr) {
-  orc_gauss_legendre(pr->q, T->tgl, T->wgl);
-  orc_vandermonde_inverse(pr->q, T->tgl, T->U);
-  orc_gauss_legendre(pr->n_omega, T->xo, T->wo);
-}
 
 /* Fit block of each patch, [P][13 np][n] (P_D, P_Sp, P_Sd, P_Sg, local scaled frame). */
 void orc_patch_fit(int64_t n_patches, int p, int q, const double *nodes, const double *normals, const double *verts,
-                   const double *edge_x, const double *edge_dx, double *fit_out, int32_t *status) {
-  orc_params pr = {p, q, 32, 3.0};
-  tables_t *T = malloc(sizeof(tables_t));
-  tables_init(T, &pr);
+                   const double *edge_x, const double *edge_dx, double *fit_out, int32_t *status, int rounding) {
+  orc_params pr = {p, q, 32, 3.0, rounding};
   int n = p * p, np = p * (p + 1) / 2;
-#pragma omp parallel for schedule(dynamic)
-  for (int64_t P = 0; P < n_patches; ++P) {
-    patch_t pt;
-    patch_build(&pt, &pr, nodes + P * n * 3, normals + P * n * 3, verts + P * 9, edge_x + P * 3 * q * 3,
-                edge_dx + P * 3 * q * 3, T->U, 1);
-    memcpy(fit_out + P * 13 * np * n, pt.fit, sizeof(double) * 13 * np * n);
-    if (status) status[P] = pt.status;
-    patch_free(&pt);
+  const int mode = fe_mode(rounding);
+#pragma omp parallel
+  {
+    const int saved = fegetround();
+    fesetround(mode);
+#pragma omp for schedule(dynamic)
+    for (int64_t P = 0; P < n_patches; ++P) {
+      patch_t pt;
+      patch_build(&pt, &pr, nodes + P * n * 3, normals + P * n * 3, verts + P * 9, edge_x + P * 3 * q * 3,
+                  edge_dx + P * 3 * q * 3, 1);
+      for (int i = 0; i < 13 * np * n; ++i) fit_out[P * 13 * np * n + i] = (double)pt.fit[i];
+      if (status) status[P] = pt.status;
+      patch_free(&pt);
+    }
+    fesetround(saved);
   }
-  free(T);
 }
 
 /* Rows of pairs (pair_target[k], pair_patch[k]) for S, D, S', D' -> vals[4][n_pairs][n]; status
- * bit0 Newton fallback, bit1 nonfinite, bit2 rank-deficient patch fit.  Pairs are processed
- * patch by patch (Steps 1-3 once per patch). */
-void orc_build_rows2(const orc_params *prm, int64_t n_patches, const double *nodes, const double *normals,
-                     const double *weights, const double *verts, const double *edge_x, const double *edge_dx,
-                     const double *tx, const double *tnormal, const int64_t *self_node, const int8_t *side,
-                     int64_t n_pairs, const int64_t *pair_target, const int32_t *pair_patch, uint32_t mask, int raw,
-                     double *vals, int32_t *pair_status, double *kappa) {
+ * bit0 Newton fallback, bit1 nonfinite, bit2 rank-deficient patch fit; zeta (optional) [n_pairs][9 np]:
+ * the Step 4-7 outputs Theta, W, dW of each pair (local scaled frame).  Pairs are processed
+ * patch by patch (Steps 1-3 once per patch).  The whole evaluation runs in the IEEE
+ * rounding mode prm->rounding (each OpenMP thread sets and restores its own mode). */
+void orc_build_rows(const orc_params *prm, int64_t n_patches, const double *nodes, const double *normals,
+                    const double *weights, const double *verts, const double *edge_x, const double *edge_dx,
+                    const double *tx, const double *tnormal, const int64_t *self_node, const int8_t *side,
+                    int64_t n_pairs, const int64_t *pair_target, const int32_t *pair_patch, uint32_t mask, int raw,
+                    double *vals, int32_t *pair_status, double *zeta) {
   orc_params pr = *prm;
   int p = pr.p, q = pr.q, n = p * p;
   tables_t *T = malloc(sizeof(tables_t));
@@ -1082,40 +1193,44 @@ void orc_build_rows2(const orc_params *prm, int64_t n_patches, const double *nod
   memcpy(fill, cnt, sizeof(int64_t) * (n_patches + 1));
   for (int64_t k = 0; k < n_pairs; ++k) ord[fill[pair_patch[k]]++] = k;
   free(fill);
-#pragma omp parallel for schedule(dynamic)
-  for (int64_t P = 0; P < n_patches; ++P) {
-    if (cnt[P + 1] == cnt[P]) continue;
-    patch_t pt;
-    patch_build(&pt, &pr, nodes + P * n * 3, normals + P * n * 3, verts + P * 9, edge_x + P * 3 * q * 3,
-                edge_dx + P * 3 * q * 3, T->U, 1);
-    double *rows = malloc(sizeof(double) * 4 * n), *krow = malloc(sizeof(double) * 4 * n);
-    for (int64_t s = cnt[P]; s < cnt[P + 1]; ++s) {
-      int64_t k = ord[s], t = pair_target[k];
-      int self_local = -1;
-      if (self_node && self_node[t] >= 0 && self_node[t] / n == P) self_local = (int)(self_node[t] % n);
-      int sd = side ? side[t] : 2;
-      int st = pair_rows(&pt, &pr, T->U, T->tgl, T->wgl, T->xo, T->wo, tx + 3 * t, tnormal ? tnormal + 3 * t : NULL,
-                         self_local, sd, mask, raw, nodes + P * n * 3, normals + P * n * 3, weights + P * n, rows, NULL,
-                         kappa ? krow : NULL);
-      if (kappa)
-        for (int kk = 0; kk < 4; ++kk) memcpy(kappa + ((size_t)kk * n_pairs + k) * n, krow + kk * n, sizeof(double) * n);
-      if (pt.status) st |= 4;
-      for (int kk = 0; kk < 4; ++kk) memcpy(vals + ((size_t)kk * n_pairs + k) * n, rows + kk * n, sizeof(double) * n);
-      if (pair_status) pair_status[k] = st;
+  const int mode = fe_mode(pr.rounding);
+#pragma omp parallel
+  {
+    const int saved = fegetround();
+    fesetround(mode);
+#pragma omp for schedule(dynamic)
+    for (int64_t P = 0; P < n_patches; ++P) {
+      if (cnt[P + 1] == cnt[P]) continue;
+      patch_t pt;
+      patch_build(&pt, &pr, nodes + P * n * 3, normals + P * n * 3, verts + P * 9, edge_x + P * 3 * q * 3,
+                  edge_dx + P * 3 * q * 3, 1);
+      real *rows = malloc(sizeof(real) * 4 * n);
+      for (int64_t s = cnt[P]; s < cnt[P + 1]; ++s) {
+        int64_t k = ord[s], t = pair_target[k];
+        int self_local = -1;
+        if (self_node && self_node[t] >= 0 && self_node[t] / n == P) self_local = (int)(self_node[t] % n);
+        int sd = side ? side[t] : 2;
+        pair_dbg dbg, *dp = NULL;
+        if (zeta) {   /* Steps 4-7 output of this pair: Theta [np], W [np][4], dW [np][4] */
+          const int np = pt.np;
+          dbg.Th = zeta + (size_t)k * 9 * np;
+          dbg.W = dbg.Th + np;
+          dbg.dW = dbg.W + 4 * np;
+          dp = &dbg;
+        }
+        int st = pair_rows(&pt, &pr, T, tx + 3 * t, tnormal ? tnormal + 3 * t : NULL, self_local, sd, mask, raw,
+                           nodes + P * n * 3, normals + P * n * 3, weights + P * n, rows, dp);
+        if (pt.status) st |= 4;
+        for (int kk = 0; kk < 4; ++kk)
+          for (int i = 0; i < n; ++i) vals[((size_t)kk * n_pairs + k) * n + i] = (double)rows[kk * n + i];
+        if (pair_status) pair_status[k] = st;
+      }
+      free(rows);
+      patch_free(&pt);
     }
-    free(rows); free(krow);
-    patch_free(&pt);
+    fesetround(saved);
   }
   free(cnt); free(ord); free(T);
-}
-
-void orc_build_rows(const orc_params *prm, int64_t n_patches, const double *nodes, const double *normals,
-                    const double *weights, const double *verts, const double *edge_x, const double *edge_dx,
-                    const double *tx, const double *tnormal, const int64_t *self_node, const int8_t *side,
-                    int64_t n_pairs, const int64_t *pair_target, const int32_t *pair_patch, uint32_t mask, int raw,
-                    double *vals, int32_t *pair_status) {
-  orc_build_rows2(prm, n_patches, nodes, normals, weights, verts, edge_x, edge_dx, tx, tnormal, self_node, side, n_pairs,
-                  pair_target, pair_patch, mask, raw, vals, pair_status, NULL);
 }
 
 /* Debug entry for one pair: intermediates (Omega_0, Omega, derivatives, t0, regimes, W, dW, Theta),
@@ -1125,83 +1240,112 @@ int orc_pair_debug(const orc_params *prm, const double *nodes, const double *nor
                    const double *nu, int self_local, int side, int raw, double *rows, double *scal, double *W,
                    double *dW, double *Th, double *frame) {
   orc_params pr = *prm;
+  const int saved = fegetround();
+  fesetround(fe_mode(pr.rounding));
   tables_t *T = malloc(sizeof(tables_t));
   tables_init(T, &pr);
   patch_t pt;
-  patch_build(&pt, &pr, nodes, normals, verts, edge_x, edge_dx, T->U, 1);
+  patch_build(&pt, &pr, nodes, normals, verts, edge_x, edge_dx, 1);
   pair_dbg dbg;
   dbg.W = W; dbg.dW = dW; dbg.Th = Th;
-  int st = pair_rows(&pt, &pr, T->U, T->tgl, T->wgl, T->xo, T->wo, x, nu, self_local, side, 15u, raw, nodes, normals,
-                     weights, rows, &dbg, NULL);
-  scal[0] = dbg.om0;
-  for (int a = 0; a < 3; ++a) scal[1 + a] = dbg.om[a];
-  scal[4] = dbg.dom0;
-  for (int a = 0; a < 3; ++a) scal[5 + a] = dbg.dom[a];
+  int n = pt.n;
+  real *rr = malloc(sizeof(real) * 4 * n);
+  int st = pair_rows(&pt, &pr, T, x, nu, self_local, side, 15u, raw, nodes, normals, weights, rr, &dbg);
+  for (int i = 0; i < 4 * n; ++i) rows[i] = (double)rr[i];
+  free(rr);
+  scal[0] = (double)dbg.om0;
+  for (int a = 0; a < 3; ++a) scal[1 + a] = (double)dbg.om[a];
+  scal[4] = (double)dbg.dom0;
+  for (int a = 0; a < 3; ++a) scal[5 + a] = (double)dbg.dom[a];
   for (int e = 0; e < 3; ++e) {
-    scal[8 + 4 * e] = dbg.t0[e][0];
-    scal[9 + 4 * e] = dbg.t0[e][1];
+    scal[8 + 4 * e] = (double)dbg.t0[e][0];
+    scal[9 + 4 * e] = (double)dbg.t0[e][1];
     scal[10 + 4 * e] = dbg.swap[e];
     scal[11 + 4 * e] = dbg.conv[e];
   }
   if (frame) {
-    for (int a = 0; a < 3; ++a) frame[a] = pt.o[a];
-    for (int a = 0; a < 9; ++a) frame[3 + a] = pt.Rm[a / 3][a % 3];
-    frame[12] = pt.h;
+    for (int a = 0; a < 3; ++a) frame[a] = (double)pt.o[a];
+    for (int a = 0; a < 9; ++a) frame[3 + a] = (double)pt.Rm[a / 3][a % 3];
+    frame[12] = (double)pt.h;
   }
   patch_free(&pt);
   free(T);
+  fesetround(saved);
   return st;
 }
 
-/* Near list (reading A6): near(t, P) iff |t - c_P| <= R_P + eta h_P, or t is a node of P; all pairs if
- * all_pairs.  Brute force O(N_T N_P).  Two-phase: counts into pair_ptr (size T+1, exclusive scan),
- * then fill if pair_patch != NULL. */
+/* ------------------------------------------------------------------------------------------------
+ * Near list (reading A6), fp64 in every build (integer work: the decision is taken in the kernel's
+ * precision).  Balls: c_P = sum_i w_i x_i / sum_i w_i summed sequentially over i,
+ * R_P = max distance of nodes, vertices and edge samples from c_P, h_P = max vertex chord; every
+ * product and sum is a separately rounded IEEE operation (no contraction: -ffp-contract=off), the
+ * order the CUDA path reproduces with __dmul_rn / __dadd_rn.
+ * ----------------------------------------------------------------------------------------------*/
+#pragma GCC push_options
+#pragma GCC optimize("fp-contract=off")
+static double dnorm3(double a, double b, double c) { return sqrt(a * a + b * b + c * c); }
+
+static void near_ball(int n, int q, const double *nodes, const double *weights, const double *verts,
+                      const double *edge_x, double *ball) {
+  double c[3] = {0, 0, 0}, ws = 0;
+  for (int i = 0; i < n; ++i) {
+    double w = weights[i];
+    ws += w;
+    for (int a = 0; a < 3; ++a) c[a] += w * nodes[i * 3 + a];
+  }
+  for (int a = 0; a < 3; ++a) c[a] /= ws;
+  double R = 0;
+  for (int i = 0; i < n; ++i) {
+    double r = dnorm3(nodes[i * 3] - c[0], nodes[i * 3 + 1] - c[1], nodes[i * 3 + 2] - c[2]);
+    if (r > R) R = r;
+  }
+  for (int v = 0; v < 3; ++v) {
+    double r = dnorm3(verts[3 * v] - c[0], verts[3 * v + 1] - c[1], verts[3 * v + 2] - c[2]);
+    if (r > R) R = r;
+  }
+  for (int k = 0; k < 3 * q; ++k) {
+    const double *y = edge_x + k * 3;
+    double r = dnorm3(y[0] - c[0], y[1] - c[1], y[2] - c[2]);
+    if (r > R) R = r;
+  }
+  double h = 0;
+  for (int e = 0; e < 3; ++e) {
+    const double *a = verts + 3 * e, *b = verts + 3 * ((e + 1) % 3);
+    double l = dnorm3(b[0] - a[0], b[1] - a[1], b[2] - a[2]);
+    if (l > h) h = l;
+  }
+  ball[0] = c[0]; ball[1] = c[1]; ball[2] = c[2]; ball[3] = R; ball[4] = h;
+}
+
+/* Test hook: the balls (c, R, h) of all patches. */
+void orc_near_balls(int64_t n_patches, int p, int q, const double *nodes, const double *weights, const double *verts,
+                    const double *edge_x, double *ball) {
+  int n = p * p;
+  for (int64_t P = 0; P < n_patches; ++P)
+    near_ball(n, q, nodes + P * n * 3, weights + P * n, verts + P * 9, edge_x + P * 3 * q * 3, ball + P * 5);
+}
+
+static int near_test(const double *tx, const double *b, double eta) {
+  return dnorm3(tx[0] - b[0], tx[1] - b[1], tx[2] - b[2]) <= b[3] + eta * b[4];
+}
+
+/* near(t, P) iff |t - c_P| <= R_P + eta h_P, or t is a node of P; all pairs if all_pairs.  Brute force
+ * O(N_T N_P).  Two-phase: counts into pair_ptr (size T+1, exclusive scan), then fill if pair_patch !=
+ * NULL. */
 void orc_near_list(int64_t n_patches, int p, int q, const double *nodes, const double *weights, const double *verts,
                    const double *edge_x, int64_t n_targets, const double *tx, const int64_t *self_node, double eta,
                    int all_pairs, int64_t *pair_ptr, int32_t *pair_patch) {
   int n = p * p;
   double *ball = malloc(sizeof(double) * n_patches * 5);
-  for (int64_t P = 0; P < n_patches; ++P) {
-    double c[3] = {0, 0, 0}, ws = 0;
-    for (int i = 0; i < n; ++i) {
-      double w = weights[P * n + i];
-      ws += w;
-      for (int a = 0; a < 3; ++a) c[a] += w * nodes[(P * n + i) * 3 + a];
-    }
-    for (int a = 0; a < 3; ++a) c[a] /= ws;
-    double R = 0;
-    for (int i = 0; i < n; ++i) {
-      double d[3] = {nodes[(P * n + i) * 3] - c[0], nodes[(P * n + i) * 3 + 1] - c[1], nodes[(P * n + i) * 3 + 2] - c[2]};
-      double r = norm3(d);
-      if (r > R) R = r;
-    }
-    for (int v = 0; v < 3; ++v) {
-      double d[3] = {verts[P * 9 + 3 * v] - c[0], verts[P * 9 + 3 * v + 1] - c[1], verts[P * 9 + 3 * v + 2] - c[2]};
-      double r = norm3(d);
-      if (r > R) R = r;
-    }
-    for (int k = 0; k < 3 * q; ++k) {
-      const double *y = edge_x + (P * 3 * q + k) * 3;
-      double d[3] = {y[0] - c[0], y[1] - c[1], y[2] - c[2]};
-      double r = norm3(d);
-      if (r > R) R = r;
-    }
-    double h;
-    double o[3], Rm[3][3];
-    patch_frame(verts + P * 9, o, Rm, &h);
-    for (int a = 0; a < 3; ++a) ball[P * 5 + a] = c[a];
-    ball[P * 5 + 3] = R;
-    ball[P * 5 + 4] = h;
-  }
+  orc_near_balls(n_patches, p, q, nodes, weights, verts, edge_x, ball);
   int fill = pair_patch != NULL;
   if (!fill) pair_ptr[0] = 0;
 #pragma omp parallel for schedule(static)
   for (int64_t t = 0; t < n_targets; ++t) {
     int64_t k = fill ? pair_ptr[t] : 0, c = 0;
     for (int64_t P = 0; P < n_patches; ++P) {
-      const double *b = ball + P * 5;
-      double d[3] = {tx[3 * t] - b[0], tx[3 * t + 1] - b[1], tx[3 * t + 2] - b[2]};
-      int near = all_pairs || norm3(d) <= b[3] + eta * b[4] || (self_node && self_node[t] >= 0 && self_node[t] / n == P);
+      int near = all_pairs || near_test(tx + 3 * t, ball + P * 5, eta) ||
+                 (self_node && self_node[t] >= 0 && self_node[t] / n == P);
       if (near) {
         if (fill) pair_patch[k++] = (int32_t)P;
         c++;
@@ -1214,10 +1358,16 @@ void orc_near_list(int64_t n_patches, int p, int q, const double *nodes, const d
   free(ball);
 }
 
-/* Test hook: the q-point U table and GL nodes/weights. */
+#pragma GCC pop_options
+
+/* Test hook: the q-point U table and GL nodes/weights (rounded to fp64). */
 void orc_tables(int q, double *t, double *w, double *U) {
-  orc_gauss_legendre(q, t, w);
-  orc_vandermonde_inverse(q, t, U);
+  real *tr = malloc(sizeof(real) * q), *wr = malloc(sizeof(real) * q), *Ur = malloc(sizeof(real) * q * q);
+  gl_real(q, tr, wr);
+  vandermonde_inverse_real(q, tr, Ur);
+  for (int i = 0; i < q; ++i) { t[i] = (double)tr[i]; w[i] = (double)wr[i]; }
+  for (int i = 0; i < q * q; ++i) U[i] = (double)Ur[i];
+  free(tr); free(wr); free(Ur);
 }
 
 /* Near pairs restricted to a list of patches (same rule as orc_near_list, reading A6), brute force
@@ -1231,35 +1381,10 @@ int64_t orc_near_pairs_for_patches(int p, int q, const double *nodes, const doub
   int64_t k = 0;
   for (int64_t s = 0; s < n_sel; ++s) {
     int64_t P = sel[s];
-    double c[3] = {0, 0, 0}, ws = 0;
-    for (int i = 0; i < n; ++i) {
-      double w = weights[P * n + i];
-      ws += w;
-      for (int a = 0; a < 3; ++a) c[a] += w * nodes[(P * n + i) * 3 + a];
-    }
-    for (int a = 0; a < 3; ++a) c[a] /= ws;
-    double R = 0;
-    for (int i = 0; i < n; ++i) {
-      double d[3] = {nodes[(P * n + i) * 3] - c[0], nodes[(P * n + i) * 3 + 1] - c[1], nodes[(P * n + i) * 3 + 2] - c[2]};
-      double r = norm3(d);
-      if (r > R) R = r;
-    }
-    for (int v = 0; v < 3; ++v) {
-      double d[3] = {verts[P * 9 + 3 * v] - c[0], verts[P * 9 + 3 * v + 1] - c[1], verts[P * 9 + 3 * v + 2] - c[2]};
-      double r = norm3(d);
-      if (r > R) R = r;
-    }
-    for (int kk = 0; kk < 3 * q; ++kk) {
-      const double *y = edge_x + (P * 3 * q + kk) * 3;
-      double d[3] = {y[0] - c[0], y[1] - c[1], y[2] - c[2]};
-      double r = norm3(d);
-      if (r > R) R = r;
-    }
-    double h, o[3], Rm[3][3];
-    patch_frame(verts + P * 9, o, Rm, &h);
+    double b[5];
+    near_ball(n, q, nodes + P * n * 3, weights + P * n, verts + P * 9, edge_x + P * 3 * q * 3, b);
     for (int64_t t = 0; t < n_targets; ++t) {
-      double d[3] = {tx[3 * t] - c[0], tx[3 * t + 1] - c[1], tx[3 * t + 2] - c[2]};
-      int near = all_pairs || norm3(d) <= R + eta * h || (self_node && self_node[t] >= 0 && self_node[t] / n == P);
+      int near = all_pairs || near_test(tx + 3 * t, b, eta) || (self_node && self_node[t] >= 0 && self_node[t] / n == P);
       if (near) {
         if (k < cap) { out_t[k] = t; out_p[k] = (int32_t)P; }
         ++k;

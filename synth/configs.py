@@ -56,7 +56,8 @@ def _assemble(S, parts, params):
 
 
 def make_config(cfg, n_off=None, include_nodes=True, freq=None, p=None, seed_offset=0):
-    """Return dict(surface, tx, tnormal, self_node, side, p, q, eta, all_pairs, name)."""
+    """Return dict(surface, tx, tnormal, self_node, side, p, q, eta, all_pairs, name[, mask]); `mask` (kernel
+    mask, default all four) is S|D for config 7, whose grid targets carry no normal."""
     rng = np.random.Generator(np.random.PCG64(CONFIG_SEEDS[cfg] + seed_offset))
     if cfg == 1:
         pp = p or 4
@@ -174,6 +175,6 @@ def make_config(cfg, n_off=None, include_nodes=True, freq=None, p=None, seed_off
         X = X[~inside_interlocked_tori(X)]
         cnt = X.shape[0]
         parts = [(X, np.zeros_like(X), np.full(cnt, -1, np.int64), np.ones(cnt, np.int8))]
-        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False,
+        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False, mask=3,
                                         name=f"cfg7-tori{S.n_patches}-grid{G}-p{pp}"))
     raise ValueError(cfg)

@@ -1,7 +1,7 @@
-"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs,
-element by element: near lists bit-exact; CSR weights per row within
-max(1e-11 * max_row |o|, 1e-13) (north star), with the conditioning band for
-targets within 1e-4 h of a patch edge or vertex (config 5)."""
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs, element by
+element: near lists bit-exact; CSR weights gated per row against the binary128 truth with
+the fp64 rounding envelope (tests/parity_util.py: e_g <= 8 s + 1e-11 M per row, and the error
+distribution within 2x of the fp64 oracle's); fit operators and the Step 4-7 vectors zeta likewise."""
 import numpy as np
 import pytest
 
@@ -13,8 +13,19 @@ import parity_util as U
 
 pytestmark = pytest.mark.gpu
 
-REL, ABS = 1e-11, 1e-13
 STATS = {}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dump_stats():
+    """Per-config / per-kernel parity statistics of this run -> gpurun_out/parity_stats.json."""
+    yield
+    import json
+    import os
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, "parity_stats.json"), "w") as f:
+        json.dump(STATS, f, indent=1, default=float)
 
 
 def _gpu_ctx(cfg):
@@ -41,23 +52,16 @@ def _gpu_rows_of(ptr, pat, tg, pa):
     return pos
 
 
-def _compare(vals_gpu, vo, pos, tg, n, band=None, kap=None, tag=""):
-    """Per-pair band relaxes the whole CSR row of that pair's target (max over its pairs)."""
-    inv = np.unique(tg, return_inverse=True)[1]
-    if band is not None:
-        rb = np.ones(inv.max() + 1)
-        np.maximum.at(rb, inv, band)
-        band = rb[inv]
-    worst = []
-    for k in range(4):
-        g = np.stack([vals_gpu[k][pp * n:(pp + 1) * n] for pp in pos]).reshape(-1)
-        st = {}
-        w, ratio = U.compare_rows(g, vo[k], inv, n, REL, ABS, band, None if kap is None else kap[k], st,
-                                  U.KAPPA_REL_DP if k == 3 else U.KAPPA_REL)
-        STATS[f"{tag}:{'S D Sp Dp'.split()[k]}"] = st
-        worst.append(w)
-    print(tag, STATS)
-    return worst
+def _gather(vals_gpu, pos, n):
+    return [np.stack([vals_gpu[k][pp * n:(pp + 1) * n] for pp in pos]) if vals_gpu[k] is not None else None
+            for k in range(4)]
+
+
+def _subsample(tg, pa, cap, rng):
+    if tg.size <= cap:
+        return tg, pa
+    sel = np.sort(rng.choice(tg.size, cap, replace=False))
+    return tg[sel], pa[sel]
 
 
 @pytest.mark.parametrize("p", [4, 6, 8, 10])
@@ -78,18 +82,14 @@ def test_cfg1_all_pairs(raw):
     ptr_o, pat_o = O.near_list(S, cfg["tx"], cfg["self_node"], cfg["eta"])
     assert np.array_equal(res["ptr"], ptr_o) and np.array_equal(res["pat"], pat_o)
     tg, pa = O.pairs_from_ptr(ptr_o, pat_o)
-    vo, sto, kap = O.build_rows(S, *tgs, tg, pa, raw=raw, kappa=True)
-    for k in range(4):
-        st = {}
-        w, _ = U.compare_rows(res["vals"][k], vo[k], tg, S.n, REL, ABS, kappa=kap[k], stats=st,
-                              kappa_rel=U.KAPPA_REL_DP if k == 3 else U.KAPPA_REL)
-        print("cfg1", k, st)
-        assert w <= 1.0, (k, w)
+    ref = U.reference(S, tgs, tg, pa, raw=raw)
+    g = [res["vals"][k][: pa.size * S.n].reshape(-1, S.n) for k in range(4)]
+    STATS[f"cfg1 raw={raw}"] = U.gate_all(g, ref, tg, tag=f"cfg1 raw={raw}")
     # columns and row pointers
     assert np.array_equal(res["row_ptr"], ptr_o * S.n)
     assert np.array_equal(res["col"][: pa.size * S.n].reshape(-1, S.n), pa[:, None] * S.n + np.arange(S.n)[None])
-    # Newton fallback flags agree except on knife-edge pairs
-    assert np.mean((res["status"][: pa.size] & 1) != (sto & 1)) < 1e-3
+    # Newton fallback flags agree with the fp64 oracle's except on knife-edge pairs
+    assert np.mean((res["status"][: pa.size] & 1) != (ref["st_o"] & 1)) < 1e-3
 
 
 def _sampled_config(cfgid, n_nodes_t, n_off, n_patches_sample, seed=0, **kw):
@@ -111,8 +111,8 @@ def _sampled_config(cfgid, n_nodes_t, n_off, n_patches_sample, seed=0, **kw):
     (6, 6000, 0, 10, {}),          # E3 stellarator, on-surface targets
 ])
 def test_full_size_surfaces_sampled_rows(cfgid, nodes, off, npatch, kw):
-    """Full-size surfaces of configs 2-4; GPU builds every row of a target subset; the oracle
-    recomputes all near pairs of a few random patches (near sets compared exactly)."""
+    """Full-size surfaces of configs 2-4 and 6; the GPU builds every row of a target subset; the near sets of
+    a few random patches are compared exactly, and a seeded sample of their pairs against the truth."""
     cfg, S, tgs, rng = _sampled_config(cfgid, nodes, off, npatch, **kw)
     res = U.gpu_build(cfg, S, tgs)
     ptr, pat = res["ptr"], res["pat"]
@@ -122,69 +122,26 @@ def test_full_size_surfaces_sampled_rows(cfgid, nodes, off, npatch, kw):
     for q in patches:
         gpu_t = np.sort(np.repeat(np.arange(ptr.size - 1), np.diff(ptr))[pat == q])
         assert np.array_equal(gpu_t, np.sort(tg[pa == q])), q
+    tg, pa = _subsample(tg, pa, 2000, rng)
     pos = _gpu_rows_of(ptr, pat, tg, pa)
-    vo, sto, kap = O.build_rows(S, *tgs, tg, pa, kappa=True)
-    band = _band_for_pairs(S, tgs[0], tg, pa)
-    worst = _compare(res["vals"], vo, pos, tg, S.n, band, kap, tag=f"cfg{cfgid}")
-    print(f"cfg{cfgid}: {tg.size} pairs, {int((band > 1).sum())} in the conditioning band, worst {worst}")
-    assert max(worst) <= 1.0, worst
-
-
-def _edge_distance(S, x, P=0):
-    """Distance of each point to the exact boundary curves of patch P (dense sampling + local
-    refinement) divided by h_P."""
-    from scipy.spatial import cKDTree
-    u = np.linspace(0, 1, 4001)
-    curves = [lambda u: (u, 0 * u), lambda u: (1 - u, u), lambda u: (0 * u, 1 - u)]
-    pts, par = [], []
-    for e, cv in enumerate(curves):
-        X, _, _ = S.eval_patch(P, *cv(u))
-        pts.append(X); par += [(e, uu) for uu in u]
-    E = np.concatenate(pts)
-    d, j = cKDTree(E).query(np.atleast_2d(x))
-    # refine around the closest sample
-    out = np.empty(d.shape)
-    for i in range(len(d)):
-        e, u0 = par[j[i]]
-        uu = np.clip(np.linspace(u0 - 3e-4, u0 + 3e-4, 2001), 0, 1)
-        X, _, _ = S.eval_patch(P, *curves[e](uu))
-        out[i] = np.min(np.linalg.norm(X - np.atleast_2d(x)[i], axis=1))
-    v = S.verts[P]
-    h = max(np.linalg.norm(v[k] - v[(k + 1) % 3]) for k in range(3))
-    return out / h
-
-
-def _band_for_pairs(S, tx, tg, pa):
-    """Conditioning band: rows within delta < 1e-4 h of an edge or vertex of P
-    have sensitivity ~ eps h / delta to input rounding; tolerance x max(1, 1e-5 h / delta)."""
-    band = np.ones(tg.shape[0])
-    for q in np.unique(pa):
-        sel = np.where(pa == q)[0]
-        delta = _edge_distance(S, tx[tg[sel]], int(q))
-        band[sel] = np.maximum(1.0, 1e-5 / np.maximum(delta, 1e-300))
-    return band
+    ref = U.reference(S, tgs, tg, pa)
+    inv = np.unique(tg, return_inverse=True)[1]
+    STATS[f"cfg{cfgid}"] = U.gate_all(_gather(res["vals"], pos, S.n), ref, inv, tag=f"cfg{cfgid}")
 
 
 def test_cfg5_close_evaluation_sweep():
-    """Config 5 (one cap, p = 10, all pairs) on 3000 of its seeded targets; rows within 1e-4 h of an
-    edge get the conditioning band max(1, 1e-5 h / delta), reported separately."""
-    cfg = make_config(5, n_off=3000)
+    """Config 5 (one cap, p = 10, all pairs): 1500 of its seeded targets (normal distance 1e-14..2h, projections
+    inside and outside the patch, near edges and vertices), every row against the truth."""
+    cfg = make_config(5, n_off=1500)
     S = cfg["surface"]
     tgs = (cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
     res = U.gpu_build(cfg, S, tgs)
     T = cfg["tx"].shape[0]
     assert np.array_equal(res["ptr"], np.arange(T + 1))
     tg = np.arange(T, dtype=np.int64); pa = np.zeros(T, np.int32)
-    vo, sto, kap = O.build_rows(S, *tgs, tg, pa, kappa=True)
-    delta = _edge_distance(S, cfg["tx"], 0)
-    band = np.maximum(1.0, 1e-5 / np.maximum(delta, 1e-300))
-    print("cfg5: rows in the conditioning band:", int((band > 1).sum()), "of", T)
-    for k in range(4):
-        st = {}
-        w, ratio = U.compare_rows(res["vals"][k], vo[k], tg, S.n, REL, ABS, band, kap[k], st,
-                                  U.KAPPA_REL_DP if k == 3 else U.KAPPA_REL)
-        print("cfg5", k, st, "worst", w)
-        assert w <= 1.0, (k, w)
+    ref = U.reference(S, tgs, tg, pa)
+    g = [res["vals"][k][: T * S.n].reshape(T, S.n) for k in range(4)]
+    STATS["cfg5"] = U.gate_all(g, ref, tg, tag="cfg5")
 
 
 def test_row_chunks_and_masks():
@@ -254,15 +211,16 @@ def test_apply_correction_spmv():
     assert np.abs(y.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-def test_fit_operators_match_oracle():
-    """The per-patch pseudo-inverse is unique (full column rank), so both sides agree to rounding."""
+def test_fit_operators_match_truth():
+    """The per-patch pseudo-inverse is unique (full column rank): per patch, the GPU's quaternion-QR operators
+    are within 4x the fp64 rounding envelope of the oracle's Householder QR (4 IEEE rounding modes) of the
+    binary128 operators (+1e-15 max|P|)."""
     cfg = make_config(2, n_off=10)
     S = cfg["surface"]
     ctx = _gpu_ctx(cfg)
     ds, dt = _upload(cfg)
     fit, st = ctx.patch_fit(ds)
     assert int(st.max()) == 0
-    import paper_2411_08342_b200.rrq  # noqa
     p, n = S.p, S.n
     npb = p * (p + 1) // 2
     stride = ctx.fit_bytes(1) // 8
@@ -274,16 +232,22 @@ def test_fit_operators_match_oracle():
     from synth.geometry import Surface
     Ssub = Surface(p=p, q=S.q, nodes=S.nodes[sel], normals=S.normals[sel], weights=S.weights[sel],
                    verts=S.verts[sel], edge_x=S.edge_x[sel], edge_dx=S.edge_dx[sel], uv=S.uv)
-    fo, _ = O.patch_fit(Ssub)
+    ft, _ = O.patch_fit(Ssub, prec="q")
+    env = np.zeros(len(sel))
+    for m in U.MODES:
+        fo, _ = O.patch_fit(Ssub, prec="d", rounding=m)
+        env = np.maximum(env, np.abs(fo - ft).reshape(len(sel), -1).max(1))
     nf = n + ((4 - n % 16) + 16) % 16   # row stride of the fit operators (Layout<P>::NF)
     for i, P in enumerate(sel):
         gb = g[P, off:off + 13 * npb * nf].reshape(13 * npb, nf)[:, :n]
-        assert np.abs(gb - fo[i]).max() <= 1e-9 * np.abs(fo[i]).max()
+        err, scale = np.abs(gb - ft[i]).max(), np.abs(ft[i]).max()
+        print(f"patch {P}: GPU fit error {err / scale:.2e}, fp64 envelope {env[i] / scale:.2e} (x max|P|)")
+        assert err <= 4 * env[i] + 1e-15 * scale
 
 
-def test_zeta_vectors_match_oracle():
-    """Element-wise parity of the Steps 4-7 output (the contraction vectors zeta = (Theta, zeta(W),
-    zeta(dW))) before the ill-conditioned Step-8 contraction: |g - o| <= 1e-10 max|zeta|."""
+def test_zeta_vectors_match_truth():
+    """Element-wise parity of the Steps 4-7 output (the contraction vectors zeta = (Theta, zeta(W), zeta(dW)))
+    before the Step-8 contraction, against the truth with the fp64 rounding envelope (tests/parity_util.py)."""
     cfg, S, tgs, rng = _sampled_config(2, 3000, 3000, 0)
     res = U.gpu_build(cfg, S, tgs)
     perm, Z = res["ctx"].debug_zeta(10 ** 8)
@@ -291,21 +255,13 @@ def test_zeta_vectors_match_oracle():
     inv[perm] = np.arange(perm.size)
     ptr, pat = res["ptr"], res["pat"]
     tgt = np.repeat(np.arange(ptr.size - 1), np.diff(ptr))
-    n, p = S.n, S.p
+    p = S.p
     npb = p * (p + 1) // 2
-    worst = 0.0
-    sample = rng.choice(np.sort(perm), 150, replace=False)
-    band = _band_for_pairs(S, tgs[0], tgt[sample], pat[sample])
-    for k, bnd in zip(sample, band):
-        t, P = tgt[k], pat[k]
-        sl = int(tgs[2][t] % n) if tgs[2][t] >= 0 and tgs[2][t] // n == P else -1
-        d = O.pair_debug(S, P, tgs[0][t], tgs[1][t], self_local=sl, side=int(tgs[3][t]))
-        W, dW, Th = d["W"], d["dW"], d["Theta"]
-        for a, b, ref, rel in [(0, npb, Th, U.KAPPA_REL),
-                               (npb, 5 * npb, np.concatenate([W[:, 0], -W[:, 1], -W[:, 2], -W[:, 3]]), U.KAPPA_REL),
-                               (5 * npb, 9 * npb, np.concatenate([dW[:, 0], -dW[:, 1], -dW[:, 2], -dW[:, 3]]),
-                                U.KAPPA_REL_DP)]:
-            worst = max(worst, np.abs(Z[inv[k]][a:b] - ref).max() / (rel * bnd * np.abs(ref).max()))
+    sample = np.sort(rng.choice(np.sort(perm), 300, replace=False))
+    ref = U.reference(S, tgs, tgt[sample], pat[sample], zeta=True)
+    zref = dict(zt=U.zeta_to_gpu_layout(ref["zt"], npb), zenv=U.zeta_env_to_gpu_layout(ref["zenv"], npb))
+    zg = np.stack([Z[inv[k]][: 9 * npb] for k in sample])
+    worst = U.gate_zeta(zg, zref, tag="cfg2")
     assert worst <= 1.0, worst
 
 
@@ -381,13 +337,13 @@ def test_cfg7_tori_volume_grid():
     for q in patches:
         gpu_t = np.sort(np.repeat(np.arange(ptr.size - 1), np.diff(ptr))[pat == q])
         assert np.array_equal(gpu_t, np.sort(tg[pa == q])), q
-    sub = rng.choice(tg.size, size=min(4000, tg.size), replace=False)
-    tg, pa = tg[sub], pa[sub]
+    tg, pa = _subsample(tg, pa, 1500, rng)
     pos = _gpu_rows_of(ptr, pat, tg, pa)
-    vo, sto, kap = O.build_rows(S, *tgs, tg, pa, kappa=True)
-    band = _band_for_pairs(S, tgs[0], tg, pa)
-    worst = _compare(res["vals"], vo, pos, tg, S.n, band, kap, tag="cfg7")
-    assert max(worst) <= 1.0, worst
+    ref = U.reference(S, tgs, tg, pa)
+    inv = np.unique(tg, return_inverse=True)[1]
+    STATS["cfg7"] = U.gate_all(_gather(res["vals"], pos, S.n), ref, inv, tag="cfg7", kernels=(0, 1))
+    for k in (2, 3):   # no target normals on the volume grid: S', D' rows are identically zero
+        assert not np.any(_gather(res["vals"], pos, S.n)[k])
     # Green's representation over all close targets
     src_rng = np.random.default_rng(11)
     src = src_rng.normal(size=(4, 3)); src = 30.0 * src / np.linalg.norm(src, axis=1, keepdims=True) + [7.4, 0, 0]
@@ -430,12 +386,13 @@ def test_cfg4_bench_launch_configuration_sampled():
     rng = np.random.default_rng(3)
     patches = rng.choice(S.n_patches, size=6, replace=False)
     tg, pa = O.near_pairs_for_patches(S, cfg["tx"], cfg["self_node"], cfg["eta"], patches)
+    tg, pa = _subsample(tg, pa, 2500, rng)
     n = S.n
     got = {k: np.zeros((tg.size, n)) for k in range(4)}
     state = {}
 
     def on_chunk(when, i, o, npairs=None):
-        if when == "before":
+        if when != "after":
             return
         hptr = state["hptr"]
         r0, r1 = state["chunks"][i]
@@ -461,19 +418,11 @@ def test_cfg4_bench_launch_configuration_sampled():
     assert len(state["chunks"]) > 1
     R.step(on_chunk=on_chunk)
     assert R.npairs == state["hptr"][-1]
-    vo, sto, kap = O.build_rows(S, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"], tg, pa, kappa=True)
-    band = _band_for_pairs(S, cfg["tx"], tg, pa)
+    tgs = (cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
+    ref = U.reference(S, tgs, tg, pa)
     inv = np.unique(tg, return_inverse=True)[1]
-    rb = np.ones(inv.max() + 1); np.maximum.at(rb, inv, band)
-    worst = []
-    for k in range(4):
-        st = {}
-        w, _ = U.compare_rows(got[k].reshape(-1), vo[k], inv, n, REL, ABS, rb[inv], kap[k], st,
-                              U.KAPPA_REL_DP if k == 3 else U.KAPPA_REL)
-        worst.append(w)
-        print("cfg4 bench-config", "S D Sp Dp".split()[k], st, "worst", w)
-    print(f"cfg4 bench launch configuration: {tg.size} pairs of {len(patches)} patches, worst {worst}")
-    assert max(worst) <= 1.0, worst
+    STATS["cfg4 bench"] = U.gate_all([got[k] for k in range(4)], ref, inv, tag="cfg4 bench launch configuration")
+    print(f"cfg4 bench launch configuration: {tg.size} pairs of {len(patches)} patches")
 
 
 def _build_with_env(cfg, env):

@@ -55,14 +55,15 @@ def _targets(S, P):
             (S.nodes[P, 7] + 0.02 * h * nrm, 1, 1e-10)]
 
 
-@pytest.mark.parametrize("geom", ["sphere", "torus"])
-def test_W_Theta_vs_bruteforce_2form(geom):
+@pytest.mark.parametrize("geom,prec", [("sphere", "d"), ("torus", "d"), ("sphere", "q")])
+def test_W_Theta_vs_bruteforce_2form(geom, prec):
+    """prec "q": the binary128 truth build of the same source meets the same pins."""
     if geom == "sphere":
         S = make_sphere_surface(2, 6, 16); P = 5
     else:
         S = make_torus_surface(2.0, 0.5, 6, 10, 6, 16); P = 7
     for x, side, tol in _targets(S, P):
-        dbg = O.pair_debug(S, P, x, None, side=side)
+        dbg = O.pair_debug(S, P, x, None, side=side, prec=prec)
         rp = (x - dbg["origin"]) @ dbg["Rm"].T / dbg["h"]
         W, Th = _brute_W_Theta(S, P, dbg, rp)
         sc = max(np.abs(W).max(), np.abs(Th).max())
