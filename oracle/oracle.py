@@ -236,6 +236,28 @@ def pair_debug(S, P, x, nu, self_local=-1, side=2, raw=True, n_omega=32, rho0=3.
                 W=W, dW=dW, Theta=Th, origin=frame[:3], Rm=frame[3:12].reshape(3, 3), h=frame[12], status=st)
 
 
+def pairs_debug(S, P, x, nu=None, self_local=None, side=None, raw=True, n_omega=32, rho0=3.0, prec="d",
+                rounding="nearest"):
+    """Intermediates of many targets against patch P (patch built once).  Returns dict of arrays: rows
+    [T, 4, n], Omega0 [T], Omega [T, 3], dOmega0 [T], dOmega [T, 3], t0 [T, 3] complex, swap/conv [T, 3],
+    status [T] (local scaled frame of the patch, as pair_debug)."""
+    x = _c(np.atleast_2d(x), np.float64)
+    T = x.shape[0]
+    n = S.n
+    rows = np.zeros((T, 4, n)); scal = np.zeros((T, 20)); st = np.zeros(T, np.int32)
+    sl = _c(np.full(T, -1) if self_local is None else self_local, np.int32)
+    sd = _c(np.full(T, 2) if side is None else side, np.int32)
+    pr = params(S.p, S.q, n_omega, rho0, rounding)
+    lib(prec).orc_pairs_debug(ctypes.byref(pr), _p(_c(S.nodes[P], np.float64)), _p(_c(S.normals[P], np.float64)),
+                              _p(_c(S.weights[P], np.float64)), _p(_c(S.verts[P], np.float64)),
+                              _p(_c(S.edge_x[P], np.float64)), _p(_c(S.edge_dx[P], np.float64)), ctypes.c_int64(T),
+                              _p(x), _p(_c(nu, np.float64)) if nu is not None else None, _p(sl), _p(sd),
+                              ctypes.c_int(int(raw)), _p(rows), _p(scal), _p(st))
+    return dict(rows=rows, Omega0=scal[:, 0], Omega=scal[:, 1:4], dOmega0=scal[:, 4], dOmega=scal[:, 5:8],
+                t0=scal[:, 8:20:4] + 1j * scal[:, 9:20:4], swap=scal[:, 10:20:4].astype(int),
+                conv=scal[:, 11:20:4].astype(int), status=st)
+
+
 def pairs_from_ptr(ptr, pat):
     T = ptr.shape[0] - 1
     tgt = np.repeat(np.arange(T, dtype=np.int64), np.diff(ptr))

@@ -1274,6 +1274,51 @@ int orc_pair_debug(const orc_params *prm, const double *nodes, const double *nor
   return st;
 }
 
+/* Batched debug entry: many targets against ONE patch (the patch, its fit and edge tables built once).
+ * Per target: rows [4][n] and scal[20] as in orc_pair_debug (Omega_0, Omega, dOmega_0, dOmega, t0/regime
+ * per edge); self_local[i] < 0 for non-self targets, side[i] as in orc_pair_debug, nu may be NULL. */
+void orc_pairs_debug(const orc_params *prm, const double *nodes, const double *normals, const double *weights,
+                     const double *verts, const double *edge_x, const double *edge_dx, int64_t n_targets,
+                     const double *x, const double *nu, const int32_t *self_local, const int32_t *side, int raw,
+                     double *rows, double *scal, int32_t *status) {
+  orc_params pr = *prm;
+  tables_t *T = malloc(sizeof(tables_t));
+  tables_init(T, &pr);
+  patch_t pt;
+  patch_build(&pt, &pr, nodes, normals, verts, edge_x, edge_dx, 1);
+  const int n = pt.n;
+#pragma omp parallel
+  {
+    const int saved = fegetround();
+    fesetround(fe_mode(pr.rounding));
+    real *rr = malloc(sizeof(real) * 4 * n);
+#pragma omp for schedule(dynamic)
+    for (int64_t i = 0; i < n_targets; ++i) {
+      pair_dbg dbg;
+      dbg.W = dbg.dW = dbg.Th = NULL;
+      int st = pair_rows(&pt, &pr, T, x + 3 * i, nu ? nu + 3 * i : NULL, self_local ? self_local[i] : -1,
+                         side ? side[i] : 2, 15u, raw, nodes, normals, weights, rr, &dbg);
+      for (int k = 0; k < 4 * n; ++k) rows[i * 4 * n + k] = (double)rr[k];
+      double *sc = scal + i * 20;
+      sc[0] = (double)dbg.om0;
+      for (int a = 0; a < 3; ++a) sc[1 + a] = (double)dbg.om[a];
+      sc[4] = (double)dbg.dom0;
+      for (int a = 0; a < 3; ++a) sc[5 + a] = (double)dbg.dom[a];
+      for (int e = 0; e < 3; ++e) {
+        sc[8 + 4 * e] = (double)dbg.t0[e][0];
+        sc[9 + 4 * e] = (double)dbg.t0[e][1];
+        sc[10 + 4 * e] = dbg.swap[e];
+        sc[11 + 4 * e] = dbg.conv[e];
+      }
+      if (status) status[i] = st;
+    }
+    free(rr);
+    fesetround(saved);
+  }
+  patch_free(&pt);
+  free(T);
+}
+
 /* ------------------------------------------------------------------------------------------------
  * Near list (reading A6), fp64 in every build (integer work: the decision is taken in the kernel's
  * precision).  Balls: c_P = sum_i w_i x_i / sum_i w_i summed sequentially over i,
