@@ -65,8 +65,9 @@ __global__ void k_near_targets(int64_t n_targets, const double *__restrict__ tx,
         for (int it = cell_start[c]; it < cell_start[c + 1]; ++it) {
           int P = cell_items[it];
           const double *b = balls + (int64_t)P * 5;
-          double d[3] = {x[0] - b[0], x[1] - b[1], x[2] - b[2]};
-          bool near = sqrt(dot3(d, d)) <= b[3] + eta * b[4];
+          // the A6 test in the oracle's arithmetic (k_patch_balls: separately rounded IEEE operations)
+          bool near = norm3_rn(__dsub_rn(x[0], b[0]), __dsub_rn(x[1], b[1]), __dsub_rn(x[2], b[2])) <=
+                      __dadd_rn(b[3], __dmul_rn(eta, b[4]));
           if (P == selfP) { near = true; self_found = true; }
           if (near) {
             if (fill) pair_patch[k] = P;

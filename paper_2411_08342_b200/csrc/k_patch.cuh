@@ -7,38 +7,43 @@
 namespace rrq {
 
 // Near ball of patch P (reading A6): c_P = sum w x / sum w, R_P = max |x - c_P| over nodes, vertices
-// and edge samples, h_P = max vertex chord.  One warp per patch.  balls[P] = (c, R, h).
+// and edge samples, h_P = max vertex chord.  One thread per patch.  balls[P] = (c, R, h).
+// The near list is integer output decided in floating point, so the decision is taken in one fixed
+// arithmetic on both sides: sums sequential over the nodes, every product, sum, quotient
+// and square root a separately rounded IEEE operation (__dmul_rn/__dadd_rn/__ddiv_rn/__dsqrt_rn, no FMA
+// contraction) -- the CPU oracle, compiled with -ffp-contract=off, does the same in the same
+// order, so both produce the same bits.
 __global__ void k_patch_balls(int64_t n_patches, int n, int q, const double *__restrict__ nodes,
                               const double *__restrict__ weights, const double *__restrict__ verts,
                               const double *__restrict__ edge_x, double *__restrict__ balls) {
-  int lane = threadIdx.x & 31;
-  int64_t P = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t P = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (P >= n_patches) return;
   const double *x = nodes + P * n * 3, *w = weights + P * n;
-  double c[3] = {0, 0, 0}, ws = 0;
-  for (int i = lane; i < n; i += 32) {
-    ws += w[i];
-    for (int a = 0; a < 3; ++a) c[a] += w[i] * x[3 * i + a];
+  double c0 = 0, c1 = 0, c2 = 0, ws = 0;
+  for (int i = 0; i < n; ++i) {
+    const double wi = w[i];
+    ws = __dadd_rn(ws, wi);
+    c0 = __dadd_rn(c0, __dmul_rn(wi, x[3 * i]));
+    c1 = __dadd_rn(c1, __dmul_rn(wi, x[3 * i + 1]));
+    c2 = __dadd_rn(c2, __dmul_rn(wi, x[3 * i + 2]));
   }
-  ws = warp_sum(ws);
-  for (int a = 0; a < 3; ++a) c[a] = warp_sum(c[a]) / ws;
+  c0 = __ddiv_rn(c0, ws);
+  c1 = __ddiv_rn(c1, ws);
+  c2 = __ddiv_rn(c2, ws);
   double R = 0;
-  for (int i = lane; i < n + 3 + 3 * q; i += 32) {
+  for (int i = 0; i < n + 3 + 3 * q; ++i) {
     const double *y = i < n ? x + 3 * i : (i < n + 3 ? verts + P * 9 + 3 * (i - n) : edge_x + (P * 3 * q + (i - n - 3)) * 3);
-    double d[3] = {y[0] - c[0], y[1] - c[1], y[2] - c[2]};
-    R = fmax(R, sqrt(dot3(d, d)));
+    const double r = norm3_rn(__dsub_rn(y[0], c0), __dsub_rn(y[1], c1), __dsub_rn(y[2], c2));
+    if (r > R) R = r;
   }
-  for (int o = 16; o > 0; o >>= 1) R = fmax(R, __shfl_xor_sync(0xffffffffu, R, o));
   double h = 0;
   for (int e = 0; e < 3; ++e) {
     const double *a = verts + P * 9 + 3 * e, *b = verts + P * 9 + 3 * ((e + 1) % 3);
-    double d[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
-    h = fmax(h, sqrt(dot3(d, d)));
+    const double l = norm3_rn(__dsub_rn(b[0], a[0]), __dsub_rn(b[1], a[1]), __dsub_rn(b[2], a[2]));
+    if (l > h) h = l;
   }
-  if (lane == 0) {
-    double *o = balls + P * 5;
-    o[0] = c[0]; o[1] = c[1]; o[2] = c[2]; o[3] = R; o[4] = h;
-  }
+  double *o = balls + P * 5;
+  o[0] = c0; o[1] = c1; o[2] = c2; o[3] = R; o[4] = h;
 }
 
 // Frame, local edge samples / tangents, Legendre coefficients of the edge interpolants (A4'), height range.

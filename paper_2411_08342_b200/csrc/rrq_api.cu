@@ -27,6 +27,7 @@ struct rrq_ctx_s {
   std::string err;
   int64_t launches = 0;
   int num_sms = 148;
+  int device = 0;                // the device current at rrq_create; every call must run with it current
   // constant tables (device) + host copies
   double *d_tab = nullptr;
   double *d_trtab = nullptr;   // k_translate schedule + scale tables (TrCfg<p>)
@@ -323,6 +324,17 @@ static std::vector<double> make_trtab_p(int p) {
   }
 }
 
+static cudaError_t set_kernel_attributes(int p);
+
+// Every entry point runs with the device the context was created on (its tables, scratch and the kernels'
+// shared-memory attributes belong to that device).
+static rrq_status check_device(rrq_ctx c) {
+  int d = -1;
+  if (cudaGetDevice(&d) != cudaSuccess || d != c->device)
+    return fail(c, RRQ_ERR_INVALID_ARG, "the current CUDA device is not the one this rrq_ctx was created on");
+  return RRQ_OK;
+}
+
 rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   if (!out) return fail(nullptr, RRQ_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
@@ -339,6 +351,7 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   c->prm = p;
   int dev = 0;
   cudaGetDevice(&dev);
+  c->device = dev;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
   {
     const char *e = std::getenv("RRQ_NO_OVERLAP");
@@ -420,6 +433,13 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
     const std::vector<double> tt = make_trtab_p(p.p);
     if (cudaMalloc(&c->d_trtab, tt.size() * sizeof(double)) == cudaSuccess)
       cudaMemcpy(c->d_trtab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  // dynamic shared-memory opt-ins of this p's kernels, on this context's device (per device, per context:
+  // no process-global state, so contexts on several devices or host threads do not race)
+  if (set_kernel_attributes(p.p) != cudaSuccess) {
+    g_create_err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(cudaGetLastError());
+    rrq_destroy(c);
+    return RRQ_ERR_CUDA;
   }
   if (cuda_check(c, "rrq_create") != RRQ_OK) {
     g_create_err = c->err;
@@ -555,7 +575,7 @@ static rrq_status check_targets(rrq_ctx c, const rrq_targets *t) {
 
 static rrq_status compute_balls(rrq_ctx c, const rrq_surface *s, cudaStream_t st) {
   if (!ensure(c, c->balls, s->n_patches * 5 * sizeof(double))) return RRQ_ERR_CUDA;
-  k_patch_balls<<<nblk(s->n_patches, 4), 128, 0, st>>>(s->n_patches, c->prm.n_nodes, c->prm.p_edge, s->nodes,
+  k_patch_balls<<<nblk(s->n_patches, 128), 128, 0, st>>>(s->n_patches, c->prm.n_nodes, c->prm.p_edge, s->nodes,
                                                        s->weights, s->verts, s->edge_x, bp<double>(c->balls));
   c->launches++;
   return cuda_check(c, "k_patch_balls");
@@ -566,7 +586,7 @@ rrq_status rrq_near_list(rrq_ctx c, const rrq_surface *s, const rrq_targets *tg,
   if (!c) return RRQ_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   rrq_status r;
-  if ((r = check_surface(c, s)) || (r = check_targets(c, tg))) return r;
+  if ((r = check_device(c)) || (r = check_surface(c, s)) || (r = check_targets(c, tg))) return r;
   if (!pair_ptr || !n_pairs) return fail(c, RRQ_ERR_INVALID_ARG, "pair_ptr and n_pairs must be non-NULL");
   const int64_t T = tg->n_targets, Pn = s->n_patches;
   const int fill = pair_patch != nullptr;
@@ -668,11 +688,6 @@ static rrq_status patch_fit_impl(rrq_ctx c, const rrq_surface *s, double *fit, i
   k_patch_geom<P><<<(unsigned)Pn, 128, 0, st>>>(Pn, s->nodes, s->verts, s->edge_x, s->edge_dx, bp<double>(c->balls), c->T, fit);
   {
     using EC = EdgeTabCfg<P>;
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(k_edge_tables<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EC::SMEM);
-      set = true;
-    }
     k_edge_tables<P><<<(unsigned)Pn, EC::THREADS, EC::SMEM, st>>>(Pn, c->T.hc, c->d_trtab + TrCfg<P>::VLAM,
                                                                   c->d_trtab + TrCfg<P>::VTH, fit);
   }
@@ -681,11 +696,6 @@ static rrq_status patch_fit_impl(rrq_ctx c, const rrq_surface *s, double *fit, i
   using FC = FitCfg<P>;
   int grid = (int)std::min<int64_t>(Pn, 2 * c->num_sms);
   if (!ensure(c, c->fitwork, (size_t)grid * FC::WS * sizeof(double))) return RRQ_ERR_CUDA;
-  static bool fattr = false;
-  if (!fattr) {
-    cudaFuncSetAttribute(k_patch_fit_q<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FC::SMEM);
-    fattr = true;
-  }
   k_patch_fit_q<P><<<grid, 256, FC::SMEM, st>>>(Pn, s->nodes, s->normals, c->T.hc, fit, bp<double>(c->fitwork), status);
   c->launches++;
   return cuda_check(c, "k_patch_fit");
@@ -694,7 +704,7 @@ static rrq_status patch_fit_impl(rrq_ctx c, const rrq_surface *s, double *fit, i
 rrq_status rrq_patch_fit(rrq_ctx c, const rrq_surface *s, void *fit, int32_t *patch_status, rrq_stream_t stream) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   rrq_status r;
-  if ((r = check_surface(c, s))) return r;
+  if ((r = check_device(c)) || (r = check_surface(c, s))) return r;
   if (!fit) return fail(c, RRQ_ERR_INVALID_ARG, "fit is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   switch (c->prm.p) {
@@ -731,7 +741,12 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   if (!ensure_hmap(c, 2 * (size_t)(Pn + 2))) return RRQ_ERR_CUDA;
   k_pair_range<<<1, 32, 0, st>>>(pair_ptr, row_begin, row_end, c->hmap);
   c->launches++;
-  cudaStreamSynchronize(st);
+  {   // the mapped pair range is only valid once the kernel ran: check before consuming it
+    rrq_status r0 = cuda_check(c, "k_pair_range");
+    if (r0) return r0;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(c, RRQ_ERR_CUDA, std::string("k_pair_range: ") + cudaGetErrorString(e));
+  }
   const int64_t obase = c->hmap[0], total = c->hmap[1] - c->hmap[0];
   if (total == 0) {
     if (row_ptr) {
@@ -770,7 +785,12 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     k_copy_i64<<<nblk(Pn + 1, 256), 256, 0, st>>>(Pn + 1, bp<int64_t>(c->items), c->hmap + Pn + 1);
     c->launches += 9;
   }
-  cudaStreamSynchronize(st);
+  {
+    rrq_status r0 = cuda_check(c, "build plumbing");
+    if (r0) return r0;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(c, RRQ_ERR_CUDA, std::string("build plumbing: ") + cudaGetErrorString(e));
+  }
   std::memcpy(hseg.data(), c->hmap, (Pn + 1) * sizeof(int64_t));
   std::memcpy(hitem.data(), c->hmap + Pn + 1, (Pn + 1) * sizeof(int64_t));
   hseg[Pn] = total;
@@ -819,14 +839,6 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
       return RRQ_ERR_CUDA;
   if (!ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxitems * CC::ZBLK * 8))
     return RRQ_ERR_CUDA;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_pair_edge<P, kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_qmap<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_translate<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM);
-    cudaFuncSetAttribute(k_contract<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
   // producer stream: a second stream when overlapping, else the caller's
   cudaStream_t sp = st;
   if (nset == 2) {
@@ -920,7 +932,7 @@ rrq_status rrq_build_correction(rrq_ctx c, const rrq_surface *s, const rrq_targe
                                 double *const vals[4], int32_t *pstat, rrq_stream_t stream) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   rrq_status r;
-  if ((r = check_surface(c, s)) || (r = check_targets(c, tg))) return r;
+  if ((r = check_device(c)) || (r = check_surface(c, s)) || (r = check_targets(c, tg))) return r;
   if (!pair_ptr || (!pair_patch && n_pairs > 0) || !fit || !vals)
     return fail(c, RRQ_ERR_INVALID_ARG, "pair_ptr, pair_patch (unless n_pairs == 0), fit, vals must be non-NULL");
   if (row_begin < 0 || row_end < row_begin || row_end > tg->n_targets)
@@ -950,7 +962,7 @@ rrq_status rrq_apply_smooth(rrq_ctx c, int64_t n_targets, const double *tx, cons
                             rrq_stream_t stream) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   rrq_status r;
-  if ((r = check_surface(c, s))) return r;
+  if ((r = check_device(c)) || (r = check_surface(c, s))) return r;
   if (n_targets < 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_targets < 0");
   if (n_targets == 0) return RRQ_OK;
   if (!tx || !density || !y) return fail(c, RRQ_ERR_INVALID_ARG, "NULL array");
@@ -965,6 +977,7 @@ rrq_status rrq_apply_smooth(rrq_ctx c, int64_t n_targets, const double *tx, cons
 rrq_status rrq_apply_correction(rrq_ctx c, int64_t n_rows, const int64_t *row_ptr, const int32_t *col_idx,
                                 const double *vals, const double *density, double *y, rrq_stream_t stream) {
   if (!c) return RRQ_ERR_INVALID_ARG;
+  if (check_device(c)) return RRQ_ERR_INVALID_ARG;
   if (n_rows < 0) return fail(c, RRQ_ERR_INVALID_ARG, "n_rows < 0");
   if (n_rows == 0) return RRQ_OK;
   if (!row_ptr || !col_idx || !vals || !density || !y) return fail(c, RRQ_ERR_INVALID_ARG, "NULL array");
@@ -973,3 +986,26 @@ rrq_status rrq_apply_correction(rrq_ctx c, int64_t n_rows, const int64_t *row_pt
   return cuda_check(c, "rrq_apply_correction");
 }
 
+
+template <int P>
+static cudaError_t set_attrs() {
+  cudaError_t e = cudaSuccess;
+  auto acc = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+  acc(cudaFuncSetAttribute(k_edge_tables<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EdgeTabCfg<P>::SMEM));
+  acc(cudaFuncSetAttribute(k_patch_fit_q<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FitCfg<P>::SMEM));
+  acc(cudaFuncSetAttribute(k_pair_edge<P, kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_qmap<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_translate<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
+  acc(cudaFuncSetAttribute(k_contract<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  return e;
+}
+
+static cudaError_t set_kernel_attributes(int p) {
+  switch (p) {
+    case 4: return set_attrs<4>();
+    case 6: return set_attrs<6>();
+    case 8: return set_attrs<8>();
+    case 10: return set_attrs<10>();
+  }
+  return cudaErrorInvalidValue;
+}

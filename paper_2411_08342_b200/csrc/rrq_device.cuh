@@ -7,6 +7,13 @@
 
 namespace rrq {
 
+// |(a, b, c)| with separately rounded IEEE operations in a fixed order (no FMA contraction): the near-list
+// arithmetic shared in definition (not in code) with the CPU oracle's near balls.
+__device__ __forceinline__ double norm3_rn(double a, double b, double c) {
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, a), __dmul_rn(b, b)), __dmul_rn(c, c)));
+}
+
+
 constexpr double kPi = 3.14159265358979323846264338327950288;
 
 struct cd {

@@ -1,0 +1,108 @@
+"""GPU coverage of the error paths and fallbacks (SURVEY §8(b) conventions): numerical
+trouble never aborts a batch, it is flagged per patch / pair with the deterministic fallback the oracle
+mirrors.
+* a degenerate patch (all nodes on one point): the least-squares fit is rank deficient -> patch_status = 1
+  on both sides (reading A1's rank test);
+* Newton non-convergence at p = 8 (far roots, where the iteration stalls at its rounding floor above the
+  tolerance): pair_status bit 0 and the plain-regime fallback on both sides, rows within the parity bar;
+* a non-finite target: pair_status bit 1 on both sides;
+* side flag absent (side = NULL): the gauge falls back to the geometric rule (reading A8 (iv)); rows of targets
+  close to and on both sides of the patches within the parity bar."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O
+from synth.configs import make_config
+from synth.geometry import Surface, make_flat_surface
+import parity_util as U
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx_build(S, tx, nu, sn, sd, eta=1.0, mask=15):
+    from paper_2411_08342_b200 import RRQ, DeviceSurface, DeviceTargets
+    ctx = RRQ(S.p, eta=eta)
+    ds = DeviceSurface.from_numpy(S)
+    dt = DeviceTargets.from_numpy(tx, nu, sn, sd)
+    ptr, pat = ctx.near_list(ds, dt)
+    fit, fst = ctx.patch_fit(ds)
+    out = ctx.build_correction(ds, dt, ptr, pat, fit, mask=mask)
+    torch.cuda.synchronize()
+    return (ptr.cpu().numpy(), pat.cpu().numpy(), fst.cpu().numpy(), out["status"].cpu().numpy(),
+            [v.cpu().numpy() if v is not None else None for v in out["vals"]])
+
+
+def test_degenerate_patch_flags_rank_deficiency():
+    cfg = make_config(1, n_off=20)
+    S = cfg["surface"]
+    nodes = S.nodes.copy()
+    nodes[7] = nodes[7].mean(0)            # patch 7: every node at the same point
+    Sd = Surface(p=S.p, q=S.q, nodes=nodes, normals=S.normals, weights=S.weights, verts=S.verts,
+                 edge_x=S.edge_x, edge_dx=S.edge_dx, uv=S.uv)
+    _, _, fst, _, _ = _ctx_build(Sd, cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
+    _, ost = O.patch_fit(Sd)
+    assert fst[7] == 1 and ost[7] == 1
+    assert np.array_equal(fst, ost)
+    assert fst.sum() == 1
+
+
+def _flat_patch(p):
+    tri = np.array([[0.0, 0.0, 0.0], [1.0, 0.125, 0.0], [0.25, 0.875, 0.0]])
+    return tri, make_flat_surface([tri], p, 2 * p)
+
+
+def test_newton_nonconvergence_falls_back_to_plain_rule():
+    """p = 8 on a coarse sphere (80 patches) with a wide near ball (eta = 1.5): a third of the pairs have an edge
+    whose root t0 lies far outside [-1, 1] (|t0| ~ 10-20), where Newton stalls at its rounding floor above the
+    1e-15 (1 + |t|) tolerance (reading A12): pair_status bit 0 and the plain rule (the far root selects it
+    anyway).  The GPU flags the same pairs as the fp64 oracle (knife-edge stalls excepted) and the rows of flagged
+    and unflagged pairs pass the parity bar."""
+    cfg = make_config(2, n_off=400, freq=2)
+    S = cfg["surface"]
+    tgs = (cfg["tx"], cfg["tnormal"], cfg["self_node"], cfg["side"])
+    ptr, pat, _, gst, gv = _ctx_build(S, *tgs, eta=1.5)
+    tg, pa = O.pairs_from_ptr(ptr, pat)
+    rng = np.random.default_rng(1)
+    sel = np.sort(rng.choice(tg.size, 1500, replace=False))
+    ref = U.reference(S, tgs, tg[sel], pa[sel])
+    g1, o1 = gst[sel] & 1, ref["st_o"] & 1
+    print(f"flagged: GPU {int(g1.sum())}, oracle {int(o1.sum())} of {sel.size}; disagree {int((g1 != o1).sum())}")
+    assert o1.sum() > 100 and np.mean(g1 != o1) < 5e-3
+    inv = np.unique(tg[sel], return_inverse=True)[1]
+    U.gate_all([gv[k].reshape(-1, S.n)[sel] for k in range(4)], ref, inv, tag="newton-fallback")
+
+
+def test_nonfinite_target_flagged():
+    tri, S = _flat_patch(4)
+    tx = np.array([[0.4, 0.3, 0.1], [0.4, np.nan, 0.1]])
+    nu = np.tile([0.0, 0.0, 1.0], (2, 1))
+    sn = np.full(2, -1, np.int64)
+    sd = np.ones(2, np.int8)
+    from paper_2411_08342_b200 import RRQ, DeviceSurface, DeviceTargets
+    ctx = RRQ(S.p, eta=1.0)
+    ds = DeviceSurface.from_numpy(S)
+    dt = DeviceTargets.from_numpy(tx, nu, sn, sd)
+    fit, _ = ctx.patch_fit(ds)
+    ptr = torch.tensor([0, 1, 2], dtype=torch.int64, device="cuda")     # force both pairs (NaN is near nothing)
+    pat = torch.zeros(2, dtype=torch.int32, device="cuda")
+    out = ctx.build_correction(ds, dt, ptr, pat, fit)
+    gst = out["status"].cpu().numpy()
+    _, ost = O.build_rows(S, tx, nu, sn, sd, np.arange(2, dtype=np.int64), np.zeros(2, np.int32))
+    assert gst[0] & 2 == 0 and gst[1] & 2, gst
+    assert (ost[1] & 2) and not (ost[0] & 2)
+
+
+def test_side_flag_absent_uses_the_geometric_gauge():
+    cfg = make_config(2, n_off=400, freq=2)
+    S = cfg["surface"]
+    keep = np.concatenate([np.arange(0, S.n_patches * S.n, 7), np.arange(S.n_patches * S.n, cfg["tx"].shape[0])])
+    tx, nu, sn = cfg["tx"][keep], cfg["tnormal"][keep], cfg["self_node"][keep]
+    ptr, pat, _, gst, gv = _ctx_build(S, tx, nu, sn, None, eta=1.5)
+    tg, pa = O.pairs_from_ptr(ptr, pat)
+    rng = np.random.default_rng(0)
+    sel = np.sort(rng.choice(tg.size, min(1500, tg.size), replace=False))
+    ref = U.reference(S, (tx, nu, sn, None), tg[sel], pa[sel])
+    inv = np.unique(tg[sel], return_inverse=True)[1]
+    U.gate_all([gv[k].reshape(-1, S.n)[sel] for k in range(4)], ref, inv, tag="side=NULL")
