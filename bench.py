@@ -307,7 +307,7 @@ def run_ours(args, ws, rank):
     total_weights = sum_over_ranks(weights_per_step * args.steps, ws)
     value = total_weights / (ms_max / 1e3)
     from paper_2411_08342_b200.flops import pair_flops, pair_bytes
-    pf = pair_flops(R.S.p)
+    pf = pair_flops(R.S.p, mask=R.mask)
     pairs_t = max(tim["pairs"], 1)
     swap_per_pair = tim["swap_edges"] / pairs_t
     kflops = {"pair_edge": (pf["edge"] + swap_per_pair * pf["swap_edge"]) * pairs_t,

@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(WPB * 32)
                 const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Arow,
                 double *__restrict__ Xrow, int32_t *__restrict__ pstat, int64_t obase,
                 unsigned long long *__restrict__ swapcnt, const double *__restrict__ trtab,
-                const PairSetup *__restrict__ setup) {
+                const PairSetup *__restrict__ setup, int want_dp) {
   using D = Dims<P>;
   const double *wS = trtab + TrCfg<P>::WS;
   using L = Layout<P>;
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(WPB * 32)
         cross3(tau, d, txd);
         for (int a = 0; a < 3; ++a) {
           Ar[QC::aoff(arow_, a * E + kap)] = w1 * d[a];                                 // row a (k = axis E + kappa)
-          Ar[QC::aoff(QC::TP + arow_, a * E + kap)] = w1 * nup[a] - w3 * nd * d[a];     // row b
+          if (want_dp) Ar[QC::aoff(QC::TP + arow_, a * E + kap)] = w1 * nup[a] - w3 * nd * d[a];   // row b (D')
           om[1 + a] -= w1 * tau[a];
           om[5 + a] += w3 * nd * tau[a];
         }
@@ -750,8 +750,8 @@ __global__ void __launch_bounds__(WPB * 32)
       const int l = tri_inv(c) + 1;   // lmidx(l, 1) <= c < lmidx(l + 1, 1)
       const int m = c - lmidx(l, 1) + 1, hs = sidx(l, m);
       const cd *g = wsc.GS[pp][hs];
-      cd hn[3];
-      hess_fast(wsc.GS[pp], l, m, nup, shc, hn);
+      cd hn[3] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
+      if (want_dp) hess_fast(wsc.GS[pp], l, m, nup, shc, hn);
       double gs = 0, dgs = 0, gv[3], dgv[3];
       for (int a = 0; a < 3; ++a) {
         gs -= Ov[a] * g[a].y;
@@ -763,10 +763,10 @@ __global__ void __launch_bounds__(WPB * 32)
       }
       const double f = -s2 * inv4pi;
       X[XR::W + c] = f * gs;
-      X[XR::DW + c] = f * dgs;
+      if (want_dp) X[XR::DW + c] = f * dgs;
       for (int a = 0; a < 3; ++a) {
         X[XR::W + (1 + a) * NP + c] = f * gv[a];
-        X[XR::DW + (1 + a) * NP + c] = f * dgv[a];
+        if (want_dp) X[XR::DW + (1 + a) * NP + c] = f * dgv[a];
       }
       X[XR::TH + c] = s2 * inv4pi * ps.R[hs].y * O0;
     }
@@ -799,7 +799,7 @@ __global__ void __launch_bounds__(WPB * 32)
 // One KC-row chunk of the k_qmap GEMM for a warp of column split NS; ZC = the quaternion component whose M
 // block is zero in this chunk's axis (compile time, so the skipped tiles cost nothing).  Tiles: component
 // c, u-th of the warp: column tile c TQC + NS + NSPLIT u; V: NTQ + vstart(NS) + u.
-template <int P, int ZC, int NS>
+template <int P, int ZC, int NS, bool DP>
 __device__ __forceinline__ void qmap_chunk(const double *arow, const double *brow, int sw, const double *bb,
                                            double (&accA)[4][QmapCfg<P>::UQ][2], double (&accB)[4][QmapCfg<P>::UQ][2],
                                            double (&accV)[QmapCfg<P>::UV][2]) {
@@ -807,7 +807,7 @@ __device__ __forceinline__ void qmap_chunk(const double *arow, const double *bro
   constexpr int NCS = Dims<P>::NCS, NQT = C::nq(NS), NVT = C::vcount(NS), V0 = C::vstart(NS);
 #pragma unroll
   for (int kk = 0; kk < C::KC; kk += 4) {
-    const double a = arow[kk ^ sw], b = brow[kk ^ sw];
+    const double a = arow[kk ^ sw], b = DP ? brow[kk ^ sw] : 0.0;
     const double *bk = bb + kk * NCS;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -816,7 +816,7 @@ __device__ __forceinline__ void qmap_chunk(const double *arow, const double *bro
       for (int u = 0; u < NQT; ++u) {
         const double bq = bk[(c * C::TQC + NS + u * C::NSPLIT) * 8];
         dmma(accA[c][u][0], accA[c][u][1], a, bq);
-        dmma(accB[c][u][0], accB[c][u][1], b, bq);
+        if constexpr (DP) dmma(accB[c][u][0], accB[c][u][1], b, bq);   // dQ rows only when D' is built
       }
     }
 #pragma unroll
@@ -859,7 +859,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
       : "memory");
 }
 
-template <int P>
+// DP = false (kernel mask without D'): the b rows (dQ) are neither copied, multiplied nor stored.
+template <int P, bool DP>
 __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     k_qmap(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, const int32_t *__restrict__ item_patch,
            const int64_t *__restrict__ seg_ptr, int64_t sA, const double *__restrict__ fit,
@@ -880,7 +881,8 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
   // pipeline: bar[b] = "stage b landed" (bulk-copy transactions), emp[b] = "all warps done with stage b" (one
   // arrival per warp); no CTA-wide barrier inside the K loop
   __shared__ uint64_t bar[C::NST], emp[C::NST];
-  constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ACHB = (unsigned)(C::ACH * sizeof(double));
+  // a chunk's a rows (0..TP-1) come first: without D' only that half is copied
+  constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ACHB = (unsigned)(C::ACH * sizeof(double)) / (DP ? 1 : 2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NST; ++i) {
@@ -920,7 +922,7 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     const double *stg = sst + (ch % C::NST) * C::STG;
     const double *arow = stg + aofs, *brow = arow + TP * KC, *bb = stg + bofs;
     const int zc = 1 + ch / C::CPA;   // axis of this chunk: component axis + 1 has a zero block
-#define RRQ_QCHUNK(Z, N) qmap_chunk<P, Z, N>(arow, brow, sw, bb, accA, accB, accV)
+#define RRQ_QCHUNK(Z, N) qmap_chunk<P, Z, N, DP>(arow, brow, sw, bb, accA, accB, accV)
 #define RRQ_QNS(N) (zc == 1 ? RRQ_QCHUNK(1, N) : zc == 2 ? RRQ_QCHUNK(2, N) : RRQ_QCHUNK(3, N))
     switch (ns) {
       case 0: RRQ_QNS(0); break;
@@ -949,7 +951,7 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         o[c] = make_double2(accA[c][u][0], accA[c][u][1]);
-        o[4 + c] = make_double2(accB[c][u][0], accB[c][u][1]);
+        if constexpr (DP) o[4 + c] = make_double2(accB[c][u][0], accB[c][u][1]);
       }
     }
     const int v0 = ns == 0 ? C::vstart(0) : ns == 1 ? C::vstart(1) : ns == 2 ? C::vstart(2) : C::vstart(3);
@@ -1020,10 +1022,12 @@ __device__ __forceinline__ double flip_if(double x, uint32_t bit) {
   return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)bit << 63));
 }
 
-template <int P>
+// DP = false (kernel mask without D'): no dQ staging, no dlambda accumulation, no zeta(dW); mask: Theta is
+// written only with S, zeta_S only with S'.
+template <int P, bool DP>
 __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     k_translate(int64_t sA, int64_t sB, const double *__restrict__ Xrow, const double *__restrict__ Qrow,
-                const double *__restrict__ trtab, double *__restrict__ Zrow) {
+                const double *__restrict__ trtab, double *__restrict__ Zrow, uint32_t mask) {
   using D = Dims<P>;
   using C = TrCfg<P>;
   using XR = XRow<P>;
@@ -1052,12 +1056,14 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
   // Q row (entry e -> position posq[e] at stride EQ; V of (j >= 2, k) next to it) and the S'/NG' block
   // (entry e -> position poss[e] at stride SXW): positions chosen by the host to spread the main loop's
   // shared-memory banks.  Destinations of this lane's 16-B chunks, fixed for every pair (registers).
-  constexpr int NCQ_ = 8 * D::NQ, NLQ = (NCQ_ + 31) / 32, NLV = (D::NV + 31) / 32, NLS = (2 * P * P + 31) / 32;
+  // 16-B chunks per Q entry staged: Q | dQ (8), or Q only (4) without D'
+  constexpr int CPE = DP ? 8 : 4, LCPE = DP ? 3 : 2;
+  constexpr int NCQ_ = CPE * D::NQ, NLQ = (NCQ_ + 31) / 32, NLV = (D::NV + 31) / 32, NLS = (2 * P * P + 31) / 32;
   int dq[NLQ], dv[NLV], ds[NLS];
 #pragma unroll
   for (int u = 0; u < NLQ; ++u) {
     const int i = lane + 32 * u;
-    dq[u] = i < NCQ_ ? EQ * posq[i >> 3] + 2 * (i & 7) : 0;
+    dq[u] = i < NCQ_ ? EQ * posq[i >> LCPE] + 2 * (i & (CPE - 1)) : 0;
   }
 #pragma unroll
   for (int u = 0; u < NLV; ++u) {
@@ -1073,8 +1079,10 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     const double *qg = Qrow + (s - sA) * QR::STRIDE, *xg = Xrow + (s - sA) * XR::STRIDE + XR::SX;
     double *qd = wb + b * C::BUF;
 #pragma unroll
-    for (int u = 0; u < NLQ; ++u)
-      if (lane + 32 * u < NCQ_) cp_async16(qd + dq[u], qg + 2 * (lane + 32 * u));
+    for (int u = 0; u < NLQ; ++u) {
+      const int i = lane + 32 * u;
+      if (i < NCQ_) cp_async16(qd + dq[u], qg + 2 * (DP ? i : ((i >> 2) << 3 | (i & 3))));
+    }
 #pragma unroll
     for (int u = 0; u < NLV; ++u)
       if (lane + 32 * u < D::NV) cp_async16(qd + dv[u], qg + QR::V + 2 * (lane + 32 * u));
@@ -1138,7 +1146,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         q[b] = *reinterpret_cast<const double2 *>(e + 2 * b);
-        dq[b] = *reinterpret_cast<const double2 *>(e + 8 + 2 * b);
+        dq[b] = DP ? *reinterpret_cast<const double2 *>(e + 8 + 2 * b) : make_double2(0.0, 0.0);
       }
       double2 v = *reinterpret_cast<const double2 *>(qb + C::SV + 2 * (qe + 2));
       // k < 0: A^{(j,-k)} = (-1)^k conj A^{(j,k)}, so Im(A S) = A.x S.y + A.y S.x takes -A.x (odd k, FA) or
@@ -1161,7 +1169,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           lam[i][b] = fma(q[b].x, A, fma(q[b].y, B, lam[i][b]));
-          dl[i][b] = fma(dq[b].x, A, fma(dq[b].y, B, fma(q[b].x, An, fma(q[b].y, Bn, dl[i][b]))));
+          if constexpr (DP) dl[i][b] = fma(dq[b].x, A, fma(dq[b].y, B, fma(q[b].x, An, fma(q[b].y, Bn, dl[i][b]))));
         }
       }
     }
@@ -1227,17 +1235,21 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
       // zeta vectors (Step 8, App. A.7; reading G3 for S')
       double nxW[3];
       cross3(nup, W + 1, nxW);
-      Zt[CC::zoff(0, zr, c)] = Th;
+      if (mask & 1) Zt[CC::zoff(0, zr, c)] = Th;
       Zt[CC::zoff(1, zr, c)] = W[0];
       Zt[CC::zoff(2, zr, c)] = -W[1];
       Zt[CC::zoff(3, zr, c)] = -W[2];
       Zt[CC::zoff(4, zr, c)] = -W[3];
-      Zt[CC::zoff(5, zr, c)] = dW[0];
-      Zt[CC::zoff(6, zr, c)] = -dW[1];
-      Zt[CC::zoff(7, zr, c)] = -dW[2];
-      Zt[CC::zoff(8, zr, c)] = -dW[3];
-      Zt[CC::zoff(9, zr, c)] = -dot3(nup, W + 1);
-      for (int a = 0; a < 3; ++a) Zt[CC::zoff(10 + a, zr, c)] = -W[0] * nup[a] - nxW[a];
+      if constexpr (DP) {
+        Zt[CC::zoff(5, zr, c)] = dW[0];
+        Zt[CC::zoff(6, zr, c)] = -dW[1];
+        Zt[CC::zoff(7, zr, c)] = -dW[2];
+        Zt[CC::zoff(8, zr, c)] = -dW[3];
+      }
+      if (mask & 4) {
+        Zt[CC::zoff(9, zr, c)] = -dot3(nup, W + 1);
+        for (int a = 0; a < 3; ++a) Zt[CC::zoff(10 + a, zr, c)] = -W[0] * nup[a] - nxW[a];
+      }
     }
     __syncwarp();
     zero_entries(cb);   // the slots overwrote them
@@ -1298,23 +1310,27 @@ __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
   }
   __syncthreads();
   // the fit operators are stored with the padded row stride NB, so a chunk of each is one contiguous copy
+  // kernel mask: an operand is staged / multiplied only if a selected kernel needs it (P_D: D, D'; P_Sp: S';
+  // P_Sg, P_Sd: S); a masked-off kernel's zeta blocks were not written by k_translate
+  const bool wS = mask & 1, wD = mask & 2, wSp = mask & 4, wDp = mask & 8;
+  const unsigned nops = (unsigned)((wD || wDp) + wSp + wS);
   auto issue = [&](int ch, unsigned extra) {
     uint64_t *br = &bar[ch & 1];
     if (threadIdx.x == 0) {
-      mbar_expect_tx(br, 3u * KC * ROWB + ZCB + extra);
+      mbar_expect_tx(br, nops * KC * ROWB + ZCB + extra);
       double *dst = sB + (ch & 1) * CC::STG;
-      bulk_g2s(dst, PD + (int64_t)ch * KC * NB, KC * ROWB, br);
-      bulk_g2s(dst + KC * NB, PSp + (int64_t)ch * KC * NB, KC * ROWB, br);
-      bulk_g2s(dst + 2 * KC * NB, PSg + (int64_t)ch * KC * NB, KC * ROWB, br);
+      if (wD || wDp) bulk_g2s(dst, PD + (int64_t)ch * KC * NB, KC * ROWB, br);
+      if (wSp) bulk_g2s(dst + KC * NB, PSp + (int64_t)ch * KC * NB, KC * ROWB, br);
+      if (wS) bulk_g2s(dst + 2 * KC * NB, PSg + (int64_t)ch * KC * NB, KC * ROWB, br);
       bulk_g2s(dst + CC::SMEM_B, Zblk + CC::ZT + (int64_t)ch * CC::ZCH, ZCB, br);
     }
   };
   {
-    const unsigned zb = (unsigned)(CC::ZT * sizeof(double)), nb3 = (unsigned)(3 * N * sizeof(double)),
+    const unsigned zb = wS ? (unsigned)(CC::ZT * sizeof(double)) : 0u, nb3 = (unsigned)(3 * N * sizeof(double)),
                    nb1 = (unsigned)(N * sizeof(double)), cb = (unsigned)(cnt * sizeof(ContractPair));
     issue(0, zb + 2 * nb3 + nb1 + cb);
     if (threadIdx.x == 32) {
-      bulk_g2s(sz, Zblk, zb, &bar[0]);
+      if (wS) bulk_g2s(sz, Zblk, zb, &bar[0]);
       bulk_g2s(sN, nodes + Pp * N * 3, nb3, &bar[0]);
       bulk_g2s(sN + 3 * N, normals + Pp * N * 3, nb3, &bar[0]);
       bulk_g2s(sN + 6 * N, weights + Pp * N, nb1, &bar[0]);
@@ -1330,7 +1346,7 @@ __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
 #pragma unroll
     for (int q = 0; q < NK; ++q) {
       const int kk = 4 * q + (lane & 3);
-      bq[tw][q] = (tile < CC::TILES && bn < N && kk < NP) ? __ldg(PSd + kk * NB + bn) : 0.0;
+      bq[tw][q] = (wS && tile < CC::TILES && bn < N && kk < NP) ? __ldg(PSd + kk * NB + bn) : 0.0;
     }
   }
   const double h = blk[L::HDR + H_H];
@@ -1344,7 +1360,7 @@ __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
 #pragma unroll
   for (int tw = 0; tw < CC::TPW; ++tw) {
     const int tile = warp + tw * CC::WARPS;
-    if (tile >= CC::TILES) continue;
+    if (tile >= CC::TILES || !wS) continue;
     const double *zr = sz + ((tile % CC::MT) * 8 + (lane >> 2)) * ZTS + (lane & 3);
 #pragma unroll
     for (int q = 0; q < NK; ++q) {
@@ -1378,10 +1394,10 @@ __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
         const bool bok = bn < N;
         const int br = (kk + (lane & 3)) * NB + bn;
         const double bd = bok ? bb[br] : 0.0, bsp = bok ? bb[KC * NB + br] : 0.0, bsg = bok ? bb[2 * KC * NB + br] : 0.0;
-        dmma(acc[tw][2], acc[tw][3], zw, bd);
-        dmma(acc[tw][6], acc[tw][7], zdw, bd);
-        dmma(acc[tw][4], acc[tw][5], zs, bsp);
-        dmma(acc[tw][0], acc[tw][1], zw, bsg);
+        if (wD) dmma(acc[tw][2], acc[tw][3], zw, bd);
+        if (wDp) dmma(acc[tw][6], acc[tw][7], zdw, bd);
+        if (wSp) dmma(acc[tw][4], acc[tw][5], zs, bsp);
+        if (wS) dmma(acc[tw][0], acc[tw][1], zw, bsg);
       }
     }
     __syncwarp();
@@ -1421,11 +1437,11 @@ __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
         Sp += inv4pi * dnp * ir3 * wi;
         Dp -= inv4pi * (nn * ir3 - 3.0 * dn * dnp * ir3 * ir * ir) * wi;
       }
-      oS[q] = (mask & 1) ? S : 0.0;
-      oD[q] = (mask & 2) ? Dv : 0.0;
-      oSp[q] = (mask & 4) ? Sp : 0.0;
-      oDp[q] = (mask & 8) ? Dp : 0.0;
-      if (i < N) bad |= !isfinite(S) || !isfinite(Dv) || !isfinite(Sp) || !isfinite(Dp);
+      oS[q] = wS ? S : 0.0;
+      oD[q] = wD ? Dv : 0.0;
+      oSp[q] = wSp ? Sp : 0.0;
+      oDp[q] = wDp ? Dp : 0.0;
+      if (i < N) bad |= !isfinite(oS[q]) || !isfinite(oD[q]) || !isfinite(oSp[q]) || !isfinite(oDp[q]);
     }
     const int64_t o = (sC[row].k - obase) * N + i0;
     if (i0 + 1 < N) {   // the usual case: both columns, 16-B stores

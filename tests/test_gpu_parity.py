@@ -170,6 +170,15 @@ def test_row_chunks_and_masks():
     assert torch.equal(sd["vals"][0], full["vals"][0]) and torch.equal(sd["vals"][1], full["vals"][1])
     with pytest.raises(RRQError):
         ctx.build_correction(ds, dtn, ptr, pat, fit, mask=15)
+    # every kernel mask: the selected kernels' values are bit-identical to the full build's (the skipped work --
+    # dQ rows and the dW translation without D', Theta without S, zeta_S without S' -- never feeds another kernel)
+    for m in (1, 2, 4, 8, 5, 10, 12, 14):
+        part = ctx.build_correction(ds, dt, ptr, pat, fit, mask=m)
+        for k in range(4):
+            if (m >> k) & 1:
+                assert torch.equal(part["vals"][k], full["vals"][k]), (m, k)
+            else:
+                assert part["vals"][k] is None
     # empty target set
     e = DeviceTargets(dt.x[:0], dt.normal[:0], dt.self_node[:0], dt.side[:0])
     p0, q0 = ctx.near_list(ds, e)
