@@ -8,7 +8,7 @@ shift
 KS=${@:-k_pair_edge k_qmap k_translate k_contract}
 for K in $KS; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K --launch-skip 12 --launch-count 1 \
-    -o gpurun_out/ncu_${TAG}_$K -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline \
+    -o gpurun_out/ncu_${TAG}_$K -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
     > gpurun_out/ncu_${TAG}_$K.log 2>&1
   echo "$K rc=$?" >> gpurun_out/ncu_${TAG}.status
 done
