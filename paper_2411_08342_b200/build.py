@@ -34,6 +34,21 @@ def build(force=False, verbose=False):
     return LIB
 
 
+def build_variant(name, defines):
+    """Experiment hook: the same sources with extra -D flags into variants/librrq_<name>.so (load it with
+    RRQ_LIBRARY=<path>); the product library is untouched."""
+    out_dir = os.path.join(ROOT, "variants")
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, f"librrq_{name}.so")
+    tab_o = os.path.join(CSRC, "rrq_tables.o")
+    if not os.path.exists(tab_o):
+        subprocess.check_call(["g++", "-O2", "-fPIC", "-c", os.path.join(CSRC, "rrq_tables.cpp"), "-o", tab_o])
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-O3",
+           *[f"-D{d}" for d in defines], os.path.join(CSRC, "rrq_api.cu"), tab_o, "-o", out, "-lquadmath"]
+    subprocess.check_call(cmd)
+    return out
+
+
 if __name__ == "__main__":
     build(force=True, verbose="-v" in sys.argv)
     print(LIB)

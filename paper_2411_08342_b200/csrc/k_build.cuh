@@ -240,24 +240,29 @@ struct QmapCfg {
   static constexpr int TQC = D::CQP / 8;                      // tiles per quaternion component
   static constexpr int NTQ = D::NCQ / 8, NTALL = D::NCP / 8, NTV = NTALL - NTQ;
   static constexpr int UQ = (TQC + NSPLIT - 1) / NSPLIT;       // a warp's tiles per component (at most)
-  // Work balance.  Column split ns takes the Q tiles tl = ns + NSPLIT u < TQC (2 DMMA each: a and b rows)
-  // and a contiguous range of V tiles (1 DMMA each), sized so that the two SM sub-partitions' loads match:
-  // warp w = ns PG + pg runs on sub-partition w % 4, so splits {0, 2} share one pair of sub-partitions and
-  // {1, 3} the other.  Counts are compile-time per split (no predicated-off DMMA).
+  // Two column passes (the accumulators of all 440 columns of a 32-row tile do not fit the register budget
+  // with room to prefetch B fragments): pass 0 = components scalar, x; pass 1 = components y, z + the V tiles.
+  // Column split ns takes the Q tiles tl = ns + NSPLIT u < TQC of its pass's two components (2 DMMA each: a
+  // and b rows) and, in pass 1, a contiguous range of V tiles (1 DMMA each) sized so that the SM
+  // sub-partitions' loads match: warp w = ns PG + pg runs on sub-partition w % 4, so splits {0, 2} share one
+  // pair of sub-partitions and {1, 3} the other.  Counts are compile-time per split (no predicated DMMA).
   __host__ __device__ static constexpr int nq(int ns) { return (TQC - ns + NSPLIT - 1) / NSPLIT; }
-  static constexpr int VA0 = (NTV + 6 * (nq(1) + nq(3)) - 6 * (nq(0) + nq(2)) + 1) / 2;
+  static constexpr int VA0 = (NTV + 4 * (nq(1) + nq(3)) - 4 * (nq(0) + nq(2)) + 1) / 2;
   static constexpr int VA = VA0 < 0 ? 0 : (VA0 > NTV ? NTV : VA0), VB = NTV - VA;
   __host__ __device__ static constexpr int vcount(int ns) { return ns == 0 ? (VA + 1) / 2 : ns == 2 ? VA / 2 : ns == 1 ? (VB + 1) / 2 : VB / 2; }
   __host__ __device__ static constexpr int vstart(int ns) { return ns == 0 ? 0 : ns == 1 ? vcount(0) : ns == 2 ? vcount(0) + vcount(1) : vcount(0) + vcount(1) + vcount(2); }
   static constexpr int UV = vcount(0) > vcount(1) ? (vcount(0) > vcount(2) ? (vcount(0) > vcount(3) ? vcount(0) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)))
                                                   : (vcount(1) > vcount(2) ? (vcount(1) > vcount(3) ? vcount(1) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)));
   static constexpr int KC = (D::E % 8 == 0) ? 8 : 12, NCH = D::K / KC, CPA = D::E / KC;   // chunks per axis
-  static constexpr int NST = 3;                                    // pipeline stages (chunks in flight)
+#ifndef RRQ_QMAP_NST
+#define RRQ_QMAP_NST 4
+#endif
+  static constexpr int NST = RRQ_QMAP_NST;                         // pipeline stages (chunks in flight)
   // A (the tile's 32 GEMM rows) is stored tile-chunked by k_pair_edge: chunk ch = [32 rows][KC] (ACH doubles,
   // rows 0..15 = a-rows of the tile's pairs, 16..31 = b-rows), so a stage = [A chunk | B chunk] is two bulk
   // copies and A needs no resident shared memory.  KC = 8: the halves of rows with (r >> 1) odd are swapped
-  // (k ^ 4) so a quarter-warp's A fragments fall in distinct banks.
-  static constexpr int ACH = ROWS * KC, ABLK = NCH * ACH, STG = ACH + KC * D::NCS;
+  // (k ^ 4) so a quarter-warp's A fragments fall in distinct banks.  A stage holds the larger pass's B chunk.
+  static constexpr int ACH = ROWS * KC, ABLK = NCH * ACH, STG = ACH + KC * D::NCSH1;
   static_assert(D::E % KC == 0, "a B chunk must lie within one axis block");
   static_assert(NSPLIT == 4 && PG == 2, "sub-partition balance assumes 4 column splits x 2 pair groups");
   static constexpr int MINB = P <= 8 ? 2 : 1;                 // CTAs per SM (register budget)
@@ -796,31 +801,40 @@ __global__ void __launch_bounds__(WPB * 32)
 // The epilogue scales by v_lambda / v_theta (TrCfg) and stores the QRow layout for k_translate.
 // ------------------------------------------------------------------------------------------------
 
-// One KC-row chunk of the k_qmap GEMM for a warp of column split NS; ZC = the quaternion component whose M
-// block is zero in this chunk's axis (compile time, so the skipped tiles cost nothing).  Tiles: component
-// c, u-th of the warp: column tile c TQC + NS + NSPLIT u; V: NTQ + vstart(NS) + u.
-template <int P, int ZC, int NS, bool DP>
+// One KC-row chunk of column pass H of the k_qmap GEMM for a warp of column split NS; ZC = the quaternion
+// component whose M block is zero in this chunk's axis, -1 if none of the pass's (compile time, so the
+// skipped tiles cost nothing).
+// Tiles: local component cl (component 2H + cl), u-th of the warp: column tile cl TQC + NS + NSPLIT u of the
+// pass's block; V (pass 1): 2 TQC + vstart(NS) + u.  The B fragments of a k-step are loaded before its DMMAs.
+template <int P, int ZC, int NS, bool DP, int H>
 __device__ __forceinline__ void qmap_chunk(const double *arow, const double *brow, int sw, const double *bb,
-                                           double (&accA)[4][QmapCfg<P>::UQ][2], double (&accB)[4][QmapCfg<P>::UQ][2],
+                                           double (&accA)[2][QmapCfg<P>::UQ][2], double (&accB)[2][QmapCfg<P>::UQ][2],
                                            double (&accV)[QmapCfg<P>::UV][2]) {
   using C = QmapCfg<P>;
-  constexpr int NCS = Dims<P>::NCS, NQT = C::nq(NS), NVT = C::vcount(NS), V0 = C::vstart(NS);
+  constexpr int NCSH = H ? Dims<P>::NCSH1 : Dims<P>::NCSH0, NQT = C::nq(NS), NVT = H ? C::vcount(NS) : 0,
+                V0 = C::vstart(NS);
 #pragma unroll
   for (int kk = 0; kk < C::KC; kk += 4) {
     const double a = arow[kk ^ sw], b = DP ? brow[kk ^ sw] : 0.0;
-    const double *bk = bb + kk * NCS;
+    const double *bk = bb + kk * NCSH;
+    double bq[2][C::UQ], bv[C::UV > 0 ? C::UV : 1];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (c == ZC) continue;
+    for (int cl = 0; cl < 2; ++cl)
+#pragma unroll
+      for (int u = 0; u < NQT; ++u) bq[cl][u] = (2 * H + cl == ZC) ? 0.0 : bk[(cl * C::TQC + NS + u * C::NSPLIT) * 8];
+#pragma unroll
+    for (int u = 0; u < NVT; ++u) bv[u] = bk[(2 * C::TQC + V0 + u) * 8];
+#pragma unroll
+    for (int cl = 0; cl < 2; ++cl) {
+      if (2 * H + cl == ZC) continue;
 #pragma unroll
       for (int u = 0; u < NQT; ++u) {
-        const double bq = bk[(c * C::TQC + NS + u * C::NSPLIT) * 8];
-        dmma(accA[c][u][0], accA[c][u][1], a, bq);
-        if constexpr (DP) dmma(accB[c][u][0], accB[c][u][1], b, bq);   // dQ rows only when D' is built
+        dmma(accA[cl][u][0], accA[cl][u][1], a, bq[cl][u]);
+        if constexpr (DP) dmma(accB[cl][u][0], accB[cl][u][1], b, bq[cl][u]);   // dQ rows only when D' is built
       }
     }
 #pragma unroll
-    for (int u = 0; u < NVT; ++u) dmma(accV[u][0], accV[u][1], a, bk[(C::NTQ + V0 + u) * 8]);
+    for (int u = 0; u < NVT; ++u) dmma(accV[u][0], accV[u][1], a, bv[u]);
   }
 }
 
@@ -869,20 +883,22 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
   using L = Layout<P>;
   using C = QmapCfg<P>;
   using QR = QRow<P>;
-  constexpr int TP = C::TP, NCS = D::NCS, KC = C::KC;
+  constexpr int TP = C::TP, KC = C::KC, NCH = C::NCH;
   extern __shared__ __align__(16) double sst[];   // [NST][A chunk | B chunk]
   const int64_t item = item0 + blockIdx.x;
   if (item >= item1) return;
   const int64_t Pp = item_patch[item];
   const int64_t s0 = seg_ptr[Pp] + (item - item_ptr[Pp]) * TP;
   const int cnt = (int)min((int64_t)TP, seg_ptr[Pp + 1] - s0);
-  const double *M = fit + Pp * (int64_t)L::STRIDE + L::MQ;
+  const double *M0 = fit + Pp * (int64_t)L::STRIDE + L::MQ, *M1 = fit + Pp * (int64_t)L::STRIDE + L::MQ1;
   const double *Ablk = Arow + (item - item0) * (int64_t)C::ABLK;   // rows of absent pairs: never read back
-  // pipeline: bar[b] = "stage b landed" (bulk-copy transactions), emp[b] = "all warps done with stage b" (one
-  // arrival per warp); no CTA-wide barrier inside the K loop
+  // pipeline over 2 NCH virtual chunks (pass h = vc / NCH, K chunk vc % NCH): bar[b] = "stage b landed"
+  // (bulk-copy transactions), emp[b] = "all warps done with stage b" (one arrival per warp); no CTA-wide
+  // barrier inside the K loop, and the pass-1 chunks stream in during the pass-0 epilogue
   __shared__ uint64_t bar[C::NST], emp[C::NST];
   // a chunk's a rows (0..TP-1) come first: without D' only that half is copied
-  constexpr unsigned CHB = (unsigned)(KC * NCS * sizeof(double)), ACHB = (unsigned)(C::ACH * sizeof(double)) / (DP ? 1 : 2);
+  constexpr unsigned ACHB = (unsigned)(C::ACH * sizeof(double)) / (DP ? 1 : 2);
+  constexpr unsigned CHB0 = (unsigned)(KC * D::NCSH0 * sizeof(double)), CHB1 = (unsigned)(KC * D::NCSH1 * sizeof(double));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::NST; ++i) {
@@ -892,75 +908,84 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
     mbar_fence_init();
   }
   __syncthreads();
-  auto issue = [&](int ch) {   // thread 0
-    const int b = ch % C::NST;
+  auto issue = [&](int vc) {   // thread 0
+    const int b = vc % C::NST, h = vc / NCH, ch = vc % NCH;
     double *st = sst + b * C::STG;
-    mbar_expect_tx(&bar[b], ACHB + CHB);
+    mbar_expect_tx(&bar[b], ACHB + (h ? CHB1 : CHB0));
     bulk_g2s(st, Ablk + (int64_t)ch * C::ACH, ACHB, &bar[b]);
-    bulk_g2s(st + C::ACH, M + (int64_t)ch * KC * NCS, CHB, &bar[b]);
+    if (h) bulk_g2s(st + C::ACH, M1 + (int64_t)ch * KC * D::NCSH1, CHB1, &bar[b]);
+    else bulk_g2s(st + C::ACH, M0 + (int64_t)ch * KC * D::NCSH0, CHB0, &bar[b]);
   };
   if (threadIdx.x == 0)   // chunks 0 .. NST-2 in flight from the start
-    for (int ch = 0; ch < C::NST - 1 && ch < C::NCH; ++ch) issue(ch);
+    for (int vc = 0; vc < C::NST - 1; ++vc) issue(vc);
   const int ns = warp / C::PG, pg = warp % C::PG;
-  double accA[4][C::UQ][2], accB[4][C::UQ][2], accV[C::UV][2];
-#pragma unroll
-  for (int c = 0; c < 4; ++c)
-#pragma unroll
-    for (int u = 0; u < C::UQ; ++u) accA[c][u][0] = accA[c][u][1] = accB[c][u][0] = accB[c][u][1] = 0.0;
-#pragma unroll
-  for (int u = 0; u < C::UV; ++u) accV[u][0] = accV[u][1] = 0.0;
+  double accA[2][C::UQ][2], accB[2][C::UQ][2], accV[C::UV][2];
   const int ar = pg * 8 + (lane >> 2), sw = C::swz(ar);
-  const int aofs = ar * KC + (lane & 3), bofs = C::ACH + (lane & 3) * NCS + (lane >> 2);
-  for (int ch = 0; ch < C::NCH; ++ch) {
-    const int nx = ch + C::NST - 1;   // chunk to issue now, into the stage chunk ch-1 used
-    if (threadIdx.x == 0 && nx < C::NCH) {
-      if (ch >= 1) mbar_wait(&emp[nx % C::NST], ((ch - 1) / C::NST) & 1);
-      fence_proxy_async();
-      issue(nx);
-    }
-    mbar_wait(&bar[ch % C::NST], (ch / C::NST) & 1);
-    const double *stg = sst + (ch % C::NST) * C::STG;
-    const double *arow = stg + aofs, *brow = arow + TP * KC, *bb = stg + bofs;
-    const int zc = 1 + ch / C::CPA;   // axis of this chunk: component axis + 1 has a zero block
-#define RRQ_QCHUNK(Z, N) qmap_chunk<P, Z, N, DP>(arow, brow, sw, bb, accA, accB, accV)
-#define RRQ_QNS(N) (zc == 1 ? RRQ_QCHUNK(1, N) : zc == 2 ? RRQ_QCHUNK(2, N) : RRQ_QCHUNK(3, N))
-    switch (ns) {
-      case 0: RRQ_QNS(0); break;
-      case 1: RRQ_QNS(1); break;
-      case 2: RRQ_QNS(2); break;
-      default: RRQ_QNS(3); break;
-    }
+  const int aofs = ar * KC + (lane & 3);
+  const int pr = pg * 8 + (lane >> 2);
+  double *out = Qrow + (s0 + pr - sA) * QR::STRIDE;
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int u = 0; u < C::UQ; ++u) accA[c][u][0] = accA[c][u][1] = accB[c][u][0] = accB[c][u][1] = 0.0;
+#pragma unroll
+    for (int u = 0; u < C::UV; ++u) accV[u][0] = accV[u][1] = 0.0;
+    const int bofs = C::ACH + (lane & 3) * (h ? D::NCSH1 : D::NCSH0) + (lane >> 2);
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int vc = h * NCH + ch;
+      const int nx = vc + C::NST - 1;   // chunk to issue now, into the stage chunk vc-1 used
+      if (threadIdx.x == 0 && nx < 2 * NCH) {
+        if (vc >= 1) mbar_wait(&emp[nx % C::NST], ((vc - 1) / C::NST) & 1);
+        fence_proxy_async();
+        issue(nx);
+      }
+      mbar_wait(&bar[vc % C::NST], (vc / C::NST) & 1);
+      const double *stg = sst + (vc % C::NST) * C::STG;
+      const double *arow = stg + aofs, *brow = arow + TP * KC, *bb = stg + bofs;
+      const int zc = 1 + ch / C::CPA;   // axis of this chunk: component axis + 1 has a zero block
+#define RRQ_QCHUNK(Z, N, HH) qmap_chunk<P, Z, N, DP, HH>(arow, brow, sw, bb, accA, accB, accV)
+      // ZC = -1: no zero block among the pass's two components in this chunk's axis
+#define RRQ_QNS(N) (h == 0 ? (zc == 1 ? RRQ_QCHUNK(1, N, 0) : RRQ_QCHUNK(-1, N, 0)) \
+                           : (zc == 2 ? RRQ_QCHUNK(2, N, 1) : zc == 3 ? RRQ_QCHUNK(3, N, 1) : RRQ_QCHUNK(-1, N, 1)))
+      switch (ns) {
+        case 0: RRQ_QNS(0); break;
+        case 1: RRQ_QNS(1); break;
+        case 2: RRQ_QNS(2); break;
+        default: RRQ_QNS(3); break;
+      }
 #undef RRQ_QNS
 #undef RRQ_QCHUNK
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&emp[ch % C::NST]);
-  }
-  // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]; a lane owns whole entries (all 4 components of Q and
-  // dQ of entry e over its c loop): 16-B stores filling the entry's 128-B line (rows are 128-B aligned).
-  // M's columns carry v_lambda / v_theta (k_edge_tables), so no scaling here.
-  const int pr = pg * 8 + (lane >> 2);
-  if (pr < cnt) {
-    double *out = Qrow + (s0 + pr - sA) * QR::STRIDE;
-#pragma unroll
-    for (int u = 0; u < C::UQ; ++u) {
-      const int tl = ns + u * C::NSPLIT;
-      if (tl >= C::TQC) continue;   // == u < nq(ns)
-      const int e = tl * 4 + (lane & 3);   // entry qidx(j,k)
-      if (e >= D::NQ) continue;
-      double2 *o = reinterpret_cast<double2 *>(out + QR::EG * e);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        o[c] = make_double2(accA[c][u][0], accA[c][u][1]);
-        if constexpr (DP) o[4 + c] = make_double2(accB[c][u][0], accB[c][u][1]);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emp[vc % C::NST]);
     }
-    const int v0 = ns == 0 ? C::vstart(0) : ns == 1 ? C::vstart(1) : ns == 2 ? C::vstart(2) : C::vstart(3);
-    const int nv = ns == 0 ? C::vcount(0) : ns == 1 ? C::vcount(1) : ns == 2 ? C::vcount(2) : C::vcount(3);
+    // store: C[row = lane/4][col = 2 (lane%4) + {0,1}]; a lane owns the pass's two components of Q (and dQ)
+    // of entry e: two 32-B sectors (rows are 128-B aligned).  M's columns carry v_lambda / v_theta.
+    if (pr < cnt) {
 #pragma unroll
-    for (int u = 0; u < C::UV; ++u) {
-      if (u >= nv) continue;
-      const int col = (v0 + u) * 8 + 2 * (lane & 3);
-      if (col < 2 * D::NV) *reinterpret_cast<double2 *>(out + QR::V + col) = make_double2(accV[u][0], accV[u][1]);
+      for (int u = 0; u < C::UQ; ++u) {
+        const int tl = ns + u * C::NSPLIT;
+        if (tl >= C::TQC) continue;   // == u < nq(ns)
+        const int e = tl * 4 + (lane & 3);   // entry qidx(j,k)
+        if (e >= D::NQ) continue;
+        double2 *o = reinterpret_cast<double2 *>(out + QR::EG * e);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          o[2 * h + c] = make_double2(accA[c][u][0], accA[c][u][1]);
+          if constexpr (DP) o[4 + 2 * h + c] = make_double2(accB[c][u][0], accB[c][u][1]);
+        }
+      }
+      if (h == 1) {
+        const int v0 = ns == 0 ? C::vstart(0) : ns == 1 ? C::vstart(1) : ns == 2 ? C::vstart(2) : C::vstart(3);
+        const int nv = ns == 0 ? C::vcount(0) : ns == 1 ? C::vcount(1) : ns == 2 ? C::vcount(2) : C::vcount(3);
+#pragma unroll
+        for (int u = 0; u < C::UV; ++u) {
+          if (u >= nv) continue;
+          const int col = (v0 + u) * 8 + 2 * (lane & 3);
+          if (col < 2 * D::NV) *reinterpret_cast<double2 *>(out + QR::V + col) = make_double2(accV[u][0], accV[u][1]);
+        }
+      }
     }
   }
 }
@@ -1272,7 +1297,9 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 // (ContractCfg: tile-chunked zeta written by k_translate), two stages, 3 CTAs per SM at p <= 8.
 // ------------------------------------------------------------------------------------------------
 
-template <int P>
+// MK: the kernel mask at compile time (15 = all four, 3 = S|D: the DMMAs of the other kernels are compiled out --
+// a predicated-off DMMA still occupies the tensor pipe), 0 = taken from `mask` at run time.
+template <int P, int MK>
 __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
     k_contract(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, const int32_t *__restrict__ item_patch,
                const int64_t *__restrict__ seg_ptr, int64_t sA, const ContractPair *__restrict__ cpair,
@@ -1312,7 +1339,8 @@ __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
   // the fit operators are stored with the padded row stride NB, so a chunk of each is one contiguous copy
   // kernel mask: an operand is staged / multiplied only if a selected kernel needs it (P_D: D, D'; P_Sp: S';
   // P_Sg, P_Sd: S); a masked-off kernel's zeta blocks were not written by k_translate
-  const bool wS = mask & 1, wD = mask & 2, wSp = mask & 4, wDp = mask & 8;
+  const uint32_t km = MK ? (uint32_t)MK : mask;
+  const bool wS = km & 1, wD = km & 2, wSp = km & 4, wDp = km & 8;
   const unsigned nops = (unsigned)((wD || wDp) + wSp + wS);
   auto issue = [&](int ch, unsigned extra) {
     uint64_t *br = &bar[ch & 1];

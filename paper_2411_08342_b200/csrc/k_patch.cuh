@@ -168,12 +168,12 @@ __global__ void __launch_bounds__(EdgeTabCfg<P>::THREADS) k_edge_tables(int64_t 
   using D = Dims<P>;
   using L = Layout<P>;
   using C = EdgeTabCfg<P>;
-  constexpr int NS = D::NS, NQ = D::NQ, NV = D::NV, E = D::E, NB = C::NB, NCS = D::NCS, CQP = D::CQP;
+  constexpr int NS = D::NS, NQ = D::NQ, NV = D::NV, E = D::E, NB = C::NB, CQP = D::CQP;
   extern __shared__ __align__(16) double es[];
   const int64_t Pp = blockIdx.x;
   if (Pp >= n_patches) return;
   double *blk = fit + Pp * (int64_t)L::STRIDE;
-  double *M = blk + L::MQ;
+  double *M = blk + L::MQ, *M1 = blk + L::MQ1;
   for (int n0 = 0; n0 < E; n0 += NB) {
     const int nb = E - n0 < NB ? E - n0 : NB;   // nodes in this round
     __syncthreads();
@@ -213,9 +213,10 @@ __global__ void __launch_bounds__(EdgeTabCfg<P>::THREADS) k_edge_tables(int64_t 
       }
     }
     __syncthreads();
-    // rows k = axis E + kappa of M (row stride NCS), column-fastest over the round's NB x 3 rows
-    for (int w = threadIdx.x; w < 3 * nb * NCS; w += blockDim.x) {
-      const int r = w / NCS, col = w % NCS, axis = r / nb, i = r % nb;
+    // rows k = axis E + kappa of M, column-fastest over the round's NB x 3 rows; columns [0, NCH0) go to
+    // half 0 (row stride NCSH0), the rest to half 1 (row stride NCSH1) -- k_qmap's two column passes
+    for (int w = threadIdx.x; w < 3 * nb * D::NCP; w += blockDim.x) {
+      const int r = w / D::NCP, col = w % D::NCP, axis = r / nb, i = r % nb;
       const cd *H = reinterpret_cast<const cd *>(es + i * C::NODE) + 4 * NS, *EV = H + 3 * NQ;
       double val = 0.0;
       if (col < D::NCQ) {
@@ -237,7 +238,8 @@ __global__ void __launch_bounds__(EdgeTabCfg<P>::THREADS) k_edge_tables(int64_t 
         const int wv = col - D::NCQ, v = wv >> 1, ri = wv & 1;
         if (v < NV) val = ri ? EV[3 * v + axis].y : EV[3 * v + axis].x;
       }
-      M[(int64_t)(axis * E + n0 + i) * NCS + col] = val;
+      if (col < D::NCH0) M[(int64_t)(axis * E + n0 + i) * D::NCSH0 + col] = val;
+      else M1[(int64_t)(axis * E + n0 + i) * D::NCSH1 + (col - D::NCH0)] = val;
     }
   }
 }

@@ -898,7 +898,9 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     if ((r = cuda_check(c, "k_translate"))) return r;
     {
       TScope t4(c, 5, st);
-      k_contract<P><<<(unsigned)(it1 - it0), CC::WARPS * 32, CC::SMEM, st>>>(
+      const uint32_t km = mask & RRQ_ALL;
+      auto *kc = km == RRQ_ALL ? k_contract<P, 15> : km == (RRQ_S | RRQ_D) ? k_contract<P, 3> : k_contract<P, 0>;
+      kc<<<(unsigned)(it1 - it0), CC::WARPS * 32, CC::SMEM, st>>>(
           it0, it1, bp<int64_t>(c->items), bp<int32_t>(c->ipatch), bp<int64_t>(c->seg), sA, cp,
           fit, bp<double>(c->Z), s->nodes, s->normals, s->weights, mask, raw, obase, col_idx, vals[0], vals[1], vals[2],
           vals[3], pstat);
@@ -1001,7 +1003,9 @@ static cudaError_t set_attrs() {
   acc(cudaFuncSetAttribute(k_qmap<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   acc(cudaFuncSetAttribute(k_translate<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
   acc(cudaFuncSetAttribute(k_translate<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_contract<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_contract<P, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_contract<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_contract<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   return e;
 }
 

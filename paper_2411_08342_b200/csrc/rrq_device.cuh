@@ -67,6 +67,10 @@ struct Dims {
   static constexpr int NV8 = (2 * NV + 7) / 8 * 8;// V columns (jk, re/im), padded
   static constexpr int NCP = NCQ + NV8;           // whole 8-wide DMMA tiles
   static constexpr int NCS = NCP + ((4 - NCP % 16) + 16) % 16; // row stride == 4 (mod 16): conflict-free B frags
+  // k_qmap runs the columns in two passes (register budget): half 0 = Q components scalar, x; half 1 = Q
+  // components y, z and the V columns.  M is stored as two blocks [K][NCSH0] | [K][NCSH1] (rows == 4 mod 16)
+  static constexpr int NCH0 = 2 * CQP, NCH1 = 2 * CQP + NV8;
+  static constexpr int NCSH0 = NCH0 + ((4 - NCH0 % 16) + 16) % 16, NCSH1 = NCH1 + ((4 - NCH1 % 16) + 16) % 16;
 };
 
 // (l, m >= 0) -> flat index
@@ -86,8 +90,9 @@ struct Layout {
   static constexpr int CM = TL + 3 * D::E;   // [3][Q][3] monomial coefficients of the edge interpolants
   static constexpr int NF = D::N + ((4 - D::N % 16) + 16) % 16;   // fit-operator row stride == 4 (mod 16)
   static constexpr int FIT = CM + 9 * D::Q;  // [13 NP][NF]: P_D (4NP) P_Sp (4NP) P_Sd (NP) P_Sg (4NP)
-  static constexpr int MQ = (FIT + 13 * D::NP * NF + 3) / 4 * 4;   // [K][NCS]: GEMM operand of the Q / V maps
-  static constexpr int END = MQ + D::K * D::NCS;
+  static constexpr int MQ = (FIT + 13 * D::NP * NF + 3) / 4 * 4;   // GEMM operand of the Q / V maps:
+  static constexpr int MQ1 = MQ + D::K * D::NCSH0;                  //   [K][NCSH0] (half 0) | [K][NCSH1] (half 1)
+  static constexpr int END = MQ1 + D::K * D::NCSH1;
   static constexpr int STRIDE = (END + 31) / 32 * 32;
 };
 enum { H_O = 0, H_RM = 3, H_H = 12, H_ZLO = 13, H_ZHI = 14, H_VL = 15, H_CP = 24, H_RP = 27, H_HP = 28 };

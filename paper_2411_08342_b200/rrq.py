@@ -10,7 +10,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "librrq.so")
+_LIB_PATH = os.environ.get("RRQ_LIBRARY") or os.path.join(_HERE, "librrq.so")   # override: kernel-variant experiments
 KERNELS = ("S", "D", "Sp", "Dp")
 RRQ_S, RRQ_D, RRQ_SP, RRQ_DP, RRQ_ALL, RRQ_RAW = 1, 2, 4, 8, 15, 16
 
