@@ -72,6 +72,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--n-off", type=int, default=None, help="override off-surface target count (debug)")
+    ap.add_argument("--p", type=int, default=None, help="override the harmonic order (4..14; e.g. the paper's Table 3 p = 12, 14)")
     ap.add_argument("--freq", type=str, default=None,
                     help="override the mesh: icosphere frequency (configs 2, 4), or NTHxNPH / NUxNV (configs 3, 6)")
     ap.add_argument("--chunk-pairs", type=int, default=16_000_000)
@@ -177,6 +178,8 @@ def make_inputs(args, rank):
     kw = {}
     if args.n_off is not None:
         kw["n_off"] = args.n_off
+    if getattr(args, "p", None) is not None:
+        kw["p"] = args.p
     if args.freq is not None:
         kw["freq"] = tuple(int(v) for v in args.freq.split("x")) if "x" in args.freq else int(args.freq)
     return make_config(args.config, seed_offset=rank, **kw)

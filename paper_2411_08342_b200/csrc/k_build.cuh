@@ -155,11 +155,14 @@ struct TrCfg {
   static constexpr int WPB_FIT = (SMEM_MAX / 8 - TAB_D) / PER_WARP;
   static constexpr int WPB = WPB_FIT > WMAX ? WMAX : WPB_FIT;
   static constexpr size_t SMEM = (size_t)(TAB_D + WPB * PER_WARP) * sizeof(double);
-  // code: Q position | new S' position << 7 | FA | FB | PRIME;  prime code: S' positions of window
-  // entries 1 .. WD-1, 7 bits each.  cinfo: l | m << 4 | i << 8 | first lane << 12 | lanes << 20.
-  static constexpr uint32_t FA = 1u << 14, FB = 1u << 15, PRIME = 1u << 17;
+  // code: Q position (7 bits) | new S' position << 7 (SEB bits: 7, or 8 once p^2 + 1 > 128) | FA | FB | PRIME;
+  // prime code: S' positions of window entries 1 .. WD-1, SEB bits each.  cinfo: l | m << 4 | i << 8 |
+  // first lane << 12 | lanes << 20.
+  static constexpr int SEB = P * P < 128 ? 7 : 8;
+  static constexpr uint32_t SEM = (1u << SEB) - 1;
+  static constexpr uint32_t FA = 1u << (7 + SEB), FB = FA << 1, PRIME = FA << 3;
   static_assert(WPB >= 2, "translate smem");
-  static_assert(D::NQ < 127 && P * P < 128 && WD <= 5, "translate code fields");
+  static_assert(D::NQ < 127 && P * P < (1 << SEB) && WD <= 5 && SEB * (WD - 1) <= 32 && P < 16, "translate code fields");
 };
 
 // D = A B + C for one 8x8x4 fp64 tile (FP64 tensor core, SASS DMMA).  Fragments: a = A[lane/4][lane%4],
@@ -257,7 +260,8 @@ struct QmapCfg {
 #ifndef RRQ_QMAP_NST
 #define RRQ_QMAP_NST 4
 #endif
-  static constexpr int NST = RRQ_QMAP_NST;                         // pipeline stages (chunks in flight)
+  // pipeline stages (chunks in flight); p >= 12: the stage is 37 KB (p = 12) / 73 KB (p = 14), 1 CTA per SM
+  static constexpr int NST = P <= 10 ? RRQ_QMAP_NST : (P == 12 ? 4 : 2);
   // A (the tile's 32 GEMM rows) is stored tile-chunked by k_pair_edge: chunk ch = [32 rows][KC] (ACH doubles,
   // rows 0..15 = a-rows of the tile's pairs, 16..31 = b-rows), so a stage = [A chunk | B chunk] is two bulk
   // copies and A needs no resident shared memory.  KC = 8: the halves of rows with (r >> 1) odd are swapped
@@ -1011,7 +1015,10 @@ struct ContractCfg {
   static constexpr size_t STG = SMEM_B + ZCH;
   static constexpr size_t SNODE = (7 * D::N + 1) / 2 * 2;   // the patch's nodes [N][3], normals [N][3], weights [N]
   static constexpr size_t SMEM = (ZT + 2 * STG + SNODE) * sizeof(double) + TP * 64;   // + ContractPair[TP]
-  static constexpr int MINB = (P <= 8 && SMEM * 3 <= 225 * 1024) ? 3 : 2;   // p = 10: registers (TPW = 4)
+  static constexpr int MINB = (P <= 8 && SMEM * 3 <= 225 * 1024) ? 3 : (P <= 10 ? 2 : 1);   // p = 10: registers (TPW = 4)
+  // p <= 10: the P_Sd fragments of Theta . P_Sd are loaded into registers before the Z tile lands; p >= 12:
+  // TPW x NK would not fit the register file, so they are read as they are used
+  static constexpr bool BQREG = P <= 10;
   __host__ __device__ static constexpr int swz(int r) { return KC == 16 ? (r & 3) << 2 : KC == 8 ? ((r >> 1) & 1) << 2 : 0; }
   // position of zeta entry (block b = 0 Theta, 1..4 zeta(W), 5..8 zeta(dW), 9..12 zeta_S; c = (l,m)) of tile row r
   __host__ __device__ static constexpr int64_t zoff(int b, int r, int c) {
@@ -1154,14 +1161,14 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 #pragma unroll
     for (int t = 0; t < C::STEPS; ++t) {
       const uint32_t cw = code[t * 32 + lane];
-      const int qe = cw & 127, se = (cw >> 7) & 127;
+      const int qe = cw & 127, se = (cw >> 7) & C::SEM;
       ws[t % WD] = *reinterpret_cast<const double2 *>(sx + SXW * se);
       wg[t % WD] = *reinterpret_cast<const double2 *>(sx + SXW * se + 2);
       if (t == 0 || (cw & C::PRIME)) {   // every piece and every sweep starts with a PRIME
         const uint32_t pw = pcode[t * 32 + lane];
 #pragma unroll
         for (int i = 1; i < WD; ++i) {
-          const int pe = (pw >> (7 * (i - 1))) & 127;
+          const int pe = (pw >> (C::SEB * (i - 1))) & C::SEM;
           ws[(t - i + WD * C::STEPS) % WD] = *reinterpret_cast<const double2 *>(sx + SXW * pe);
           wg[(t - i + WD * C::STEPS) % WD] = *reinterpret_cast<const double2 *>(sx + SXW * pe + 2);
         }
@@ -1176,7 +1183,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
       double2 v = *reinterpret_cast<const double2 *>(qb + C::SV + 2 * (qe + 2));
       // k < 0: A^{(j,-k)} = (-1)^k conj A^{(j,k)}, so Im(A S) = A.x S.y + A.y S.x takes -A.x (odd k, FA) or
       // -A.y (even k, FB): flipped in place on this step's Q operands (used by all WD outputs)
-      const uint32_t fa = (cw >> 14) & 1, fb = (cw >> 15) & 1;
+      const uint32_t fa = (cw & C::FA) ? 1u : 0u, fb = (cw & C::FB) ? 1u : 0u;
       v.x = flip_if(v.x, fa);
       v.y = flip_if(v.y, fb);
 #pragma unroll
@@ -1367,15 +1374,16 @@ __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
   }
   // P_Sd fragments for Theta . P_Sd straight from global, issued before waiting for the Z tile
   constexpr int NK = (NP + 3) / 4;
-  double bq[CC::TPW][NK];
+  double bq[CC::BQREG ? CC::TPW : 1][CC::BQREG ? NK : 1];
+  auto psd = [&](int tw, int q) {
+    const int tile = warp + tw * CC::WARPS, bn = (tile / CC::MT) * 8 + (lane >> 2), kk = 4 * q + (lane & 3);
+    return (wS && tile < CC::TILES && bn < N && kk < NP) ? __ldg(PSd + kk * NB + bn) : 0.0;
+  };
+  if constexpr (CC::BQREG) {
 #pragma unroll
-  for (int tw = 0; tw < CC::TPW; ++tw) {
-    const int tile = warp + tw * CC::WARPS, bn = (tile / CC::MT) * 8 + (lane >> 2);
+    for (int tw = 0; tw < CC::TPW; ++tw)
 #pragma unroll
-    for (int q = 0; q < NK; ++q) {
-      const int kk = 4 * q + (lane & 3);
-      bq[tw][q] = (wS && tile < CC::TILES && bn < N && kk < NP) ? __ldg(PSd + kk * NB + bn) : 0.0;
-    }
+      for (int q = 0; q < NK; ++q) bq[tw][q] = psd(tw, q);
   }
   const double h = blk[L::HDR + H_H];
   const double inv4pi = 1.0 / (4.0 * kPi);
@@ -1393,7 +1401,10 @@ __global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
 #pragma unroll
     for (int q = 0; q < NK; ++q) {
       const int kk = 4 * q + (lane & 3);
-      dmma(acc[tw][0], acc[tw][1], kk < NP ? zr[4 * q] : 0.0, bq[tw][q]);
+      double bv;
+      if constexpr (CC::BQREG) bv = bq[tw][q];
+      else bv = psd(tw, q);
+      dmma(acc[tw][0], acc[tw][1], kk < NP ? zr[4 * q] : 0.0, bv);
     }
   }
   // the 4 NP blocks, B double-buffered through shared memory; emp[b] = "every warp is done with buffer b"

@@ -275,11 +275,13 @@ struct FitCfg {
   // shared: Fq [NP][N][4] | rd [NP][4] | beta [NP] | rdb [NP] | betab [NP] | xl,nl [N][3] | sh [64] |
   // vd [NP][4] | cn2 [NP + 1]
   static constexpr size_t FQ = (size_t)NP * N * 4, RD = 4 * NP;
-  static constexpr size_t SMEM_D = FQ + RD + 3 * NP + 6 * N + 64 + 4 * NP + NP + 1;
+  // p >= 12: the quaternion matrix (359 KB at p = 12) lives in the CTA's global workspace (L2-resident)
+  static constexpr bool FQ_GLOBAL = FQ * sizeof(double) > 160 * 1024;
+  static constexpr size_t SMEM_D = (FQ_GLOBAL ? 0 : FQ) + RD + 3 * NP + 6 * N + 64 + 4 * NP + NP + 1;
   static constexpr size_t SMEM = SMEM_D * sizeof(double);
-  static constexpr int MINB = 2 * SMEM <= 227 * 1024 ? 2 : 1;   // CTAs per SM the shared memory allows
-  // per-CTA global workspace (doubles): W [N][N][4] | Xs [N][N] | B [NP][N] | Hm [N][NP]
-  static constexpr int64_t WS = (int64_t)N * N * 4 + (int64_t)N * N + 2 * (int64_t)N * NP;
+  static constexpr int MINB = FQ_GLOBAL ? 1 : (2 * SMEM <= 227 * 1024 ? 2 : 1);   // CTAs per SM
+  // per-CTA global workspace (doubles): W [N][N][4] | Xs [N][N] | B [NP][N] | Hm [N][NP] (| Fq)
+  static constexpr int64_t WS = (int64_t)N * N * 4 + (int64_t)N * N + 2 * (int64_t)N * NP + (FQ_GLOBAL ? (int64_t)FQ : 0);
 };
 
 template <int P>
@@ -292,8 +294,8 @@ __global__ void __launch_bounds__(256, FitCfg<P>::MINB) k_patch_fit_q(int64_t n_
   using FC = FitCfg<P>;
   constexpr int N = D::N, NP = D::NP;
   extern __shared__ double fs[];
-  double *Fq = fs;                      // column lm: Fq[(lm N + i) 4 + comp]
-  double *rd = Fq + FC::FQ;             // [NP][4] diagonal of R
+  double *Fq = FC::FQ_GLOBAL ? work + blockIdx.x * FC::WS + (FC::WS - (int64_t)FC::FQ) : fs;   // Fq[(lm N + i) 4 + comp]
+  double *rd = FC::FQ_GLOBAL ? fs : Fq + FC::FQ;   // [NP][4] diagonal of R
   double *beta = rd + FC::RD;           // [NP]
   double *rdb = beta + NP, *betab = rdb + NP;
   double *xl = betab + NP, *nl = xl + 3 * N;
@@ -416,7 +418,8 @@ __global__ void __launch_bounds__(256, FitCfg<P>::MINB) k_patch_fit_q(int64_t n_
     // ---- Q^H e_c (warp per two or four columns, the columns in registers: entry i = lane + 32 u), the first
     // NP entries stored for the back substitution
     {
-      constexpr int NU = (N + 31) / 32, CW = FC::MINB == 2 ? 2 : 4;   // 2 under the 128-register bound
+      // 2 under the 128-register bound, 1 at p >= 12 (NU = 5, 7 quaternions per column)
+      constexpr int NU = (N + 31) / 32, CW = FC::FQ_GLOBAL ? 1 : (FC::MINB == 2 ? 2 : 4);
       for (int c0 = CW * warp; c0 < N; c0 += CW * nw) {
         qd y[CW][NU];
 #pragma unroll

@@ -320,7 +320,9 @@ static std::vector<double> make_trtab_p(int p) {
     case 4: return make_trtab<4>();
     case 6: return make_trtab<6>();
     case 8: return make_trtab<8>();
-    default: return make_trtab<10>();
+    case 10: return make_trtab<10>();
+    case 12: return make_trtab<12>();
+    default: return make_trtab<14>();
   }
 }
 
@@ -340,8 +342,8 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   *out = nullptr;
   if (!params) return fail(nullptr, RRQ_ERR_INVALID_ARG, "params is NULL");
   const rrq_params &p = *params;
-  if (p.p != 4 && p.p != 6 && p.p != 8 && p.p != 10)
-    return fail(nullptr, RRQ_ERR_NOT_IMPLEMENTED, "p must be one of 4, 6, 8, 10");
+  if (p.p != 4 && p.p != 6 && p.p != 8 && p.p != 10 && p.p != 12 && p.p != 14)
+    return fail(nullptr, RRQ_ERR_NOT_IMPLEMENTED, "p must be one of 4, 6, 8, 10, 12, 14");
   if (p.n_nodes != p.p * p.p) return fail(nullptr, RRQ_ERR_INVALID_ARG, "n_nodes must be p*p (collapsed GL, A1)");
   if (p.p_edge != 2 * p.p) return fail(nullptr, RRQ_ERR_NOT_IMPLEMENTED, "p_edge must be 2p (reading A4)");
   if (p.n_omega < 1 || p.n_omega > 128) return fail(nullptr, RRQ_ERR_INVALID_ARG, "n_omega must be in [1,128]");
@@ -487,7 +489,9 @@ rrq_status rrq_debug_zeta(rrq_ctx c, int64_t max_pairs, int64_t *perm, double *Z
       case 4: k_debug_zeta<4><<<g, 256>>>(n, su, zb, tmp); break;
       case 6: k_debug_zeta<6><<<g, 256>>>(n, su, zb, tmp); break;
       case 8: k_debug_zeta<8><<<g, 256>>>(n, su, zb, tmp); break;
-      default: k_debug_zeta<10><<<g, 256>>>(n, su, zb, tmp); break;
+      case 10: k_debug_zeta<10><<<g, 256>>>(n, su, zb, tmp); break;
+      case 12: k_debug_zeta<12><<<g, 256>>>(n, su, zb, tmp); break;
+      default: k_debug_zeta<14><<<g, 256>>>(n, su, zb, tmp); break;
     }
     cudaMemcpy(Z, tmp, (size_t)n * c->last_nz * sizeof(double), cudaMemcpyDeviceToHost);
     cudaFree(tmp);
@@ -674,6 +678,8 @@ size_t rrq_fit_bytes(rrq_ctx c, int64_t n_patches) {
     case 6: s = stride_bytes<6>(); break;
     case 8: s = stride_bytes<8>(); break;
     case 10: s = stride_bytes<10>(); break;
+    case 12: s = stride_bytes<12>(); break;
+    case 14: s = stride_bytes<14>(); break;
   }
   return s * (size_t)n_patches;
 }
@@ -712,18 +718,22 @@ rrq_status rrq_patch_fit(rrq_ctx c, const rrq_surface *s, void *fit, int32_t *pa
     case 6: return patch_fit_impl<6>(c, s, (double *)fit, patch_status, st);
     case 8: return patch_fit_impl<8>(c, s, (double *)fit, patch_status, st);
     case 10: return patch_fit_impl<10>(c, s, (double *)fit, patch_status, st);
+    case 12: return patch_fit_impl<12>(c, s, (double *)fit, patch_status, st);
+    case 14: return patch_fit_impl<14>(c, s, (double *)fit, patch_status, st);
   }
   return RRQ_ERR_NOT_IMPLEMENTED;
 }
 
-constexpr int kWPB = 8;   // warps per CTA of k_pair_edge
+// warps per CTA of k_pair_edge: 8, 6 at p = 14 (shared memory: the per-warp gradient tables grow as p^2)
+template <int P>
+constexpr int kWPB = P >= 14 ? 6 : 8;
 
 template <int P>
 static size_t edge_smem(int n_omega) {
   using D = Dims<P>;
   int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + HC_SIZE + kNDirect * D::Q;
   tab = (tab + 1) & ~1;
-  return (size_t)tab * sizeof(double) + kWPB * kPPW * sizeof(PairState<P>) + kWPB * sizeof(WarpScr<P>);
+  return (size_t)tab * sizeof(double) + kWPB<P> * kPPW * sizeof(PairState<P>) + kWPB<P> * sizeof(WarpScr<P>);
 }
 
 template <int P>
@@ -869,8 +879,9 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
       k_pair_setup<P><<<nblk(np_, 256), 256, 0, sp>>>(sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase,
                                                        pair_patch, fit, tg->x, tg->normal, tg->self_node, tg->side,
                                                        bp<int64_t>(c->seg), bp<int64_t>(c->items), it0, ps, cp);
-      unsigned grid = (unsigned)std::min<int64_t>((np_ + kWPB * kPPW - 1) / (kWPB * kPPW), (int64_t)c->num_sms * 4);
-      k_pair_edge<P, kWPB><<<grid, kWPB * 32, edge_smem<P>(c->prm.n_omega), sp>>>(
+      constexpr int WPB = kWPB<P>;
+      unsigned grid = (unsigned)std::min<int64_t>((np_ + WPB * kPPW - 1) / (WPB * kPPW), (int64_t)c->num_sms * 4);
+      k_pair_edge<P, WPB><<<grid, WPB * 32, edge_smem<P>(c->prm.n_omega), sp>>>(
           sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
           tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, Ar, Xr,
           pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, ps, want_dp);
@@ -958,6 +969,8 @@ rrq_status rrq_build_correction(rrq_ctx c, const rrq_surface *s, const rrq_targe
     case 6: return build_impl<6>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
     case 8: return build_impl<8>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
     case 10: return build_impl<10>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
+    case 12: return build_impl<12>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
+    case 14: return build_impl<14>(c, s, tg, pair_ptr, pair_patch, row_begin, row_end, (const double *)fit, mask, row_ptr, col_idx, vals, pstat, st);
   }
   return RRQ_ERR_NOT_IMPLEMENTED;
 }
@@ -998,14 +1011,14 @@ static cudaError_t set_attrs() {
   auto acc = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
   acc(cudaFuncSetAttribute(k_edge_tables<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EdgeTabCfg<P>::SMEM));
   acc(cudaFuncSetAttribute(k_patch_fit_q<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FitCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_pair_edge<P, kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  acc(cudaFuncSetAttribute(k_qmap<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  acc(cudaFuncSetAttribute(k_qmap<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_pair_edge<P, kWPB<P>>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_smem<P>(128)));
+  acc(cudaFuncSetAttribute(k_qmap<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QmapCfg<P>::SMEM));
+  acc(cudaFuncSetAttribute(k_qmap<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QmapCfg<P>::SMEM));
   acc(cudaFuncSetAttribute(k_translate<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
   acc(cudaFuncSetAttribute(k_translate<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_contract<P, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  acc(cudaFuncSetAttribute(k_contract<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  acc(cudaFuncSetAttribute(k_contract<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  acc(cudaFuncSetAttribute(k_contract<P, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ContractCfg<P>::SMEM));
+  acc(cudaFuncSetAttribute(k_contract<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ContractCfg<P>::SMEM));
+  acc(cudaFuncSetAttribute(k_contract<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ContractCfg<P>::SMEM));
   return e;
 }
 
@@ -1015,6 +1028,8 @@ static cudaError_t set_kernel_attributes(int p) {
     case 6: return set_attrs<6>();
     case 8: return set_attrs<8>();
     case 10: return set_attrs<10>();
+    case 12: return set_attrs<12>();
+    case 14: return set_attrs<14>();
   }
   return cudaErrorInvalidValue;
 }

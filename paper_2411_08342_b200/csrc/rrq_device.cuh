@@ -112,10 +112,10 @@ constexpr double kRhoDirect = 1.6;
 
 // Harmonic coefficient table (host-built by rrq_create, copied to shared memory by the kernels that use
 // it), so no square root is taken on the hot path:
-//   HC_DC + 3 (l*l + l + m) + {0,1,2} = sqrt((l-m)(l+m)), sqrt((l-m)(l-m-1)), sqrt((l+m)(l+m-1))  (|m|<=l<=10)
-//   HC_DG + m  = sqrt((2m-1)/(2m)),  HC_SB + m = sqrt(2m+1)                                       (m <= 10)
+//   HC_DC + 3 (l*l + l + m) + {0,1,2} = sqrt((l-m)(l+m)), sqrt((l-m)(l-m-1)), sqrt((l+m)(l+m-1))  (|m|<=l<=14)
+//   HC_DG + m  = sqrt((2m-1)/(2m)),  HC_SB + m = sqrt(2m+1)                                       (m <= 14)
 //   HC_RA + sidx(l,m) = (2l+1)/sqrt((l+1+m)(l+1-m)),  HC_RB + sidx(l,m) = sqrt((l+m)(l-m))/sqrt((l+1+m)(l+1-m))
-constexpr int HC_LMAX = 10;
+constexpr int HC_LMAX = 14;
 constexpr int HC_DC = 0, HC_DG = 3 * (HC_LMAX + 1) * (HC_LMAX + 1), HC_SB = HC_DG + HC_LMAX + 1,
               HC_RA = HC_SB + HC_LMAX + 1, HC_RB = HC_RA + (HC_LMAX + 1) * (HC_LMAX + 2) / 2,
               HC_SIZE = HC_RB + (HC_LMAX + 1) * (HC_LMAX + 2) / 2;

@@ -66,7 +66,7 @@ def make_config(cfg, n_off=None, include_nodes=True, freq=None, p=None, seed_off
         cnt = 1000 if n_off is None else n_off
         parts.append(offsurface_normal_targets(
             S, rng, cnt, lambda r, c: -r.integers(1, 9, size=c).astype(np.float64)))
-        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.0, all_pairs=False, name="cfg1-sphere20-p4"))
+        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.0, all_pairs=False, name=f"cfg1-sphere{S.n_patches}-p{pp}"))
     if cfg == 2:
         pp = p or 8
         S = make_sphere_surface(freq or 8, pp, 2 * pp)
@@ -89,7 +89,7 @@ def make_config(cfg, n_off=None, include_nodes=True, freq=None, p=None, seed_off
         sides = np.where(rng.random(cnt) < 0.5, -1, 1)
         x = xs * (1.0 + sides * 10.0 ** e * h[pid])[:, None]
         parts.append((x, xs.copy(), np.full(cnt, -1, np.int64), sides.astype(np.int8)))
-        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False, name="cfg2-sphere1280-p8"))
+        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False, name=f"cfg2-sphere{S.n_patches}-p{pp}"))
     if cfg == 3:
         pp = p or 6
         nth, nph = (64, 80) if freq is None else freq
@@ -112,7 +112,7 @@ def make_config(cfg, n_off=None, include_nodes=True, freq=None, p=None, seed_off
         nu = np.stack([np.cos(th) * np.cos(ph), np.cos(th) * np.sin(ph), np.sin(th)], 1)
         x = x0 + (sides * 10.0 ** e * h[pid])[:, None] * nu
         parts.append((x, nu, np.full(cnt, -1, np.int64), sides.astype(np.int8)))
-        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False, name="cfg3-torus10240-p6"))
+        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False, name=f"cfg3-torus{S.n_patches}-p{pp}"))
     if cfg == 4:
         pp = p or 8
         while True:
@@ -131,7 +131,7 @@ def make_config(cfg, n_off=None, include_nodes=True, freq=None, p=None, seed_off
         sides = np.where(np.arange(cnt) < cnt // 2, -1, 1)
         sides = rng.permutation(sides)
         parts.append(offsurface_normal_targets(S, rng, cnt, lambda r, c: r.uniform(-12.0, 0.0, c), sides))
-        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False, name="cfg4-bumpy50000-p8"))
+        return _assemble(S, parts, dict(p=pp, q=2 * pp, eta=1.5, all_pairs=False, name=f"cfg4-bumpy{S.n_patches}-p{pp}"))
     if cfg == 5:
         pp = p or 10
         chord = 0.2

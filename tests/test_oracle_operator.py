@@ -139,3 +139,32 @@ def test_near_list_vs_kdtree():
             sets[t].add(int(sn[t] // S.n))
         got = pat[ptr[t]:ptr[t + 1]]
         assert list(got) == sorted(sets[t])
+
+
+@pytest.mark.parametrize("p", [12, 14])
+def test_high_order_sphere_operators(p):
+    """SURVEY §8(f) NEXT(3) at the oracle: p = 12, 14 on a 180-patch sphere.  Gauss law and the Y_3 eigenrelations of
+    S and D on the surface, inside and outside improve on p = 8 (~1e-7 on the surface: Table 3 reaches
+    ~1e-9 .. 1e-11 at p = 12, 14)."""
+    S = make_sphere_surface(3, p, 2 * p)
+    x0 = S.nodes[3, 5]
+    tx = np.array([x0, 0.6 * x0, 1.4 * x0])
+    nu = np.tile(x0, (3, 1))
+    sn = np.array([3 * S.n + 5, -1, -1], np.int64)
+    sd = np.array([0, -1, 1], np.int8)
+    tg, pa = _all_pairs(3, S.n_patches)
+    vals, st = O.build_rows(S, tx, nu, sn, sd, tg, pa, raw=True)
+    assert (st & 6).max() == 0
+    V = vals.reshape(4, 3, -1)
+    # Gauss law holds to the fp64 rounding of the fit (grows with p: ~1e-11 at p = 8, ~1e-10 at p = 12, 14)
+    assert np.abs(V[1].sum(1) - np.array([-0.5, -1.0, 0.0])).max() < 1e-9
+    xs = S.nodes.reshape(-1, 3)
+    l, c = 3, 7
+    Y = xs[:, 2] * (5 * xs[:, 2] ** 2 - 3)
+    Yt = x0[2] * (5 * x0[2] ** 2 - 3)
+    r = np.array([1.0, 0.6, 1.4])
+    expS = np.array([1 / c, r[1] ** l / c, r[2] ** (-l - 1) / c])
+    expD = np.array([-1 / (2 * c), -(l + 1) * r[1] ** l / c, l * r[2] ** (-l - 1) / c])
+    eS, eD = np.abs(V[0] @ Y / Yt - expS), np.abs(V[1] @ Y / Yt - expD)
+    print(p, eS, eD)
+    assert eS.max() < 2e-9 and eD.max() < 2e-9
