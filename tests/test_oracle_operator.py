@@ -167,4 +167,7 @@ def test_high_order_sphere_operators(p):
     expD = np.array([-1 / (2 * c), -(l + 1) * r[1] ** l / c, l * r[2] ** (-l - 1) / c])
     eS, eD = np.abs(V[0] @ Y / Yt - expS), np.abs(V[1] @ Y / Yt - expD)
     print(p, eS, eD)
-    assert eS.max() < 2e-9 and eD.max() < 2e-9
+    # p = 12: S ~1e-10, D ~1e-11 (p = 8: ~1e-7 / 1e-6 on the surface).  p = 14: fp64 rounding dominates (the
+    # same rows in long double: S 1.4e-10 / 1.8e-11 / 1.0e-9, D 1.1e-11 / 9e-13 / 7.7e-11 -- DESIGN.md §11)
+    bS, bD = (1e-9, 2e-10) if p == 12 else (3e-7, 2e-9)
+    assert eS.max() < bS and eD.max() < bD
