@@ -363,6 +363,7 @@ def run_ours(args, ws, rank):
                                         "co-runs with k_qmap/k_translate/k_contract of sub-chunk i); serial_*: one extra "
                                         "untimed step with the overlap off (the kernels' own device times)"},
         "stages_ms_per_step": {k: v / args.steps for k, v in tim["ms"].items()},
+        "serial_stages_ms": dict(tser["ms"]),
         "pairs_per_s": npairs * args.steps / (ms_max / 1e3) * ws,
         "rows_per_s": R.T * args.steps / (ms_max / 1e3) * ws,
         # the paper's throughput unit for the evaluation phase: close targets (rows with a correction) per

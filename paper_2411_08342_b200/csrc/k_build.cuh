@@ -357,6 +357,229 @@ __global__ void k_pair_setup(int64_t sA, int64_t sB, const int64_t *__restrict__
         cp[3] = make_double2(__longlong_as_double(k), __longlong_as_double((long long)(uint32_t)self_local));
 }
 
+// ------------------------------------------------------------------------------------------------
+// k_newton: the near-singular parameter t0 of every (pair, edge) (Step 5; readings A12, A12',
+// A12''), one lane per edge.  Work index w = e np + i (edge-major over the sub-chunk's patch-major pairs), so
+// the lanes of a warp share the edge number and - but for patch boundaries - the patch: the Legendre
+// coefficients of the edge interpolant (A4') are read through warp-uniform cached loads instead of living
+// in registers, the three components of x(t) share one Legendre recurrence, and the sums over components
+// are local to a lane (no shuffles).
+// The complex Newton iteration count varies from 2 to 20 between edges, so a warp is a small work queue:
+// it draws batches of 32 consecutive edges (one atomic per batch), computes their starting guesses
+// together (3 real Newton steps + the quadratic model: uniform work) into shared-memory slots, and a lane
+// whose edge has converged takes the next slot while the other lanes keep iterating.
+// Output per edge: t0 (re, |im|) and a flag byte (bit 0 converged, bit 1 swap regime A5, bit 2 direct rule
+// A11').
+// ------------------------------------------------------------------------------------------------
+constexpr int kNewtonThreads = 128, kNewtonSlot = 7;
+// Bonnet recurrence constants: a[j] = (2j+1)/(j+1), b[j] = j/(j+1), d[j] = 2j+1
+struct LegTab { double a[32], b[32], d[32]; };
+constexpr LegTab make_leg_tab() {
+  LegTab t{};
+  for (int j = 0; j < 32; ++j) { t.a[j] = (2.0 * j + 1.0) / (j + 1.0); t.b[j] = (double)j / (j + 1.0); t.d[j] = 2.0 * j + 1.0; }
+  return t;
+}
+__constant__ LegTab kLeg = make_leg_tab();
+
+// Starting guess of one edge: chord projection, 3 real Newton steps on (x - r').x', quadratic-model complex
+// guess (A12).  C2 = the edge's 3 Q Legendre coefficients [j][c] as 16-B pairs.
+template <int Q>
+__device__ __forceinline__ cd newton_guess(const double2 *__restrict__ C2, const double (&rc)[3]) {
+  // chord projection: x(1) = sum_j C_j, x(-1) = sum_j (-1)^j C_j
+  double abab = 0, arab = 0;
+  {
+    double v[3] = {0, 0, 0}, A[3] = {0, 0, 0};
+#pragma unroll 1
+    for (int j = 0; j < Q; j += 2) {   // coefficients of P_j, P_{j+1}: 3 aligned 16-B loads
+      const double2 u0 = __ldg(C2 + 3 * (j >> 1)), u1 = __ldg(C2 + 3 * (j >> 1) + 1), u2 = __ldg(C2 + 3 * (j >> 1) + 2);
+      v[0] += u0.x; A[0] += u0.x; v[1] += u0.y; A[1] += u0.y; v[2] += u1.x; A[2] += u1.x;
+      v[0] += u1.y; A[0] -= u1.y; v[1] += u2.x; A[1] -= u2.x; v[2] += u2.y; A[2] -= u2.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double ab = v[c] - A[c], ar = rc[c] - A[c];
+      abab += ab * ab;
+      arab += ar * ab;
+    }
+  }
+  double tc = -1.0 + 2.0 * arab / (abab > 0 ? abab : 1.0);
+  // x(t) - r', x'(t), x''(t) at real t (Bonnet's recurrence and its derivatives, one recurrence for the 3
+  // components).  The j loop is rolled two steps at a time (recurrence constants from kLeg) so that the
+  // compiler does not hoist all 3 Q coefficient loads into registers.
+  double xr[3], d1[3], d2[3];
+  auto eval_r = [&](double t) {
+    double P0 = 1, P1 = t, a0 = 0, a1 = 1, b0 = 0, b1 = 0;
+    {
+      const double2 u0 = __ldg(C2), u1 = __ldg(C2 + 1), u2 = __ldg(C2 + 2);
+      const double c0[3] = {u0.x, u0.y, u1.x}, c1[3] = {u1.y, u2.x, u2.y};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { xr[c] = fma(c1[c], t, c0[c]) - rc[c]; d1[c] = c1[c]; d2[c] = 0; }
+    }
+#pragma unroll 1
+    for (int j = 1; j + 1 < Q; j += 2) {   // coefficients of P_{j+1}, P_{j+2}: flat index 3 (j + 1), even
+      const double2 *cp = C2 + 3 * ((j + 1) >> 1);
+      const double2 u0 = __ldg(cp), u1 = __ldg(cp + 1), u2 = __ldg(cp + 2);
+      const double cj[2][3] = {{u0.x, u0.y, u1.x}, {u1.y, u2.x, u2.y}};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double P2 = kLeg.a[j + h] * t * P1 - kLeg.b[j + h] * P0;
+        const double a2 = fma(kLeg.d[j + h], P1, a0), b2 = fma(kLeg.d[j + h], a1, b0);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          xr[c] = fma(cj[h][c], P2, xr[c]);
+          d1[c] = fma(cj[h][c], a2, d1[c]);
+          d2[c] = fma(cj[h][c], b2, d2[c]);
+        }
+        P0 = P1; P1 = P2; a0 = a1; a1 = a2; b0 = b1; b1 = b2;
+      }
+    }
+  };
+  bool go = true;
+#pragma unroll 1
+  for (int it = 0; it < 3; ++it) {
+    eval_r(tc);
+    const double g = xr[0] * d1[0] + xr[1] * d1[1] + xr[2] * d1[2];
+    const double gp = (d1[0] * d1[0] + xr[0] * d2[0]) + (d1[1] * d1[1] + xr[1] * d2[1]) + (d1[2] * d1[2] + xr[2] * d2[2]);
+    go = go && (gp > 0);
+    if (go) tc -= g * rcp_nr(gp);
+  }
+  eval_r(tc);
+  const double f = xr[0] * xr[0] + xr[1] * xr[1] + xr[2] * xr[2], xp2 = d1[0] * d1[0] + d1[1] * d1[1] + d1[2] * d1[2];
+  double dd = (d1[0] * d1[0] + xr[0] * d2[0]) + (d1[1] * d1[1] + xr[1] * d2[1]) + (d1[2] * d1[2] + xr[2] * d2[2]);
+  if (!(dd > 0)) dd = xp2;
+  return mk(tc, sqrt_nn(f * rcp_nr(dd > 0 ? dd : 1.0)));
+}
+
+// One complex Newton step t <- t - F / F', F(t) = (x(t) - r').(x(t) - r'); returns the step dt.
+template <int Q>
+__device__ __forceinline__ cd newton_step(const double2 *__restrict__ C2, const double (&rc)[3], cd tz) {
+  cd P0 = mk(1, 0), P1 = tz, a0 = mk(0, 0), a1 = mk(1, 0), xv[3], xd[3];
+  {
+    const double2 u0 = __ldg(C2), u1 = __ldg(C2 + 1), u2 = __ldg(C2 + 2);
+    const double c0[3] = {u0.x, u0.y, u1.x}, c1[3] = {u1.y, u2.x, u2.y};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      xv[c] = mk(fma(c1[c], tz.x, c0[c]) - rc[c], c1[c] * tz.y);
+      xd[c] = mk(c1[c], 0);
+    }
+  }
+#pragma unroll 1
+  for (int j = 1; j + 1 < Q; j += 2) {
+    const double2 *cp = C2 + 3 * ((j + 1) >> 1);
+    const double2 u0 = __ldg(cp), u1 = __ldg(cp + 1), u2 = __ldg(cp + 2);
+    const double cj[2][3] = {{u0.x, u0.y, u1.x}, {u1.y, u2.x, u2.y}};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double ca = kLeg.a[j + h], cb = kLeg.b[j + h], dj = kLeg.d[j + h];
+      const cd tp = tz * P1;
+      const cd P2 = mk(ca * tp.x - cb * P0.x, ca * tp.y - cb * P0.y);
+      const cd a2 = mk(fma(dj, P1.x, a0.x), fma(dj, P1.y, a0.y));
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        xv[c] = mk(fma(cj[h][c], P2.x, xv[c].x), fma(cj[h][c], P2.y, xv[c].y));
+        xd[c] = mk(fma(cj[h][c], a2.x, xd[c].x), fma(cj[h][c], a2.y, xd[c].y));
+      }
+      P0 = P1; P1 = P2; a0 = a1; a1 = a2;
+    }
+  }
+  cd F = mk(0, 0), Fp = mk(0, 0);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) { F = F + xv[c] * xv[c]; Fp = Fp + xv[c] * xd[c]; }
+  return cdiv(F, 2.0 * Fp);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kNewtonThreads, 4)
+    k_newton(int64_t np_, const PairSetup *__restrict__ setup, const double *__restrict__ fit, double rho0,
+             double2 *__restrict__ T0, uint8_t *__restrict__ EF, unsigned long long *__restrict__ counter) {
+  using D = Dims<P>;
+  using L = Layout<P>;
+  constexpr int Q = D::Q;
+  __shared__ double slots[kNewtonThreads / 32][32][kNewtonSlot];   // tz, r'[3], w, patch (odd stride)
+  const int lane = threadIdx.x & 31;
+  double (*sl)[kNewtonSlot] = slots[threadIdx.x >> 5];
+  const long long total = 3 * np_;
+  auto coef = [&](long long w, int Pp) {
+    const int e = w >= 2 * np_ ? 2 : (w >= np_ ? 1 : 0);
+    return reinterpret_cast<const double2 *>(fit + (int64_t)Pp * L::STRIDE + L::CM + e * Q * 3);
+  };
+  // lane state: the edge being iterated
+  bool have = false;
+  long long w = 0;
+  cd tz = mk(0, 0);
+  double rc[3] = {0, 0, 0}, dt2_prev = 0;
+  const double2 *C2 = nullptr;
+  int it = 0;
+  int avail = 0, head = 0;   // warp-uniform: unclaimed slots of the current batch
+  bool more = true;
+  for (;;) {
+    unsigned need = __ballot_sync(0xffffffffu, !have);
+    while (need && (avail > 0 || more)) {
+      if (avail == 0) {   // draw the next batch and compute its starting guesses (all lanes together)
+        long long b = 0;
+        if (lane == 0) b = (long long)atomicAdd(counter, 32ull);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b >= total) { more = false; break; }
+        avail = (int)(total - b < 32 ? total - b : 32);
+        head = 0;
+        __syncwarp();
+        if (lane < avail) {
+          const long long wn = b + lane;
+          const int e = wn >= 2 * np_ ? 2 : (wn >= np_ ? 1 : 0);
+          const PairSetup &q = setup[wn - e * np_];
+          const double r3[3] = {q.rp[0], q.rp[1], q.rp[2]};
+          const int Pp = q.Pp;
+          const cd g = newton_guess<Q>(coef(wn, Pp), r3);
+          double *o = sl[lane];
+          o[0] = g.x; o[1] = g.y; o[2] = r3[0]; o[3] = r3[1]; o[4] = r3[2];
+          o[5] = __longlong_as_double(wn); o[6] = __longlong_as_double((long long)Pp);
+        }
+        __syncwarp();
+      }
+      const int rank = __popc(need & ((1u << lane) - 1u));
+      if (!have && rank < avail) {
+        const double *o = sl[head + rank];
+        tz = mk(o[0], o[1]);
+        rc[0] = o[2]; rc[1] = o[3]; rc[2] = o[4];
+        w = __double_as_longlong(o[5]);
+        C2 = coef(w, (int)__double_as_longlong(o[6]));
+        have = true;
+        it = 0;
+        dt2_prev = 0;
+      }
+      const int nt = min(__popc(need), avail);
+      head += nt;
+      avail -= nt;
+      need = __ballot_sync(0xffffffffu, !have);
+    }
+    if (!__any_sync(0xffffffffu, have)) break;
+    if (have) {
+      const cd dt = newton_step<Q>(C2, rc, tz);
+      tz = tz - dt;
+      bool conv = false;
+      // |dt| < 1e-15 (1 + |t|) and |dt| < 1e-3 |t| compared as squares (no hypot)
+      const double dt2 = dt.x * dt.x + dt.y * dt.y, tz2 = tz.x * tz.x + tz.y * tz.y;
+      const double tza = tz2 > 0 ? tz2 * rsqrt_nr(tz2) : 0.0;
+      const double tol2 = 1e-30 * (1.0 + tza) * (1.0 + tza);
+      if (dt2 < tol2) conv = true;
+      // A12'': quadratic regime and the predicted next step |dt|^3 / |dt_prev|^2 below the tolerance
+      else if (dt2_prev > 0 && dt2 < 1e-2 * dt2_prev && dt2 * dt2 * dt2 < tol2 * dt2_prev * dt2_prev) conv = true;
+      // A12': root certainly outside the swap ellipse
+      else if (it >= 1 && dt2 < 1e-6 * tz2 && bernstein_rho(tz.x, tz.y) > 2.0 * rho0) conv = true;
+      dt2_prev = dt2;
+      ++it;
+      if (conv || it == 20) {
+        if (tz.y < 0) tz.y = -tz.y;
+        conv = conv && isfinite(tz.x) && isfinite(tz.y);
+        const double rho = bernstein_rho(tz.x, tz.y);
+        T0[w] = make_double2(tz.x, tz.y);
+        EF[w] = (uint8_t)((conv ? 1 : 0) | ((conv && rho < rho0) ? 2 : 0) | ((rho >= kRhoDirect) ? 4 : 0));
+        have = false;
+      }
+    }
+  }
+}
+
 // Per-pair state of k_pair_edge (shared memory; one per pair of the CTA round).
 template <int P>
 struct PairState {
@@ -380,15 +603,17 @@ struct WarpScr {
   double r13[2][kNDirect];
 };
 
+// p <= 8: two CTAs per SM (shared memory 113 KB at p = 8), so at most 128 registers
 template <int P, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
+__global__ void __launch_bounds__(WPB * 32, P <= 8 ? 2 : 1)
     k_pair_edge(int64_t sA, int64_t sB, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt,
                 int64_t kbase, const int32_t *__restrict__ pair_patch, const double *__restrict__ fit,
                 const double *__restrict__ tx, const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
                 const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Arow,
                 double *__restrict__ Xrow, int32_t *__restrict__ pstat, int64_t obase,
                 unsigned long long *__restrict__ swapcnt, const double *__restrict__ trtab,
-                const PairSetup *__restrict__ setup, int want_dp) {
+                const PairSetup *__restrict__ setup, int want_dp, const double2 *__restrict__ T0,
+                const uint8_t *__restrict__ EF) {
   using D = Dims<P>;
   const double *wS = trtab + TrCfg<P>::WS;
   using L = Layout<P>;
@@ -398,15 +623,15 @@ __global__ void __launch_bounds__(WPB * 32)
   double *sU = smem;                  // [Q][Q]
   double *stgl = sU + Q * Q, *swgl = stgl + Q;
   double *sxo = swgl + Q, *swo = sxo + n_omega;
-  double *shc = swo + n_omega;        // [HC_SIZE]
-  double *sxdp = shc + HC_SIZE;       // [kNDirect][Q] powers of the direct-rule nodes (reading A11')
-  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + HC_SIZE + kNDirect * Q;
+  double *shc = swo + n_omega;        // [hc_size(P)]
+  double *sxdp = shc + hc_size(P);       // [kNDirect][Q] powers of the direct-rule nodes (reading A11')
+  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + hc_size(P) + kNDirect * Q;
   tab_doubles = (tab_doubles + 1) & ~1;
   PairState<P> *pst = reinterpret_cast<PairState<P> *>(smem + tab_doubles);
   __shared__ int nsw;                          // swap edges of the round (CTA-wide list, phases 2b and 4)
   __shared__ int swl[WPB * kPPW * 3];
   WarpScr<P> *wscr = reinterpret_cast<WarpScr<P> *>(pst + WPB * kPPW);
-  for (int i = threadIdx.x; i < HC_SIZE; i += blockDim.x) shc[i] = T.hc[i];
+  for (int i = threadIdx.x; i < hc_size(P); i += blockDim.x) shc[i] = T.hc[i];
   for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) sU[i] = T.U[i];
   for (int i = threadIdx.x; i < Q; i += blockDim.x) { stgl[i] = T.tgl[i]; swgl[i] = T.wgl[i]; }
   for (int i = threadIdx.x; i < n_omega; i += blockDim.x) { sxo[i] = T.xo[i]; swo[i] = T.wo[i]; }
@@ -537,76 +762,21 @@ __global__ void __launch_bounds__(WPB * 32)
       Xrow[(base + warp * kPPW + lane - sA) * XR::STRIDE + XR::NU + 3] = __longlong_as_double(mine[lane].aslot);
     __syncwarp();   // next phase only reads this warp's pairs
     RRQ_PHASE_MARK(0);
-    // ---------------- phase 2: t0 per edge (reading A12, A12'), lanes (pair, edge, comp) = 27 lanes
-    {
-      const int L27 = lane < 27 ? lane : 26, pp = L27 / 9, e = (L27 % 9) / 3, c = L27 % 3, base3 = 9 * pp + 3 * e;
-      PairState<P> &ps = mine[pp];
-      const bool act = ps.active;
-      const double *C = fit + (int64_t)(act ? ps.Pp : 0) * L::STRIDE + L::CM + e * Q * 3;
-      const double rc = act ? ps.rp[c] : 0.0;
-      double Cl[Q];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) Cl[q] = act ? C[q * 3 + c] : 0.0;
-      double v = 0, A = 0;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) { v += Cl[q]; A += (q & 1) ? -Cl[q] : Cl[q]; }
-      double d1, d2;
-      const double ab = v - A, ar = rc - A;
-      const double abab = tri_sum(ab * ab, base3);
-      double tc = -1.0 + 2.0 * tri_sum(ar * ab, base3) / (abab > 0 ? abab : 1.0);
-      bool go = true;
-      for (int it = 0; it < 3; ++it) {
-        leg_r<Q>(Cl, tc, v, d1, d2);
-        const double xr = v - rc;
-        const double g = tri_sum(xr * d1, base3), gp = tri_sum(d1 * d1 + xr * d2, base3);
-        go = go && (gp > 0);
-        if (go) tc -= g * rcp_nr(gp);
-      }
-      leg_r<Q>(Cl, tc, v, d1, d2);
-      const double xr = v - rc;
-      const double f = tri_sum(xr * xr, base3), xp2 = tri_sum(d1 * d1, base3);
-      double dd = tri_sum(d1 * d1 + xr * d2, base3);
-      if (!(dd > 0)) dd = xp2;
-      cd tz = mk(tc, sqrt_nn(f * rcp_nr(dd > 0 ? dd : 1.0)));
-      bool conv = !act;
-      double dt2_prev = 0.0;
-      for (int it = 0; it < 20; ++it) {
-        cd xv, xd;
-        leg_c<Q>(Cl, tz, xv, xd);
-        const cd xrr = xv - mk(rc, 0);
-        const cd sq = xrr * xrr, pr = xrr * xd;
-        const cd F = mk(tri_sum(sq.x, base3), tri_sum(sq.y, base3));
-        const cd Fp = 2.0 * mk(tri_sum(pr.x, base3), tri_sum(pr.y, base3));
-        if (!conv) {
-          const cd dt = cdiv(F, Fp);
-          tz = tz - dt;
-          // |dt| < 1e-15 (1 + |t|) and |dt| < 1e-3 |t| compared as squares (no hypot)
-          const double dt2 = dt.x * dt.x + dt.y * dt.y, tz2 = tz.x * tz.x + tz.y * tz.y;
-          const double tza = tz2 > 0 ? tz2 * rsqrt_nr(tz2) : 0.0;
-          const double tol2 = 1e-30 * (1.0 + tza) * (1.0 + tza);
-          if (dt2 < tol2) conv = true;
-          // quadratic convergence: the step after this one is ~C |dt|^2 with C ~ |dt| / |dt_prev|^2, so
-          // once (|dt|^3 / |dt_prev|^2)^2 < tol^2 the updated t is already within the tolerance (saves the
-          // confirming iteration; t agrees with the full iteration to rounding)
-          else if (dt2_prev > 0 && dt2 < 1e-2 * dt2_prev && dt2 * dt2 * dt2 < tol2 * dt2_prev * dt2_prev) conv = true;
-          else if (it >= 1 && dt2 < 1e-6 * tz2 && bernstein_rho(tz.x, tz.y) > 2.0 * rho0)
-            conv = true;   // reading A12': root certainly outside the swap ellipse
-          dt2_prev = dt2;
-        }
-        if (__all_sync(0xffffffffu, conv || lane >= 27)) break;
-      }
-      if (tz.y < 0) tz.y = -tz.y;
-      conv = conv && isfinite(tz.x) && isfinite(tz.y);
-      if (lane < 27 && c == 0 && act) {
+    // ---------------- phase 2: t0 and the regime flags of the warp's 9 edges (k_newton's output)
+    if (lane < 3 * kPPW) {
+      PairState<P> &ps = mine[lane / 3];
+      if (ps.active) {
+        const int e = lane % 3;
+        const int64_t w = e * (sB - sA) + (base + warp * kPPW + lane / 3 - sA);
+        const double2 tz = T0[w];
+        const int fl = EF[w];
         ps.t0[e][0] = tz.x;
         ps.t0[e][1] = tz.y;
-        ps.conv[e] = conv;
-        const double rho = bernstein_rho(tz.x, tz.y);
-        ps.swap[e] = conv && rho < rho0;
-        ps.direct[e] = rho >= kRhoDirect;
+        ps.conv[e] = fl & 1;
+        ps.swap[e] = (fl >> 1) & 1;
+        ps.direct[e] = (fl >> 2) & 1;
       }
     }
-    __syncwarp();
     // the round's swap edges -> CTA-wide list (phases 2b and 4)
     __syncwarp();
     if (lane < 3 * kPPW) {
@@ -1205,11 +1375,13 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
         }
       }
     }
-    // j = 1 theta terms of this lane's outputs c = lane, lane + 32 (no lambda part: C_1 = 0; |m - k| > l - 1
+    // j = 1 theta terms of this lane's outputs c = lane, lane + 32, ... (no lambda part: C_1 = 0; |m - k| > l - 1
     // reads the zero S' entry), taken before the slots overwrite the buffer
-    double T1[2] = {0, 0};
+    constexpr int NH = (NP + 31) / 32;   // outputs per lane
+    double T1[NH];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NH; ++h) {
+      T1[h] = 0;
       const int c = lane + 32 * h;
       if (c >= NP) continue;
       const uint32_t ci = cinfo[c];
@@ -1243,7 +1415,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
     double *Zt = Zrow + (aslot >> 5) * CC::ZBLK;
     const int zr = (int)(aslot & 31);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NH; ++h) {
       const int c = lane + 32 * h;
       if (c >= NP) continue;
       const uint32_t ci = cinfo[c];

@@ -43,7 +43,7 @@ struct rrq_ctx_s {
   // k_pair_edge's outputs are double-buffered (set = sub-chunk parity) so that the producer stream (k_pair_setup,
   // k_pair_edge of sub-chunk i+1) runs concurrently with the consumer stream (k_qmap, k_translate, k_contract of
   // sub-chunk i): the edge kernel is FP64-latency bound and the GEMM kernels leave the FP64 pipe ~40 % idle.
-  Buf Arow[2], Xrow[2], psetup[2], cpair[2], Qrow, ipatch;
+  Buf Arow[2], Xrow[2], psetup[2], cpair[2], et0[2], Qrow, ipatch;
   cudaStream_t st2 = nullptr;                      // producer stream (created on first use)
   cudaEvent_t ev_edge[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_fork = nullptr, ev_join = nullptr;
   bool overlap = true;                             // RRQ_NO_OVERLAP=1 runs everything on the caller's stream
@@ -57,8 +57,8 @@ struct rrq_ctx_s {
   size_t hmap_n = 0;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
-  double t_ms[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int64_t t_n[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double t_ms[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t t_n[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   int64_t stats[2] = {0, 0};
   struct Pend {
     int stage;
@@ -228,10 +228,12 @@ static std::vector<double> make_trtab() {
   for (int e = 0; e <= D::NQ; ++e) pq[e] = e;
   for (int e = 0; e <= ZE; ++e) ps[e] = e;
   auto mult = [](const int *ent, const int *grp, int n) {
-    uint64_t m[8][2] = {};
+    uint64_t m[8][4] = {};   // entries < 256 (p = 14: p^2 + 1 = 197)
     for (int i = 0; i < n; ++i) m[grp[i]][ent[i] >> 6] |= 1ull << (ent[i] & 63);
     int best = 1;
-    for (int g = 0; g < 8; ++g) best = std::max(best, __builtin_popcountll(m[g][0]) + __builtin_popcountll(m[g][1]));
+    for (int g = 0; g < 8; ++g)
+      best = std::max(best, __builtin_popcountll(m[g][0]) + __builtin_popcountll(m[g][1]) + __builtin_popcountll(m[g][2]) +
+                                __builtin_popcountll(m[g][3]));
     return best;
   };
   auto cost = [&]() {
@@ -279,7 +281,7 @@ static std::vector<double> make_trtab() {
       const Step &s = lanes[l2][t];
       w[t * 32 + l2] = (uint32_t)pq[s.qe] | (uint32_t)ps[s.se] << 7 | (uint32_t)s.flags;
       uint32_t pw = 0;
-      for (int i = 0; i < WD - 1; ++i) pw |= (uint32_t)ps[s.pe[i]] << (7 * i);
+      for (int i = 0; i < WD - 1; ++i) pw |= (uint32_t)ps[s.pe[i]] << (C::SEB * i);
       w[ST * 32 + t * 32 + l2] = pw;
     }
   uint32_t *ci = w.data() + 2 * ST * 32;
@@ -326,7 +328,7 @@ static std::vector<double> make_trtab_p(int p) {
   }
 }
 
-static cudaError_t set_kernel_attributes(int p);
+static cudaError_t set_kernel_attributes(int p, int n_omega);
 
 // Every entry point runs with the device the context was created on (its tables, scratch and the kernels'
 // shared-memory attributes belong to that device).
@@ -438,7 +440,7 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   }
   // dynamic shared-memory opt-ins of this p's kernels, on this context's device (per device, per context:
   // no process-global state, so contexts on several devices or host threads do not race)
-  if (set_kernel_attributes(p.p) != cudaSuccess) {
+  if (set_kernel_attributes(p.p, p.n_omega) != cudaSuccess) {
     g_create_err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(cudaGetLastError());
     rrq_destroy(c);
     return RRQ_ERR_CUDA;
@@ -463,7 +465,7 @@ void rrq_destroy(rrq_ctx c) {
   if (c->st2) cudaStreamDestroy(c->st2);
   for (cudaEvent_t e : {c->ev_edge[0], c->ev_edge[1], c->ev_free[0], c->ev_free[1], c->ev_fork, c->ev_join})
     if (e) cudaEventDestroy(e);
-  for (auto *b : {&c->Arow[0], &c->Arow[1], &c->Xrow[0], &c->Xrow[1], &c->psetup[0], &c->psetup[1], &c->cpair[0],
+  for (auto *b : {&c->Arow[0], &c->Arow[1], &c->Xrow[0], &c->Xrow[1], &c->psetup[0], &c->psetup[1], &c->et0[0], &c->et0[1], &c->cpair[0],
                   &c->cpair[1], &c->Qrow, &c->ipatch, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
                   &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
     if (b->p) cudaFree(b->p);
@@ -537,7 +539,7 @@ rrq_status rrq_set_overlap(rrq_ctx c, int enable) {
 rrq_status rrq_reset_timing(rrq_ctx c) {
   if (!c) return RRQ_ERR_INVALID_ARG;
   t_flush(c);
-  for (int i = 0; i < 7; ++i) { c->t_ms[i] = 0; c->t_n[i] = 0; }
+  for (int i = 0; i < RRQ_NSTAGES; ++i) { c->t_ms[i] = 0; c->t_n[i] = 0; }
   c->stats[0] = c->stats[1] = 0;
   return RRQ_OK;
 }
@@ -731,7 +733,7 @@ constexpr int kWPB = P >= 14 ? 6 : 8;
 template <int P>
 static size_t edge_smem(int n_omega) {
   using D = Dims<P>;
-  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + HC_SIZE + kNDirect * D::Q;
+  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + hc_size(P) + kNDirect * D::Q;
   tab = (tab + 1) & ~1;
   return (size_t)tab * sizeof(double) + kWPB<P> * kPPW * sizeof(PairState<P>) + kWPB<P> * sizeof(WarpScr<P>);
 }
@@ -808,7 +810,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   // ---- sub-chunks: ranges of whole patches with at most `cap` pairs (scratch ~24 KB per pair at p = 8:
   // the double-buffered pair_edge outputs plus the Q and Z rows)
   const int64_t per_pair = (int64_t)(2 * (2 * D::K + XRow<P>::STRIDE) + QRow<P>::STRIDE + CC::ZBLK / CC::TP) * 8 +
-                           2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair));
+                           2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair) + 3 * (sizeof(double2) + 1));
   const int64_t cap = std::max<int64_t>(2 * TP, (int64_t)(c->scratch_bytes / per_pair));
   // sub-chunks = contiguous ranges of work items (tiles of TP pairs of one patch): whole patches while they
   // fit, a patch with more than `cap` pairs (config 5: one patch, 10M targets) split at tile boundaries
@@ -846,7 +848,8 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   for (int b = 0; b < nset; ++b)
     if (!ensure(c, c->Arow[b], (size_t)maxitems * QC::ABLK * 8) || !ensure(c, c->Xrow[b], (size_t)maxsub * XRow<P>::STRIDE * 8) ||
         !ensure(c, c->psetup[b], (size_t)maxsub * sizeof(PairSetup)) ||
-        !ensure(c, c->cpair[b], (size_t)maxsub * sizeof(ContractPair)))
+        !ensure(c, c->cpair[b], (size_t)maxsub * sizeof(ContractPair)) ||
+        !ensure(c, c->et0[b], (size_t)maxsub * 3 * (sizeof(double2) + 1) + 64))   // k_newton: t0 + flag byte per edge, batch counter
       return RRQ_ERR_CUDA;
   if (!ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxitems * CC::ZBLK * 8))
     return RRQ_ERR_CUDA;
@@ -879,12 +882,22 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
       k_pair_setup<P><<<nblk(np_, 256), 256, 0, sp>>>(sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase,
                                                        pair_patch, fit, tg->x, tg->normal, tg->self_node, tg->side,
                                                        bp<int64_t>(c->seg), bp<int64_t>(c->items), it0, ps, cp);
+      double2 *T0 = bp<double2>(c->et0[b]);
+      uint8_t *EF = reinterpret_cast<uint8_t *>(T0 + 3 * np_);
+      {
+        TScope t8(c, 8, sp);
+        unsigned long long *ctr = reinterpret_cast<unsigned long long *>(EF + ((3 * np_ + 15) / 16) * 16);
+        cudaMemsetAsync(ctr, 0, 8, sp);
+        // persistent warps drawing batches of 32 edges; 4 CTAs of 4 warps per SM
+        const unsigned gn = (unsigned)std::min<int64_t>(nblk(3 * np_, kNewtonThreads), (int64_t)c->num_sms * 4);
+        k_newton<P><<<gn, kNewtonThreads, 0, sp>>>(np_, ps, fit, c->prm.rho_swap, T0, EF, ctr);
+      }
       constexpr int WPB = kWPB<P>;
       unsigned grid = (unsigned)std::min<int64_t>((np_ + WPB * kPPW - 1) / (WPB * kPPW), (int64_t)c->num_sms * 4);
       k_pair_edge<P, WPB><<<grid, WPB * 32, edge_smem<P>(c->prm.n_omega), sp>>>(
           sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
           tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, Ar, Xr,
-          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, ps, want_dp);
+          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, ps, want_dp, T0, EF);
     }
     if ((r = cuda_check(c, "k_pair_edge"))) return r;
     if (nset == 2) {
@@ -918,7 +931,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     }
     if ((r = cuda_check(c, "k_contract"))) return r;
     if (nset == 2) cudaEventRecord(c->ev_free[b], st);
-    c->launches += 5;
+    c->launches += 6;
     c->last_sA = sA;
     c->last_np = np_;
     c->last_set = b;
@@ -1005,31 +1018,51 @@ rrq_status rrq_apply_correction(rrq_ctx c, int64_t n_rows, const int64_t *row_pt
 }
 
 
-template <int P>
-static cudaError_t set_attrs() {
-  cudaError_t e = cudaSuccess;
-  auto acc = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
-  acc(cudaFuncSetAttribute(k_edge_tables<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EdgeTabCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_patch_fit_q<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FitCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_pair_edge<P, kWPB<P>>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_smem<P>(128)));
-  acc(cudaFuncSetAttribute(k_qmap<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QmapCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_qmap<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QmapCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_translate<P, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_translate<P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TrCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_contract<P, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ContractCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_contract<P, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ContractCfg<P>::SMEM));
-  acc(cudaFuncSetAttribute(k_contract<P, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ContractCfg<P>::SMEM));
+// Dynamic shared memory limit of one kernel (the carveout is left to the driver: forcing the maximum costs
+// k_qmap 3 % through the smaller L1); RRQ_DEBUG_OCC=1 prints the resulting CTAs per SM.
+template <typename K>
+static cudaError_t set_smem(K *kern, const char *name, size_t smem, int threads) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && std::getenv("RRQ_DEBUG_OCC")) {
+    int nb = -1;
+    cudaFuncAttributes fa{};
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
+    cudaFuncGetAttributes(&fa, kern);
+    std::fprintf(stderr, "rrq: %-22s %4d threads %7zu B smem %3d regs -> %d CTAs/SM\n", name, threads, smem, fa.numRegs, nb);
+  }
   return e;
 }
 
-static cudaError_t set_kernel_attributes(int p) {
+template <int P>
+static cudaError_t set_attrs(int n_omega) {
+  cudaError_t e = cudaSuccess;
+  auto acc = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+  acc(set_smem(k_edge_tables<P>, "k_edge_tables", EdgeTabCfg<P>::SMEM, EdgeTabCfg<P>::THREADS));
+  acc(set_smem(k_patch_fit_q<P>, "k_patch_fit_q", FitCfg<P>::SMEM, 256));
+  acc(set_smem(k_pair_edge<P, kWPB<P>>, "k_pair_edge", edge_smem<P>(n_omega), kWPB<P> * 32));
+  acc(set_smem(k_qmap<P, true>, "k_qmap<dp>", QmapCfg<P>::SMEM, QmapCfg<P>::WARPS * 32));
+  acc(set_smem(k_qmap<P, false>, "k_qmap", QmapCfg<P>::SMEM, QmapCfg<P>::WARPS * 32));
+  acc(set_smem(k_translate<P, true>, "k_translate<dp>", TrCfg<P>::SMEM, TrCfg<P>::WPB * 32));
+  acc(set_smem(k_translate<P, false>, "k_translate", TrCfg<P>::SMEM, TrCfg<P>::WPB * 32));
+  acc(set_smem(k_contract<P, 15>, "k_contract<15>", ContractCfg<P>::SMEM, ContractCfg<P>::WARPS * 32));
+  acc(set_smem(k_contract<P, 3>, "k_contract<3>", ContractCfg<P>::SMEM, ContractCfg<P>::WARPS * 32));
+  acc(set_smem(k_contract<P, 0>, "k_contract<0>", ContractCfg<P>::SMEM, ContractCfg<P>::WARPS * 32));
+  if (std::getenv("RRQ_DEBUG_OCC")) {
+    int nb = -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_newton<P>, kNewtonThreads, 0);
+    std::fprintf(stderr, "rrq: %-22s -> %d CTAs/SM\n", "k_newton", nb);
+  }
+  return e;
+}
+
+static cudaError_t set_kernel_attributes(int p, int n_omega) {
   switch (p) {
-    case 4: return set_attrs<4>();
-    case 6: return set_attrs<6>();
-    case 8: return set_attrs<8>();
-    case 10: return set_attrs<10>();
-    case 12: return set_attrs<12>();
-    case 14: return set_attrs<14>();
+    case 4: return set_attrs<4>(n_omega);
+    case 6: return set_attrs<6>(n_omega);
+    case 8: return set_attrs<8>(n_omega);
+    case 10: return set_attrs<10>(n_omega);
+    case 12: return set_attrs<12>(n_omega);
+    case 14: return set_attrs<14>(n_omega);
   }
   return cudaErrorInvalidValue;
 }

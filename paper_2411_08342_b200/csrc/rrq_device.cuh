@@ -116,9 +116,12 @@ constexpr double kRhoDirect = 1.6;
 //   HC_DG + m  = sqrt((2m-1)/(2m)),  HC_SB + m = sqrt(2m+1)                                       (m <= 14)
 //   HC_RA + sidx(l,m) = (2l+1)/sqrt((l+1+m)(l+1-m)),  HC_RB + sidx(l,m) = sqrt((l+m)(l-m))/sqrt((l+1+m)(l+1-m))
 constexpr int HC_LMAX = 14;
-constexpr int HC_DC = 0, HC_DG = 3 * (HC_LMAX + 1) * (HC_LMAX + 1), HC_SB = HC_DG + HC_LMAX + 1,
-              HC_RA = HC_SB + HC_LMAX + 1, HC_RB = HC_RA + (HC_LMAX + 1) * (HC_LMAX + 2) / 2,
-              HC_SIZE = HC_RB + (HC_LMAX + 1) * (HC_LMAX + 2) / 2;
+// The l-ordered derivative block comes last, so a kernel instantiated for order P stages only the first
+// hc_size(P) entries in shared memory.
+constexpr int HC_DG = 0, HC_SB = HC_DG + HC_LMAX + 1, HC_RA = HC_SB + HC_LMAX + 1,
+              HC_RB = HC_RA + (HC_LMAX + 1) * (HC_LMAX + 2) / 2, HC_DC = HC_RB + (HC_LMAX + 1) * (HC_LMAX + 2) / 2,
+              HC_SIZE = HC_DC + 3 * (HC_LMAX + 1) * (HC_LMAX + 1);
+__host__ __device__ constexpr int hc_size(int P) { return (HC_DC + 3 * (P + 1) * (P + 1) + 1) / 2 * 2; }
 
 // R_l^m(X,Y,Z), 0 <= m <= l <= P (no Condon-Shortley phase, reading G5) by the Cartesian recurrences
 //  R_m^m = sqrt((2m-1)/(2m)) (X + iY) R_{m-1}^{m-1},  R_{m+1}^m = sqrt(2m+1) Z R_m^m,

@@ -12,4 +12,4 @@ for f in sys.argv[1:]:
     pk = {k: round(v["serial_ms_per_step"], 1) for k, v in r["per_kernel"].items()}
     print(f"{f}: {d['value']:.4e} {d['unit']} {d['ms_per_step']:.0f} ms/step build {r['build_stage_frac']:.3f} "
           f"{r['kernel']} {r['frac']:.3f} kernels={d['config']['kernels']} serial={pk} fit={d['stages_ms_per_step']['patch_fit']:.0f}"
-          f" clocks={d['clocks'].get('sm_mhz')}")
+          f" clocks={d['clocks'].get('sm_mhz')} newton_serial={d.get('serial_stages_ms', {}).get('newton')}")
