@@ -157,7 +157,8 @@ int64_t rrq_launch_count(rrq_ctx ctx);
 /* Device-time accounting.  When enabled, every launch of the build is bracketed by CUDA events
  * recorded on the stream it runs on; rrq_get_timing returns the accumulated milliseconds and launch
  * counts per stage: [0] near list, [1] patch fit (geometry, edge tables, QR), [2] k_pair_setup +
- * k_newton + k_pair_edge (Steps 4-5, scalar line integrals, I[gamma]; [8] = k_newton's share of it), [3] k_qmap (Step 6 line-integral maps,
+ * k_newton + k_edge_lines + k_target_gamma (Steps 4-5, scalar line integrals, I[gamma]; [8], [9], [10] = the
+ * shares of k_newton, k_edge_lines, k_target_gamma), [3] k_qmap (Step 6 line-integral maps,
  * DMMA GEMM), [4] k_translate (Step 7), [5] k_contract (Step 8 DMMA GEMMs + smooth subtraction +
  * store), [6] build plumbing (pair permutation, work items), [7] whole rrq_build_correction calls
  * (caller's stream).  rrq_build_correction runs stage [2] of sub-chunk i+1 on an internal stream
@@ -166,7 +167,7 @@ int64_t rrq_launch_count(rrq_ctx ctx);
  * whole patches (or tile ranges of one patch) within a scratch budget of 24 GB (RRQ_SCRATCH_BYTES
  * overrides it; a test hook).  stats[0] = pairs built, stats[1] =
  * swap-regime edges (reading A5).  The build synchronises the stream before the events are read. */
-#define RRQ_NSTAGES 9
+#define RRQ_NSTAGES 11
 rrq_status rrq_set_timing(rrq_ctx ctx, int enable);
 rrq_status rrq_get_timing(rrq_ctx ctx, double ms[RRQ_NSTAGES], int64_t launches[RRQ_NSTAGES], int64_t stats[2]);
 rrq_status rrq_reset_timing(rrq_ctx ctx);
@@ -181,8 +182,8 @@ rrq_status rrq_set_overlap(rrq_ctx ctx, int enable);
  * c-layout.  At most max_pairs rows; returns the row count in *n_out. */
 rrq_status rrq_debug_zeta(rrq_ctx ctx, int64_t max_pairs, int64_t *perm, double *Z, int64_t *n_out);
 
-/* Profiling hook: SM cycles spent by k_pair_edge in each of its phases (harmonics, Newton + model
- * integrals, weights, Omega_0 sinh rule, I[gamma]), summed over CTAs, into HOST out[8]; reset if set. */
+/* Profiling hook: SM cycles spent by k_edge_lines in each of its steps ([0] pair load + swap-edge list,
+ * [1] model integrals + Omega_0 sinh rule, [2] weights), summed over CTAs, into HOST out[8]; reset if set. */
 rrq_status rrq_debug_phase_cycles(rrq_ctx ctx, uint64_t out[8], int reset);
 
 /* Profiling hook: SM cycles spent by k_patch_fit_q in its phases (node tables, quaternion QR, Q^H e_c,

@@ -1,11 +1,16 @@
 // The per-pair hot path, Steps 4-8 + smooth-rule subtraction (A14), as
-// four kernels over a sub-chunk of pairs in patch-major order (s = position in the permutation):
+// kernels over a sub-chunk of pairs in patch-major order (s = position in the permutation):
 //
-// k_pair_setup (thread per pair) + k_pair_edge (warp per 3 pairs, phase-synchronous): target frame,
-//   harmonics at the target (Step 4), per-edge Newton / regime / model integrals / SSQ weights (Step 5),
-//   the GEMM rows a = omega1 d and b = omega1 nu' - omega3 (nu'.d) d (tile-chunked for k_qmap), the scalar
-//   line integrals Omega, Omega_0 and derivatives (Step 6), and the I[gamma] part of W, dW and the
-//   S(r') Omega_0 part of Theta (Step 7).  Runs on a producer stream one sub-chunk ahead of the others.
+// Producer stream (one sub-chunk ahead of the consumer):
+// k_pair_setup (thread per pair): target frame, gauge, tile slots.
+// k_newton (lane per edge, warp work queue): the near-singular parameter t0 of every (pair, edge) and the
+//   regime flags (Step 5).
+// k_edge_lines (CTA rounds; LP lanes per pair): model integrals and SSQ weights of the swap edges, the GEMM
+//   rows a = omega1 d and b = omega1 nu' - omega3 (nu'.d) d (tile-chunked for k_qmap), the scalar line
+//   integrals Omega, Omega_0 and derivatives (Steps 5-6).
+// k_target_gamma (warp per 3 pairs): harmonics at the target (Step 4) -> translation operands S', NG', and the
+//   I[gamma] part of W, dW and the S(r') Omega_0 part of Theta (Step 7).
+// Consumer stream:
 // k_qmap (CTA per tile of 16 pairs of one patch): the line-integral maps [Q | V](pair) = a M,
 //   dQ(pair) = b M_Q as one FP64 tensor-core GEMM (mma.sync m8n8k4 f64 = DMMA) against the patch's
 //   operand M (built in k_edge_tables).
@@ -64,7 +69,7 @@ __device__ __noinline__ void model_integrals(double a, double b, double *I, doub
   }
 }
 
-// Phase profiling of k_pair_edge (SM cycles between the CTA barriers, accumulated by thread 0 of each
+// Phase profiling of k_edge_lines (SM cycles between the CTA barriers, accumulated by thread 0 of each
 // CTA; read back with rrq_debug_phase_cycles); slots 8-15: k_patch_fit_q's phases (rrq_debug_fit_cycles).
 __device__ unsigned long long g_phase_cycles[16];
 #define RRQ_PHASE_MARK(ph)                                                         \
@@ -74,7 +79,7 @@ __device__ unsigned long long g_phase_cycles[16];
     ph_t = now;                                                                    \
   }
 
-// Per-pair row of k_pair_edge's output for k_translate (doubles): the translation operands
+// Per-pair row of k_target_gamma's output for k_translate (doubles): the translation operands
 // S'^{(l',m')} = w(l',m') S^{(l',m')}(r') and NG' = w(l',m') nu'.grad S^{(l',m')} for l' < p, all m' (expanded
 // over m' < 0 by S^{(l,-m)} = (-1)^m conj S^{(l,m)}), stored per (l',m') at l'^2 + l' + m' as
 // (S'.y, S'.x, NG'.y, NG'.x); the I[gamma] parts of W and dW ([4][NP], zeta sign convention NOT applied);
@@ -234,7 +239,7 @@ __device__ __forceinline__ double tri_sum(double v, int base) {
   return a + b + c;
 }
 
-// k_qmap's tile configuration (see k_qmap); k_pair_edge writes the A rows in its tile-chunked layout.
+// k_qmap's tile configuration (see k_qmap); k_edge_lines writes the A rows in its tile-chunked layout.
 template <int P>
 struct QmapCfg {
   using D = Dims<P>;
@@ -262,7 +267,7 @@ struct QmapCfg {
 #endif
   // pipeline stages (chunks in flight); p >= 12: the stage is 37 KB (p = 12) / 73 KB (p = 14), 1 CTA per SM
   static constexpr int NST = P <= 10 ? RRQ_QMAP_NST : (P == 12 ? 4 : 2);
-  // A (the tile's 32 GEMM rows) is stored tile-chunked by k_pair_edge: chunk ch = [32 rows][KC] (ACH doubles,
+  // A (the tile's 32 GEMM rows) is stored tile-chunked by k_edge_lines: chunk ch = [32 rows][KC] (ACH doubles,
   // rows 0..15 = a-rows of the tile's pairs, 16..31 = b-rows), so a stage = [A chunk | B chunk] is two bulk
   // copies and A needs no resident shared memory.  KC = 8: the halves of rows with (r >> 1) odd are swapped
   // (k ^ 4) so a quarter-warp's A fragments fall in distinct banks.  A stage holds the larger pass's B chunk.
@@ -580,80 +585,101 @@ __global__ void __launch_bounds__(kNewtonThreads, 4)
   }
 }
 
-// Per-pair state of k_pair_edge (shared memory; one per pair of the CTA round).
+// ------------------------------------------------------------------------------------------------
+// k_edge_lines: the edge work of a pair after k_newton (Steps 5-6):
+// model integrals and SSQ weights of the swap-regime edges, the GEMM rows a = omega1 d and
+// b = omega1 nu' - omega3 (nu'.d) d (tile-chunked for k_qmap), the scalar line integrals Omega, Omega_0 and
+// their nu'-derivatives (OM, 8 doubles per pair), Omega_0 on swap edges by the sinh rule (A9).
+// CTA rounds of WPB * PPW pairs in three barrier-separated steps: (1) every warp loads its pairs' setup and
+// t0 / flags and lists the swap edges CTA-wide; (2) the model integrals (a thread per edge inside rho = 1.6,
+// a warp per edge with the 48-point rule outside) and the sinh rule (a warp per edge), drawn from the list
+// through a shared counter; (3) the weights: LP lanes per pair sweep its 3 p~ edge nodes (p = 8: a half-warp
+// per pair, one edge per sweep).
+// ------------------------------------------------------------------------------------------------
 template <int P>
-struct PairState {
+struct EdgeCfg {
   using D = Dims<P>;
-  cd R[D::NS];                 // R_l^m at (y', z', x'): S^{(l,m)}(r') for m >= 0
+  static constexpr int WPB = 8;
+  static constexpr int LP = (D::E % 32 == 0 || P > 8) ? 32 : 16;   // lanes per pair in the weights step
+  static constexpr int HW = 32 / LP;                               // pairs side by side in a warp
+  static constexpr int PPW = 2 * HW;                               // pairs per warp per round
+  static constexpr int MINB = P <= 8 ? 3 : 2;
+};
+template <int P>
+struct EdgePair {
+  using D = Dims<P>;
   double I[3][D::Q], J[3][D::Q];
   double t0[3][2];
-  double rp[3], nup[3], u3, om[8], o0e[3];
-  int64_t k, t;
-  int64_t aslot;               // PairSetup::aslot
+  double rp[3], nup[3], u3, o0e[3];
+  int64_t k, aslot;               // PairSetup::k, aslot
   int Pp, self_local, active, pad;
-  int swap[3], conv[3], direct[3];
+  int swap[3], conv[3], direct[3], pad2;
 };
-constexpr int kPPW = 3;   // pairs per warp per round (the Newton phase packs 3 x 9 = 27 lanes)
 
-// Per-warp scratch: gradient tables of the warp's pairs (phase 1 -> phase 5) and the direct-rule buffer.
+// Sums of 8 values over the LP lanes of a group (LP = 16: 8 shuffles; LP = 32: warp_sum8): on return lane L
+// holds the sum of value index ((L >> 2) & 7) (LP = 32) or ((L >> 1) & 7) (LP = 16) of its group.
+template <int LP>
+__device__ __forceinline__ double group_sum8(const double (&v)[8], int lane) {
+  if constexpr (LP == 32) {
+    return warp_sum8(v, lane);
+  } else {
+    const bool b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1;
+    double w[4], x[2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double keep = b3 ? v[4 + j] : v[j], send = b3 ? v[j] : v[4 + j];
+      w[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double keep = b2 ? w[2 + j] : w[j], send = b2 ? w[j] : w[2 + j];
+      x[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    double y = (b1 ? x[1] : x[0]) + __shfl_xor_sync(0xffffffffu, b1 ? x[0] : x[1], 2);
+    y += __shfl_xor_sync(0xffffffffu, y, 1);
+    return y;
+  }
+}
+
 template <int P>
-struct WarpScr {
+__global__ void __launch_bounds__(EdgeCfg<P>::WPB * 32, EdgeCfg<P>::MINB)
+    k_edge_lines(int64_t sA, int64_t sB, const double *__restrict__ fit, Tables T, int n_omega,
+                 double *__restrict__ Arow, double *__restrict__ OM, int32_t *__restrict__ pstat, int64_t obase,
+                 unsigned long long *__restrict__ swapcnt, const PairSetup *__restrict__ setup, int want_dp,
+                 const double2 *__restrict__ T0, const uint8_t *__restrict__ EF) {
   using D = Dims<P>;
-  cd GS[kPPW][D::NS][3];
-  double r13[2][kNDirect];
-};
-
-// p <= 8: two CTAs per SM (shared memory 113 KB at p = 8), so at most 128 registers
-template <int P, int WPB>
-__global__ void __launch_bounds__(WPB * 32, P <= 8 ? 2 : 1)
-    k_pair_edge(int64_t sA, int64_t sB, const int64_t *__restrict__ perm, const int64_t *__restrict__ ptgt,
-                int64_t kbase, const int32_t *__restrict__ pair_patch, const double *__restrict__ fit,
-                const double *__restrict__ tx, const double *__restrict__ tnorm, const int64_t *__restrict__ self_node,
-                const int8_t *__restrict__ side, Tables T, int n_omega, double rho0, double *__restrict__ Arow,
-                double *__restrict__ Xrow, int32_t *__restrict__ pstat, int64_t obase,
-                unsigned long long *__restrict__ swapcnt, const double *__restrict__ trtab,
-                const PairSetup *__restrict__ setup, int want_dp, const double2 *__restrict__ T0,
-                const uint8_t *__restrict__ EF) {
-  using D = Dims<P>;
-  const double *wS = trtab + TrCfg<P>::WS;
   using L = Layout<P>;
-  using XR = XRow<P>;
-  constexpr int Q = D::Q, E = D::E, NP = D::NP, NS = D::NS;
+  using EC = EdgeCfg<P>;
+  using QC = QmapCfg<P>;
+  constexpr int Q = D::Q, E = D::E, WPB = EC::WPB, PPW = EC::PPW, LP = EC::LP, HW = EC::HW;
   extern __shared__ double smem[];
   double *sU = smem;                  // [Q][Q]
   double *stgl = sU + Q * Q, *swgl = stgl + Q;
   double *sxo = swgl + Q, *swo = sxo + n_omega;
-  double *shc = swo + n_omega;        // [hc_size(P)]
-  double *sxdp = shc + hc_size(P);       // [kNDirect][Q] powers of the direct-rule nodes (reading A11')
-  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + hc_size(P) + kNDirect * Q;
+  double *sxdp = swo + n_omega;       // [kNDirect][Q] powers of the direct-rule nodes (reading A11')
+  double *sr13 = sxdp + kNDirect * Q; // [WPB][2][kNDirect] direct-rule scratch
+  int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + kNDirect * Q + WPB * 2 * kNDirect;
   tab_doubles = (tab_doubles + 1) & ~1;
-  PairState<P> *pst = reinterpret_cast<PairState<P> *>(smem + tab_doubles);
-  __shared__ int nsw;                          // swap edges of the round (CTA-wide list, phases 2b and 4)
-  __shared__ int swl[WPB * kPPW * 3];
-  WarpScr<P> *wscr = reinterpret_cast<WarpScr<P> *>(pst + WPB * kPPW);
-  for (int i = threadIdx.x; i < hc_size(P); i += blockDim.x) shc[i] = T.hc[i];
+  EdgePair<P> *pst = reinterpret_cast<EdgePair<P> *>(smem + tab_doubles);
+  __shared__ int nsw, wctr;                    // swap edges of the round (CTA-wide list), work counter
+  __shared__ int swl[WPB * PPW * 3];
   for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) sU[i] = T.U[i];
   for (int i = threadIdx.x; i < Q; i += blockDim.x) { stgl[i] = T.tgl[i]; swgl[i] = T.wgl[i]; }
   for (int i = threadIdx.x; i < n_omega; i += blockDim.x) { sxo[i] = T.xo[i]; swo[i] = T.wo[i]; }
   for (int i = threadIdx.x; i < kNDirect * Q; i += blockDim.x) sxdp[i] = T.xdp[i];
-  if (threadIdx.x == 0) nsw = 0;
+  if (threadIdx.x == 0) { nsw = 0; wctr = 0; }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpScr<P> &wsc = wscr[warp];
-  PairState<P> *mine = pst + warp * kPPW;      // this warp's 3 pairs
-  const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
+  double *r13 = sr13 + warp * 2 * kNDirect;
+  EdgePair<P> *mine = pst + warp * PPW;
   unsigned long long nswap = 0;
-
-  // Phase-synchronous rounds of WPB * 3 pairs: all warps of the CTA step through the phases together
-  // (__syncthreads between phases), so the SM's instruction working set is one phase (v1 was bound by
-  // instruction fetch).  Phase 2 (Newton) packs the 3 pairs of a warp into 27 lanes.
+  const int64_t np_ = sB - sA;
   long long ph_t = clock64();
-  for (int64_t base = sA + (int64_t)blockIdx.x * WPB * kPPW; base < sB; base += (int64_t)gridDim.x * WPB * kPPW) {
-    // ---------------- phase 1: frame, gauge (A2, A8), harmonics at the target (Step 4)
-    if (lane < kPPW) {   // one lane per pair: the per-pair setup from k_pair_setup
-      const int pp = lane;
-      PairState<P> &ps = mine[pp];
-      const int64_t s = base + warp * kPPW + pp;
+  for (int64_t base = sA + (int64_t)blockIdx.x * WPB * PPW; base < sB; base += (int64_t)gridDim.x * WPB * PPW) {
+    // ---------------- step 1: the warp's pairs (k_pair_setup, k_newton) and the swap-edge list
+    if (lane < PPW) {
+      EdgePair<P> &ps = mine[lane];
+      const int64_t s = base + warp * PPW + lane;
       const bool active = s < sB;
       ps.active = active;
       if (active) {
@@ -662,112 +688,12 @@ __global__ void __launch_bounds__(WPB * 32, P <= 8 ? 2 : 1)
         for (int a = 0; a < 3; ++a) { ps.rp[a] = q.rp[a]; ps.nup[a] = q.nup[a]; }
       }
     }
-    __syncwarp();
-    if constexpr (kPPW * (P + 1) <= 32) {
-      // lane = (pair, column m): R_l^m of its column in registers (the r_column recurrence), the
-      // neighbour columns m +- 1 by shuffles for grad S^{(l,m)} (grad_fast's rules), then straight away the
-      // translation operands S', NG' of (l, +-m) (XRow) and the R / grad tables phase 5 reads
-      const int pp = lane / (P + 1) < kPPW ? lane / (P + 1) : kPPW - 1, m = lane % (P + 1);
-      const bool in = lane < kPPW * (P + 1);
-      PairState<P> &ps = mine[pp];
-      const bool act = in && ps.active;
-      const double X = ps.rp[1], Y = ps.rp[2], Z = ps.rp[0], r2 = X * X + Y * Y + Z * Z;
-      cd rmm = mk(1.0, 0.0);
-      for (int k = 1; k <= m; ++k) rmm = shc[HC_DG + k] * (mk(X, Y) * rmm);
-      cd Rc[P + 1];
-#pragma unroll
-      for (int l = 0; l <= P; ++l) {
-        cd v = mk(0.0, 0.0);
-        if (l == m) v = rmm;
-        else if (l == m + 1) v = shc[HC_SB + m] * Z * rmm;
-        else if (l > m + 1)
-          v = (shc[HC_RA + sidx(l - 1, m)] * Z) * Rc[l - 1] - (shc[HC_RB + sidx(l - 1, m)] * r2) * Rc[l - 2];
-        Rc[l] = act ? v : mk(0.0, 0.0);
-        if (act && l >= m) ps.R[sidx(l, m)] = Rc[l];
-      }
-      const double nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
-      double2 *xo = reinterpret_cast<double2 *>(Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE + XR::SX);
-      const bool last = m == P;
-#pragma unroll
-      for (int l = 0; l <= P; ++l) {
-        cd g[3] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
-        if (l >= 1) {
-          const cd r0 = Rc[l - 1];
-          cd rp = mk(__shfl_down_sync(0xffffffffu, r0.x, 1), __shfl_down_sync(0xffffffffu, r0.y, 1));
-          cd rm = mk(__shfl_up_sync(0xffffffffu, r0.x, 1), __shfl_up_sync(0xffffffffu, r0.y, 1));
-          if (last) rp = mk(0.0, 0.0);               // R^{m+1} with m + 1 > l - 1
-          if (m == 0) rm = mk(-rp.x, rp.y);          // R_{l-1}^{-1} = -conj R_{l-1}^{1}
-          const double *dc = shc + HC_DC + 3 * (l * l + l + m);
-          g[0] = dc[0] * r0;
-          g[1] = 0.5 * (dc[2] * rm - dc[1] * rp);
-          const cd t = 0.5 * (dc[1] * rp + dc[2] * rm);
-          g[2] = mk(-t.y, t.x);
-        }
-        if (!act || l < m) continue;
-        cd *gs = wsc.GS[pp][sidx(l, m)];
-        gs[0] = g[0]; gs[1] = g[1]; gs[2] = g[2];
-        if (l < P) {   // translation operands, l' < p
-          const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2], r = Rc[l];
-          const double w = __ldg(wS + l * l + l + m);
-          double2 *o = xo + 2 * (l * l + l + m);
-          o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
-          o[1] = make_double2(w * ng.y, w * ng.x);
-          if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
-            const double sg = (m & 1) ? -w : w;
-            o -= 4 * m;
-            o[0] = make_double2(-sg * r.y, sg * r.x);
-            o[1] = make_double2(-sg * ng.y, sg * ng.x);
-          }
-        }
-      }
-    } else {
-      // solid harmonics of the warp's pairs: lanes (pair, column m)
-      for (int i = lane; i < kPPW * (P + 1); i += 32) {
-        PairState<P> &ps = mine[i / (P + 1)];
-        if (ps.active) r_column<P>(ps.rp[1], ps.rp[2], ps.rp[0], i % (P + 1), ps.R, shc);
-      }
-      __syncwarp();
-      // gradient tables (kept for phase 5), then the translation operands S', NG' (XRow): flat over pairs
-      for (int i = lane; i < kPPW * NS; i += 32) {
-        const int pp = i / NS, e = i % NS;
-        if (!mine[pp].active) continue;
-        const int l = tri_inv(e);   // sidx(l, 0) <= e < sidx(l + 1, 0)
-        grad_fast(mine[pp].R, l, e - sidx(l, 0), shc, wsc.GS[pp][e]);
-      }
-      __syncwarp();
-      constexpr int NSX = sidx(P, 0);   // l' < p
-      for (int i = lane; i < kPPW * NSX; i += 32) {
-        const int pp = i / NSX, e = i % NSX;
-        PairState<P> &ps = mine[pp];
-        if (!ps.active) continue;
-        const int l = tri_inv(e);   // sidx(l, 0) <= e < sidx(l + 1, 0)
-        const int m = e - sidx(l, 0);
-        const cd *g = wsc.GS[pp][e];
-        const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
-        const double w = __ldg(wS + l * l + l + m);
-        double2 *o = reinterpret_cast<double2 *>(Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m));
-        o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
-        o[1] = make_double2(w * ng.y, w * ng.x);
-        if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
-          const double sg = (m & 1) ? -w : w;
-          o -= 4 * m;
-          o[0] = make_double2(-sg * r.y, sg * r.x);
-          o[1] = make_double2(-sg * ng.y, sg * ng.x);
-        }
-      }
-    }
-    if (lane < 3 * kPPW && mine[lane / 3].active)
-      Xrow[(base + warp * kPPW + lane / 3 - sA) * XR::STRIDE + XR::NU + lane % 3] = mine[lane / 3].nup[lane % 3];
-    if (lane < kPPW && mine[lane].active)   // k_contract tile slot (k_translate writes zeta there)
-      Xrow[(base + warp * kPPW + lane - sA) * XR::STRIDE + XR::NU + 3] = __longlong_as_double(mine[lane].aslot);
-    __syncwarp();   // next phase only reads this warp's pairs
-    RRQ_PHASE_MARK(0);
-    // ---------------- phase 2: t0 and the regime flags of the warp's 9 edges (k_newton's output)
-    if (lane < 3 * kPPW) {
-      PairState<P> &ps = mine[lane / 3];
-      if (ps.active) {
-        const int e = lane % 3;
-        const int64_t w = e * (sB - sA) + (base + warp * kPPW + lane / 3 - sA);
+    if (lane >= 8 && lane < 8 + 3 * PPW) {
+      const int pp = (lane - 8) / 3, e = (lane - 8) % 3;
+      EdgePair<P> &ps = mine[pp];
+      const int64_t s = base + warp * PPW + pp;
+      if (s < sB) {
+        const int64_t w = e * np_ + (s - sA);
         const double2 tz = T0[w];
         const int fl = EF[w];
         ps.t0[e][0] = tz.x;
@@ -775,110 +701,51 @@ __global__ void __launch_bounds__(WPB * 32, P <= 8 ? 2 : 1)
         ps.conv[e] = fl & 1;
         ps.swap[e] = (fl >> 1) & 1;
         ps.direct[e] = (fl >> 2) & 1;
+        if (fl & 2) swl[atomicAdd(&nsw, 1)] = (warp * PPW + pp) * 3 + e;
       }
     }
-    // the round's swap edges -> CTA-wide list (phases 2b and 4)
-    __syncwarp();
-    if (lane < 3 * kPPW) {
-      const PairState<P> &ps = mine[lane / 3];
-      if (ps.active && ps.swap[lane % 3]) swl[atomicAdd(&nsw, 1)] = warp * 3 * kPPW + lane;
-    }
     __syncthreads();
-    // phase 2b, model integrals (reading A11 / A11'): recurrences inside rho = 1.6 (one thread per swap
-    // edge of the CTA), a 48-point rule outside (one warp per edge)
-    for (int q = threadIdx.x; q < nsw; q += blockDim.x) {
-      PairState<P> &ps = pst[swl[q] / 3];
+    RRQ_PHASE_MARK(0);
+    // ---------------- step 2: model integrals (reading A11 / A11') and Omega_0 on the swap edges by the
+    // sinh-split Gauss-Legendre rule (reading A9)
+    const int nsw_ = nsw;
+    for (int q = threadIdx.x; q < nsw_; q += blockDim.x) {
+      EdgePair<P> &ps = pst[swl[q] / 3];
       const int e = swl[q] % 3;
       if (!ps.direct[e]) model_integrals<Q>(ps.t0[e][0], fabs(ps.t0[e][1]), ps.I[e], ps.J[e]);
     }
-    for (int q = warp; q < nsw; q += WPB) {
-      PairState<P> &ps = pst[swl[q] / 3];
-      const int e = swl[q] % 3;
-      if (!ps.direct[e]) continue;
-      const double a = ps.t0[e][0], b = fabs(ps.t0[e][1]);
-      for (int j = lane; j < kNDirect; j += 32) {
-        const double xj = T.xd[j], Qv = (xj - a) * (xj - a) + b * b, rs = rsqrt(Qv);
-        const double r1 = T.wd[j] * rs;
-        wsc.r13[0][j] = r1;
-        wsc.r13[1][j] = r1 * rs * rs;
-      }
-      __syncwarp();
-      if (lane < Q) {   // two interleaved partial sums (shorter dependency chains)
-        double si0 = 0, sj0 = 0, si1 = 0, sj1 = 0;
-#pragma unroll 4
-        for (int j = 0; j < kNDirect; j += 2) {
-          const double pw0 = sxdp[j * Q + lane], pw1 = sxdp[(j + 1) * Q + lane];
-          si0 = fma(pw0, wsc.r13[0][j], si0);
-          sj0 = fma(pw0, wsc.r13[1][j], sj0);
-          si1 = fma(pw1, wsc.r13[0][j + 1], si1);
-          sj1 = fma(pw1, wsc.r13[1][j + 1], sj1);
-        }
-        ps.I[e][lane] = si0 + si1;
-        ps.J[e][lane] = sj0 + sj1;
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-    RRQ_PHASE_MARK(1);
-    // ---------------- phase 3: weights and the scalar line integrals (Step 6)
-    for (int pp = 0; pp < kPPW; ++pp) {
-      PairState<P> &ps = mine[pp];
-      if (!ps.active) continue;
-      const int64_t s = base + warp * kPPW + pp;
-      const double *blk = fit + (int64_t)ps.Pp * L::STRIDE;
-      using QC = QmapCfg<P>;
-      double *Ar = Arow + (ps.aslot >> 5) * QC::ABLK;   // k_qmap's tile block (tile-chunked rows)
-      const int arow_ = (int)(ps.aslot & 31);
-      (void)s;
-      const double rp[3] = {ps.rp[0], ps.rp[1], ps.rp[2]}, nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
-      const double u[3] = {0.0, 0.0, ps.u3};
-      double om[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // Omega_0(plain) Omega[3] dOmega_0 dOmega[3]
-      for (int kap = lane; kap < E; kap += 32) {
-        const int e = kap / Q, kk = kap % Q;
-        const double *y = blk + L::YL + 3 * kap, *tau = blk + L::TL + 3 * kap;
-        const double d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
-        const double d2 = dot3(d, d), idn = rsqrt_nr(d2), dn = d2 * idn;   // |d| > 0: targets are off the edges
-        double w1, w3;
-        if (ps.swap[e]) {
-          double mu1 = 0, mu3 = 0;
-#pragma unroll 4
-          for (int c = 0; c < Q; ++c) {
-            mu1 = fma(ps.I[e][c], sU[c * Q + kk], mu1);
-            mu3 = fma(ps.J[e][c], sU[c * Q + kk], mu3);
-          }
-          const double ta = stgl[kk] - ps.t0[e][0], tb = ps.t0[e][1];
-          const double tt2 = ta * ta + tb * tb, r1 = tt2 * rsqrt_nr(tt2) * idn;
-          w1 = mu1 * r1;
-          w3 = mu3 * r1 * r1 * r1;
-        } else {
-          w1 = swgl[kk] * idn;
-          w3 = w1 * idn * idn;
-          double dxu[3];
-          cross3(d, u, dxu);
-          om[0] += swgl[kk] * (-dot3(dxu, tau) * rcp_nr(dn * (dn + dot3(u, d))));
-        }
-        const double nd = dot3(nup, d);
-        double txd[3];
-        cross3(tau, d, txd);
-        for (int a = 0; a < 3; ++a) {
-          Ar[QC::aoff(arow_, a * E + kap)] = w1 * d[a];                                 // row a (k = axis E + kappa)
-          if (want_dp) Ar[QC::aoff(QC::TP + arow_, a * E + kap)] = w1 * nup[a] - w3 * nd * d[a];   // row b (D')
-          om[1 + a] -= w1 * tau[a];
-          om[5 + a] += w3 * nd * tau[a];
-        }
-        om[4] += w3 * dot3(nup, txd);
-      }
-      const double red = warp_sum8(om, lane);
-      if ((lane & 3) == 0) ps.om[(lane >> 2) & 7] = red;   // value index 4 b4 + 2 b3 + b2 = (lane >> 2) & 7
-    }
-    __syncwarp();   // next phase only reads this warp's pairs
-    RRQ_PHASE_MARK(2);
-    // ---------------- phase 4: Omega_0 on swap edges: sinh-split Gauss-Legendre (reading A9); the round's
-    // swap edges are spread over all warps of the CTA (warp per edge)
-    for (int q = warp; q < nsw; q += WPB) {
+    for (;;) {
+      int q = 0;
+      if (lane == 0) q = atomicAdd(&wctr, 1);
+      q = __shfl_sync(0xffffffffu, q, 0);
+      if (q >= nsw_) break;
       const int code = swl[q], e = code % 3;
-      PairState<P> &ps = pst[code / 3];
+      EdgePair<P> &ps = pst[code / 3];
       const double *blk = fit + (int64_t)ps.Pp * L::STRIDE;
+      if (ps.direct[e]) {   // 48-point rule for rho(t0) >= 1.6
+        const double a = ps.t0[e][0], b = fabs(ps.t0[e][1]);
+        for (int j = lane; j < kNDirect; j += 32) {
+          const double xj = T.xd[j], Qv = (xj - a) * (xj - a) + b * b, rs = rsqrt(Qv);
+          const double r1 = T.wd[j] * rs;
+          r13[j] = r1;
+          r13[kNDirect + j] = r1 * rs * rs;
+        }
+        __syncwarp();
+        if (lane < Q) {   // two interleaved partial sums (shorter dependency chains)
+          double si0 = 0, sj0 = 0, si1 = 0, sj1 = 0;
+#pragma unroll 4
+          for (int j = 0; j < kNDirect; j += 2) {
+            const double pw0 = sxdp[j * Q + lane], pw1 = sxdp[(j + 1) * Q + lane];
+            si0 = fma(pw0, r13[j], si0);
+            sj0 = fma(pw0, r13[kNDirect + j], sj0);
+            si1 = fma(pw1, r13[j + 1], si1);
+            sj1 = fma(pw1, r13[kNDirect + j + 1], sj1);
+          }
+          ps.I[e][lane] = si0 + si1;
+          ps.J[e][lane] = sj0 + sj1;
+        }
+        __syncwarp();
+      }
       const double rp[3] = {ps.rp[0], ps.rp[1], ps.rp[2]};
       const double u[3] = {0.0, 0.0, ps.u3};
       const double a = fmin(1.0, fmax(-1.0, ps.t0[e][0])), b = fabs(ps.t0[e][1]);
@@ -904,33 +771,257 @@ __global__ void __launch_bounds__(WPB * 32, P <= 8 ? 2 : 1)
       if (lane == 0) ps.o0e[e] = acc;
     }
     __syncthreads();
-    RRQ_PHASE_MARK(3);
-    // ---------------- phase 5: I[gamma]: (Omega_0, Omega)(0, grad S(r')), omega
-    // first; its nu'-derivative with Hess S nu'; W_gamma = -sqrt2 Im I[gamma]; the
-    // S(r') Omega_0 part of Theta (G2).  k_translate adds the lambda_1 / theta_1 parts.
-    if (lane < kPPW) {
-      PairState<P> &ps = mine[lane];
-      if (ps.active) {
-        double add = 0;
-        for (int e = 0; e < 3; ++e)
-          if (ps.swap[e]) add += ps.o0e[e];
-        ps.om[0] += add - (ps.self_local >= 0 ? 2.0 * kPi : 0.0);   // PV shift (reading A7)
+    RRQ_PHASE_MARK(1);
+    // ---------------- step 3: weights and the scalar line integrals (Step 6)
+    if (threadIdx.x == 0) { nsw = 0; wctr = 0; }   // read last in step 2; written next after the round's barrier
+    const int sub = lane % LP, grp = lane / LP;
+#pragma unroll 1
+    for (int r = 0; r < PPW / HW; ++r) {
+      const int pp = r * HW + grp;
+      EdgePair<P> &ps = mine[pp];
+      const bool act = ps.active;
+      const double *blk = fit + (int64_t)(act ? ps.Pp : 0) * L::STRIDE;
+      const int64_t aslot = act ? ps.aslot : 0;
+      double *Ar = Arow + (aslot >> 5) * QC::ABLK;   // k_qmap's tile block (tile-chunked rows)
+      const int arow_ = (int)(aslot & 31);
+      const double rp[3] = {ps.rp[0], ps.rp[1], ps.rp[2]}, nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
+      const double u[3] = {0.0, 0.0, ps.u3};
+      double om[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // Omega_0(plain) Omega[3] dOmega_0 dOmega[3]
+      if (act) {
+        for (int kap = sub; kap < E; kap += LP) {
+          const int e = kap / Q, kk = kap % Q;
+          const double *y = blk + L::YL + 3 * kap, *tau = blk + L::TL + 3 * kap;
+          const double d[3] = {rp[0] - y[0], rp[1] - y[1], rp[2] - y[2]};
+          const double d2 = dot3(d, d), idn = rsqrt_nr(d2), dn = d2 * idn;   // |d| > 0: targets are off the edges
+          double w1, w3;
+          if (ps.swap[e]) {
+            double mu1 = 0, mu3 = 0;
+#pragma unroll 4
+            for (int c = 0; c < Q; ++c) {
+              mu1 = fma(ps.I[e][c], sU[c * Q + kk], mu1);
+              mu3 = fma(ps.J[e][c], sU[c * Q + kk], mu3);
+            }
+            const double ta = stgl[kk] - ps.t0[e][0], tb = ps.t0[e][1];
+            const double tt2 = ta * ta + tb * tb, r1 = tt2 * rsqrt_nr(tt2) * idn;
+            w1 = mu1 * r1;
+            w3 = mu3 * r1 * r1 * r1;
+          } else {
+            w1 = swgl[kk] * idn;
+            w3 = w1 * idn * idn;
+            double dxu[3];
+            cross3(d, u, dxu);
+            om[0] += swgl[kk] * (-dot3(dxu, tau) * rcp_nr(dn * (dn + dot3(u, d))));
+          }
+          const double nd = dot3(nup, d);
+          double txd[3];
+          cross3(tau, d, txd);
+          for (int a = 0; a < 3; ++a) {
+            Ar[QC::aoff(arow_, a * E + kap)] = w1 * d[a];                                 // row a (k = axis E + kappa)
+            if (want_dp) Ar[QC::aoff(QC::TP + arow_, a * E + kap)] = w1 * nup[a] - w3 * nd * d[a];   // row b (D')
+            om[1 + a] -= w1 * tau[a];
+            om[5 + a] += w3 * nd * tau[a];
+          }
+          om[4] += w3 * dot3(nup, txd);
+        }
+      }
+      double red = group_sum8<LP>(om, lane);
+      const int vi = LP == 32 ? (lane >> 2) & 7 : (lane >> 1) & 7;
+      const bool writer = LP == 32 ? (lane & 3) == 0 : (lane & 1) == 0;
+      if (act && writer) {
+        if (vi == 0) {   // Omega_0: the swap edges' sinh-rule parts and the principal-value shift (reading A7)
+          for (int e = 0; e < 3; ++e)
+            if (ps.swap[e]) red += ps.o0e[e];
+          if (ps.self_local >= 0) red -= 2.0 * kPi;
+        }
+        OM[(base + warp * PPW + pp - sA) * 8 + vi] = red;
       }
     }
+    if (lane < PPW) {
+      EdgePair<P> &ps = mine[lane];
+      if (ps.active) {
+        if (pstat) pstat[ps.k - obase] = (ps.conv[0] && ps.conv[1] && ps.conv[2]) ? 0 : 1;
+        nswap += ps.swap[0] + ps.swap[1] + ps.swap[2];
+      }
+    }
+    __syncthreads();
+    RRQ_PHASE_MARK(2);
+  }
+  if (swapcnt && nswap) atomicAdd(swapcnt, nswap);
+}
+
+// ------------------------------------------------------------------------------------------------
+// k_target_gamma: the target-side harmonics of a pair (Step 4) and the I[gamma] parts (Step 7):
+// S, grad S, nu'.grad S, Hess S nu' at r' -> the translation operands S', NG' (XRow), and with the scalar
+// line integrals OM of k_edge_lines: I[gamma] = (Omega_0, Omega)(0, grad S(r')), its
+// nu'-derivative, W_gamma = -sqrt2 Im I[gamma], and the S(r') Omega_0 part of Theta (G2).
+// k_translate adds the lambda_1 / theta_1 parts.  Warp per 3 pairs, no CTA barrier: lane = (pair, column m)
+// holds R_l^m of its column in registers, neighbour columns by shuffles.
+// ------------------------------------------------------------------------------------------------
+constexpr int kPPW = 3;   // pairs per warp per round (3 x (p + 1) columns <= 32 lanes up to p = 8)
+template <int P>
+struct TgtPair {
+  using D = Dims<P>;
+  cd R[D::NS];                 // R_l^m at (y', z', x'): S^{(l,m)}(r') for m >= 0
+  double rp[3], nup[3], om[8];
+  int64_t aslot;
+  int active, pad;
+};
+template <int P>
+struct TgtCfg {
+  using D = Dims<P>;
+  static constexpr int WPB = P >= 14 ? 4 : 8;
+  static constexpr size_t PER_WARP = sizeof(cd) * kPPW * D::NS * 3 + kPPW * sizeof(TgtPair<P>);
+  static constexpr size_t SMEM = (size_t)hc_size(P) * sizeof(double) + WPB * PER_WARP;
+  static constexpr int MINB = P <= 8 ? 2 : 1;
+};
+
+template <int P>
+__global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
+    k_target_gamma(int64_t sA, int64_t sB, Tables T, double *__restrict__ Xrow, const double *__restrict__ OM,
+                   const double *__restrict__ trtab, const PairSetup *__restrict__ setup, int want_dp) {
+  using D = Dims<P>;
+  using XR = XRow<P>;
+  constexpr int NP = D::NP, NS = D::NS, WPB = TgtCfg<P>::WPB;
+  const double *wS = trtab + TrCfg<P>::WS;
+  extern __shared__ double smem[];
+  double *shc = smem;   // [hc_size(P)]
+  for (int i = threadIdx.x; i < hc_size(P); i += blockDim.x) shc[i] = T.hc[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char *wbase = reinterpret_cast<unsigned char *>(smem + hc_size(P)) + (size_t)warp * TgtCfg<P>::PER_WARP;
+  cd (*GS)[NS][3] = reinterpret_cast<cd (*)[NS][3]>(wbase);
+  TgtPair<P> *mine = reinterpret_cast<TgtPair<P> *>(wbase + sizeof(cd) * kPPW * NS * 3);
+  const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
+  for (int64_t base = sA + ((int64_t)blockIdx.x * WPB + warp) * kPPW; base < sB; base += (int64_t)gridDim.x * WPB * kPPW) {
+    if (lane < kPPW) {
+      TgtPair<P> &ps = mine[lane];
+      const int64_t s = base + lane;
+      const bool active = s < sB;
+      ps.active = active;
+      if (active) {
+        const PairSetup &q = setup[s - sA];
+        ps.aslot = q.aslot;
+        for (int a = 0; a < 3; ++a) { ps.rp[a] = q.rp[a]; ps.nup[a] = q.nup[a]; }
+      }
+    }
+    if (lane >= 8 && lane < 8 + 8 * kPPW) {
+      const int pp = (lane - 8) >> 3, i = (lane - 8) & 7;
+      if (base + pp < sB) mine[pp].om[i] = OM[(base + pp - sA) * 8 + i];
+    }
     __syncwarp();
+    if constexpr (kPPW * (P + 1) <= 32) {
+      // lane = (pair, column m): R_l^m of its column in registers (the r_column recurrence), the
+      // neighbour columns m +- 1 by shuffles for grad S^{(l,m)} (grad_fast's rules), then straight away the
+      // translation operands S', NG' of (l, +-m) (XRow) and the R / grad tables the gamma step reads
+      const int pp = lane / (P + 1) < kPPW ? lane / (P + 1) : kPPW - 1, m = lane % (P + 1);
+      const bool in = lane < kPPW * (P + 1);
+      TgtPair<P> &ps = mine[pp];
+      const bool act = in && ps.active;
+      const double X = ps.rp[1], Y = ps.rp[2], Z = ps.rp[0], r2 = X * X + Y * Y + Z * Z;
+      cd rmm = mk(1.0, 0.0);
+      for (int k = 1; k <= m; ++k) rmm = shc[HC_DG + k] * (mk(X, Y) * rmm);
+      cd Rc[P + 1];
+#pragma unroll
+      for (int l = 0; l <= P; ++l) {
+        cd v = mk(0.0, 0.0);
+        if (l == m) v = rmm;
+        else if (l == m + 1) v = shc[HC_SB + m] * Z * rmm;
+        else if (l > m + 1)
+          v = (shc[HC_RA + sidx(l - 1, m)] * Z) * Rc[l - 1] - (shc[HC_RB + sidx(l - 1, m)] * r2) * Rc[l - 2];
+        Rc[l] = act ? v : mk(0.0, 0.0);
+        if (act && l >= m) ps.R[sidx(l, m)] = Rc[l];
+      }
+      const double nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
+      double2 *xo = reinterpret_cast<double2 *>(Xrow + (base + pp - sA) * XR::STRIDE + XR::SX);
+      const bool last = m == P;
+#pragma unroll
+      for (int l = 0; l <= P; ++l) {
+        cd g[3] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
+        if (l >= 1) {
+          const cd r0 = Rc[l - 1];
+          cd rp = mk(__shfl_down_sync(0xffffffffu, r0.x, 1), __shfl_down_sync(0xffffffffu, r0.y, 1));
+          cd rm = mk(__shfl_up_sync(0xffffffffu, r0.x, 1), __shfl_up_sync(0xffffffffu, r0.y, 1));
+          if (last) rp = mk(0.0, 0.0);               // R^{m+1} with m + 1 > l - 1
+          if (m == 0) rm = mk(-rp.x, rp.y);          // R_{l-1}^{-1} = -conj R_{l-1}^{1}
+          const double *dc = shc + HC_DC + 3 * (l * l + l + m);
+          g[0] = dc[0] * r0;
+          g[1] = 0.5 * (dc[2] * rm - dc[1] * rp);
+          const cd t = 0.5 * (dc[1] * rp + dc[2] * rm);
+          g[2] = mk(-t.y, t.x);
+        }
+        if (!act || l < m) continue;
+        cd *gs = GS[pp][sidx(l, m)];
+        gs[0] = g[0]; gs[1] = g[1]; gs[2] = g[2];
+        if (l < P) {   // translation operands, l' < p
+          const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2], r = Rc[l];
+          const double w = __ldg(wS + l * l + l + m);
+          double2 *o = xo + 2 * (l * l + l + m);
+          o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
+          o[1] = make_double2(w * ng.y, w * ng.x);
+          if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
+            const double sg = (m & 1) ? -w : w;
+            o -= 4 * m;
+            o[0] = make_double2(-sg * r.y, sg * r.x);
+            o[1] = make_double2(-sg * ng.y, sg * ng.x);
+          }
+        }
+      }
+    } else {
+      // solid harmonics of the warp's pairs: lanes (pair, column m)
+      for (int i = lane; i < kPPW * (P + 1); i += 32) {
+        TgtPair<P> &ps = mine[i / (P + 1)];
+        if (ps.active) r_column<P>(ps.rp[1], ps.rp[2], ps.rp[0], i % (P + 1), ps.R, shc);
+      }
+      __syncwarp();
+      // gradient tables (kept for the gamma step), then the translation operands S', NG' (XRow): flat over pairs
+      for (int i = lane; i < kPPW * NS; i += 32) {
+        const int pp = i / NS, e = i % NS;
+        if (!mine[pp].active) continue;
+        const int l = tri_inv(e);   // sidx(l, 0) <= e < sidx(l + 1, 0)
+        grad_fast(mine[pp].R, l, e - sidx(l, 0), shc, GS[pp][e]);
+      }
+      __syncwarp();
+      constexpr int NSX = sidx(P, 0);   // l' < p
+      for (int i = lane; i < kPPW * NSX; i += 32) {
+        const int pp = i / NSX, e = i % NSX;
+        TgtPair<P> &ps = mine[pp];
+        if (!ps.active) continue;
+        const int l = tri_inv(e);   // sidx(l, 0) <= e < sidx(l + 1, 0)
+        const int m = e - sidx(l, 0);
+        const cd *g = GS[pp][e];
+        const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
+        const double w = __ldg(wS + l * l + l + m);
+        double2 *o = reinterpret_cast<double2 *>(Xrow + (base + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m));
+        o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
+        o[1] = make_double2(w * ng.y, w * ng.x);
+        if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
+          const double sg = (m & 1) ? -w : w;
+          o -= 4 * m;
+          o[0] = make_double2(-sg * r.y, sg * r.x);
+          o[1] = make_double2(-sg * ng.y, sg * ng.x);
+        }
+      }
+    }
+    if (lane < 3 * kPPW && mine[lane / 3].active)
+      Xrow[(base + lane / 3 - sA) * XR::STRIDE + XR::NU + lane % 3] = mine[lane / 3].nup[lane % 3];
+    if (lane < kPPW && mine[lane].active)   // k_contract tile slot (k_translate writes zeta there)
+      Xrow[(base + lane - sA) * XR::STRIDE + XR::NU + 3] = __longlong_as_double(mine[lane].aslot);
+    __syncwarp();
+    // ---------------- I[gamma]: (Omega_0, Omega)(0, grad S(r')), omega first; its nu'-derivative with
+    // Hess S nu'; W_gamma = -sqrt2 Im I[gamma]; the S(r') Omega_0 part of Theta
     for (int i = lane; i < kPPW * NP; i += 32) {
       const int pp = i / NP, c = i % NP;
-      PairState<P> &ps = mine[pp];
+      TgtPair<P> &ps = mine[pp];
       if (!ps.active) continue;
-      double *X = Xrow + (base + warp * kPPW + pp - sA) * XR::STRIDE;
+      double *X = Xrow + (base + pp - sA) * XR::STRIDE;
       const double nup[3] = {ps.nup[0], ps.nup[1], ps.nup[2]};
       const double O0 = ps.om[0], Ov[3] = {ps.om[1], ps.om[2], ps.om[3]}, dO0 = ps.om[4],
                    dOv[3] = {ps.om[5], ps.om[6], ps.om[7]};
       const int l = tri_inv(c) + 1;   // lmidx(l, 1) <= c < lmidx(l + 1, 1)
       const int m = c - lmidx(l, 1) + 1, hs = sidx(l, m);
-      const cd *g = wsc.GS[pp][hs];
+      const cd *g = GS[pp][hs];
       cd hn[3] = {mk(0.0, 0.0), mk(0.0, 0.0), mk(0.0, 0.0)};
-      if (want_dp) hess_fast(wsc.GS[pp], l, m, nup, shc, hn);
+      if (want_dp) hess_fast(GS[pp], l, m, nup, shc, hn);
       double gs = 0, dgs = 0, gv[3], dgv[3];
       for (int a = 0; a < 3; ++a) {
         gs -= Ov[a] * g[a].y;
@@ -949,19 +1040,8 @@ __global__ void __launch_bounds__(WPB * 32, P <= 8 ? 2 : 1)
       }
       X[XR::TH + c] = s2 * inv4pi * ps.R[hs].y * O0;
     }
-    if (lane < kPPW) {
-      PairState<P> &ps = mine[lane];
-      if (ps.active) {
-        if (pstat) pstat[ps.k - obase] = (ps.conv[0] && ps.conv[1] && ps.conv[2]) ? 0 : 1;
-        nswap += ps.swap[0] + ps.swap[1] + ps.swap[2];
-      }
-    }
     __syncwarp();
-    if (threadIdx.x == 0) nsw = 0;   // the list was last read in phase 4
-    __syncthreads();
-    RRQ_PHASE_MARK(4);
   }
-  if (swapcnt && nswap) atomicAdd(swapcnt, nswap);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1201,11 +1281,11 @@ struct ContractCfg {
 // ------------------------------------------------------------------------------------------------
 // k_translate: Step 7 (P:L1263-1268 eq cdlp1dintegral): for each (l,m),
 // lambda_1, its nu'-derivative and theta_1 from Q^{(j,k)}, dQ^{(j,k)}, V^{(j,k)} and S(r'), plus the
-// gamma parts from k_pair_edge -> W, dW, Theta -> zeta = (Theta, zeta(W), zeta(dW), zeta_S).
+// gamma parts from k_target_gamma -> W, dW, Theta -> zeta = (Theta, zeta(W), zeta(dW), zeta_S).
 //
 // The translation is a 2-D convolution  out(l,m) = sum_{j,k} c(l,m,j,k) A^{(j,k)} S^{(l-j,m-k)}  whose
 // coefficient factors as u(l,m) v(j,k) w(l-j,m-k) (T = F(l,m)/(F(j,k) F(l',m')), F(a,b) = sqrt((a+b)!(a-b)!),
-// and the factorial ratios of C_j, D_j split the same way).  k_qmap stores A = v A and k_pair_edge stores
+// and the factorial ratios of C_j, D_j split the same way).  k_qmap stores A = v A and k_target_gamma stores
 // S' = w S (expanded over m' < 0), so the inner loop is pure FMAs on the Im parts (only Im(lambda),
 // Im(theta) enter W, dW, Theta): Im(A S) = A.x S.y + A.y S.x, with A^{(j,-k)} = (-1)^k conj A^{(j,k)} folded
 // into sign flips of (A.x, A.y).

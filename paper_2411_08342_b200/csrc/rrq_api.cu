@@ -40,10 +40,10 @@ struct rrq_ctx_s {
   };
   int64_t last_np = 0, last_nz = 0, last_sA = 0;
   int last_set = 0;
-  // k_pair_edge's outputs are double-buffered (set = sub-chunk parity) so that the producer stream (k_pair_setup,
-  // k_pair_edge of sub-chunk i+1) runs concurrently with the consumer stream (k_qmap, k_translate, k_contract of
+  // The producer kernels' outputs are double-buffered (set = sub-chunk parity) so that the producer stream (k_pair_setup,
+  // k_newton, k_edge_lines, k_target_gamma of sub-chunk i+1) runs concurrently with the consumer stream (k_qmap, k_translate, k_contract of
   // sub-chunk i): the edge kernel is FP64-latency bound and the GEMM kernels leave the FP64 pipe ~40 % idle.
-  Buf Arow[2], Xrow[2], psetup[2], cpair[2], et0[2], Qrow, ipatch;
+  Buf Arow[2], Xrow[2], psetup[2], cpair[2], et0[2], om[2], Qrow, ipatch;
   cudaStream_t st2 = nullptr;                      // producer stream (created on first use)
   cudaEvent_t ev_edge[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_fork = nullptr, ev_join = nullptr;
   bool overlap = true;                             // RRQ_NO_OVERLAP=1 runs everything on the caller's stream
@@ -57,8 +57,8 @@ struct rrq_ctx_s {
   size_t hmap_n = 0;
   // device-time accounting (rrq_set_timing)
   bool timing = false;
-  double t_ms[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  int64_t t_n[RRQ_NSTAGES] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double t_ms[RRQ_NSTAGES] = {};
+  int64_t t_n[RRQ_NSTAGES] = {};
   int64_t stats[2] = {0, 0};
   struct Pend {
     int stage;
@@ -465,7 +465,7 @@ void rrq_destroy(rrq_ctx c) {
   if (c->st2) cudaStreamDestroy(c->st2);
   for (cudaEvent_t e : {c->ev_edge[0], c->ev_edge[1], c->ev_free[0], c->ev_free[1], c->ev_fork, c->ev_join})
     if (e) cudaEventDestroy(e);
-  for (auto *b : {&c->Arow[0], &c->Arow[1], &c->Xrow[0], &c->Xrow[1], &c->psetup[0], &c->psetup[1], &c->et0[0], &c->et0[1], &c->cpair[0],
+  for (auto *b : {&c->Arow[0], &c->Arow[1], &c->Xrow[0], &c->Xrow[1], &c->psetup[0], &c->psetup[1], &c->et0[0], &c->et0[1], &c->om[0], &c->om[1], &c->cpair[0],
                   &c->cpair[1], &c->Qrow, &c->ipatch, &c->balls, &c->cell_cnt, &c->cell_items, &c->patch_cell, &c->tcnt, &c->ptgt, &c->perm, &c->seg,
                   &c->cursor, &c->items, &c->Z, &c->fitwork, &c->one})
     if (b->p) cudaFree(b->p);
@@ -726,16 +726,13 @@ rrq_status rrq_patch_fit(rrq_ctx c, const rrq_surface *s, void *fit, int32_t *pa
   return RRQ_ERR_NOT_IMPLEMENTED;
 }
 
-// warps per CTA of k_pair_edge: 8, 6 at p = 14 (shared memory: the per-warp gradient tables grow as p^2)
-template <int P>
-constexpr int kWPB = P >= 14 ? 6 : 8;
-
 template <int P>
 static size_t edge_smem(int n_omega) {
   using D = Dims<P>;
-  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + hc_size(P) + kNDirect * D::Q;
+  using EC = EdgeCfg<P>;
+  int tab = D::Q * D::Q + 2 * D::Q + 2 * n_omega + kNDirect * D::Q + EC::WPB * 2 * kNDirect;
   tab = (tab + 1) & ~1;
-  return (size_t)tab * sizeof(double) + kWPB<P> * kPPW * sizeof(PairState<P>) + kWPB<P> * sizeof(WarpScr<P>);
+  return (size_t)tab * sizeof(double) + EC::WPB * EC::PPW * sizeof(EdgePair<P>);
 }
 
 template <int P>
@@ -808,9 +805,9 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
   std::memcpy(hitem.data(), c->hmap + Pn + 1, (Pn + 1) * sizeof(int64_t));
   hseg[Pn] = total;
   // ---- sub-chunks: ranges of whole patches with at most `cap` pairs (scratch ~24 KB per pair at p = 8:
-  // the double-buffered pair_edge outputs plus the Q and Z rows)
+  // the double-buffered producer outputs plus the Q and Z rows)
   const int64_t per_pair = (int64_t)(2 * (2 * D::K + XRow<P>::STRIDE) + QRow<P>::STRIDE + CC::ZBLK / CC::TP) * 8 +
-                           2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair) + 3 * (sizeof(double2) + 1));
+                           2 * (int64_t)(sizeof(PairSetup) + sizeof(ContractPair) + 3 * (sizeof(double2) + 1) + 8 * sizeof(double));
   const int64_t cap = std::max<int64_t>(2 * TP, (int64_t)(c->scratch_bytes / per_pair));
   // sub-chunks = contiguous ranges of work items (tiles of TP pairs of one patch): whole patches while they
   // fit, a patch with more than `cap` pairs (config 5: one patch, 10M targets) split at tile boundaries
@@ -849,6 +846,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     if (!ensure(c, c->Arow[b], (size_t)maxitems * QC::ABLK * 8) || !ensure(c, c->Xrow[b], (size_t)maxsub * XRow<P>::STRIDE * 8) ||
         !ensure(c, c->psetup[b], (size_t)maxsub * sizeof(PairSetup)) ||
         !ensure(c, c->cpair[b], (size_t)maxsub * sizeof(ContractPair)) ||
+        !ensure(c, c->om[b], (size_t)maxsub * 8 * sizeof(double)) ||   // k_edge_lines: scalar line integrals
         !ensure(c, c->et0[b], (size_t)maxsub * 3 * (sizeof(double2) + 1) + 64))   // k_newton: t0 + flag byte per edge, batch counter
       return RRQ_ERR_CUDA;
   if (!ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxitems * CC::ZBLK * 8))
@@ -892,14 +890,25 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
         const unsigned gn = (unsigned)std::min<int64_t>(nblk(3 * np_, kNewtonThreads), (int64_t)c->num_sms * 4);
         k_newton<P><<<gn, kNewtonThreads, 0, sp>>>(np_, ps, fit, c->prm.rho_swap, T0, EF, ctr);
       }
-      constexpr int WPB = kWPB<P>;
-      unsigned grid = (unsigned)std::min<int64_t>((np_ + WPB * kPPW - 1) / (WPB * kPPW), (int64_t)c->num_sms * 4);
-      k_pair_edge<P, WPB><<<grid, WPB * 32, edge_smem<P>(c->prm.n_omega), sp>>>(
-          sA, sB, bp<int64_t>(c->perm), bp<int64_t>(c->ptgt), obase, pair_patch, fit, tg->x, tg->normal,
-          tg->self_node, tg->side, c->T, c->prm.n_omega, c->prm.rho_swap, Ar, Xr,
-          pstat, obase, c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, c->d_trtab, ps, want_dp, T0, EF);
+      double *OMb = bp<double>(c->om[b]);
+      {
+        TScope t9(c, 9, sp);
+        using EC = EdgeCfg<P>;
+        constexpr int PR = EC::WPB * EC::PPW;   // pairs per CTA round
+        unsigned grid = (unsigned)std::min<int64_t>((np_ + PR - 1) / PR, (int64_t)c->num_sms * EC::MINB * 2);
+        k_edge_lines<P><<<grid, EC::WPB * 32, edge_smem<P>(c->prm.n_omega), sp>>>(
+            sA, sB, fit, c->T, c->prm.n_omega, Ar, OMb, pstat, obase,
+            c->timing ? bp<unsigned long long>(c->swapcnt) : nullptr, ps, want_dp, T0, EF);
+      }
+      {
+        TScope t10(c, 10, sp);
+        using TC = TgtCfg<P>;
+        constexpr int PR = TC::WPB * kPPW;
+        unsigned grid = (unsigned)std::min<int64_t>((np_ + PR - 1) / PR, (int64_t)c->num_sms * TC::MINB * 2);
+        k_target_gamma<P><<<grid, TC::WPB * 32, TC::SMEM, sp>>>(sA, sB, c->T, Xr, OMb, c->d_trtab, ps, want_dp);
+      }
     }
-    if ((r = cuda_check(c, "k_pair_edge"))) return r;
+    if ((r = cuda_check(c, "k_edge_lines / k_target_gamma"))) return r;
     if (nset == 2) {
       cudaEventRecord(c->ev_edge[b], sp);
       cudaStreamWaitEvent(st, c->ev_edge[b], 0);
@@ -931,7 +940,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
     }
     if ((r = cuda_check(c, "k_contract"))) return r;
     if (nset == 2) cudaEventRecord(c->ev_free[b], st);
-    c->launches += 6;
+    c->launches += 7;
     c->last_sA = sA;
     c->last_np = np_;
     c->last_set = b;
@@ -1039,7 +1048,8 @@ static cudaError_t set_attrs(int n_omega) {
   auto acc = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
   acc(set_smem(k_edge_tables<P>, "k_edge_tables", EdgeTabCfg<P>::SMEM, EdgeTabCfg<P>::THREADS));
   acc(set_smem(k_patch_fit_q<P>, "k_patch_fit_q", FitCfg<P>::SMEM, 256));
-  acc(set_smem(k_pair_edge<P, kWPB<P>>, "k_pair_edge", edge_smem<P>(n_omega), kWPB<P> * 32));
+  acc(set_smem(k_edge_lines<P>, "k_edge_lines", edge_smem<P>(n_omega), EdgeCfg<P>::WPB * 32));
+  acc(set_smem(k_target_gamma<P>, "k_target_gamma", TgtCfg<P>::SMEM, TgtCfg<P>::WPB * 32));
   acc(set_smem(k_qmap<P, true>, "k_qmap<dp>", QmapCfg<P>::SMEM, QmapCfg<P>::WARPS * 32));
   acc(set_smem(k_qmap<P, false>, "k_qmap", QmapCfg<P>::SMEM, QmapCfg<P>::WARPS * 32));
   acc(set_smem(k_translate<P, true>, "k_translate<dp>", TrCfg<P>::SMEM, TrCfg<P>::WPB * 32));

@@ -167,7 +167,7 @@ class RRQ:
     def launch_count(self):
         return int(self.lib.rrq_launch_count(self.h))
 
-    STAGES = ("near_list", "patch_fit", "pair_edge", "qmap", "translate", "contract", "plumbing", "build", "newton")
+    STAGES = ("near_list", "patch_fit", "pair_edge", "qmap", "translate", "contract", "plumbing", "build", "newton", "edge_lines", "target_gamma")
 
     def set_timing(self, on=True):
         self._check(self.lib.rrq_set_timing(self.h, int(on)), "rrq_set_timing")

@@ -9,6 +9,6 @@ lib = pkg.load_library()
 lib.rrq_debug_phase_cycles.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
 out = np.zeros(8, np.uint64)
 lib.rrq_debug_phase_cycles(res['ctx'].h, out.ctypes.data, 1)
-tot = out[:5].sum()
-for i, n in enumerate(['harmonics', 'newton+model', 'weights', 'sinh', 'gamma']):
+tot = out[:3].sum()
+for i, n in enumerate(['load+list', 'model+sinh', 'weights']):   # k_edge_lines' steps
     print('%-14s %5.1f%%' % (n, 100 * out[i] / tot))
