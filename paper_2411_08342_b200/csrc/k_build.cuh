@@ -592,8 +592,8 @@ __global__ void __launch_bounds__(kNewtonThreads, 4)
 // their nu'-derivatives (OM, 8 doubles per pair), Omega_0 on swap edges by the sinh rule (A9).
 // CTA rounds of WPB * PPW pairs in three barrier-separated steps: (1) every warp loads its pairs' setup and
 // t0 / flags and lists the swap edges CTA-wide; (2) the model integrals (a thread per edge inside rho = 1.6,
-// a warp per edge with the 48-point rule outside) and the sinh rule (a warp per edge), drawn from the list
-// through a shared counter; (3) the weights: LP lanes per pair sweep its 3 p~ edge nodes (p = 8: a half-warp
+// a warp per edge with the 48-point rule outside) and the sinh rule (a warp per edge, round-robin over the
+// list); (3) the weights: LP lanes per pair sweep its 3 p~ edge nodes (p = 8: a half-warp
 // per pair, one edge per sweep).
 // ------------------------------------------------------------------------------------------------
 template <int P>
@@ -661,13 +661,13 @@ __global__ void __launch_bounds__(EdgeCfg<P>::WPB * 32, EdgeCfg<P>::MINB)
   int tab_doubles = Q * Q + 2 * Q + 2 * n_omega + kNDirect * Q + WPB * 2 * kNDirect;
   tab_doubles = (tab_doubles + 1) & ~1;
   EdgePair<P> *pst = reinterpret_cast<EdgePair<P> *>(smem + tab_doubles);
-  __shared__ int nsw, wctr;                    // swap edges of the round (CTA-wide list), work counter
+  __shared__ int nsw;                          // swap edges of the round (CTA-wide list)
   __shared__ int swl[WPB * PPW * 3];
   for (int i = threadIdx.x; i < Q * Q; i += blockDim.x) sU[i] = T.U[i];
   for (int i = threadIdx.x; i < Q; i += blockDim.x) { stgl[i] = T.tgl[i]; swgl[i] = T.wgl[i]; }
   for (int i = threadIdx.x; i < n_omega; i += blockDim.x) { sxo[i] = T.xo[i]; swo[i] = T.wo[i]; }
   for (int i = threadIdx.x; i < kNDirect * Q; i += blockDim.x) sxdp[i] = T.xdp[i];
-  if (threadIdx.x == 0) { nsw = 0; wctr = 0; }
+  if (threadIdx.x == 0) nsw = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double *r13 = sr13 + warp * 2 * kNDirect;
@@ -714,11 +714,7 @@ __global__ void __launch_bounds__(EdgeCfg<P>::WPB * 32, EdgeCfg<P>::MINB)
       const int e = swl[q] % 3;
       if (!ps.direct[e]) model_integrals<Q>(ps.t0[e][0], fabs(ps.t0[e][1]), ps.I[e], ps.J[e]);
     }
-    for (;;) {
-      int q = 0;
-      if (lane == 0) q = atomicAdd(&wctr, 1);
-      q = __shfl_sync(0xffffffffu, q, 0);
-      if (q >= nsw_) break;
+    for (int q = warp; q < nsw_; q += WPB) {
       const int code = swl[q], e = code % 3;
       EdgePair<P> &ps = pst[code / 3];
       const double *blk = fit + (int64_t)ps.Pp * L::STRIDE;
@@ -773,7 +769,7 @@ __global__ void __launch_bounds__(EdgeCfg<P>::WPB * 32, EdgeCfg<P>::MINB)
     __syncthreads();
     RRQ_PHASE_MARK(1);
     // ---------------- step 3: weights and the scalar line integrals (Step 6)
-    if (threadIdx.x == 0) { nsw = 0; wctr = 0; }   // read last in step 2; written next after the round's barrier
+    if (threadIdx.x == 0) nsw = 0;   // read last in step 2; written next after the round's barrier
     const int sub = lane % LP, grp = lane / LP;
 #pragma unroll 1
     for (int r = 0; r < PPW / HW; ++r) {

@@ -31,7 +31,7 @@ for p in [int(a) for a in sys.argv[1:]] or [10, 12]:
     perm, Z = res["ctx"].debug_zeta(10 ** 8)
     ptr, pat = res["ptr"], res["pat"]
     tgt = np.repeat(np.arange(ptr.size - 1), np.diff(ptr))
-    sample = np.sort(perm)[:: max(1, perm.size // 200)]
+    sample = np.sort(perm)[:: max(1, perm.size // int(__import__("os").environ.get("DBG_N", "200")))]
     inv = np.empty(perm.max() + 1, np.int64); inv[perm] = np.arange(perm.size)
     r = O.build_rows(S, *tgs, tgt[sample], pat[sample], prec="d", zeta=True)
     zo = U.zeta_to_gpu_layout(r[2], npb)
@@ -55,3 +55,13 @@ for p in [int(a) for a in sys.argv[1:]] or [10, 12]:
         o = r[0][k]
         er = np.abs(go[k] - o).max(1) / np.abs(o).max(1)
         print(f"  rows {nm}: rel err median {np.median(er):.2e} max {er.max():.2e}")
+    # which pairs are off (Theta block), by position in the patch-major order
+    a, b = 0, npb
+    sc = np.abs(zo[:, a:b]).max(1); er = np.abs(zg[:, a:b] - zo[:, a:b]).max(1) / sc
+    bad = np.where(er > 1e-6)[0]
+    pos = inv[sample]
+    print(f"  bad pairs {bad.size} of {sample.size}; positions mod 32: {np.bincount(pos[bad] % 32, minlength=32).tolist()}")
+    print(f"  positions mod 24: {np.bincount(pos[bad] % 24, minlength=24).tolist()}")
+    print("  first bad: pos", pos[bad][:12].tolist(), "k", sample[bad][:12].tolist(), "status", res["status"][sample[bad]][:12].tolist(),
+          "self", (tgs[2][tgt[sample[bad]]] >= 0)[:12].tolist())
+    print("  status of all sampled:", np.bincount(res["status"][sample]).tolist(), " of bad:", np.bincount(res["status"][sample[bad]]).tolist())
