@@ -5,7 +5,7 @@ cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${1:-v}
 shift
-KS=${@:-k_pair_edge k_qmap k_translate k_contract}
+KS=${@:-k_newton k_edge_lines k_target_gamma k_qmap k_translate k_contract}
 for K in $KS; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K --launch-skip 12 --launch-count 1 \
     -o gpurun_out/ncu_${TAG}_$K -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
