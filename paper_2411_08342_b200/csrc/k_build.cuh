@@ -708,13 +708,16 @@ __global__ void __launch_bounds__(EdgeCfg<P>::WPB * 32, EdgeCfg<P>::MINB)
     RRQ_PHASE_MARK(0);
     // ---------------- step 2: model integrals (reading A11 / A11') and Omega_0 on the swap edges by the
     // sinh-split Gauss-Legendre rule (reading A9)
+    // warp 0: the recurrences (a lane per edge; one long scalar dependency chain each); warps 1 ..: the per-edge
+    // warp work, so no warp has both on its critical path to the barrier
     const int nsw_ = nsw;
-    for (int q = threadIdx.x; q < nsw_; q += blockDim.x) {
-      EdgePair<P> &ps = pst[swl[q] / 3];
-      const int e = swl[q] % 3;
-      if (!ps.direct[e]) model_integrals<Q>(ps.t0[e][0], fabs(ps.t0[e][1]), ps.I[e], ps.J[e]);
-    }
-    for (int q = warp; q < nsw_; q += WPB) {
+    if (warp == 0)
+      for (int q = lane; q < nsw_; q += 32) {
+        EdgePair<P> &ps = pst[swl[q] / 3];
+        const int e = swl[q] % 3;
+        if (!ps.direct[e]) model_integrals<Q>(ps.t0[e][0], fabs(ps.t0[e][1]), ps.I[e], ps.J[e]);
+      }
+    for (int q = warp - 1; q >= 0 && q < nsw_; q += WPB - 1) {
       const int code = swl[q], e = code % 3;
       EdgePair<P> &ps = pst[code / 3];
       const double *blk = fit + (int64_t)ps.Pp * L::STRIDE;
@@ -867,7 +870,7 @@ struct TgtCfg {
   using D = Dims<P>;
   static constexpr int WPB = P >= 14 ? 4 : 8;
   static constexpr size_t PER_WARP = sizeof(cd) * kPPW * D::NS * 3 + kPPW * sizeof(TgtPair<P>);
-  static constexpr size_t SMEM = (size_t)hc_size(P) * sizeof(double) + WPB * PER_WARP;
+  static constexpr size_t SMEM = (size_t)(hc_size(P) + P * P) * sizeof(double) + WPB * PER_WARP;
   static constexpr int MINB = P <= 8 ? 2 : 1;
 };
 
@@ -878,32 +881,44 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
   using D = Dims<P>;
   using XR = XRow<P>;
   constexpr int NP = D::NP, NS = D::NS, WPB = TgtCfg<P>::WPB;
-  const double *wS = trtab + TrCfg<P>::WS;
   extern __shared__ double smem[];
   double *shc = smem;   // [hc_size(P)]
+  double *wS = smem + hc_size(P);   // [P * P] w(l', m') of the translation operands (TrCfg)
   for (int i = threadIdx.x; i < hc_size(P); i += blockDim.x) shc[i] = T.hc[i];
+  for (int i = threadIdx.x; i < P * P; i += blockDim.x) wS[i] = trtab[TrCfg<P>::WS + i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char *wbase = reinterpret_cast<unsigned char *>(smem + hc_size(P)) + (size_t)warp * TgtCfg<P>::PER_WARP;
+  unsigned char *wbase = reinterpret_cast<unsigned char *>(smem + hc_size(P) + P * P) + (size_t)warp * TgtCfg<P>::PER_WARP;
   cd (*GS)[NS][3] = reinterpret_cast<cd (*)[NS][3]>(wbase);
   TgtPair<P> *mine = reinterpret_cast<TgtPair<P> *>(wbase + sizeof(cd) * kPPW * NS * 3);
   const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
-  for (int64_t base = sA + ((int64_t)blockIdx.x * WPB + warp) * kPPW; base < sB; base += (int64_t)gridDim.x * WPB * kPPW) {
+  // the round's inputs (lanes 0..2: a pair's setup record; lanes 8..31: its scalar line integrals) are loaded
+  // one round ahead into registers, so their latency is covered by the previous round's work
+  const int64_t stride = (int64_t)gridDim.x * WPB * kPPW;
+  double pv[6] = {0, 0, 0, 0, 0, 0}, po = 0;
+  int64_t pa = 0;
+  auto prefetch = [&](int64_t b) {
+    if (lane < kPPW && b + lane < sB) {
+      const PairSetup &q = setup[b + lane - sA];
+      pa = q.aslot;
+      for (int a = 0; a < 3; ++a) { pv[a] = q.rp[a]; pv[3 + a] = q.nup[a]; }
+    }
+    if (lane >= 8 && b + ((lane - 8) >> 3) < sB) po = OM[(b + ((lane - 8) >> 3) - sA) * 8 + ((lane - 8) & 7)];
+  };
+  int64_t base = sA + ((int64_t)blockIdx.x * WPB + warp) * kPPW;
+  if (base < sB) prefetch(base);
+  for (; base < sB; base += stride) {
     if (lane < kPPW) {
       TgtPair<P> &ps = mine[lane];
-      const int64_t s = base + lane;
-      const bool active = s < sB;
+      const bool active = base + lane < sB;
       ps.active = active;
       if (active) {
-        const PairSetup &q = setup[s - sA];
-        ps.aslot = q.aslot;
-        for (int a = 0; a < 3; ++a) { ps.rp[a] = q.rp[a]; ps.nup[a] = q.nup[a]; }
+        ps.aslot = pa;
+        for (int a = 0; a < 3; ++a) { ps.rp[a] = pv[a]; ps.nup[a] = pv[3 + a]; }
       }
     }
-    if (lane >= 8 && lane < 8 + 8 * kPPW) {
-      const int pp = (lane - 8) >> 3, i = (lane - 8) & 7;
-      if (base + pp < sB) mine[pp].om[i] = OM[(base + pp - sA) * 8 + i];
-    }
+    if (lane >= 8 && base + ((lane - 8) >> 3) < sB) mine[(lane - 8) >> 3].om[(lane - 8) & 7] = po;
+    if (base + stride < sB) prefetch(base + stride);
     __syncwarp();
     if constexpr (kPPW * (P + 1) <= 32) {
       // lane = (pair, column m): R_l^m of its column in registers (the r_column recurrence), the
@@ -950,7 +965,7 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
         gs[0] = g[0]; gs[1] = g[1]; gs[2] = g[2];
         if (l < P) {   // translation operands, l' < p
           const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2], r = Rc[l];
-          const double w = __ldg(wS + l * l + l + m);
+          const double w = wS[l * l + l + m];
           double2 *o = xo + 2 * (l * l + l + m);
           o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
           o[1] = make_double2(w * ng.y, w * ng.x);
@@ -986,7 +1001,7 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
         const int m = e - sidx(l, 0);
         const cd *g = GS[pp][e];
         const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
-        const double w = __ldg(wS + l * l + l + m);
+        const double w = wS[l * l + l + m];
         double2 *o = reinterpret_cast<double2 *>(Xrow + (base + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m));
         o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
         o[1] = make_double2(w * ng.y, w * ng.x);

@@ -1,6 +1,7 @@
 #!/bin/bash
-# ncu --set full captures of one launch of each build kernel in the bench's own cfg4 launch configuration.
-# usage (on the GPU box): bash tools/ncu_cfg4.sh TAG [kernels...]
+# ncu --set full captures of one launch of each build kernel in the bench's own cfg4 launch configuration,
+# summarised on the box (tools/ncu_hot.py: key metrics, stall reasons, hottest SASS lines); the reports stay in /tmp
+# (gpurun_out/ is capped at 64 MiB).  usage (on the GPU box): bash tools/ncu_cfg4.sh TAG [kernels...]
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${1:-v}
@@ -8,7 +9,11 @@ shift
 KS=${@:-k_newton k_edge_lines k_target_gamma k_qmap k_translate k_contract}
 for K in $KS; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$K --launch-skip 12 --launch-count 1 \
-    -o gpurun_out/ncu_${TAG}_$K -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
+    -o /tmp/ncu_${TAG}_$K -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
     > gpurun_out/ncu_${TAG}_$K.log 2>&1
   echo "$K rc=$?" >> gpurun_out/ncu_${TAG}.status
+  { echo "# ncu --set full --import-source on --clock-control none -k regex:$K --launch-skip 12 --launch-count 1 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline";
+    echo "# (cfg4 launch configuration, 13th launch of the kernel; summary by tools/ncu_hot.py)";
+    python tools/ncu_hot.py /tmp/ncu_${TAG}_$K.ncu-rep 30; } > gpurun_out/ncu_${TAG}_$K.txt 2>&1
 done
+exit 0
