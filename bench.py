@@ -47,11 +47,15 @@ def traffic_per_launch(kernel, pairs, launches):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full capture (bytes per pair measured
     there x this run's average pairs per launch), or None."""
     import json as _j
-    f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")
-    try:
-        rec = _j.load(open(f)).get("k_" + kernel)
-    except (OSError, ValueError):
-        return None, None
+    rec = None
+    for name in ("r02_traffic.json", "r01_traffic.json"):   # the latest committed capture
+        f = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", name)
+        try:
+            rec = _j.load(open(f)).get("k_" + kernel)
+        except (OSError, ValueError):
+            rec = None
+        if rec:
+            break
     if not rec or not launches:
         return None, None
     return rec["dram_bytes_per_pair"] * pairs / launches, rec["source"]

@@ -16,14 +16,15 @@ for k in ("k_qmap", "k_contract", "k_newton", "k_edge_lines", "k_target_gamma", 
     g = lambda n: float(v[h.index(n)].replace(",", "")) if n in h else None
     recs[k] = dict(grid=g("launch__grid_size"), rd=g("dram__bytes_read.sum"), wr=g("dram__bytes_write.sum"),
                    ns=g("gpu__time_duration.sum"), rd_unit=r[1][h.index("dram__bytes_read.sum")],
+                   wr_unit=r[1][h.index("dram__bytes_write.sum")],
                    t_unit=r[1][h.index("gpu__time_duration.sum")])
 if "k_qmap" in recs:
     pairs = recs["k_qmap"]["grid"] * 16
 scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 for k, r in recs.items():
-    sc = scale.get(r["rd_unit"], 1.0)
-    out[k] = {"dram_bytes_per_pair": (r["rd"] + r["wr"]) * sc / pairs if pairs else None,
-              "dram_read_bytes": r["rd"] * sc, "dram_write_bytes": r["wr"] * sc, "pairs_in_launch_upper_bound": pairs,
+    sc, sw = scale.get(r["rd_unit"], 1.0), scale.get(r["wr_unit"], 1.0)
+    out[k] = {"dram_bytes_per_pair": (r["rd"] * sc + r["wr"] * sw) / pairs if pairs else None,
+              "dram_read_bytes": r["rd"] * sc, "dram_write_bytes": r["wr"] * sw, "pairs_in_launch_upper_bound": pairs,
               "duration": r["ns"], "duration_unit": r["t_unit"], "grid": r["grid"],
               "source": f"profiles/r02_ncu_{k}_cfg4.txt (ncu --set full, cfg4 launch configuration, 13th launch)"}
 print(json.dumps(out, indent=1))
