@@ -1259,7 +1259,10 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
 template <int P>
 struct ContractCfg {
   using D = Dims<P>;
-  static constexpr int TP = 16, MT = TP / 8, NT = (D::N + 7) / 8, WARPS = 8;
+  static constexpr int TP = 16, MT = TP / 8, NT = (D::N + 7) / 8;
+  // warps per CTA (even: a warp's tiles share one M-tile) chosen so the MT x NT output tiles divide evenly:
+  // p = 6: 10 tiles on 10 warps, p = 8: 16 on 8, p = 10: 26 on 14 (2 each), p = 12: 36 on 12, p = 14: 50 on 10
+  static constexpr int WARPS = P == 4 ? 4 : P == 6 ? 10 : P == 8 ? 8 : P == 10 ? 14 : P == 12 ? 12 : 10;
   static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
   static constexpr int NB = Layout<P>::NF;   // B row stride (== the fit operators' row stride)
   // k-rows per chunk: 16 where it divides 4 NP (a Z chunk row is then one 128-B line), else 12, 8, 4
@@ -1570,7 +1573,7 @@ __global__ void __launch_bounds__(TrCfg<P>::WPB * 32, 1)
 // MK: the kernel mask at compile time (15 = all four, 3 = S|D: the DMMAs of the other kernels are compiled out --
 // a predicated-off DMMA still occupies the tensor pipe), 0 = taken from `mask` at run time.
 template <int P, int MK>
-__global__ void __launch_bounds__(256, ContractCfg<P>::MINB)
+__global__ void __launch_bounds__(ContractCfg<P>::WARPS * 32, ContractCfg<P>::MINB)
     k_contract(int64_t item0, int64_t item1, const int64_t *__restrict__ item_ptr, const int32_t *__restrict__ item_patch,
                const int64_t *__restrict__ seg_ptr, int64_t sA, const ContractPair *__restrict__ cpair,
                const double *__restrict__ fit, const double *__restrict__ Zrow, const double *__restrict__ nodes,
