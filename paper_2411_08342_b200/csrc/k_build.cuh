@@ -1265,9 +1265,13 @@ struct ContractCfg {
   static constexpr int WARPS = P == 4 ? 4 : P == 6 ? 10 : P == 8 ? 8 : P == 10 ? 14 : P == 12 ? 12 : 10;
   static constexpr int TILES = MT * NT, TPW = (TILES + WARPS - 1) / WARPS;
   static constexpr int NB = Layout<P>::NF;   // B row stride (== the fit operators' row stride)
-  // k-rows per chunk: 16 where it divides 4 NP (a Z chunk row is then one 128-B line), else 12, 8, 4
-  static constexpr int KC = (D::NP % 4 == 0) ? 16 : (D::NP % 3 == 0) ? 12 : ((D::NP % 2 == 0) ? 8 : 4);
-  static constexpr int NCH = 4 * D::NP / KC;
+  // k-rows per chunk: 16 where it divides 4 NP (a Z chunk row is then one 128-B line), else 12 or 8; where none
+  // divides (p = 10: 4 NP = 220) 16 with a zero-padded last chunk: its Z entries beyond 4 NP are never written
+  // (the Z buffer is zeroed when allocated) and multiply the rows that follow the operator in the fit block
+  static constexpr int K4 = 4 * D::NP;
+  static constexpr int KC = (K4 % 16 == 0) ? 16 : (K4 % 12 == 0) ? 12 : ((K4 % 8 == 0) ? 8 : 16);
+  static constexpr int NCH = (K4 + KC - 1) / KC;
+  static constexpr bool KPAD = K4 % KC != 0;
   // Z is stored tile-chunked by k_translate (a tile's block of ZBLK doubles): the Theta part [TP][ZTS]
   // (ZTS == 4 mod 16: conflict-free A fragments), then per K chunk ch the W | dW | S slices [3][TP][KC]
   // (k = component NP + c of zeta(W), zeta(dW), zeta_S).  A pipeline stage = [B chunk | Z chunk], two

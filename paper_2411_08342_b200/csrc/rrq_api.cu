@@ -849,8 +849,10 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
         !ensure(c, c->om[b], (size_t)maxsub * 8 * sizeof(double)) ||   // k_edge_lines: scalar line integrals
         !ensure(c, c->et0[b], (size_t)maxsub * 3 * (sizeof(double2) + 1) + 64))   // k_newton: t0 + flag byte per edge, batch counter
       return RRQ_ERR_CUDA;
+  const void *z_before = c->Z.p;
   if (!ensure(c, c->Qrow, (size_t)maxsub * QRow<P>::STRIDE * 8) || !ensure(c, c->Z, (size_t)maxitems * CC::ZBLK * 8))
     return RRQ_ERR_CUDA;
+  if (CC::KPAD && c->Z.p != z_before) cudaMemsetAsync(c->Z.p, 0, c->Z.n, st);   // the padded k-entries stay zero
   // producer stream: a second stream when overlapping, else the caller's
   cudaStream_t sp = st;
   if (nset == 2) {
