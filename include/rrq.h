@@ -182,6 +182,12 @@ rrq_status rrq_set_overlap(rrq_ctx ctx, int enable);
  * c-layout.  At most max_pairs rows; returns the row count in *n_out. */
 rrq_status rrq_debug_zeta(rrq_ctx ctx, int64_t max_pairs, int64_t *perm, double *Z, int64_t *n_out);
 
+/* Host-only self-test (no device needed): decodes k_translate's packed schedule for order p (4..14, even) the way
+ * the kernel does and checks that every output W^{(l,m)} receives exactly the terms Q^{(j,k)} S'^{(l-j,m-k)} of the
+ * direct translation (reading G4), each once, with the conjugate-symmetry sign flags.  Returns 0 when
+ * the schedule is correct, a positive code naming the failed check otherwise, -1 for an unsupported p. */
+int rrq_selftest_translate_schedule(int p);
+
 /* Profiling hook: SM cycles spent by k_edge_lines in each of its steps ([0] pair load + swap-edge list,
  * [1] model integrals + Omega_0 sinh rule, [2] weights), summed over CTAs, into HOST out[8]; reset if set. */
 rrq_status rrq_debug_phase_cycles(rrq_ctx ctx, uint64_t out[8], int reset);

@@ -328,6 +328,89 @@ static std::vector<double> make_trtab_p(int p) {
   }
 }
 
+// Host-side check of k_translate's packed schedule (no CUDA call): decode the table exactly as the kernel's main
+// loop and epilogue do (TrCfg field widths, window ring, prime codes, slot sums) and compare the terms every
+// output (l, m) receives with the definition of the direct translation (G4):
+//   W^{(l,m)} <- sum_{j=2..l} sum_{|k|<=j, |m-k|<=l-j} Q^{(j,k)} S'^{(l-j, m-k)},  k < 0 by conjugate symmetry
+// (sign flags FA for odd k, FB for even k).  Returns 0 if every output gets exactly its terms once.
+template <int P>
+static int check_trtab() {
+  using C = TrCfg<P>;
+  using D = Dims<P>;
+  constexpr int WD = C::WD, ST = C::STEPS, ZE = P * P, ZQ = C::ZQ;
+  const std::vector<double> tab = make_trtab<P>();
+  const uint32_t *code = reinterpret_cast<const uint32_t *>(tab.data());
+  const uint32_t *pcode = code + ST * 32, *cinfo = pcode + ST * 32;
+  const uint8_t *posq = reinterpret_cast<const uint8_t *>(cinfo + D::NP), *poss = posq + D::NQ;
+  // position -> entry (the zero entries keep the last positions)
+  std::vector<int> qent(D::NQ + 1, -1), sent(ZE + 1, -1);
+  for (int e = 0; e < D::NQ; ++e) { if (posq[e] > D::NQ || qent[posq[e]] >= 0) return 1; qent[posq[e]] = e; }
+  for (int e = 0; e < ZE; ++e) { if (poss[e] > ZE || sent[poss[e]] >= 0) return 2; sent[poss[e]] = e; }
+  if (qent[ZQ] >= 0 || sent[ZE] >= 0) return 3;   // the zero entries' positions must be free
+  qent[ZQ] = ZQ; sent[ZE] = ZE;
+  // a term: Q entry, sign flags, S' entry;  acc[lane][i] = terms accumulated for output i of the lane's block
+  struct Term { int q, fl, s; bool operator<(const Term &o) const { return q != o.q ? q < o.q : fl != o.fl ? fl < o.fl : s < o.s; } bool operator==(const Term &o) const { return q == o.q && fl == o.fl && s == o.s; } };
+  std::vector<std::vector<Term>> acc(32 * WD);
+  for (int lane = 0; lane < 32; ++lane) {
+    int ring[8];
+    for (int i = 0; i < WD; ++i) ring[i] = ZE;
+    for (int t = 0; t < ST; ++t) {
+      const uint32_t cw = code[t * 32 + lane];
+      const int qe = cw & 127, se = (cw >> 7) & C::SEM;
+      if (qe > D::NQ || se > ZE) return 4;
+      ring[t % WD] = sent[se];
+      if (t == 0 || (cw & C::PRIME)) {
+        const uint32_t pw = pcode[t * 32 + lane];
+        for (int i = 1; i < WD; ++i) {
+          const int pe = (pw >> (C::SEB * (i - 1))) & C::SEM;
+          if (pe > ZE) return 5;
+          ring[(t - i + WD * ST) % WD] = sent[pe];
+        }
+      }
+      const int fl = ((cw & C::FA) ? 1 : 0) | ((cw & C::FB) ? 2 : 0);
+      for (int i = 0; i < WD; ++i) {
+        const int s = ring[(t - i + WD * ST) % WD];
+        if (qent[qe] == ZQ || s == ZE) continue;   // a zero operand: no contribution
+        acc[lane * WD + i].push_back(Term{qent[qe], fl, s});
+      }
+    }
+  }
+  for (int l = 1; l <= P; ++l)
+    for (int m = 1; m <= l; ++m) {
+      const uint32_t ci = cinfo[lmidx(l, m)];
+      if ((int)(ci & 15) != l || (int)((ci >> 4) & 15) != m) return 6;
+      const int ib = (ci >> 8) & 15, fl0 = (ci >> 12) & 255, nl = (ci >> 20) & 63;
+      std::vector<Term> got, want;
+      for (int q = 0; q < nl; ++q) {
+        if (fl0 + q >= 32 || ib >= WD) return 7;
+        const auto &v = acc[(fl0 + q) * WD + ib];
+        got.insert(got.end(), v.begin(), v.end());
+      }
+      for (int j = 2; j <= l; ++j)
+        for (int k = -j; k <= j; ++k) {
+          const int lp = l - j, mp = m - k;
+          if (mp < -lp || mp > lp) continue;
+          want.push_back(Term{qidx(j, k < 0 ? -k : k), k < 0 ? ((-k) & 1 ? 1 : 2) : 0, lp * lp + lp + mp});
+        }
+      std::sort(got.begin(), got.end());
+      std::sort(want.begin(), want.end());
+      if (!(got == want)) return 100 + lmidx(l, m);
+    }
+  return 0;
+}
+
+int rrq_selftest_translate_schedule(int p) {
+  switch (p) {
+    case 4: return check_trtab<4>();
+    case 6: return check_trtab<6>();
+    case 8: return check_trtab<8>();
+    case 10: return check_trtab<10>();
+    case 12: return check_trtab<12>();
+    case 14: return check_trtab<14>();
+  }
+  return -1;
+}
+
 static cudaError_t set_kernel_attributes(int p, int n_omega);
 
 // Every entry point runs with the device the context was created on (its tables, scratch and the kernels'

@@ -46,3 +46,16 @@ def test_flop_model_matches_survey():
     from paper_2411_08342_b200.flops import pair_flops, translation_terms
     assert translation_terms(8, 2) == 489 and translation_terms(8, 1) == 574
     assert pair_flops(8)["total"] == 302368
+
+
+@pytest.mark.parametrize("p", [4, 6, 8, 10, 12, 14])
+def test_translate_schedule_selftest(p):
+    """Host logic: the packed k_translate schedule (lane pieces, window ring, prime codes, field widths -- 8-bit S'
+    positions from p = 12 on) decodes to exactly the terms of the direct translation for every output (l, m)."""
+    import ctypes
+    import paper_2411_08342_b200 as pkg
+    lib = pkg.load_library()
+    lib.rrq_selftest_translate_schedule.argtypes = [ctypes.c_int]
+    lib.rrq_selftest_translate_schedule.restype = ctypes.c_int
+    assert lib.rrq_selftest_translate_schedule(p) == 0
+    assert lib.rrq_selftest_translate_schedule(5) == -1
