@@ -856,7 +856,6 @@ __global__ void __launch_bounds__(EdgeCfg<P>::WPB * 32, EdgeCfg<P>::MINB)
 // k_translate adds the lambda_1 / theta_1 parts.  Warp per 3 pairs, no CTA barrier: lane = (pair, column m)
 // holds R_l^m of its column in registers, neighbour columns by shuffles.
 // ------------------------------------------------------------------------------------------------
-constexpr int kPPW = 3;   // pairs per warp per round (3 x (p + 1) columns <= 32 lanes up to p = 8)
 template <int P>
 struct TgtPair {
   using D = Dims<P>;
@@ -869,7 +868,10 @@ template <int P>
 struct TgtCfg {
   using D = Dims<P>;
   static constexpr int WPB = P >= 14 ? 4 : 8;
-  static constexpr size_t PER_WARP = sizeof(cd) * kPPW * D::NS * 3 + kPPW * sizeof(TgtPair<P>);
+  // pairs per warp per round: as many as fit with one lane per (pair, column m), m = 0..p (the register-column
+  // path); p = 10: 3 pairs through the shared-memory table path (2 pairs of 11 columns measured 40 % slower)
+  static constexpr int PPW = P == 10 ? 3 : (32 / (P + 1) > 6 ? 6 : 32 / (P + 1));
+  static constexpr size_t PER_WARP = sizeof(cd) * PPW * D::NS * 3 + PPW * sizeof(TgtPair<P>);
   static constexpr size_t SMEM = (size_t)(hc_size(P) + P * P) * sizeof(double) + WPB * PER_WARP;
   static constexpr int MINB = P <= 8 ? 2 : 1;
 };
@@ -880,7 +882,7 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
                    const double *__restrict__ trtab, const PairSetup *__restrict__ setup, int want_dp) {
   using D = Dims<P>;
   using XR = XRow<P>;
-  constexpr int NP = D::NP, NS = D::NS, WPB = TgtCfg<P>::WPB;
+  constexpr int NP = D::NP, NS = D::NS, WPB = TgtCfg<P>::WPB, kPPW = TgtCfg<P>::PPW, NPO = (8 * kPPW + 31) / 32;
   extern __shared__ double smem[];
   double *shc = smem;   // [hc_size(P)]
   double *wS = smem + hc_size(P);   // [P * P] w(l', m') of the translation operands (TrCfg)
@@ -892,10 +894,10 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
   cd (*GS)[NS][3] = reinterpret_cast<cd (*)[NS][3]>(wbase);
   TgtPair<P> *mine = reinterpret_cast<TgtPair<P> *>(wbase + sizeof(cd) * kPPW * NS * 3);
   const double inv4pi = 1.0 / (4.0 * kPi), s2 = 1.4142135623730950488;
-  // the round's inputs (lanes 0..2: a pair's setup record; lanes 8..31: its scalar line integrals) are loaded
-  // one round ahead into registers, so their latency is covered by the previous round's work
+  // the round's inputs (lanes < PPW: a pair's setup record; all lanes: the 8 PPW scalar line integrals) are
+  // loaded one round ahead into registers, so their latency is covered by the previous round's work
   const int64_t stride = (int64_t)gridDim.x * WPB * kPPW;
-  double pv[6] = {0, 0, 0, 0, 0, 0}, po = 0;
+  double pv[6] = {0, 0, 0, 0, 0, 0}, po[NPO];
   int64_t pa = 0;
   auto prefetch = [&](int64_t b) {
     if (lane < kPPW && b + lane < sB) {
@@ -903,7 +905,11 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
       pa = q.aslot;
       for (int a = 0; a < 3; ++a) { pv[a] = q.rp[a]; pv[3 + a] = q.nup[a]; }
     }
-    if (lane >= 8 && b + ((lane - 8) >> 3) < sB) po = OM[(b + ((lane - 8) >> 3) - sA) * 8 + ((lane - 8) & 7)];
+#pragma unroll
+    for (int j = 0; j < NPO; ++j) {
+      const int i = lane + 32 * j;
+      po[j] = (i < 8 * kPPW && b + (i >> 3) < sB) ? OM[(b + (i >> 3) - sA) * 8 + (i & 7)] : 0.0;
+    }
   };
   int64_t base = sA + ((int64_t)blockIdx.x * WPB + warp) * kPPW;
   if (base < sB) prefetch(base);
@@ -917,7 +923,11 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
         for (int a = 0; a < 3; ++a) { ps.rp[a] = pv[a]; ps.nup[a] = pv[3 + a]; }
       }
     }
-    if (lane >= 8 && base + ((lane - 8) >> 3) < sB) mine[(lane - 8) >> 3].om[(lane - 8) & 7] = po;
+#pragma unroll
+    for (int j = 0; j < NPO; ++j) {
+      const int i = lane + 32 * j;
+      if (i < 8 * kPPW) mine[i >> 3].om[i & 7] = po[j];
+    }
     if (base + stride < sB) prefetch(base + stride);
     __syncwarp();
     if constexpr (kPPW * (P + 1) <= 32) {

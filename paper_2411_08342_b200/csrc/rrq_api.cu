@@ -988,7 +988,7 @@ static rrq_status build_impl(rrq_ctx c, const rrq_surface *s, const rrq_targets 
       {
         TScope t10(c, 10, sp);
         using TC = TgtCfg<P>;
-        constexpr int PR = TC::WPB * kPPW;
+        constexpr int PR = TC::WPB * TC::PPW;
         unsigned grid = (unsigned)std::min<int64_t>((np_ + PR - 1) / PR, (int64_t)c->num_sms * TC::MINB * 2);
         k_target_gamma<P><<<grid, TC::WPB * 32, TC::SMEM, sp>>>(sA, sB, c->T, Xr, OMb, c->d_trtab, ps, want_dp);
       }
