@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -198,28 +200,45 @@ static std::vector<double> make_trtab() {
       if ((int)B.st.size() != tr_block_len(l, m0, WD)) { std::fprintf(stderr, "rrq: translate block length\n"); std::abort(); }
       blks.push_back(B);
     }
-  // lanes: pieces of each block; per lane the list of steps (padded to ST)
-  std::vector<std::vector<Step>> lanes(32);
-  std::vector<int> bfirst(blks.size()), bcnt(blks.size());
-  int L = 0;
+  // pieces of each block (near-equal contiguous parts of at most ST steps, one lane each, padded to ST); the
+  // blocks are laid over the 32 lanes in the order `order` (a block's pieces on consecutive lanes), which the
+  // bank search below may permute
+  std::vector<std::vector<std::vector<Step>>> pieces(blks.size());
+  int total_lanes = 0;
   for (size_t b = 0; b < blks.size(); ++b) {
     const int len = (int)blks[b].st.size(), n = (len + ST - 1) / ST;
-    bfirst[b] = L;
-    bcnt[b] = n;
-    for (int q = 0; q < n; ++q, ++L) {
-      if (L >= 32) { std::fprintf(stderr, "rrq: translate schedule needs more than 32 lanes\n"); std::abort(); }
+    for (int q = 0; q < n; ++q) {
       const int f = (int)((int64_t)q * len / n), e = (int)((int64_t)(q + 1) * len / n);
+      std::vector<Step> pc;
       for (int i = f; i < e; ++i) {
         Step t = blks[b].st[i];
         if (i == f) t.flags = (t.flags & (C::FA | C::FB)) | C::PRIME;
-        lanes[L].push_back(t);
+        pc.push_back(t);
       }
+      if ((int)pc.size() > ST) { std::fprintf(stderr, "rrq: translate piece too long\n"); std::abort(); }
+      while ((int)pc.size() < ST) pc.push_back(Step{ZQ, ZE, 0, 0, {ZE, ZE, ZE, ZE}});
+      pieces[b].push_back(pc);
     }
+    total_lanes += n;
   }
-  for (int l2 = 0; l2 < 32; ++l2) {
-    if ((int)lanes[l2].size() > ST) { std::fprintf(stderr, "rrq: translate piece too long\n"); std::abort(); }
-    while ((int)lanes[l2].size() < ST) lanes[l2].push_back(Step{ZQ, ZE, 0, lanes[l2].empty() ? (int)C::PRIME : 0, {ZE, ZE, ZE, ZE}});
-  }
+  if (total_lanes > 32) { std::fprintf(stderr, "rrq: translate schedule needs more than 32 lanes\n"); std::abort(); }
+  std::vector<int> order(blks.size());
+  for (size_t b = 0; b < blks.size(); ++b) order[b] = (int)b;
+  std::vector<std::vector<Step>> lanes(32);
+  std::vector<int> bfirst(blks.size()), bcnt(blks.size());
+  auto assign = [&]() {
+    int L = 0;
+    for (int b : order) {
+      bfirst[b] = L;
+      bcnt[b] = (int)pieces[b].size();
+      for (auto &pc : pieces[b]) lanes[L++] = pc;
+    }
+    for (; L < 32; ++L) {
+      lanes[L].assign(ST, Step{ZQ, ZE, 0, 0, {ZE, ZE, ZE, ZE}});
+      lanes[L][0].flags = (int)C::PRIME;
+    }
+  };
+  assign();
   // Bank model (quarter-warp: 8 lanes per wavefront of 16-B accesses, tools/lds_banks.cu): a Q entry at
   // position x starts in 16-B group x mod 8 (stride 144 B) and its 8 chunks and V follow; an S' entry at
   // position y starts in group 3y mod 8 (stride 48 B).  Cost of a quarter = 9 x (max distinct Q entries in
@@ -260,21 +279,39 @@ static std::vector<double> make_trtab() {
   uint64_t rng = 0x9E3779B97F4A7C15ull;
   auto rnd = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
   double T = 3.0;
-  for (int it = 0; it < 24000; ++it) {
-    const bool onq = (rnd() & 1) != 0;
-    std::vector<int> &v = onq ? pq : ps;
-    const int n = onq ? D::NQ : ZE;   // the zero entries keep the last positions
-    const int a = (int)(rnd() % n), b2 = (int)(rnd() % n);
-    if (a == b2) continue;
-    std::swap(v[a], v[b2]);
+  // search length: ~100k moves at p = 8 (0.8 s, once per process and order: make_trtab_p caches), fewer for the
+  // long schedules of the high orders
+  static const int n_anneal = std::getenv("RRQ_TRTAB_ITERS") ? std::atoi(std::getenv("RRQ_TRTAB_ITERS")) : (900000 / ST > 200000 ? 200000 : 900000 / ST);
+  std::vector<int> best_order = order;
+  for (int it = 0; it < n_anneal; ++it) {
+    const int kind = (int)(rnd() % 3);   // 0: Q positions, 1: S' positions, 2: block order over the lanes
+    int a, b2;
+    if (kind == 2) {
+      a = (int)(rnd() % order.size()); b2 = (int)(rnd() % order.size());
+      if (a == b2) continue;
+      std::swap(order[a], order[b2]);
+      assign();
+    } else {
+      std::vector<int> &v = kind == 0 ? pq : ps;
+      const int n = kind == 0 ? D::NQ : ZE;   // the zero entries keep the last positions
+      a = (int)(rnd() % n); b2 = (int)(rnd() % n);
+      if (a == b2) continue;
+      std::swap(v[a], v[b2]);
+    }
     const int c = cost();
     const double u = (double)(rnd() >> 11) * (1.0 / 9007199254740992.0);
     if (c <= cur || u < std::exp((cur - c) / T)) cur = c;
-    else std::swap(v[a], v[b2]);
-    if (cur < best) { best = cur; best_pq = pq; best_ps = ps; }
+    else if (kind == 2) { std::swap(order[a], order[b2]); assign(); }
+    else std::swap(kind == 0 ? pq[a] : ps[a], kind == 0 ? pq[b2] : ps[b2]);
+    if (cur < best) { best = cur; best_pq = pq; best_ps = ps; best_order = order; }
     T = std::max(0.05, T * 0.9997);
   }
+  order = best_order;
+  assign();
   pq = best_pq; ps = best_ps;
+  if (std::getenv("RRQ_DEBUG_TRTAB"))   // modelled shared-memory wavefronts of the main loop against the conflict-free count
+    std::fprintf(stderr, "rrq: translate schedule p = %d: %d steps, bank cost %d (conflict-free %d)\n", P, ST, best,
+                 ST * 4 * 11 + 4 * 2 * (WD - 1));
   std::vector<uint32_t> w(C::NWORD, 0u);
   for (int l2 = 0; l2 < 32; ++l2)
     for (int t = 0; t < ST; ++t) {
@@ -317,7 +354,17 @@ static std::vector<double> make_trtab() {
   return out;
 }
 
-static std::vector<double> make_trtab_p(int p) {
+static std::vector<double> make_trtab_p_uncached(int p);
+// the schedule search is deterministic: one table per order and process
+static const std::vector<double> &make_trtab_p(int p) {
+  static std::mutex mu;
+  static std::map<int, std::vector<double>> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(p);
+  if (it == cache.end()) it = cache.emplace(p, make_trtab_p_uncached(p)).first;
+  return it->second;
+}
+static std::vector<double> make_trtab_p_uncached(int p) {
   switch (p) {
     case 4: return make_trtab<4>();
     case 6: return make_trtab<6>();
@@ -338,7 +385,7 @@ static int check_trtab() {
   using C = TrCfg<P>;
   using D = Dims<P>;
   constexpr int WD = C::WD, ST = C::STEPS, ZE = P * P, ZQ = C::ZQ;
-  const std::vector<double> tab = make_trtab<P>();
+  const std::vector<double> &tab = make_trtab_p(P);
   const uint32_t *code = reinterpret_cast<const uint32_t *>(tab.data());
   const uint32_t *pcode = code + ST * 32, *cinfo = pcode + ST * 32;
   const uint8_t *posq = reinterpret_cast<const uint8_t *>(cinfo + D::NP), *poss = posq + D::NQ;
@@ -517,7 +564,7 @@ rrq_status rrq_create(const rrq_params *params, rrq_ctx *out) {
   c->T.xdp = c->T.wd + kNDirect;
   c->T.hc = c->T.xdp + kNDirect * q;
   {
-    const std::vector<double> tt = make_trtab_p(p.p);
+    const std::vector<double> &tt = make_trtab_p(p.p);
     if (cudaMalloc(&c->d_trtab, tt.size() * sizeof(double)) == cudaSuccess)
       cudaMemcpy(c->d_trtab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
