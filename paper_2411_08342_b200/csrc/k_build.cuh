@@ -602,7 +602,7 @@ struct EdgeCfg {
   static constexpr int WPB = 8;
   static constexpr int LP = (D::E % 32 == 0 || P > 8) ? 32 : 16;   // lanes per pair in the weights step
   static constexpr int HW = 32 / LP;                               // pairs side by side in a warp
-  static constexpr int PPW = 2 * HW;                               // pairs per warp per round
+  static constexpr int PPW = 3 * HW;                               // pairs per warp per round (48-pair CTA rounds at p <= 8)
   static constexpr int MINB = P <= 8 ? 3 : 2;
 };
 template <int P>
