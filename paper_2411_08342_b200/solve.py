@@ -6,8 +6,8 @@
 discretised as smooth rule + near correction: A sigma = 1/2 sigma + (S + D)_smooth sigma
 + (C_S + C_D) sigma, with the smooth part from rrq_apply_smooth (direct sum; FMM is out of scope) and the
 correction rows from rrq_build_correction at the nodes (self targets, principal value, A7).  The linear
-system is solved by restarted GMRES (modified Gram-Schmidt with one reorthogonalisation, Givens rotations)
-on device vectors; torch supplies only vector arithmetic and dot products (plumbing): every operator
+system is solved by restarted GMRES (classical Gram-Schmidt applied twice, Givens rotations; one host
+synchronisation per iteration) on device vectors; torch supplies only vector arithmetic and dot products (plumbing): every operator
 application runs in the library's kernels.  Evaluation at off-surface targets builds their correction
 rows the same way (close evaluation)."""
 import numpy as np
@@ -31,19 +31,25 @@ def gmres(matvec, b, tol=1e-12, restart=60, maxiter=400):
         if beta / bnorm < tol:
             break
         m = min(restart, maxiter - it)
-        V = [r / beta]
+        # Krylov basis as one matrix; classical Gram-Schmidt applied twice (CGS2: as stable as modified
+        # Gram-Schmidt with reorthogonalisation) so that an iteration costs two matrix-vector products with
+        # the basis and ONE host synchronisation (the column of H and the new norm in one transfer)
+        Vm = torch.empty((m + 1, b.shape[0]), dtype=b.dtype, device=b.device)
+        Vm[0] = r / beta
         H = np.zeros((m + 1, m))
         g = np.zeros(m + 1); g[0] = beta
         cs, sn = np.zeros(m), np.zeros(m)
         k = 0
         for j in range(m):
-            w = matvec(V[j])
-            for _ in range(2):   # MGS + one reorthogonalisation
-                for i in range(j + 1):
-                    h = float(torch.dot(w, V[i]))
-                    H[i, j] += h
-                    w = w - h * V[i]
-            hn = float(torch.linalg.vector_norm(w))
+            w = matvec(Vm[j])
+            B = Vm[: j + 1]
+            h1 = B @ w
+            w = w - B.T @ h1
+            h2 = B @ w
+            w = w - B.T @ h2
+            col = torch.cat([h1 + h2, torch.linalg.vector_norm(w).reshape(1)]).cpu().numpy()
+            H[: j + 1, j] = col[: j + 1]
+            hn = float(col[j + 1])
             H[j + 1, j] = hn
             for i in range(j):   # previous rotations
                 a, c = H[i, j], H[i + 1, j]
@@ -58,10 +64,10 @@ def gmres(matvec, b, tol=1e-12, restart=60, maxiter=400):
             hist.append(abs(g[j + 1]) / bnorm)
             if abs(g[j + 1]) / bnorm < tol or hn == 0.0:
                 break
-            V.append(w / hn)
+            Vm[j + 1] = w / hn
         y = np.linalg.solve(np.triu(H[:k, :k]), g[:k]) if k else np.zeros(0)
-        for i in range(k):
-            x = x + float(y[i]) * V[i]
+        if k:
+            x = x + Vm[:k].T @ torch.as_tensor(y, dtype=b.dtype, device=b.device)
     return x, hist, it
 
 
