@@ -263,12 +263,20 @@ struct QmapCfg {
                                                   : (vcount(1) > vcount(2) ? (vcount(1) > vcount(3) ? vcount(1) : vcount(3)) : (vcount(2) > vcount(3) ? vcount(2) : vcount(3)));
   // k-rows per chunk: 16 where it divides an axis block (p = 8): with 2 stages it costs the shared memory of 4
   // stages of 8 rows and is 5 % faster (half as many barrier round trips, 4 k-steps to schedule per chunk)
+#ifdef RRQ_QMAP_KC   // experiments: chunk rows (must divide 3 p~) and stage count from the command line
+  static constexpr int KC = (D::E % RRQ_QMAP_KC == 0) ? RRQ_QMAP_KC : ((D::E % 8 == 0) ? 8 : 12), NCH = D::K / KC, CPA = D::E / KC;
+#else
   static constexpr int KC = (D::E % 16 == 0) ? 16 : ((D::E % 8 == 0) ? 8 : 12), NCH = D::K / KC, CPA = D::E / KC;
+#endif
 #ifndef RRQ_QMAP_NST
 #define RRQ_QMAP_NST 4
 #endif
   // pipeline stages (chunks in flight); p >= 12: the stage is 37 KB (p = 12) / 73 KB (p = 14), 1 CTA per SM
+#ifdef RRQ_QMAP_KC
+  static constexpr int NST = P <= 10 ? RRQ_QMAP_NST : (P == 12 ? 4 : 2);
+#else
   static constexpr int NST = KC == 16 ? 2 : (P <= 10 ? RRQ_QMAP_NST : (P == 12 ? 4 : 2));
+#endif
   // A (the tile's 32 GEMM rows) is stored tile-chunked by k_edge_lines: chunk ch = [32 rows][KC] (ACH doubles,
   // rows 0..15 = a-rows of the tile's pairs, 16..31 = b-rows), so a stage = [A chunk | B chunk] is two bulk
   // copies and A needs no resident shared memory.  KC = 8: the halves of rows with (r >> 1) odd are swapped
