@@ -986,14 +986,11 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
         if (l < P) {   // translation operands, l' < p
           const cd ng = nup[0] * g[0] + nup[1] * g[1] + nup[2] * g[2], r = Rc[l];
           const double w = wS[l * l + l + m];
-          double2 *o = xo + 2 * (l * l + l + m);
-          o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
-          o[1] = make_double2(w * ng.y, w * ng.x);
+          double *o = reinterpret_cast<double *>(xo + 2 * (l * l + l + m));
+          st_global_256(o, w * r.y, w * r.x, w * ng.y, w * ng.x);   // a whole 32-B entry per store
           if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
             const double sg = (m & 1) ? -w : w;
-            o -= 4 * m;
-            o[0] = make_double2(-sg * r.y, sg * r.x);
-            o[1] = make_double2(-sg * ng.y, sg * ng.x);
+            st_global_256(o - 8 * m, -sg * r.y, sg * r.x, -sg * ng.y, sg * ng.x);
           }
         }
       }
@@ -1022,14 +1019,11 @@ __global__ void __launch_bounds__(TgtCfg<P>::WPB * 32, TgtCfg<P>::MINB)
         const cd *g = GS[pp][e];
         const cd ng = ps.nup[0] * g[0] + ps.nup[1] * g[1] + ps.nup[2] * g[2], r = ps.R[e];
         const double w = wS[l * l + l + m];
-        double2 *o = reinterpret_cast<double2 *>(Xrow + (base + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m));
-        o[0] = make_double2(w * r.y, w * r.x);   // whole 32-B entries (16-B stores)
-        o[1] = make_double2(w * ng.y, w * ng.x);
+        double *o = Xrow + (base + pp - sA) * XR::STRIDE + XR::SX + 4 * (l * l + l + m);
+        st_global_256(o, w * r.y, w * r.x, w * ng.y, w * ng.x);   // a whole 32-B entry per store
         if (m > 0) {   // S^{(l,-m)} = (-1)^m conj S^{(l,m)}, same for nu'.grad S
           const double sg = (m & 1) ? -w : w;
-          o -= 4 * m;
-          o[0] = make_double2(-sg * r.y, sg * r.x);
-          o[1] = make_double2(-sg * ng.y, sg * ng.x);
+          st_global_256(o - 8 * m, -sg * r.y, sg * r.x, -sg * ng.y, sg * ng.x);
         }
       }
     }
@@ -1254,12 +1248,10 @@ __global__ void __launch_bounds__(QmapCfg<P>::WARPS * 32, QmapCfg<P>::MINB)
         if (tl >= C::TQC) continue;   // == u < nq(ns)
         const int e = tl * 4 + (lane & 3);   // entry qidx(j,k)
         if (e >= D::NQ) continue;
-        double2 *o = reinterpret_cast<double2 *>(out + QR::EG * e);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          o[2 * h + c] = make_double2(accA[c][u][0], accA[c][u][1]);
-          if constexpr (DP) o[4 + 2 * h + c] = make_double2(accB[c][u][0], accB[c][u][1]);
-        }
+        // the pass's two components of Q (and of dQ) of the entry are 32 contiguous bytes each: one STG.256
+        double *o = out + QR::EG * e + 4 * h;
+        st_global_256(o, accA[0][u][0], accA[0][u][1], accA[1][u][0], accA[1][u][1]);
+        if constexpr (DP) st_global_256(o + 8, accB[0][u][0], accB[0][u][1], accB[1][u][0], accB[1][u][1]);
       }
       if (h == 1) {
         const int v0 = ns == 0 ? C::vstart(0) : ns == 1 ? C::vstart(1) : ns == 2 ? C::vstart(2) : C::vstart(3);

@@ -265,6 +265,11 @@ __device__ __forceinline__ cq qzero() {
   return r;
 }
 
+// One 32-byte global store (STG.256, sm_100): p must be 32-byte aligned.
+__device__ __forceinline__ void st_global_256(double *p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 __device__ __forceinline__ double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
 __device__ __forceinline__ void cross3(const double *a, const double *b, double *c) {
   c[0] = a[1] * b[2] - a[2] * b[1];
