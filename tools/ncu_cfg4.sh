@@ -16,4 +16,6 @@ for K in $KS; do
     echo "# (cfg4 launch configuration, 13th launch of the kernel; summary by tools/ncu_hot.py)";
     python tools/ncu_hot.py /tmp/ncu_${TAG}_$K.ncu-rep 30; } > gpurun_out/ncu_${TAG}_$K.txt 2>&1
 done
+python tools/ncu_traffic.py $TAG > gpurun_out/traffic_$TAG.json 2> gpurun_out/traffic_$TAG.err
+for K in $KS; do python tools/ncu_regions.py /tmp/ncu_${TAG}_$K.ncu-rep 800 > gpurun_out/ncu_${TAG}_${K}_regions.txt 2>&1; done
 exit 0
