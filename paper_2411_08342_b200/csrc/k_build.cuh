@@ -1724,8 +1724,8 @@ __global__ void __launch_bounds__(ContractCfg<P>::WARPS * 32, ContractCfg<P>::MI
     __syncwarp();
     if (lane == 0) mbar_arrive(&emp[ch & 1]);
   }
-  // unrolled for TPW <= 2 (the accumulators stay in registers; a rolled loop indexes them through local memory)
-#pragma unroll(CC::TPW <= 2 ? 2 : 1)
+  // unrolled (the accumulators stay in registers; a rolled loop indexes them through local memory)
+#pragma unroll
   for (int tw = 0; tw < CC::TPW; ++tw) {
     const int tile = warp + tw * CC::WARPS;
     if (tile >= CC::TILES) continue;
